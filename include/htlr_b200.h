@@ -1,0 +1,144 @@
+/*
+ * htlr_b200.h -- C ABI of the B200-native HTLR hot path.
+ *
+ * Drop-in boundary for the reference package `htlr`
+ * (/root/reference/pkg/src/htlr).  The reference exposes an in-process
+ * Python API only; these entry points are what its Python layer would bind
+ * (ctypes / cffi) to replace, as one unit, the pair
+ *     construct(cfg, grid, threads)   operators.py:121-126
+ *     matvec(op, u)                   operators.py:159-161
+ * together with the tree/list builders they call
+ *     build_cluster_tree              grids.py:210-234
+ *     build_block_cluster_tree        grids.py:268-296
+ * and the accounting the reference reports
+ *     storage_report / operation_counts  operators.py:175-209.
+ * INTEGRATION.md shows the binding stub.
+ *
+ * Conventions
+ *   - Plain C types only; device buffers are raw pointers owned by the caller
+ *     (typically torch tensors' data_ptr()); `stream` is a cudaStream_t passed
+ *     as void*.  The plan owns every internal device buffer (lists, factors,
+ *     deduplicated cores / near blocks, workspaces).
+ *   - Vectors use the reference's grid linearisation (first index fastest,
+ *     tensor.py:4-8).  A block of R right-hand sides is row-major [N][R].
+ *   - Status codes: 0 ok; negative = invalid argument (the Python layer
+ *     raises ValueError, as the reference does); positive = CUDA failure
+ *     (RuntimeError).  htlr_last_error() returns a thread-local message.
+ *   - A plan is not thread-safe; different plans may be used concurrently.
+ *   - There is no CPU fallback: every numeric step runs in sm_100a kernels.
+ */
+#ifndef HTLR_B200_H
+#define HTLR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct htlr_plan htlr_plan;
+
+/* kernels.py:33-103.  `scale` multiplies the reference formula, so the
+ * BASELINE kernels are  -log r = 2*pi*SLP2D,  1/r = 4*pi*SLP3D,
+ * exp(-r^2/s^2) = GAUSSIAN with sigma = s/sqrt(2). */
+enum htlr_kernel_kind { HTLR_KERNEL_GAUSSIAN = 0, HTLR_KERNEL_SLP2D = 1, HTLR_KERNEL_SLP3D = 2 };
+
+/* grids.py:130-165 */
+enum htlr_rule_kind { HTLR_RULE_WEAK = 0, HTLR_RULE_STRONG = 1 };
+
+/* leaf kinds in exported lists (grids.py:377-378) */
+enum htlr_leaf_kind { HTLR_LEAF_ADMISSIBLE = 0, HTLR_LEAF_INADMISSIBLE = 1 };
+
+typedef struct htlr_desc {
+  int32_t d;                  /* 2 or 3 (UniformGrid, grids.py:26-27)          */
+  int32_t n;                  /* points per side, h = 1/n                      */
+  int32_t leaf_side_max;      /* BuildConfig.leaf_side (operators.py:43)        */
+  int32_t rank;               /* BuildConfig.rank = Chebyshev order p           */
+  int32_t rule;               /* htlr_rule_kind                                 */
+  double eta;                 /* AdmissibilityRule.eta (strong only)            */
+  int32_t kernel;             /* htlr_kernel_kind                               */
+  double sigma;               /* KernelSpec.sigma (gaussian)                    */
+  double scale;               /* multiplies the reference kernel formula        */
+  int32_t quad_q;             /* QuadratureConfig.q (kernels.py:187)            */
+  int32_t corner_subdivision; /* 1: singular corner-subdivided rule, i.e.
+                               * !smooth_at_diagonal && QuadratureConfig.
+                               * corner_subdivision (kernels.py:263-265)       */
+  double coeff_const;         /* CoefficientFn.constant(c); see htlr_set_coeff  */
+} htlr_desc;
+
+/* Create a plan on `device` (-1: host-only plan that can build and export
+ * the trees/lists and the storage accounting, but does no device work);
+ * validates the descriptor like the reference's
+ * constructors (UniformGrid, _leaf_side, BuildConfig).  Replaces the argument
+ * checking of grids.py:23-27,196-207 and operators.py:49-59. */
+int htlr_plan_create(const htlr_desc* desc, int device, htlr_plan** out);
+int htlr_plan_destroy(htlr_plan* plan);
+
+/* Cluster tree + block cluster tree, bit-exact with grids.py:210-296 (host
+ * C++, -ffp-contract=off), flattened into per-level device CSR / offset
+ * tables.  Replaces build_cluster_tree + build_block_cluster_tree. */
+int htlr_build_lists(htlr_plan* plan);
+
+/* Tree summary: depth, leaf side, leaf counts (operation_counts,
+ * operators.py:200-209).  Any pointer may be NULL. */
+int htlr_tree_info(const htlr_plan* plan, int32_t* depth, int32_t* leaf_side,
+                   int64_t* num_leaves, int64_t* num_admissible, int64_t* num_inadmissible);
+
+/* DFS leaf list (BlockClusterTree.leaves, grids.py:268-296) as int32 rows
+ * [leaf_id, kind, level, tau lo/hi per dim, sigma lo/hi per dim]:
+ * num_leaves x (3 + 4d) values.  `cap` = capacity of `rows` in int32s. */
+int htlr_export_lists(const htlr_plan* plan, int32_t* rows, int64_t cap);
+
+/* Per-point coefficient a(x_i) (CoefficientFn evaluated by the caller on the
+ * grid points, kernels.py:162-175); host array of N doubles, F-order.  If
+ * never called, coeff_const is used. */
+int htlr_set_coeff(htlr_plan* plan, const double* a_host);
+
+/* Construction on the device: diagonal cell quadrature (kernels.py:195-265),
+ * per-level Lagrange factors + Householder QR (chebyshev.py:52-66,
+ * tensor.py:107-115), Chebyshev kernel sampling + R folding of every unique
+ * (level, offset) core (chebyshev.py:69-85, blocks.py:126-164), and the
+ * unique near-field blocks (blocks.py:190-227).  Replaces _build_payloads
+ * (operators.py:102-118).  Stream-ordered. */
+int htlr_construct(htlr_plan* plan, void* stream);
+
+/* f = A u for R right-hand sides (operators.py:138-161 applied column-wise):
+ * u, f are DEVICE pointers to row-major [N][nrhs] doubles.  Stream-ordered,
+ * asynchronous.  Replaces matvec / _hierarchical_matvec. */
+int htlr_matvec(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
+
+/* Diagonal cell average used by the inadmissible tau == sigma blocks
+ * (operators.py:95-99).  Synchronises. */
+int htlr_diag_value(htlr_plan* plan, double* out);
+
+/* Payload of one DFS leaf, as the reference stores it (blocks.py:33-73):
+ *   admissible: core (p^(2d), F-order, target modes first) into `core_or_dense`,
+ *               per dim u then v factors (s x p, row-major) into `factors`
+ *               (dims whose box side equals p store nothing: factor None);
+ *   inadmissible: dense |tau| x |sigma| row-major into `core_or_dense`.
+ * shapes[0] = kind, shapes[1] = rows, shapes[2] = cols, shapes[3] = number of
+ * factor scalars written.  Synchronises. */
+int htlr_export_block(htlr_plan* plan, int64_t leaf_id, double* core_or_dense, int64_t cap,
+                      double* factors, int64_t factor_cap, int32_t* shapes);
+
+/* storage_report equivalent (operators.py:175-197): scalars the reference
+ * would store: [dense, factor, core, total]; plus what this plan stores
+ * on the device after deduplication in out[4]. */
+int htlr_storage(const htlr_plan* plan, int64_t out[5]);
+
+/* Diagonal cell average of a translation-invariant kernel over a width-h
+ * cell (diagonal_entry, kernels.py:252-265), computed by the device
+ * quadrature kernel on `device`; corner_subdivision as in htlr_desc.
+ * Synchronous. */
+int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,
+                      int32_t corner_subdivision, int device, double* out);
+
+/* Number of CUDA kernel launches issued by the last htlr_matvec call. */
+int64_t htlr_last_launch_count(const htlr_plan* plan);
+
+const char* htlr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HTLR_B200_H */

@@ -1,0 +1,576 @@
+"""CPU oracle for the HTLR hot path.  TEST INFRASTRUCTURE ONLY.
+
+This module is the parity checker, never the product: only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and the
+``--impl reference`` arm) may import it.  The product package
+``paper_2508_05958_b200`` never imports anything under ``oracle/``.
+
+It restates, in plain numpy, the algorithm of the reference package ``htlr``
+(``/root/reference/pkg/src/htlr``) on the hot path named by BASELINE.json:
+cluster tree + block cluster tree (``grids.py``), kernel evaluation and the
+diagonal cell quadrature (``kernels.py``), Chebyshev nodes / Lagrange factors /
+kernel cores (``chebyshev.py``), Tucker and dense leaf payloads
+(``blocks.py``), and the leaf-by-leaf matvec (``operators.py``).  Every
+function cites the reference lines it follows.
+
+Parity pin: ``tests/golden/make_golden.py`` imports the reference itself (in
+the build container, where ``/root/reference`` exists) and writes the
+fixtures under ``tests/golden/``; ``tests/test_oracle_golden.py`` checks this
+restatement against every fixture (lists bit-exact, diagonal constants and
+matvec results to rounding).  The reference computes with numpy/OpenBLAS
+(unvendored, pinned only as ``numpy>=1.24``, ``scipy>=1.10`` in
+``pkg/pyproject.toml:10-13``); the fixtures were produced with numpy 2.3.5.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+ADM = 0     # grids.py:377 ADMISSIBLE
+NEAR = 1    # grids.py:378 INADMISSIBLE
+
+# --------------------------------------------------------------------------
+# kernels (kernels.py:33-117).  `scale` multiplies the reference formula; the
+# BASELINE.json kernels are -log r = 2*pi*slp2d, 1/r = 4*pi*slp3d and
+# exp(-r^2/s^2) = gaussian(s/sqrt(2)).
+# --------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Kernel:
+    kind: str                      # "gaussian" | "slp2d" | "slp3d"
+    sigma: float = 0.0
+    scale: float = 1.0
+
+    @property
+    def smooth_at_diagonal(self) -> bool:      # kernels.py:50-70
+        return self.kind == "gaussian"
+
+
+def kernel_values(k: Kernel, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """k(x, y) over broadcast point arrays with a trailing coordinate axis
+    (kernels.py:88-103)."""
+    diff = x - y
+    r2 = np.sum(diff * diff, axis=-1)
+    if k.kind == "gaussian":
+        out = np.exp(-r2 / (2.0 * k.sigma * k.sigma))
+    elif k.kind == "slp2d":
+        if np.any(r2 == 0.0):
+            raise ValueError("SLP kernel evaluated on the diagonal")
+        out = -0.5 * np.log(r2) / (2.0 * np.pi)
+    elif k.kind == "slp3d":
+        r = np.sqrt(r2)
+        if np.any(r == 0.0):
+            raise ValueError("SLP kernel evaluated on the diagonal")
+        out = 1.0 / (4.0 * np.pi * r)
+    else:
+        raise ValueError(f"unknown kernel kind {k.kind!r}")
+    return out if k.scale == 1.0 else k.scale * out
+
+
+def kernel_pairs(k: Kernel, xs: np.ndarray, ys: np.ndarray) -> np.ndarray:
+    """(m1, d) x (m2, d) -> (m1, m2) (kernels.py:113-117)."""
+    return kernel_values(k, xs[:, None, :], ys[None, :, :])
+
+
+def kernel_pairs_self(k: Kernel, pts: np.ndarray, diag: np.ndarray) -> np.ndarray:
+    """Square block of a point set with itself; coincident pairs are kept off
+    the singular formula (r^2 := 1) and then overwritten by `diag`
+    (kernels.py:120-149)."""
+    diff = pts[:, None, :] - pts[None, :, :]
+    r2 = np.sum(diff * diff, axis=-1)
+    idx = np.arange(len(pts))
+    if k.kind == "gaussian":
+        out = np.exp(-r2 / (2.0 * k.sigma * k.sigma))
+    else:
+        r2[idx, idx] = 1.0
+        if k.kind == "slp2d":
+            out = -0.5 * np.log(r2) / (2.0 * np.pi)
+        else:
+            out = 1.0 / (4.0 * np.pi * np.sqrt(r2))
+    if k.scale != 1.0:
+        out = k.scale * out
+    out[idx, idx] = diag
+    return out
+
+
+# -- diagonal cell average (kernels.py:195-265) -----------------------------
+
+GRADING = 3   # kernels.py:28 RADIAL_GRADING
+
+
+def _gl01(q: int):
+    """Gauss-Legendre rule mapped to [0, 1] (kernels.py:195-198)."""
+    x, w = np.polynomial.legendre.leggauss(q)
+    return 0.5 * (x + 1.0), 0.5 * w
+
+
+def _tensor_weights(ws: Sequence[np.ndarray]) -> np.ndarray:
+    """Outer product of per-axis weights in 'ij' order (kernels.py:200-207)."""
+    out = np.ones([len(w) for w in ws])
+    for ax, w in enumerate(ws):
+        shape = [1] * len(ws)
+        shape[ax] = len(w)
+        out = out * w.reshape(shape)
+    return out
+
+
+def cell_average(k: Kernel, d: int, h: float, q: int = 10,
+                 corner_subdivision: bool = True) -> float:
+    """Average of k(0, .) over the width-h cell centred at the origin
+    (translation-invariant kernels, kernels.py:252-265 with center := 0)."""
+    if h <= 0:
+        raise ValueError("cell width must be positive")
+    center = np.zeros(d)
+    gx, gw = _gl01(q)
+    if k.smooth_at_diagonal or not corner_subdivision:
+        # kernels.py:210-219: plain tensor rule over the cell
+        axes = [center[a] - h / 2 + h * gx for a in range(d)]
+        mesh = np.meshgrid(*axes, indexing="ij")
+        w = _tensor_weights([h * gw] * d)
+        pts = np.stack([m.ravel() for m in mesh], axis=-1)
+        vals = kernel_values(k, np.broadcast_to(center, pts.shape), pts)
+        return float(np.sum(vals * w.ravel())) / h ** d
+    # kernels.py:222-249: 2^d corner sub-cells x d Duffy pyramids, cubic
+    # radial grading toward the singular centre
+    half = h / 2.0
+    rad = gx ** GRADING
+    rad_w = GRADING * gx ** (GRADING - 1) * gw
+    total = 0.0
+    for corner in np.ndindex(*([2] * d)):
+        sgn = np.array([1.0 if c else -1.0 for c in corner])
+        for axis in range(d):
+            nodes = [rad if a == axis else gx for a in range(d)]
+            mesh = np.meshgrid(*nodes, indexing="ij")
+            w = _tensor_weights([rad_w if a == axis else gw for a in range(d)])
+            t = mesh[axis]
+            z = np.empty(t.shape + (d,))
+            for a in range(d):
+                z[..., a] = half * t if a == axis else half * t * mesh[a]
+            pts = (center + sgn * z).reshape(-1, d)
+            jac = half ** d * t ** (d - 1)
+            vals = kernel_values(k, np.broadcast_to(center, pts.shape), pts)
+            total += float(np.sum(vals * (jac * w).ravel()))
+    return total / h ** d
+
+
+# --------------------------------------------------------------------------
+# grid, cluster tree, block cluster tree (grids.py:18-296)
+# --------------------------------------------------------------------------
+
+Ranges = tuple  # tuple of (lo, hi) per dimension, half-open, 0-based
+
+
+def grid_points(n: int, ranges: Ranges) -> np.ndarray:
+    """Cell-centred points (i + 1/2) h of an index box, first index fastest
+    (grids.py:39-50)."""
+    h = 1.0 / n
+    axes = [(np.arange(lo, hi) + 0.5) * h for lo, hi in ranges]
+    mesh = np.meshgrid(*axes, indexing="ij")
+    return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
+
+
+def box_linear_indices(n: int, ranges: Ranges) -> np.ndarray:
+    """F-order global ids of the points of an index box (grids.py:82-92)."""
+    mesh = np.meshgrid(*[np.arange(lo, hi, dtype=np.int64) for lo, hi in ranges], indexing="ij")
+    lin = np.zeros_like(mesh[0])
+    stride = 1
+    for m in mesh:
+        lin = lin + m * stride
+        stride *= n
+    return lin.ravel(order="F")
+
+
+def leaf_side(n: int, leaf_side_max: int) -> int:
+    """Exact repeated halving down to the threshold (grids.py:196-207)."""
+    if leaf_side_max < 1:
+        raise ValueError("leaf threshold must be positive")
+    side = n
+    while side > leaf_side_max:
+        if side % 2:
+            raise ValueError(f"grid side {n} cannot be halved evenly down to "
+                             f"the leaf threshold {leaf_side_max}")
+        side //= 2
+    return side
+
+
+@dataclass
+class Cluster:
+    ranges: Ranges
+    level: int
+    kids: list = field(default_factory=list)
+
+
+def cluster_tree(n: int, d: int, leaf_side_max: int) -> Cluster:
+    """Midpoint 2^d split, children in ndindex order (last dim fastest),
+    leaf iff max side <= threshold (grids.py:210-234)."""
+    leaf_side(n, leaf_side_max)
+
+    def grow(ranges: Ranges, level: int) -> Cluster:
+        node = Cluster(ranges, level)
+        if max(hi - lo for lo, hi in ranges) <= leaf_side_max:
+            return node
+        halves = [((lo, (lo + hi) // 2), ((lo + hi) // 2, hi)) for lo, hi in ranges]
+        for combo in np.ndindex(*([2] * d)):
+            node.kids.append(grow(tuple(halves[a][combo[a]] for a in range(d)), level + 1))
+        return node
+
+    return grow(tuple((0, n) for _ in range(d)), 0)
+
+
+def domain(n: int, ranges: Ranges):
+    """Real box covered by the cells (grids.py:237-242): (lo*h, hi*h)."""
+    h = 1.0 / n
+    return tuple((lo * h, hi * h) for lo, hi in ranges)
+
+
+def admissible(rule: str, eta: Optional[float], dt, ds) -> bool:
+    """Weak: zero-volume overlap; strong: diam^2 <= eta^2 dist^2 (1+1e-12),
+    evaluated in the reference's operation order (grids.py:110-127,153-165)."""
+    if rule == "weak":
+        return _overlap_volume(dt, ds) == 0.0
+    dist = 0.0
+    for (a1, b1), (a2, b2) in zip(dt, ds):
+        gap = max(a1 - b2, a2 - b1, 0.0)
+        dist += gap * gap
+    diam_t = 0
+    for a, b in dt:
+        diam_t = diam_t + (b - a) ** 2
+    diam_s = 0
+    for a, b in ds:
+        diam_s = diam_s + (b - a) ** 2
+    diam = max(float(diam_t), float(diam_s))
+    return diam <= eta * eta * dist * (1.0 + 1e-12)
+
+
+@dataclass
+class Leaf:
+    leaf_id: int
+    kind: int
+    level: int
+    tau: Ranges
+    sigma: Ranges
+
+
+def block_leaves(n: int, d: int, leaf_side_max: int, rule: str = "strong",
+                 eta: Optional[float] = 1.0) -> list:
+    """DFS leaf list of the block cluster tree: admissible first, then
+    leaf-leaf -> dense, else recurse sigma-children outer / tau-children
+    inner; leaf_id in creation order (grids.py:268-296)."""
+    root = cluster_tree(n, d, leaf_side_max)
+    out: list = []
+
+    def visit(t: Cluster, s: Cluster, level: int):
+        if admissible(rule, eta, domain(n, t.ranges), domain(n, s.ranges)):
+            out.append(Leaf(len(out), ADM, level, t.ranges, s.ranges))
+            return
+        if not t.kids or not s.kids:
+            assert not t.kids and not s.kids
+            out.append(Leaf(len(out), NEAR, level, t.ranges, s.ranges))
+            return
+        for sk in s.kids:
+            for tk in t.kids:
+                visit(tk, sk, level + 1)
+
+    import sys
+    sys.setrecursionlimit(max(10000, sys.getrecursionlimit()))
+    visit(root, root, 0)
+    return out
+
+
+def leaves_to_array(leaves: list, d: int) -> np.ndarray:
+    """Leaf list as int64 rows: leaf_id, kind, level, tau lo/hi per dim,
+    sigma lo/hi per dim (the export format of htlr_export_lists)."""
+    arr = np.empty((len(leaves), 3 + 4 * d), dtype=np.int64)
+    for i, lf in enumerate(leaves):
+        arr[i, 0] = lf.leaf_id
+        arr[i, 1] = lf.kind
+        arr[i, 2] = lf.level
+        arr[i, 3:3 + 2 * d] = np.asarray(lf.tau, dtype=np.int64).ravel()
+        arr[i, 3 + 2 * d:] = np.asarray(lf.sigma, dtype=np.int64).ravel()
+    return arr
+
+
+# --------------------------------------------------------------------------
+# Chebyshev interpolation (chebyshev.py:31-85)
+# --------------------------------------------------------------------------
+
+
+def cheb_nodes(lo: float, hi: float, p: int) -> np.ndarray:
+    """First-kind nodes in decreasing order (chebyshev.py:31-38)."""
+    t = np.arange(1, p + 1)
+    return 0.5 * (hi - lo) * np.cos((2 * t - 1) * np.pi / (2 * p)) + 0.5 * (hi + lo)
+
+
+def lagrange_matrix(x: np.ndarray, nodes: np.ndarray) -> np.ndarray:
+    """L[i, t] = prod_{j != t} (x_i - xi_j) / (xi_t - xi_j), product taken in
+    ascending j (chebyshev.py:52-66)."""
+    p = len(nodes)
+    out = np.empty((len(x), p))
+    for t in range(p):
+        others = np.array([j for j in range(p) if j != t], dtype=np.int64)
+        out[:, t] = np.prod((x[:, None] - nodes[None, others]) / (nodes[t] - nodes[others]), axis=1)
+    return out
+
+
+def kernel_core(k: Kernel, nodes_t: Sequence[np.ndarray], nodes_s: Sequence[np.ndarray]) -> np.ndarray:
+    """k at all tensor node pairs, order-2d tensor with target modes first
+    (chebyshev.py:69-85)."""
+    def tensor_pts(nodes):
+        mesh = np.meshgrid(*nodes, indexing="ij")
+        return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
+    vals = kernel_pairs(k, tensor_pts(nodes_t), tensor_pts(nodes_s))
+    shape = tuple(len(a) for a in nodes_t) + tuple(len(a) for a in nodes_s)
+    return vals.ravel(order="F").reshape(shape, order="F")
+
+
+# --------------------------------------------------------------------------
+# tensor helpers (tensor.py:35-132)
+# --------------------------------------------------------------------------
+
+
+def mode_mul(t: np.ndarray, m: np.ndarray, mode: int) -> np.ndarray:
+    """Contract axis `mode` (1-based) of t with the columns of m
+    (tensor.py:35-52)."""
+    moved = np.moveaxis(t, mode - 1, 0)
+    out = np.tensordot(m, moved, axes=([1], [0]))
+    return np.moveaxis(out, 0, mode - 1)
+
+
+# --------------------------------------------------------------------------
+# leaf payloads (blocks.py:89-227) and their application (blocks.py:230-286)
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class Tucker:
+    core: np.ndarray
+    ufac: list     # per-dim (s x p) orthonormal factor or None (square)
+    vfac: list
+
+
+def tucker_block(k: Kernel, n: int, tau: Ranges, sigma: Ranges, p: int) -> Tucker:
+    """Interpolate over the box pair, QR every non-square factor, fold h^d and
+    the triangular factors (raw factor when square) into the core in the
+    interleaved order u1, v1, u2, v2, ... (blocks.py:89-106,126-164)."""
+    d = len(tau)
+    h = 1.0 / n
+    dt, ds = domain(n, tau), domain(n, sigma)
+    if _overlap_volume(dt, ds) > 0.0:
+        raise ValueError("interpolation blocks require disjoint domains")
+    nt = [cheb_nodes(lo, hi, p) for lo, hi in dt]
+    ns = [cheb_nodes(lo, hi, p) for lo, hi in ds]
+    raw_u = [lagrange_matrix((np.arange(*tau[a]) + 0.5) * h, nt[a]) for a in range(d)]
+    raw_v = [lagrange_matrix((np.arange(*sigma[a]) + 0.5) * h, ns[a]) for a in range(d)]
+    core = h ** d * kernel_core(k, nt, ns)
+    ufac, vfac = [], []
+    for a in range(d):
+        for raw, facs, mode in ((raw_u[a], ufac, a + 1), (raw_v[a], vfac, d + a + 1)):
+            if raw.shape[0] < raw.shape[1]:
+                raise ValueError(f"qr requires rows >= cols, got shape {raw.shape}")
+            if raw.shape[0] == raw.shape[1]:
+                facs.append(None)
+                core = mode_mul(core, raw, mode)
+            else:
+                q, r = np.linalg.qr(raw, mode="reduced")
+                facs.append(q)
+                core = mode_mul(core, r, mode)
+    return Tucker(core, ufac, vfac)
+
+
+def _overlap_volume(dt, ds) -> float:
+    vol = 1.0
+    for (a1, b1), (a2, b2) in zip(dt, ds):
+        length = min(b1, b2) - max(a1, a2)
+        if length <= 0.0:
+            return 0.0
+        vol *= length
+    return vol
+
+
+def dense_block(k: Kernel, coeff: Callable[[np.ndarray], np.ndarray], n: int,
+                tau: Ranges, sigma: Ranges, diag: float) -> np.ndarray:
+    """a(x_i) 1[i=j] + K_ij h^d; the tau == sigma diagonal is the cached cell
+    average (blocks.py:190-227, operators.py:95-99)."""
+    d = len(tau)
+    h = 1.0 / n
+    xs = grid_points(n, tau)
+    ys = grid_points(n, sigma)
+    if tau == sigma:
+        mat = kernel_pairs_self(k, xs, np.full(len(xs), diag)) * h ** d
+        idx = np.arange(len(xs))
+        mat[idx, idx] += np.asarray(coeff(xs), dtype=np.float64)
+        return mat
+    return kernel_pairs(k, xs, ys) * h ** d
+
+
+def tucker_apply(b: Tucker, seg: np.ndarray) -> np.ndarray:
+    """V^T mode products, core contraction over the source modes, U mode
+    products (blocks.py:230-259)."""
+    d = len(b.ufac)
+    core_shape = b.core.shape
+    cols = tuple(f.shape[0] if f is not None else core_shape[d + a] for a, f in enumerate(b.vfac))
+    w = np.reshape(seg, cols, order="F")
+    for a, f in enumerate(b.vfac):
+        if f is not None:
+            w = mode_mul(w, f.T, a + 1)
+    hvec = np.tensordot(b.core, w, axes=(list(range(d, 2 * d)), list(range(d))))
+    for a, f in enumerate(b.ufac):
+        if f is not None:
+            hvec = mode_mul(hvec, f, a + 1)
+    return hvec.ravel(order="F")
+
+
+def materialize_tucker(b: Tucker) -> np.ndarray:
+    """Full matrix of a Tucker block (blocks.py:267-286)."""
+    d = len(b.ufac)
+    full = b.core
+    for a, f in enumerate(b.ufac):
+        if f is not None:
+            full = mode_mul(full, f, a + 1)
+    for a, f in enumerate(b.vfac):
+        if f is not None:
+            full = mode_mul(full, f, d + a + 1)
+    rows = int(np.prod(full.shape[:d]))
+    return full.reshape(rows, -1, order="F")
+
+
+# --------------------------------------------------------------------------
+# operator + matvec (operators.py:95-161)
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class Problem:
+    d: int
+    n: int
+    rank: int
+    leaf_side_max: int
+    kernel: Kernel
+    coeff: Callable[[np.ndarray], np.ndarray]
+    rule: str = "strong"
+    eta: Optional[float] = 1.0
+    q: int = 10
+
+    @property
+    def h(self) -> float:
+        return 1.0 / self.n
+
+    @property
+    def num_points(self) -> int:
+        return self.n ** self.d
+
+    def diag(self) -> float:
+        """operators.py:95-99 (cell centred at the origin: translation-invariant)."""
+        return cell_average(self.kernel, self.d, self.h, self.q)
+
+
+def constant_coeff(c: float):
+    return lambda pts: np.full(len(pts), float(c))
+
+
+def build_payload(pb: Problem, leaf: Leaf, diag: float):
+    if leaf.kind == ADM:
+        return tucker_block(pb.kernel, pb.n, leaf.tau, leaf.sigma, pb.rank)
+    return dense_block(pb.kernel, pb.coeff, pb.n, leaf.tau, leaf.sigma, diag)
+
+
+def apply_payload(payload, seg: np.ndarray) -> np.ndarray:
+    if isinstance(payload, Tucker):
+        return tucker_apply(payload, seg)
+    return payload @ seg
+
+
+def _slices(ranges: Ranges):
+    return tuple(slice(lo, hi) for lo, hi in ranges)
+
+
+def matvec(pb: Problem, u: np.ndarray, leaves: Optional[list] = None,
+           payloads: Optional[list] = None) -> np.ndarray:
+    """f = A u accumulated leaf by leaf in DFS order (operators.py:138-161).
+    `u` may be (N,) or (N, R); columns are independent right-hand sides."""
+    u = np.asarray(u, dtype=np.float64)
+    cols = u.reshape(pb.num_points, -1)
+    if cols.shape[0] != pb.num_points:
+        raise ValueError("vector length mismatch")
+    if leaves is None:
+        leaves = block_leaves(pb.n, pb.d, pb.leaf_side_max, pb.rule, pb.eta)
+    diag = pb.diag()
+    shape = (pb.n,) * pb.d
+    out = np.zeros_like(cols)
+    for r in range(cols.shape[1]):
+        ut = cols[:, r].reshape(shape, order="F")
+        ft = np.zeros(shape)
+        for lf in leaves:
+            pl = payloads[lf.leaf_id] if payloads is not None else build_payload(pb, lf, diag)
+            seg = ut[_slices(lf.sigma)].ravel(order="F")
+            res = apply_payload(pl, seg)
+            ft[_slices(lf.tau)] += res.reshape([hi - lo for lo, hi in lf.tau], order="F")
+        out[:, r] = ft.ravel(order="F")
+    return out.reshape(u.shape)
+
+
+def _contains(outer: Ranges, inner: Ranges) -> bool:
+    return all(lo_o <= lo_i and hi_i <= hi_o for (lo_o, hi_o), (lo_i, hi_i) in zip(outer, inner))
+
+
+def sampled_matvec(pb: Problem, u: np.ndarray, targets: Sequence[Ranges],
+                   leaves: Optional[list] = None) -> np.ndarray:
+    """Rows of f = A u on the given leaf target boxes only: iterate the DFS
+    leaves, keep those whose tau contains a target box, build and apply them
+    exactly as operators.py:146-155 does.  Accumulation per row follows the
+    same DFS order as the full matvec, so the sampled rows equal the full
+    reference matvec's rows bit for bit.  Returns an array
+    (len(targets), box points, R)."""
+    u = np.asarray(u, dtype=np.float64)
+    cols = u.reshape(pb.num_points, -1)
+    if leaves is None:
+        leaves = block_leaves(pb.n, pb.d, pb.leaf_side_max, pb.rule, pb.eta)
+    diag = pb.diag()
+    shape = (pb.n,) * pb.d
+    R = cols.shape[1]
+    uts = [cols[:, r].reshape(shape, order="F") for r in range(R)]
+    acc = {}
+    for lf in leaves:
+        hit = [i for i, tb in enumerate(targets) if _contains(lf.tau, tb)]
+        if not hit:
+            continue
+        pl = build_payload(pb, lf, diag)
+        tsz = [hi - lo for lo, hi in lf.tau]
+        for r in range(R):
+            seg = uts[r][_slices(lf.sigma)].ravel(order="F")
+            res = apply_payload(pl, seg).reshape(tsz, order="F")
+            for i in hit:
+                sub = tuple(slice(lo - tlo, hi - tlo) for (lo, hi), (tlo, _) in zip(targets[i], lf.tau))
+                key = (i, r)
+                if key not in acc:
+                    acc[key] = np.zeros([hi - lo for lo, hi in targets[i]])
+                acc[key] += res[sub]
+    npts = int(np.prod([hi - lo for lo, hi in targets[0]]))
+    out = np.zeros((len(targets), npts, R))
+    for (i, r), v in acc.items():
+        out[i, :, r] = v.ravel(order="F")
+    return out
+
+
+def storage_counts(pb: Problem, leaves: list) -> dict:
+    """Scalar counts by category for the reference's per-leaf storage
+    (blocks.py:289-299, operators.py:175-197)."""
+    p, d = pb.rank, pb.d
+    dense = factors = cores = 0
+    for lf in leaves:
+        nt = int(np.prod([hi - lo for lo, hi in lf.tau]))
+        ns = int(np.prod([hi - lo for lo, hi in lf.sigma]))
+        if lf.kind == NEAR:
+            dense += nt * ns
+            continue
+        cores += p ** (2 * d)
+        for lo, hi in lf.tau + lf.sigma:
+            if hi - lo != p:
+                factors += (hi - lo) * p
+    return {"dense": dense, "factors": factors, "cores": cores,
+            "total": dense + factors + cores}

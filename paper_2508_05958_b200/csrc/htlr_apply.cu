@@ -1,0 +1,398 @@
+// Matvec kernels of the B200 HTLR plan (sm_100a).
+//
+// The reference applies every leaf independently (operators.py:138-161,
+// blocks.py:230-259): W = V^T-mode products of u_sigma, H = core . W,
+// f_tau += U-mode products of H.  Factors depend only on a box, so the same
+// algebra is regrouped exactly into
+//   permute_in   u (F-order) -> leaf-box-major ub         (operators.py:144-148)
+//   upward       W_l[c] = (V^T x V^T x V^T) u_c per cluster (blocks.py:239-247)
+//   gemm         H_l[t] += G_l[o(t,s)] W_l[s] over the admissible list, and
+//                Y[t]   += D[o(t,s)] ub[s] over the near list, as batched
+//                fp64 tensor-core GEMMs (mma.sync m16n8k8 -> DMMA) with
+//                gathered B columns                  (blocks.py:248-250, operators.py:150)
+//   downward     f = Y + a u + sum_l (U x U x U) H_l[anc] per leaf box, written
+//                back in F-order                     (blocks.py:251-259, operators.py:153-156)
+#include "htlr_kernels.h"
+
+namespace htlr {
+
+// ---------------------------------------------------------------------------
+// permute: ub[(b*R + r)*K_pad + k] = u[(global point of (b, k))*R + r]
+// ---------------------------------------------------------------------------
+__global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
+                                  int s, int R, int K_pad) {
+  const int m = n / s;
+  int b = blockIdx.x;
+  int bc[3] = {b % m, (b / m) % m, b / (m * m)};
+  const int P = (d == 2) ? s * s : s * s * s;
+  for (int idx = threadIdx.x; idx < R * K_pad; idx += blockDim.x) {
+    int r = idx % R, k = idx / R;
+    double v = 0.0;
+    if (k < P) {
+      int x = k % s, y = (k / s) % s, z = k / (s * s);
+      int64_t g = (int64_t)(bc[0] * s + x) + (int64_t)n * (bc[1] * s + y);
+      if (d == 3) g += (int64_t)n * n * (bc[2] * s + z);
+      v = u[g * R + r];
+    }
+    ub[((int64_t)b * R + r) * K_pad + k] = v;
+  }
+}
+
+void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad,
+                       cudaStream_t st) {
+  int m = n / s;
+  int nb = (d == 2) ? m * m : m * m * m;
+  permute_in_kernel<<<nb, 256, 0, st>>>(u, ub, d, n, s, R, K_pad);
+}
+
+// ---------------------------------------------------------------------------
+// upward pass: one CTA per (cluster, rhs); mode 1 (x), then 2 (y), with the
+// mode-3 (z) product accumulated slab by slab, so shared memory holds only
+// p*s + p^2 + p^3 values whatever the box side.
+// ---------------------------------------------------------------------------
+__global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
+                              int p, int R, int K_pad, const double* __restrict__ Q) {
+  extern __shared__ double sm[];
+  double* sQ = sm;             // s*p
+  double* T1 = sQ + s * p;     // p*s
+  double* T2 = T1 + p * s;     // p*p
+  double* acc = T2 + p * p;    // p^d
+  const int m = n / s;
+  const int c = blockIdx.x, r = blockIdx.y;
+  const int cc[3] = {c % m, (c / m) % m, c / (m * m)};
+  for (int i = threadIdx.x; i < s * p; i += blockDim.x) sQ[i] = Q[i];
+  const int P = (d == 2) ? p * p : p * p * p;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) acc[i] = 0.0;
+  __syncthreads();
+  const int nz = (d == 3) ? s : 1;
+  for (int z = 0; z < nz; ++z) {
+    // T1[a1 + p*y] = sum_x Q[x][a1] u[x, y, z]
+    for (int i = threadIdx.x; i < p * s; i += blockDim.x) {
+      int a1 = i % p, y = i / p;
+      int64_t g = (int64_t)cc[0] * s + (int64_t)n * (cc[1] * s + y);
+      if (d == 3) g += (int64_t)n * n * (cc[2] * s + z);
+      double v = 0.0;
+      for (int x = 0; x < s; ++x) v += sQ[x * p + a1] * u[(g + x) * R + r];
+      T1[i] = v;
+    }
+    __syncthreads();
+    if (d == 2) {
+      for (int i = threadIdx.x; i < p * p; i += blockDim.x) {
+        int a1 = i % p, a2 = i / p;
+        double v = 0.0;
+        for (int y = 0; y < s; ++y) v += sQ[y * p + a2] * T1[a1 + p * y];
+        acc[i] = v;
+      }
+      __syncthreads();
+    } else {
+      for (int i = threadIdx.x; i < p * p; i += blockDim.x) {
+        int a1 = i % p, a2 = i / p;
+        double v = 0.0;
+        for (int y = 0; y < s; ++y) v += sQ[y * p + a2] * T1[a1 + p * y];
+        T2[i] = v;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int a12 = i % (p * p), a3 = i / (p * p);
+        acc[i] += sQ[z * p + a3] * T2[a12];
+      }
+      __syncthreads();
+    }
+  }
+  double* dst = W + ((int64_t)c * R + r) * K_pad;
+  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) dst[i] = i < P ? acc[i] : 0.0;
+}
+
+void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
+                   int K_pad, const double* Q, cudaStream_t st) {
+  int m = n / side;
+  int nc = (d == 2) ? m * m : m * m * m;
+  int P = (d == 2) ? p * p : p * p * p;
+  size_t smem = sizeof(double) * (size_t)(side * p + p * side + p * p + P);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (void)level;
+  upward_kernel<<<dim3(nc, R), 256, smem, st>>>(u, W, d, n, side, p, R, K_pad, Q);
+}
+
+// ---------------------------------------------------------------------------
+// gathered fp64 tensor-core GEMM
+//
+// task = (mat, pairs [b, b+cnt), r0): for its pairs (tgt, src) and rhs r the
+// CTA computes C[tgt][r][rows] += A_mat[rows][:] . B[src][r][:], rows = its
+// MT-row tile.  Columns n = j*Rc + (r - r0).  Warp tile 32x32 = 2 x 4
+// m16n8k8 fragments; A comes pre-tiled (one contiguous chunk per stage),
+// B columns are gathered with cp.async (zero-filled when a column is empty).
+// Tasks of one offset are consecutive so the 148 SMs share G[o] in L2.
+// The epilogue adds with fp64 RED into L2-resident accumulators; rows of one
+// target get contributions from many offsets.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void mma_m16n8k8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+template <int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32, 2)
+    gemm_gather_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
+                       double* __restrict__ C, const GemmTask* __restrict__ tasks,
+                       const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
+                       int RT) {
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC, BST = KC + 4;
+  constexpr int NTH = WM * WN * 32;
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * MT * KC;
+  __shared__ int64_t colB[NT];
+  __shared__ int64_t colC[NT];
+
+  const int task = blockIdx.x / RT, rt = blockIdx.x % RT;
+  const GemmTask tk = tasks[task];
+  for (int n = threadIdx.x; n < NT; n += NTH) {
+    int j = n / Rc, r = tk.r0 + n % Rc;
+    if (j < tk.pair_count && r < R) {
+      int2 pr = pairs[tk.pair_begin + j];
+      colB[n] = ((int64_t)pr.y * R + r) * K_pad;
+      colC[n] = ((int64_t)pr.x * R + r) * ldc;
+    } else {
+      colB[n] = -1;
+      colC[n] = -1;
+    }
+  }
+  __syncthreads();
+
+  const double* Ablk = A + (int64_t)tk.mat * mat_stride + (int64_t)rt * MT * K_pad;
+  const int nk = K_pad / KC;
+  const int tid = threadIdx.x;
+
+  auto load_stage = [&](int kc, int st) {
+    const double* src = Ablk + (int64_t)kc * (MT * KC);
+    double* dA = sA + st * MT * KC;
+#pragma unroll
+    for (int i = tid; i < MT * KC / 2; i += NTH) cp_async16(dA + 2 * i, src + 2 * i, 16);
+    double* dB = sB + st * NT * BST;
+#pragma unroll
+    for (int i = tid; i < NT * KC / 2; i += NTH) {
+      int n = i / (KC / 2), c2 = i % (KC / 2);
+      int64_t cb = colB[n];
+      const double* g = cb >= 0 ? B + cb + kc * KC + 2 * c2 : B;
+      cp_async16(dB + n * BST + 2 * c2, g, cb >= 0 ? 16 : 0);
+    }
+  };
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    int nxt = kc + STAGES - 1;
+    if (nxt < nk) load_stage(nxt, nxt % STAGES);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    const double* cA = sA + (kc % STAGES) * MT * KC;
+    const double* cB = sB + (kc % STAGES) * NT * BST;
+#pragma unroll
+    for (int ks = 0; ks < KC / 8; ++ks) {
+      double a[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const double2* pa = reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
+        double2 v0 = pa[0], v1 = pa[1];
+        a[mi][0] = v0.x;
+        a[mi][1] = v0.y;
+        a[mi][2] = v1.x;
+        a[mi][3] = v1.y;
+      }
+      double b[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const double* pb = cB + (wn * 32 + ni * 8 + g) * BST + ks * 8 + t;
+        b[ni][0] = pb[0];
+        b[ni][1] = pb[4];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) mma_m16n8k8(acc[mi][ni], a[mi], b[ni]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+    for (int cix = 0; cix < 2; ++cix) {
+      int n = wn * 32 + ni * 8 + 2 * t + cix;
+      int64_t cc = colC[n];
+      if (cc < 0) continue;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          int m = rt * MT + wm * 32 + mi * 16 + g + 8 * hi;
+          if (m < M_valid) atomicAdd(C + cc + m, acc[mi][ni][2 * hi + cix]);
+        }
+      }
+    }
+  }
+}
+
+int gemm_mt_for(int P_out) { return P_out <= 64 ? 64 : 128; }
+int gemm_nt(int MT) { return 64; }
+
+template <int WM, int WN, int STAGES>
+static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, double* C,
+                          const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                          int M_valid, int ldc, int RT, cudaStream_t st) {
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC;
+  size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4));
+  cudaFuncSetAttribute(gemm_gather_kernel<WM, WN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  int64_t nblocks = (int64_t)ntasks * RT;
+  if (nblocks == 0) return;
+  gemm_gather_kernel<WM, WN, STAGES><<<(unsigned)nblocks, WM * WN * 32, smem, st>>>(
+      A, mat_stride, B, C, tasks, pairs, R, Rc, K_pad, M_valid, ldc, RT);
+}
+
+void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                 int M_valid, int ldc, int RT, cudaStream_t st) {
+  if (MT == 64)
+    launch_gemm_t<2, 2, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+  else
+    launch_gemm_t<4, 2, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+}
+
+// ---------------------------------------------------------------------------
+// fused downward pass + epilogue: one CTA per (leaf box, rhs)
+//   facc = sum_l (U_l[sub] x U_l[sub] x U_l[sub]) H_l[ancestor]
+//   f    = facc + Y + a u      (scattered back to F-order)
+// ---------------------------------------------------------------------------
+__global__ void downward_kernel(const double* __restrict__ u, double* __restrict__ f,
+                                const double* __restrict__ Y, int ldy, const double* __restrict__ avec,
+                                double aconst, int d, int n, int sL, int L, int R, int p, DownParams dp) {
+  extern __shared__ double sm[];
+  const int PL = (d == 2) ? sL * sL : sL * sL * sL;
+  const int P = (d == 2) ? p * p : p * p * p;
+  double* facc = sm;                 // PL
+  double* Hs = facc + PL;            // P
+  double* E1 = Hs + P;               // sL * p^(d-1)
+  double* E2 = E1 + sL * ((d == 2) ? p : p * p);   // sL^2 * p (3-D only)
+  double* Us = E2 + ((d == 3) ? sL * sL * p : 0);  // d * sL * p
+  const int mL = n / sL;
+  const int b = blockIdx.x, r = blockIdx.y;
+  const int bc[3] = {b % mL, (b / mL) % mL, b / (mL * mL)};
+  for (int i = threadIdx.x; i < PL; i += blockDim.x) facc[i] = 0.0;
+  for (int li = 0; li < dp.nlev; ++li) {
+    const DownLevel lv = dp.lev[li];
+    const int shift = L - lv.level;
+    const int ml = n / lv.side;
+    int ac[3], off[3];
+    for (int a = 0; a < 3; ++a) {
+      ac[a] = bc[a] >> shift;
+      off[a] = (bc[a] - (ac[a] << shift)) * sL;
+    }
+    int64_t anc = ac[0] + (int64_t)ml * ac[1];
+    if (d == 3) anc += (int64_t)ml * ml * ac[2];
+    __syncthreads();
+    const double* Hsrc = lv.H + (anc * R + r) * (int64_t)lv.P;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) Hs[i] = Hsrc[i];
+    for (int i = threadIdx.x; i < d * sL * p; i += blockDim.x) {
+      int a = i / (sL * p), rem = i % (sL * p);
+      int x = rem / p, col = rem % p;
+      Us[i] = lv.Q[(off[a] + x) * p + col];
+    }
+    __syncthreads();
+    const double* U1 = Us;
+    const double* U2 = Us + sL * p;
+    const double* U3 = Us + 2 * sL * p;
+    if (d == 2) {
+      // E1[x + sL*a2] = sum_a1 U1[x][a1] H[a1 + p*a2]
+      for (int i = threadIdx.x; i < sL * p; i += blockDim.x) {
+        int x = i % sL, a2 = i / sL;
+        double v = 0.0;
+        for (int a1 = 0; a1 < p; ++a1) v += U1[x * p + a1] * Hs[a1 + p * a2];
+        E1[i] = v;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+        int x = i % sL, y = i / sL;
+        double v = 0.0;
+        for (int a2 = 0; a2 < p; ++a2) v += U2[y * p + a2] * E1[x + sL * a2];
+        facc[i] += v;
+      }
+    } else {
+      for (int i = threadIdx.x; i < sL * p * p; i += blockDim.x) {
+        int x = i % sL, a23 = i / sL;
+        double v = 0.0;
+        for (int a1 = 0; a1 < p; ++a1) v += U1[x * p + a1] * Hs[a1 + p * a23];
+        E1[i] = v;   // E1[x + sL*(a2 + p*a3)]
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < sL * sL * p; i += blockDim.x) {
+        int x = i % sL, y = (i / sL) % sL, a3 = i / (sL * sL);
+        double v = 0.0;
+        for (int a2 = 0; a2 < p; ++a2) v += U2[y * p + a2] * E1[x + sL * (a2 + p * a3)];
+        E2[i] = v;   // E2[x + sL*(y + sL*a3)]
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+        int xy = i % (sL * sL), z = i / (sL * sL);
+        double v = 0.0;
+        for (int a3 = 0; a3 < p; ++a3) v += U3[z * p + a3] * E2[xy + sL * sL * a3];
+        facc[i] += v;
+      }
+    }
+  }
+  __syncthreads();
+  const double* Yb = Y ? Y + ((int64_t)b * R + r) * ldy : nullptr;
+  for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+    int x = i % sL, y = (i / sL) % sL, z = i / (sL * sL);
+    int64_t gidx = (int64_t)(bc[0] * sL + x) + (int64_t)n * (bc[1] * sL + y);
+    if (d == 3) gidx += (int64_t)n * n * (bc[2] * sL + z);
+    double uv = u[gidx * R + r];
+    double a = avec ? avec[gidx] : aconst;
+    double v = facc[i];
+    if (Yb) v += Yb[i];
+    f[gidx * R + r] = v + a * uv;
+  }
+}
+
+void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
+                     double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
+                     cudaStream_t st) {
+  int mL = n / sL;
+  int nb = (d == 2) ? mL * mL : mL * mL * mL;
+  int P = (d == 2) ? p * p : p * p * p;
+  int PL = (d == 2) ? sL * sL : sL * sL * sL;
+  size_t words = PL + P + sL * ((d == 2) ? p : p * p) + ((d == 3) ? sL * sL * p : 0) + d * sL * p;
+  size_t smem = words * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(downward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  downward_kernel<<<dim3(nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, d, n, sL, L, R, p, dp);
+}
+
+}  // namespace htlr

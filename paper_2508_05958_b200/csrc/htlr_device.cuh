@@ -1,0 +1,66 @@
+// Shared device helpers for the B200 HTLR kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace htlr {
+
+// ---------------------------------------------------------------------------
+// kernel functions (kernels.py:88-103), arithmetic in the reference's order;
+// __dmul_rn/__dadd_rn keep nvcc from contracting r^2 into FMAs so r^2 is the
+// value numpy computes.
+// ---------------------------------------------------------------------------
+struct KernelParams {
+  int kind;        // 0 gaussian, 1 slp2d, 2 slp3d
+  double denom;    // gaussian: (2.0 * sigma) * sigma
+  double scale;    // multiplies the reference formula
+};
+
+__device__ __forceinline__ double kernel_from_r2(const KernelParams& kp, double r2) {
+  double v;
+  if (kp.kind == 0) {
+    v = exp(-r2 / kp.denom);
+  } else if (kp.kind == 1) {
+    v = (-0.5 * log(r2)) / (2.0 * 3.141592653589793);
+  } else {
+    v = 1.0 / ((4.0 * 3.141592653589793) * sqrt(r2));
+  }
+  return kp.scale == 1.0 ? v : kp.scale * v;
+}
+
+__device__ __forceinline__ double r2_of(int d, const double* x, const double* y) {
+  double d0 = __dadd_rn(x[0], -y[0]);
+  double r2 = __dmul_rn(d0, d0);
+  double d1 = __dadd_rn(x[1], -y[1]);
+  r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+  if (d == 3) {
+    double d2 = __dadd_rn(x[2], -y[2]);
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+  }
+  return r2;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM A-operand tiling.  Every deduplicated core / near block is stored
+// pre-tiled for mma.sync.m16n8k8.f64 so a CTA stage (MT rows x KC cols) is one
+// contiguous chunk and each lane's fragment (a0..a3) is 32 contiguous bytes:
+//   [row tile][k chunk][m16 block][k8 block][lane][4]
+// lane = g*4 + t holds A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4].
+// ---------------------------------------------------------------------------
+constexpr int kKC = 32;
+
+__host__ __device__ __forceinline__ int64_t tiled_offset(int m, int k, int MT, int K_pad) {
+  int rt = m / MT, mm = m % MT;
+  int kc = k / kKC, kk = k % kKC;
+  int mi = mm >> 4, r16 = mm & 15;
+  int ki = kk >> 3, c8 = kk & 7;
+  int g = r16 & 7, hi = r16 >> 3;
+  int t = c8 & 3, hk = c8 >> 2;
+  int lane = g * 4 + t;
+  int reg = hi + 2 * hk;
+  int64_t chunk = (int64_t)rt * (K_pad / kKC) + kc;
+  return chunk * (int64_t)(MT * kKC) + (int64_t)((mi * (kKC / 8) + ki) * 128 + lane * 4 + reg);
+}
+
+}  // namespace htlr

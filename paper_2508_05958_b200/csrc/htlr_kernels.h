@@ -1,0 +1,85 @@
+// Kernel launch interface shared by the plan (htlr_plan.cu) and the kernel
+// translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "htlr_device.cuh"
+
+namespace htlr {
+
+constexpr int kMaxRank = 16;
+constexpr int kMaxLevels = 16;
+
+struct FactorJob {
+  int side;
+  double* Q;      // side x p row-major (identity when side == p)
+  double* R;      // p x p row-major (raw square factor when side == p)
+  double* work;   // side x p scratch
+  double* work2;  // side x p scratch
+};
+
+struct CoreJob {
+  int tlo[3];
+  int slo[3];
+  int side;
+  const double* R;   // level factor folded into the core
+  double* dst;       // tiled GEMM table slot
+};
+
+struct NearJob {
+  int tlo[3];
+  int slo[3];
+  int self;
+  double* dst;
+};
+
+// one GEMM task: rows of `mat` applied to up to NT columns (pairs x rhs)
+struct GemmTask {
+  int mat;
+  int pair_begin;
+  int pair_count;
+  int r0;
+};
+
+// coarse-level contribution gathered by the fused downward kernel
+struct DownLevel {
+  int level;
+  int side;        // box side at this level
+  int P;           // p^d
+  const double* Q; // side x p row-major
+  const double* H; // [cluster][R][P]
+};
+
+struct DownParams {
+  int nlev;
+  DownLevel lev[kMaxLevels];
+};
+
+void launch_diag(const KernelParams& kp, int d, double h, int q, const double* gx, const double* gw,
+                 int singular, double* out, cudaStream_t st);
+void launch_factor_qr(int nlev, const FactorJob* jobs, double h, int p, cudaStream_t st);
+void launch_core_batch(const CoreJob* jobs, int nbatch, int d, int p, double h, double hd,
+                       const KernelParams& kp, double* buf0, double* buf1, int MT, int M_pad, int K_pad,
+                       cudaStream_t st);
+void launch_near_blocks(const NearJob* jobs, int njobs, int d, int s, double h, double hd,
+                        const KernelParams& kp, const double* diag, int MT, int M_pad, int K_pad,
+                        cudaStream_t st);
+
+// matvec kernels (htlr_apply.cu)
+void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad,
+                       cudaStream_t st);
+void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
+                   int K_pad, const double* Q, cudaStream_t st);
+// MT selects the tile config (64 or 128)
+int gemm_mt_for(int P_out);
+void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                 int M_valid, int ldc, int RT, cudaStream_t st);
+int gemm_nt(int MT);
+void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
+                     double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
+                     cudaStream_t st);
+
+}  // namespace htlr

@@ -1,0 +1,201 @@
+// Cluster tree + block cluster tree, bit-exact with the reference.
+//
+// Reference: /root/reference/pkg/src/htlr/grids.py
+//   _leaf_side               :196-207   exact halving to the threshold
+//   build_cluster_tree       :210-234   midpoint split, children in
+//                                       np.ndindex order (last dim fastest)
+//   domain_of                :237-242   [lo*h, hi*h], h = 1.0/n
+//   DomainBox                :110-127   diameter_sq / distance_sq / overlap
+//   is_admissible            :153-165   strong: diam <= eta*eta*dist*(1+1e-12)
+//   build_block_cluster_tree :268-296   DFS, sigma children outer, tau inner
+//
+// Every level of the reference tree is uniform (all boxes at level l have
+// side n >> l, guaranteed by the exact halving), so a cluster is identified by
+// its integer coordinates at its level; children of c are 2c + combo.
+// This file must be compiled with -ffp-contract=off: the predicate is
+// evaluated with separate IEEE multiplies and adds in Python's order.
+#include "htlr_lists.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace htlr {
+
+int compute_leaf_side(int n, int leaf_side_max, int* side, std::string& err) {
+  if (leaf_side_max < 1) {
+    err = "leaf threshold must be positive";
+    return -1;
+  }
+  int s = n;
+  while (s > leaf_side_max) {
+    if (s % 2) {
+      char buf[160];
+      snprintf(buf, sizeof buf,
+               "grid side %d cannot be halved evenly down to the leaf threshold %d", n,
+               leaf_side_max);
+      err = buf;
+      return -1;
+    }
+    s /= 2;
+  }
+  *side = s;
+  return 0;
+}
+
+namespace {
+
+// Python: float(sum((b - a) ** 2 for a, b in intervals)); the int start 0
+// makes the first term exact, then sequential float adds.
+double diameter_sq(int d, const double* lo, const double* hi) {
+  double total = 0.0;
+  for (int a = 0; a < d; ++a) {
+    double e = hi[a] - lo[a];
+    double sq = e * e;   // pow(x, 2.0) is correctly rounded == x*x
+    total = (a == 0) ? sq : total + sq;
+  }
+  return total;
+}
+
+double distance_sq(int d, const double* lo1, const double* hi1, const double* lo2,
+                   const double* hi2) {
+  double total = 0.0;
+  for (int a = 0; a < d; ++a) {
+    double g1 = lo1[a] - hi2[a];
+    double g2 = lo2[a] - hi1[a];
+    double gap = g1;
+    if (g2 > gap) gap = g2;
+    if (0.0 > gap) gap = 0.0;
+    double sq = gap * gap;
+    total = total + sq;
+  }
+  return total;
+}
+
+double overlap_volume(int d, const double* lo1, const double* hi1, const double* lo2,
+                      const double* hi2) {
+  double vol = 1.0;
+  for (int a = 0; a < d; ++a) {
+    double mn = hi1[a] < hi2[a] ? hi1[a] : hi2[a];
+    double mx = lo1[a] > lo2[a] ? lo1[a] : lo2[a];
+    double length = mn - mx;
+    if (length <= 0.0) return 0.0;
+    vol = vol * length;
+  }
+  return vol;
+}
+
+}  // namespace
+
+bool admissible_boxes(const TreeSpec& spec, const int* tlo, const int* thi, const int* slo,
+                      const int* shi) {
+  const double h = 1.0 / (double)spec.n;
+  double a1[3], b1[3], a2[3], b2[3];
+  for (int a = 0; a < spec.d; ++a) {
+    a1[a] = (double)tlo[a] * h;
+    b1[a] = (double)thi[a] * h;
+    a2[a] = (double)slo[a] * h;
+    b2[a] = (double)shi[a] * h;
+  }
+  if (spec.rule == 0) return overlap_volume(spec.d, a1, b1, a2, b2) == 0.0;
+  double dist = distance_sq(spec.d, a1, b1, a2, b2);
+  double dt = diameter_sq(spec.d, a1, b1);
+  double ds = diameter_sq(spec.d, a2, b2);
+  double diam = dt >= ds ? dt : ds;   // Python max() keeps the first on ties
+  double rhs = spec.eta * spec.eta;
+  rhs = rhs * dist;
+  rhs = rhs * (1.0 + 1e-12);
+  return diam <= rhs;
+}
+
+namespace {
+
+struct Builder {
+  const TreeSpec& spec;
+  Tree& tree;
+  int combos[8][3];
+  int ncombo;
+
+  explicit Builder(const TreeSpec& s, Tree& t) : spec(s), tree(t) {
+    // np.ndindex(*([2] * d)): last dimension varies fastest
+    ncombo = 1 << spec.d;
+    for (int i = 0; i < ncombo; ++i) {
+      for (int a = 0; a < spec.d; ++a) {
+        int shift = spec.d - 1 - a;
+        combos[i][a] = (i >> shift) & 1;
+      }
+    }
+  }
+
+  void visit(const int* tc, const int* sc, int level) {
+    const int side = tree.side(level);
+    int tlo[3], thi[3], slo[3], shi[3];
+    for (int a = 0; a < spec.d; ++a) {
+      tlo[a] = tc[a] * side;
+      thi[a] = tlo[a] + side;
+      slo[a] = sc[a] * side;
+      shi[a] = slo[a] + side;
+    }
+    if (admissible_boxes(spec, tlo, thi, slo, shi)) {
+      push(0, level, tc, sc);
+      return;
+    }
+    if (level == tree.depth) {   // both leaves (lock-step refinement)
+      push(1, level, tc, sc);
+      return;
+    }
+    int tk[3], sk[3];
+    for (int si = 0; si < ncombo; ++si) {
+      for (int a = 0; a < spec.d; ++a) sk[a] = 2 * sc[a] + combos[si][a];
+      for (int ti = 0; ti < ncombo; ++ti) {
+        for (int a = 0; a < spec.d; ++a) tk[a] = 2 * tc[a] + combos[ti][a];
+        visit(tk, sk, level + 1);
+      }
+    }
+  }
+
+  void push(int kind, int level, const int* tc, const int* sc) {
+    LeafRec r;
+    r.kind = kind;
+    r.level = level;
+    for (int a = 0; a < 3; ++a) {
+      r.tc[a] = a < spec.d ? tc[a] : 0;
+      r.sc[a] = a < spec.d ? sc[a] : 0;
+    }
+    tree.leaves.push_back(r);
+    if (kind == 0)
+      ++tree.num_adm;
+    else
+      ++tree.num_near;
+  }
+};
+
+}  // namespace
+
+int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
+  if (spec.d != 2 && spec.d != 3) {
+    err = "only d = 2 and d = 3 are supported";
+    return -1;
+  }
+  if (spec.n < 1) {
+    err = "n must be positive";
+    return -1;
+  }
+  if (spec.rule == 1 && !(spec.eta > 0)) {
+    err = "strong admissibility needs eta > 0";
+    return -1;
+  }
+  int side = 0;
+  if (compute_leaf_side(spec.n, spec.leaf_side_max, &side, err)) return -1;
+  out = Tree();
+  out.spec = spec;
+  out.leaf_side = side;
+  int depth = 0;
+  for (int s = spec.n; s > side; s /= 2) ++depth;
+  out.depth = depth;
+  Builder b(spec, out);
+  int root[3] = {0, 0, 0};
+  b.visit(root, root, 0);
+  return 0;
+}
+
+}  // namespace htlr

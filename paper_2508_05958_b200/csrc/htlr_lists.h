@@ -1,0 +1,49 @@
+// Host-side cluster tree / block cluster tree for the B200 HTLR plan.
+//
+// Restates grids.py:196-296 of the reference with IEEE-double arithmetic in
+// the reference's evaluation order (compiled with -ffp-contract=off), so the
+// DFS leaf list is bit-identical to BlockClusterTree.leaves.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace htlr {
+
+struct TreeSpec {
+  int d = 3;
+  int n = 0;
+  int leaf_side_max = 0;
+  int rule = 1;        // 0 weak, 1 strong
+  double eta = 1.0;
+};
+
+// One admissible or inadmissible leaf, in cluster coordinates of its level.
+struct LeafRec {
+  int32_t kind;        // 0 admissible, 1 inadmissible
+  int32_t level;
+  int32_t tc[3];       // target cluster coords (box lo = tc * side(level))
+  int32_t sc[3];       // source cluster coords
+};
+
+struct Tree {
+  TreeSpec spec;
+  int leaf_side = 0;   // side of the leaf boxes (grids.py:196-207)
+  int depth = 0;       // number of halvings
+  std::vector<LeafRec> leaves;   // DFS order == reference leaf_id order
+  int64_t num_adm = 0, num_near = 0;
+
+  int side(int level) const { return spec.n >> level; }
+  int clusters_per_dim(int level) const { return 1 << level; }
+};
+
+// Returns 0 on success, negative with `err` set on invalid input.
+int compute_leaf_side(int n, int leaf_side_max, int* side, std::string& err);
+int build_tree(const TreeSpec& spec, Tree& out, std::string& err);
+
+// Reference admissibility predicate on index boxes (grids.py:110-127,153-165).
+bool admissible_boxes(const TreeSpec& spec, const int* tlo, const int* thi,
+                      const int* slo, const int* shi);
+
+}  // namespace htlr

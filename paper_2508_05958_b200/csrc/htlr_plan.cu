@@ -1,0 +1,780 @@
+// C ABI (include/htlr_b200.h) and host orchestration of the B200 HTLR plan.
+//
+// construct (operators.py:121-126):
+//   host   : block cluster tree, bit-exact DFS leaf list (htlr_lists.cpp)
+//            -> per level: admissible (tgt, src) pairs keyed by the unique
+//               cluster offset; leaf level: inadmissible pairs likewise
+//   device : diagonal quadrature, per-level factor + QR, one core per unique
+//            (level, offset), one dense block per unique near offset, all
+//            stored pre-tiled for the fp64 tensor-core GEMM
+// matvec (operators.py:138-161):
+//   permute_in -> upward (per level) -> gathered GEMM passes -> fused downward
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/htlr_b200.h"
+#include "htlr_kernels.h"
+#include "htlr_lists.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(1, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+  } while (0)
+
+int ipow(int b, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int alloc(size_t nbytes) {
+    if (nbytes <= bytes && ptr) return 0;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    if (nbytes == 0) return 0;
+    cudaError_t e = cudaMalloc(&ptr, nbytes);
+    if (e != cudaSuccess) return fail(1, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    bytes = nbytes;
+    return 0;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(ptr); }
+};
+
+// A batched gathered-GEMM pass over one interaction list.
+struct Pass {
+  int level = 0;
+  int P = 0;               // rows == cols of every matrix (p^d or leaf side^d)
+  int MT = 128, M_pad = 0, K_pad = 0, RT = 0;
+  int64_t mat_stride = 0;  // doubles per tiled matrix
+  int nmats = 0;
+  DevBuf table;            // tiled matrices
+  std::vector<int> seg;    // pairs of matrix i: [seg[i], seg[i+1])
+  DevBuf pairs;            // int2 (tgt, src), sorted by (matrix, tgt)
+  std::vector<int2> pairs_host;
+  int npairs = 0;
+  std::map<int, std::pair<DevBuf, int>> tasks;   // per R
+  bool from_ub = false;    // B operand = leaf-box-major u (else W of `level`)
+  bool to_y = false;       // C accumulator = Y (else H of `level`)
+};
+
+struct OffsetTable {
+  std::unordered_map<int64_t, int> id;   // packed offset -> id
+  std::vector<std::array<int, 6>> rep;    // representative (tc, sc)
+  std::vector<std::vector<std::pair<int, int>>> members;   // (tgt, src) per id
+};
+
+int64_t pack_offset(const int* tc, const int* sc, int d, int m) {
+  int64_t key = 0;
+  for (int a = d - 1; a >= 0; --a) key = key * (2 * m + 1) + (sc[a] - tc[a] + m);
+  return key;
+}
+
+struct Level {
+  int level = 0, side = 0, m = 0;
+  int64_t nclusters = 0;
+  int64_t num_adm = 0;
+  OffsetTable adm;
+  DevBuf Q, R;             // side x p, p x p
+  DevBuf W, H;             // workspaces
+  bool needs_up = false;   // W via upward pass, H via downward pass
+};
+
+}  // namespace
+
+struct htlr_plan {
+  htlr_desc desc{};
+  int device = 0;
+  htlr::Tree tree;
+  bool lists_built = false, constructed = false;
+  int d = 3, n = 0, p = 0, L = 0, sL = 0;
+  int64_t N = 0;
+  double h = 0, hd = 0;
+  htlr::KernelParams kp{};
+  std::vector<Level> levels;
+  OffsetTable near;
+  int64_t num_near = 0;
+  std::vector<Pass> passes;   // adm passes for non-merged levels, then the leaf pass
+  int leaf_pass = -1;
+  int near_mats = 0;          // leaf pass: matrices [0, near_mats) are near blocks
+  bool merged = false;        // leaf-level admissible cores live in the leaf pass
+  DevBuf diag, coeff, gl, ub, Y;
+  bool has_coeff = false;
+  int ws_R = 0;
+  int64_t last_launches = 0;
+  int64_t device_scalars = 0;
+};
+
+using htlr::Tree;
+
+namespace {
+
+// Gauss-Legendre nodes/weights on [0,1] (kernels.py:195-198 maps numpy's
+// leggauss rule the same way); Newton on P_q.
+void gauss01(int q, std::vector<double>& x, std::vector<double>& w) {
+  x.resize(q);
+  w.resize(q);
+  for (int i = 0; i < q; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (q + 0.5));
+    double pp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= q; ++j) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = q * (z * p1 - p2) / (z * z - 1.0);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-17) break;
+    }
+    double p1 = 1.0, p2 = 0.0;
+    for (int j = 1; j <= q; ++j) {
+      double p3 = p2;
+      p2 = p1;
+      p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+    }
+    pp = q * (z * p1 - p2) / (z * z - 1.0);
+    double wt = 2.0 / ((1.0 - z * z) * pp * pp);
+    x[i] = 0.5 * (-z + 1.0);   // ascending after the map
+    w[i] = 0.5 * wt;
+  }
+}
+
+int validate(const htlr_desc& ds, std::string& err) {
+  if (ds.d != 2 && ds.d != 3) return err = "only d = 2 and d = 3 are supported", -1;
+  if (ds.n < 1) return err = "n must be positive", -1;
+  if (ds.rank < 1) return err = "rank must be positive", -1;
+  if (ds.rank > htlr::kMaxRank) return err = "rank above the B200 kernel limit (16)", -1;
+  if (ds.rule != 0 && ds.rule != 1) return err = "kind must be 'weak' or 'strong'", -1;
+  if (ds.rule == 1 && !(ds.eta > 0)) return err = "strong admissibility needs eta > 0", -1;
+  if (ds.kernel < 0 || ds.kernel > 2) return err = "unknown kernel kind", -1;
+  if (ds.kernel == HTLR_KERNEL_GAUSSIAN && !(ds.sigma > 0)) return err = "gaussian kernel needs sigma > 0", -1;
+  if (ds.kernel == HTLR_KERNEL_SLP2D && ds.d != 2) return err = "slp2d requires dimension 2", -1;
+  if (ds.kernel == HTLR_KERNEL_SLP3D && ds.d != 3) return err = "slp3d requires dimension 3", -1;
+  if (ds.quad_q < 2) return err = "quadrature order must be >= 2", -1;
+  if (ds.quad_q > 64) return err = "quadrature order above 64", -1;
+  return 0;
+}
+
+int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
+  const int NT = htlr::gemm_nt(ps.MT);
+  const int Rc = std::min(R, NT);
+  const int npt = std::max(1, NT / Rc);
+  out.clear();
+  for (int mat = 0; mat < ps.nmats; ++mat) {
+    for (int b = ps.seg[mat]; b < ps.seg[mat + 1]; b += npt) {
+      int cnt = std::min(npt, ps.seg[mat + 1] - b);
+      for (int r0 = 0; r0 < R; r0 += Rc) out.push_back({mat, b, cnt, r0});
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* htlr_last_error(void) { return g_last_error.c_str(); }
+
+int htlr_plan_create(const htlr_desc* desc, int device, htlr_plan** out) {
+  if (!desc || !out) return fail(-1, "null argument");
+  std::string err;
+  if (validate(*desc, err)) return fail(-1, err);
+  int side = 0;
+  if (htlr::compute_leaf_side(desc->n, desc->leaf_side_max, &side, err)) return fail(-1, err);
+  if (device != -1) {   // -1: host-only plan (trees, lists, accounting; no device work)
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      return fail(2, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(-1, "device index out of range");
+  }
+  htlr_plan* pl = new htlr_plan();
+  pl->desc = *desc;
+  pl->device = device;
+  pl->d = desc->d;
+  pl->n = desc->n;
+  pl->p = desc->rank;
+  pl->N = 1;
+  for (int a = 0; a < pl->d; ++a) pl->N *= desc->n;
+  pl->h = 1.0 / (double)desc->n;
+  pl->hd = std::pow(pl->h, (double)pl->d);   // Python h**d
+  pl->kp.kind = desc->kernel;
+  pl->kp.denom = (2.0 * desc->sigma) * desc->sigma;
+  pl->kp.scale = desc->scale;
+  *out = pl;
+  return 0;
+}
+
+int htlr_plan_destroy(htlr_plan* pl) {
+  if (!pl) return 0;
+  if (pl->device < 0) {
+    delete pl;
+    return 0;
+  }
+  cudaSetDevice(pl->device);
+  for (auto& lv : pl->levels) {
+    lv.Q.release();
+    lv.R.release();
+    lv.W.release();
+    lv.H.release();
+  }
+  for (auto& ps : pl->passes) {
+    ps.table.release();
+    ps.pairs.release();
+    for (auto& kv : ps.tasks) kv.second.first.release();
+  }
+  pl->diag.release();
+  pl->coeff.release();
+  pl->gl.release();
+  pl->ub.release();
+  pl->Y.release();
+  delete pl;
+  return 0;
+}
+
+int htlr_build_lists(htlr_plan* pl) {
+  if (!pl) return fail(-1, "null plan");
+  htlr::TreeSpec ts;
+  ts.d = pl->d;
+  ts.n = pl->n;
+  ts.leaf_side_max = pl->desc.leaf_side_max;
+  ts.rule = pl->desc.rule;
+  ts.eta = pl->desc.eta;
+  std::string err;
+  if (htlr::build_tree(ts, pl->tree, err)) return fail(-1, err);
+  const Tree& tr = pl->tree;
+  pl->L = tr.depth;
+  pl->sL = tr.leaf_side;
+  const int d = pl->d, p = pl->p;
+  pl->levels.assign(pl->L + 1, Level());
+  for (int l = 0; l <= pl->L; ++l) {
+    Level& lv = pl->levels[l];
+    lv.level = l;
+    lv.side = tr.side(l);
+    lv.m = tr.clusters_per_dim(l);
+    lv.nclusters = 1;
+    for (int a = 0; a < d; ++a) lv.nclusters *= lv.m;
+  }
+  pl->near = OffsetTable();
+  pl->num_near = 0;
+  for (const auto& lf : tr.leaves) {
+    OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
+    const int m = pl->levels[lf.level].m;
+    int64_t key = pack_offset(lf.tc, lf.sc, d, m);
+    auto it = tab.id.find(key);
+    int id;
+    if (it == tab.id.end()) {
+      id = (int)tab.rep.size();
+      tab.id.emplace(key, id);
+      tab.rep.push_back({lf.tc[0], lf.tc[1], lf.tc[2], lf.sc[0], lf.sc[1], lf.sc[2]});
+      tab.members.emplace_back();
+    } else {
+      id = it->second;
+    }
+    int64_t tl = lf.tc[0] + (int64_t)m * lf.tc[1] + (int64_t)m * m * (d == 3 ? lf.tc[2] : 0);
+    int64_t sl = lf.sc[0] + (int64_t)m * lf.sc[1] + (int64_t)m * m * (d == 3 ? lf.sc[2] : 0);
+    tab.members[id].emplace_back((int)tl, (int)sl);
+    if (lf.kind == 0)
+      pl->levels[lf.level].num_adm++;
+    else
+      pl->num_near++;
+  }
+  // validation the reference performs at build time (tensor.py:112-113 via
+  // blocks.py:160): admissible blocks need box side >= rank
+  for (const auto& lv : pl->levels) {
+    if (lv.num_adm > 0 && lv.side < p) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "qr requires rows >= cols, got shape (%d, %d)", lv.side, p);
+      return fail(-1, buf);
+    }
+  }
+  const int PL = ipow(pl->sL, d);
+  const int P = ipow(p, d);
+  if (PL > 4096) return fail(-1, "leaf boxes above 4096 points are not supported by the B200 path");
+  if (P > 4096) return fail(-1, "rank^d above 4096 is not supported by the B200 path");
+  pl->merged = pl->levels[pl->L].num_adm > 0 && pl->sL == p;
+  // passes
+  pl->passes.clear();
+  auto fill_pass = [&](Pass& ps, std::vector<const OffsetTable*> tabs) {
+    ps.MT = htlr::gemm_mt_for(ps.P);
+    ps.M_pad = round_up(ps.P, ps.MT);
+    ps.K_pad = round_up(ps.P, htlr::kKC);
+    ps.RT = ps.M_pad / ps.MT;
+    ps.mat_stride = (int64_t)ps.M_pad * ps.K_pad;
+    ps.seg.assign(1, 0);
+    std::vector<int2> pr;
+    for (const OffsetTable* tab : tabs) {
+      for (const auto& mem : tab->members) {
+        std::vector<std::pair<int, int>> v = mem;
+        std::sort(v.begin(), v.end());
+        for (auto& q : v) pr.push_back(make_int2(q.first, q.second));
+        ps.seg.push_back((int)pr.size());
+      }
+    }
+    ps.nmats = (int)ps.seg.size() - 1;
+    ps.npairs = (int)pr.size();
+    ps.pairs_host.swap(pr);
+    return 0;
+  };
+  for (int l = 0; l <= pl->L; ++l) {
+    Level& lv = pl->levels[l];
+    lv.needs_up = lv.num_adm > 0 && !(l == pl->L && pl->merged);
+    if (!lv.needs_up) continue;
+    pl->passes.emplace_back();
+    Pass& ps = pl->passes.back();
+    ps.level = l;
+    ps.P = P;
+    ps.from_ub = false;
+    ps.to_y = false;
+    if (fill_pass(ps, {&lv.adm})) return 1;
+  }
+  pl->passes.emplace_back();
+  pl->leaf_pass = (int)pl->passes.size() - 1;
+  {
+    Pass& ps = pl->passes.back();
+    ps.level = pl->L;
+    ps.P = PL;
+    ps.from_ub = true;
+    ps.to_y = true;
+    std::vector<const OffsetTable*> tabs = {&pl->near};
+    if (pl->merged) tabs.push_back(&pl->levels[pl->L].adm);
+    pl->near_mats = (int)pl->near.members.size();
+    if (fill_pass(ps, tabs)) return 1;
+  }
+  pl->lists_built = true;
+  pl->constructed = false;
+  return 0;
+}
+
+int htlr_tree_info(const htlr_plan* pl, int32_t* depth, int32_t* leaf_side, int64_t* num_leaves,
+                   int64_t* num_adm, int64_t* num_near) {
+  if (!pl) return fail(-1, "null plan");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  if (depth) *depth = pl->tree.depth;
+  if (leaf_side) *leaf_side = pl->tree.leaf_side;
+  if (num_leaves) *num_leaves = (int64_t)pl->tree.leaves.size();
+  if (num_adm) *num_adm = pl->tree.num_adm;
+  if (num_near) *num_near = pl->tree.num_near;
+  return 0;
+}
+
+int htlr_export_lists(const htlr_plan* pl, int32_t* rows, int64_t cap) {
+  if (!pl || !rows) return fail(-1, "null argument");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  const int d = pl->d, w = 3 + 4 * d;
+  const auto& lv = pl->tree.leaves;
+  if (cap < (int64_t)lv.size() * w) return fail(-1, "export buffer too small");
+  for (size_t i = 0; i < lv.size(); ++i) {
+    int32_t* r = rows + i * w;
+    const int side = pl->tree.side(lv[i].level);
+    r[0] = (int32_t)i;
+    r[1] = lv[i].kind;
+    r[2] = lv[i].level;
+    for (int a = 0; a < d; ++a) {
+      r[3 + 2 * a] = lv[i].tc[a] * side;
+      r[4 + 2 * a] = lv[i].tc[a] * side + side;
+      r[3 + 2 * d + 2 * a] = lv[i].sc[a] * side;
+      r[4 + 2 * d + 2 * a] = lv[i].sc[a] * side + side;
+    }
+  }
+  return 0;
+}
+
+int htlr_set_coeff(htlr_plan* pl, const double* a_host) {
+  if (!pl) return fail(-1, "null plan");
+  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  if (!a_host) {
+    pl->has_coeff = false;
+    return 0;
+  }
+  if (pl->coeff.alloc(pl->N * sizeof(double))) return 1;
+  CUDA_TRY(cudaMemcpy(pl->coeff.ptr, a_host, pl->N * sizeof(double), cudaMemcpyHostToDevice));
+  pl->has_coeff = true;
+  return 0;
+}
+
+int htlr_construct(htlr_plan* pl, void* stream) {
+  if (!pl) return fail(-1, "null plan");
+  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
+  if (!pl->lists_built) {
+    int rc = htlr_build_lists(pl);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (auto& ps : pl->passes) {
+    if (ps.pairs.alloc(std::max<size_t>(1, ps.pairs_host.size()) * sizeof(int2))) return 1;
+    if (!ps.pairs_host.empty())
+      CUDA_TRY(cudaMemcpy(ps.pairs.ptr, ps.pairs_host.data(), ps.pairs_host.size() * sizeof(int2),
+                          cudaMemcpyHostToDevice));
+  }
+  const int d = pl->d, p = pl->p;
+  // diagonal cell average (operators.py:95-99)
+  std::vector<double> gx, gw;
+  gauss01(pl->desc.quad_q, gx, gw);
+  if (pl->gl.alloc(2 * gx.size() * sizeof(double))) return 1;
+  if (pl->diag.alloc(sizeof(double))) return 1;
+  std::vector<double> glh(gx);
+  glh.insert(glh.end(), gw.begin(), gw.end());
+  CUDA_TRY(cudaMemcpyAsync(pl->gl.ptr, glh.data(), glh.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  const bool singular = pl->desc.corner_subdivision != 0;   // caller: !smooth_at_diagonal && corner_subdivision
+  htlr::launch_diag(pl->kp, d, pl->h, pl->desc.quad_q, pl->gl.d(), pl->gl.d() + gx.size(), singular ? 1 : 0,
+                    pl->diag.d(), st);
+  // per-level factors (one representative box per level)
+  std::vector<htlr::FactorJob> fj;
+  std::vector<int> fj_level;
+  DevBuf scratch;
+  size_t scratch_words = 0;
+  for (auto& lv : pl->levels)
+    if (lv.num_adm > 0) scratch_words += 2 * (size_t)lv.side * p;
+  if (scratch.alloc(std::max<size_t>(scratch_words, 1) * sizeof(double))) return 1;
+  size_t soff = 0;
+  for (auto& lv : pl->levels) {
+    if (lv.num_adm == 0) continue;
+    if (lv.Q.alloc((size_t)lv.side * p * sizeof(double))) return 1;
+    if (lv.R.alloc((size_t)p * p * sizeof(double))) return 1;
+    htlr::FactorJob j;
+    j.side = lv.side;
+    j.Q = lv.Q.d();
+    j.R = lv.R.d();
+    j.work = scratch.d() + soff;
+    soff += (size_t)lv.side * p;
+    j.work2 = scratch.d() + soff;
+    soff += (size_t)lv.side * p;
+    fj.push_back(j);
+  }
+  DevBuf jobsbuf;
+  if (!fj.empty()) {
+    if (jobsbuf.alloc(fj.size() * sizeof(htlr::FactorJob))) return 1;
+    CUDA_TRY(cudaMemcpyAsync(jobsbuf.ptr, fj.data(), fj.size() * sizeof(htlr::FactorJob), cudaMemcpyHostToDevice, st));
+    htlr::launch_factor_qr((int)fj.size(), (const htlr::FactorJob*)jobsbuf.ptr, pl->h, p, st);
+  }
+  // tables
+  pl->device_scalars = 0;
+  for (auto& ps : pl->passes) {
+    if (ps.table.alloc((size_t)ps.nmats * ps.mat_stride * sizeof(double))) return 1;
+    pl->device_scalars += (int64_t)ps.nmats * ps.mat_stride;
+  }
+  // cores, batched
+  const int P = ipow(p, d);
+  const int64_t PP = (int64_t)P * P;
+  int batch = (int)std::max<int64_t>(1, std::min<int64_t>(512, (int64_t)(256ll << 20) / (PP * 8)));
+  DevBuf cbuf0, cbuf1, cjobs;
+  std::vector<htlr::CoreJob> cj;
+  auto flush_cores = [&](int MT, int M_pad, int K_pad) -> int {
+    if (cj.empty()) return 0;
+    if (cjobs.alloc(cj.size() * sizeof(htlr::CoreJob))) return 1;
+    CUDA_TRY(cudaMemcpyAsync(cjobs.ptr, cj.data(), cj.size() * sizeof(htlr::CoreJob), cudaMemcpyHostToDevice, st));
+    htlr::launch_core_batch((const htlr::CoreJob*)cjobs.ptr, (int)cj.size(), d, p, pl->h, pl->hd, pl->kp,
+                            cbuf0.d(), cbuf1.d(), MT, M_pad, K_pad, st);
+    // the job array is reused: wait before overwriting it
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cj.clear();
+    return 0;
+  };
+  for (int l = 0; l <= pl->L; ++l) {
+    Level& lv = pl->levels[l];
+    if (lv.num_adm == 0) continue;
+    Pass* ps = nullptr;
+    int mat0 = 0;
+    for (auto& q : pl->passes)
+      if (!q.to_y && q.level == l) ps = &q;
+    if (!ps) {
+      ps = &pl->passes[pl->leaf_pass];
+      mat0 = pl->near_mats;
+    }
+    if (cbuf0.alloc((size_t)batch * PP * sizeof(double))) return 1;
+    if (cbuf1.alloc((size_t)batch * PP * sizeof(double))) return 1;
+    for (size_t o = 0; o < lv.adm.rep.size(); ++o) {
+      htlr::CoreJob j;
+      for (int a = 0; a < 3; ++a) {
+        j.tlo[a] = lv.adm.rep[o][a] * lv.side;
+        j.slo[a] = lv.adm.rep[o][3 + a] * lv.side;
+      }
+      j.side = lv.side;
+      j.R = lv.R.d();
+      j.dst = ps->table.d() + (int64_t)(mat0 + o) * ps->mat_stride;
+      cj.push_back(j);
+      if ((int)cj.size() == batch && flush_cores(ps->MT, ps->M_pad, ps->K_pad)) return 1;
+    }
+    if (flush_cores(ps->MT, ps->M_pad, ps->K_pad)) return 1;
+  }
+  // unique near blocks
+  {
+    Pass& ps = pl->passes[pl->leaf_pass];
+    std::vector<htlr::NearJob> nj;
+    for (size_t o = 0; o < pl->near.rep.size(); ++o) {
+      htlr::NearJob j;
+      bool self = true;
+      for (int a = 0; a < 3; ++a) {
+        j.tlo[a] = pl->near.rep[o][a] * pl->sL;
+        j.slo[a] = pl->near.rep[o][3 + a] * pl->sL;
+        if (pl->near.rep[o][a] != pl->near.rep[o][3 + a]) self = false;
+      }
+      j.self = self ? 1 : 0;
+      j.dst = ps.table.d() + (int64_t)o * ps.mat_stride;
+      nj.push_back(j);
+    }
+    DevBuf njobs;
+    if (!nj.empty()) {
+      if (njobs.alloc(nj.size() * sizeof(htlr::NearJob))) return 1;
+      CUDA_TRY(cudaMemcpyAsync(njobs.ptr, nj.data(), nj.size() * sizeof(htlr::NearJob), cudaMemcpyHostToDevice, st));
+      htlr::launch_near_blocks((const htlr::NearJob*)njobs.ptr, (int)nj.size(), d, pl->sL, pl->h, pl->hd, pl->kp,
+                               pl->diag.d(), ps.MT, ps.M_pad, ps.K_pad, st);
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    njobs.release();
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  scratch.release();
+  jobsbuf.release();
+  cbuf0.release();
+  cbuf1.release();
+  cjobs.release();
+  pl->constructed = true;
+  return 0;
+}
+
+static int ensure_workspace(htlr_plan* pl, int R) {
+  if (pl->ws_R >= R) return 0;
+  const int d = pl->d, p = pl->p;
+  const int P = ipow(p, d);
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int64_t nleaf = pl->levels[pl->L].nclusters;
+  if (pl->ub.alloc((size_t)nleaf * R * lp.K_pad * sizeof(double))) return 1;
+  if (pl->Y.alloc((size_t)nleaf * R * lp.P * sizeof(double))) return 1;
+  for (auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    Level& lv = pl->levels[ps.level];
+    if (lv.W.alloc((size_t)lv.nclusters * R * ps.K_pad * sizeof(double))) return 1;
+    if (lv.H.alloc((size_t)lv.nclusters * R * P * sizeof(double))) return 1;
+  }
+  pl->ws_R = R;
+  return 0;
+}
+
+int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  if (!pl) return fail(-1, "null plan");
+  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  if (nrhs < 1 || nrhs > 4096) return fail(-1, "nrhs must be in [1, 4096]");
+  if (!u || !f) return fail(-1, "null vector");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int R = (int)nrhs;
+  const int d = pl->d, p = pl->p;
+  const int P = ipow(p, d);
+  if (ensure_workspace(pl, R)) return 1;
+  for (auto& ps : pl->passes) {
+    if (ps.tasks.count(R)) continue;
+    std::vector<htlr::GemmTask> tv;
+    make_tasks(ps, R, tv);
+    auto& slot = ps.tasks[R];
+    if (slot.first.alloc(std::max<size_t>(1, tv.size()) * sizeof(htlr::GemmTask))) return 1;
+    if (!tv.empty())
+      CUDA_TRY(cudaMemcpy(slot.first.ptr, tv.data(), tv.size() * sizeof(htlr::GemmTask), cudaMemcpyHostToDevice));
+    slot.second = (int)tv.size();
+  }
+  int64_t launches = 0;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  htlr::launch_permute_in(u, pl->ub.d(), d, pl->n, pl->sL, R, lp.K_pad, st);
+  ++launches;
+  for (auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    Level& lv = pl->levels[ps.level];
+    htlr::launch_upward(u, lv.W.d(), d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), st);
+    ++launches;
+    CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), st));
+  }
+  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)pl->levels[pl->L].nclusters * R * lp.P * sizeof(double), st));
+  for (auto& ps : pl->passes) {
+    auto& slot = ps.tasks[R];
+    if (slot.second == 0) continue;
+    const int NT = htlr::gemm_nt(ps.MT);
+    const int Rc = std::min(R, NT);
+    const double* B = ps.from_ub ? pl->ub.d() : pl->levels[ps.level].W.d();
+    double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
+    htlr::launch_gemm(ps.MT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
+                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, st);
+    ++launches;
+  }
+  htlr::DownParams dp{};
+  dp.nlev = 0;
+  for (auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    Level& lv = pl->levels[ps.level];
+    if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d()};
+  }
+  htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, d,
+                        pl->n, pl->sL, pl->L, R, p, dp, st);
+  ++launches;
+  CUDA_TRY(cudaGetLastError());
+  pl->last_launches = launches;
+  return 0;
+}
+
+int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,
+                      int32_t corner_subdivision, int device, double* out) {
+  if (!out) return fail(-1, "null argument");
+  if (!(h > 0)) return fail(-1, "cell width must be positive");
+  if (d != 2 && d != 3) return fail(-1, "only d = 2 and d = 3 are supported");
+  if (q < 2 || q > 64) return fail(-1, "quadrature order must be in [2, 64]");
+  if (kernel < 0 || kernel > 2) return fail(-1, "unknown kernel kind");
+  if (kernel == HTLR_KERNEL_GAUSSIAN && !(sigma > 0)) return fail(-1, "gaussian kernel needs sigma > 0");
+  CUDA_TRY(cudaSetDevice(device));
+  std::vector<double> gx, gw;
+  gauss01(q, gx, gw);
+  gx.insert(gx.end(), gw.begin(), gw.end());
+  DevBuf g, o;
+  if (g.alloc(gx.size() * sizeof(double)) || o.alloc(sizeof(double))) return 1;
+  CUDA_TRY(cudaMemcpy(g.ptr, gx.data(), gx.size() * sizeof(double), cudaMemcpyHostToDevice));
+  htlr::KernelParams kp;
+  kp.kind = kernel;
+  kp.denom = (2.0 * sigma) * sigma;
+  kp.scale = scale;
+  const bool singular = corner_subdivision != 0;
+  htlr::launch_diag(kp, d, h, q, g.d(), g.d() + q, singular ? 1 : 0, o.d(), 0);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpy(out, o.ptr, sizeof(double), cudaMemcpyDeviceToHost));
+  g.release();
+  o.release();
+  return 0;
+}
+
+int64_t htlr_last_launch_count(const htlr_plan* pl) { return pl ? pl->last_launches : -1; }
+
+int htlr_diag_value(htlr_plan* pl, double* out) {
+  if (!pl || !out) return fail(-1, "null argument");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out, pl->diag.ptr, sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int64_t cap, double* factors,
+                      int64_t factor_cap, int32_t* shapes) {
+  if (!pl || !core_or_dense || !shapes) return fail(-1, "null argument");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  if (leaf_id < 0 || leaf_id >= (int64_t)pl->tree.leaves.size()) return fail(-1, "leaf id out of range");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const auto& lf = pl->tree.leaves[leaf_id];
+  const int d = pl->d, p = pl->p;
+  const Level& lv = pl->levels[lf.level];
+  const OffsetTable& tab = lf.kind == 0 ? lv.adm : pl->near;
+  int64_t key = pack_offset(lf.tc, lf.sc, d, lv.m);
+  int id = tab.id.at(key);
+  const Pass* ps = nullptr;
+  int mat = id;
+  if (lf.kind == 0) {
+    for (auto& q : pl->passes)
+      if (!q.to_y && q.level == lf.level) ps = &q;
+    if (!ps) {
+      ps = &pl->passes[pl->leaf_pass];
+      mat = pl->near_mats + id;
+    }
+  } else {
+    ps = &pl->passes[pl->leaf_pass];
+  }
+  std::vector<double> tiled((size_t)ps->mat_stride);
+  CUDA_TRY(cudaMemcpy(tiled.data(), ps->table.d() + (int64_t)mat * ps->mat_stride, tiled.size() * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+  const int P = ps->P;
+  if ((int64_t)P * P > cap) return fail(-1, "block buffer too small");
+  shapes[0] = lf.kind;
+  shapes[1] = P;
+  shapes[2] = P;
+  shapes[3] = 0;
+  if (lf.kind == 0) {
+    // core tensor, F-order with target modes first: element (m, k) at m + P*k
+    for (int k = 0; k < P; ++k)
+      for (int m = 0; m < P; ++m) core_or_dense[m + (int64_t)P * k] = tiled[htlr::tiled_offset(m, k, ps->MT, ps->K_pad)];
+    if (lv.side != p) {
+      std::vector<double> q((size_t)lv.side * p);
+      CUDA_TRY(cudaMemcpy(q.data(), lv.Q.ptr, q.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      int64_t need = (int64_t)2 * d * lv.side * p;
+      if (!factors || factor_cap < need) return fail(-1, "factor buffer too small");
+      for (int f = 0; f < 2 * d; ++f) std::memcpy(factors + (int64_t)f * lv.side * p, q.data(), q.size() * sizeof(double));
+      shapes[3] = (int32_t)need;
+      shapes[1] = ipow(lv.side, d);
+      shapes[2] = ipow(lv.side, d);
+    }
+  } else {
+    // dense rows x cols, row-major, with a(x_i) on the tau == sigma diagonal
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j) core_or_dense[(int64_t)i * P + j] = tiled[htlr::tiled_offset(i, j, ps->MT, ps->K_pad)];
+    bool self = true;
+    for (int a = 0; a < d; ++a)
+      if (lf.tc[a] != lf.sc[a]) self = false;
+    if (self) {
+      std::vector<double> a(P, pl->desc.coeff_const);
+      if (pl->has_coeff) {
+        std::vector<double> all((size_t)pl->N);
+        CUDA_TRY(cudaMemcpy(all.data(), pl->coeff.ptr, all.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        const int s = pl->sL;
+        for (int k = 0; k < P; ++k) {
+          int x = k % s, y = (k / s) % s, z = k / (s * s);
+          int64_t g = (int64_t)(lf.tc[0] * s + x) + (int64_t)pl->n * (lf.tc[1] * s + y);
+          if (d == 3) g += (int64_t)pl->n * pl->n * (lf.tc[2] * s + z);
+          a[k] = all[g];
+        }
+      }
+      for (int i = 0; i < P; ++i) core_or_dense[(int64_t)i * P + i] += a[i];
+    }
+  }
+  return 0;
+}
+
+int htlr_storage(const htlr_plan* pl, int64_t out[5]) {
+  if (!pl || !out) return fail(-1, "null argument");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  const int d = pl->d, p = pl->p;
+  const int64_t PL = ipow(pl->sL, d);
+  int64_t dense = pl->num_near * PL * PL, fac = 0, core = 0;
+  for (const auto& lv : pl->levels) {
+    core += lv.num_adm * (int64_t)ipow(p, 2 * d);
+    if (lv.side != p) fac += lv.num_adm * (int64_t)2 * d * lv.side * p;
+  }
+  out[0] = dense;
+  out[1] = fac;
+  out[2] = core;
+  out[3] = dense + fac + core;
+  out[4] = pl->device_scalars;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+"""Hierarchical Tucker operator: construct and matvec on the B200 (drop-in for
+``htlr.operators``, /root/reference/pkg/src/htlr/operators.py).
+
+``construct`` builds the interaction lists (C++, bit-exact with the
+reference) and runs every numeric construction step on the device;
+``matvec`` / ``matmat`` apply the operator with the sm_100a kernels.  Host
+numpy vectors are accepted (copied to and from the device, as a drop-in for
+the reference's numpy API); CUDA torch tensors stay on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import warnings
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from .blocks import DenseBlock, TuckerBlock
+from .grids import (ADMISSIBLE, AdmissibilityRule, BlockClusterTree, UniformGrid,
+                    build_cluster_tree, export_leaf_array)
+from .kernels import CoefficientFn, KernelSpec, QuadratureConfig, singular_rule
+
+
+@dataclass(frozen=True)
+class BuildConfig:
+    """operators.py:38-59."""
+
+    rank: int
+    leaf_side: int
+    rule: AdmissibilityRule
+    kernel: KernelSpec
+    coeff: CoefficientFn
+    quadrature: QuadratureConfig = field(default_factory=QuadratureConfig)
+
+    def __post_init__(self):
+        if self.rank < 1:
+            raise ValueError("rank must be positive")
+        if not self.rank <= self.leaf_side <= 2 * self.rank:
+            warnings.warn(
+                f"leaf side {self.leaf_side} outside the recommended range "
+                f"[rank, 2*rank] = [{self.rank}, {2 * self.rank}]; the linear "
+                "storage bound assumes it",
+                stacklevel=2,
+            )
+
+
+@dataclass(frozen=True)
+class StorageReport:
+    dense_scalars: int
+    factor_scalars: int
+    core_scalars: int
+    total_scalars: int
+    theoretical_bound: float
+    device_scalars: int = 0   # what the B200 plan actually stores (deduplicated)
+
+
+def _desc(cfg: BuildConfig, grid: UniformGrid) -> _lib.HtlrDesc:
+    k = cfg.kernel
+    coeff = cfg.coeff.constant_value if cfg.coeff.constant_value is not None else 0.0
+    return _lib.HtlrDesc(
+        d=grid.d, n=grid.n, leaf_side_max=cfg.leaf_side, rank=cfg.rank,
+        rule=_lib.HTLR_RULE_WEAK if cfg.rule.kind == "weak" else _lib.HTLR_RULE_STRONG,
+        eta=float(cfg.rule.eta or 0.0), kernel=k.device_code, sigma=float(k.sigma or 0.0),
+        scale=float(k.scale), quad_q=int(cfg.quadrature.q),
+        corner_subdivision=singular_rule(k, cfg.quadrature), coeff_const=float(coeff))
+
+
+class _Payloads:
+    """Lazy leaf_id -> TuckerBlock | DenseBlock view (exports from the device)."""
+
+    def __init__(self, op: "HTLRMatrix"):
+        self._op = op
+
+    def __len__(self):
+        return self._op.num_leaves
+
+    def __getitem__(self, leaf_id: int):
+        if leaf_id < 0:
+            leaf_id += len(self)
+        return self._op.export_block(leaf_id)
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
+class HTLRMatrix:
+    """Device-resident HTLR operator (operators.py:62-71 attribute names)."""
+
+    def __init__(self, grid: UniformGrid, config: BuildConfig, device: int):
+        self.grid = grid
+        self.config = config
+        self.device = device
+        self._plan = ctypes.c_void_p()
+        _lib.check(_lib.lib().htlr_plan_create(ctypes.byref(_desc(config, grid)), device,
+                                               ctypes.byref(self._plan)))
+        self._block_tree: Optional[BlockClusterTree] = None
+        self.payloads = _Payloads(self)
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan:
+            try:
+                _lib.lib().htlr_plan_destroy(plan)
+            except Exception:
+                pass
+            self._plan = None
+
+    @property
+    def num_points(self) -> int:
+        return self.grid.num_points
+
+    def _info(self):
+        depth, side = ctypes.c_int32(), ctypes.c_int32()
+        nl, na, nn = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().htlr_tree_info(self._plan, ctypes.byref(depth), ctypes.byref(side),
+                                             ctypes.byref(nl), ctypes.byref(na), ctypes.byref(nn)))
+        return depth.value, side.value, nl.value, na.value, nn.value
+
+    @property
+    def num_leaves(self) -> int:
+        return self._info()[2]
+
+    @property
+    def block_tree(self) -> BlockClusterTree:
+        if self._block_tree is None:
+            arr = export_leaf_array(self._plan, self.grid.d)
+            tree = build_cluster_tree(self.grid, self.config.leaf_side)
+            self._block_tree = BlockClusterTree(self.grid, self.config.rule, tree, arr)
+        return self._block_tree
+
+    def diag_value(self) -> float:
+        out = ctypes.c_double()
+        _lib.check(_lib.lib().htlr_diag_value(self._plan, ctypes.byref(out)))
+        return out.value
+
+    def export_block(self, leaf_id: int):
+        """Reference-layout payload of one leaf (blocks.py:33-73)."""
+        depth, side, nl, _, _ = self._info()
+        d, p = self.grid.d, self.config.rank
+        cap = max(p ** (2 * d), side ** (2 * d))
+        buf = np.zeros(cap)
+        fac = np.zeros(2 * d * self.grid.n * p)
+        shapes = np.zeros(4, dtype=np.int32)
+        _lib.check(_lib.lib().htlr_export_block(self._plan, int(leaf_id), buf.ctypes.data, buf.size,
+                                                fac.ctypes.data, fac.size, shapes.ctypes.data))
+        kind, rows, cols, nfac = (int(v) for v in shapes)
+        if kind == 1:
+            return DenseBlock(matrix=buf[: rows * cols].reshape(rows, cols).copy())
+        core = buf[: p ** (2 * d)].reshape((p,) * (2 * d), order="F").copy()
+        if nfac == 0:
+            return TuckerBlock(core=core, u_factors=[None] * d, v_factors=[None] * d)
+        s = nfac // (2 * d * p)
+        mats = [fac[i * s * p:(i + 1) * s * p].reshape(s, p).copy() for i in range(2 * d)]
+        return TuckerBlock(core=core, u_factors=mats[:d], v_factors=mats[d:])
+
+    def last_launch_count(self) -> int:
+        return int(_lib.lib().htlr_last_launch_count(self._plan))
+
+
+def _current_stream_ptr(device: int) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def construct(cfg: BuildConfig, grid: UniformGrid, threads: int = 1,
+              device: Optional[int] = None) -> HTLRMatrix:
+    """Build the hierarchical Tucker operator (operators.py:121-126).
+    `threads` is accepted for API compatibility; construction runs on the
+    GPU."""
+    import torch
+    if cfg.kernel.kind not in ("gaussian", "slp2d", "slp3d"):
+        cfg.kernel.device_code  # raises ValueError with the explanation
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    op = HTLRMatrix(grid, cfg, int(device))
+    L = _lib.lib()
+    _lib.check(L.htlr_build_lists(op._plan))
+    if cfg.coeff.constant_value is None:
+        a = np.ascontiguousarray(cfg.coeff(_all_points(grid)), dtype=np.float64)
+        if a.shape != (grid.num_points,):
+            raise ValueError("coefficient evaluator must return one value per point")
+        _lib.check(L.htlr_set_coeff(op._plan, a.ctypes.data))
+    with torch.cuda.device(device):
+        _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(_current_stream_ptr(device))))
+    return op
+
+
+def _all_points(grid: UniformGrid) -> np.ndarray:
+    axes = [grid.coords1d()] * grid.d
+    mesh = np.meshgrid(*axes, indexing="ij")
+    return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
+
+
+def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int]):
+    import torch
+    is_torch = isinstance(u, torch.Tensor)
+    if is_torch:
+        x = u.to(dtype=torch.float64)
+        host = x.device.type != "cuda"
+    else:
+        x = torch.from_numpy(np.ascontiguousarray(np.asarray(u, dtype=np.float64)))
+        host = True
+    n_pts = op.num_points
+    if nrhs_expected == 1:
+        flat = x.reshape(-1)
+        if flat.numel() != n_pts:
+            raise ValueError(f"vector length {flat.numel()} != {n_pts}")
+        x2 = flat.reshape(n_pts, 1)
+    else:
+        if x.dim() != 2 or x.shape[0] != n_pts:
+            raise ValueError(f"expected an ({n_pts}, R) block, got shape {tuple(x.shape)}")
+        x2 = x
+    R = int(x2.shape[1])
+    dev = torch.device("cuda", op.device)
+    ud = x2.to(dev, non_blocking=True).contiguous()
+    fd = torch.empty_like(ud)
+    with torch.cuda.device(op.device):
+        stream = torch.cuda.current_stream(op.device).cuda_stream
+        _lib.check(_lib.lib().htlr_matvec(op._plan, ctypes.c_void_p(ud.data_ptr()),
+                                          ctypes.c_void_p(fd.data_ptr()), R, ctypes.c_void_p(stream)))
+    out = fd.reshape(-1) if nrhs_expected == 1 else fd
+    if host:
+        res = out.cpu()
+        return res.numpy() if not is_torch else res
+    return out
+
+
+def matvec(op: HTLRMatrix, u):
+    """f = A u (operators.py:159-161).  numpy in -> numpy out; CUDA tensor in
+    -> CUDA tensor out (no host copies)."""
+    return _apply(op, u, 1)
+
+
+def matmat(op: HTLRMatrix, U):
+    """F = A U for a block of right-hand sides U of shape (N, R)."""
+    return _apply(op, U, None)
+
+
+def weak_storage_bound(d: int, rank: int, num_points: int) -> float:
+    """operators.py:164-172."""
+    p = float(rank)
+    return (16.0 * d * p ** (2 - d) + p ** d + 2 ** d * p ** d) * num_points
+
+
+def storage_report(op: HTLRMatrix) -> StorageReport:
+    """Scalars the reference would store per leaf (operators.py:175-197), plus
+    the deduplicated device storage of this plan."""
+    out = np.zeros(5, dtype=np.int64)
+    _lib.check(_lib.lib().htlr_storage(op._plan, out.ctypes.data))
+    return StorageReport(
+        dense_scalars=int(out[0]), factor_scalars=int(out[1]), core_scalars=int(out[2]),
+        total_scalars=int(out[3]),
+        theoretical_bound=weak_storage_bound(op.grid.d, op.config.rank, op.num_points),
+        device_scalars=int(out[4]))
+
+
+def operation_counts(op: HTLRMatrix) -> dict:
+    """operators.py:200-209."""
+    _, _, nl, na, nn = op._info()
+    return {"dense_leaves": nn, "compressed_leaves": na, "total_leaves": nl}
