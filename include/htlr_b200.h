@@ -133,6 +133,16 @@ int htlr_storage(const htlr_plan* plan, int64_t out[5]);
 int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,
                       int32_t corner_subdivision, int device, double* out);
 
+/* Per-launch profiling of htlr_matvec: when enabled, every kernel launch of
+ * a matvec is bracketed by CUDA events on the launching stream.
+ * htlr_profile_read returns, for the last matvec, one entry per launch:
+ * kind (0 permute, 1 upward, 2 level GEMM, 3 leaf GEMM, 4 downward), tree
+ * level, device milliseconds, algorithmic flops and algorithmic bytes.
+ * Any output pointer may be NULL; synchronises on the last event. */
+int htlr_profile_enable(htlr_plan* plan, int32_t on);
+int htlr_profile_read(htlr_plan* plan, int32_t* kinds, int32_t* levels, double* ms, double* flops,
+                      double* bytes, int64_t cap, int64_t* count);
+
 /* Number of CUDA kernel launches issued by the last htlr_matvec call. */
 int64_t htlr_last_launch_count(const htlr_plan* plan);
 

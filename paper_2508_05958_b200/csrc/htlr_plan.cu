@@ -130,6 +130,13 @@ struct htlr_plan {
   int ws_R = 0;
   int64_t last_launches = 0;
   int64_t device_scalars = 0;
+  // per-launch profiling of the last matvec (htlr_profile_*)
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_ev;      // 2 per launch
+  std::vector<int32_t> prof_kind;
+  std::vector<int32_t> prof_level;
+  std::vector<double> prof_flops;
+  std::vector<double> prof_bytes;
 };
 
 using htlr::Tree;
@@ -242,6 +249,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
     return 0;
   }
   cudaSetDevice(pl->device);
+  for (auto e : pl->prof_ev) cudaEventDestroy(e);
   for (auto& lv : pl->levels) {
     lv.Q.release();
     lv.R.release();
@@ -609,16 +617,51 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
   }
   int64_t launches = 0;
   const Pass& lp = pl->passes[pl->leaf_pass];
+  pl->prof_kind.clear();
+  pl->prof_level.clear();
+  pl->prof_flops.clear();
+  pl->prof_bytes.clear();
+  size_t ev_used = 0;
+  auto prof_begin = [&](int kind, int level, double flops, double bytes) -> int {
+    if (!pl->profiling) return 0;
+    while (pl->prof_ev.size() < ev_used + 2) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      pl->prof_ev.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(pl->prof_ev[ev_used], st));
+    pl->prof_kind.push_back(kind);
+    pl->prof_level.push_back(level);
+    pl->prof_flops.push_back(flops);
+    pl->prof_bytes.push_back(bytes);
+    return 0;
+  };
+  auto prof_end = [&]() -> int {
+    if (!pl->profiling) return 0;
+    CUDA_TRY(cudaEventRecord(pl->prof_ev[ev_used + 1], st));
+    ev_used += 2;
+    return 0;
+  };
+  const double R8 = 8.0 * R;
+  const int64_t nleaf = pl->levels[pl->L].nclusters;
+  if (prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N)) return 1;
   htlr::launch_permute_in(u, pl->ub.d(), d, pl->n, pl->sL, R, lp.K_pad, st);
+  if (prof_end()) return 1;
   ++launches;
   for (auto& ps : pl->passes) {
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
+    double s1 = lv.side;
+    double macs = (d == 2) ? (p * s1 * s1 + (double)p * p * s1)
+                           : (p * s1 * s1 * s1 + (double)p * p * s1 * s1 + (double)p * p * p * s1);
+    if (prof_begin(1, lv.level, 2.0 * macs * lv.nclusters * R, R8 * ((double)pl->N + (double)lv.nclusters * P)))
+      return 1;
     htlr::launch_upward(u, lv.W.d(), d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), st);
+    if (prof_end()) return 1;
     ++launches;
     CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), st));
   }
-  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)pl->levels[pl->L].nclusters * R * lp.P * sizeof(double), st));
+  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), st));
   for (auto& ps : pl->passes) {
     auto& slot = ps.tasks[R];
     if (slot.second == 0) continue;
@@ -626,20 +669,30 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     const int Rc = std::min(R, NT);
     const double* B = ps.from_ub ? pl->ub.d() : pl->levels[ps.level].W.d();
     double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
+    // algorithmic work: 2 P^2 per (pair, rhs); bytes: every unique matrix once + B gather + C
+    double flops = 2.0 * (double)ps.P * ps.P * (double)ps.npairs * R;
+    double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ps.npairs;
+    if (prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
                       slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, st);
+    if (prof_end()) return 1;
     ++launches;
   }
   htlr::DownParams dp{};
   dp.nlev = 0;
+  double down_macs = 0.0;
   for (auto& ps : pl->passes) {
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
     dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d()};
+    double sl = pl->sL;
+    down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
+  if (prof_begin(4, pl->L, 2.0 * down_macs * nleaf * R, R8 * 3.0 * (double)pl->N)) return 1;
   htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, d,
                         pl->n, pl->sL, pl->L, R, p, dp, st);
+  if (prof_end()) return 1;
   ++launches;
   CUDA_TRY(cudaGetLastError());
   pl->last_launches = launches;
@@ -671,6 +724,33 @@ int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, dou
   CUDA_TRY(cudaMemcpy(out, o.ptr, sizeof(double), cudaMemcpyDeviceToHost));
   g.release();
   o.release();
+  return 0;
+}
+
+int htlr_profile_enable(htlr_plan* pl, int32_t on) {
+  if (!pl) return fail(-1, "null plan");
+  pl->profiling = on != 0;
+  return 0;
+}
+
+int htlr_profile_read(htlr_plan* pl, int32_t* kinds, int32_t* levels, double* ms, double* flops, double* bytes,
+                      int64_t cap, int64_t* count) {
+  if (!pl || !count) return fail(-1, "null argument");
+  const int64_t nl = (int64_t)pl->prof_kind.size();
+  *count = nl;
+  if (!pl->profiling || nl == 0) return 0;
+  if (cap < nl) return fail(-1, "profile buffer too small");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  CUDA_TRY(cudaEventSynchronize(pl->prof_ev[2 * nl - 1]));
+  for (int64_t i = 0; i < nl; ++i) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, pl->prof_ev[2 * i], pl->prof_ev[2 * i + 1]));
+    if (kinds) kinds[i] = pl->prof_kind[i];
+    if (levels) levels[i] = pl->prof_level[i];
+    if (ms) ms[i] = t;
+    if (flops) flops[i] = pl->prof_flops[i];
+    if (bytes) bytes[i] = pl->prof_bytes[i];
+  }
   return 0;
 }
 

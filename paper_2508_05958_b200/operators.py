@@ -160,6 +160,30 @@ class HTLRMatrix:
     def last_launch_count(self) -> int:
         return int(_lib.lib().htlr_last_launch_count(self._plan))
 
+    PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward")
+
+    def profile(self, on: bool = True) -> None:
+        """Bracket every kernel launch of later matvecs with CUDA events."""
+        _lib.check(_lib.lib().htlr_profile_enable(self._plan, int(bool(on))))
+
+    def profile_read(self) -> list:
+        """Per-launch records of the last matvec: phase, level, device ms,
+        algorithmic flops and bytes (synchronises)."""
+        cnt = ctypes.c_int64()
+        _lib.check(_lib.lib().htlr_profile_read(self._plan, None, None, None, None, None, 0, ctypes.byref(cnt)))
+        n = cnt.value
+        if n == 0:
+            return []
+        kinds = np.zeros(n, dtype=np.int32)
+        levels = np.zeros(n, dtype=np.int32)
+        ms = np.zeros(n)
+        fl = np.zeros(n)
+        by = np.zeros(n)
+        _lib.check(_lib.lib().htlr_profile_read(self._plan, kinds.ctypes.data, levels.ctypes.data, ms.ctypes.data,
+                                                fl.ctypes.data, by.ctypes.data, n, ctypes.byref(cnt)))
+        return [{"phase": self.PHASES[k], "level": int(lv), "ms": float(t), "flops": float(f), "bytes": float(b)}
+                for k, lv, t, f, b in zip(kinds, levels, ms, fl, by)]
+
 
 def _current_stream_ptr(device: int) -> int:
     import torch
