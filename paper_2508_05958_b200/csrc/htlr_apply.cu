@@ -193,6 +193,12 @@ __global__ void __launch_bounds__(WM* WN * 32, 2)
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, t = lane & 3;
+  // warp-uniform extent of real work: empty n8 column tiles (offsets with
+  // few pairs) and padded m16 row tiles (P not a multiple of MT) are skipped
+  const int ncols = (Rc == NT) ? min(NT, R - tk.r0) : tk.pair_count * Rc;
+  const int n_tiles = max(0, min(4, (ncols - wn * 32 + 7) >> 3));
+  const int row0 = rt * MT + wm * 32;
+  const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
   double acc[2][4][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -214,29 +220,35 @@ __global__ void __launch_bounds__(WM* WN * 32, 2)
     __syncthreads();
     const double* cA = sA + (kc % STAGES) * MT * KC;
     const double* cB = sB + (kc % STAGES) * NT * BST;
+    if (n_tiles > 0 && m_tiles > 0) {
 #pragma unroll
-    for (int ks = 0; ks < KC / 8; ++ks) {
-      double a[2][4];
+      for (int ks = 0; ks < KC / 8; ++ks) {
+        double a[2][4];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const double2* pa = reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
-        double2 v0 = pa[0], v1 = pa[1];
-        a[mi][0] = v0.x;
-        a[mi][1] = v0.y;
-        a[mi][2] = v1.x;
-        a[mi][3] = v1.y;
+        for (int mi = 0; mi < 2; ++mi) {
+          const double2* pa =
+              reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
+          double2 v0 = pa[0], v1 = pa[1];
+          a[mi][0] = v0.x;
+          a[mi][1] = v0.y;
+          a[mi][2] = v1.x;
+          a[mi][3] = v1.y;
+        }
+        double b[4][2];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          if (ni < n_tiles) {
+            const double* pb = cB + (wn * 32 + ni * 8 + g) * BST + ks * 8 + t;
+            b[ni][0] = pb[0];
+            b[ni][1] = pb[4];
+          }
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            if (mi < m_tiles && ni < n_tiles) mma_m16n8k8(acc[mi][ni], a[mi], b[ni]);
       }
-      double b[4][2];
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const double* pb = cB + (wn * 32 + ni * 8 + g) * BST + ks * 8 + t;
-        b[ni][0] = pb[0];
-        b[ni][1] = pb[4];
-      }
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) mma_m16n8k8(acc[mi][ni], a[mi], b[ni]);
     }
     __syncthreads();
   }

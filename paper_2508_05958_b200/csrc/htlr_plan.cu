@@ -739,6 +739,7 @@ int htlr_profile_read(htlr_plan* pl, int32_t* kinds, int32_t* levels, double* ms
   const int64_t nl = (int64_t)pl->prof_kind.size();
   *count = nl;
   if (!pl->profiling || nl == 0) return 0;
+  if (!kinds && !levels && !ms && !flops && !bytes) return 0;   // count query
   if (cap < nl) return fail(-1, "profile buffer too small");
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaEventSynchronize(pl->prof_ev[2 * nl - 1]));
