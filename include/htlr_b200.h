@@ -107,6 +107,34 @@ int htlr_construct(htlr_plan* plan, void* stream);
  * asynchronous.  Replaces matvec / _hierarchical_matvec. */
 int htlr_matvec(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
 
+/* ---- multi-GPU: shard the target boxes by cluster subtrees --------------
+ * Clusters are numbered in Morton order with the reference's child order, so
+ * every subtree is a contiguous id range on every level.  With `world` (a
+ * power of two) shards, shard `rank` owns the contiguous range
+ * [rank, rank+1) * M_l / world of the M_l clusters of each level l: its
+ * target rows, its leaf boxes and its source clusters' upward data.
+ * Call htlr_set_shard before htlr_build_lists / htlr_construct. */
+int htlr_set_shard(htlr_plan* plan, int32_t rank, int32_t world);
+/* Owned leaf-box range (Morton ids), owned (target, source) pairs and their
+ * GEMM flops per right-hand side. */
+int htlr_shard_info(const htlr_plan* plan, int64_t* own_leaf_lo, int64_t* own_leaf_hi,
+                    int64_t* own_pairs, double* own_flops);
+/* The exchange step: buffers every shard must all-gather between the local
+ * and the remote phase -- the leaf-box-major input ub and the upward
+ * coefficients W_l of each compressed level.  Each is cluster-major in Morton
+ * order, so shard r's part is the contiguous r-th 1/world of its bytes.
+ * exchange_info reports the count and total bytes per buffer for `nrhs`;
+ * bind_exchange hands the plan caller-owned device buffers of those sizes
+ * (e.g. torch tensors all-gathered with NCCL by the caller). */
+int htlr_exchange_info(const htlr_plan* plan, int64_t nrhs, int64_t* count, int64_t* bytes, int64_t cap);
+int htlr_bind_exchange(htlr_plan* plan, int64_t nrhs, void* const* ptrs, int64_t count);
+/* local: permute + upward of the own clusters into the exchange buffers;
+ * remote: GEMMs of the own targets and the fused downward pass, writing the
+ * f rows of the own leaf boxes (other rows untouched).  htlr_matvec is
+ * local + remote for an unsharded plan. */
+int htlr_matvec_local(htlr_plan* plan, const double* u, int64_t nrhs, void* stream);
+int htlr_matvec_remote(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
+
 /* Diagonal cell average used by the inadmissible tau == sigma blocks
  * (operators.py:95-99).  Synchronises. */
 int htlr_diag_value(htlr_plan* plan, double* out);

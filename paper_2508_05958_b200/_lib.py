@@ -53,6 +53,13 @@ SYMBOLS = [
     ("htlr_set_coeff", ctypes.c_int, [_P, _P]),
     ("htlr_construct", ctypes.c_int, [_P, _P]),
     ("htlr_matvec", ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    ("htlr_set_shard", ctypes.c_int, [_P, _I32, _I32]),
+    ("htlr_shard_info", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                       ctypes.POINTER(_D)]),
+    ("htlr_exchange_info", ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), _P, _I64]),
+    ("htlr_bind_exchange", ctypes.c_int, [_P, _I64, _P, _I64]),
+    ("htlr_matvec_local", ctypes.c_int, [_P, _P, _I64, _P]),
+    ("htlr_matvec_remote", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("htlr_diag_value", ctypes.c_int, [_P, ctypes.POINTER(_D)]),
     ("htlr_export_block", ctypes.c_int, [_P, _I64, _P, _I64, _P, _I64, _P]),
     ("htlr_storage", ctypes.c_int, [_P, _P]),

@@ -20,10 +20,10 @@ namespace htlr {
 // permute: ub[(b*R + r)*K_pad + k] = u[(global point of (b, k))*R + r]
 // ---------------------------------------------------------------------------
 __global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
-                                  int s, int R, int K_pad) {
-  const int m = n / s;
-  int b = blockIdx.x;
-  int bc[3] = {b % m, (b / m) % m, b / (m * m)};
+                                  int s, int bits, int R, int K_pad, int64_t b0) {
+  const int64_t b = b0 + blockIdx.x;   // leaf box, Morton id
+  int bc[3];
+  morton_decode(b, d, bits, bc);
   const int P = (d == 2) ? s * s : s * s * s;
   for (int idx = threadIdx.x; idx < R * K_pad; idx += blockDim.x) {
     int r = idx % R, k = idx / R;
@@ -38,11 +38,11 @@ __global__ void permute_in_kernel(const double* __restrict__ u, double* __restri
   }
 }
 
-void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad,
-                       cudaStream_t st) {
-  int m = n / s;
-  int nb = (d == 2) ? m * m : m * m * m;
-  permute_in_kernel<<<nb, 256, 0, st>>>(u, ub, d, n, s, R, K_pad);
+void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
+                       int64_t nb, cudaStream_t st) {
+  int bits = 0;
+  while ((s << bits) < n) ++bits;
+  if (nb > 0) permute_in_kernel<<<(unsigned)nb, 256, 0, st>>>(u, ub, d, n, s, bits, R, K_pad, b0);
 }
 
 // ---------------------------------------------------------------------------
@@ -51,15 +51,16 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
 // p*s + p^2 + p^3 values whatever the box side.
 // ---------------------------------------------------------------------------
 __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
-                              int p, int R, int K_pad, const double* __restrict__ Q) {
+                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t c0) {
   extern __shared__ double sm[];
   double* sQ = sm;             // s*p
   double* T1 = sQ + s * p;     // p*s
   double* T2 = T1 + p * s;     // p*p
   double* acc = T2 + p * p;    // p^d
-  const int m = n / s;
-  const int c = blockIdx.x, r = blockIdx.y;
-  const int cc[3] = {c % m, (c / m) % m, c / (m * m)};
+  const int64_t c = c0 + blockIdx.x;   // cluster, Morton id
+  const int r = blockIdx.y;
+  int cc[3];
+  morton_decode(c, d, bits, cc);
   for (int i = threadIdx.x; i < s * p; i += blockDim.x) sQ[i] = Q[i];
   const int P = (d == 2) ? p * p : p * p * p;
   for (int i = threadIdx.x; i < P; i += blockDim.x) acc[i] = 0.0;
@@ -104,14 +105,11 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
 }
 
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, cudaStream_t st) {
-  int m = n / side;
-  int nc = (d == 2) ? m * m : m * m * m;
+                   int K_pad, const double* Q, int64_t c0, int64_t nc, cudaStream_t st) {
   int P = (d == 2) ? p * p : p * p * p;
   size_t smem = sizeof(double) * (size_t)(side * p + p * side + p * p + P);
   if (smem > 48 * 1024) cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  (void)level;
-  upward_kernel<<<dim3(nc, R), 256, smem, st>>>(u, W, d, n, side, p, R, K_pad, Q);
+  if (nc > 0) upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, c0);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,7 +303,8 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
 // ---------------------------------------------------------------------------
 __global__ void downward_kernel(const double* __restrict__ u, double* __restrict__ f,
                                 const double* __restrict__ Y, int ldy, const double* __restrict__ avec,
-                                double aconst, int d, int n, int sL, int L, int R, int p, DownParams dp) {
+                                double aconst, int d, int n, int sL, int L, int R, int p, DownParams dp,
+                                int64_t b0) {
   extern __shared__ double sm[];
   const int PL = (d == 2) ? sL * sL : sL * sL * sL;
   const int P = (d == 2) ? p * p : p * p * p;
@@ -314,21 +313,17 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
   double* E1 = Hs + P;               // sL * p^(d-1)
   double* E2 = E1 + sL * ((d == 2) ? p : p * p);   // sL^2 * p (3-D only)
   double* Us = E2 + ((d == 3) ? sL * sL * p : 0);  // d * sL * p
-  const int mL = n / sL;
-  const int b = blockIdx.x, r = blockIdx.y;
-  const int bc[3] = {b % mL, (b / mL) % mL, b / (mL * mL)};
+  const int64_t b = b0 + blockIdx.x;   // leaf box, Morton id
+  const int r = blockIdx.y;
+  int bc[3];
+  morton_decode(b, d, L, bc);
   for (int i = threadIdx.x; i < PL; i += blockDim.x) facc[i] = 0.0;
   for (int li = 0; li < dp.nlev; ++li) {
     const DownLevel lv = dp.lev[li];
     const int shift = L - lv.level;
-    const int ml = n / lv.side;
-    int ac[3], off[3];
-    for (int a = 0; a < 3; ++a) {
-      ac[a] = bc[a] >> shift;
-      off[a] = (bc[a] - (ac[a] << shift)) * sL;
-    }
-    int64_t anc = ac[0] + (int64_t)ml * ac[1];
-    if (d == 3) anc += (int64_t)ml * ml * ac[2];
+    int off[3];
+    for (int a = 0; a < 3; ++a) off[a] = (bc[a] & ((1 << shift) - 1)) * sL;
+    const int64_t anc = b >> (d * shift);   // Morton parent chain
     __syncthreads();
     const double* Hsrc = lv.H + (anc * R + r) * (int64_t)lv.P;
     for (int i = threadIdx.x; i < P; i += blockDim.x) Hs[i] = Hsrc[i];
@@ -395,16 +390,16 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
 
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
                      double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
-                     cudaStream_t st) {
-  int mL = n / sL;
-  int nb = (d == 2) ? mL * mL : mL * mL * mL;
+                     int64_t b0, int64_t nb, cudaStream_t st) {
   int P = (d == 2) ? p * p : p * p * p;
   int PL = (d == 2) ? sL * sL : sL * sL * sL;
   size_t words = PL + P + sL * ((d == 2) ? p : p * p) + ((d == 3) ? sL * sL * p : 0) + d * sL * p;
   size_t smem = words * sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(downward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  downward_kernel<<<dim3(nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, d, n, sL, L, R, p, dp);
+  if (nb > 0)
+    downward_kernel<<<dim3((unsigned)nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, d, n, sL, L, R, p, dp,
+                                                             b0);
 }
 
 }  // namespace htlr

@@ -63,4 +63,24 @@ __host__ __device__ __forceinline__ int64_t tiled_offset(int m, int k, int MT, i
   return chunk * (int64_t)(MT * kKC) + (int64_t)((mi * (kKC / 8) + ki) * 128 + lane * 4 + reg);
 }
 
+// ---------------------------------------------------------------------------
+// Cluster numbering: Morton (Z) order with the reference's child order
+// (np.ndindex, last dimension fastest, grids.py:226-230): coordinate a's bit b
+// sits at bit d*b + (d-1-a).  Every subtree is a contiguous id range at every
+// deeper level, the parent of id c is c >> d, and the order of leaf boxes is
+// the reference's DFS order of cluster-tree leaves.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t morton_encode(const int* c, int d, int bits) {
+  int64_t id = 0;
+  for (int b = 0; b < bits; ++b)
+    for (int a = 0; a < d; ++a) id |= (int64_t)((c[a] >> b) & 1) << (d * b + (d - 1 - a));
+  return id;
+}
+
+__host__ __device__ __forceinline__ void morton_decode(int64_t id, int d, int bits, int* c) {
+  c[0] = c[1] = c[2] = 0;
+  for (int b = 0; b < bits; ++b)
+    for (int a = 0; a < d; ++a) c[a] |= (int)((id >> (d * b + (d - 1 - a))) & 1) << b;
+}
+
 }  // namespace htlr

@@ -68,10 +68,11 @@ void launch_near_blocks(const NearJob* jobs, int njobs, int d, int s, double h, 
                         cudaStream_t st);
 
 // matvec kernels (htlr_apply.cu)
-void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad,
-                       cudaStream_t st);
+// index ranges are Morton ids (see htlr_device.cuh)
+void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
+                       int64_t nb, cudaStream_t st);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, cudaStream_t st);
+                   int K_pad, const double* Q, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
 void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
@@ -80,6 +81,6 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
 int gemm_nt(int MT);
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
                      double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
-                     cudaStream_t st);
+                     int64_t b0, int64_t nb, cudaStream_t st);
 
 }  // namespace htlr

@@ -131,6 +131,14 @@ struct htlr_plan {
   int64_t last_launches = 0;
   int64_t device_scalars = 0;
   // per-launch profiling of the last matvec (htlr_profile_*)
+  // sharding by cluster subtrees (multi-GPU): this plan computes the f rows
+  // of leaf boxes [own_lo[L], own_hi[L]) and the upward data of its own
+  // source clusters; every level's own range is a contiguous Morton range
+  int shard_rank = 0, shard_world = 1;
+  std::vector<int64_t> own_lo, own_hi;
+  // caller-bound exchange buffers (ub, then W of each level pass), per R
+  int ext_R = 0;
+  std::vector<double*> ext_ptrs;
   bool profiling = false;
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
@@ -295,6 +303,20 @@ int htlr_build_lists(htlr_plan* pl) {
   }
   pl->near = OffsetTable();
   pl->num_near = 0;
+  const int world = pl->shard_world, rank = pl->shard_rank;
+  pl->own_lo.assign(pl->L + 1, 0);
+  pl->own_hi.assign(pl->L + 1, 0);
+  for (int l = 0; l <= pl->L; ++l) {
+    const int64_t M = pl->levels[l].nclusters;
+    if (M % world == 0) {
+      pl->own_lo[l] = M / world * rank;
+      pl->own_hi[l] = M / world * (rank + 1);
+    } else {
+      pl->own_lo[l] = pl->own_hi[l] = -1;   // level cannot be split evenly
+    }
+  }
+  if (pl->own_lo[pl->L] < 0)
+    return fail(-1, "the leaf level has fewer boxes than shards (or not a multiple of them)");
   for (const auto& lf : tr.leaves) {
     OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
     const int m = pl->levels[lf.level].m;
@@ -309,8 +331,20 @@ int htlr_build_lists(htlr_plan* pl) {
     } else {
       id = it->second;
     }
-    int64_t tl = lf.tc[0] + (int64_t)m * lf.tc[1] + (int64_t)m * m * (d == 3 ? lf.tc[2] : 0);
-    int64_t sl = lf.sc[0] + (int64_t)m * lf.sc[1] + (int64_t)m * m * (d == 3 ? lf.sc[2] : 0);
+    (void)m;
+    const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
+    const int64_t sl = htlr::morton_encode(lf.sc, d, lf.level);
+    if (world > 1) {
+      if (pl->own_lo[lf.level] < 0)
+        return fail(-1, "admissible blocks on a level with fewer clusters than shards");
+      if (tl < pl->own_lo[lf.level] || tl >= pl->own_hi[lf.level]) {
+        if (lf.kind == 0)
+          pl->levels[lf.level].num_adm++;
+        else
+          pl->num_near++;
+        continue;   // another shard's target
+      }
+    }
     tab.members[id].emplace_back((int)tl, (int)sl);
     if (lf.kind == 0)
       pl->levels[lf.level].num_adm++;
@@ -381,6 +415,77 @@ int htlr_build_lists(htlr_plan* pl) {
   }
   pl->lists_built = true;
   pl->constructed = false;
+  return 0;
+}
+
+int htlr_set_shard(htlr_plan* pl, int32_t rank, int32_t world) {
+  if (!pl) return fail(-1, "null plan");
+  if (world < 1 || rank < 0 || rank >= world) return fail(-1, "invalid shard rank/world");
+  if (world & (world - 1)) return fail(-1, "the number of shards must be a power of two");
+  if (pl->constructed) return fail(-1, "set the shard before construct");
+  pl->shard_rank = rank;
+  pl->shard_world = world;
+  pl->lists_built = false;
+  return 0;
+}
+
+int htlr_shard_info(const htlr_plan* pl, int64_t* own_leaf_lo, int64_t* own_leaf_hi, int64_t* own_pairs,
+                    double* own_flops) {
+  if (!pl) return fail(-1, "null plan");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  int64_t pairs = 0;
+  double fl = 0.0;
+  for (const auto& ps : pl->passes) {
+    pairs += ps.npairs;
+    fl += 2.0 * (double)ps.P * ps.P * ps.npairs;
+  }
+  if (own_leaf_lo) *own_leaf_lo = pl->own_lo[pl->L];
+  if (own_leaf_hi) *own_leaf_hi = pl->own_hi[pl->L];
+  if (own_pairs) *own_pairs = pairs;
+  if (own_flops) *own_flops = fl;
+  return 0;
+}
+
+static void exchange_sizes(const htlr_plan* pl, int R, std::vector<int64_t>& bytes) {
+  bytes.clear();
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  bytes.push_back(pl->levels[pl->L].nclusters * (int64_t)R * lp.K_pad * (int64_t)sizeof(double));
+  for (const auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    bytes.push_back(pl->levels[ps.level].nclusters * (int64_t)R * ps.K_pad * (int64_t)sizeof(double));
+  }
+}
+
+int htlr_exchange_info(const htlr_plan* pl, int64_t nrhs, int64_t* count, int64_t* bytes, int64_t cap) {
+  if (!pl || !count) return fail(-1, "null argument");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  std::vector<int64_t> b;
+  exchange_sizes(pl, (int)nrhs, b);
+  *count = (int64_t)b.size();
+  if (bytes) {
+    if (cap < (int64_t)b.size()) return fail(-1, "exchange info buffer too small");
+    for (size_t i = 0; i < b.size(); ++i) bytes[i] = b[i];
+  }
+  return 0;
+}
+
+int htlr_bind_exchange(htlr_plan* pl, int64_t nrhs, void* const* ptrs, int64_t count) {
+  if (!pl) return fail(-1, "null plan");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  std::vector<int64_t> b;
+  exchange_sizes(pl, (int)nrhs, b);
+  if (!ptrs || count == 0) {
+    pl->ext_R = 0;
+    pl->ext_ptrs.clear();
+    return 0;
+  }
+  if (count != (int64_t)b.size()) return fail(-1, "exchange buffer count mismatch");
+  pl->ext_ptrs.assign(count, nullptr);
+  for (int64_t i = 0; i < count; ++i) {
+    if (!ptrs[i]) return fail(-1, "null exchange buffer");
+    pl->ext_ptrs[i] = static_cast<double*>(ptrs[i]);
+  }
+  pl->ext_R = (int)nrhs;
   return 0;
 }
 
@@ -593,36 +698,22 @@ static int ensure_workspace(htlr_plan* pl, int R) {
   return 0;
 }
 
-int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
-  if (!pl) return fail(-1, "null plan");
-  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
-  if (!pl->constructed) return fail(-1, "plan not constructed");
-  if (nrhs < 1 || nrhs > 4096) return fail(-1, "nrhs must be in [1, 4096]");
-  if (!u || !f) return fail(-1, "null vector");
-  CUDA_TRY(cudaSetDevice(pl->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  const int R = (int)nrhs;
-  const int d = pl->d, p = pl->p;
-  const int P = ipow(p, d);
-  if (ensure_workspace(pl, R)) return 1;
-  for (auto& ps : pl->passes) {
-    if (ps.tasks.count(R)) continue;
-    std::vector<htlr::GemmTask> tv;
-    make_tasks(ps, R, tv);
-    auto& slot = ps.tasks[R];
-    if (slot.first.alloc(std::max<size_t>(1, tv.size()) * sizeof(htlr::GemmTask))) return 1;
-    if (!tv.empty())
-      CUDA_TRY(cudaMemcpy(slot.first.ptr, tv.data(), tv.size() * sizeof(htlr::GemmTask), cudaMemcpyHostToDevice));
-    slot.second = (int)tv.size();
-  }
-  int64_t launches = 0;
-  const Pass& lp = pl->passes[pl->leaf_pass];
-  pl->prof_kind.clear();
-  pl->prof_level.clear();
-  pl->prof_flops.clear();
-  pl->prof_bytes.clear();
+// Matvec phases.  local: permute own leaf boxes + upward of own source
+// clusters into the exchange buffers (ub, W_l); remote: gathered GEMMs for the
+// own target clusters + fused downward of the own leaf boxes.  Between them a
+// multi-GPU caller all-gathers the exchange buffers (contiguous Morton chunks).
+namespace {
+
+struct MvCtx {
+  htlr_plan* pl;
+  cudaStream_t st;
+  int R, d, p, P;
+  double* ub;
+  std::vector<double*> W;   // per pass (nullptr for the leaf pass)
   size_t ev_used = 0;
-  auto prof_begin = [&](int kind, int level, double flops, double bytes) -> int {
+  int64_t launches = 0;
+
+  int prof_begin(int kind, int level, double flops, double bytes) {
     if (!pl->profiling) return 0;
     while (pl->prof_ev.size() < ev_used + 2) {
       cudaEvent_t e;
@@ -635,48 +726,109 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     pl->prof_flops.push_back(flops);
     pl->prof_bytes.push_back(bytes);
     return 0;
-  };
-  auto prof_end = [&]() -> int {
+  }
+  int prof_end() {
+    ++launches;
     if (!pl->profiling) return 0;
     CUDA_TRY(cudaEventRecord(pl->prof_ev[ev_used + 1], st));
     ev_used += 2;
     return 0;
-  };
-  const double R8 = 8.0 * R;
-  const int64_t nleaf = pl->levels[pl->L].nclusters;
-  if (prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N)) return 1;
-  htlr::launch_permute_in(u, pl->ub.d(), d, pl->n, pl->sL, R, lp.K_pad, st);
-  if (prof_end()) return 1;
-  ++launches;
+  }
+};
+
+int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
+  if (!pl) return fail(-1, "null plan");
+  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  if (nrhs < 1 || nrhs > 4096) return fail(-1, "nrhs must be in [1, 4096]");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cx.pl = pl;
+  cx.st = (cudaStream_t)stream;
+  cx.R = (int)nrhs;
+  cx.d = pl->d;
+  cx.p = pl->p;
+  cx.P = ipow(pl->p, pl->d);
+  if (ensure_workspace(pl, cx.R)) return 1;
   for (auto& ps : pl->passes) {
+    if (ps.tasks.count(cx.R)) continue;
+    std::vector<htlr::GemmTask> tv;
+    make_tasks(ps, cx.R, tv);
+    auto& slot = ps.tasks[cx.R];
+    if (slot.first.alloc(std::max<size_t>(1, tv.size()) * sizeof(htlr::GemmTask))) return 1;
+    if (!tv.empty())
+      CUDA_TRY(cudaMemcpy(slot.first.ptr, tv.data(), tv.size() * sizeof(htlr::GemmTask), cudaMemcpyHostToDevice));
+    slot.second = (int)tv.size();
+  }
+  const bool ext = pl->ext_R == cx.R && !pl->ext_ptrs.empty();
+  size_t xi = 0;
+  cx.ub = ext ? pl->ext_ptrs[xi++] : pl->ub.d();
+  cx.W.assign(pl->passes.size(), nullptr);
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    if (pl->passes[i].to_y) continue;
+    cx.W[i] = ext ? pl->ext_ptrs[xi++] : pl->levels[pl->passes[i].level].W.d();
+  }
+  return 0;
+}
+
+void prof_reset(htlr_plan* pl) {
+  pl->prof_kind.clear();
+  pl->prof_level.clear();
+  pl->prof_flops.clear();
+  pl->prof_bytes.clear();
+}
+
+int mv_local(MvCtx& cx, const double* u) {
+  htlr_plan* pl = cx.pl;
+  const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
+  const double R8 = 8.0 * R;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
+  const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
+  if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
+  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st);
+  if (cx.prof_end()) return 1;
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    const Pass& ps = pl->passes[i];
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
+    const int64_t c0 = pl->own_lo[ps.level], nc = pl->own_hi[ps.level] - c0;
     double s1 = lv.side;
     double macs = (d == 2) ? (p * s1 * s1 + (double)p * p * s1)
                            : (p * s1 * s1 * s1 + (double)p * p * s1 * s1 + (double)p * p * p * s1);
-    if (prof_begin(1, lv.level, 2.0 * macs * lv.nclusters * R, R8 * ((double)pl->N + (double)lv.nclusters * P)))
-      return 1;
-    htlr::launch_upward(u, lv.W.d(), d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), st);
-    if (prof_end()) return 1;
-    ++launches;
-    CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), st));
+    if (cx.prof_begin(1, lv.level, 2.0 * macs * nc * R, R8 * ((double)pl->N * frac + (double)nc * P))) return 1;
+    htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), c0, nc, cx.st);
+    if (cx.prof_end()) return 1;
   }
-  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), st));
+  return 0;
+}
+
+int mv_remote(MvCtx& cx, const double* u, double* f) {
+  htlr_plan* pl = cx.pl;
+  const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
+  const double R8 = 8.0 * R;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int64_t nleaf = pl->levels[pl->L].nclusters;
   for (auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    Level& lv = pl->levels[ps.level];
+    CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), cx.st));
+  }
+  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    Pass& ps = pl->passes[i];
     auto& slot = ps.tasks[R];
     if (slot.second == 0) continue;
     const int NT = htlr::gemm_nt(ps.MT);
     const int Rc = std::min(R, NT);
-    const double* B = ps.from_ub ? pl->ub.d() : pl->levels[ps.level].W.d();
+    const double* B = ps.from_ub ? cx.ub : cx.W[i];
     double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
     // algorithmic work: 2 P^2 per (pair, rhs); bytes: every unique matrix once + B gather + C
     double flops = 2.0 * (double)ps.P * ps.P * (double)ps.npairs * R;
     double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ps.npairs;
-    if (prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
+    if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
-                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, st);
-    if (prof_end()) return 1;
-    ++launches;
+                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st);
+    if (cx.prof_end()) return 1;
   }
   htlr::DownParams dp{};
   dp.nlev = 0;
@@ -689,13 +841,47 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     double sl = pl->sL;
     down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
-  if (prof_begin(4, pl->L, 2.0 * down_macs * nleaf * R, R8 * 3.0 * (double)pl->N)) return 1;
+  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
+  const double frac = (double)nb / (double)nleaf;
+  if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
   htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, d,
-                        pl->n, pl->sL, pl->L, R, p, dp, st);
-  if (prof_end()) return 1;
-  ++launches;
+                        pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
+  if (cx.prof_end()) return 1;
   CUDA_TRY(cudaGetLastError());
-  pl->last_launches = launches;
+  return 0;
+}
+
+}  // namespace
+
+int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  MvCtx cx;
+  if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
+  if (!u || !f) return fail(-1, "null vector");
+  if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
+  prof_reset(pl);
+  if (int rc = mv_local(cx, u)) return rc;
+  if (int rc = mv_remote(cx, u, f)) return rc;
+  pl->last_launches = cx.launches;
+  return 0;
+}
+
+int htlr_matvec_local(htlr_plan* pl, const double* u, int64_t nrhs, void* stream) {
+  MvCtx cx;
+  if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
+  if (!u) return fail(-1, "null vector");
+  prof_reset(pl);
+  if (int rc = mv_local(cx, u)) return rc;
+  pl->last_launches = cx.launches;
+  return 0;
+}
+
+int htlr_matvec_remote(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  MvCtx cx;
+  if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
+  if (!u || !f) return fail(-1, "null vector");
+  cx.ev_used = 2 * pl->prof_kind.size();   // continue the local phase's records
+  if (int rc = mv_remote(cx, u, f)) return rc;
+  pl->last_launches += cx.launches;
   return 0;
 }
 
