@@ -290,6 +290,10 @@ static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, 
 void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st) {
+  if (gemm_use_persistent()) {
+    launch_gemm_persistent(MT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+    return;
+  }
   if (MT == 64)
     launch_gemm_t<2, 2, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
   else

@@ -1,0 +1,265 @@
+// Persistent, warp-specialised gathered fp64 tensor-core GEMM (sm_100a).
+//
+// Same contract as gemm_gather_kernel (htlr_apply.cu): a work item is
+// (task, row tile); the item computes C[tgt][r][rows] += A_mat[rows][:] .
+// B[src][r][:] over its (tgt, src) pairs x RHS columns.  This version keeps
+// one CTA resident per SM and streams items through a STAGES-deep shared
+// memory ring:
+//   * a producer warp issues 1-D TMA bulk copies (cp.async.bulk ->
+//     UBLKCP) -- one contiguous copy for the pre-tiled A slab of a 32-wide K
+//     chunk and one 256-byte copy per gathered B column -- completing a
+//     `full` mbarrier by transaction count;
+//   * 8 consumer warps run mma.sync.m16n8k8.f64 (DMMA) from the ring and
+//     release each slot with an `empty` mbarrier arrive, so no CTA-wide
+//     barrier stalls the tensor pipe and the next item's loads overlap the
+//     current item's last chunks and epilogue (fp64 RED into L2).
+// Items are assigned round-robin, so at any moment the 148 CTAs work on
+// consecutive items (the same or neighbouring offsets): each unique core is
+// fetched from HBM once and served to the other CTAs from L2.
+#include <cstdlib>
+#include <cstring>
+
+#include "htlr_kernels.h"
+
+namespace htlr {
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mma16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+struct ItemInfo {
+  int mat, pair_begin, pair_count, r0, rt, ncols;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, int RT, int R, int Rc, int NT) {
+  ItemInfo it;
+  const GemmTask tk = tasks[item / RT];
+  it.rt = item % RT;
+  it.mat = tk.mat;
+  it.pair_begin = tk.pair_begin;
+  it.pair_count = tk.pair_count;
+  it.r0 = tk.r0;
+  it.ncols = (Rc == NT) ? min(NT, R - tk.r0) : tk.pair_count * Rc;
+  return it;
+}
+
+}  // namespace
+
+template <int WM, int WN, int STAGES>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
+                           double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
+                           const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
+                           int RT) {
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC, BST = KC + 4;
+  constexpr int NCW = WM * WN;   // consumer warps
+  extern __shared__ __align__(128) double smem[];
+  double* sA = smem;                                  // STAGES x MT*KC
+  double* sB = smem + STAGES * MT * KC;               // STAGES x NT*BST
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NT * BST);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int nk = K_pad / KC;
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------ producer
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const ItemInfo it = item_info(tasks, item, RT, R, Rc, NT);
+      // gathered B column bases (two columns per lane)
+      int64_t cb[NT / 32];
+#pragma unroll
+      for (int q = 0; q < NT / 32; ++q) {
+        const int n = lane + 32 * q;
+        cb[q] = -1;
+        if (n < it.ncols) {
+          const int j = n / Rc, r = it.r0 + n % Rc;
+          const int2 pr = pairs[it.pair_begin + j];
+          cb[q] = ((int64_t)pr.y * R + r) * K_pad;
+        }
+      }
+      const double* Ablk = A + (int64_t)it.mat * mat_stride + (int64_t)it.rt * MT * K_pad;
+      const unsigned bytes = (unsigned)(MT * KC * 8 + it.ncols * KC * 8);
+      for (int kc = 0; kc < nk; ++kc, ++g) {
+        const int s = g % STAGES;
+        if (g >= (uint32_t)STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(sA + s * MT * KC, Ablk + (int64_t)kc * MT * KC, MT * KC * 8, &full[s]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NT / 32; ++q) {
+          const int n = lane + 32 * q;
+          if (cb[q] >= 0) bulk_g2s(sB + s * NT * BST + n * BST, B + cb[q] + kc * KC, KC * 8, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int wm = warp % WM, wn = warp / WM;
+  const int g8 = lane >> 2, t = lane & 3;
+  uint32_t g = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const ItemInfo it = item_info(tasks, item, RT, R, Rc, NT);
+    const int n_tiles = max(0, min(4, (it.ncols - wn * 32 + 7) >> 3));
+    const int row0 = it.rt * MT + wm * 32;
+    const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
+    double acc[2][4][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+    for (int kc = 0; kc < nk; ++kc, ++g) {
+      const int s = g % STAGES;
+      mbar_wait(&full[s], (g / STAGES) & 1);
+      const double* cA = sA + s * MT * KC;
+      const double* cB = sB + s * NT * BST;
+      if (n_tiles > 0 && m_tiles > 0) {
+#pragma unroll
+        for (int ks = 0; ks < KC / 8; ++ks) {
+          double a[2][4];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const double2* pa =
+                reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
+            const double2 v0 = pa[0], v1 = pa[1];
+            a[mi][0] = v0.x;
+            a[mi][1] = v0.y;
+            a[mi][2] = v1.x;
+            a[mi][3] = v1.y;
+          }
+          double b[4][2];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            const double* pb = cB + (wn * 32 + ni * 8 + g8) * BST + ks * 8 + t;
+            b[ni][0] = pb[0];
+            b[ni][1] = pb[4];
+          }
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni)
+              if (mi < m_tiles && ni < n_tiles) mma16x8x8(acc[mi][ni], a[mi], b[ni]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // epilogue: fp64 RED into the accumulators (columns of stale B slots in a
+    // partially filled n8 tile only pollute their own, never-stored columns)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int cix = 0; cix < 2; ++cix) {
+        const int n = wn * 32 + ni * 8 + 2 * t + cix;
+        if (n >= it.ncols) continue;
+        const int j = n / Rc, r = it.r0 + n % Rc;
+        const int2 pr = pairs[it.pair_begin + j];
+        double* cc = C + ((int64_t)pr.x * R + r) * ldc;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+#pragma unroll
+          for (int hi = 0; hi < 2; ++hi) {
+            const int m = row0 + mi * 16 + g8 + 8 * hi;
+            if (m < M_valid) atomicAdd(cc + m, acc[mi][ni][2 * hi + cix]);
+          }
+        }
+      }
+    }
+  }
+}
+
+bool gemm_use_persistent() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("HTLR_GEMM");
+    mode = (e && std::strcmp(e, "legacy") == 0) ? 0 : 1;
+  }
+  return mode == 1;
+}
+
+template <int WM, int WN, int STAGES>
+static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
+                                const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                                int M_valid, int ldc, int RT, cudaStream_t st) {
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC;
+  const size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
+  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const int nitems = ntasks * RT;
+  if (nitems == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = nitems < sms ? nitems : sms;
+  gemm_persistent_kernel<WM, WN, STAGES><<<grid, (WM * WN + 1) * 32, smem, st>>>(
+      A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid, ldc, RT);
+}
+
+void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+                            const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                            int M_valid, int ldc, int RT, cudaStream_t st) {
+  if (MT == 64)
+    launch_persistent_t<2, 2, 6>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+  else
+    launch_persistent_t<4, 2, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+}
+
+}  // namespace htlr

@@ -79,6 +79,12 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st);
 int gemm_nt(int MT);
+// persistent warp-specialised variant (htlr_gemm.cu); HTLR_GEMM=legacy selects
+// the one-CTA-per-item cp.async kernel instead
+bool gemm_use_persistent();
+void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+                            const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                            int M_valid, int ldc, int RT, cudaStream_t st);
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
                      double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
                      int64_t b0, int64_t nb, cudaStream_t st);
