@@ -270,7 +270,14 @@ __global__ void __launch_bounds__(WM* WN * 32, 2)
   }
 }
 
-int gemm_mt_for(int P_out) { return P_out <= 64 ? 64 : 128; }
+// Tile layout per matrix size: "thin" (MT = -M_pad, whole matrix per item,
+// m8n8k4 chains) when 8-row padding of P is a supported instantiation, else
+// 128- (or 64-) row tiles of m16n8k8 fragments.
+int gemm_mt_for(int P_out) {
+  const int m8 = (P_out + 7) / 8;
+  if (gemm_use_persistent() && thin_m8_supported(m8) && P_out != 64) return -8 * m8;
+  return P_out <= 64 ? 64 : 128;
+}
 int gemm_nt(int MT) { return 64; }
 
 template <int WM, int WN, int STAGES>
@@ -290,6 +297,10 @@ static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, 
 void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st) {
+  if (MT < 0) {
+    launch_gemm_thin(-MT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+    return;
+  }
   if (gemm_use_persistent()) {
     launch_gemm_persistent(MT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
     return;

@@ -50,7 +50,17 @@ __device__ __forceinline__ double r2_of(int d, const double* x, const double* y)
 // ---------------------------------------------------------------------------
 constexpr int kKC = 32;
 
+// MT < 0 selects the "thin" layout of gemm_thin_kernel (htlr_gemm.cu): one row
+// tile of M_pad = -MT rows, stored per 32-wide K chunk as
+//   [k4 (8)][m8 (M_pad/8)][lane][1],  lane = (m%8)*4 + k%4
+// i.e. the mma.m8n8k4 A fragment of every 8x4 sub-block is 256 contiguous bytes.
 __host__ __device__ __forceinline__ int64_t tiled_offset(int m, int k, int MT, int K_pad) {
+  if (MT < 0) {
+    const int M_pad = -MT;
+    const int kc = k / kKC, kk = k % kKC;
+    const int lane = (m & 7) * 4 + (kk & 3);
+    return ((int64_t)kc * (kKC / 4) + (kk >> 2)) * (int64_t)(M_pad / 8 * 32) + (int64_t)((m >> 3) * 32 + lane);
+  }
   int rt = m / MT, mm = m % MT;
   int kc = k / kKC, kk = k % kKC;
   int mi = mm >> 4, r16 = mm & 15;

@@ -226,6 +226,148 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   }
 }
 
+__device__ __forceinline__ void mma8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// "thin" variant for matrices of at most 256 rows (p^d = 216, 64, 36, ...):
+// one item covers ALL rows of its matrix (M_pad = 8*M8, no row-tile padding
+// beyond 7 rows) and 64 columns; each of the 8 consumer warps owns 8 columns
+// and runs M8 independent mma.m8n8k4 chains per k4 step.  Rows tiled in m8
+// units keep every SM sub-partition equally busy for P = 216, which the
+// 128-row tiles of the wide kernel cannot (216 = 128 + 88).
+// ---------------------------------------------------------------------------
+template <int M8, int STAGES>
+__global__ void __launch_bounds__(9 * 32, 1)
+    gemm_thin_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
+                     double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
+                     const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc) {
+  constexpr int MP = 8 * M8, NT = 64, KC = kKC, BST = KC + 4, NCW = 8;
+  extern __shared__ __align__(128) double smem[];
+  double* sA = smem;                      // STAGES x MP*KC
+  double* sB = smem + STAGES * MP * KC;   // STAGES x NT*BST
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NT * BST);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int nk = K_pad / KC;
+  if (warp == NCW) {
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const ItemInfo it = item_info(tasks, item, 1, R, Rc, NT);
+      int64_t cb[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int n = lane + 32 * q;
+        cb[q] = -1;
+        if (n < it.ncols) {
+          const int j = n / Rc, r = it.r0 + n % Rc;
+          const int2 pr = pairs[it.pair_begin + j];
+          cb[q] = ((int64_t)pr.y * R + r) * K_pad;
+        }
+      }
+      const double* Ablk = A + (int64_t)it.mat * mat_stride;
+      const unsigned bytes = (unsigned)(MP * KC * 8 + it.ncols * KC * 8);
+      for (int kc = 0; kc < nk; ++kc, ++g) {
+        const int s = g % STAGES;
+        if (g >= (uint32_t)STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_g2s(sA + s * MP * KC, Ablk + (int64_t)kc * MP * KC, MP * KC * 8, &full[s]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = lane + 32 * q;
+          if (cb[q] >= 0) bulk_g2s(sB + s * NT * BST + n * BST, B + cb[q] + kc * KC, KC * 8, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int g8 = lane >> 2, t = lane & 3;
+  const int n0 = warp * 8;
+  uint32_t g = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const ItemInfo it = item_info(tasks, item, 1, R, Rc, NT);
+    const bool active = n0 < it.ncols;
+    double acc[M8][2];
+#pragma unroll
+    for (int i = 0; i < M8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int kc = 0; kc < nk; ++kc, ++g) {
+      const int s = g % STAGES;
+      mbar_wait(&full[s], (g / STAGES) & 1);
+      if (active) {
+        const double* cA = sA + s * MP * KC;
+        const double* cB = sB + s * NT * BST + (n0 + g8) * BST + t;
+#pragma unroll
+        for (int k4 = 0; k4 < KC / 4; ++k4) {
+          const double b = cB[k4 * 4];
+          const double* pa = cA + k4 * (M8 * 32) + lane;
+#pragma unroll
+          for (int i = 0; i < M8; ++i) mma8x8x4(acc[i], pa[i * 32], b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (!active) continue;
+#pragma unroll
+    for (int cix = 0; cix < 2; ++cix) {
+      const int n = n0 + 2 * t + cix;
+      if (n >= it.ncols) continue;
+      const int j = n / Rc, r = it.r0 + n % Rc;
+      const int2 pr = pairs[it.pair_begin + j];
+      double* cc = C + ((int64_t)pr.x * R + r) * ldc;
+#pragma unroll
+      for (int i = 0; i < M8; ++i) {
+        const int m = i * 8 + g8;
+        if (m < M_valid) atomicAdd(cc + m, acc[i][cix]);
+      }
+    }
+  }
+}
+
+template <int M8, int STAGES>
+static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, double* C, const GemmTask* tasks,
+                          int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
+                          cudaStream_t st) {
+  constexpr int MP = 8 * M8, KC = kKC;
+  const size_t smem = sizeof(double) * STAGES * (size_t)(MP * KC + 64 * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
+  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ntasks == 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = ntasks < sms ? ntasks : sms;
+  gemm_thin_kernel<M8, STAGES><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
+                                                            K_pad, M_valid, ldc);
+}
+
+int thin_m8_supported(int m8) { return m8 == 5 || m8 == 8 || m8 == 16 || m8 == 27; }
+
+void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
+                      const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,
+                      int ldc, cudaStream_t st) {
+  switch (M_pad / 8) {
+    case 5: launch_thin_t<5, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 8: launch_thin_t<8, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 16: launch_thin_t<16, 3>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 27: launch_thin_t<27, 3>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    default: break;   // not reachable: gemm_mt_for only selects supported sizes
+  }
+}
+
 bool gemm_use_persistent() {
   static int mode = -1;
   if (mode < 0) {

@@ -82,6 +82,10 @@ int gemm_nt(int MT);
 // persistent warp-specialised variant (htlr_gemm.cu); HTLR_GEMM=legacy selects
 // the one-CTA-per-item cp.async kernel instead
 bool gemm_use_persistent();
+int thin_m8_supported(int m8);
+void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
+                      const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,
+                      int ldc, cudaStream_t st);
 void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st);

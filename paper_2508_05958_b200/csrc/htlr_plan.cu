@@ -369,9 +369,9 @@ int htlr_build_lists(htlr_plan* pl) {
   pl->passes.clear();
   auto fill_pass = [&](Pass& ps, std::vector<const OffsetTable*> tabs) {
     ps.MT = htlr::gemm_mt_for(ps.P);
-    ps.M_pad = round_up(ps.P, ps.MT);
+    ps.M_pad = ps.MT < 0 ? -ps.MT : round_up(ps.P, ps.MT);
     ps.K_pad = round_up(ps.P, htlr::kKC);
-    ps.RT = ps.M_pad / ps.MT;
+    ps.RT = ps.MT < 0 ? 1 : ps.M_pad / ps.MT;
     ps.mat_stride = (int64_t)ps.M_pad * ps.K_pad;
     ps.seg.assign(1, 0);
     std::vector<int2> pr;
