@@ -64,6 +64,11 @@ typedef struct htlr_desc {
                                * !smooth_at_diagonal && QuadratureConfig.
                                * corner_subdivision (kernels.py:263-265)       */
   double coeff_const;         /* CoefficientFn.constant(c); see htlr_set_coeff  */
+  int32_t grid_kind;          /* 0 UniformGrid (grids.py:18-50); 1 mapped
+                               * quasi-uniform tensor grid of BASELINE config
+                               * 5: x_i = phi((i+1/2)/n), cells [phi(i/n),
+                               * phi((i+1)/n)], phi(t) = t + A sin(2 pi t)/(2 pi) */
+  double amplitude;           /* A (mapped grid only)                          */
 } htlr_desc;
 
 /* Create a plan on `device` (-1: host-only plan that can build and export

@@ -574,3 +574,216 @@ def storage_counts(pb: Problem, leaves: list) -> dict:
                 factors += (hi - lo) * p
     return {"dense": dense, "factors": factors, "cores": cores,
             "total": dense + factors + cores}
+
+
+# --------------------------------------------------------------------------
+# BASELINE config 5: mapped quasi-uniform tensor grid.  The reference cannot
+# represent it (UniformGrid only, grids.py:18-43), so this restatement is the
+# oracle (parity UNPINNED by the reference; pinned instead by the
+# amplitude-0 limit, which reproduces the reference's uniform results, and by
+# dense-vs-HTLR agreement).  It follows the reference's algorithm with the
+# mapped geometry substituted:
+#   points x_i = phi((i + 1/2)/n), cell [phi(i/n), phi((i+1)/n)], weight
+#   w_i = prod_a (cell width)  (grids.py:39-50, 237-242 with phi applied);
+#   domain boxes from the cell boundaries; Chebyshev nodes on the mapped
+#   intervals (chebyshev.py:31-85); Tucker blocks as blocks.py:126-164 with the
+#   source weights folded into the source factors instead of h^d;
+#   dense blocks K_ij w_j with the diagonal = integral of k(x_i, .) over the
+#   (off-centre, rectangular) cell: kernels.py:222-249 generalised to 2^d
+#   rectangular corner boxes.
+# phi(t) = t + A sin(2 pi t) / (2 pi)  (BASELINE.json configs[4]).
+# --------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class MappedGeometry:
+    n: int
+    amplitude: float = 0.05
+
+    def phi(self, t: float) -> float:
+        return t + self.amplitude * math.sin(2 * math.pi * t) / (2 * math.pi)
+
+    def boundaries(self) -> np.ndarray:
+        return np.array([self.phi(i / self.n) for i in range(self.n + 1)])
+
+    def coords(self) -> np.ndarray:
+        return np.array([self.phi((i + 0.5) / self.n) for i in range(self.n)])
+
+    def widths(self) -> np.ndarray:
+        b = self.boundaries()
+        return b[1:] - b[:-1]
+
+
+def mapped_points(geo: MappedGeometry, ranges: Ranges) -> np.ndarray:
+    x = geo.coords()
+    mesh = np.meshgrid(*[x[lo:hi] for lo, hi in ranges], indexing="ij")
+    return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
+
+
+def mapped_weights(geo: MappedGeometry, ranges: Ranges) -> np.ndarray:
+    c = geo.widths()
+    w = np.ones(1)
+    for lo, hi in ranges:    # F-order tensor product: first index fastest
+        w = np.outer(c[lo:hi], w).ravel()
+    return w
+
+
+def mapped_domain(geo: MappedGeometry, ranges: Ranges):
+    b = geo.boundaries()
+    return tuple((b[lo], b[hi]) for lo, hi in ranges)
+
+
+def mapped_block_leaves(geo: MappedGeometry, d: int, leaf_side_max: int, rule: str = "strong",
+                        eta: Optional[float] = 1.0) -> list:
+    """grids.py:268-296 on the mapped domains."""
+    root = cluster_tree(geo.n, d, leaf_side_max)
+    out: list = []
+
+    def visit(t: Cluster, s: Cluster, level: int):
+        if admissible(rule, eta, mapped_domain(geo, t.ranges), mapped_domain(geo, s.ranges)):
+            out.append(Leaf(len(out), ADM, level, t.ranges, s.ranges))
+            return
+        if not t.kids or not s.kids:
+            out.append(Leaf(len(out), NEAR, level, t.ranges, s.ranges))
+            return
+        for sk in s.kids:
+            for tk in t.kids:
+                visit(tk, sk, level + 1)
+
+    visit(root, root, 0)
+    return out
+
+
+def mapped_tucker_block(k: Kernel, geo: MappedGeometry, tau: Ranges, sigma: Ranges, p: int) -> Tucker:
+    d = len(tau)
+    x = geo.coords()
+    c = geo.widths()
+    dt, ds = mapped_domain(geo, tau), mapped_domain(geo, sigma)
+    if _overlap_volume(dt, ds) > 0.0:
+        raise ValueError("interpolation blocks require disjoint domains")
+    nt = [cheb_nodes(lo, hi, p) for lo, hi in dt]
+    ns = [cheb_nodes(lo, hi, p) for lo, hi in ds]
+    raw_u = [lagrange_matrix(x[tau[a][0]:tau[a][1]], nt[a]) for a in range(d)]
+    raw_v = [c[sigma[a][0]:sigma[a][1], None] * lagrange_matrix(x[sigma[a][0]:sigma[a][1]], ns[a])
+             for a in range(d)]
+    core = kernel_core(k, nt, ns)
+    ufac, vfac = [], []
+    for a in range(d):
+        for raw, facs, mode in ((raw_u[a], ufac, a + 1), (raw_v[a], vfac, d + a + 1)):
+            if raw.shape[0] < raw.shape[1]:
+                raise ValueError(f"qr requires rows >= cols, got shape {raw.shape}")
+            if raw.shape[0] == raw.shape[1]:
+                facs.append(None)
+                core = mode_mul(core, raw, mode)
+            else:
+                q, r = np.linalg.qr(raw, mode="reduced")
+                facs.append(q)
+                core = mode_mul(core, r, mode)
+    return Tucker(core, ufac, vfac)
+
+
+def mapped_cell_integrals(k: Kernel, geo: MappedGeometry, idx: np.ndarray, q: int = 10) -> np.ndarray:
+    """Integral of k(x_i, .) over the rectangular cell of each point (rows of
+    the multi-index array `idx`), split at x_i into 2^d corner boxes, each
+    integrated with the d-pyramid Duffy rule and cubic radial grading of
+    kernels.py:222-249 (there: equal corner boxes of side h/2)."""
+    idx = np.atleast_2d(np.asarray(idx, dtype=np.int64))
+    npts, d = idx.shape
+    b = geo.boundaries()
+    x = geo.coords()
+    gx, gw = _gl01(q)
+    rad = gx ** GRADING
+    rad_w = GRADING * gx ** (GRADING - 1) * gw
+    total = np.zeros(npts)
+    for corner in np.ndindex(*([2] * d)):
+        ext = np.stack([(b[idx[:, a] + 1] - x[idx[:, a]]) if corner[a] else (x[idx[:, a]] - b[idx[:, a]])
+                        for a in range(d)], axis=-1)                       # (npts, d)
+        for axis in range(d):
+            nodes = [rad if a == axis else gx for a in range(d)]
+            mesh = np.meshgrid(*nodes, indexing="ij")
+            w = _tensor_weights([rad_w if a == axis else gw for a in range(d)]).ravel()
+            t = mesh[axis].ravel()
+            unit = np.stack([t if a == axis else t * mesh[a].ravel() for a in range(d)], axis=-1)   # (m, d)
+            pts = ext[:, None, :] * unit[None, :, :]                          # (npts, m, d)
+            jac = np.prod(ext, axis=1)[:, None] * t[None, :] ** (d - 1)
+            vals = kernel_values(k, np.zeros_like(pts), pts)
+            total += np.sum(vals * (jac * w[None, :]), axis=1)
+    return total
+
+
+def mapped_cell_integral(k: Kernel, geo: MappedGeometry, idx, q: int = 10) -> float:
+    return float(mapped_cell_integrals(k, geo, np.asarray([idx]), q)[0])
+
+
+def mapped_dense_block(k: Kernel, coeff, geo: MappedGeometry, tau: Ranges, sigma: Ranges,
+                       q: int = 10) -> np.ndarray:
+    xs = mapped_points(geo, tau)
+    ys = mapped_points(geo, sigma)
+    w = mapped_weights(geo, sigma)
+    if tau == sigma:
+        d = len(tau)
+        diag = mapped_cell_integrals(k, geo, np.asarray(_box_multi_indices(tau)), q)
+        mat = kernel_pairs_self(k, xs, np.zeros(len(xs))) * w[None, :]
+        i = np.arange(len(xs))
+        mat[i, i] = diag + np.asarray(coeff(xs), dtype=np.float64)
+        return mat
+    return kernel_pairs(k, xs, ys) * w[None, :]
+
+
+def _box_multi_indices(ranges: Ranges):
+    """Multi-indices of a box in F-order (first index fastest)."""
+    mesh = np.meshgrid(*[np.arange(lo, hi) for lo, hi in ranges], indexing="ij")
+    return list(zip(*[m.ravel(order="F") for m in mesh]))
+
+
+@dataclass
+class MappedProblem:
+    d: int
+    geo: MappedGeometry
+    rank: int
+    leaf_side_max: int
+    kernel: Kernel
+    coeff: Callable[[np.ndarray], np.ndarray]
+    rule: str = "strong"
+    eta: Optional[float] = 1.0
+    q: int = 10
+
+    @property
+    def n(self) -> int:
+        return self.geo.n
+
+    @property
+    def num_points(self) -> int:
+        return self.geo.n ** self.d
+
+
+def mapped_matvec(pb: MappedProblem, u: np.ndarray, leaves: Optional[list] = None) -> np.ndarray:
+    """Leaf-by-leaf matvec on the mapped grid (operators.py:138-161)."""
+    u = np.asarray(u, dtype=np.float64)
+    cols = u.reshape(pb.num_points, -1)
+    if leaves is None:
+        leaves = mapped_block_leaves(pb.geo, pb.d, pb.leaf_side_max, pb.rule, pb.eta)
+    shape = (pb.n,) * pb.d
+    out = np.zeros_like(cols)
+    payloads = []
+    for lf in leaves:
+        if lf.kind == ADM:
+            payloads.append(mapped_tucker_block(pb.kernel, pb.geo, lf.tau, lf.sigma, pb.rank))
+        else:
+            payloads.append(mapped_dense_block(pb.kernel, pb.coeff, pb.geo, lf.tau, lf.sigma, pb.q))
+    for r in range(cols.shape[1]):
+        ut = cols[:, r].reshape(shape, order="F")
+        ft = np.zeros(shape)
+        for lf, pl in zip(leaves, payloads):
+            seg = ut[_slices(lf.sigma)].ravel(order="F")
+            res = apply_payload(pl, seg)
+            ft[_slices(lf.tau)] += res.reshape([hi - lo for lo, hi in lf.tau], order="F")
+        out[:, r] = ft.ravel(order="F")
+    return out.reshape(u.shape)
+
+
+def mapped_dense_matrix(pb: MappedProblem) -> np.ndarray:
+    """Full Nystrom matrix on the mapped grid (small n; exactness check of the
+    compressed operator)."""
+    full = tuple((0, pb.n) for _ in range(pb.d))
+    return mapped_dense_block(pb.kernel, pb.coeff, pb.geo, full, full, pb.q)

@@ -35,6 +35,8 @@ class HtlrDesc(ctypes.Structure):
         ("quad_q", ctypes.c_int32),
         ("corner_subdivision", ctypes.c_int32),
         ("coeff_const", ctypes.c_double),
+        ("grid_kind", ctypes.c_int32),
+        ("amplitude", ctypes.c_double),
     ]
 
 

@@ -1,9 +1,10 @@
 """The BASELINE.json workloads as (grid, BuildConfig, input) recipes.
 
-configs[0..3] of /root/repo/BASELINE.json; inputs follow its seeds in the
-reference's F-order grid linearisation.  Config 5 (mapped quasi-uniform
-grid) is not representable by the reference's UniformGrid and is not part
-of this round's hot path.
+configs[0..4] of /root/repo/BASELINE.json; inputs follow its seeds in the
+reference's F-order grid linearisation.  Config 5 uses the mapped
+quasi-uniform grid (not representable by the reference's UniformGrid) with
+the reference's leaf semantics: leaf_side 8 at n = 96 gives side-6 leaves
+(grids.py:196-207).
 """
 
 from __future__ import annotations
@@ -13,7 +14,7 @@ from typing import Callable
 
 import numpy as np
 
-from .grids import AdmissibilityRule, UniformGrid
+from .grids import AdmissibilityRule, MappedGrid, UniformGrid
 from .kernels import CoefficientFn, KernelSpec, gaussian_bw, inv_r_3d, neg_log_2d
 from .operators import BuildConfig
 
@@ -30,9 +31,12 @@ class Workload:
     nrhs: int
     matvecs: int
     description: str
+    amplitude: float = -1.0   # >= 0: MappedGrid with this amplitude
 
     @property
-    def grid(self) -> UniformGrid:
+    def grid(self):
+        if self.amplitude >= 0:
+            return MappedGrid(self.d, self.n, self.amplitude)
         return UniformGrid(self.d, self.n)
 
     def build_config(self) -> BuildConfig:
@@ -57,4 +61,7 @@ WORKLOADS = {
                      "3D n=64 1/|x-y| leaf 8 eta=1 p=6, 16 RHS batched matvec"),
     "cfg4": Workload("cfg4", 3, 128, 8, 8, lambda: gaussian_bw(0.1), 0.0, 1, 1,
                      "3D n=128 exp(-|x-y|^2/0.01) leaf 8 eta=1 p=8, matvec"),
+    "cfg5": Workload("cfg5", 3, 96, 8, 6, inv_r_3d, 0.0, 1, 1,
+                     "3D mapped quasi-uniform n=96 (x=t+0.05 sin(2 pi t)/(2 pi)) 1/|x-y| leaf 8 (side 6) "
+                     "eta=1 p=6, construct + matvec", amplitude=0.05),
 }

@@ -51,17 +51,24 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
 // p*s + p^2 + p^3 values whatever the box side.
 // ---------------------------------------------------------------------------
 __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
-                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t c0) {
+                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
+                              int64_t c0) {
   extern __shared__ double sm[];
-  double* sQ = sm;             // s*p
-  double* T1 = sQ + s * p;     // p*s
+  double* sQ = sm;             // d x s*p (factor of each dimension)
+  double* T1 = sQ + d * s * p; // p*s
   double* T2 = T1 + p * s;     // p*p
   double* acc = T2 + p * p;    // p^d
   const int64_t c = c0 + blockIdx.x;   // cluster, Morton id
   const int r = blockIdx.y;
   int cc[3];
   morton_decode(c, d, bits, cc);
-  for (int i = threadIdx.x; i < s * p; i += blockDim.x) sQ[i] = Q[i];
+  for (int i = threadIdx.x; i < d * s * p; i += blockDim.x) {
+    const int a = i / (s * p);
+    sQ[i] = Q[(qstride ? cc[a] * qstride : 0) + i % (s * p)];
+  }
+  const double* sQx = sQ;
+  const double* sQy = sQ + s * p;
+  const double* sQz = sQ + 2 * s * p;
   const int P = (d == 2) ? p * p : p * p * p;
   for (int i = threadIdx.x; i < P; i += blockDim.x) acc[i] = 0.0;
   __syncthreads();
@@ -73,7 +80,7 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
       int64_t g = (int64_t)cc[0] * s + (int64_t)n * (cc[1] * s + y);
       if (d == 3) g += (int64_t)n * n * (cc[2] * s + z);
       double v = 0.0;
-      for (int x = 0; x < s; ++x) v += sQ[x * p + a1] * u[(g + x) * R + r];
+      for (int x = 0; x < s; ++x) v += sQx[x * p + a1] * u[(g + x) * R + r];
       T1[i] = v;
     }
     __syncthreads();
@@ -81,7 +88,7 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
       for (int i = threadIdx.x; i < p * p; i += blockDim.x) {
         int a1 = i % p, a2 = i / p;
         double v = 0.0;
-        for (int y = 0; y < s; ++y) v += sQ[y * p + a2] * T1[a1 + p * y];
+        for (int y = 0; y < s; ++y) v += sQy[y * p + a2] * T1[a1 + p * y];
         acc[i] = v;
       }
       __syncthreads();
@@ -89,13 +96,13 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
       for (int i = threadIdx.x; i < p * p; i += blockDim.x) {
         int a1 = i % p, a2 = i / p;
         double v = 0.0;
-        for (int y = 0; y < s; ++y) v += sQ[y * p + a2] * T1[a1 + p * y];
+        for (int y = 0; y < s; ++y) v += sQy[y * p + a2] * T1[a1 + p * y];
         T2[i] = v;
       }
       __syncthreads();
       for (int i = threadIdx.x; i < P; i += blockDim.x) {
         int a12 = i % (p * p), a3 = i / (p * p);
-        acc[i] += sQ[z * p + a3] * T2[a12];
+        acc[i] += sQz[z * p + a3] * T2[a12];
       }
       __syncthreads();
     }
@@ -105,11 +112,12 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
 }
 
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, int64_t c0, int64_t nc, cudaStream_t st) {
+                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st) {
   int P = (d == 2) ? p * p : p * p * p;
-  size_t smem = sizeof(double) * (size_t)(side * p + p * side + p * p + P);
+  size_t smem = sizeof(double) * (size_t)(d * side * p + p * side + p * p + P);
   if (smem > 48 * 1024) cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (nc > 0) upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, c0);
+  if (nc > 0)
+    upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride, c0);
 }
 
 // ---------------------------------------------------------------------------
@@ -318,8 +326,8 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
 // ---------------------------------------------------------------------------
 __global__ void downward_kernel(const double* __restrict__ u, double* __restrict__ f,
                                 const double* __restrict__ Y, int ldy, const double* __restrict__ avec,
-                                double aconst, int d, int n, int sL, int L, int R, int p, DownParams dp,
-                                int64_t b0) {
+                                double aconst, const double* __restrict__ dvec, int d, int n, int sL, int L, int R,
+                                int p, DownParams dp, int64_t b0) {
   extern __shared__ double sm[];
   const int PL = (d == 2) ? sL * sL : sL * sL * sL;
   const int P = (d == 2) ? p * p : p * p * p;
@@ -345,7 +353,8 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
     for (int i = threadIdx.x; i < d * sL * p; i += blockDim.x) {
       int a = i / (sL * p), rem = i % (sL * p);
       int x = rem / p, col = rem % p;
-      Us[i] = lv.Q[(off[a] + x) * p + col];
+      const int64_t base = lv.qstride ? (int64_t)(bc[a] >> shift) * lv.qstride : 0;
+      Us[i] = lv.Q[base + (off[a] + x) * p + col];
     }
     __syncthreads();
     const double* U1 = Us;
@@ -397,6 +406,7 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
     if (d == 3) gidx += (int64_t)n * n * (bc[2] * sL + z);
     double uv = u[gidx * R + r];
     double a = avec ? avec[gidx] : aconst;
+    if (dvec) a = dvec[gidx] + a;   // mapped grid: per-point cell integral
     double v = facc[i];
     if (Yb) v += Yb[i];
     f[gidx * R + r] = v + a * uv;
@@ -404,8 +414,8 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
 }
 
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
-                     double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
-                     int64_t b0, int64_t nb, cudaStream_t st) {
+                     double a_const, const double* dvec, int d, int n, int sL, int L, int R, int p,
+                     const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st) {
   int P = (d == 2) ? p * p : p * p * p;
   int PL = (d == 2) ? sL * sL : sL * sL * sL;
   size_t words = PL + P + sL * ((d == 2) ? p : p * p) + ((d == 3) ? sL * sL * p : 0) + d * sL * p;
@@ -413,8 +423,8 @@ void launch_downward(const double* u, double* f, const double* Y, int ldy, const
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(downward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (nb > 0)
-    downward_kernel<<<dim3((unsigned)nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, d, n, sL, L, R, p, dp,
-                                                             b0);
+    downward_kernel<<<dim3((unsigned)nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, dvec, d, n, sL, L, R, p,
+                                                             dp, b0);
 }
 
 }  // namespace htlr

@@ -48,8 +48,18 @@ struct DownLevel {
   int level;
   int side;        // box side at this level
   int P;           // p^d
-  const double* Q; // side x p row-major
+  const double* Q; // side x p row-major (uniform), or per-interval tables
   const double* H; // [cluster][R][P]
+  int64_t qstride; // 0: one factor for the level; else doubles per interval
+};
+
+// mapped grid: per (level, interval) nodes and raw factors
+struct MappedFactorJob {
+  int side;
+  int nint;        // intervals per dimension at this level
+  double* nodes;   // [nint][p]
+  double* L;       // [nint][side][p]   raw Lagrange factor (target side)
+  double* WL;      // [nint][side][p]   cell widths x factor (source side)
 };
 
 struct DownParams {
@@ -72,7 +82,7 @@ void launch_near_blocks(const NearJob* jobs, int njobs, int d, int s, double h, 
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
                        int64_t nb, cudaStream_t st);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, int64_t c0, int64_t nc, cudaStream_t st);
+                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
 void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
@@ -90,7 +100,23 @@ void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const d
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st);
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
-                     double a_const, int d, int n, int sL, int L, int R, int p, const DownParams& dp,
-                     int64_t b0, int64_t nb, cudaStream_t st);
+                     double a_const, const double* dvec, int d, int n, int sL, int L, int R, int p,
+                     const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st);
+
+// mapped grid (htlr_mapped.cu)
+void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,
+                           const double* coords, const double* widths, int p, cudaStream_t st);
+void launch_mapped_diag(const KernelParams& kp, int d, int n, int q, const double* gx, const double* gw,
+                        const double* bounds, const double* coords, double* out, int64_t npts, cudaStream_t st);
+void launch_regen_adm(const KernelParams& kp, int d, int p, int level, const double* nodes, const int64_t* rowptr,
+                      const int* cols, int64_t t0, int64_t nt, const double* W, int K_pad, double* H, int R,
+                      cudaStream_t st);
+void launch_regen_near(const KernelParams& kp, int d, int sL, int L, const double* coords, const double* widths,
+                       const int64_t* rowptr, const int* cols, int64_t t0, int64_t nt, const double* ub, int K_pad,
+                       double* Y, int R, cudaStream_t st);
+void launch_mapped_core_export(const KernelParams& kp, int d, int p, const double* nt, const double* ns, double* out,
+                               cudaStream_t st);
+void launch_mapped_near_export(const KernelParams& kp, int d, int sL, const double* xt, const double* ys,
+                               const double* ws, int self, double* out, cudaStream_t st);
 
 }  // namespace htlr

@@ -17,6 +17,7 @@
 #include "htlr_lists.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 namespace htlr {
@@ -90,11 +91,12 @@ bool admissible_boxes(const TreeSpec& spec, const int* tlo, const int* thi, cons
                       const int* shi) {
   const double h = 1.0 / (double)spec.n;
   double a1[3], b1[3], a2[3], b2[3];
+  const bool mapped = !spec.bounds.empty();
   for (int a = 0; a < spec.d; ++a) {
-    a1[a] = (double)tlo[a] * h;
-    b1[a] = (double)thi[a] * h;
-    a2[a] = (double)slo[a] * h;
-    b2[a] = (double)shi[a] * h;
+    a1[a] = mapped ? spec.bounds[tlo[a]] : (double)tlo[a] * h;
+    b1[a] = mapped ? spec.bounds[thi[a]] : (double)thi[a] * h;
+    a2[a] = mapped ? spec.bounds[slo[a]] : (double)slo[a] * h;
+    b2[a] = mapped ? spec.bounds[shi[a]] : (double)shi[a] * h;
   }
   if (spec.rule == 0) return overlap_volume(spec.d, a1, b1, a2, b2) == 0.0;
   double dist = distance_sq(spec.d, a1, b1, a2, b2);
@@ -170,6 +172,26 @@ struct Builder {
 };
 
 }  // namespace
+
+double mapped_phi(double t, double amplitude) {
+  const double two_pi = 2.0 * 3.141592653589793;
+  double arg = two_pi * t;
+  double v = amplitude * std::sin(arg);
+  v = v / two_pi;
+  return t + v;
+}
+
+void mapped_tables(int n, double amplitude, std::vector<double>& bounds, std::vector<double>& coords,
+                   std::vector<double>& widths) {
+  bounds.resize(n + 1);
+  coords.resize(n);
+  widths.resize(n);
+  for (int i = 0; i <= n; ++i) bounds[i] = mapped_phi((double)i / (double)n, amplitude);
+  for (int i = 0; i < n; ++i) {
+    coords[i] = mapped_phi(((double)i + 0.5) / (double)n, amplitude);
+    widths[i] = bounds[i + 1] - bounds[i];
+  }
+}
 
 int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
   if (spec.d != 2 && spec.d != 3) {

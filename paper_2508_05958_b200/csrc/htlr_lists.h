@@ -17,7 +17,16 @@ struct TreeSpec {
   int leaf_side_max = 0;
   int rule = 1;        // 0 weak, 1 strong
   double eta = 1.0;
+  // mapped tensor grid (BASELINE config 5): cell boundaries phi(i/n),
+  // i = 0..n, used for the domain boxes; empty = uniform grid (i*h)
+  std::vector<double> bounds;
 };
+
+// phi(t) = t + A sin(2 pi t) / (2 pi), evaluated in the same operation order
+// as the oracle's Python expression (oracle/htlr_oracle.py MappedGeometry).
+double mapped_phi(double t, double amplitude);
+void mapped_tables(int n, double amplitude, std::vector<double>& bounds, std::vector<double>& coords,
+                   std::vector<double>& widths);
 
 // One admissible or inadmissible leaf, in cluster coordinates of its level.
 struct LeafRec {

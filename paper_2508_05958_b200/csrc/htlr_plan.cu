@@ -105,6 +105,11 @@ struct Level {
   DevBuf Q, R;             // side x p, p x p
   DevBuf W, H;             // workspaces
   bool needs_up = false;   // W via upward pass, H via downward pass
+  // mapped grid: per-interval nodes / raw factors, CSR of own targets
+  DevBuf nodes, Lm, WLm;
+  std::vector<int64_t> csr_ptr;
+  std::vector<int> csr_cols;
+  DevBuf d_ptr, d_cols;
 };
 
 }  // namespace
@@ -131,6 +136,14 @@ struct htlr_plan {
   int64_t last_launches = 0;
   int64_t device_scalars = 0;
   // per-launch profiling of the last matvec (htlr_profile_*)
+  // mapped quasi-uniform grid (BASELINE config 5): no translation invariance,
+  // cores regenerated in the matvec (htlr_mapped.cu)
+  bool mapped = false;
+  std::vector<double> mb, mx, mc;          // cell bounds, coords, widths (per dim)
+  DevBuf d_mb, d_mx, d_mc, dvec;
+  std::vector<int64_t> near_ptr;
+  std::vector<int> near_cols;
+  DevBuf d_near_ptr, d_near_cols;
   // sharding by cluster subtrees (multi-GPU): this plan computes the f rows
   // of leaf boxes [own_lo[L], own_hi[L]) and the upward data of its own
   // source clusters; every level's own range is a contiguous Morton range
@@ -243,6 +256,12 @@ int htlr_plan_create(const htlr_desc* desc, int device, htlr_plan** out) {
   for (int a = 0; a < pl->d; ++a) pl->N *= desc->n;
   pl->h = 1.0 / (double)desc->n;
   pl->hd = std::pow(pl->h, (double)pl->d);   // Python h**d
+  if (desc->grid_kind != 0 && desc->grid_kind != 1) {
+    delete pl;
+    return fail(-1, "unknown grid kind");
+  }
+  pl->mapped = desc->grid_kind == 1;
+  if (pl->mapped) htlr::mapped_tables(desc->n, desc->amplitude, pl->mb, pl->mx, pl->mc);
   pl->kp.kind = desc->kernel;
   pl->kp.denom = (2.0 * desc->sigma) * desc->sigma;
   pl->kp.scale = desc->scale;
@@ -263,7 +282,18 @@ int htlr_plan_destroy(htlr_plan* pl) {
     lv.R.release();
     lv.W.release();
     lv.H.release();
+    lv.nodes.release();
+    lv.Lm.release();
+    lv.WLm.release();
+    lv.d_ptr.release();
+    lv.d_cols.release();
   }
+  pl->d_mb.release();
+  pl->d_mx.release();
+  pl->d_mc.release();
+  pl->dvec.release();
+  pl->d_near_ptr.release();
+  pl->d_near_cols.release();
   for (auto& ps : pl->passes) {
     ps.table.release();
     ps.pairs.release();
@@ -286,6 +316,7 @@ int htlr_build_lists(htlr_plan* pl) {
   ts.leaf_side_max = pl->desc.leaf_side_max;
   ts.rule = pl->desc.rule;
   ts.eta = pl->desc.eta;
+  if (pl->mapped) ts.bounds = pl->mb;
   std::string err;
   if (htlr::build_tree(ts, pl->tree, err)) return fail(-1, err);
   const Tree& tr = pl->tree;
@@ -364,9 +395,39 @@ int htlr_build_lists(htlr_plan* pl) {
   const int P = ipow(p, d);
   if (PL > 4096) return fail(-1, "leaf boxes above 4096 points are not supported by the B200 path");
   if (P > 4096) return fail(-1, "rank^d above 4096 is not supported by the B200 path");
+  pl->passes.clear();
+  if (pl->mapped) {
+    // CSR of the own targets per level (sources sorted by Morton id)
+    auto csr = [&](const OffsetTable& tab, int level, std::vector<int64_t>& ptr, std::vector<int>& cols) {
+      std::vector<std::pair<int, int>> all;
+      for (const auto& mem : tab.members) all.insert(all.end(), mem.begin(), mem.end());
+      std::sort(all.begin(), all.end());
+      const int64_t lo = pl->own_lo[level], hi = pl->own_hi[level];
+      ptr.assign(hi - lo + 1, 0);
+      cols.clear();
+      size_t k = 0;
+      for (int64_t tgt = lo; tgt < hi; ++tgt) {
+        while (k < all.size() && all[k].first == tgt) cols.push_back(all[k++].second);
+        ptr[tgt - lo + 1] = (int64_t)cols.size();
+      }
+    };
+    for (int l = 0; l <= pl->L; ++l) {
+      Level& lv = pl->levels[l];
+      lv.needs_up = lv.num_adm > 0;
+      if (lv.needs_up) {
+        if (pl->own_lo[l] < 0) return fail(-1, "admissible blocks on a level with fewer clusters than shards");
+        csr(lv.adm, l, lv.csr_ptr, lv.csr_cols);
+      }
+    }
+    csr(pl->near, pl->L, pl->near_ptr, pl->near_cols);
+    if (pl->sL > 16) return fail(-1, "mapped grids support leaf sides up to 16");
+    pl->merged = false;
+    pl->lists_built = true;
+    pl->constructed = false;
+    return 0;
+  }
   pl->merged = pl->levels[pl->L].num_adm > 0 && pl->sL == p;
   // passes
-  pl->passes.clear();
   auto fill_pass = [&](Pass& ps, std::vector<const OffsetTable*> tabs) {
     ps.MT = htlr::gemm_mt_for(ps.P);
     ps.M_pad = ps.MT < 0 ? -ps.MT : round_up(ps.P, ps.MT);
@@ -439,6 +500,15 @@ int htlr_shard_info(const htlr_plan* pl, int64_t* own_leaf_lo, int64_t* own_leaf
     pairs += ps.npairs;
     fl += 2.0 * (double)ps.P * ps.P * ps.npairs;
   }
+  if (pl->mapped) {
+    const double P = ipow(pl->p, pl->d), PL = ipow(pl->sL, pl->d);
+    for (const auto& lv : pl->levels) {
+      pairs += (int64_t)lv.csr_cols.size();
+      fl += 2.0 * P * P * (double)lv.csr_cols.size();
+    }
+    pairs += (int64_t)pl->near_cols.size();
+    fl += 2.0 * PL * PL * (double)pl->near_cols.size();
+  }
   if (own_leaf_lo) *own_leaf_lo = pl->own_lo[pl->L];
   if (own_leaf_hi) *own_leaf_hi = pl->own_hi[pl->L];
   if (own_pairs) *own_pairs = pairs;
@@ -448,6 +518,13 @@ int htlr_shard_info(const htlr_plan* pl, int64_t* own_leaf_lo, int64_t* own_leaf
 
 static void exchange_sizes(const htlr_plan* pl, int R, std::vector<int64_t>& bytes) {
   bytes.clear();
+  if (pl->mapped) {
+    const int P = ipow(pl->p, pl->d), PL = ipow(pl->sL, pl->d);
+    bytes.push_back(pl->levels[pl->L].nclusters * (int64_t)R * PL * (int64_t)sizeof(double));
+    for (const auto& lv : pl->levels)
+      if (lv.needs_up) bytes.push_back(lv.nclusters * (int64_t)R * P * (int64_t)sizeof(double));
+    return;
+  }
   const Pass& lp = pl->passes[pl->leaf_pass];
   bytes.push_back(pl->levels[pl->L].nclusters * (int64_t)R * lp.K_pad * (int64_t)sizeof(double));
   for (const auto& ps : pl->passes) {
@@ -537,6 +614,60 @@ int htlr_set_coeff(htlr_plan* pl, const double* a_host) {
   return 0;
 }
 
+static int upload(DevBuf& buf, const void* src, size_t bytes) {
+  if (buf.alloc(std::max<size_t>(bytes, 8))) return 1;
+  if (bytes) CUDA_TRY(cudaMemcpy(buf.ptr, src, bytes, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// Mapped grid construction: geometry tables, per (level, interval) nodes and
+// raw factors, per-point diagonal cell integrals, CSR lists of own targets.
+static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
+  const int d = pl->d, p = pl->p, n = pl->n;
+  if (upload(pl->d_mb, pl->mb.data(), pl->mb.size() * sizeof(double))) return 1;
+  if (upload(pl->d_mx, pl->mx.data(), pl->mx.size() * sizeof(double))) return 1;
+  if (upload(pl->d_mc, pl->mc.data(), pl->mc.size() * sizeof(double))) return 1;
+  std::vector<htlr::MappedFactorJob> jobs;
+  int total = 0;
+  pl->device_scalars = 0;
+  for (auto& lv : pl->levels) {
+    if (!lv.needs_up) continue;
+    const int nint = lv.m;
+    if (lv.nodes.alloc((size_t)nint * p * sizeof(double))) return 1;
+    if (lv.Lm.alloc((size_t)nint * lv.side * p * sizeof(double))) return 1;
+    if (lv.WLm.alloc((size_t)nint * lv.side * p * sizeof(double))) return 1;
+    jobs.push_back({lv.side, nint, lv.nodes.d(), lv.Lm.d(), lv.WLm.d()});
+    total += nint;
+    pl->device_scalars += (int64_t)nint * p * (1 + 2 * lv.side);
+    if (upload(lv.d_ptr, lv.csr_ptr.data(), lv.csr_ptr.size() * sizeof(int64_t))) return 1;
+    if (upload(lv.d_cols, lv.csr_cols.data(), lv.csr_cols.size() * sizeof(int))) return 1;
+  }
+  if (upload(pl->d_near_ptr, pl->near_ptr.data(), pl->near_ptr.size() * sizeof(int64_t))) return 1;
+  if (upload(pl->d_near_cols, pl->near_cols.data(), pl->near_cols.size() * sizeof(int))) return 1;
+  DevBuf djobs;
+  if (!jobs.empty()) {
+    if (upload(djobs, jobs.data(), jobs.size() * sizeof(htlr::MappedFactorJob))) return 1;
+    htlr::launch_mapped_factors((const htlr::MappedFactorJob*)djobs.ptr, (int)jobs.size(), total, pl->d_mb.d(),
+                                pl->d_mx.d(), pl->d_mc.d(), p, st);
+  }
+  // Nystrom diagonal: integral of k(x_i, .) over each point's cell
+  std::vector<double> gx, gw;
+  gauss01(pl->desc.quad_q, gx, gw);
+  gx.insert(gx.end(), gw.begin(), gw.end());
+  if (upload(pl->gl, gx.data(), gx.size() * sizeof(double))) return 1;
+  if (pl->dvec.alloc(pl->N * sizeof(double))) return 1;
+  pl->device_scalars += pl->N;
+  htlr::launch_mapped_diag(pl->kp, d, n, pl->desc.quad_q, pl->gl.d(), pl->gl.d() + pl->desc.quad_q, pl->d_mb.d(),
+                           pl->d_mx.d(), pl->dvec.d(), pl->N, st);
+  if (pl->diag.alloc(sizeof(double))) return 1;
+  CUDA_TRY(cudaMemsetAsync(pl->diag.ptr, 0, sizeof(double), st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  djobs.release();
+  pl->constructed = true;
+  return 0;
+}
+
 int htlr_construct(htlr_plan* pl, void* stream) {
   if (!pl) return fail(-1, "null plan");
   if (pl->device < 0) return fail(-1, "host-only plan: no device work");
@@ -552,6 +683,7 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       CUDA_TRY(cudaMemcpy(ps.pairs.ptr, ps.pairs_host.data(), ps.pairs_host.size() * sizeof(int2),
                           cudaMemcpyHostToDevice));
   }
+  if (pl->mapped) return construct_mapped(pl, st);
   const int d = pl->d, p = pl->p;
   // diagonal cell average (operators.py:95-99)
   std::vector<double> gx, gw;
@@ -684,6 +816,19 @@ static int ensure_workspace(htlr_plan* pl, int R) {
   if (pl->ws_R >= R) return 0;
   const int d = pl->d, p = pl->p;
   const int P = ipow(p, d);
+  if (pl->mapped) {
+    const int PL = ipow(pl->sL, d);
+    const int64_t nleaf = pl->levels[pl->L].nclusters;
+    if (pl->ub.alloc((size_t)nleaf * R * PL * sizeof(double))) return 1;
+    if (pl->Y.alloc((size_t)nleaf * R * PL * sizeof(double))) return 1;
+    for (auto& lv : pl->levels) {
+      if (!lv.needs_up) continue;
+      if (lv.W.alloc((size_t)lv.nclusters * R * P * sizeof(double))) return 1;
+      if (lv.H.alloc((size_t)lv.nclusters * R * P * sizeof(double))) return 1;
+    }
+    pl->ws_R = R;
+    return 0;
+  }
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int64_t nleaf = pl->levels[pl->L].nclusters;
   if (pl->ub.alloc((size_t)nleaf * R * lp.K_pad * sizeof(double))) return 1;
@@ -710,6 +855,7 @@ struct MvCtx {
   int R, d, p, P;
   double* ub;
   std::vector<double*> W;   // per pass (nullptr for the leaf pass)
+  std::vector<double*> Wl;  // mapped grid: per level
   size_t ev_used = 0;
   int64_t launches = 0;
 
@@ -762,6 +908,12 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   const bool ext = pl->ext_R == cx.R && !pl->ext_ptrs.empty();
   size_t xi = 0;
   cx.ub = ext ? pl->ext_ptrs[xi++] : pl->ub.d();
+  cx.Wl.assign(pl->levels.size(), nullptr);
+  if (pl->mapped) {
+    for (size_t l = 0; l < pl->levels.size(); ++l)
+      if (pl->levels[l].needs_up) cx.Wl[l] = ext ? pl->ext_ptrs[xi++] : pl->levels[l].W.d();
+    return 0;
+  }
   cx.W.assign(pl->passes.size(), nullptr);
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     if (pl->passes[i].to_y) continue;
@@ -777,8 +929,72 @@ void prof_reset(htlr_plan* pl) {
   pl->prof_bytes.clear();
 }
 
+int mv_local_mapped(MvCtx& cx, const double* u) {
+  htlr_plan* pl = cx.pl;
+  const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
+  const double R8 = 8.0 * R;
+  const int PL = ipow(pl->sL, d);
+  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
+  const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
+  if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
+  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, PL, b0, nb, cx.st);
+  if (cx.prof_end()) return 1;
+  for (auto& lv : pl->levels) {
+    if (!lv.needs_up) continue;
+    const int64_t c0 = pl->own_lo[lv.level], nc = pl->own_hi[lv.level] - c0;
+    double s1 = lv.side;
+    double macs = (d == 2) ? (p * s1 * s1 + (double)p * p * s1)
+                           : (p * s1 * s1 * s1 + (double)p * p * s1 * s1 + (double)p * p * p * s1);
+    if (cx.prof_begin(1, lv.level, 2.0 * macs * nc * R, R8 * ((double)pl->N * frac + (double)nc * P))) return 1;
+    htlr::launch_upward(u, cx.Wl[lv.level], d, pl->n, lv.side, p, lv.level, R, P, lv.WLm.d(),
+                        (int64_t)lv.side * p, c0, nc, cx.st);
+    if (cx.prof_end()) return 1;
+  }
+  return 0;
+}
+
+// kernel sampling is counted as 10 flops per evaluation plus the MAC
+int mv_remote_mapped(MvCtx& cx, const double* u, double* f) {
+  htlr_plan* pl = cx.pl;
+  const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
+  const int PL = ipow(pl->sL, d);
+  const double R8 = 8.0 * R;
+  htlr::DownParams dp{};
+  dp.nlev = 0;
+  double down_macs = 0.0;
+  for (auto& lv : pl->levels) {
+    if (!lv.needs_up) continue;
+    const int64_t t0 = pl->own_lo[lv.level], nt = pl->own_hi[lv.level] - t0;
+    const double npair = (double)lv.csr_cols.size();
+    if (cx.prof_begin(5, lv.level, npair * P * P * (10.0 + 2.0 * R), R8 * npair * P)) return 1;
+    htlr::launch_regen_adm(pl->kp, d, p, lv.level, lv.nodes.d(), (const int64_t*)lv.d_ptr.ptr,
+                           (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, lv.H.d(), R, cx.st);
+    if (cx.prof_end()) return 1;
+    if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), lv.H.d(), (int64_t)lv.side * p};
+    double sl = pl->sL;
+    down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
+  }
+  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
+  {
+    const double npair = (double)pl->near_cols.size();
+    if (cx.prof_begin(6, pl->L, npair * PL * PL * (10.0 + 2.0 * R), R8 * npair * PL)) return 1;
+    htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(), (const int64_t*)pl->d_near_ptr.ptr,
+                            (const int*)pl->d_near_cols.ptr, b0, nb, cx.ub, PL, pl->Y.d(), R, cx.st);
+    if (cx.prof_end()) return 1;
+  }
+  const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
+  if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
+  htlr::launch_downward(u, f, pl->Y.d(), PL, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
+                        pl->dvec.d(), d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
+  if (cx.prof_end()) return 1;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int mv_local(MvCtx& cx, const double* u) {
   htlr_plan* pl = cx.pl;
+  if (pl->mapped) return mv_local_mapped(cx, u);
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const double R8 = 8.0 * R;
   const Pass& lp = pl->passes[pl->leaf_pass];
@@ -796,7 +1012,7 @@ int mv_local(MvCtx& cx, const double* u) {
     double macs = (d == 2) ? (p * s1 * s1 + (double)p * p * s1)
                            : (p * s1 * s1 * s1 + (double)p * p * s1 * s1 + (double)p * p * p * s1);
     if (cx.prof_begin(1, lv.level, 2.0 * macs * nc * R, R8 * ((double)pl->N * frac + (double)nc * P))) return 1;
-    htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), c0, nc, cx.st);
+    htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st);
     if (cx.prof_end()) return 1;
   }
   return 0;
@@ -804,6 +1020,7 @@ int mv_local(MvCtx& cx, const double* u) {
 
 int mv_remote(MvCtx& cx, const double* u, double* f) {
   htlr_plan* pl = cx.pl;
+  if (pl->mapped) return mv_remote_mapped(cx, u, f);
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const double R8 = 8.0 * R;
   const Pass& lp = pl->passes[pl->leaf_pass];
@@ -837,15 +1054,15 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
-    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d()};
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0};
     double sl = pl->sL;
     down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
   const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   const double frac = (double)nb / (double)nleaf;
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
-  htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, d,
-                        pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
+  htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
+                        nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
   if (cx.prof_end()) return 1;
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -952,6 +1169,76 @@ int htlr_diag_value(htlr_plan* pl, double* out) {
   return 0;
 }
 
+// Mapped grid export: the regenerated block with raw factors (target: Lagrange
+// factor at the mapped points; source: cell widths x factor), same operator as
+// the reference-style Q/R representation.
+static int export_block_mapped(htlr_plan* pl, const htlr::LeafRec& lf, double* out, int64_t cap, double* factors,
+                               int64_t factor_cap, int32_t* shapes) {
+  const int d = pl->d, p = pl->p;
+  const Level& lv = pl->levels[lf.level];
+  DevBuf tmp, dout;
+  if (lf.kind == 0) {
+    const int s = lv.side, P = ipow(p, d);
+    if ((int64_t)P * P > cap) return fail(-1, "block buffer too small");
+    if (!factors || factor_cap < (int64_t)2 * d * s * p) return fail(-1, "factor buffer too small");
+    std::vector<double> nodes((size_t)lv.m * p), L((size_t)lv.m * s * p), WL((size_t)lv.m * s * p);
+    CUDA_TRY(cudaMemcpy(nodes.data(), lv.nodes.ptr, nodes.size() * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(L.data(), lv.Lm.ptr, L.size() * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(WL.data(), lv.WLm.ptr, WL.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> ntns(2 * 3 * p, 0.0);
+    for (int a = 0; a < d; ++a)
+      for (int t = 0; t < p; ++t) {
+        ntns[a * p + t] = nodes[(size_t)lf.tc[a] * p + t];
+        ntns[3 * p + a * p + t] = nodes[(size_t)lf.sc[a] * p + t];
+      }
+    if (upload(tmp, ntns.data(), ntns.size() * 8) || dout.alloc((size_t)P * P * 8)) return 1;
+    htlr::launch_mapped_core_export(pl->kp, d, p, tmp.d(), tmp.d() + 3 * p, dout.d(), 0);
+    CUDA_TRY(cudaMemcpy(out, dout.ptr, (size_t)P * P * 8, cudaMemcpyDeviceToHost));
+    for (int a = 0; a < d; ++a) {
+      std::memcpy(factors + (int64_t)a * s * p, &L[(size_t)lf.tc[a] * s * p], (size_t)s * p * 8);
+      std::memcpy(factors + (int64_t)(d + a) * s * p, &WL[(size_t)lf.sc[a] * s * p], (size_t)s * p * 8);
+    }
+    shapes[0] = 0;
+    shapes[1] = ipow(s, d);
+    shapes[2] = ipow(s, d);
+    shapes[3] = 2 * d * s * p;
+    return 0;
+  }
+  const int sL = pl->sL, P = ipow(sL, d);
+  if ((int64_t)P * P > cap) return fail(-1, "block buffer too small");
+  std::vector<double> geo(3 * 3 * sL, 0.0);   // xt, ys, ws
+  for (int a = 0; a < d; ++a)
+    for (int i = 0; i < sL; ++i) {
+      geo[a * sL + i] = pl->mx[(size_t)lf.tc[a] * sL + i];
+      geo[3 * sL + a * sL + i] = pl->mx[(size_t)lf.sc[a] * sL + i];
+      geo[6 * sL + a * sL + i] = pl->mc[(size_t)lf.sc[a] * sL + i];
+    }
+  bool self = true;
+  for (int a = 0; a < d; ++a) self = self && lf.tc[a] == lf.sc[a];
+  if (upload(tmp, geo.data(), geo.size() * 8) || dout.alloc((size_t)P * P * 8)) return 1;
+  htlr::launch_mapped_near_export(pl->kp, d, sL, tmp.d(), tmp.d() + 3 * sL, tmp.d() + 6 * sL, self ? 1 : 0, dout.d(), 0);
+  CUDA_TRY(cudaMemcpy(out, dout.ptr, (size_t)P * P * 8, cudaMemcpyDeviceToHost));
+  if (self) {
+    std::vector<double> dv((size_t)pl->N), av;
+    CUDA_TRY(cudaMemcpy(dv.data(), pl->dvec.ptr, dv.size() * 8, cudaMemcpyDeviceToHost));
+    if (pl->has_coeff) {
+      av.resize((size_t)pl->N);
+      CUDA_TRY(cudaMemcpy(av.data(), pl->coeff.ptr, av.size() * 8, cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < P; ++k) {
+      int x = k % sL, y = (k / sL) % sL, z = k / (sL * sL);
+      int64_t g = (int64_t)(lf.tc[0] * sL + x) + (int64_t)pl->n * (lf.tc[1] * sL + y);
+      if (d == 3) g += (int64_t)pl->n * pl->n * (lf.tc[2] * sL + z);
+      out[(int64_t)k * P + k] = dv[g] + (pl->has_coeff ? av[g] : pl->desc.coeff_const);
+    }
+  }
+  shapes[0] = 1;
+  shapes[1] = P;
+  shapes[2] = P;
+  shapes[3] = 0;
+  return 0;
+}
+
 int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int64_t cap, double* factors,
                       int64_t factor_cap, int32_t* shapes) {
   if (!pl || !core_or_dense || !shapes) return fail(-1, "null argument");
@@ -960,6 +1247,7 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaDeviceSynchronize());
   const auto& lf = pl->tree.leaves[leaf_id];
+  if (pl->mapped) return export_block_mapped(pl, lf, core_or_dense, cap, factors, factor_cap, shapes);
   const int d = pl->d, p = pl->p;
   const Level& lv = pl->levels[lf.level];
   const OffsetTable& tab = lf.kind == 0 ? lv.adm : pl->near;

@@ -59,6 +59,44 @@ class UniformGrid:
 
 
 @dataclass(frozen=True)
+class MappedGrid:
+    """Quasi-uniform tensor grid of BASELINE config 5 (not representable by
+    the reference's UniformGrid): per dimension x_i = phi((i + 1/2)/n) with
+    phi(t) = t + A sin(2 pi t) / (2 pi), cell i = [phi(i/n), phi((i+1)/n)],
+    Nystrom weight = product of the cell widths.  Same interface as
+    UniformGrid; A = 0 is the uniform grid."""
+
+    d: int
+    n: int
+    amplitude: float = 0.05
+
+    def __post_init__(self):
+        if self.d not in (2, 3):
+            raise ValueError("only d = 2 and d = 3 are supported")
+        if self.n < 1:
+            raise ValueError("n must be positive")
+
+    @property
+    def num_points(self) -> int:
+        return self.n ** self.d
+
+    def phi(self, t: float) -> float:
+        return t + self.amplitude * math.sin(2 * math.pi * t) / (2 * math.pi)
+
+    def coords1d(self, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
+        top = self.n if hi is None else hi
+        return np.array([self.phi((i + 0.5) / self.n) for i in range(lo, top)])
+
+    def bounds1d(self) -> np.ndarray:
+        return np.array([self.phi(i / self.n) for i in range(self.n + 1)])
+
+    def points(self, box: "IndexBox") -> np.ndarray:
+        axes = [self.coords1d(lo, hi) for lo, hi in box.ranges]
+        grids = np.meshgrid(*axes, indexing="ij")
+        return np.stack([g.ravel(order="F") for g in grids], axis=-1)
+
+
+@dataclass(frozen=True)
 class IndexBox:
     """Half-open 0-based index ranges per dimension (grids.py:53-92)."""
 
@@ -233,10 +271,12 @@ def build_cluster_tree(grid: UniformGrid, leaf_side_max: int) -> ClusterTree:
     return ClusterTree(grid=grid, root=root, leaf_side=side, depth=depth)
 
 
-def domain_of(grid: UniformGrid, box: IndexBox) -> DomainBox:
-    """grids.py:237-242."""
+def domain_of(grid, box: IndexBox) -> DomainBox:
+    """grids.py:237-242 (cell images for a MappedGrid)."""
     if any(hi > grid.n for _, hi in box.ranges):
         raise ValueError("index box exceeds the grid")
+    if isinstance(grid, MappedGrid):
+        return DomainBox(tuple((grid.phi(lo / grid.n), grid.phi(hi / grid.n)) for lo, hi in box.ranges))
     return DomainBox(tuple((lo * grid.h, hi * grid.h) for lo, hi in box.ranges))
 
 
@@ -344,12 +384,21 @@ class BlockClusterTree:
         return self._root
 
 
-def _host_plan(d: int, n: int, leaf_side_max: int, rule: AdmissibilityRule):
+def grid_kind(grid) -> tuple:
+    """(grid_kind, amplitude) of the C ABI descriptor."""
+    if isinstance(grid, MappedGrid):
+        return 1, float(grid.amplitude)
+    return 0, 0.0
+
+
+def _host_plan(d: int, n: int, leaf_side_max: int, rule: AdmissibilityRule, grid=None):
     L = _lib.lib()
+    gk, amp = grid_kind(grid)
     desc = _lib.HtlrDesc(d=d, n=n, leaf_side_max=leaf_side_max, rank=1,
                          rule=_lib.HTLR_RULE_WEAK if rule.kind == "weak" else _lib.HTLR_RULE_STRONG,
                          eta=float(rule.eta or 0.0), kernel=_lib.HTLR_KERNEL_GAUSSIAN, sigma=1.0,
-                         scale=1.0, quad_q=10, corner_subdivision=1, coeff_const=0.0)
+                         scale=1.0, quad_q=10, corner_subdivision=1, coeff_const=0.0,
+                         grid_kind=gk, amplitude=amp)
     plan = ctypes.c_void_p()
     _lib.check(L.htlr_plan_create(ctypes.byref(desc), -1, ctypes.byref(plan)))
     return plan
@@ -369,7 +418,7 @@ def build_block_cluster_tree(tree: ClusterTree, rule: AdmissibilityRule,
     """Interaction lists via the C++ builder (grids.py:268-296, bit-exact)."""
     grid = tree.grid if grid is None else grid
     L = _lib.lib()
-    plan = _host_plan(grid.d, grid.n, tree.leaf_side, rule)
+    plan = _host_plan(grid.d, grid.n, tree.leaf_side, rule, grid)
     try:
         _lib.check(L.htlr_build_lists(plan))
         arr = export_leaf_array(plan, grid.d)

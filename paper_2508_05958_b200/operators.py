@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .blocks import DenseBlock, TuckerBlock
 from .grids import (ADMISSIBLE, AdmissibilityRule, BlockClusterTree, UniformGrid,
-                    build_cluster_tree, export_leaf_array)
+                    build_cluster_tree, export_leaf_array, grid_kind)
 from .kernels import CoefficientFn, KernelSpec, QuadratureConfig, singular_rule
 
 
@@ -65,7 +65,8 @@ def _desc(cfg: BuildConfig, grid: UniformGrid) -> _lib.HtlrDesc:
         rule=_lib.HTLR_RULE_WEAK if cfg.rule.kind == "weak" else _lib.HTLR_RULE_STRONG,
         eta=float(cfg.rule.eta or 0.0), kernel=k.device_code, sigma=float(k.sigma or 0.0),
         scale=float(k.scale), quad_q=int(cfg.quadrature.q),
-        corner_subdivision=singular_rule(k, cfg.quadrature), coeff_const=float(coeff))
+        corner_subdivision=singular_rule(k, cfg.quadrature), coeff_const=float(coeff),
+        grid_kind=grid_kind(grid)[0], amplitude=grid_kind(grid)[1])
 
 
 class _Payloads:
@@ -153,6 +154,8 @@ class HTLRMatrix:
         core = buf[: p ** (2 * d)].reshape((p,) * (2 * d), order="F").copy()
         if nfac == 0:
             return TuckerBlock(core=core, u_factors=[None] * d, v_factors=[None] * d)
+        # (mapped grids export raw factors: target Lagrange factor, source
+        # cell-width-weighted factor; square factors included)
         s = nfac // (2 * d * p)
         mats = [fac[i * s * p:(i + 1) * s * p].reshape(s, p).copy() for i in range(2 * d)]
         return TuckerBlock(core=core, u_factors=mats[:d], v_factors=mats[d:])
@@ -160,7 +163,7 @@ class HTLRMatrix:
     def last_launch_count(self) -> int:
         return int(_lib.lib().htlr_last_launch_count(self._plan))
 
-    PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward")
+    PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward", "regen_level", "regen_near")
 
     def profile(self, on: bool = True) -> None:
         """Bracket every kernel launch of later matvecs with CUDA events."""
@@ -198,6 +201,8 @@ def construct(cfg: BuildConfig, grid: UniformGrid, threads: int = 1,
     import torch
     if cfg.kernel.kind not in ("gaussian", "slp2d", "slp3d"):
         cfg.kernel.device_code  # raises ValueError with the explanation
+    if grid_kind(grid)[0] == 1 and not cfg.kernel.translation_invariant:
+        raise ValueError("mapped grids need a translation-invariant kernel formula")
     if device is None:
         device = torch.cuda.current_device() if torch.cuda.is_available() else 0
     op = HTLRMatrix(grid, cfg, int(device))
