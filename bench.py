@@ -44,7 +44,7 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="budget of the cpu_baseline sample (rank 0, N=1)")
@@ -125,7 +125,11 @@ def oracle_problem(name):
         "cfg2": O.Kernel("slp3d", scale=4 * math.pi),
         "cfg3": O.Kernel("slp3d", scale=4 * math.pi),
         "cfg4": O.Kernel("gaussian", sigma=0.1 / math.sqrt(2.0)),
+        "cfg5": O.Kernel("slp3d", scale=4 * math.pi),
     }[name]
+    if w.amplitude >= 0:
+        return w, O.MappedProblem(d=w.d, geo=O.MappedGeometry(w.n, w.amplitude), rank=w.rank,
+                                  leaf_side_max=w.leaf, kernel=kern, coeff=O.constant_coeff(w.a))
     return w, O.Problem(d=w.d, n=w.n, rank=w.rank, leaf_side_max=w.leaf, kernel=kern,
                         coeff=O.constant_coeff(w.a))
 
@@ -161,7 +165,8 @@ class CpuSample:
         groups = leaf_groups(name)
         rng = np.random.default_rng(seed)
         d = self.w.d
-        diag = self.pb.diag()
+        mapped = isinstance(self.pb, O.MappedProblem)
+        diag = None if mapped else self.pb.diag()
         self.items = []      # (group, leaf, payload)
         self.counts = {}
         for key, rows in groups.items():
@@ -172,7 +177,13 @@ class CpuSample:
                 lf = O.Leaf(int(r[0]), int(r[1]), int(r[2]),
                             tuple((int(r[3 + 2 * a]), int(r[4 + 2 * a])) for a in range(d)),
                             tuple((int(r[3 + 2 * d + 2 * a]), int(r[4 + 2 * d + 2 * a])) for a in range(d)))
-                self.items.append((key, lf, O.build_payload(self.pb, lf, diag)))
+                if mapped:
+                    pl = (O.mapped_tucker_block(self.pb.kernel, self.pb.geo, lf.tau, lf.sigma, self.pb.rank)
+                          if lf.kind == O.ADM else
+                          O.mapped_dense_block(self.pb.kernel, self.pb.coeff, self.pb.geo, lf.tau, lf.sigma))
+                else:
+                    pl = O.build_payload(self.pb, lf, diag)
+                self.items.append((key, lf, pl))
         u = self.w.input()
         self.R = 1 if u.ndim == 1 else u.shape[1]
         shape = (self.w.n,) * d

@@ -29,6 +29,34 @@ __device__ __forceinline__ double kernel_from_r2(const KernelParams& kp, double 
   return kp.scale == 1.0 ? v : kp.scale * v;
 }
 
+// Regeneration fast path (mapped grid): k(r^2) = kernel_coef * kernel_shape(r^2),
+// division-free (rsqrt / log / exp with the constant hoisted and folded into
+// the operand vector).  Each differs from the reference formula by <= a few
+// ulp, far below the 1e-12 parity bar.
+__host__ __device__ __forceinline__ double kernel_coef(const KernelParams& kp) {
+  if (kp.kind == 0) return kp.scale;
+  if (kp.kind == 1) return kp.scale * (-0.5 / (2.0 * 3.141592653589793));
+  return kp.scale / (4.0 * 3.141592653589793);
+}
+
+// 1/sqrt(x) for normal positive x (squared distances of distinct points):
+// MUFU.RSQ64H seed + two Newton steps, no special-case slow path.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y * y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x, y * y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
+template <int KIND>
+__device__ __forceinline__ double kernel_shape(double r2, double neg_inv_denom) {
+  if (KIND == 0) return exp(r2 * neg_inv_denom);
+  if (KIND == 1) return log(r2);
+  return rsqrt_pos(r2);
+}
+
 __device__ __forceinline__ double r2_of(int d, const double* x, const double* y) {
   double d0 = __dadd_rn(x[0], -y[0]);
   double r2 = __dmul_rn(d0, d0);

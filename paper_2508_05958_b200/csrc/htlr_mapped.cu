@@ -124,11 +124,12 @@ __global__ void mapped_diag_kernel(KernelParams kp, int d, int n, int q, const d
 // ((dx^2 + dy^2) + dz^2).  PP = p as a compile-time constant keeps the
 // innermost x-differences in registers (0: generic, slower).
 // ---------------------------------------------------------------------------
-template <int RB, int PP>
+template <int RB, int PP, int KIND>
 __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, const double* __restrict__ nodes,
                                  const int64_t* __restrict__ rowptr, const int* __restrict__ cols, int64_t t0,
                                  const double* __restrict__ W, int K_pad, double* __restrict__ H, int R, int r0) {
   extern __shared__ double sm[];
+  const double nid = -1.0 / kp.denom;
   const int p = PP ? PP : p_rt;
   const int P = (d == 2) ? p * p : p * p * p;
   double* sW = sm;                       // RB x P
@@ -155,9 +156,10 @@ __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, co
     morton_decode(sigma, d, level, sc);
     __syncthreads();
     for (int i = threadIdx.x; i < d * p; i += blockDim.x) sEta[(i / p) * kMaxRank + i % p] = nodes[sc[i / p] * p + i % p];
+    const double coef = kernel_coef(kp);
     for (int i = threadIdx.x; i < nrb * P; i += blockDim.x) {
       const int q = i / P, s = i % P;
-      sW[i] = W[((int64_t)sigma * R + r0 + q) * K_pad + s];
+      sW[i] = coef * W[((int64_t)sigma * R + r0 + q) * K_pad + s];
     }
     __syncthreads();
     if (!act) continue;
@@ -181,14 +183,12 @@ __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, co
     for (int s3 = 0; s3 < n3; ++s3) {
       const double z2 = (d == 3) ? myYZ[p + s3] : 0.0;
       for (int s2 = 0; s2 < p; ++s2) {
-        const double y2 = myYZ[s2];
+        const double yz = myYZ[s2] + z2;
         const double* w = sW + (s2 + p * s3) * p;
 #pragma unroll
         for (int s1 = 0; s1 < (PP ? PP : kMaxRank); ++s1) {
           if (s1 < p) {
-            double r2 = __dadd_rn(dx2[s1], y2);
-            if (d == 3) r2 = __dadd_rn(r2, z2);
-            const double kv = kernel_from_r2(kp, r2);
+            const double kv = kernel_shape<KIND>(dx2[s1] + yz, nid);
 #pragma unroll
             for (int q = 0; q < RB; ++q)
               if (q < nrb) acc[q] += kv * w[q * P + s1];
@@ -206,12 +206,13 @@ __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, co
 // the coincident pair skipped (its value is the per-point cell integral,
 // added by the downward kernel); thread = target point i.
 // ---------------------------------------------------------------------------
-template <int RB, int SS>
+template <int RB, int SS, int KIND>
 __global__ void regen_near_kernel(KernelParams kp, int d, int sL_rt, int L, const double* __restrict__ coords,
                                   const double* __restrict__ widths, const int64_t* __restrict__ rowptr,
                                   const int* __restrict__ cols, int64_t t0, const double* __restrict__ ub, int K_pad,
                                   double* __restrict__ Y, int R, int r0) {
   extern __shared__ double sm[];
+  const double nid = -1.0 / kp.denom;
   const int sL = SS ? SS : sL_rt;
   const int P = (d == 2) ? sL * sL : sL * sL * sL;
   double* sV = sm;                   // RB x P   (w_j u_j)
@@ -243,7 +244,7 @@ __global__ void regen_near_kernel(KernelParams kp, int d, int sL_rt, int L, cons
       const int j1 = j % sL, j2 = (j / sL) % sL, j3 = j / (sL * sL);
       double w = widths[sc[0] * sL + j1] * widths[sc[1] * sL + j2];
       if (d == 3) w = w * widths[sc[2] * sL + j3];
-      sV[k] = w * ub[((int64_t)sigma * R + r0 + q) * K_pad + j];
+      sV[k] = kernel_coef(kp) * (w * ub[((int64_t)sigma * R + r0 + q) * K_pad + j]);
     }
     __syncthreads();
     if (!act) continue;
@@ -268,16 +269,14 @@ __global__ void regen_near_kernel(KernelParams kp, int d, int sL_rt, int L, cons
     for (int j3 = 0; j3 < n3; ++j3) {
       const double z2 = (d == 3) ? myYZ[sL + j3] : 0.0;
       for (int j2 = 0; j2 < sL; ++j2) {
-        const double y2 = myYZ[j2];
+        const double yz = myYZ[j2] + z2;
         const int jb = (j2 + sL * j3) * sL;
         const double* v = sV + jb;
 #pragma unroll
         for (int j1 = 0; j1 < (SS ? SS : 16); ++j1) {
           if (j1 < sL) {
             if (self && jb + j1 == i) continue;
-            double r2 = __dadd_rn(dx2[j1], y2);
-            if (d == 3) r2 = __dadd_rn(r2, z2);
-            const double kv = kernel_from_r2(kp, r2);
+            const double kv = kernel_shape<KIND>(dx2[j1] + yz, nid);
 #pragma unroll
             for (int q = 0; q < RB; ++q)
               if (q < nrb) acc[q] += kv * v[q * P + j1];
@@ -350,16 +349,28 @@ void launch_mapped_diag(const KernelParams& kp, int d, int n, int q, const doubl
 
 static int regen_threads(int P) { return ((P + 31) / 32) * 32; }
 
-template <int RB, int PP>
-static void adm_t(const KernelParams& kp, int d, int p, int level, const double* nodes, const int64_t* rowptr,
+template <int RB, int PP, int KIND>
+static void adm_k(const KernelParams& kp, int d, int p, int level, const double* nodes, const int64_t* rowptr,
                   const int* cols, int64_t t0, int64_t nt, const double* W, int K_pad, double* H, int R, int r0,
                   cudaStream_t st) {
   const int P = (d == 2) ? p * p : p * p * p;
   const int thr = regen_threads(P);
   size_t smem = sizeof(double) * ((size_t)RB * P + 3 * kMaxRank + (size_t)thr * 2 * p);
-  cudaFuncSetAttribute(regen_adm_kernel<RB, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  regen_adm_kernel<RB, PP><<<(unsigned)nt, thr, smem, st>>>(kp, d, p, level, nodes, rowptr, cols, t0, W, K_pad, H, R,
-                                                           r0);
+  cudaFuncSetAttribute(regen_adm_kernel<RB, PP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  regen_adm_kernel<RB, PP, KIND><<<(unsigned)nt, thr, smem, st>>>(kp, d, p, level, nodes, rowptr, cols, t0, W, K_pad,
+                                                                 H, R, r0);
+}
+
+template <int RB, int PP>
+static void adm_t(const KernelParams& kp, int d, int p, int level, const double* nodes, const int64_t* rowptr,
+                  const int* cols, int64_t t0, int64_t nt, const double* W, int K_pad, double* H, int R, int r0,
+                  cudaStream_t st) {
+  if (kp.kind == 0)
+    adm_k<RB, PP, 0>(kp, d, p, level, nodes, rowptr, cols, t0, nt, W, K_pad, H, R, r0, st);
+  else if (kp.kind == 1)
+    adm_k<RB, PP, 1>(kp, d, p, level, nodes, rowptr, cols, t0, nt, W, K_pad, H, R, r0, st);
+  else
+    adm_k<RB, PP, 2>(kp, d, p, level, nodes, rowptr, cols, t0, nt, W, K_pad, H, R, r0, st);
 }
 
 template <int RB>
@@ -393,16 +404,28 @@ void launch_regen_adm(const KernelParams& kp, int d, int p, int level, const dou
   }
 }
 
-template <int RB, int SS>
-static void near_t(const KernelParams& kp, int d, int sL, int L, const double* coords, const double* widths,
+template <int RB, int SS, int KIND>
+static void near_k(const KernelParams& kp, int d, int sL, int L, const double* coords, const double* widths,
                    const int64_t* rowptr, const int* cols, int64_t t0, int64_t nt, const double* ub, int K_pad,
                    double* Y, int R, int r0, cudaStream_t st) {
   const int P = (d == 2) ? sL * sL : sL * sL * sL;
   const int thr = regen_threads(P);
   size_t smem = sizeof(double) * ((size_t)RB * P + 3 * 16 + (size_t)thr * 2 * sL);
-  cudaFuncSetAttribute(regen_near_kernel<RB, SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  regen_near_kernel<RB, SS><<<(unsigned)nt, thr, smem, st>>>(kp, d, sL, L, coords, widths, rowptr, cols, t0, ub,
-                                                            K_pad, Y, R, r0);
+  cudaFuncSetAttribute(regen_near_kernel<RB, SS, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  regen_near_kernel<RB, SS, KIND><<<(unsigned)nt, thr, smem, st>>>(kp, d, sL, L, coords, widths, rowptr, cols, t0,
+                                                                  ub, K_pad, Y, R, r0);
+}
+
+template <int RB, int SS>
+static void near_t(const KernelParams& kp, int d, int sL, int L, const double* coords, const double* widths,
+                   const int64_t* rowptr, const int* cols, int64_t t0, int64_t nt, const double* ub, int K_pad,
+                   double* Y, int R, int r0, cudaStream_t st) {
+  if (kp.kind == 0)
+    near_k<RB, SS, 0>(kp, d, sL, L, coords, widths, rowptr, cols, t0, nt, ub, K_pad, Y, R, r0, st);
+  else if (kp.kind == 1)
+    near_k<RB, SS, 1>(kp, d, sL, L, coords, widths, rowptr, cols, t0, nt, ub, K_pad, Y, R, r0, st);
+  else
+    near_k<RB, SS, 2>(kp, d, sL, L, coords, widths, rowptr, cols, t0, nt, ub, K_pad, Y, R, r0, st);
 }
 
 template <int RB>
