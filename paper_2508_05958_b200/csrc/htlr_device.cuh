@@ -40,14 +40,14 @@ __host__ __device__ __forceinline__ double kernel_coef(const KernelParams& kp) {
 }
 
 // 1/sqrt(x) for normal positive x (squared distances of distinct points):
-// MUFU.RSQ64H seed + two Newton steps, no special-case slow path.
+// MUFU.RSQ64H seed (measured max rel. error 9.1e-7, tools/rsqrt_probe.cu) and
+// one third-order correction y (1 + e/2 + 3e^2/8), e = 1 - x y^2 (measured
+// 1.1e-16, same as libdevice rsqrt) -- 5 fp64 ops, no slow path.
 __device__ __forceinline__ double rsqrt_pos(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y * y, 1.0);
-  y = fma(0.5 * y, e, y);
-  e = fma(-x, y * y, 1.0);
-  return fma(0.5 * y, e, y);
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 template <int KIND>
