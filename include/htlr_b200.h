@@ -166,6 +166,13 @@ int htlr_storage(const htlr_plan* plan, int64_t out[5]);
 int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,
                       int32_t corner_subdivision, int device, double* out);
 
+/* Exact rows of the Nystrom system (exact_row_evaluator, oracles.py:65-100):
+ * out[r] = sum_{j != i} k(x_i, x_j) w_j u_j + (diag_i + a_i) u_i for
+ * i = rows[r]; rows, u, out are device pointers (u of N doubles, F-order).
+ * Needs only htlr_plan_create (+ htlr_set_coeff).  Synchronises. */
+int htlr_exact_rows(htlr_plan* plan, const int64_t* rows, int64_t nrows, const double* u, double* out,
+                    void* stream);
+
 /* Per-launch profiling of htlr_matvec: when enabled, every kernel launch of
  * a matvec is bracketed by CUDA events on the launching stream.
  * htlr_profile_read returns, for the last matvec, one entry per launch:

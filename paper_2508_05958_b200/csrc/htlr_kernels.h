@@ -119,4 +119,10 @@ void launch_mapped_core_export(const KernelParams& kp, int d, int p, const doubl
 void launch_mapped_near_export(const KernelParams& kp, int d, int sL, const double* xt, const double* ys,
                                const double* ws, int self, double* out, cudaStream_t st);
 
+// exact rows (htlr_rows.cu)
+void launch_exact_rows(const KernelParams& kp, int d, int n, double h, double hd, const double* coords,
+                       const double* widths, const int64_t* rows, int64_t nrows, const double* cell_avg,
+                       const double* dvec_all, double* diag_rows, const double* avec, double aconst,
+                       const double* u, double* out, cudaStream_t st);
+
 }  // namespace htlr

@@ -1158,6 +1158,46 @@ int htlr_profile_read(htlr_plan* pl, int32_t* kinds, int32_t* levels, double* ms
   return 0;
 }
 
+int htlr_exact_rows(htlr_plan* pl, const int64_t* rows, int64_t nrows, const double* u, double* out,
+                    void* stream) {
+  if (!pl || !rows || !u || !out) return fail(-1, "null argument");
+  if (pl->device < 0) return fail(-1, "host-only plan: no device work");
+  if (nrows < 0) return fail(-1, "negative row count");
+  CUDA_TRY(cudaSetDevice(pl->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = pl->d, n = pl->n;
+  std::vector<double> gx, gw;
+  gauss01(pl->desc.quad_q, gx, gw);
+  gx.insert(gx.end(), gw.begin(), gw.end());
+  DevBuf gl, cavg, drows;
+  if (upload(gl, gx.data(), gx.size() * sizeof(double))) return 1;
+  if (cavg.alloc(sizeof(double)) || drows.alloc(std::max<int64_t>(nrows, 1) * sizeof(double))) return 1;
+  const double* dv = nullptr;
+  if (pl->mapped) {
+    if (!pl->dvec.ptr) {   // per-point cell integrals (also built by construct)
+      if (upload(pl->d_mb, pl->mb.data(), pl->mb.size() * sizeof(double))) return 1;
+      if (upload(pl->d_mx, pl->mx.data(), pl->mx.size() * sizeof(double))) return 1;
+      if (upload(pl->d_mc, pl->mc.data(), pl->mc.size() * sizeof(double))) return 1;
+      if (pl->dvec.alloc(pl->N * sizeof(double))) return 1;
+      htlr::launch_mapped_diag(pl->kp, d, n, pl->desc.quad_q, gl.d(), gl.d() + pl->desc.quad_q, pl->d_mb.d(),
+                               pl->d_mx.d(), pl->dvec.d(), pl->N, st);
+    }
+    dv = pl->dvec.d();
+  } else {
+    htlr::launch_diag(pl->kp, d, pl->h, pl->desc.quad_q, gl.d(), gl.d() + pl->desc.quad_q,
+                      pl->desc.corner_subdivision ? 1 : 0, cavg.d(), st);
+  }
+  htlr::launch_exact_rows(pl->kp, d, n, pl->h, pl->hd, pl->mapped ? pl->d_mx.d() : nullptr,
+                          pl->mapped ? pl->d_mc.d() : nullptr, rows, nrows, cavg.d(), dv, drows.d(),
+                          pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, u, out, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  gl.release();
+  cavg.release();
+  drows.release();
+  return 0;
+}
+
 int64_t htlr_last_launch_count(const htlr_plan* pl) { return pl ? pl->last_launches : -1; }
 
 int htlr_diag_value(htlr_plan* pl, double* out) {

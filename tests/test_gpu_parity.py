@@ -268,3 +268,40 @@ def test_rank_above_box_side_raises_like_reference():
                         kernel=H.slp_3d(), coeff=H.CoefficientFn.constant(0.0))
     with pytest.raises(ValueError, match="qr requires rows >= cols"):
         H.construct(cfg, H.UniformGrid(3, 16))
+
+
+# ------------------------------------------------------------------ exact rows / sampled error (8(f) f2)
+
+
+def test_exact_rows_match_dense_reference_operator():
+    """Device exact rows == rows of the reference-built dense operator (small
+    grid, oracle dense blocks are the reference's build_dense restated)."""
+    grid = H.UniformGrid(2, 16)
+    k, a = H.slp_2d(), 0.5
+    ev = H.exact_row_evaluator(k, H.CoefficientFn.constant(a), grid, H.QuadratureConfig())
+    pb = O.Problem(d=2, n=16, rank=4, leaf_side_max=16, kernel=O.Kernel("slp2d"), coeff=O.constant_coeff(a))
+    full = ((0, 16), (0, 16))
+    D = O.dense_block(pb.kernel, pb.coeff, 16, full, full, pb.diag())
+    u = np.random.default_rng(8).standard_normal(256)
+    rows = np.array([0, 17, 100, 255])
+    assert rel(ev(rows, u), (D @ u)[rows]) <= 1e-13
+
+
+def test_exact_rows_mapped_match_oracle_dense():
+    grid = H.MappedGrid(2, 16, 0.05)
+    ev = H.exact_row_evaluator(H.slp_2d(), H.CoefficientFn.constant(0.0), grid, H.QuadratureConfig())
+    pb = O.MappedProblem(d=2, geo=O.MappedGeometry(16, 0.05), rank=4, leaf_side_max=16, kernel=O.Kernel("slp2d"),
+                         coeff=O.constant_coeff(0.0))
+    D = O.mapped_dense_matrix(pb)
+    u = np.random.default_rng(9).standard_normal(256)
+    rows = np.array([3, 77, 200])
+    assert rel(ev(rows, u), (D @ u)[rows]) <= 1e-12
+
+
+def test_estimate_rel_error_cfg4_scale():
+    """Accuracy (not parity) of config 4 at full scale: 1000 exact rows."""
+    w, op = build("cfg4")
+    cfg = w.build_config()
+    ev = H.exact_row_evaluator(cfg.kernel, cfg.coeff, w.grid, cfg.quadrature)
+    err = H.estimate_rel_error_random(op, ev, w.input(), sample_size=1000, seed=1)
+    assert err < 1e-6
