@@ -159,6 +159,18 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     const int n_tiles = max(0, min(4, (it.ncols - wn * 32 + 7) >> 3));
     const int row0 = it.rt * MT + wm * 32;
     const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
+    // epilogue targets of this thread's 8 columns, fetched now so the pair
+    // loads' latency hides under the K loop
+    int64_t cbase[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int n = wn * 32 + (q >> 1) * 8 + 2 * t + (q & 1);
+      cbase[q] = -1;
+      if (n < it.ncols) {
+        const int j = n / Rc, r = it.r0 + n % Rc;
+        cbase[q] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
+      }
+    }
     double acc[2][4][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -208,11 +220,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     for (int ni = 0; ni < 4; ++ni) {
 #pragma unroll
       for (int cix = 0; cix < 2; ++cix) {
-        const int n = wn * 32 + ni * 8 + 2 * t + cix;
-        if (n >= it.ncols) continue;
-        const int j = n / Rc, r = it.r0 + n % Rc;
-        const int2 pr = pairs[it.pair_begin + j];
-        double* cc = C + ((int64_t)pr.x * R + r) * ldc;
+        const int64_t cb = cbase[ni * 2 + cix];
+        if (cb < 0) continue;
+        double* cc = C + cb;
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
 #pragma unroll
@@ -301,6 +311,16 @@ __global__ void __launch_bounds__(9 * 32, 1)
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const ItemInfo it = item_info(tasks, item, 1, R, Rc, NT);
     const bool active = n0 < it.ncols;
+    int64_t cbase[2];
+#pragma unroll
+    for (int cix = 0; cix < 2; ++cix) {
+      const int n = n0 + 2 * t + cix;
+      cbase[cix] = -1;
+      if (n < it.ncols) {
+        const int j = n / Rc, r = it.r0 + n % Rc;
+        cbase[cix] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
+      }
+    }
     double acc[M8][2];
 #pragma unroll
     for (int i = 0; i < M8; ++i) acc[i][0] = acc[i][1] = 0.0;
@@ -324,11 +344,8 @@ __global__ void __launch_bounds__(9 * 32, 1)
     if (!active) continue;
 #pragma unroll
     for (int cix = 0; cix < 2; ++cix) {
-      const int n = n0 + 2 * t + cix;
-      if (n >= it.ncols) continue;
-      const int j = n / Rc, r = it.r0 + n % Rc;
-      const int2 pr = pairs[it.pair_begin + j];
-      double* cc = C + ((int64_t)pr.x * R + r) * ldc;
+      if (cbase[cix] < 0) continue;
+      double* cc = C + cbase[cix];
 #pragma unroll
       for (int i = 0; i < M8; ++i) {
         const int m = i * 8 + g8;
