@@ -88,13 +88,16 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
 
 }  // namespace
 
-template <int WM, int WN, int STAGES>
+template <int WM, int WN, int STAGES, int KCS>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                            double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
                            const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
                            int RT) {
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC, BST = KC + 4;
+  // a pipeline stage covers KCS = 32 or 64 of K (one or two tiled 32-chunks,
+  // adjacent in the A layout); fewer, larger stages halve the mbarrier
+  // round trips per unit of tensor work
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = KCS, BST = KC + 4;
   constexpr int NCW = WM * WN;   // consumer warps
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;                                  // STAGES x MT*KC
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
           double a[2][4];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
-            const double2* pa =
-                reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
+            const double2* pa = reinterpret_cast<const double2*>(
+                cA + (ks >> 2) * (MT * kKC) + ((wm * 2 + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
             const double2 v0 = pa[0], v1 = pa[1];
             a[mi][0] = v0.x;
             a[mi][1] = v0.y;
@@ -394,13 +397,13 @@ bool gemm_use_persistent() {
   return mode == 1;
 }
 
-template <int WM, int WN, int STAGES>
+template <int WM, int WN, int STAGES, int KCS>
 static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
                                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                                 int M_valid, int ldc, int RT, cudaStream_t st) {
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC;
+  constexpr int MT = 32 * WM, NT = 32 * WN, KC = KCS;
   const size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES, KCS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const int nitems = ntasks * RT;
   if (nitems == 0) return;
@@ -408,17 +411,25 @@ static void launch_persistent_t(const double* A, int64_t mat_stride, const doubl
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = nitems < sms ? nitems : sms;
-  gemm_persistent_kernel<WM, WN, STAGES><<<grid, (WM * WN + 1) * 32, smem, st>>>(
+  gemm_persistent_kernel<WM, WN, STAGES, KCS><<<grid, (WM * WN + 1) * 32, smem, st>>>(
       A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid, ldc, RT);
 }
 
 void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st) {
+  static int kcs = -1;
+  if (kcs < 0) {
+    const char* e = std::getenv("HTLR_GEMM_KCS");
+    kcs = (e && std::strcmp(e, "32") == 0) ? 32 : 64;
+  }
   if (MT == 64)
-    launch_persistent_t<2, 2, 6>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+    launch_persistent_t<2, 2, 6, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+  else if (kcs == 64 && K_pad % 64 == 0)
+    launch_persistent_t<4, 2, 2, 64>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
   else
-    launch_persistent_t<4, 2, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+    launch_persistent_t<4, 2, 4, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
+                                     st);
 }
 
 }  // namespace htlr
