@@ -70,6 +70,13 @@ __device__ __forceinline__ void mma16x8x8(double (&c)[4], const double (&a)[4], 
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
+// one mma.m8n8k4: (c0, c1) += a (8x4 row) . b (4x8 col)
+__device__ __forceinline__ void mma8x8x4_pair(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 struct ItemInfo {
   int mat, pair_begin, pair_count, r0, rt, ncols;
 };
@@ -186,7 +193,42 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       mbar_wait(&full[s], (g / STAGES) & 1);
       const double* cA = sA + s * MT * KC;
       const double* cB = sB + s * NT * BST;
-      if (n_tiles > 0 && m_tiles > 0) {
+      if (n_tiles == 4 && m_tiles == 2) {
+        // full tile: explicit m8n8k4 issue order -- the k0..3 products of all
+        // 16 (m8, n8) accumulators first, then the k4..7 products, so every
+        // dependent DMMA pair is 16 instructions apart (mma.m16n8k8 would
+        // emit each dependent pair back to back)
+#pragma unroll
+        for (int ks = 0; ks < KC / 8; ++ks) {
+          double a[2][4];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const double2* pa = reinterpret_cast<const double2*>(
+                cA + (ks >> 2) * (MT * kKC) + ((wm * 2 + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
+            const double2 v0 = pa[0], v1 = pa[1];
+            a[mi][0] = v0.x;
+            a[mi][1] = v0.y;
+            a[mi][2] = v1.x;
+            a[mi][3] = v1.y;
+          }
+          double b[4][2];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            const double* pb = cB + (wn * 32 + ni * 8 + g8) * BST + ks * 8 + t;
+            b[ni][0] = pb[0];
+            b[ni][1] = pb[4];
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni) {
+                mma8x8x4_pair(acc[mi][ni][0], acc[mi][ni][1], a[mi][2 * h], b[ni][h]);
+                mma8x8x4_pair(acc[mi][ni][2], acc[mi][ni][3], a[mi][2 * h + 1], b[ni][h]);
+              }
+        }
+      } else if (n_tiles > 0 && m_tiles > 0) {
 #pragma unroll
         for (int ks = 0; ks < KC / 8; ++ks) {
           double a[2][4];
