@@ -166,6 +166,10 @@ int htlr_storage(const htlr_plan* plan, int64_t out[5]);
 int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,
                       int32_t corner_subdivision, int device, double* out);
 
+/* CUDA-graph replay of htlr_matvec (default on): the first call with a given
+ * (nrhs, u, f) captures the launch sequence, later calls replay it. */
+int htlr_set_graphs(htlr_plan* plan, int32_t on);
+
 /* Exact rows of the Nystrom system (exact_row_evaluator, oracles.py:65-100):
  * out[r] = sum_{j != i} k(x_i, x_j) w_j u_j + (diag_i + a_i) u_i for
  * i = rows[r]; rows, u, out are device pointers (u of N doubles, F-order).

@@ -153,6 +153,20 @@ struct htlr_plan {
   int ext_R = 0;
   std::vector<double*> ext_ptrs;
   bool profiling = false;
+  // CUDA-graph replay of the whole matvec, keyed by (R, u, f, profiling)
+  bool graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  struct GraphEntry {
+    int R;
+    const double* u;
+    double* f;
+    bool prof;
+    cudaGraphExec_t exec;
+    std::vector<int32_t> kind, level;
+    std::vector<double> flops, bytes;
+    int64_t launches;
+  };
+  std::vector<GraphEntry> graph_cache;
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
   std::vector<int32_t> prof_level;
@@ -277,6 +291,8 @@ int htlr_plan_destroy(htlr_plan* pl) {
   }
   cudaSetDevice(pl->device);
   for (auto e : pl->prof_ev) cudaEventDestroy(e);
+  for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
+  if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   for (auto& lv : pl->levels) {
     lv.Q.release();
     lv.R.release();
@@ -546,8 +562,11 @@ int htlr_exchange_info(const htlr_plan* pl, int64_t nrhs, int64_t* count, int64_
   return 0;
 }
 
+static void drop_graphs(htlr_plan* pl);
+
 int htlr_bind_exchange(htlr_plan* pl, int64_t nrhs, void* const* ptrs, int64_t count) {
   if (!pl) return fail(-1, "null plan");
+  drop_graphs(pl);
   if (!pl->lists_built) return fail(-1, "lists not built");
   std::vector<int64_t> b;
   exchange_sizes(pl, (int)nrhs, b);
@@ -812,8 +831,11 @@ int htlr_construct(htlr_plan* pl, void* stream) {
   return 0;
 }
 
+static void drop_graphs(htlr_plan* pl);
+
 static int ensure_workspace(htlr_plan* pl, int R) {
   if (pl->ws_R >= R) return 0;
+  drop_graphs(pl);   // captured graphs hold the old workspace addresses
   const int d = pl->d, p = pl->p;
   const int P = ipow(p, d);
   if (pl->mapped) {
@@ -1070,15 +1092,69 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
 
 }  // namespace
 
+static void drop_graphs(htlr_plan* pl) {
+  for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
+  pl->graph_cache.clear();
+}
+
 int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
   MvCtx cx;
   if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
   if (!u || !f) return fail(-1, "null vector");
   if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
+  if (pl->graphs) {
+    // replay a captured graph of the whole launch sequence (one CPU call
+    // instead of ~10 launches + memsets; matters for the small configs)
+    for (auto& g : pl->graph_cache) {
+      if (g.R == cx.R && g.u == u && g.f == f && g.prof == pl->profiling) {
+        pl->prof_kind = g.kind;
+        pl->prof_level = g.level;
+        pl->prof_flops = g.flops;
+        pl->prof_bytes = g.bytes;
+        CUDA_TRY(cudaGraphLaunch(g.exec, cx.st));
+        pl->last_launches = g.launches;
+        return 0;
+      }
+    }
+    if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+    MvCtx cc = cx;
+    cc.st = pl->cap_stream;
+    prof_reset(pl);
+    CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
+    int rc = mv_local(cc, u);
+    if (!rc) rc = mv_remote(cc, u, f);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (!rc && ce == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+      cudaGraphDestroy(graph);
+      if (pl->graph_cache.size() >= 8) drop_graphs(pl);
+      pl->graph_cache.push_back({cx.R, u, f, pl->profiling, exec, pl->prof_kind, pl->prof_level, pl->prof_flops,
+                                 pl->prof_bytes, cc.launches});
+      CUDA_TRY(cudaGraphLaunch(exec, cx.st));
+      pl->last_launches = cc.launches;
+      return 0;
+    }
+    // capture not possible here: fall back to direct launches from now on
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    pl->graphs = false;
+    if (rc > 0) return rc;
+  }
   prof_reset(pl);
   if (int rc = mv_local(cx, u)) return rc;
   if (int rc = mv_remote(cx, u, f)) return rc;
   pl->last_launches = cx.launches;
+  return 0;
+}
+
+int htlr_set_graphs(htlr_plan* pl, int32_t on) {
+  if (!pl) return fail(-1, "null plan");
+  pl->graphs = on != 0;
+  if (!pl->graphs && pl->device >= 0) {
+    cudaSetDevice(pl->device);
+    drop_graphs(pl);
+  }
   return 0;
 }
 

@@ -253,6 +253,13 @@ def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int]):
                                           ctypes.c_void_p(fd.data_ptr()), R, ctypes.c_void_p(stream)))
     out = fd.reshape(-1) if nrhs_expected == 1 else fd
     if host:
+        if is_torch and x.is_pinned():
+            # pinned in -> pinned out (torch's caching host allocator), one
+            # async D2H copy on the same stream
+            res = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            res.copy_(out, non_blocking=True)
+            torch.cuda.current_stream(op.device).synchronize()
+            return res
         res = out.cpu()
         return res.numpy() if not is_torch else res
     return out
