@@ -888,7 +888,7 @@ struct MvCtx {
       CUDA_TRY(cudaEventCreate(&e));
       pl->prof_ev.push_back(e);
     }
-    CUDA_TRY(cudaEventRecord(pl->prof_ev[ev_used], st));
+    CUDA_TRY(cudaEventRecordWithFlags(pl->prof_ev[ev_used], st, cudaEventRecordExternal));
     pl->prof_kind.push_back(kind);
     pl->prof_level.push_back(level);
     pl->prof_flops.push_back(flops);
@@ -898,7 +898,7 @@ struct MvCtx {
   int prof_end() {
     ++launches;
     if (!pl->profiling) return 0;
-    CUDA_TRY(cudaEventRecord(pl->prof_ev[ev_used + 1], st));
+    CUDA_TRY(cudaEventRecordWithFlags(pl->prof_ev[ev_used + 1], st, cudaEventRecordExternal));
     ev_used += 2;
     return 0;
   }
