@@ -1,0 +1,91 @@
+"""Edge cases of the B200 path against the oracle (relative 2-norm <= 1e-12):
+every GEMM layout/tile variant, right-hand-side chunking, square leaves
+merged into the leaf pass, deep weak trees, per-point coefficients."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2508_05958_b200 as H
+from oracle import htlr_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel(a, b):
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def make(d, n, leaf, p, rule, eta, kd, a=0.0):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        r = H.AdmissibilityRule.weak() if rule == "weak" else H.AdmissibilityRule.strong(eta)
+        cfg = H.BuildConfig(rank=p, leaf_side=leaf, rule=r, kernel=kd, coeff=H.CoefficientFn.constant(a))
+    return H.construct(cfg, H.UniformGrid(d, n))
+
+
+def test_many_rhs_chunked_columns():
+    """R = 70 > 64 columns per item: RHS split across items."""
+    op = make(3, 16, 4, 4, "strong", 1.0, H.slp_3d())
+    U = np.random.default_rng(1).standard_normal((16 ** 3, 70))
+    F = H.matmat(op, U)
+    for r in (0, 33, 64, 69):
+        assert rel(F[:, r], H.matvec(op, U[:, r])) <= 1e-14
+
+
+def test_rank5_square_leaf_thin_layout():
+    """p = 5, leaf side 5: P = 125 -> thin 16 x m8 layout, merged leaf pass."""
+    op = make(3, 20, 5, 5, "strong", 1.0, H.slp_3d(scale=2.0), a=0.3)
+    pb = O.Problem(d=3, n=20, rank=5, leaf_side_max=5, kernel=O.Kernel("slp3d", scale=2.0),
+                   coeff=O.constant_coeff(0.3))
+    u = np.random.default_rng(2).standard_normal(20 ** 3)
+    assert rel(H.matvec(op, u), O.matvec(pb, u)) <= TOL
+
+
+def test_side6_square_leaf_sampled():
+    """n = 48, leaf 6, p = 6 (config-5-like tree on a uniform grid): square
+    leaves, P = 216 thin leaf pass with near and admissible matrices."""
+    op = make(3, 48, 6, 6, "strong", 1.0, H.inv_r_3d())
+    pb = O.Problem(d=3, n=48, rank=6, leaf_side_max=6, kernel=O.Kernel("slp3d", scale=4 * np.pi),
+                   coeff=O.constant_coeff(0.0))
+    u = np.random.default_rng(3).uniform(-1, 1, 48 ** 3)
+    f = H.matvec(op, u)
+    boxes = [((0, 6), (0, 6), (0, 6)), ((18, 24), (24, 30), (42, 48))]
+    rows = O.sampled_matvec(pb, u, boxes)
+    for i, bx in enumerate(boxes):
+        assert rel(f[O.box_linear_indices(48, bx)], rows[i, :, 0]) <= TOL
+
+
+def test_deep_weak_2d():
+    op = make(2, 128, 8, 8, "weak", None, H.gaussian(0.5))
+    pb = O.Problem(d=2, n=128, rank=8, leaf_side_max=8, kernel=O.Kernel("gaussian", sigma=0.5),
+                   coeff=O.constant_coeff(0.0), rule="weak", eta=None)
+    u = np.random.default_rng(4).standard_normal(128 ** 2)
+    assert rel(H.matvec(op, u), O.matvec(pb, u)) <= TOL
+
+
+def test_pointwise_coefficient_3d_multi_rhs():
+    fn = lambda pts: np.cos(3 * pts[:, 0]) + pts[:, 1] * pts[:, 2]   # noqa: E731
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        cfg = H.BuildConfig(rank=4, leaf_side=4, rule=H.AdmissibilityRule.strong(1.0), kernel=H.slp_3d(),
+                            coeff=H.CoefficientFn(fn))
+    op = H.construct(cfg, H.UniformGrid(3, 16))
+    pb = O.Problem(d=3, n=16, rank=4, leaf_side_max=4, kernel=O.Kernel("slp3d"), coeff=fn)
+    U = np.random.default_rng(5).standard_normal((16 ** 3, 3))
+    assert rel(H.matmat(op, U), O.matvec(pb, U)) <= TOL
+
+
+def test_legacy_and_graph_paths_agree():
+    """Direct launches (graphs off) and graph replay give identical results
+    up to the order of the fp64 atomic adds."""
+    op = make(3, 32, 8, 6, "strong", 1.0, H.inv_r_3d())
+    u = np.random.default_rng(6).standard_normal(32 ** 3)
+    f_graph = H.matvec(op, u)
+    H._lib.check(H._lib.lib().htlr_set_graphs(op._plan, 0))
+    f_direct = H.matvec(op, u)
+    assert rel(f_direct, f_graph) <= 1e-15
