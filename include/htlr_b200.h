@@ -177,6 +177,18 @@ int htlr_set_graphs(htlr_plan* plan, int32_t on);
 int htlr_exact_rows(htlr_plan* plan, const int64_t* rows, int64_t nrows, const double* u, double* out,
                     void* stream);
 
+/* Quasi-uniform (triangle mesh) front end, SURVEY 8(f) f3 (quasi.py):
+ * areas[c] = |triangle t  intersect  cell (i, j)| of the uniform m_side x
+ * m_side grid for candidate c = (t, i, j) (Sutherland-Hodgman clipping +
+ * shoelace, quasi.py:123-171); tri_xy = F x 6 doubles (x0 y0 x1 y1 x2 y2);
+ * all device pointers; stream-ordered. */
+int htlr_overlap_areas(const double* tri_xy, const int32_t* cand, int64_t ncand, int32_t m_side, double* areas,
+                       void* stream);
+/* y = A x for a CSR matrix (the transfer matrices S and T, quasi.py:174-261);
+ * device pointers; stream-ordered. */
+int htlr_csr_spmv(const int64_t* rowptr, const int32_t* cols, const double* vals, int64_t nrows, const double* x,
+                  double* y, void* stream);
+
 /* Per-launch profiling of htlr_matvec: when enabled, every kernel launch of
  * a matvec is bracketed by CUDA events on the launching stream.
  * htlr_profile_read returns, for the last matvec, one entry per launch:

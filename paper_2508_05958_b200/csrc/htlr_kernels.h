@@ -125,4 +125,10 @@ void launch_exact_rows(const KernelParams& kp, int d, int n, double h, double hd
                        const double* dvec_all, double* diag_rows, const double* avec, double aconst,
                        const double* u, double* out, cudaStream_t st);
 
+// quasi-uniform front end (htlr_quasi.cu)
+void launch_overlap(const double* tri_xy, const int* cand, int64_t ncand, int m_side, double* areas,
+                    cudaStream_t st);
+void launch_csr_spmv(const int64_t* rowptr, const int* cols, const double* vals, int64_t nrows, const double* x,
+                     double* y, cudaStream_t st);
+
 }  // namespace htlr

@@ -1274,6 +1274,23 @@ int htlr_exact_rows(htlr_plan* pl, const int64_t* rows, int64_t nrows, const dou
   return 0;
 }
 
+int htlr_overlap_areas(const double* tri_xy, const int32_t* cand, int64_t ncand, int32_t m_side, double* areas,
+                       void* stream) {
+  if (!tri_xy || !cand || !areas) return fail(-1, "null argument");
+  if (m_side < 1 || ncand < 0) return fail(-1, "invalid sizes");
+  htlr::launch_overlap(tri_xy, cand, ncand, m_side, areas, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int htlr_csr_spmv(const int64_t* rowptr, const int32_t* cols, const double* vals, int64_t nrows, const double* x,
+                  double* y, void* stream) {
+  if (!rowptr || !x || !y) return fail(-1, "null argument");
+  htlr::launch_csr_spmv(rowptr, cols, vals, nrows, x, y, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int64_t htlr_last_launch_count(const htlr_plan* pl) { return pl ? pl->last_launches : -1; }
 
 int htlr_diag_value(htlr_plan* pl, double* out) {

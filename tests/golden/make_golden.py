@@ -370,8 +370,46 @@ def check_sampled():
         assert diff == 0.0
 
 
+# ---------------------------------------------------------------- quasi-uniform pipeline (8(f) f3)
+
+
+def jittered_mesh(k, seed):
+    """Structured mesh with interior vertices moved (still a valid cover)."""
+    from htlr import quasi as rq
+    m = rq.structured_trimesh(k)
+    v = m.vertices.copy()
+    rng = np.random.default_rng(seed)
+    interior = (v[:, 0] > 0) & (v[:, 0] < 1) & (v[:, 1] > 0) & (v[:, 1] < 1)
+    v[interior] += rng.uniform(-0.25, 0.25, (interior.sum(), 2)) / k
+    return rq.TriMesh(vertices=v, triangles=m.triangles)
+
+
+def gen_quasi():
+    from htlr import quasi as rq
+    out = {}
+    cfg = htlr.BuildConfig(rank=4, leaf_side=4, rule=htlr.AdmissibilityRule.weak(),
+                           kernel=htlr.gaussian(np.sqrt(2.0)), coeff=htlr.CoefficientFn.constant(0.0))
+    for key, mesh in (("structured", rq.structured_trimesh(8)), ("jittered", jittered_mesh(8, 5))):
+        out[key + "_vertices"] = mesh.vertices
+        out[key + "_triangles"] = mesh.triangles
+        pipe = rq.build_pipeline(mesh, cfg, 2.0)
+        out[key + "_m_side"] = np.asarray([pipe.m_side])
+        out[key + "_S"] = pipe.to_uniform.matrix.toarray()
+        out[key + "_T"] = pipe.to_quasi.matrix.toarray()
+        u = np.random.default_rng(11).standard_normal(mesh.num_triangles)
+        out[key + "_u"] = u
+        out[key + "_f"] = rq.apply_pipeline(pipe, u)
+    tri = np.array([[0.1, 0.05], [0.9, 0.3], [0.35, 0.95]])
+    cells = [(0.0, 0.0, 0.5, 0.5), (0.25, 0.25, 0.75, 0.75), (0.5, 0.0, 1.0, 0.5), (0.9, 0.9, 1.0, 1.0)]
+    out["ov_tri"] = tri
+    out["ov_cells"] = np.asarray(cells)
+    out["ov_areas"] = np.asarray([rq.overlap_area(tri, c) for c in cells])
+    save("quasi", **out)
+
+
 def main(argv):
     jobs = {
+        "quasi": gen_quasi,
         "lists": gen_lists, "diag": gen_diag, "functions": gen_functions, "small": gen_small,
         "cfg1": lambda: gen_cfg("cfg1"), "cfg2": lambda: gen_cfg("cfg2"),
         "cfg2_sampled_check": check_sampled,
