@@ -112,6 +112,14 @@ int htlr_construct(htlr_plan* plan, void* stream);
  * asynchronous.  Replaces matvec / _hierarchical_matvec. */
 int htlr_matvec(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
 
+/* H-matrix baseline (construct_hmatrix / hmatrix_matvec, operators.py:129-135,
+ * 164-165; LowRankBlock blocks.py:76-86,167-187,262-264): the admissible
+ * blocks' factors are applied as dense kron(Q,..,Q) (s^d x p^d) matrices
+ * instead of mode products; same cores, same operator.  Call before
+ * htlr_construct; uniform grids only.  Exported admissible blocks then have
+ * kind 2 (u = v = dense factor, g = core matrix). */
+int htlr_set_lowrank(htlr_plan* plan, int32_t on);
+
 /* ---- multi-GPU: shard the target boxes by cluster subtrees --------------
  * Clusters are numbered in Morton order with the reference's child order, so
  * every subtree is a contiguous id range on every level.  With `world` (a

@@ -42,6 +42,20 @@ class TuckerBlock:
 
 
 @dataclass
+class LowRankBlock:
+    """Conventional low-rank block u g v^T of the H-matrix baseline
+    (blocks.py:76-86)."""
+
+    u: np.ndarray
+    g: np.ndarray
+    v: np.ndarray
+
+    @property
+    def shape(self) -> tuple:
+        return self.u.shape[0], self.v.shape[0]
+
+
+@dataclass
 class DenseBlock:
     matrix: np.ndarray
 
@@ -59,6 +73,8 @@ def materialize(block) -> np.ndarray:
     """Full matrix of an exported block (host helper for parity tools)."""
     if isinstance(block, DenseBlock):
         return block.matrix
+    if isinstance(block, LowRankBlock):
+        return block.u @ block.g @ block.v.T
     d = len(block.u_factors)
     full = block.core
     for a, f in enumerate(block.u_factors):
@@ -75,5 +91,7 @@ def storage_count(block) -> int:
     """Scalars the reference stores for this block (blocks.py:289-299)."""
     if isinstance(block, DenseBlock):
         return block.matrix.size
+    if isinstance(block, LowRankBlock):
+        return block.u.size + block.g.size + block.v.size
     return (sum(f.size for f in block.u_factors if f is not None)
             + sum(f.size for f in block.v_factors if f is not None) + block.core.size)

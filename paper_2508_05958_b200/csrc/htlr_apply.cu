@@ -350,6 +350,22 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
     __syncthreads();
     const double* Hsrc = lv.H + (anc * R + r) * (int64_t)lv.P;
     for (int i = threadIdx.x; i < P; i += blockDim.x) Hs[i] = Hsrc[i];
+    if (lv.K) {
+      // H-matrix baseline: dense factor row of each point of this leaf box
+      // inside its level-l ancestor box (F-order), times H
+      __syncthreads();
+      const int sl = lv.side;
+      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+        const int x = i % sL, y = (i / sL) % sL, z = i / (sL * sL);
+        int64_t row = (off[0] + x) + (int64_t)sl * (off[1] + y);
+        if (d == 3) row += (int64_t)sl * sl * (off[2] + z);
+        const double* kr = lv.K + row * P;
+        double v = 0.0;
+        for (int a = 0; a < P; ++a) v += kr[a] * Hs[a];
+        facc[i] += v;
+      }
+      continue;
+    }
     for (int i = threadIdx.x; i < d * sL * p; i += blockDim.x) {
       int a = i / (sL * p), rem = i % (sL * p);
       int x = rem / p, col = rem % p;

@@ -51,6 +51,7 @@ struct DownLevel {
   const double* Q; // side x p row-major (uniform), or per-interval tables
   const double* H; // [cluster][R][P]
   int64_t qstride; // 0: one factor for the level; else doubles per interval
+  const double* K; // H-matrix baseline: dense Kronecker factor (side^d x P), else null
 };
 
 // mapped grid: per (level, interval) nodes and raw factors
@@ -124,6 +125,11 @@ void launch_exact_rows(const KernelParams& kp, int d, int n, double h, double hd
                        const double* widths, const int64_t* rows, int64_t nrows, const double* cell_avg,
                        const double* dvec_all, double* diag_rows, const double* avec, double aconst,
                        const double* u, double* out, cudaStream_t st);
+
+// H-matrix baseline (htlr_lowrank.cu): dense Kronecker factors
+void launch_kron_factor(const double* Q, int d, int s, int p, double* K, cudaStream_t st);
+void launch_dense_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R, int K_pad,
+                         const double* K, int64_t c0, int64_t nc, cudaStream_t st);
 
 // quasi-uniform front end (htlr_quasi.cu)
 void launch_overlap(const double* tri_xy, const int* cand, int64_t ncand, int m_side, double* areas,

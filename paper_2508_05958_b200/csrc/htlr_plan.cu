@@ -103,6 +103,7 @@ struct Level {
   int64_t num_adm = 0;
   OffsetTable adm;
   DevBuf Q, R;             // side x p, p x p
+  DevBuf Kron;             // H-matrix baseline: dense kron(Q,..,Q), side^d x p^d
   DevBuf W, H;             // workspaces
   bool needs_up = false;   // W via upward pass, H via downward pass
   // mapped grid: per-interval nodes / raw factors, CSR of own targets
@@ -139,6 +140,8 @@ struct htlr_plan {
   // mapped quasi-uniform grid (BASELINE config 5): no translation invariance,
   // cores regenerated in the matvec (htlr_mapped.cu)
   bool mapped = false;
+  // H-matrix baseline (dense Kronecker factors, same cores)
+  bool lowrank = false;
   std::vector<double> mb, mx, mc;          // cell bounds, coords, widths (per dim)
   DevBuf d_mb, d_mx, d_mc, dvec;
   std::vector<int64_t> near_ptr;
@@ -299,6 +302,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
     lv.W.release();
     lv.H.release();
     lv.nodes.release();
+    lv.Kron.release();
     lv.Lm.release();
     lv.WLm.release();
     lv.d_ptr.release();
@@ -492,6 +496,14 @@ int htlr_build_lists(htlr_plan* pl) {
   }
   pl->lists_built = true;
   pl->constructed = false;
+  return 0;
+}
+
+int htlr_set_lowrank(htlr_plan* pl, int32_t on) {
+  if (!pl) return fail(-1, "null plan");
+  if (pl->constructed) return fail(-1, "select the representation before construct");
+  if (on && pl->mapped) return fail(-1, "the H-matrix baseline is built for uniform grids only");
+  pl->lowrank = on != 0;
   return 0;
 }
 
@@ -744,8 +756,18 @@ int htlr_construct(htlr_plan* pl, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(jobsbuf.ptr, fj.data(), fj.size() * sizeof(htlr::FactorJob), cudaMemcpyHostToDevice, st));
     htlr::launch_factor_qr((int)fj.size(), (const htlr::FactorJob*)jobsbuf.ptr, pl->h, p, st);
   }
-  // tables
+  // H-matrix baseline: dense Kronecker factors of the levels with a factor
   pl->device_scalars = 0;
+  if (pl->lowrank) {
+    for (auto& lv : pl->levels) {
+      if (!lv.needs_up || lv.side == p) continue;
+      const int64_t S = ipow(lv.side, d), P = ipow(p, d);
+      if (lv.Kron.alloc((size_t)(S * P) * sizeof(double))) return 1;
+      htlr::launch_kron_factor(lv.Q.d(), d, lv.side, p, lv.Kron.d(), st);
+      pl->device_scalars += S * P;
+    }
+  }
+  // tables
   for (auto& ps : pl->passes) {
     if (ps.table.alloc((size_t)ps.nmats * ps.mat_stride * sizeof(double))) return 1;
     pl->device_scalars += (int64_t)ps.nmats * ps.mat_stride;
@@ -993,7 +1015,7 @@ int mv_remote_mapped(MvCtx& cx, const double* u, double* f) {
                            (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, lv.H.d(), R, cx.st);
     if (cx.prof_end()) return 1;
     if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
-    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), lv.H.d(), (int64_t)lv.side * p};
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), lv.H.d(), (int64_t)lv.side * p, nullptr};
     double sl = pl->sL;
     down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
@@ -1034,7 +1056,10 @@ int mv_local(MvCtx& cx, const double* u) {
     double macs = (d == 2) ? (p * s1 * s1 + (double)p * p * s1)
                            : (p * s1 * s1 * s1 + (double)p * p * s1 * s1 + (double)p * p * p * s1);
     if (cx.prof_begin(1, lv.level, 2.0 * macs * nc * R, R8 * ((double)pl->N * frac + (double)nc * P))) return 1;
-    htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st);
+    if (lv.Kron.ptr)
+      htlr::launch_dense_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Kron.d(), c0, nc, cx.st);
+    else
+      htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st);
     if (cx.prof_end()) return 1;
   }
   return 0;
@@ -1076,7 +1101,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
-    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0};
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0, lv.Kron.d()};
     double sl = pl->sL;
     down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
@@ -1411,6 +1436,27 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
     // core tensor, F-order with target modes first: element (m, k) at m + P*k
     for (int k = 0; k < P; ++k)
       for (int m = 0; m < P; ++m) core_or_dense[m + (int64_t)P * k] = tiled[htlr::tiled_offset(m, k, ps->MT, ps->K_pad)];
+    if (pl->lowrank) {
+      // LowRankBlock(u, g, v): g = core as a P x P matrix (row-major), u = v =
+      // dense Kronecker factor (identity where the side equals p)
+      const int64_t S = ipow(lv.side, d);
+      std::vector<double> g((size_t)P * P);
+      for (int k = 0; k < P; ++k)
+        for (int m = 0; m < P; ++m) g[(size_t)m * P + k] = core_or_dense[m + (int64_t)P * k];
+      std::memcpy(core_or_dense, g.data(), g.size() * sizeof(double));
+      if (!factors || factor_cap < 2 * S * P) return fail(-1, "factor buffer too small");
+      if (lv.Kron.ptr) {
+        CUDA_TRY(cudaMemcpy(factors, lv.Kron.ptr, (size_t)(S * P) * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {
+        for (int64_t e = 0; e < S * P; ++e) factors[e] = (e / P == e % P) ? 1.0 : 0.0;
+      }
+      std::memcpy(factors + S * P, factors, (size_t)(S * P) * sizeof(double));
+      shapes[0] = 2;
+      shapes[1] = (int32_t)S;
+      shapes[2] = (int32_t)S;
+      shapes[3] = (int32_t)(2 * S * P);
+      return 0;
+    }
     if (lv.side != p) {
       std::vector<double> q((size_t)lv.side * p);
       CUDA_TRY(cudaMemcpy(q.data(), lv.Q.ptr, q.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1455,7 +1501,10 @@ int htlr_storage(const htlr_plan* pl, int64_t out[5]) {
   int64_t dense = pl->num_near * PL * PL, fac = 0, core = 0;
   for (const auto& lv : pl->levels) {
     core += lv.num_adm * (int64_t)ipow(p, 2 * d);
-    if (lv.side != p) fac += lv.num_adm * (int64_t)2 * d * lv.side * p;
+    if (pl->lowrank)   // LowRankBlock u and v: s^d x p^d each (blocks.py:294)
+      fac += lv.num_adm * (int64_t)2 * ipow(lv.side, d) * ipow(p, d);
+    else if (lv.side != p)
+      fac += lv.num_adm * (int64_t)2 * d * lv.side * p;
   }
   out[0] = dense;
   out[1] = fac;

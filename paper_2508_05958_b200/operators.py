@@ -18,7 +18,7 @@ from typing import Callable, Optional
 import numpy as np
 
 from . import _lib
-from .blocks import DenseBlock, TuckerBlock
+from .blocks import DenseBlock, LowRankBlock, TuckerBlock
 from .grids import (ADMISSIBLE, AdmissibilityRule, BlockClusterTree, UniformGrid,
                     build_cluster_tree, export_leaf_array, grid_kind)
 from .kernels import CoefficientFn, KernelSpec, QuadratureConfig, singular_rule
@@ -144,13 +144,22 @@ class HTLRMatrix:
         d, p = self.grid.d, self.config.rank
         cap = max(p ** (2 * d), side ** (2 * d))
         buf = np.zeros(cap)
-        fac = np.zeros(2 * d * self.grid.n * p)
+        nfac_max = 2 * d * self.grid.n * p
+        if isinstance(self, HMatrix):   # dense factors: 2 x side^d x p^d at the coarsest level
+            nfac_max = max(nfac_max, 2 * max(self.grid.n // 2, 1) ** d * p ** d)
+        fac = np.zeros(nfac_max)
         shapes = np.zeros(4, dtype=np.int32)
         _lib.check(_lib.lib().htlr_export_block(self._plan, int(leaf_id), buf.ctypes.data, buf.size,
                                                 fac.ctypes.data, fac.size, shapes.ctypes.data))
         kind, rows, cols, nfac = (int(v) for v in shapes)
         if kind == 1:
             return DenseBlock(matrix=buf[: rows * cols].reshape(rows, cols).copy())
+        if kind == 2:
+            P = p ** d
+            g = buf[: P * P].reshape(P, P).copy()
+            u = fac[: rows * P].reshape(rows, P).copy()
+            v = fac[rows * P: 2 * rows * P].reshape(rows, P).copy()
+            return LowRankBlock(u=u, g=g, v=v)
         core = buf[: p ** (2 * d)].reshape((p,) * (2 * d), order="F").copy()
         if nfac == 0:
             return TuckerBlock(core=core, u_factors=[None] * d, v_factors=[None] * d)
@@ -216,6 +225,37 @@ def construct(cfg: BuildConfig, grid: UniformGrid, threads: int = 1,
     with torch.cuda.device(device):
         _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(_current_stream_ptr(device))))
     return op
+
+
+class HMatrix(HTLRMatrix):
+    """H-matrix baseline handle (operators.py:74-83)."""
+
+
+def construct_hmatrix(cfg: BuildConfig, grid: UniformGrid, threads: int = 1,
+                      device: Optional[int] = None) -> HMatrix:
+    """Baseline with conventional low-rank leaves (operators.py:129-135): same
+    interpolant and cores, factors applied as dense kron(Q,..,Q) matrices."""
+    import torch
+    cfg.kernel.device_code
+    if grid_kind(grid)[0] != 0:
+        raise ValueError("the H-matrix baseline is built for uniform grids only")
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    op = HMatrix(grid, cfg, int(device))
+    L = _lib.lib()
+    _lib.check(L.htlr_set_lowrank(op._plan, 1))
+    _lib.check(L.htlr_build_lists(op._plan))
+    if cfg.coeff.constant_value is None:
+        a = np.ascontiguousarray(cfg.coeff(_all_points(grid)), dtype=np.float64)
+        _lib.check(L.htlr_set_coeff(op._plan, a.ctypes.data))
+    with torch.cuda.device(device):
+        _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(_current_stream_ptr(device))))
+    return op
+
+
+def hmatrix_matvec(op: HMatrix, u):
+    """operators.py:164-165."""
+    return _apply(op, u, 1)
 
 
 def _all_points(grid: UniformGrid) -> np.ndarray:

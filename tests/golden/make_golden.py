@@ -407,8 +407,33 @@ def gen_quasi():
     save("quasi", **out)
 
 
+def gen_hmatrix():
+    """H-matrix baseline (construct_hmatrix / hmatrix_matvec) on small grids."""
+    out = {}
+    cases = {
+        "h2_weak_gauss": (2, 64, 8, 4, htlr.AdmissibilityRule.weak(), htlr.gaussian(np.sqrt(2.0)), 41),
+        "h3_eta1_slp": (3, 16, 4, 3, htlr.AdmissibilityRule.strong(1.0), htlr.slp_3d(), 42),
+    }
+    for key, (d, n, leaf, p, rule, k, seed) in cases.items():
+        cfg = htlr.BuildConfig(rank=p, leaf_side=leaf, rule=rule, kernel=k, coeff=htlr.CoefficientFn.constant(0.0))
+        grid = htlr.UniformGrid(d, n)
+        hop = htlr.construct_hmatrix(cfg, grid)
+        u = np.random.default_rng(seed).standard_normal(grid.num_points)
+        out[key + "_f"] = htlr.hmatrix_matvec(hop, u)
+        rep = htlr.storage_report(hop)
+        out[key + "_storage"] = np.asarray([rep.dense_scalars, rep.factor_scalars, rep.core_scalars,
+                                            rep.total_scalars], dtype=np.int64)
+        for lf in hop.block_tree.leaves:
+            if lf.kind == rgrids.ADMISSIBLE:
+                out[key + "_adm_leaf"] = np.asarray([lf.leaf_id])
+                out[key + "_adm_mat"] = htlr.materialize(hop.payloads[lf.leaf_id])
+                break
+    save("hmatrix", **out)
+
+
 def main(argv):
     jobs = {
+        "hmatrix": gen_hmatrix,
         "quasi": gen_quasi,
         "lists": gen_lists, "diag": gen_diag, "functions": gen_functions, "small": gen_small,
         "cfg1": lambda: gen_cfg("cfg1"), "cfg2": lambda: gen_cfg("cfg2"),
