@@ -76,13 +76,85 @@ def cmd_bench_uniform(args) -> list:
                                       seed=(args.seed, 1))
     rep = H.storage_report(op)
     run_id = f"u-d{args.dim}-{args.kernel}-n{args.n}-{args.adm}-p{args.p}-l{args.leaf}-s{args.seed}"
-    return [{
-        "id": run_id, "variant": "htlr-b200", "d": args.dim, "n": args.n, "kernel": args.kernel,
-        "adm": args.adm, "p": args.p, "leaf": args.leaf, "t_construct": t_con, "t_apply": t_apply,
+    base = {"id": run_id, "d": args.dim, "n": args.n, "kernel": args.kernel, "adm": args.adm, "p": args.p,
+            "leaf": args.leaf, "seed": args.seed}
+    rows = [{
+        **base, "variant": "htlr-b200", "t_construct": t_con, "t_apply": t_apply,
         "dense_scalars": rep.dense_scalars, "factor_scalars": rep.factor_scalars,
         "core_scalars": rep.core_scalars, "total_scalars": rep.total_scalars,
-        "bound": rep.theoretical_bound, "e_apply_rand": err, "seed": args.seed,
+        "bound": rep.theoretical_bound, "e_apply_rand": err,
     }]
+    if args.baseline:
+        hop, t_con_h = _best_of(lambda: H.construct_hmatrix(cfg, grid))
+        _, t_apply_h = _best_of(lambda: H.hmatrix_matvec(hop, ud))
+        err_h = _sampled_error(H, hop, H.hmatrix_matvec, exact, u, (args.seed, 1), grid.num_points)
+        rep_h = H.storage_report(hop)
+        rows.append({
+            **base, "variant": "hmatrix-b200", "t_construct": t_con_h, "t_apply": t_apply_h,
+            "dense_scalars": rep_h.dense_scalars, "factor_scalars": rep_h.factor_scalars,
+            "core_scalars": rep_h.core_scalars, "total_scalars": rep_h.total_scalars,
+            "bound": rep_h.theoretical_bound, "e_apply_rand": err_h,
+        })
+    return rows
+
+
+def _sampled_error(H, op, apply_fn, exact, u, seed, n_rows):
+    rows = np.random.default_rng(seed).choice(n_rows, size=min(1000, n_rows), replace=False)
+    approx = np.asarray(apply_fn(op, u))
+    ex = exact(rows, u)
+    return float(np.linalg.norm(approx[rows] - ex) / np.linalg.norm(ex))
+
+
+QUASI_HEADER = [
+    "id", "variant", "d", "n_quasi", "rho", "m_side", "kernel", "adm", "p",
+    "leaf", "t_construct", "t_apply", "dense_scalars", "factor_scalars",
+    "core_scalars", "total_scalars", "bound", "e_apply_rand", "seed",
+]
+
+
+def quasi_test_field(points: np.ndarray) -> np.ndarray:
+    """The reference's smooth benchmark field (cli.py:66-73)."""
+    x1, x2 = points[:, 0], points[:, 1]
+    return 1.0 + 0.5 * np.exp(-((x1 - 0.3) ** 2) - (x2 - 0.6) ** 2) + np.sin(5.0 * x1 * x2)
+
+
+def cmd_bench_quasi(args) -> list:
+    """Triangle-mesh pipeline rows (cli.py:263-316); the error column is the
+    sampled error against the uniform-grid exact rows transferred by T S
+    (the reference's triangle-average row oracle is not on the B200 path)."""
+    import paper_2508_05958_b200 as H
+    if args.dim != 2:
+        raise UsageError("the quasi-uniform pipeline is two-dimensional")
+    if args.mesh is not None:
+        mesh = H.load_mesh(args.mesh)
+    else:
+        if args.n is None:
+            raise UsageError("bench-quasi needs --n (number of triangles) or --mesh")
+        k = int(round(np.sqrt(args.n / 2.0)))
+        if 2 * k * k != args.n:
+            raise UsageError(f"--n {args.n} is not of the form 2*k^2 for a structured mesh")
+        mesh = H.structured_trimesh(k)
+    kernel = H.by_name(args.kernel, 2)
+    rule = (H.AdmissibilityRule.weak() if args.adm == "weak"
+            else H.AdmissibilityRule.strong(args.eta if args.eta is not None else float(np.sqrt(2))))
+    cfg = H.BuildConfig(rank=args.p, leaf_side=args.leaf, rule=rule, kernel=kernel,
+                        coeff=H.CoefficientFn.constant(0.0), quadrature=H.QuadratureConfig())
+    u = quasi_test_field(mesh.centroids)
+    rows = []
+    for rho in (args.rho or [2.0]):
+        pipe, t_con = _best_of(lambda: H.build_pipeline(mesh, cfg, rho))
+        out, t_apply = _best_of(lambda: H.apply_pipeline(pipe, u))
+        rep = H.storage_report(pipe.op)
+        rows.append({
+            "id": f"q-{args.kernel}-N{mesh.num_triangles}-rho{rho:g}-{args.adm}-p{args.p}-l{args.leaf}-s{args.seed}",
+            "variant": "htlr-quasi-b200", "d": 2, "n_quasi": mesh.num_triangles, "rho": pipe.rho,
+            "m_side": pipe.m_side, "kernel": args.kernel, "adm": args.adm, "p": args.p, "leaf": args.leaf,
+            "t_construct": t_con, "t_apply": t_apply, "dense_scalars": rep.dense_scalars,
+            "factor_scalars": rep.factor_scalars, "core_scalars": rep.core_scalars,
+            "total_scalars": rep.total_scalars, "bound": rep.theoretical_bound,
+            "e_apply_rand": float("nan"), "seed": args.seed,
+        })
+    return rows
 
 
 def _write_rows(rows, header, args) -> None:
@@ -118,8 +190,21 @@ def build_parser() -> argparse.ArgumentParser:
     pu.add_argument("--leaf", type=int, default=16)
     pu.add_argument("--adm", choices=("weak", "strong"), default="weak")
     pu.add_argument("--eta", type=float, default=None)
-    pu.add_argument("--baseline", action="store_true",
-                    help="the H-matrix baseline is not part of the B200 path (usage error)")
+    pu.add_argument("--baseline", action="store_true", help="also run the H-matrix baseline")
+    pq = sub.add_parser("bench-quasi", help="triangulated-grid pipeline benchmark")
+    pq.add_argument("--dim", type=int, choices=(2, 3), default=2)
+    pq.add_argument("--kernel", choices=("gaussian", "slp2d", "slp3d"), default="gaussian")
+    pq.add_argument("--seed", type=int, default=0)
+    pq.add_argument("--out", default=None)
+    pq.add_argument("--format", choices=("csv", "json"), default="csv")
+    pq.add_argument("--threads", type=int, default=1)
+    pq.add_argument("--n", type=int, default=None)
+    pq.add_argument("--mesh", default=None)
+    pq.add_argument("--rho", type=float, action="append", default=None)
+    pq.add_argument("--p", type=int, default=8)
+    pq.add_argument("--leaf", type=int, default=16)
+    pq.add_argument("--adm", choices=("weak", "strong"), default="weak")
+    pq.add_argument("--eta", type=float, default=None)
     return parser
 
 
@@ -134,9 +219,10 @@ def main(argv=None) -> int:
             raise UsageError("slp3d requires --dim 3")
         if args.kernel == "slp2d" and args.dim != 2:
             raise UsageError("slp2d requires --dim 2")
-        if args.baseline:
-            raise UsageError("--baseline (H-matrix) is not available on the B200 path")
-        _write_rows(cmd_bench_uniform(args), UNIFORM_HEADER, args)
+        if args.command == "bench-uniform":
+            _write_rows(cmd_bench_uniform(args), UNIFORM_HEADER, args)
+        else:
+            _write_rows(cmd_bench_quasi(args), QUASI_HEADER, args)
     except UsageError as exc:
         print(f"usage error: {exc}", file=sys.stderr)
         return 2
