@@ -119,9 +119,9 @@ def quasi_test_field(points: np.ndarray) -> np.ndarray:
 
 
 def cmd_bench_quasi(args) -> list:
-    """Triangle-mesh pipeline rows (cli.py:263-316); the error column is the
-    sampled error against the uniform-grid exact rows transferred by T S
-    (the reference's triangle-average row oracle is not on the B200 path)."""
+    """Triangle-mesh pipeline rows (cli.py:263-316).  e_apply_rand is left NaN:
+    the reference computes it with a triangle-average row oracle
+    (oracles.py:186-209) that is not part of the B200 path."""
     import paper_2508_05958_b200 as H
     if args.dim != 2:
         raise UsageError("the quasi-uniform pipeline is two-dimensional")
