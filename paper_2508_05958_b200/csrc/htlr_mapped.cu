@@ -128,13 +128,16 @@ template <int RB, int PP, int KIND>
 __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, const double* __restrict__ nodes,
                                  const int64_t* __restrict__ rowptr, const int* __restrict__ cols, int64_t t0,
                                  const double* __restrict__ W, int K_pad, double* __restrict__ H, int R, int r0) {
+  // SB sources are staged per barrier pair (fewer barriers, more loads in
+  // flight); their W vectors arrive pre-scaled by the kernel constant
+  constexpr int SB = RB >= 16 ? 1 : 4;
   extern __shared__ double sm[];
   const double nid = -1.0 / kp.denom;
   const int p = PP ? PP : p_rt;
   const int P = (d == 2) ? p * p : p * p * p;
-  double* sW = sm;                       // RB x P
-  double* sEta = sW + RB * P;            // d x p
-  double* sYZ = sEta + 3 * kMaxRank;     // per thread: dy^2[p], dz^2[p]
+  double* sW = sm;                            // SB x RB x P
+  double* sEta = sW + SB * RB * P;            // SB x 3 x kMaxRank
+  double* sYZ = sEta + SB * 3 * kMaxRank;     // per thread: dy^2[p], dz^2[p]
   const int64_t row = blockIdx.x;
   const int64_t tau = t0 + row;
   int tc[3];
@@ -150,48 +153,58 @@ __global__ void regen_adm_kernel(KernelParams kp, int d, int p_rt, int level, co
 #pragma unroll
   for (int q = 0; q < RB; ++q) acc[q] = 0.0;
   const int nrb = min(RB, R - r0);
-  for (int64_t e = rowptr[row]; e < rowptr[row + 1]; ++e) {
-    const int sigma = cols[e];
-    int sc[3];
-    morton_decode(sigma, d, level, sc);
+  const double coef = kernel_coef(kp);
+  const int64_t e_end = rowptr[row + 1];
+  for (int64_t e0 = rowptr[row]; e0 < e_end; e0 += SB) {
+    const int nsb = (int)min((int64_t)SB, e_end - e0);
     __syncthreads();
-    for (int i = threadIdx.x; i < d * p; i += blockDim.x) sEta[(i / p) * kMaxRank + i % p] = nodes[sc[i / p] * p + i % p];
-    const double coef = kernel_coef(kp);
-    for (int i = threadIdx.x; i < nrb * P; i += blockDim.x) {
-      const int q = i / P, s = i % P;
-      sW[i] = coef * W[((int64_t)sigma * R + r0 + q) * K_pad + s];
+    for (int i = threadIdx.x; i < nsb * d * p; i += blockDim.x) {
+      const int b = i / (d * p), rem = i % (d * p), a = rem / p, k = rem % p;
+      const int sigma = cols[e0 + b];
+      int sc[3];
+      morton_decode(sigma, d, level, sc);
+      sEta[(b * 3 + a) * kMaxRank + k] = nodes[sc[a] * p + k];
+    }
+    for (int i = threadIdx.x; i < nsb * nrb * P; i += blockDim.x) {
+      const int b = i / (nrb * P), rem = i % (nrb * P), q = rem / P, sidx = rem % P;
+      const int sigma = cols[e0 + b];
+      sW[(b * RB + q) * P + sidx] = coef * W[((int64_t)sigma * R + r0 + q) * K_pad + sidx];
     }
     __syncthreads();
     if (!act) continue;
-    double dx2[PP ? PP : kMaxRank];
+    for (int b = 0; b < nsb; ++b) {
+      const double* eta = sEta + b * 3 * kMaxRank;
+      const double* wb = sW + b * RB * P;
+      double dx2[PP ? PP : kMaxRank];
 #pragma unroll
-    for (int s = 0; s < (PP ? PP : kMaxRank); ++s) {
-      if (s < p) {
-        const double a = __dadd_rn(xi0, -sEta[s]);
-        dx2[s] = __dmul_rn(a, a);
+      for (int s = 0; s < (PP ? PP : kMaxRank); ++s) {
+        if (s < p) {
+          const double a = __dadd_rn(xi0, -eta[s]);
+          dx2[s] = __dmul_rn(a, a);
+        }
       }
-    }
-    for (int s = 0; s < p; ++s) {
-      const double b = __dadd_rn(xi1, -sEta[kMaxRank + s]);
-      myYZ[s] = __dmul_rn(b, b);
-      if (d == 3) {
-        const double c = __dadd_rn(xi2, -sEta[2 * kMaxRank + s]);
-        myYZ[p + s] = __dmul_rn(c, c);
+      for (int s = 0; s < p; ++s) {
+        const double bb = __dadd_rn(xi1, -eta[kMaxRank + s]);
+        myYZ[s] = __dmul_rn(bb, bb);
+        if (d == 3) {
+          const double c = __dadd_rn(xi2, -eta[2 * kMaxRank + s]);
+          myYZ[p + s] = __dmul_rn(c, c);
+        }
       }
-    }
-    const int n3 = (d == 3) ? p : 1;
-    for (int s3 = 0; s3 < n3; ++s3) {
-      const double z2 = (d == 3) ? myYZ[p + s3] : 0.0;
-      for (int s2 = 0; s2 < p; ++s2) {
-        const double yz = myYZ[s2] + z2;
-        const double* w = sW + (s2 + p * s3) * p;
+      const int n3 = (d == 3) ? p : 1;
+      for (int s3 = 0; s3 < n3; ++s3) {
+        const double z2 = (d == 3) ? myYZ[p + s3] : 0.0;
+        for (int s2 = 0; s2 < p; ++s2) {
+          const double yz = myYZ[s2] + z2;
+          const double* w = wb + (s2 + p * s3) * p;
 #pragma unroll
-        for (int s1 = 0; s1 < (PP ? PP : kMaxRank); ++s1) {
-          if (s1 < p) {
-            const double kv = kernel_shape<KIND>(dx2[s1] + yz, nid);
+          for (int s1 = 0; s1 < (PP ? PP : kMaxRank); ++s1) {
+            if (s1 < p) {
+              const double kv = kernel_shape<KIND>(dx2[s1] + yz, nid);
 #pragma unroll
-            for (int q = 0; q < RB; ++q)
-              if (q < nrb) acc[q] += kv * w[q * P + s1];
+              for (int q = 0; q < RB; ++q)
+                if (q < nrb) acc[q] += kv * w[q * P + s1];
+            }
           }
         }
       }
@@ -211,13 +224,14 @@ __global__ void regen_near_kernel(KernelParams kp, int d, int sL_rt, int L, cons
                                   const double* __restrict__ widths, const int64_t* __restrict__ rowptr,
                                   const int* __restrict__ cols, int64_t t0, const double* __restrict__ ub, int K_pad,
                                   double* __restrict__ Y, int R, int r0) {
+  constexpr int SB = RB >= 16 ? 1 : 4;
   extern __shared__ double sm[];
   const double nid = -1.0 / kp.denom;
   const int sL = SS ? SS : sL_rt;
   const int P = (d == 2) ? sL * sL : sL * sL * sL;
-  double* sV = sm;                   // RB x P   (w_j u_j)
-  double* sY = sV + RB * P;          // 3 x 16   (source coordinates)
-  double* sYZ = sY + 3 * 16;         // per thread dy^2[sL], dz^2[sL]
+  double* sV = sm;                   // SB x RB x P   (c w_j u_j)
+  double* sY = sV + SB * RB * P;     // SB x 3 x 16   (source coordinates)
+  double* sYZ = sY + SB * 3 * 16;    // per thread dy^2[sL], dz^2[sL]
   const int64_t row = blockIdx.x;
   const int64_t tau = t0 + row;
   int tc[3];
@@ -233,53 +247,65 @@ __global__ void regen_near_kernel(KernelParams kp, int d, int sL_rt, int L, cons
 #pragma unroll
   for (int q = 0; q < RB; ++q) acc[q] = 0.0;
   const int nrb = min(RB, R - r0);
-  for (int64_t e = rowptr[row]; e < rowptr[row + 1]; ++e) {
-    const int sigma = cols[e];
-    int sc[3];
-    morton_decode(sigma, d, L, sc);
+  const double coef = kernel_coef(kp);
+  const int64_t e_end = rowptr[row + 1];
+  for (int64_t e0 = rowptr[row]; e0 < e_end; e0 += SB) {
+    const int nsb = (int)min((int64_t)SB, e_end - e0);
     __syncthreads();
-    for (int k = threadIdx.x; k < d * sL; k += blockDim.x) sY[(k / sL) * 16 + k % sL] = coords[sc[k / sL] * sL + k % sL];
-    for (int k = threadIdx.x; k < nrb * P; k += blockDim.x) {
-      const int q = k / P, j = k % P;
+    for (int k = threadIdx.x; k < nsb * d * sL; k += blockDim.x) {
+      const int b = k / (d * sL), rem = k % (d * sL), a = rem / sL, j = rem % sL;
+      int sc[3];
+      morton_decode(cols[e0 + b], d, L, sc);
+      sY[(b * 3 + a) * 16 + j] = coords[sc[a] * sL + j];
+    }
+    for (int k = threadIdx.x; k < nsb * nrb * P; k += blockDim.x) {
+      const int b = k / (nrb * P), rem = k % (nrb * P), q = rem / P, j = rem % P;
+      const int sigma = cols[e0 + b];
+      int sc[3];
+      morton_decode(sigma, d, L, sc);
       const int j1 = j % sL, j2 = (j / sL) % sL, j3 = j / (sL * sL);
       double w = widths[sc[0] * sL + j1] * widths[sc[1] * sL + j2];
       if (d == 3) w = w * widths[sc[2] * sL + j3];
-      sV[k] = kernel_coef(kp) * (w * ub[((int64_t)sigma * R + r0 + q) * K_pad + j]);
+      sV[(b * RB + q) * P + j] = coef * (w * ub[((int64_t)sigma * R + r0 + q) * K_pad + j]);
     }
     __syncthreads();
     if (!act) continue;
-    const bool self = sigma == tau;
-    double dx2[SS ? SS : 16];
+    for (int b = 0; b < nsb; ++b) {
+      const bool self = cols[e0 + b] == tau;
+      const double* yb = sY + b * 3 * 16;
+      const double* vb = sV + b * RB * P;
+      double dx2[SS ? SS : 16];
 #pragma unroll
-    for (int s = 0; s < (SS ? SS : 16); ++s) {
-      if (s < sL) {
-        const double a = __dadd_rn(x0, -sY[s]);
-        dx2[s] = __dmul_rn(a, a);
+      for (int s = 0; s < (SS ? SS : 16); ++s) {
+        if (s < sL) {
+          const double a = __dadd_rn(x0, -yb[s]);
+          dx2[s] = __dmul_rn(a, a);
+        }
       }
-    }
-    for (int s = 0; s < sL; ++s) {
-      const double b = __dadd_rn(x1, -sY[16 + s]);
-      myYZ[s] = __dmul_rn(b, b);
-      if (d == 3) {
-        const double c = __dadd_rn(x2, -sY[32 + s]);
-        myYZ[sL + s] = __dmul_rn(c, c);
+      for (int s = 0; s < sL; ++s) {
+        const double bb = __dadd_rn(x1, -yb[16 + s]);
+        myYZ[s] = __dmul_rn(bb, bb);
+        if (d == 3) {
+          const double c = __dadd_rn(x2, -yb[32 + s]);
+          myYZ[sL + s] = __dmul_rn(c, c);
+        }
       }
-    }
-    const int n3 = (d == 3) ? sL : 1;
-    for (int j3 = 0; j3 < n3; ++j3) {
-      const double z2 = (d == 3) ? myYZ[sL + j3] : 0.0;
-      for (int j2 = 0; j2 < sL; ++j2) {
-        const double yz = myYZ[j2] + z2;
-        const int jb = (j2 + sL * j3) * sL;
-        const double* v = sV + jb;
+      const int n3 = (d == 3) ? sL : 1;
+      for (int j3 = 0; j3 < n3; ++j3) {
+        const double z2 = (d == 3) ? myYZ[sL + j3] : 0.0;
+        for (int j2 = 0; j2 < sL; ++j2) {
+          const double yz = myYZ[j2] + z2;
+          const int jb = (j2 + sL * j3) * sL;
+          const double* v = vb + jb;
 #pragma unroll
-        for (int j1 = 0; j1 < (SS ? SS : 16); ++j1) {
-          if (j1 < sL) {
-            if (self && jb + j1 == i) continue;
-            const double kv = kernel_shape<KIND>(dx2[j1] + yz, nid);
+          for (int j1 = 0; j1 < (SS ? SS : 16); ++j1) {
+            if (j1 < sL) {
+              if (self && jb + j1 == i) continue;
+              const double kv = kernel_shape<KIND>(dx2[j1] + yz, nid);
 #pragma unroll
-            for (int q = 0; q < RB; ++q)
-              if (q < nrb) acc[q] += kv * v[q * P + j1];
+              for (int q = 0; q < RB; ++q)
+                if (q < nrb) acc[q] += kv * v[q * P + j1];
+            }
           }
         }
       }
@@ -355,7 +381,8 @@ static void adm_k(const KernelParams& kp, int d, int p, int level, const double*
                   cudaStream_t st) {
   const int P = (d == 2) ? p * p : p * p * p;
   const int thr = regen_threads(P);
-  size_t smem = sizeof(double) * ((size_t)RB * P + 3 * kMaxRank + (size_t)thr * 2 * p);
+  const size_t SB = RB >= 16 ? 1 : 4;
+  size_t smem = sizeof(double) * (SB * RB * P + SB * 3 * kMaxRank + (size_t)thr * 2 * p);
   cudaFuncSetAttribute(regen_adm_kernel<RB, PP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   regen_adm_kernel<RB, PP, KIND><<<(unsigned)nt, thr, smem, st>>>(kp, d, p, level, nodes, rowptr, cols, t0, W, K_pad,
                                                                  H, R, r0);
@@ -410,7 +437,8 @@ static void near_k(const KernelParams& kp, int d, int sL, int L, const double* c
                    double* Y, int R, int r0, cudaStream_t st) {
   const int P = (d == 2) ? sL * sL : sL * sL * sL;
   const int thr = regen_threads(P);
-  size_t smem = sizeof(double) * ((size_t)RB * P + 3 * 16 + (size_t)thr * 2 * sL);
+  const size_t SB = RB >= 16 ? 1 : 4;
+  size_t smem = sizeof(double) * (SB * RB * P + SB * 3 * 16 + (size_t)thr * 2 * sL);
   cudaFuncSetAttribute(regen_near_kernel<RB, SS, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   regen_near_kernel<RB, SS, KIND><<<(unsigned)nt, thr, smem, st>>>(kp, d, sL, L, coords, widths, rowptr, cols, t0,
                                                                   ub, K_pad, Y, R, r0);
