@@ -197,6 +197,17 @@ int htlr_overlap_areas(const double* tri_xy, const int32_t* cand, int64_t ncand,
 int htlr_csr_spmv(const int64_t* rowptr, const int32_t* cols, const double* vals, int64_t nrows, const double* x,
                   double* y, void* stream);
 
+/* Building blocks of the public API, computed on the current device from
+ * host arrays (synchronous): Chebyshev nodes (cheb_points, chebyshev.py:31-38),
+ * Lagrange factor matrix npts x order (factor_matrix, chebyshev.py:52-66),
+ * kernel values m1 x m2 for d-dimensional point sets (pairwise,
+ * kernels.py:113-117; -1 "SLP kernel evaluated on the diagonal" on r = 0). */
+int htlr_cheb_nodes(double lo, double hi, int32_t order, double* out_host);
+int htlr_lagrange_matrix(const double* pts_host, int64_t npts, const double* nodes_host, int32_t order,
+                         double* out_host);
+int htlr_kernel_pairs(int32_t kernel, double sigma, double scale, int32_t d, const double* x_host, int64_t m1,
+                      const double* y_host, int64_t m2, double* out_host);
+
 /* Per-launch profiling of htlr_matvec: when enabled, every kernel launch of
  * a matvec is bracketed by CUDA events on the launching stream.
  * htlr_profile_read returns, for the last matvec, one entry per launch:

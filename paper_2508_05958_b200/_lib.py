@@ -70,6 +70,9 @@ SYMBOLS = [
     ("htlr_exact_rows", ctypes.c_int, [_P, _P, _I64, _P, _P, _P]),
     ("htlr_set_graphs", ctypes.c_int, [_P, _I32]),
     ("htlr_overlap_areas", ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    ("htlr_cheb_nodes", ctypes.c_int, [_D, _D, _I32, _P]),
+    ("htlr_lagrange_matrix", ctypes.c_int, [_P, _I64, _P, _I32, _P]),
+    ("htlr_kernel_pairs", ctypes.c_int, [_I32, _D, _D, _I32, _P, _I64, _P, _I64, _P]),
     ("htlr_csr_spmv", ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P]),
     ("htlr_profile_enable", ctypes.c_int, [_P, _I32]),
     ("htlr_profile_read", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, ctypes.POINTER(_I64)]),

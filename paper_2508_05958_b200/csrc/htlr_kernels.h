@@ -131,6 +131,12 @@ void launch_kron_factor(const double* Q, int d, int s, int p, double* K, cudaStr
 void launch_dense_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R, int K_pad,
                          const double* K, int64_t c0, int64_t nc, cudaStream_t st);
 
+// API building blocks (htlr_interp.cu)
+void launch_cheb_nodes(double lo, double hi, int p, double* out, cudaStream_t st);
+void launch_lagrange(const double* pts, int64_t n, const double* nodes, int p, double* out, cudaStream_t st);
+void launch_pairs(const KernelParams& kp, int d, const double* x, int64_t m1, const double* y, int64_t m2, double* out,
+                  int* coincident, cudaStream_t st);
+
 // quasi-uniform front end (htlr_quasi.cu)
 void launch_overlap(const double* tri_xy, const int* cand, int64_t ncand, int m_side, double* areas,
                     cudaStream_t st);

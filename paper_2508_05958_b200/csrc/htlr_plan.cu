@@ -1316,6 +1316,52 @@ int htlr_csr_spmv(const int64_t* rowptr, const int32_t* cols, const double* vals
   return 0;
 }
 
+int htlr_cheb_nodes(double lo, double hi, int32_t order, double* out_host) {
+  if (!out_host) return fail(-1, "null argument");
+  if (!(lo < hi)) return fail(-1, "interval must satisfy lo < hi");
+  if (order < 1 || order > 64) return fail(-1, "order must be in [1, 64]");
+  DevBuf o;
+  if (o.alloc(order * sizeof(double))) return 1;
+  htlr::launch_cheb_nodes(lo, hi, order, o.d(), 0);
+  CUDA_TRY(cudaMemcpy(out_host, o.ptr, order * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int htlr_lagrange_matrix(const double* pts_host, int64_t npts, const double* nodes_host, int32_t order,
+                         double* out_host) {
+  if ((!pts_host && npts) || !nodes_host || !out_host) return fail(-1, "null argument");
+  if (order < 1 || order > 64) return fail(-1, "order must be in [1, 64]");
+  DevBuf dp, dn, o;
+  if (upload(dp, pts_host, npts * sizeof(double)) || upload(dn, nodes_host, order * sizeof(double)) ||
+      o.alloc(std::max<int64_t>(1, npts * order) * sizeof(double)))
+    return 1;
+  htlr::launch_lagrange(dp.d(), npts, dn.d(), order, o.d(), 0);
+  CUDA_TRY(cudaMemcpy(out_host, o.ptr, npts * order * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int htlr_kernel_pairs(int32_t kernel, double sigma, double scale, int32_t d, const double* x_host, int64_t m1,
+                      const double* y_host, int64_t m2, double* out_host) {
+  if (!out_host || (!x_host && m1) || (!y_host && m2)) return fail(-1, "null argument");
+  if (d < 1 || d > 3) return fail(-1, "dimension must be 1..3 for device kernel pairs");
+  if (kernel < 0 || kernel > 2) return fail(-1, "unknown kernel kind");
+  htlr::KernelParams kp;
+  kp.kind = kernel;
+  kp.denom = (2.0 * sigma) * sigma;
+  kp.scale = scale;
+  DevBuf dx, dy, o, flag;
+  if (upload(dx, x_host, m1 * d * sizeof(double)) || upload(dy, y_host, m2 * d * sizeof(double)) ||
+      o.alloc(std::max<int64_t>(1, m1 * m2) * sizeof(double)) || flag.alloc(sizeof(int)))
+    return 1;
+  CUDA_TRY(cudaMemset(flag.ptr, 0, sizeof(int)));
+  htlr::launch_pairs(kp, d, dx.d(), m1, dy.d(), m2, o.d(), (int*)flag.ptr, 0);
+  int hit = 0;
+  CUDA_TRY(cudaMemcpy(&hit, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hit) return fail(-1, "SLP kernel evaluated on the diagonal");
+  CUDA_TRY(cudaMemcpy(out_host, o.ptr, m1 * m2 * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int64_t htlr_last_launch_count(const htlr_plan* pl) { return pl ? pl->last_launches : -1; }
 
 int htlr_diag_value(htlr_plan* pl, double* out) {

@@ -139,6 +139,24 @@ class QuadratureConfig:
             raise ValueError("quadrature order must be >= 2")
 
 
+def pairwise(k: KernelSpec, xpts: np.ndarray, ypts: np.ndarray) -> np.ndarray:
+    """Kernel values on all pairs, (m1, d) x (m2, d) -> (m1, m2), evaluated on
+    the device with the reference formula (kernels.py:113-117)."""
+    x = np.ascontiguousarray(np.atleast_2d(np.asarray(xpts, dtype=np.float64)))
+    y = np.ascontiguousarray(np.atleast_2d(np.asarray(ypts, dtype=np.float64)))
+    if x.shape[1] != y.shape[1]:
+        raise ValueError("point dimensions differ")
+    out = np.empty((x.shape[0], y.shape[0]))
+    _lib.check(_lib.lib().htlr_kernel_pairs(k.device_code, float(k.sigma or 0.0), float(k.scale), x.shape[1],
+                                            x.ctypes.data, x.shape[0], y.ctypes.data, y.shape[0], out.ctypes.data))
+    return out
+
+
+def evaluate(k: KernelSpec, x, y) -> float:
+    """Kernel value at one point pair (kernels.py:106-110)."""
+    return float(pairwise(k, np.atleast_2d(x), np.atleast_2d(y))[0, 0])
+
+
 def singular_rule(k: KernelSpec, cfg: QuadratureConfig) -> int:
     """1 when the Duffy corner rule applies (kernels.py:263-265)."""
     return int((not k.smooth_at_diagonal) and bool(cfg.corner_subdivision))
