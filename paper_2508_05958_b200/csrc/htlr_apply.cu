@@ -12,6 +12,8 @@
 //                gathered B columns                  (blocks.py:248-250, operators.py:150)
 //   downward     f = Y + a u + sum_l (U x U x U) H_l[anc] per leaf box, written
 //                back in F-order                     (blocks.py:251-259, operators.py:153-156)
+#include <cstdlib>
+
 #include "htlr_kernels.h"
 
 namespace htlr {
@@ -286,7 +288,15 @@ int gemm_mt_for(int P_out) {
   if (gemm_use_persistent() && thin_m8_supported(m8) && P_out != 64) return -8 * m8;
   return P_out <= 64 ? 64 : 128;
 }
-int gemm_nt(int MT) { return 64; }
+int gemm_wide_wn() {
+  static int wn = -1;
+  if (wn < 0) {
+    const char* e = std::getenv("HTLR_GEMM_WN");
+    wn = (e && e[0] == '3') ? 3 : 2;
+  }
+  return wn;
+}
+int gemm_nt(int MT) { return (MT == 128 && gemm_use_persistent()) ? 32 * gemm_wide_wn() : 64; }
 
 template <int WM, int WN, int STAGES>
 static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, double* C,
