@@ -90,7 +90,7 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st);
 int gemm_nt(int MT);
-int gemm_wide_wn();   // warps along N of the wide persistent kernel (HTLR_GEMM_WN=3: 96 columns)
+int gemm_wide_wn();   // warps along N of the wide persistent kernel (default 3: 96 columns; HTLR_GEMM_WN=2: 64)
 // persistent warp-specialised variant (htlr_gemm.cu); HTLR_GEMM=legacy selects
 // the one-CTA-per-item cp.async kernel instead
 bool gemm_use_persistent();
