@@ -132,6 +132,7 @@ struct htlr_plan {
   int near_mats = 0;          // leaf pass: matrices [0, near_mats) are near blocks
   bool merged = false;        // leaf-level admissible cores live in the leaf pass
   DevBuf diag, coeff, gl, ub, Y;
+  DevBuf u_stage, f_stage;   // graph-replay staging vectors
   bool has_coeff = false;
   int ws_R = 0;
   int64_t last_launches = 0;
@@ -324,6 +325,8 @@ int htlr_plan_destroy(htlr_plan* pl) {
   pl->gl.release();
   pl->ub.release();
   pl->Y.release();
+  pl->u_stage.release();
+  pl->f_stage.release();
   delete pl;
   return 0;
 }
@@ -1129,14 +1132,23 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
   if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
   if (pl->graphs) {
     // replay a captured graph of the whole launch sequence (one CPU call
-    // instead of ~10 launches + memsets; matters for the small configs)
+    // instead of ~10 launches + memsets).  The graph reads/writes plan-owned
+    // staging vectors, so it does not depend on the caller's pointers: the
+    // caller's u / f are copied in and out around the replay (2 N R doubles
+    // each way, D2D).
+    const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
+    if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;
+    const double* us = pl->u_stage.d();
+    double* fs = pl->f_stage.d();
     for (auto& g : pl->graph_cache) {
-      if (g.R == cx.R && g.u == u && g.f == f && g.prof == pl->profiling) {
+      if (g.R == cx.R && g.u == us && g.f == fs && g.prof == pl->profiling) {
         pl->prof_kind = g.kind;
         pl->prof_level = g.level;
         pl->prof_flops = g.flops;
         pl->prof_bytes = g.bytes;
+        CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         CUDA_TRY(cudaGraphLaunch(g.exec, cx.st));
+        CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         pl->last_launches = g.launches;
         return 0;
       }
@@ -1146,17 +1158,19 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     cc.st = pl->cap_stream;
     prof_reset(pl);
     CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
-    int rc = mv_local(cc, u);
-    if (!rc) rc = mv_remote(cc, u, f);
+    int rc = mv_local(cc, us);
+    if (!rc) rc = mv_remote(cc, us, fs);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
     cudaGraphExec_t exec = nullptr;
     if (!rc && ce == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
       cudaGraphDestroy(graph);
       if (pl->graph_cache.size() >= 8) drop_graphs(pl);
-      pl->graph_cache.push_back({cx.R, u, f, pl->profiling, exec, pl->prof_kind, pl->prof_level, pl->prof_flops,
+      pl->graph_cache.push_back({cx.R, us, fs, pl->profiling, exec, pl->prof_kind, pl->prof_level, pl->prof_flops,
                                  pl->prof_bytes, cc.launches});
+      CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
       CUDA_TRY(cudaGraphLaunch(exec, cx.st));
+      CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
       pl->last_launches = cc.launches;
       return 0;
     }
