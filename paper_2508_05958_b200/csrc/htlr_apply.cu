@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(WM* WN * 32, 2)
   }
   __syncthreads();
 
-  const double* Ablk = A + (int64_t)tk.mat * mat_stride + (int64_t)rt * MT * K_pad;
-  const int nk = K_pad / KC;
+  const double* Ablk = A + (int64_t)tk.mat * mat_stride + (int64_t)rt * MT * K_pad + (int64_t)tk.kc0 * MT * KC;
+  const int nk = tk.nkc;
   const int tid = threadIdx.x;
 
   auto load_stage = [&](int kc, int st) {
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(WM* WN * 32, 2)
     for (int i = tid; i < NT * KC / 2; i += NTH) {
       int n = i / (KC / 2), c2 = i % (KC / 2);
       int64_t cb = colB[n];
-      const double* g = cb >= 0 ? B + cb + kc * KC + 2 * c2 : B;
+      const double* g = cb >= 0 ? B + cb + (tk.kc0 + kc) * KC + 2 * c2 : B;
       cp_async16(dB + n * BST + 2 * c2, g, cb >= 0 ? 16 : 0);
     }
   };

@@ -78,7 +78,7 @@ __device__ __forceinline__ void mma8x8x4_pair(double& c0, double& c1, double a, 
 }
 
 struct ItemInfo {
-  int mat, pair_begin, pair_count, r0, rt, ncols;
+  int mat, pair_begin, pair_count, r0, rt, ncols, kc0, nkc;
 };
 
 __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, int RT, int R, int Rc, int NT) {
@@ -90,6 +90,8 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
   it.pair_count = tk.pair_count;
   it.r0 = tk.r0;
   it.ncols = (Rc == NT) ? min(NT, R - tk.r0) : tk.pair_count * Rc;
+  it.kc0 = tk.kc0;
+  it.nkc = tk.nkc;
   return it;
 }
 
@@ -121,7 +123,6 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int nk = K_pad / KC;
 
   if (warp == NCW) {
     // ------------------------------------------------------------ producer
@@ -142,7 +143,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       }
       const double* Ablk = A + (int64_t)it.mat * mat_stride + (int64_t)it.rt * MT * K_pad;
       const unsigned bytes = (unsigned)(MT * KC * 8 + it.ncols * KC * 8);
-      for (int kc = 0; kc < nk; ++kc, ++g) {
+      const int kbeg = it.kc0 * kKC / KC, kend = kbeg + it.nkc * kKC / KC;   // stage units
+      for (int kc = kbeg; kc < kend; ++kc, ++g) {
         const int s = g % STAGES;
         if (g >= (uint32_t)STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
         if (lane == 0) {
@@ -188,7 +190,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-    for (int kc = 0; kc < nk; ++kc, ++g) {
+    const int nstage = it.nkc * kKC / KC;
+    for (int kc = 0; kc < nstage; ++kc, ++g) {
       const int s = g % STAGES;
       mbar_wait(&full[s], (g / STAGES) & 1);
       const double* cA = sA + s * MT * KC;
@@ -315,7 +318,6 @@ __global__ void __launch_bounds__(9 * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int nk = K_pad / KC;
   if (warp == NCW) {
     uint32_t g = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -333,7 +335,8 @@ __global__ void __launch_bounds__(9 * 32, 1)
       }
       const double* Ablk = A + (int64_t)it.mat * mat_stride;
       const unsigned bytes = (unsigned)(MP * KC * 8 + it.ncols * KC * 8);
-      for (int kc = 0; kc < nk; ++kc, ++g) {
+      const int kbeg = it.kc0 * kKC / KC, kend = kbeg + it.nkc * kKC / KC;   // stage units
+      for (int kc = kbeg; kc < kend; ++kc, ++g) {
         const int s = g % STAGES;
         if (g >= (uint32_t)STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
         if (lane == 0) {
@@ -369,7 +372,8 @@ __global__ void __launch_bounds__(9 * 32, 1)
     double acc[M8][2];
 #pragma unroll
     for (int i = 0; i < M8; ++i) acc[i][0] = acc[i][1] = 0.0;
-    for (int kc = 0; kc < nk; ++kc, ++g) {
+    const int nstage = it.nkc * kKC / KC;
+    for (int kc = 0; kc < nstage; ++kc, ++g) {
       const int s = g % STAGES;
       mbar_wait(&full[s], (g / STAGES) & 1);
       if (active) {
@@ -414,6 +418,16 @@ static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, 
   const int grid = ntasks < sms ? ntasks : sms;
   gemm_thin_kernel<M8, STAGES><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
                                                             K_pad, M_valid, ldc);
+}
+
+int gemm_stage_chunks(int MT, int K_pad) {
+  if (MT < 0 || MT == 64 || !gemm_use_persistent()) return 1;
+  static int kcs = -1;
+  if (kcs < 0) {
+    const char* e = std::getenv("HTLR_GEMM_KCS");
+    kcs = (e && std::strcmp(e, "32") == 0) ? 32 : 64;
+  }
+  return (gemm_wide_wn() == 2 && kcs == 64 && K_pad % 64 == 0) ? 2 : 1;
 }
 
 int thin_m8_supported(int m8) { return m8 == 5 || m8 == 8 || m8 == 16 || m8 == 27; }

@@ -41,6 +41,8 @@ struct GemmTask {
   int pair_begin;
   int pair_count;
   int r0;
+  int kc0;   // K range of the item in 32-wide chunks: split-K for passes with
+  int nkc;   // too few items to fill the GPU (partial sums meet in the RED epilogue)
 };
 
 // coarse-level contribution gathered by the fused downward kernel
@@ -94,6 +96,7 @@ int gemm_wide_wn();   // warps along N of the wide persistent kernel (default 3:
 // persistent warp-specialised variant (htlr_gemm.cu); HTLR_GEMM=legacy selects
 // the one-CTA-per-item cp.async kernel instead
 bool gemm_use_persistent();
+int gemm_stage_chunks(int MT, int K_pad);   // 32-wide K chunks per pipeline stage
 int thin_m8_supported(int m8);
 void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
                       const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,

@@ -231,15 +231,33 @@ int validate(const htlr_desc& ds, std::string& err) {
   return 0;
 }
 
-int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
+int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
   const int NT = htlr::gemm_nt(ps.MT);
   const int Rc = std::min(R, NT);
   const int npt = std::max(1, NT / Rc);
+  const int nk = ps.K_pad / htlr::kKC;
+  // split K until the pass has ~8 work items per SM (small passes are
+  // otherwise a few waves of long, memory-bound items on part of the GPU)
+  int64_t base = 0;
+  for (int mat = 0; mat < ps.nmats; ++mat) {
+    const int64_t np = ps.seg[mat + 1] - ps.seg[mat];
+    base += ((np + npt - 1) / npt) * ((R + Rc - 1) / Rc);
+  }
+  const int64_t items = base * ps.RT;
+  const int64_t want = 8LL * sms;
+  const int kstep = htlr::gemm_stage_chunks(ps.MT, ps.K_pad);   // split granularity (chunks per stage)
+  int ksplit = 1;
+  while (items * ksplit < want && ksplit * 2 * kstep <= nk) ksplit *= 2;
+  const int nunits = nk / kstep;
   out.clear();
   for (int mat = 0; mat < ps.nmats; ++mat) {
     for (int b = ps.seg[mat]; b < ps.seg[mat + 1]; b += npt) {
       int cnt = std::min(npt, ps.seg[mat + 1] - b);
-      for (int r0 = 0; r0 < R; r0 += Rc) out.push_back({mat, b, cnt, r0});
+      for (int r0 = 0; r0 < R; r0 += Rc)
+        for (int k = 0; k < ksplit; ++k) {
+          const int u0 = (int)((int64_t)k * nunits / ksplit), u1 = (int)((int64_t)(k + 1) * nunits / ksplit);
+          out.push_back({mat, b, cnt, r0, u0 * kstep, (u1 - u0) * kstep});
+        }
     }
   }
   return 0;
@@ -945,7 +963,9 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   for (auto& ps : pl->passes) {
     if (ps.tasks.count(cx.R)) continue;
     std::vector<htlr::GemmTask> tv;
-    make_tasks(ps, cx.R, tv);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
+    make_tasks(ps, cx.R, sms, tv);
     auto& slot = ps.tasks[cx.R];
     if (slot.first.alloc(std::max<size_t>(1, tv.size()) * sizeof(htlr::GemmTask))) return 1;
     if (!tv.empty())
