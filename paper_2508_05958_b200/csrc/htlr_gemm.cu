@@ -98,7 +98,7 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
 }  // namespace
 
 template <int WM, int WN, int STAGES, int KCS>
-__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+__global__ void __maxnreg__(152)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                            double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
                            const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
@@ -126,20 +126,35 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 
   if (warp == NCW) {
     // ------------------------------------------------------------ producer
+    // the next item's task record and gathered-column bases are loaded while
+    // the current item's stages are issued (short items would otherwise
+    // stall the ring on two dependent global loads per item)
     uint32_t g = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-      const ItemInfo it = item_info(tasks, item, RT, R, Rc, NT);
-      // gathered B column bases (two columns per lane)
-      int64_t cb[NT / 32];
+    int item = blockIdx.x;
+    ItemInfo it{};
+    int64_t cb[NT / 32];
+    auto load_cols = [&](const ItemInfo& x, int64_t (&c)[NT / 32]) {
 #pragma unroll
       for (int q = 0; q < NT / 32; ++q) {
         const int n = lane + 32 * q;
-        cb[q] = -1;
-        if (n < it.ncols) {
-          const int j = n / Rc, r = it.r0 + n % Rc;
-          const int2 pr = pairs[it.pair_begin + j];
-          cb[q] = ((int64_t)pr.y * R + r) * K_pad;
+        c[q] = -1;
+        if (n < x.ncols) {
+          const int j = n / Rc, r = x.r0 + n % Rc;
+          c[q] = ((int64_t)pairs[x.pair_begin + j].y * R + r) * K_pad;
         }
+      }
+    };
+    if (item < nitems) {
+      it = item_info(tasks, item, RT, R, Rc, NT);
+      load_cols(it, cb);
+    }
+    for (; item < nitems; item += gridDim.x) {
+      const int nxt = item + gridDim.x;
+      ItemInfo itn{};
+      int64_t cbn[NT / 32];
+      if (nxt < nitems) {
+        itn = item_info(tasks, nxt, RT, R, Rc, NT);
+        load_cols(itn, cbn);
       }
       const double* Ablk = A + (int64_t)it.mat * mat_stride + (int64_t)it.rt * MT * K_pad;
       const unsigned bytes = (unsigned)(MT * KC * 8 + it.ncols * KC * 8);
@@ -158,6 +173,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
           if (cb[q] >= 0) bulk_g2s(sB + s * NT * BST + n * BST, B + cb[q] + kc * KC, KC * 8, &full[s]);
         }
       }
+      it = itn;
+#pragma unroll
+      for (int q = 0; q < NT / 32; ++q) cb[q] = cbn[q];
     }
     return;
   }
@@ -166,8 +184,11 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   const int wm = warp % WM, wn = warp / WM;
   const int g8 = lane >> 2, t = lane & 3;
   uint32_t g = 0;
+  ItemInfo itn{};
+  if (blockIdx.x < nitems) itn = item_info(tasks, blockIdx.x, RT, R, Rc, NT);
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const ItemInfo it = item_info(tasks, item, RT, R, Rc, NT);
+    const ItemInfo it = itn;
+    if (item + (int)gridDim.x < nitems) itn = item_info(tasks, item + gridDim.x, RT, R, Rc, NT);
     const int n_tiles = max(0, min(4, (it.ncols - wn * 32 + 7) >> 3));
     const int row0 = it.rt * MT + wm * 32;
     const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
@@ -320,18 +341,31 @@ __global__ void __launch_bounds__(9 * 32, 1)
   __syncthreads();
   if (warp == NCW) {
     uint32_t g = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-      const ItemInfo it = item_info(tasks, item, 1, R, Rc, NT);
-      int64_t cb[2];
+    int item = blockIdx.x;
+    ItemInfo it{};
+    int64_t cb[2];
+    auto load_cols = [&](const ItemInfo& x, int64_t (&c)[2]) {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int n = lane + 32 * q;
-        cb[q] = -1;
-        if (n < it.ncols) {
-          const int j = n / Rc, r = it.r0 + n % Rc;
-          const int2 pr = pairs[it.pair_begin + j];
-          cb[q] = ((int64_t)pr.y * R + r) * K_pad;
+        c[q] = -1;
+        if (n < x.ncols) {
+          const int j = n / Rc, r = x.r0 + n % Rc;
+          c[q] = ((int64_t)pairs[x.pair_begin + j].y * R + r) * K_pad;
         }
+      }
+    };
+    if (item < nitems) {
+      it = item_info(tasks, item, 1, R, Rc, NT);
+      load_cols(it, cb);
+    }
+    for (; item < nitems; item += gridDim.x) {
+      const int nxt = item + gridDim.x;
+      ItemInfo itn{};
+      int64_t cbn[2];
+      if (nxt < nitems) {
+        itn = item_info(tasks, nxt, 1, R, Rc, NT);
+        load_cols(itn, cbn);
       }
       const double* Ablk = A + (int64_t)it.mat * mat_stride;
       const unsigned bytes = (unsigned)(MP * KC * 8 + it.ncols * KC * 8);
@@ -350,14 +384,20 @@ __global__ void __launch_bounds__(9 * 32, 1)
           if (cb[q] >= 0) bulk_g2s(sB + s * NT * BST + n * BST, B + cb[q] + kc * KC, KC * 8, &full[s]);
         }
       }
+      it = itn;
+      cb[0] = cbn[0];
+      cb[1] = cbn[1];
     }
     return;
   }
   const int g8 = lane >> 2, t = lane & 3;
   const int n0 = warp * 8;
   uint32_t g = 0;
+  ItemInfo itn{};
+  if (blockIdx.x < nitems) itn = item_info(tasks, blockIdx.x, 1, R, Rc, NT);
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const ItemInfo it = item_info(tasks, item, 1, R, Rc, NT);
+    const ItemInfo it = itn;
+    if (item + (int)gridDim.x < nitems) itn = item_info(tasks, item + gridDim.x, 1, R, Rc, NT);
     const bool active = n0 < it.ncols;
     int64_t cbase[2];
 #pragma unroll
