@@ -98,7 +98,7 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
 }  // namespace
 
 template <int WM, int WN, int STAGES, int KCS>
-__global__ void __maxnreg__(152)
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                            double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
                            const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
@@ -194,14 +194,14 @@ __global__ void __maxnreg__(152)
     const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
     // epilogue targets of this thread's 8 columns, fetched now so the pair
     // loads' latency hides under the K loop
-    int64_t cbase[8];
+    int cvec[8];   // target vector index (tgt * R + r) of each of this thread's columns, -1 if empty
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int n = wn * 32 + (q >> 1) * 8 + 2 * t + (q & 1);
-      cbase[q] = -1;
+      cvec[q] = -1;
       if (n < it.ncols) {
         const int j = n / Rc, r = it.r0 + n % Rc;
-        cbase[q] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
+        cvec[q] = pairs[it.pair_begin + j].x * R + r;
       }
     }
     double acc[2][4][4];
@@ -289,9 +289,9 @@ __global__ void __maxnreg__(152)
     for (int ni = 0; ni < 4; ++ni) {
 #pragma unroll
       for (int cix = 0; cix < 2; ++cix) {
-        const int64_t cb = cbase[ni * 2 + cix];
-        if (cb < 0) continue;
-        double* cc = C + cb;
+        const int cv = cvec[ni * 2 + cix];
+        if (cv < 0) continue;
+        double* cc = C + (int64_t)cv * ldc;
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi) {
 #pragma unroll
