@@ -13,6 +13,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -246,8 +247,15 @@ int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
   const int64_t items = base * ps.RT;
   const int64_t want = 8LL * sms;
   const int kstep = htlr::gemm_stage_chunks(ps.MT, ps.K_pad);   // split granularity (chunks per stage)
+  // measured: no gain for the small configs (their items are bound by the
+  // few active consumer warps, not by load balance), so split-K is opt-in
+  static int splitk = -1;
+  if (splitk < 0) {
+    const char* e = std::getenv("HTLR_SPLITK");
+    splitk = (e && e[0] == '1') ? 1 : 0;
+  }
   int ksplit = 1;
-  while (items * ksplit < want && ksplit * 2 * kstep <= nk) ksplit *= 2;
+  while (splitk && items * ksplit < want && ksplit * 2 * kstep <= nk) ksplit *= 2;
   const int nunits = nk / kstep;
   out.clear();
   for (int mat = 0; mat < ps.nmats; ++mat) {
