@@ -312,7 +312,7 @@ static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, 
       A, mat_stride, B, C, tasks, pairs, R, Rc, K_pad, M_valid, ldc, RT);
 }
 
-void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st) {
   if (MT < 0) {
@@ -320,7 +320,7 @@ void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, d
     return;
   }
   if (gemm_use_persistent()) {
-    launch_gemm_persistent(MT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+    launch_gemm_persistent(MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
     return;
   }
   if (MT == 64)

@@ -97,7 +97,7 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
 
 }  // namespace
 
-template <int WM, int WN, int STAGES, int KCS>
+template <int WM, int WN, int STAGES, int KCS, int MI = 2>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                            double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
@@ -106,7 +106,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   // a pipeline stage covers KCS = 32 or 64 of K (one or two tiled 32-chunks,
   // adjacent in the A layout); fewer, larger stages halve the mbarrier
   // round trips per unit of tensor work
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = KCS, BST = KC + 4;
+  // warp tile = MI m16 row tiles x 4 n8 column tiles (MI = 1: "narrow" items
+  // of 32 columns for passes with few pairs per matrix)
+  constexpr int MT = 16 * MI * WM, NT = 32 * WN, KC = KCS, BST = KC + 4;
   constexpr int NCW = WM * WN;   // consumer warps
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;                                  // STAGES x MT*KC
@@ -190,8 +192,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     const ItemInfo it = itn;
     if (item + (int)gridDim.x < nitems) itn = item_info(tasks, item + gridDim.x, RT, R, Rc, NT);
     const int n_tiles = max(0, min(4, (it.ncols - wn * 32 + 7) >> 3));
-    const int row0 = it.rt * MT + wm * 32;
-    const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
+    const int row0 = it.rt * MT + wm * 16 * MI;
+    const int m_tiles = max(0, min(MI, (M_valid - row0 + 15) >> 4));
     // epilogue targets of this thread's 8 columns, fetched now so the pair
     // loads' latency hides under the K loop
     int cvec[8];   // target vector index (tgt * R + r) of each of this thread's columns, -1 if empty
@@ -204,9 +206,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         cvec[q] = pairs[it.pair_begin + j].x * R + r;
       }
     }
-    double acc[2][4][4];
+    double acc[MI][4][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -217,18 +219,18 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       mbar_wait(&full[s], (g / STAGES) & 1);
       const double* cA = sA + s * MT * KC;
       const double* cB = sB + s * NT * BST;
-      if (n_tiles == 4 && m_tiles == 2) {
+      if (n_tiles == 4 && m_tiles == MI) {
         // full tile: explicit m8n8k4 issue order -- the k0..3 products of all
         // 16 (m8, n8) accumulators first, then the k4..7 products, so every
         // dependent DMMA pair is 16 instructions apart (mma.m16n8k8 would
         // emit each dependent pair back to back)
 #pragma unroll
         for (int ks = 0; ks < KC / 8; ++ks) {
-          double a[2][4];
+          double a[MI][4];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
+          for (int mi = 0; mi < MI; ++mi) {
             const double2* pa = reinterpret_cast<const double2*>(
-                cA + (ks >> 2) * (MT * kKC) + ((wm * 2 + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
+                cA + (ks >> 2) * (MT * kKC) + ((wm * MI + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
             const double2 v0 = pa[0], v1 = pa[1];
             a[mi][0] = v0.x;
             a[mi][1] = v0.y;
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
+            for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
               for (int ni = 0; ni < 4; ++ni) {
                 mma8x8x4_pair(acc[mi][ni][0], acc[mi][ni][1], a[mi][2 * h], b[ni][h]);
@@ -255,11 +257,11 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       } else if (n_tiles > 0 && m_tiles > 0) {
 #pragma unroll
         for (int ks = 0; ks < KC / 8; ++ks) {
-          double a[2][4];
+          double a[MI][4];
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
+          for (int mi = 0; mi < MI; ++mi) {
             const double2* pa = reinterpret_cast<const double2*>(
-                cA + (ks >> 2) * (MT * kKC) + ((wm * 2 + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
+                cA + (ks >> 2) * (MT * kKC) + ((wm * MI + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
             const double2 v0 = pa[0], v1 = pa[1];
             a[mi][0] = v0.x;
             a[mi][1] = v0.y;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
             b[ni][1] = pb[4];
           }
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
+          for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni)
               if (mi < m_tiles && ni < n_tiles) mma16x8x8(acc[mi][ni], a[mi], b[ni]);
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         if (cv < 0) continue;
         double* cc = C + (int64_t)cv * ldc;
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
+        for (int mi = 0; mi < MI; ++mi) {
 #pragma unroll
           for (int hi = 0; hi < 2; ++hi) {
             const int m = row0 + mi * 16 + g8 + 8 * hi;
@@ -493,13 +495,13 @@ bool gemm_use_persistent() {
   return mode == 1;
 }
 
-template <int WM, int WN, int STAGES, int KCS>
+template <int WM, int WN, int STAGES, int KCS, int MI = 2>
 static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
                                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                                 int M_valid, int ldc, int RT, cudaStream_t st) {
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = KCS;
+  constexpr int MT = 16 * MI * WM, NT = 32 * WN, KC = KCS;
   const size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES, KCS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES, KCS, MI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const int nitems = ntasks * RT;
   if (nitems == 0) return;
@@ -507,13 +509,18 @@ static void launch_persistent_t(const double* A, int64_t mat_stride, const doubl
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = nitems < sms ? nitems : sms;
-  gemm_persistent_kernel<WM, WN, STAGES, KCS><<<grid, (WM * WN + 1) * 32, smem, st>>>(
+  gemm_persistent_kernel<WM, WN, STAGES, KCS, MI><<<grid, (WM * WN + 1) * 32, smem, st>>>(
       A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid, ldc, RT);
 }
 
-void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st) {
+  if (MT == 128 && NT == 32) {   // narrow items: 8 warps x (16 rows x 32 columns)
+    launch_persistent_t<8, 1, 4, 32, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
+                                        st);
+    return;
+  }
   static int kcs = -1;
   if (kcs < 0) {
     const char* e = std::getenv("HTLR_GEMM_KCS");

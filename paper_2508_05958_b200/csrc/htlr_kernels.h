@@ -88,7 +88,7 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
-void launch_gemm(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st);
 int gemm_nt(int MT);
@@ -101,7 +101,7 @@ int thin_m8_supported(int m8);
 void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
                       const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,
                       int ldc, cudaStream_t st);
-void launch_gemm_persistent(int MT, const double* A, int64_t mat_stride, const double* B, double* C,
+void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st);
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,

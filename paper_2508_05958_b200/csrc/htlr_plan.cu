@@ -82,6 +82,7 @@ struct Pass {
   std::vector<int2> pairs_host;
   int npairs = 0;
   std::map<int, std::pair<DevBuf, int>> tasks;   // per R
+  std::map<int, int> task_nt;                     // columns per item of the R slot's tasks
   bool from_ub = false;    // B operand = leaf-box-major u (else W of `level`)
   bool to_y = false;       // C accumulator = Y (else H of `level`)
 };
@@ -232,8 +233,28 @@ int validate(const htlr_desc& ds, std::string& err) {
   return 0;
 }
 
-int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
+// Columns per work item.  The wide 128-row kernel takes 96 columns; a pass
+// whose matrices have few (pair, rhs) columns each (the near-field of small
+// grids, the coarse far-field levels) would leave two of its three column
+// warp groups idle, so it gets the narrow 32-column variant instead, whose
+// eight warps all work on the one 32-column slab.  HTLR_GEMM_NARROW=0/1
+// forces the choice for A/B runs.
+int choose_nt(const Pass& ps, int R) {
   const int NT = htlr::gemm_nt(ps.MT);
+  if (ps.MT != 128 || NT != 96) return NT;
+  static int force = -2;
+  if (force == -2) {
+    const char* e = std::getenv("HTLR_GEMM_NARROW");
+    force = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : -1;
+  }
+  if (force >= 0) return force ? 32 : NT;
+  const double cols = (double)ps.npairs / std::max(1, ps.nmats) * std::min(R, NT);
+  return cols < 48.0 ? 32 : NT;
+}
+
+int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
+  const int NT = choose_nt(ps, R);
+  ps.task_nt[R] = NT;
   const int Rc = std::min(R, NT);
   const int npt = std::max(1, NT / Rc);
   const int nk = ps.K_pad / htlr::kKC;
@@ -1113,7 +1134,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
     Pass& ps = pl->passes[i];
     auto& slot = ps.tasks[R];
     if (slot.second == 0) continue;
-    const int NT = htlr::gemm_nt(ps.MT);
+    const int NT = ps.task_nt[R];
     const int Rc = std::min(R, NT);
     const double* B = ps.from_ub ? cx.ub : cx.W[i];
     double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
@@ -1121,7 +1142,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
     double flops = 2.0 * (double)ps.P * ps.P * (double)ps.npairs * R;
     double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ps.npairs;
     if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
-    htlr::launch_gemm(ps.MT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
+    htlr::launch_gemm(ps.MT, NT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
                       slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st);
     if (cx.prof_end()) return 1;
   }
