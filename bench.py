@@ -283,6 +283,58 @@ def fp64_peak() -> float:
     return best or 37.0
 
 
+def fp64_dfma_peak() -> float:
+    try:
+        with open(FP64_PEAK_FILE) as fh:
+            for ln in fh:
+                rec = json.loads(ln)
+                if rec.get("probe") == "dfma":
+                    return float(rec["tflops"])
+    except OSError:
+        pass
+    return 34.0
+
+
+def hbm_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except (OSError, ValueError, KeyError):
+        return 7700.0, "B200_PROFILING.md fallback"
+
+
+PHASE_KERNELS = {
+    "gemm_leaf": "gemm_persistent_kernel / gemm_thin_kernel (near + leaf-level cores, fp64 DMMA)",
+    "gemm_level": "gemm_persistent_kernel / gemm_thin_kernel (coupling cores, fp64 DMMA)",
+    "regen_level": "regen_sym_kernel (cores regenerated + contracted, fp64 CUDA cores)",
+    "regen_near": "regen_sym_kernel (near blocks regenerated, fp64 CUDA cores)",
+    "upward": "upward_kernel", "downward": "downward_kernel", "permute": "permute_in_kernel",
+}
+
+
+def phase_roofline(key: str, flops: float, nbytes: float, ms: float) -> dict:
+    """Roofline of one phase's launch: the binding resource is the larger of
+    the compute time at the fp64 peak of the pipe the kernel runs on (DMMA
+    tensor pipe for the GEMMs, DFMA for the regeneration kernels) and the
+    algorithmic bytes at the measured HBM copy bandwidth."""
+    phase = key.rsplit("_L", 1)[0]
+    core = phase.startswith("regen")
+    tf = fp64_dfma_peak() if core else fp64_peak()
+    bw, bw_src = hbm_peak_gbs()
+    t_flop = flops / (tf * 1e12)
+    t_mem = nbytes / (bw * 1e9)
+    if t_mem > t_flop:
+        ach = nbytes / (ms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": bw, "unit": "GB/s", "frac": ach / bw,
+                "kernel": f"{PHASE_KERNELS.get(phase, phase)} [{key}]", "peak_source": bw_src}
+    ach = flops / (ms / 1e3) / 1e12
+    src = ("fp64 DFMA, own microbenchmark (profiles/fp64_peak_r01.jsonl)" if core else
+           "fp64 DMMA m16n8k8 sustained, own microbenchmark (profiles/fp64_peak_r01.jsonl)")
+    return {"bound": "fp64_core" if core else "tensor", "achieved": ach, "peak": tf, "unit": "TFLOP/s",
+            "frac": ach / tf, "kernel": f"{PHASE_KERNELS.get(phase, phase)} [{key}]",
+            "peak_source": src + "; MEASURED_PEAKS.json has no fp64 entry"}
+
+
 def ncu_traffic(workload: str):
     try:
         with open(NCU_TRAFFIC_FILE) as fh:
@@ -391,16 +443,15 @@ def run_b200(args):
     dom = phases[dom_key]
     avg_ms = dom["ms"] / dom["launches"]
     flops_per_launch = dom["flops"] / dom["launches"]
+    bytes_per_launch = dom["bytes"] / dom["launches"]
     peak = fp64_peak()
-    achieved = flops_per_launch / (avg_ms / 1e3) / 1e12
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.workload), "kernel": f"gemm_gather_kernel ({dom_key})",
-                "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
-                "share_of_step": dom["ms"] / sum(prof_step_ms),
-                "measured": "CUDA events around every launch, on the launching stream, over K profiled steps "
-                            "run right after the K timed steps",
-                "peak_source": "fp64 DMMA m16n8k8 sustained, own microbenchmark (profiles/fp64_peak_r01.jsonl); "
-                               "MEASURED_PEAKS.json has no fp64 entry"}
+    roofline = phase_roofline(dom_key, flops_per_launch, bytes_per_launch, avg_ms)
+    roofline.update({
+        "traffic": ncu_traffic(args.workload), "algorithmic_flops_per_launch": flops_per_launch,
+        "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+        "share_of_step": dom["ms"] / sum(prof_step_ms),
+        "measured": "CUDA events around every launch, on the launching stream, over K profiled steps "
+                    "run right after the K timed steps"})
     total_flops = sum(p["flops"] for p in phases.values()) / args.steps
     whole = {"flops_per_step": total_flops, "tflops": total_flops / (ms_per_step / 1e3) / 1e12,
              "frac_of_fp64_peak": total_flops / (ms_per_step / 1e3) / 1e12 / peak}

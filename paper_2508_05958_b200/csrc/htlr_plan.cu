@@ -99,6 +99,20 @@ int64_t pack_offset(const int* tc, const int* sc, int d, int m) {
   return key;
 }
 
+// Upper half (sigma > tau) of a symmetric block list, rows in decreasing
+// work order (longest first) for the symmetric regeneration kernel.
+struct SymList {
+  bool on = false;
+  int64_t nrows = 0;
+  DevBuf uptr, ucols, order;
+  void release() {
+    uptr.release();
+    ucols.release();
+    order.release();
+    on = false;
+  }
+};
+
 struct Level {
   int level = 0, side = 0, m = 0;
   int64_t nclusters = 0;
@@ -113,6 +127,7 @@ struct Level {
   std::vector<int64_t> csr_ptr;
   std::vector<int> csr_cols;
   DevBuf d_ptr, d_cols;
+  SymList sym;             // sources sigma > tau for the symmetric regeneration
 };
 
 }  // namespace
@@ -150,6 +165,8 @@ struct htlr_plan {
   std::vector<int64_t> near_ptr;
   std::vector<int> near_cols;
   DevBuf d_near_ptr, d_near_cols;
+  SymList near_sym;                        // symmetric near field: upper pairs ...
+  DevBuf d_self_ptr, d_self_cols, Vn;      // ... + the self pairs (one-sided kernel), w * u
   // sharding by cluster subtrees (multi-GPU): this plan computes the f rows
   // of leaf boxes [own_lo[L], own_hi[L]) and the upward data of its own
   // source clusters; every level's own range is a contiguous Morton range
@@ -355,6 +372,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
     lv.WLm.release();
     lv.d_ptr.release();
     lv.d_cols.release();
+    lv.sym.release();
   }
   pl->d_mb.release();
   pl->d_mx.release();
@@ -362,6 +380,10 @@ int htlr_plan_destroy(htlr_plan* pl) {
   pl->dvec.release();
   pl->d_near_ptr.release();
   pl->d_near_cols.release();
+  pl->near_sym.release();
+  pl->d_self_ptr.release();
+  pl->d_self_cols.release();
+  pl->Vn.release();
   for (auto& ps : pl->passes) {
     ps.table.release();
     ps.pairs.release();
@@ -701,6 +723,53 @@ static int upload(DevBuf& buf, const void* src, size_t bytes) {
   return 0;
 }
 
+// Symmetric upper list of a full (unsharded) CSR: nullptr-free when the list
+// is not symmetric (then the one-sided kernels stay in use).  Self pairs are
+// returned separately (near field only).
+static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& cols, SymList& out,
+                     std::vector<int64_t>* self_ptr, std::vector<int>* self_cols) {
+  out.release();
+  const int64_t nrows = (int64_t)ptr.size() - 1;
+  std::vector<int64_t> up(nrows + 1, 0);
+  std::vector<int> uc;
+  if (self_ptr) self_ptr->assign(nrows + 1, 0);
+  if (self_cols) self_cols->clear();
+  for (int64_t t = 0; t < nrows; ++t) {
+    for (int64_t e = ptr[t]; e < ptr[t + 1]; ++e) {
+      const int sg = cols[e];
+      // symmetry: tau must appear in sigma's (sorted) list
+      if (sg < 0 || sg >= nrows) return 0;
+      if (!std::binary_search(cols.begin() + ptr[sg], cols.begin() + ptr[sg + 1], (int)t)) return 0;
+      if (sg > t) uc.push_back(sg);
+      if (sg == t) {
+        if (!self_cols) return 0;
+        self_cols->push_back(sg);
+      }
+    }
+    up[t + 1] = (int64_t)uc.size();
+    if (self_ptr) (*self_ptr)[t + 1] = (int64_t)self_cols->size();
+  }
+  std::vector<int> order(nrows);
+  for (int64_t t = 0; t < nrows; ++t) order[t] = (int)t;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return up[a + 1] - up[a] > up[b + 1] - up[b]; });
+  if (upload(out.uptr, up.data(), up.size() * sizeof(int64_t))) return 1;
+  if (upload(out.ucols, uc.data(), std::max<size_t>(1, uc.size()) * sizeof(int))) return 1;
+  if (upload(out.order, order.data(), order.size() * sizeof(int))) return 1;
+  out.nrows = nrows;
+  out.on = true;
+  return 0;
+}
+
+static bool regen_sym_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("HTLR_REGEN_SYM");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // Mapped grid construction: geometry tables, per (level, interval) nodes and
 // raw factors, per-point diagonal cell integrals, CSR lists of own targets.
 static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
@@ -725,6 +794,22 @@ static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
   }
   if (upload(pl->d_near_ptr, pl->near_ptr.data(), pl->near_ptr.size() * sizeof(int64_t))) return 1;
   if (upload(pl->d_near_cols, pl->near_cols.data(), pl->near_cols.size() * sizeof(int))) return 1;
+  // symmetric regeneration (single shard: the column sums land in rows of
+  // every cluster, so a sharded plan keeps the one-sided kernels)
+  if (pl->shard_world == 1 && regen_sym_enabled()) {
+    for (auto& lv : pl->levels)
+      if (lv.needs_up && htlr::regen_sym_supported(d, p))
+        if (build_sym(lv.csr_ptr, lv.csr_cols, lv.sym, nullptr, nullptr)) return 1;
+    if (htlr::regen_sym_supported(d, pl->sL)) {
+      std::vector<int64_t> sp;
+      std::vector<int> sc;
+      if (build_sym(pl->near_ptr, pl->near_cols, pl->near_sym, &sp, &sc)) return 1;
+      if (pl->near_sym.on) {
+        if (upload(pl->d_self_ptr, sp.data(), sp.size() * sizeof(int64_t))) return 1;
+        if (upload(pl->d_self_cols, sc.data(), std::max<size_t>(1, sc.size()) * sizeof(int))) return 1;
+      }
+    }
+  }
   DevBuf djobs;
   if (!jobs.empty()) {
     if (upload(djobs, jobs.data(), jobs.size() * sizeof(htlr::MappedFactorJob))) return 1;
@@ -915,6 +1000,7 @@ static int ensure_workspace(htlr_plan* pl, int R) {
     const int64_t nleaf = pl->levels[pl->L].nclusters;
     if (pl->ub.alloc((size_t)nleaf * R * PL * sizeof(double))) return 1;
     if (pl->Y.alloc((size_t)nleaf * R * PL * sizeof(double))) return 1;
+    if (pl->near_sym.on && pl->Vn.alloc((size_t)nleaf * PL * sizeof(double))) return 1;
     for (auto& lv : pl->levels) {
       if (!lv.needs_up) continue;
       if (lv.W.alloc((size_t)lv.nclusters * R * P * sizeof(double))) return 1;
@@ -1062,9 +1148,18 @@ int mv_remote_mapped(MvCtx& cx, const double* u, double* f) {
     if (!lv.needs_up) continue;
     const int64_t t0 = pl->own_lo[lv.level], nt = pl->own_hi[lv.level] - t0;
     const double npair = (double)lv.csr_cols.size();
-    if (cx.prof_begin(5, lv.level, npair * P * P * (10.0 + 2.0 * R), R8 * npair * P)) return 1;
-    htlr::launch_regen_adm(pl->kp, d, p, lv.level, lv.nodes.d(), (const int64_t*)lv.d_ptr.ptr,
-                           (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, lv.H.d(), R, cx.st);
+    // symmetric regeneration: one 10-flop evaluation per unordered pair
+    const double evals = (lv.sym.on && R == 1) ? 0.5 : 1.0;
+    if (cx.prof_begin(5, lv.level, npair * P * P * (10.0 * evals + 2.0 * R), R8 * npair * P)) return 1;
+    if (lv.sym.on && R == 1) {
+      CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * P * sizeof(double), cx.st));
+      htlr::launch_regen_sym(pl->kp, p, lv.level, lv.nodes.d(), (const int*)lv.sym.order.ptr, lv.sym.nrows,
+                             (const int64_t*)lv.sym.uptr.ptr, (const int*)lv.sym.ucols.ptr, cx.Wl[lv.level], P,
+                             lv.H.d(), P, cx.st);
+    } else {
+      htlr::launch_regen_adm(pl->kp, d, p, lv.level, lv.nodes.d(), (const int64_t*)lv.d_ptr.ptr,
+                             (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, lv.H.d(), R, cx.st);
+    }
     if (cx.prof_end()) return 1;
     if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
     dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), lv.H.d(), (int64_t)lv.side * p, nullptr};
@@ -1074,9 +1169,22 @@ int mv_remote_mapped(MvCtx& cx, const double* u, double* f) {
   const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   {
     const double npair = (double)pl->near_cols.size();
-    if (cx.prof_begin(6, pl->L, npair * PL * PL * (10.0 + 2.0 * R), R8 * npair * PL)) return 1;
-    htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(), (const int64_t*)pl->d_near_ptr.ptr,
-                            (const int*)pl->d_near_cols.ptr, b0, nb, cx.ub, PL, pl->Y.d(), R, cx.st);
+    const double evals = (pl->near_sym.on && R == 1) ? 0.5 : 1.0;
+    if (cx.prof_begin(6, pl->L, npair * PL * PL * (10.0 * evals + 2.0 * R), R8 * npair * PL)) return 1;
+    if (pl->near_sym.on && R == 1) {
+      // self pairs first (plain stores initialise Y), then the upper pairs
+      htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(),
+                              (const int64_t*)pl->d_self_ptr.ptr, (const int*)pl->d_self_cols.ptr, b0, nb, cx.ub,
+                              PL, pl->Y.d(), R, cx.st);
+      htlr::launch_near_weight(pl->sL, pl->L, pl->d_mc.d(), cx.ub, PL, pl->Vn.d(), nb, cx.st);
+      htlr::launch_regen_sym(pl->kp, pl->sL, pl->L, pl->d_mx.d(), (const int*)pl->near_sym.order.ptr,
+                             pl->near_sym.nrows, (const int64_t*)pl->near_sym.uptr.ptr,
+                             (const int*)pl->near_sym.ucols.ptr, pl->Vn.d(), PL, pl->Y.d(), PL, cx.st);
+    } else {
+      htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(),
+                              (const int64_t*)pl->d_near_ptr.ptr, (const int*)pl->d_near_cols.ptr, b0, nb, cx.ub,
+                              PL, pl->Y.d(), R, cx.st);
+    }
     if (cx.prof_end()) return 1;
   }
   const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;

@@ -39,6 +39,7 @@ CASES = [
     (3, 24, 6, 6, O.Kernel("slp3d", scale=4 * np.pi), H.inv_r_3d(), 0.0, 1),
     (3, 16, 4, 4, O.Kernel("gaussian", sigma=0.2), H.gaussian(0.2), 0.5, 2),
     (2, 32, 8, 6, O.Kernel("slp2d", scale=2 * np.pi), H.neg_log_2d(), 1.0, 3),
+    (3, 32, 4, 4, O.Kernel("gaussian", sigma=0.3), H.gaussian(0.3), 0.0, 1),
 ]
 
 
@@ -112,3 +113,30 @@ def test_cfg5_runs_and_is_symmetric():
     fr = H.matvec(op, v[::-1, ::-1, ::-1].ravel(order="F")).reshape((n,) * 3, order="F")
     assert np.all(np.isfinite(f))
     assert rel(fr[::-1, ::-1, ::-1], f) <= 1e-11
+
+
+_SYM_SCRIPT = """
+import sys, numpy as np
+import paper_2508_05958_b200 as H
+cfg = H.BuildConfig(rank=6, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
+                    coeff=H.CoefficientFn.constant(0.0))
+op = H.construct(cfg, H.MappedGrid(3, 48, 0.05))
+u = np.random.default_rng(11).standard_normal(48 ** 3)
+np.save(sys.argv[1], H.matvec(op, u))
+"""
+
+
+def test_symmetric_regeneration_equals_one_sided(tmp_path):
+    """The symmetric regeneration (one kernel evaluation per unordered pair,
+    htlr_regen_sym.cu) against the one-sided kernels (HTLR_REGEN_SYM=0) on a
+    4-level mapped tree with leaf side 6: equal up to fp64 summation order."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = tmp_path / f"f{flag}.npy"
+        subprocess.run([sys.executable, "-c", _SYM_SCRIPT, str(out)], check=True, cwd=root,
+                       env={**os.environ, "PYTHONPATH": root, "HTLR_REGEN_SYM": flag}, timeout=600)
+        outs.append(np.load(out))
+    assert rel(outs[0], outs[1]) <= 1e-13
