@@ -316,7 +316,7 @@ void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const doub
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st) {
   if (MT < 0) {
-    launch_gemm_thin(-MT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+    launch_gemm_thin(-MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
     return;
   }
   if (gemm_use_persistent()) {

@@ -321,12 +321,17 @@ __device__ __forceinline__ void mma8x8x4(double (&c)[2], double a, double b) {
 // units keep every SM sub-partition equally busy for P = 216, which the
 // 128-row tiles of the wide kernel cannot (216 = 128 + 88).
 // ---------------------------------------------------------------------------
-template <int M8, int STAGES>
+template <int M8, int STAGES, int CW>
 __global__ void __launch_bounds__(9 * 32, 1)
     gemm_thin_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                      double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
                      const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc) {
-  constexpr int MP = 8 * M8, NT = 64, KC = kKC, BST = KC + 4, NCW = 8;
+  // CW column warps x (8 / CW) row warps: CW = 8 gives each warp 8 columns
+  // and all M8 row tiles (64 columns per item); CW = 2 / 1 (16 / 8 columns
+  // per item, for passes with few pairs per matrix) split the row tiles
+  // round-robin over 4 / 8 warps so every warp has work
+  constexpr int MP = 8 * M8, NT = 8 * CW, KC = kKC, BST = KC + 4, NCW = 8;
+  constexpr int RG = 8 / CW, MJ = (M8 + RG - 1) / RG;
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;                      // STAGES x MP*KC
   double* sB = smem + STAGES * MP * KC;   // STAGES x NT*BST
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
       for (int q = 0; q < 2; ++q) {
         const int n = lane + 32 * q;
         c[q] = -1;
-        if (n < x.ncols) {
+        if (n < x.ncols && n < NT) {
           const int j = n / Rc, r = x.r0 + n % Rc;
           c[q] = ((int64_t)pairs[x.pair_begin + j].y * R + r) * K_pad;
         }
@@ -364,7 +369,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     for (; item < nitems; item += gridDim.x) {
       const int nxt = item + gridDim.x;
       ItemInfo itn{};
-      int64_t cbn[2];
+      int64_t cbn[2] = {-1, -1};
       if (nxt < nitems) {
         itn = item_info(tasks, nxt, 1, R, Rc, NT);
         load_cols(itn, cbn);
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     return;
   }
   const int g8 = lane >> 2, t = lane & 3;
-  const int n0 = warp * 8;
+  const int n0 = (warp % CW) * 8, rw = warp / CW;
   uint32_t g = 0;
   ItemInfo itn{};
   if (blockIdx.x < nitems) itn = item_info(tasks, blockIdx.x, 1, R, Rc, NT);
@@ -411,9 +416,9 @@ __global__ void __launch_bounds__(9 * 32, 1)
         cbase[cix] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
       }
     }
-    double acc[M8][2];
+    double acc[MJ][2];
 #pragma unroll
-    for (int i = 0; i < M8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int i = 0; i < MJ; ++i) acc[i][0] = acc[i][1] = 0.0;
     const int nstage = it.nkc * kKC / KC;
     for (int kc = 0; kc < nstage; ++kc, ++g) {
       const int s = g % STAGES;
@@ -426,7 +431,8 @@ __global__ void __launch_bounds__(9 * 32, 1)
           const double b = cB[k4 * 4];
           const double* pa = cA + k4 * (M8 * 32) + lane;
 #pragma unroll
-          for (int i = 0; i < M8; ++i) mma8x8x4(acc[i], pa[i * 32], b);
+          for (int i = 0; i < MJ; ++i)
+            if (rw + RG * i < M8) mma8x8x4(acc[i], pa[(rw + RG * i) * 32], b);
         }
       }
       __syncwarp();
@@ -438,27 +444,28 @@ __global__ void __launch_bounds__(9 * 32, 1)
       if (cbase[cix] < 0) continue;
       double* cc = C + cbase[cix];
 #pragma unroll
-      for (int i = 0; i < M8; ++i) {
-        const int m = i * 8 + g8;
-        if (m < M_valid) atomicAdd(cc + m, acc[i][cix]);
+      for (int i = 0; i < MJ; ++i) {
+        const int m = (rw + RG * i) * 8 + g8;
+        if (rw + RG * i < M8 && m < M_valid) atomicAdd(cc + m, acc[i][cix]);
       }
     }
   }
 }
 
-template <int M8, int STAGES>
+template <int M8, int STAGES, int CW>
 static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, double* C, const GemmTask* tasks,
                           int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
                           cudaStream_t st) {
   constexpr int MP = 8 * M8, KC = kKC;
-  const size_t smem = sizeof(double) * STAGES * (size_t)(MP * KC + 64 * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem =
+      sizeof(double) * STAGES * (size_t)(MP * KC + 8 * CW * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
+  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (ntasks == 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = ntasks < sms ? ntasks : sms;
-  gemm_thin_kernel<M8, STAGES><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
+  gemm_thin_kernel<M8, STAGES, CW><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
                                                             K_pad, M_valid, ldc);
 }
 
@@ -474,14 +481,30 @@ int gemm_stage_chunks(int MT, int K_pad) {
 
 int thin_m8_supported(int m8) { return m8 == 5 || m8 == 8 || m8 == 16 || m8 == 27; }
 
-void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
+template <int M8, int STAGES>
+static void launch_thin_cw(int NT, const double* A, int64_t mat_stride, const double* B, double* C,
+                           const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
+                           int M_valid, int ldc, cudaStream_t st) {
+  if (NT == 8)
+    launch_thin_t<M8, STAGES, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+  else if (NT == 16)
+    launch_thin_t<M8, STAGES, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+  else
+    launch_thin_t<M8, STAGES, 8>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+}
+
+void launch_gemm_thin(int M_pad, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                       const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,
                       int ldc, cudaStream_t st) {
   switch (M_pad / 8) {
-    case 5: launch_thin_t<5, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
-    case 8: launch_thin_t<8, 4>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
-    case 16: launch_thin_t<16, 3>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
-    case 27: launch_thin_t<27, 3>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 5: launch_thin_cw<5, 4>(NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 8: launch_thin_cw<8, 4>(NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st); break;
+    case 16:
+      launch_thin_cw<16, 3>(NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+      break;
+    case 27:
+      launch_thin_cw<27, 3>(NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+      break;
     default: break;   // not reachable: gemm_mt_for only selects supported sizes
   }
 }

@@ -98,7 +98,7 @@ int gemm_wide_wn();   // warps along N of the wide persistent kernel (default 3:
 bool gemm_use_persistent();
 int gemm_stage_chunks(int MT, int K_pad);   // 32-wide K chunks per pipeline stage
 int thin_m8_supported(int m8);
-void launch_gemm_thin(int M_pad, const double* A, int64_t mat_stride, const double* B, double* C,
+void launch_gemm_thin(int M_pad, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                       const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid,
                       int ldc, cudaStream_t st);
 void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,

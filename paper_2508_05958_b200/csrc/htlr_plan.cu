@@ -258,14 +258,21 @@ int validate(const htlr_desc& ds, std::string& err) {
 // forces the choice for A/B runs.
 int choose_nt(const Pass& ps, int R) {
   const int NT = htlr::gemm_nt(ps.MT);
-  if (ps.MT != 128 || NT != 96) return NT;
   static int force = -2;
   if (force == -2) {
     const char* e = std::getenv("HTLR_GEMM_NARROW");
     force = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : -1;
   }
-  if (force >= 0) return force ? 32 : NT;
   const double cols = (double)ps.npairs / std::max(1, ps.nmats) * std::min(R, NT);
+  if (ps.MT < 0 && htlr::gemm_use_persistent()) {
+    // thin passes: 8 or 16 columns per item when the matrices have few
+    // pairs each (all 8 warps then split the rows of one or two n8 tiles)
+    if (force == 0) return NT;
+    if (force == 1 || cols <= 8.0) return 8;
+    return cols <= 16.0 ? 16 : NT;
+  }
+  if (ps.MT != 128 || NT != 96) return NT;
+  if (force >= 0) return force ? 32 : NT;
   return cols < 48.0 ? 32 : NT;
 }
 

@@ -95,29 +95,31 @@ _VARIANT_SCRIPT = """
 import sys, numpy as np, warnings
 import paper_2508_05958_b200 as H
 warnings.simplefilter("ignore")
-cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
-                    coeff=H.CoefficientFn.constant(0.0))
+cfg = H.BuildConfig(rank=int(sys.argv[2]), leaf_side=8, rule=H.AdmissibilityRule.strong(1.0),
+                    kernel=H.inv_r_3d(), coeff=H.CoefficientFn.constant(0.0))
 op = H.construct(cfg, H.UniformGrid(3, 64))
 U = np.random.default_rng(7).standard_normal((64 ** 3, 2))
 np.save(sys.argv[1], H.matmat(op, U))
 """
 
 
+@pytest.mark.parametrize("rank", [8, 6])
 @pytest.mark.parametrize("env", [{"HTLR_GEMM_NARROW": "0"}, {"HTLR_GEMM_NARROW": "1"},
                                  {"HTLR_GEMM_WN": "2"}, {"HTLR_GEMM": "legacy"}])
-def test_gemm_variants_match_oracle(tmp_path, env):
-    """Every persistent-GEMM variant (wide 96/64-column, narrow 32-column,
-    legacy per-task blocks), forced per process, against the oracle on a
-    cfg-2-shaped problem with two right-hand sides."""
+def test_gemm_variants_match_oracle(tmp_path, env, rank):
+    """Every GEMM variant, forced per process, against the oracle with two
+    right-hand sides: wide 96/64-column and narrow 32-column persistent items
+    (P = 512), thin 64/8-column items (p = 6: P = 216 coupling passes), and
+    the legacy per-task blocks."""
     import os
     import subprocess
     import sys
     out = tmp_path / "f.npy"
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(out)], check=True, cwd=root,
+    subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, str(out), str(rank)], check=True, cwd=root,
                    env={**os.environ, "PYTHONPATH": root, **env}, timeout=600)
     F = np.load(out)
-    pb = O.Problem(d=3, n=64, rank=8, leaf_side_max=8, kernel=O.Kernel("slp3d", scale=4 * np.pi),
+    pb = O.Problem(d=3, n=64, rank=rank, leaf_side_max=8, kernel=O.Kernel("slp3d", scale=4 * np.pi),
                    coeff=O.constant_coeff(0.0))
     U = np.random.default_rng(7).standard_normal((64 ** 3, 2))
     boxes = [((0, 8), (0, 8), (0, 8)), ((24, 32), (40, 48), (56, 64))]
