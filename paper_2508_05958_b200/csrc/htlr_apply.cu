@@ -12,6 +12,7 @@
 //                gathered B columns                  (blocks.py:248-250, operators.py:150)
 //   downward     f = Y + a u + sum_l (U x U x U) H_l[anc] per leaf box, written
 //                back in F-order                     (blocks.py:251-259, operators.py:153-156)
+#include <algorithm>
 #include <cstdlib>
 
 #include "htlr_kernels.h"
@@ -48,11 +49,76 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
 }
 
 // ---------------------------------------------------------------------------
-// upward pass: one CTA per (cluster, rhs); mode 1 (x), then 2 (y), with the
-// mode-3 (z) product accumulated slab by slab, so shared memory holds only
-// p*s + p^2 + p^3 values whatever the box side.
+// upward pass: one CTA per (cluster, rhs); the three mode products run as
+// three whole-box phases (every global load of the box is issued in phase 1,
+// so the CTA pays one memory latency, not one per slab):
+//   T1[a1, y, z] = sum_x Qx[x][a1] u[x, y, z]
+//   T2[a1, a2, z] = sum_y Qy[y][a2] T1[a1, y, z]
+//   W[a1, a2, a3] = sum_z Qz[z][a3] T2[a1, a2, z]
 // ---------------------------------------------------------------------------
 __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
+                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
+                              int64_t c0) {
+  extern __shared__ double sm[];
+  double* sQ = sm;                          // d x s*p (factor of each dimension)
+  double* T1 = sQ + d * s * p;              // p*s*s (3-D) / p*s (2-D)
+  double* T2 = T1 + p * s * (d == 3 ? s : 1);   // p*p*s (3-D)
+  const int64_t c = c0 + blockIdx.x;   // cluster, Morton id
+  const int r = blockIdx.y;
+  int cc[3];
+  morton_decode(c, d, bits, cc);
+  for (int i = threadIdx.x; i < d * s * p; i += blockDim.x) {
+    const int a = i / (s * p);
+    sQ[i] = Q[(qstride ? cc[a] * qstride : 0) + i % (s * p)];
+  }
+  const double* sQx = sQ;
+  const double* sQy = sQ + s * p;
+  const double* sQz = sQ + 2 * s * p;
+  const int P = (d == 2) ? p * p : p * p * p;
+  const int nz = (d == 3) ? s : 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < p * s * nz; i += blockDim.x) {
+    const int a1 = i % p, y = (i / p) % s, z = i / (p * s);
+    int64_t g = (int64_t)cc[0] * s + (int64_t)n * (cc[1] * s + y);
+    if (d == 3) g += (int64_t)n * n * (cc[2] * s + z);
+    double v = 0.0;
+    for (int x = 0; x < s; ++x) v += sQx[x * p + a1] * u[(g + x) * R + r];
+    T1[i] = v;
+  }
+  __syncthreads();
+  double* dst = W + ((int64_t)c * R + r) * K_pad;
+  if (d == 2) {
+    for (int i = threadIdx.x; i < K_pad; i += blockDim.x) {
+      double v = 0.0;
+      if (i < P) {
+        const int a1 = i % p, a2 = i / p;
+        for (int y = 0; y < s; ++y) v += sQy[y * p + a2] * T1[a1 + p * y];
+      }
+      dst[i] = v;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < p * p * s; i += blockDim.x) {
+    const int a1 = i % p, a2 = (i / p) % p, z = i / (p * p);
+    const double* t1 = T1 + a1 + p * s * z;
+    double v = 0.0;
+    for (int y = 0; y < s; ++y) v += sQy[y * p + a2] * t1[p * y];
+    T2[i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) {
+    double v = 0.0;
+    if (i < P) {
+      const int a12 = i % (p * p), a3 = i / (p * p);
+      for (int z = 0; z < s; ++z) v += sQz[z * p + a3] * T2[a12 + p * p * z];
+    }
+    dst[i] = v;
+  }
+}
+
+// large boxes (whole-box phases above ~200 KB of shared memory): mode 1 and 2
+// per z-slab, the mode-3 product accumulated slab by slab
+__global__ void upward_slab_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
                               int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
                               int64_t c0) {
   extern __shared__ double sm[];
@@ -115,11 +181,27 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
 
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st) {
-  int P = (d == 2) ? p * p : p * p * p;
-  size_t smem = sizeof(double) * (size_t)(d * side * p + p * side + p * p + P);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (nc > 0)
+  const size_t words = (size_t)d * side * p + (size_t)p * side * (d == 3 ? side : 1) +
+                       (d == 3 ? (size_t)p * p * side : 0);
+  const size_t smem = sizeof(double) * words;
+  if (nc <= 0) return;
+  static int force_slab = -1;   // HTLR_UPWARD_SLAB=1: slab kernel for every box (tests)
+  if (force_slab < 0) {
+    const char* e = std::getenv("HTLR_UPWARD_SLAB");
+    force_slab = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (smem <= 200 * 1024 && !force_slab) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride, c0);
+    return;
+  }
+  const int P = (d == 2) ? p * p : p * p * p;
+  const size_t smem2 = sizeof(double) * (size_t)(d * side * p + p * side + p * p + P);
+  if (smem2 > 48 * 1024)
+    cudaFuncSetAttribute(upward_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  upward_slab_kernel<<<dim3((unsigned)nc, R), 256, smem2, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride,
+                                                                c0);
 }
 
 // ---------------------------------------------------------------------------
@@ -348,9 +430,14 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
   double* Us = E2 + ((d == 3) ? sL * sL * p : 0);  // d * sL * p
   const int64_t b = b0 + blockIdx.x;   // leaf box, Morton id
   const int r = blockIdx.y;
+  // blockIdx.z: range of slabs of the last axis (small grids split a box
+  // over several CTAs; the cheap E1/E2 stages are recomputed by each)
+  const int slab = (d == 2) ? sL : sL * sL;
+  const int i_lo = (int)((int64_t)blockIdx.z * sL / gridDim.z) * slab;
+  const int i_hi = (int)((int64_t)(blockIdx.z + 1) * sL / gridDim.z) * slab;
   int bc[3];
   morton_decode(b, d, L, bc);
-  for (int i = threadIdx.x; i < PL; i += blockDim.x) facc[i] = 0.0;
+  for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) facc[i] = 0.0;
   for (int li = 0; li < dp.nlev; ++li) {
     const DownLevel lv = dp.lev[li];
     const int shift = L - lv.level;
@@ -365,7 +452,7 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
       // inside its level-l ancestor box (F-order), times H
       __syncthreads();
       const int sl = lv.side;
-      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+      for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) {
         const int x = i % sL, y = (i / sL) % sL, z = i / (sL * sL);
         int64_t row = (off[0] + x) + (int64_t)sl * (off[1] + y);
         if (d == 3) row += (int64_t)sl * sl * (off[2] + z);
@@ -395,7 +482,7 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
         E1[i] = v;
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+      for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) {
         int x = i % sL, y = i / sL;
         double v = 0.0;
         for (int a2 = 0; a2 < p; ++a2) v += U2[y * p + a2] * E1[x + sL * a2];
@@ -416,7 +503,7 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
         E2[i] = v;   // E2[x + sL*(y + sL*a3)]
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+      for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) {
         int xy = i % (sL * sL), z = i / (sL * sL);
         double v = 0.0;
         for (int a3 = 0; a3 < p; ++a3) v += U3[z * p + a3] * E2[xy + sL * sL * a3];
@@ -426,7 +513,7 @@ __global__ void downward_kernel(const double* __restrict__ u, double* __restrict
   }
   __syncthreads();
   const double* Yb = Y ? Y + ((int64_t)b * R + r) * ldy : nullptr;
-  for (int i = threadIdx.x; i < PL; i += blockDim.x) {
+  for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) {
     int x = i % sL, y = (i / sL) % sL, z = i / (sL * sL);
     int64_t gidx = (int64_t)(bc[0] * sL + x) + (int64_t)n * (bc[1] * sL + y);
     if (d == 3) gidx += (int64_t)n * n * (bc[2] * sL + z);
@@ -448,9 +535,14 @@ void launch_downward(const double* u, double* f, const double* Y, int ldy, const
   size_t smem = words * sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(downward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (nb > 0)
-    downward_kernel<<<dim3((unsigned)nb, R), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, dvec, d, n, sL, L, R, p,
-                                                             dp, b0);
+  if (nb <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ctas = nb * R;
+  const int zs = ctas >= 2 * sms ? 1 : (int)std::min<int64_t>(sL, (2 * sms + ctas - 1) / ctas);
+  downward_kernel<<<dim3((unsigned)nb, R, zs), 256, smem, st>>>(u, f, Y, ldy, a_vec, a_const, dvec, d, n, sL, L, R,
+                                                               p, dp, b0);
 }
 
 }  // namespace htlr

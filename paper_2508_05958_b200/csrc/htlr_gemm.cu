@@ -97,6 +97,45 @@ __device__ __forceinline__ ItemInfo item_info(const GemmTask* tasks, int item, i
 
 }  // namespace
 
+// One pipeline stage of a warp's (16 MI x 8 NTL) tile: the k0..3 products of
+// all (m8, n8) accumulators first, then the k4..7 products, so every
+// dependent DMMA pair is 2 MI NTL instructions apart (mma.m16n8k8 would emit
+// each dependent pair back to back).
+template <int NTL, int MI, int KC, int MT, int BST>
+__device__ __forceinline__ void stage_mma(double (&acc)[MI][4][4], const double* cA, const double* cB, int wm,
+                                          int wn, int lane, int g8, int t) {
+#pragma unroll
+  for (int ks = 0; ks < KC / 8; ++ks) {
+    double a[MI][4];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const double2* pa = reinterpret_cast<const double2*>(
+          cA + (ks >> 2) * (MT * kKC) + ((wm * MI + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
+      const double2 v0 = pa[0], v1 = pa[1];
+      a[mi][0] = v0.x;
+      a[mi][1] = v0.y;
+      a[mi][2] = v1.x;
+      a[mi][3] = v1.y;
+    }
+    double b[NTL][2];
+#pragma unroll
+    for (int ni = 0; ni < NTL; ++ni) {
+      const double* pb = cB + (wn * 32 + ni * 8 + g8) * BST + ks * 8 + t;
+      b[ni][0] = pb[0];
+      b[ni][1] = pb[4];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NTL; ++ni) {
+          mma8x8x4_pair(acc[mi][ni][0], acc[mi][ni][1], a[mi][2 * h], b[ni][h]);
+          mma8x8x4_pair(acc[mi][ni][2], acc[mi][ni][3], a[mi][2 * h + 1], b[ni][h]);
+        }
+  }
+}
+
 template <int WM, int WN, int STAGES, int KCS, int MI = 2>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
@@ -219,42 +258,21 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       mbar_wait(&full[s], (g / STAGES) & 1);
       const double* cA = sA + s * MT * KC;
       const double* cB = sB + s * NT * BST;
-      if (n_tiles == 4 && m_tiles == MI) {
-        // full tile: explicit m8n8k4 issue order -- the k0..3 products of all
-        // 16 (m8, n8) accumulators first, then the k4..7 products, so every
-        // dependent DMMA pair is 16 instructions apart (mma.m16n8k8 would
-        // emit each dependent pair back to back)
-#pragma unroll
-        for (int ks = 0; ks < KC / 8; ++ks) {
-          double a[MI][4];
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi) {
-            const double2* pa = reinterpret_cast<const double2*>(
-                cA + (ks >> 2) * (MT * kKC) + ((wm * MI + mi) * (kKC / 8) + (ks & 3)) * 128 + lane * 4);
-            const double2 v0 = pa[0], v1 = pa[1];
-            a[mi][0] = v0.x;
-            a[mi][1] = v0.y;
-            a[mi][2] = v1.x;
-            a[mi][3] = v1.y;
-          }
-          double b[4][2];
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
-            const double* pb = cB + (wn * 32 + ni * 8 + g8) * BST + ks * 8 + t;
-            b[ni][0] = pb[0];
-            b[ni][1] = pb[4];
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < 4; ++ni) {
-                mma8x8x4_pair(acc[mi][ni][0], acc[mi][ni][1], a[mi][2 * h], b[ni][h]);
-                mma8x8x4_pair(acc[mi][ni][2], acc[mi][ni][3], a[mi][2 * h + 1], b[ni][h]);
-              }
-        }
-      } else if (n_tiles > 0 && m_tiles > 0) {
+      // full row tiles: explicit m8n8k4 issue order.  The narrow variant
+      // (MI = 1, passes whose items are mostly partial) also gets the 1..3
+      // column-tile counts as compile-time constants: a predicated-off DMMA
+      // still occupies the tensor pipe (measured 1.45x the issued work on
+      // cfg 2's leaf pass).  The wide variants keep one specialised body:
+      // four of them cost more in instruction-cache misses (cfg 3: +48%).
+      if (m_tiles == MI && n_tiles == 4)
+        stage_mma<4, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
+      else if (MI == 1 && m_tiles == MI && n_tiles == 3)
+        stage_mma<3, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
+      else if (MI == 1 && m_tiles == MI && n_tiles == 2)
+        stage_mma<2, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
+      else if (MI == 1 && m_tiles == MI && n_tiles == 1)
+        stage_mma<1, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
+      else if (n_tiles > 0 && m_tiles > 0) {
 #pragma unroll
         for (int ks = 0; ks < KC / 8; ++ks) {
           double a[MI][4];
@@ -518,7 +536,7 @@ bool gemm_use_persistent() {
   return mode == 1;
 }
 
-template <int WM, int WN, int STAGES, int KCS, int MI = 2>
+template <int WM, int WN, int STAGES, int KCS, int MI = 2, int CPS = 1>
 static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
                                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                                 int M_valid, int ldc, int RT, cudaStream_t st) {
@@ -531,7 +549,7 @@ static void launch_persistent_t(const double* A, int64_t mat_stride, const doubl
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = nitems < sms ? nitems : sms;
+  const int grid = nitems < CPS * sms ? nitems : CPS * sms;   // CPS resident CTAs per SM
   gemm_persistent_kernel<WM, WN, STAGES, KCS, MI><<<grid, (WM * WN + 1) * 32, smem, st>>>(
       A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid, ldc, RT);
 }
@@ -540,8 +558,19 @@ void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                             int M_valid, int ldc, int RT, cudaStream_t st) {
   if (MT == 128 && NT == 32) {   // narrow items: 8 warps x (16 rows x 32 columns)
-    launch_persistent_t<8, 1, 4, 32, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
-                                        st);
+    // two CTAs per SM, two stages each (measured: cfg 2 leaf pass -7%
+    // against one CTA with four stages; HTLR_NARROW_CPS=1 for the latter)
+    static int v = -1;
+    if (v < 0) {
+      const char* e = std::getenv("HTLR_NARROW_CPS");
+      v = e ? std::atoi(e) : 2;
+    }
+    if (v == 2)
+      launch_persistent_t<8, 1, 2, 32, 1, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc,
+                                             RT, st);
+    else
+      launch_persistent_t<8, 1, 4, 32, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
+                                          st);
     return;
   }
   static int kcs = -1;
