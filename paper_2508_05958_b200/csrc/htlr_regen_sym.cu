@@ -29,58 +29,43 @@
 #include <algorithm>
 
 #include "htlr_kernels.h"
+#include "htlr_mbarrier.cuh"
 
 namespace htlr {
 
-namespace {
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-
-}  // namespace
-
-template <int PP, int KIND, int SB, int MINB, bool DXS = false>
-__global__ void __launch_bounds__(PP * PP * 8, MINB)
+template <int PP, int KIND, int NS, int MINB>
+__global__ void __launch_bounds__(PP * PP * 8 + 32, MINB)
     regen_sym_kernel(KernelParams kp, int level, const double* __restrict__ ax, const int* __restrict__ order,
                      const int64_t* __restrict__ uptr, const int* __restrict__ ucols, const double* __restrict__ V,
                      int64_t vstride, double* __restrict__ OUT, int64_t ostride, double coef) {
   constexpr int P = PP * PP * PP, HALF = PP / 2, U = PP * PP / 4;
-  constexpr int SE = P + 3 * PP;   // staged doubles per source: V then 3 x PP coordinates
+  constexpr int NCT = PP * PP * 8, NCW = NCT / 32;   // consumer threads / warps
+  constexpr int SE = P + 3 * PP;                     // staged doubles per source: V then 3 x PP coordinates
+  constexpr int TE = 3 * PP * PP;                    // squared axis differences per source
   extern __shared__ __align__(16) double sm[];
-  double* stage = sm;                         // 2 x SB x SE
-  double* tab = stage + 2 * SB * SE;          // SB x 3 x PP x PP   squared axis differences
-  double* vt = tab + SB * 3 * PP * PP;        // P                  V[tau]
-  double* xt = vt + P;                        // 3 x PP             tau coordinates
-  double* racc = xt + 3 * PP;                 // U x HALF x NT      row sums (thread-minor)
-  constexpr int NT = PP * PP * 8;
+  double* stage = sm;                      // NS x SE      (bulk copies)
+  double* tab = stage + NS * SE;           // NS x TE      (producer warp)
+  double* vt = tab + NS * TE;              // P            V[tau]
+  double* xt = vt + P;                     // 3 x PP       tau coordinates
+  double* racc = xt + 3 * PP;              // U x HALF x NCT row sums (thread-minor)
+  uint64_t* full = reinterpret_cast<uint64_t*>(racc + U * HALF * NCT);
+  uint64_t* ready = full + NS;
+  uint64_t* empty = ready + NS;
+  int* sig = reinterpret_cast<int*>(empty + NS);
   const double nid = -1.0 / kp.denom;
   const int tau = order[blockIdx.x];
-  const int t = threadIdx.x, cg = t >> 3, s = t & 7;
-  const int j2 = cg % PP, j3 = cg / PP, ih = s & 1;
-  const int64_t e0 = uptr[tau], ns = uptr[tau + 1] - e0;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int64_t e0 = uptr[tau];
+  const int ns = (int)(uptr[tau + 1] - e0);
 
-  auto issue = [&](int64_t b) {   // stage sources [b*SB, b*SB + SB) into buffer b & 1
-    double* dst = stage + (b & 1) * SB * SE;
-    const int nsb = (int)min((int64_t)SB, ns - b * SB);
-    for (int e = t; e < nsb * SE; e += blockDim.x) {
-      const int q = e / SE, r = e % SE;
-      const int sigma = ucols[e0 + b * SB + q];
-      if (r < P) {
-        cp_async8(dst + e, V + (int64_t)sigma * vstride + r);
-      } else {
-        const int a = (r - P) / PP, k = (r - P) % PP;
-        int sc[3];
-        morton_decode(sigma, 3, level, sc);
-        cp_async8(dst + e, ax + (int64_t)sc[a] * PP + k);
-      }
+  if (t == 0) {
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&ready[q], 1);
+      mbar_init(&empty[q], NCW);
     }
-    cp_async_commit();
-  };
-
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   {
     int tc[3];
     morton_decode(tau, 3, level, tc);
@@ -91,92 +76,114 @@ __global__ void __launch_bounds__(PP * PP * 8, MINB)
         xt[e - P] = ax[(int64_t)tc[(e - P) / PP] * PP + (e - P) % PP];
     }
   }
-#pragma unroll
-  for (int k = 0; k < U * HALF; ++k) racc[k * NT + t] = 0.0;
+  if (t < NCT)
+    for (int k = 0; k < U * HALF; ++k) racc[k * NCT + t] = 0.0;
+  __syncthreads();
 
-  const int64_t nbatch = (ns + SB - 1) / SB;
-  if (nbatch > 0) issue(0);
-  for (int64_t b = 0; b < nbatch; ++b) {
-    if (b + 1 < nbatch)
-      issue(b + 1);
-    else
-      cp_async_commit();   // empty group keeps the wait count uniform
-    cp_async_wait1();
-    __syncthreads();
-    const double* sb = stage + (b & 1) * SB * SE;
-    const int nsb = (int)min((int64_t)SB, ns - b * SB);
-    for (int e = t; e < nsb * 3 * PP * PP; e += blockDim.x) {
-      const int q = e / (3 * PP * PP), r = e % (3 * PP * PP);
-      const int a = r / (PP * PP), i = (r / PP) % PP, j = r % PP;
-      const double df = __dadd_rn(xt[a * PP + i], -sb[q * SE + P + a * PP + j]);
-      tab[e] = __dmul_rn(df, df);
+  if (warp == NCW) {
+    // ---------------------------------------------------------- producer
+    // bulk-copies source q + NS - 1 while the consumers work on earlier
+    // ones; squares the axis differences of source q once it has landed
+    auto issue = [&](int q) {
+      const int slot = q % NS;
+      if (q >= NS) mbar_wait(&empty[slot], (unsigned)(((q / NS) - 1) & 1));
+      if (lane == 0) {
+        const int sigma = ucols[e0 + q];
+        int sc[3];
+        morton_decode(sigma, 3, level, sc);
+        sig[slot] = sigma;
+        double* dst = stage + slot * SE;
+        mbar_arrive_expect_tx(&full[slot], (unsigned)(SE * 8));
+        bulk_g2s(dst, V + (int64_t)sigma * vstride, P * 8, &full[slot]);
+        for (int a = 0; a < 3; ++a) bulk_g2s(dst + P + a * PP, ax + (int64_t)sc[a] * PP, PP * 8, &full[slot]);
+      }
+      __syncwarp();
+    };
+    for (int q = 0; q < ns && q < NS - 1; ++q) issue(q);
+    for (int q = 0; q < ns; ++q) {
+      const int slot = q % NS;
+      mbar_wait(&full[slot], (unsigned)((q / NS) & 1));
+      const double* eta = stage + slot * SE + P;
+      double* tq = tab + slot * TE;
+      for (int e = lane; e < TE; e += 32) {
+        const int a = e / (PP * PP), i = (e / PP) % PP, j = e % PP;
+        const double df = __dadd_rn(xt[a * PP + i], -eta[a * PP + j]);
+        tq[e] = __dmul_rn(df, df);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[slot]);
+      if (q + NS - 1 < ns) issue(q + NS - 1);
     }
-    __syncthreads();
-    for (int q = 0; q < nsb; ++q) {
-      const double* vs = sb + q * SE + cg * PP;   // V[sigma] of my PP columns
-      const double* tq = tab + q * 3 * PP * PP;
-      double vc[PP], dxr[HALF][PP], cacc[PP];
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int cg = t >> 3, s = t & 7;
+  const int j2 = cg % PP, j3 = cg / PP, ih = s & 1;
+  for (int q = 0; q < ns; ++q) {
+    const int slot = q % NS;
+    mbar_wait(&ready[slot], (unsigned)((q / NS) & 1));
+    const double* vs = stage + slot * SE + cg * PP;   // V[sigma] of my PP columns
+    const double* tq = tab + slot * TE;
+    double vc[PP], dxr[HALF][PP], cacc[PP];
 #pragma unroll
-      for (int c = 0; c < PP; ++c) {
-        vc[c] = vs[c];
-        cacc[c] = 0.0;
+    for (int c = 0; c < PP; ++c) {
+      vc[c] = vs[c];
+      cacc[c] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < HALF; ++r)
+#pragma unroll
+      for (int c = 0; c < PP; ++c) dxr[r][c] = tq[(ih * HALF + r) * PP + c];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int rg = (s >> 1) + 4 * k, i2 = rg % PP, i3 = rg / PP;
+      const double yz = tq[PP * PP + i2 * PP + j2] + tq[2 * PP * PP + i3 * PP + j3];
+      double wt[HALF], ra[HALF];
+#pragma unroll
+      for (int r = 0; r < HALF; ++r) {
+        wt[r] = vt[rg * PP + ih * HALF + r];
+        ra[r] = racc[(k * HALF + r) * NCT + t];
       }
-      if (!DXS) {
 #pragma unroll
-        for (int r = 0; r < HALF; ++r)
+      for (int r = 0; r < HALF; ++r)
 #pragma unroll
-          for (int c = 0; c < PP; ++c) dxr[r][c] = tq[(ih * HALF + r) * PP + c];
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int rg = (s >> 1) + 4 * k, i2 = rg % PP, i3 = rg / PP;
-        const double yz = tq[PP * PP + i2 * PP + j2] + tq[2 * PP * PP + i3 * PP + j3];
-        double wt[HALF], ra[HALF];
-#pragma unroll
-        for (int r = 0; r < HALF; ++r) {
-          wt[r] = vt[rg * PP + ih * HALF + r];
-          ra[r] = racc[(k * HALF + r) * NT + t];
+        for (int c = 0; c < PP; ++c) {
+          const double kv = kernel_shape<KIND>(dxr[r][c] + yz, nid);
+          ra[r] = fma(kv, vc[c], ra[r]);
+          cacc[c] = fma(kv, wt[r], cacc[c]);
         }
 #pragma unroll
-        for (int r = 0; r < HALF; ++r)
-#pragma unroll
-          for (int c = 0; c < PP; ++c) {
-            const double dx = DXS ? tq[(ih * HALF + r) * PP + c] : dxr[r][c];
-            const double kv = kernel_shape<KIND>(dx + yz, nid);
-            ra[r] = fma(kv, vc[c], ra[r]);
-            cacc[c] = fma(kv, wt[r], cacc[c]);
-          }
-#pragma unroll
-        for (int r = 0; r < HALF; ++r) racc[(k * HALF + r) * NT + t] = ra[r];
-      }
-      // column sums over the 8 slices (lanes xor 4, 2, 1): after the xor-4
-      // step a lane keeps the half of the columns selected by its bit 2
-      constexpr int H2 = PP / 2;
-      const bool hi = (s & 4) != 0;
-      double keep[H2];
-#pragma unroll
-      for (int c = 0; c < H2; ++c) {
-        const double send = hi ? cacc[c] : cacc[H2 + c];
-        const double mine = hi ? cacc[H2 + c] : cacc[c];
-        keep[c] = mine + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-#pragma unroll
-      for (int c = 0; c < H2; ++c) {
-        keep[c] += __shfl_xor_sync(0xffffffffu, keep[c], 2);
-        keep[c] += __shfl_xor_sync(0xffffffffu, keep[c], 1);
-      }
-      const int r3 = s & 3;
-      if (r3 < H2) {
-        const int sigma = ucols[e0 + b * SB + q];
-        double v = keep[0];
-#pragma unroll
-        for (int c = 1; c < H2; ++c)
-          if (c == r3) v = keep[c];
-        const int j1 = (hi ? H2 : 0) + r3;
-        atomicAdd(OUT + (int64_t)sigma * ostride + cg * PP + j1, coef * v);
-      }
+      for (int r = 0; r < HALF; ++r) racc[(k * HALF + r) * NCT + t] = ra[r];
     }
-    __syncthreads();   // buffer b & 1 and tab are rewritten next iteration
+    const int sigma = sig[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    // column sums over the 8 slices (lanes xor 4, 2, 1): after the xor-4
+    // step a lane keeps the half of the columns selected by its bit 2
+    constexpr int H2 = PP / 2;
+    const bool hi = (s & 4) != 0;
+    double keep[H2];
+#pragma unroll
+    for (int c = 0; c < H2; ++c) {
+      const double send = hi ? cacc[c] : cacc[H2 + c];
+      const double mine = hi ? cacc[H2 + c] : cacc[c];
+      keep[c] = mine + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int c = 0; c < H2; ++c) {
+      keep[c] += __shfl_xor_sync(0xffffffffu, keep[c], 2);
+      keep[c] += __shfl_xor_sync(0xffffffffu, keep[c], 1);
+    }
+    const int r3 = s & 3;
+    if (r3 < H2) {
+      double v = keep[0];
+#pragma unroll
+      for (int c = 1; c < H2; ++c)
+        if (c == r3) v = keep[c];
+      const int j1 = (hi ? H2 : 0) + r3;
+      atomicAdd(OUT + (int64_t)sigma * ostride + cg * PP + j1, coef * v);
+    }
   }
   // row sums: reduce over the 4 column groups of the warp (lanes xor 8, 16),
   // then one RED per row from the lanes of column group 0 mod 4
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(PP * PP * 8, MINB)
     const int rg = (s >> 1) + 4 * k;
 #pragma unroll
     for (int r = 0; r < HALF; ++r) {
-      double v = racc[(k * HALF + r) * NT + t];
+      double v = racc[(k * HALF + r) * NCT + t];
       v += __shfl_xor_sync(0xffffffffu, v, 8);
       v += __shfl_xor_sync(0xffffffffu, v, 16);
       if ((cg & 3) == 0) atomicAdd(OUT + (int64_t)tau * ostride + rg * PP + ih * HALF + r, coef * v);
@@ -211,17 +218,17 @@ __global__ void near_weight_kernel(int sL, int L, const double* __restrict__ wid
 
 bool regen_sym_supported(int d, int pp) { return d == 3 && (pp == 4 || pp == 6); }
 
-template <int PP, int KIND, int SB, int MINB, bool DXS = false>
+template <int PP, int KIND, int NS, int MINB>
 static void sym_k(KernelParams kp, int level, const double* ax, const int* order, int64_t nrows,
                   const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                   int64_t ostride, double coef, cudaStream_t st) {
-  constexpr int P = PP * PP * PP;
-  const size_t smem =
-      sizeof(double) * (2 * SB * (P + 3 * PP) + SB * 3 * PP * PP + P + 3 * PP + (size_t)(P / 8) * PP * PP * 8);
-  cudaFuncSetAttribute(regen_sym_kernel<PP, KIND, SB, MINB, DXS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  regen_sym_kernel<PP, KIND, SB, MINB, DXS><<<(unsigned)nrows, PP * PP * 8, smem, st>>>(kp, level, ax, order, uptr, ucols, V,
-                                                                         vstride, OUT, ostride, coef);
+  constexpr int P = PP * PP * PP, NCT = PP * PP * 8;
+  const size_t smem = sizeof(double) * ((size_t)NS * (P + 3 * PP + 3 * PP * PP) + P + 3 * PP +
+                                        (size_t)(PP * PP / 4) * (PP / 2) * NCT) +
+                      3 * NS * sizeof(uint64_t) + NS * sizeof(int);
+  cudaFuncSetAttribute(regen_sym_kernel<PP, KIND, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  regen_sym_kernel<PP, KIND, NS, MINB><<<(unsigned)nrows, NCT + 32, smem, st>>>(kp, level, ax, order, uptr, ucols, V,
+                                                                          vstride, OUT, ostride, coef);
 }
 
 template <int PP>
@@ -229,12 +236,12 @@ static void sym_p(KernelParams kp, int level, const double* ax, const int* order
                   const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                   int64_t ostride, cudaStream_t st) {
   const double coef = kernel_coef(kp);
-  // 8 sources per stage, two CTAs per SM (measured: 3 CTAs per SM with the
-  // x-differences in shared memory, or 4-source stages, are 1-8% slower)
+  // 12-source ring, two CTAs per SM (the Gaussian's exp needs the
+  // registers of one)
   if (kp.kind == 0)
-    sym_k<PP, 0, 8, 2>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
+    sym_k<PP, 0, 12, 1>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
   else
-    sym_k<PP, 2, 8, 2>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
+    sym_k<PP, 2, 12, 2>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
 }
 
 void launch_regen_sym(const KernelParams& kp, int pp, int level, const double* ax, const int* order, int64_t nrows,
