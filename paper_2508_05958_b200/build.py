@@ -12,6 +12,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -40,12 +41,12 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(HERE, "..", "include", "htlr_b200.h"))
-    objs = []
+    objs, jobs = [], []
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + headers):
-            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", s, "-o", o])
+            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", s, "-o", o])
         objs.append(o)
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
@@ -55,8 +56,12 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
                    "-c", s, "-o", o]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
-            _run(cmd)
+            jobs.append(cmd)
         objs.append(o)
+    # independent translation units compile in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for fut in [ex.submit(_run, j) for j in jobs]:
+            fut.result()
     if force or _stale(OUT, objs):
         _run([NVCC, "-shared", *ARCH, "-o", OUT, *objs, "-lcudart"])
     return OUT
