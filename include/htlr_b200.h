@@ -147,6 +147,20 @@ int htlr_bind_exchange(htlr_plan* plan, int64_t nrhs, void* const* ptrs, int64_t
  * local + remote for an unsharded plan. */
 int htlr_matvec_local(htlr_plan* plan, const double* u, int64_t nrhs, void* stream);
 int htlr_matvec_remote(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
+/* The remote phase in two halves: contract (GEMMs / regenerated blocks into
+ * the accumulators H_l, Y) and expand (downward pass into f).  A sharded plan
+ * on a mapped grid with the symmetric regeneration evaluates every unordered
+ * block pair once, so its column sums land in other shards' rows: it
+ * accumulates into full-size buffers that the caller binds (bind_reduce, sizes
+ * from reduce_info; cluster-major, shard r's rows = the r-th 1/world of the
+ * bytes) and must sum-reduce-scatter between contract and expand.
+ * reduce_info reports count 0 for every other plan; htlr_matvec_remote then
+ * equals contract + expand (and refuses a plan that needs the reduction).
+ * No reference counterpart: the reference has no parallel matvec. */
+int htlr_reduce_info(const htlr_plan* plan, int64_t nrhs, int64_t* count, int64_t* bytes, int64_t cap);
+int htlr_bind_reduce(htlr_plan* plan, int64_t nrhs, void* const* ptrs, int64_t count);
+int htlr_matvec_contract(htlr_plan* plan, const double* u, int64_t nrhs, void* stream);
+int htlr_matvec_expand(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
 
 /* Diagonal cell average used by the inadmissible tau == sigma blocks
  * (operators.py:95-99).  Synchronises. */

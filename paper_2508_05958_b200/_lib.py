@@ -63,6 +63,10 @@ SYMBOLS = [
     ("htlr_bind_exchange", ctypes.c_int, [_P, _I64, _P, _I64]),
     ("htlr_matvec_local", ctypes.c_int, [_P, _P, _I64, _P]),
     ("htlr_matvec_remote", ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    ("htlr_reduce_info", ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), _P, _I64]),
+    ("htlr_bind_reduce", ctypes.c_int, [_P, _I64, _P, _I64]),
+    ("htlr_matvec_contract", ctypes.c_int, [_P, _P, _I64, _P]),
+    ("htlr_matvec_expand", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("htlr_diag_value", ctypes.c_int, [_P, ctypes.POINTER(_D)]),
     ("htlr_export_block", ctypes.c_int, [_P, _I64, _P, _I64, _P, _I64, _P]),
     ("htlr_storage", ctypes.c_int, [_P, _P]),

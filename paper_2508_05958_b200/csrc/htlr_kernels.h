@@ -119,11 +119,12 @@ void launch_regen_adm(const KernelParams& kp, int d, int p, int level, const dou
 void launch_regen_near(const KernelParams& kp, int d, int sL, int L, const double* coords, const double* widths,
                        const int64_t* rowptr, const int* cols, int64_t t0, int64_t nt, const double* ub, int K_pad,
                        double* Y, int R, cudaStream_t st);
-// symmetric regeneration (htlr_regen_sym.cu): one CTA per row of `order`,
-// sources sigma > tau from (uptr, ucols); OUT must be initialised
+// symmetric regeneration (htlr_regen_sym.cu): one CTA per own row of
+// `order` (global id t0 + row), its owned pairs from (uptr, ucols); OUT must
+// be initialised
 bool regen_sym_supported(int d, int pp);
 void launch_regen_sym(const KernelParams& kp, int pp, int level, const double* ax, const int* order, int64_t nrows,
-                      const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
+                      int64_t t0, const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                       int64_t ostride, cudaStream_t st);
 void launch_near_weight(int sL, int L, const double* widths, const double* ub, int K_pad, double* V, int64_t nleaf,
                         cudaStream_t st);

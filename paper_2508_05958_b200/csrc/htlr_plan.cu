@@ -175,6 +175,11 @@ struct htlr_plan {
   // caller-bound exchange buffers (ub, then W of each level pass), per R
   int ext_R = 0;
   std::vector<double*> ext_ptrs;
+  // caller-bound reduce buffers (mapped grid, symmetric regeneration on a
+  // sharded plan): H_l of each symmetric level, then Y; full size, summed
+  // over the shards between htlr_matvec_contract and htlr_matvec_expand
+  int red_R = 0;
+  std::vector<double*> red_ptrs;
   bool profiling = false;
   // CUDA-graph replay of the whole matvec, keyed by (R, u, f, profiling)
   bool graphs = true;
@@ -730,34 +735,46 @@ static int upload(DevBuf& buf, const void* src, size_t bytes) {
   return 0;
 }
 
-// Symmetric upper list of a full (unsharded) CSR: nullptr-free when the list
-// is not symmetric (then the one-sided kernels stay in use).  Self pairs are
-// returned separately (near field only).
-static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& cols, SymList& out,
-                     std::vector<int64_t>* self_ptr, std::vector<int>* self_cols) {
+// Pair lists of the symmetric regeneration.  Every unordered pair {a, b}
+// (a < b) is evaluated once, by the CTA of its owning endpoint: a when a + b
+// is even, else b -- about half of every row's list, so rows (and shards)
+// stay balanced.  `ptr`/`cols` is the CSR of the own rows [t0, t0 + rows);
+// self pairs (near field) are returned separately for the one-sided kernel.
+// `full` (unsharded plans) lets the symmetry of the lists be checked; a
+// non-symmetric list leaves the symmetric path off.
+static bool pair_owner_is_row(int64_t row, int64_t other) {
+  const int64_t a = std::min(row, other), b = std::max(row, other);
+  return (((a + b) & 1) == 0) ? row == a : row == b;
+}
+
+static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& cols, int64_t t0, bool full,
+                     SymList& out, std::vector<int64_t>* self_ptr, std::vector<int>* self_cols) {
   out.release();
   const int64_t nrows = (int64_t)ptr.size() - 1;
   std::vector<int64_t> up(nrows + 1, 0);
   std::vector<int> uc;
   if (self_ptr) self_ptr->assign(nrows + 1, 0);
   if (self_cols) self_cols->clear();
-  for (int64_t t = 0; t < nrows; ++t) {
-    for (int64_t e = ptr[t]; e < ptr[t + 1]; ++e) {
+  for (int64_t r = 0; r < nrows; ++r) {
+    const int64_t t = t0 + r;
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
       const int sg = cols[e];
-      // symmetry: tau must appear in sigma's (sorted) list
-      if (sg < 0 || sg >= nrows) return 0;
-      if (!std::binary_search(cols.begin() + ptr[sg], cols.begin() + ptr[sg + 1], (int)t)) return 0;
-      if (sg > t) uc.push_back(sg);
+      if (full) {   // symmetry: tau must appear in sigma's (sorted) list
+        if (sg < 0 || sg >= nrows) return 0;
+        if (!std::binary_search(cols.begin() + ptr[sg], cols.begin() + ptr[sg + 1], (int)t)) return 0;
+      }
       if (sg == t) {
         if (!self_cols) return 0;
         self_cols->push_back(sg);
+      } else if (pair_owner_is_row(t, sg)) {
+        uc.push_back(sg);
       }
     }
-    up[t + 1] = (int64_t)uc.size();
-    if (self_ptr) (*self_ptr)[t + 1] = (int64_t)self_cols->size();
+    up[r + 1] = (int64_t)uc.size();
+    if (self_ptr) (*self_ptr)[r + 1] = (int64_t)self_cols->size();
   }
   std::vector<int> order(nrows);
-  for (int64_t t = 0; t < nrows; ++t) order[t] = (int)t;
+  for (int64_t r = 0; r < nrows; ++r) order[r] = (int)r;
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return up[a + 1] - up[a] > up[b + 1] - up[b]; });
   if (upload(out.uptr, up.data(), up.size() * sizeof(int64_t))) return 1;
@@ -801,16 +818,18 @@ static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
   }
   if (upload(pl->d_near_ptr, pl->near_ptr.data(), pl->near_ptr.size() * sizeof(int64_t))) return 1;
   if (upload(pl->d_near_cols, pl->near_cols.data(), pl->near_cols.size() * sizeof(int))) return 1;
-  // symmetric regeneration (single shard: the column sums land in rows of
-  // every cluster, so a sharded plan keeps the one-sided kernels)
-  if (pl->shard_world == 1 && regen_sym_enabled()) {
+  // symmetric regeneration: the column sums land in rows of any cluster, so
+  // a sharded plan accumulates full-size H_l / Y, summed over the shards by
+  // the caller between htlr_matvec_contract and htlr_matvec_expand
+  if (regen_sym_enabled()) {
+    const bool full = pl->shard_world == 1;
     for (auto& lv : pl->levels)
       if (lv.needs_up && htlr::regen_sym_supported(d, p))
-        if (build_sym(lv.csr_ptr, lv.csr_cols, lv.sym, nullptr, nullptr)) return 1;
+        if (build_sym(lv.csr_ptr, lv.csr_cols, pl->own_lo[lv.level], full, lv.sym, nullptr, nullptr)) return 1;
     if (htlr::regen_sym_supported(d, pl->sL)) {
       std::vector<int64_t> sp;
       std::vector<int> sc;
-      if (build_sym(pl->near_ptr, pl->near_cols, pl->near_sym, &sp, &sc)) return 1;
+      if (build_sym(pl->near_ptr, pl->near_cols, pl->own_lo[pl->L], full, pl->near_sym, &sp, &sc)) return 1;
       if (pl->near_sym.on) {
         if (upload(pl->d_self_ptr, sp.data(), sp.size() * sizeof(int64_t))) return 1;
         if (upload(pl->d_self_cols, sc.data(), std::max<size_t>(1, sc.size()) * sizeof(int))) return 1;
@@ -1143,62 +1162,98 @@ int mv_local_mapped(MvCtx& cx, const double* u) {
 }
 
 // kernel sampling is counted as 10 flops per evaluation plus the MAC
-int mv_remote_mapped(MvCtx& cx, const double* u, double* f) {
+// Accumulators of the mapped remote phase: H_l per level and Y, or the
+// caller-bound full-size reduce buffers of a sharded symmetric plan.
+static bool mapped_sym(const htlr_plan* pl, int R) {
+  if (R != 1) return false;
+  for (const auto& lv : pl->levels)
+    if (lv.needs_up && lv.sym.on) return true;
+  return pl->near_sym.on;
+}
+
+static void mapped_accumulators(htlr_plan* pl, int R, std::vector<double*>& H, double*& Y) {
+  const bool bound = pl->shard_world > 1 && pl->red_R == R && !pl->red_ptrs.empty();
+  size_t k = 0;
+  H.assign(pl->levels.size(), nullptr);
+  for (size_t l = 0; l < pl->levels.size(); ++l) {
+    Level& lv = pl->levels[l];
+    if (!lv.needs_up) continue;
+    H[l] = (bound && lv.sym.on) ? pl->red_ptrs[k++] : lv.H.d();
+  }
+  Y = (bound && pl->near_sym.on) ? pl->red_ptrs[k++] : pl->Y.d();
+}
+
+// stages: bit 0 = contract (regenerated cores and near blocks into H_l, Y),
+// bit 1 = expand (downward pass).  A sharded symmetric plan needs the shards'
+// H_l / Y summed in between (htlr_reduce_info); otherwise stages = 3.
+int mv_remote_mapped(MvCtx& cx, const double* u, double* f, int stages) {
   htlr_plan* pl = cx.pl;
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const int PL = ipow(pl->sL, d);
   const double R8 = 8.0 * R;
+  const bool sharded = pl->shard_world > 1;
+  std::vector<double*> Hl;
+  double* Y = nullptr;
+  mapped_accumulators(pl, R, Hl, Y);
   htlr::DownParams dp{};
   dp.nlev = 0;
   double down_macs = 0.0;
+  const int64_t nleaf = pl->levels[pl->L].nclusters;
+  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   for (auto& lv : pl->levels) {
     if (!lv.needs_up) continue;
+    if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), Hl[lv.level], (int64_t)lv.side * p, nullptr};
+    double sl = pl->sL;
+    down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
+    if (!(stages & 1)) continue;
     const int64_t t0 = pl->own_lo[lv.level], nt = pl->own_hi[lv.level] - t0;
     const double npair = (double)lv.csr_cols.size();
     // symmetric regeneration: one 10-flop evaluation per unordered pair
-    const double evals = (lv.sym.on && R == 1) ? 0.5 : 1.0;
+    const bool sym = lv.sym.on && R == 1;
+    const double evals = sym ? 0.5 : 1.0;
     if (cx.prof_begin(5, lv.level, npair * P * P * (10.0 * evals + 2.0 * R), R8 * npair * P)) return 1;
-    if (lv.sym.on && R == 1) {
-      CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * P * sizeof(double), cx.st));
-      htlr::launch_regen_sym(pl->kp, p, lv.level, lv.nodes.d(), (const int*)lv.sym.order.ptr, lv.sym.nrows,
+    if (sym) {
+      CUDA_TRY(cudaMemsetAsync(Hl[lv.level], 0, (size_t)lv.nclusters * P * sizeof(double), cx.st));
+      htlr::launch_regen_sym(pl->kp, p, lv.level, lv.nodes.d(), (const int*)lv.sym.order.ptr, lv.sym.nrows, t0,
                              (const int64_t*)lv.sym.uptr.ptr, (const int*)lv.sym.ucols.ptr, cx.Wl[lv.level], P,
-                             lv.H.d(), P, cx.st);
+                             Hl[lv.level], P, cx.st);
     } else {
       htlr::launch_regen_adm(pl->kp, d, p, lv.level, lv.nodes.d(), (const int64_t*)lv.d_ptr.ptr,
-                             (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, lv.H.d(), R, cx.st);
+                             (const int*)lv.d_cols.ptr, t0, nt, cx.Wl[lv.level], P, Hl[lv.level], R, cx.st);
     }
     if (cx.prof_end()) return 1;
-    if (dp.nlev >= htlr::kMaxLevels) return fail(-1, "too many levels");
-    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Lm.d(), lv.H.d(), (int64_t)lv.side * p, nullptr};
-    double sl = pl->sL;
-    down_macs += (d == 2) ? (sl * p * p + sl * sl * p) : (sl * p * p * p + sl * sl * p * p + sl * sl * sl * p);
   }
-  const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
-  {
+  if (stages & 1) {
     const double npair = (double)pl->near_cols.size();
-    const double evals = (pl->near_sym.on && R == 1) ? 0.5 : 1.0;
+    const bool sym = pl->near_sym.on && R == 1;
+    const double evals = sym ? 0.5 : 1.0;
     if (cx.prof_begin(6, pl->L, npair * PL * PL * (10.0 * evals + 2.0 * R), R8 * npair * PL)) return 1;
-    if (pl->near_sym.on && R == 1) {
-      // self pairs first (plain stores initialise Y), then the upper pairs
+    if (sym) {
+      // self pairs first (plain stores initialise the own rows of Y), then
+      // the owned pairs, whose column sums may land in any leaf's rows
+      if (sharded) CUDA_TRY(cudaMemsetAsync(Y, 0, (size_t)nleaf * PL * sizeof(double), cx.st));
       htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(),
                               (const int64_t*)pl->d_self_ptr.ptr, (const int*)pl->d_self_cols.ptr, b0, nb, cx.ub,
-                              PL, pl->Y.d(), R, cx.st);
-      htlr::launch_near_weight(pl->sL, pl->L, pl->d_mc.d(), cx.ub, PL, pl->Vn.d(), nb, cx.st);
+                              PL, Y, R, cx.st);
+      htlr::launch_near_weight(pl->sL, pl->L, pl->d_mc.d(), cx.ub, PL, pl->Vn.d(), nleaf, cx.st);
       htlr::launch_regen_sym(pl->kp, pl->sL, pl->L, pl->d_mx.d(), (const int*)pl->near_sym.order.ptr,
-                             pl->near_sym.nrows, (const int64_t*)pl->near_sym.uptr.ptr,
-                             (const int*)pl->near_sym.ucols.ptr, pl->Vn.d(), PL, pl->Y.d(), PL, cx.st);
+                             pl->near_sym.nrows, b0, (const int64_t*)pl->near_sym.uptr.ptr,
+                             (const int*)pl->near_sym.ucols.ptr, pl->Vn.d(), PL, Y, PL, cx.st);
     } else {
       htlr::launch_regen_near(pl->kp, d, pl->sL, pl->L, pl->d_mx.d(), pl->d_mc.d(),
                               (const int64_t*)pl->d_near_ptr.ptr, (const int*)pl->d_near_cols.ptr, b0, nb, cx.ub,
-                              PL, pl->Y.d(), R, cx.st);
+                              PL, Y, R, cx.st);
     }
     if (cx.prof_end()) return 1;
   }
-  const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
-  if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
-  htlr::launch_downward(u, f, pl->Y.d(), PL, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
-                        pl->dvec.d(), d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
-  if (cx.prof_end()) return 1;
+  if (stages & 2) {
+    const double frac = (double)nb / (double)nleaf;
+    if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
+    htlr::launch_downward(u, f, Y, PL, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
+                          pl->dvec.d(), d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
+    if (cx.prof_end()) return 1;
+  }
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -1232,20 +1287,21 @@ int mv_local(MvCtx& cx, const double* u) {
   return 0;
 }
 
-int mv_remote(MvCtx& cx, const double* u, double* f) {
+int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   htlr_plan* pl = cx.pl;
-  if (pl->mapped) return mv_remote_mapped(cx, u, f);
+  if (pl->mapped) return mv_remote_mapped(cx, u, f, stages);
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const double R8 = 8.0 * R;
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int64_t nleaf = pl->levels[pl->L].nclusters;
   for (auto& ps : pl->passes) {
+    if (!(stages & 1)) break;
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), cx.st));
   }
-  CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
-  for (size_t i = 0; i < pl->passes.size(); ++i) {
+  if (stages & 1) CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
+  for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     auto& slot = ps.tasks[R];
     if (slot.second == 0) continue;
@@ -1274,6 +1330,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f) {
   }
   const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   const double frac = (double)nb / (double)nleaf;
+  if (!(stages & 2)) return 0;
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
   htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
                         nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
@@ -1371,14 +1428,88 @@ int htlr_matvec_local(htlr_plan* pl, const double* u, int64_t nrhs, void* stream
   return 0;
 }
 
+static void reduce_sizes(const htlr_plan* pl, int R, std::vector<int64_t>& b);
+
 int htlr_matvec_remote(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
   MvCtx cx;
   if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
   if (!u || !f) return fail(-1, "null vector");
+  {
+    std::vector<int64_t> b;
+    reduce_sizes(pl, cx.R, b);
+    if (!b.empty())
+      return fail(-1, "sharded symmetric plan: use htlr_matvec_contract, the reduction, htlr_matvec_expand");
+  }
   cx.ev_used = 2 * pl->prof_kind.size();   // continue the local phase's records
   if (int rc = mv_remote(cx, u, f)) return rc;
   pl->last_launches += cx.launches;
   return 0;
+}
+
+// full-size accumulators a sharded symmetric plan sums over the shards
+static void reduce_sizes(const htlr_plan* pl, int R, std::vector<int64_t>& b) {
+  b.clear();
+  if (!pl->mapped || pl->shard_world == 1 || !mapped_sym(pl, R)) return;
+  const int P = ipow(pl->p, pl->d), PL = ipow(pl->sL, pl->d);
+  for (const auto& lv : pl->levels)
+    if (lv.needs_up && lv.sym.on) b.push_back(lv.nclusters * (int64_t)R * P * (int64_t)sizeof(double));
+  if (pl->near_sym.on) b.push_back(pl->levels[pl->L].nclusters * (int64_t)R * PL * (int64_t)sizeof(double));
+}
+
+int htlr_reduce_info(const htlr_plan* pl, int64_t nrhs, int64_t* count, int64_t* bytes, int64_t cap) {
+  if (!pl || !count) return fail(-1, "null argument");
+  if (!pl->lists_built) return fail(-1, "lists not built");
+  if (pl->mapped && !pl->constructed) return fail(-1, "plan not constructed");
+  std::vector<int64_t> b;
+  reduce_sizes(pl, (int)nrhs, b);
+  *count = (int64_t)b.size();
+  if (bytes) {
+    if (cap < (int64_t)b.size()) return fail(-1, "reduce info buffer too small");
+    for (size_t i = 0; i < b.size(); ++i) bytes[i] = b[i];
+  }
+  return 0;
+}
+
+int htlr_bind_reduce(htlr_plan* pl, int64_t nrhs, void* const* ptrs, int64_t count) {
+  if (!pl) return fail(-1, "null plan");
+  drop_graphs(pl);
+  std::vector<int64_t> b;
+  reduce_sizes(pl, (int)nrhs, b);
+  if (!ptrs || count == 0) {
+    pl->red_R = 0;
+    pl->red_ptrs.clear();
+    return 0;
+  }
+  if (count != (int64_t)b.size()) return fail(-1, "reduce buffer count mismatch");
+  pl->red_ptrs.assign(count, nullptr);
+  for (int64_t i = 0; i < count; ++i) {
+    if (!ptrs[i]) return fail(-1, "null reduce buffer");
+    pl->red_ptrs[i] = static_cast<double*>(ptrs[i]);
+  }
+  pl->red_R = (int)nrhs;
+  return 0;
+}
+
+static int matvec_stage(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream, int stages) {
+  MvCtx cx;
+  if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
+  if (!u || (!f && (stages & 2))) return fail(-1, "null vector");
+  std::vector<int64_t> b;
+  reduce_sizes(pl, cx.R, b);
+  if (!b.empty() && !(pl->red_R == cx.R && pl->red_ptrs.size() == b.size()))
+    return fail(-1, "sharded symmetric plan: bind the reduce buffers first (htlr_bind_reduce)");
+  cx.ev_used = 2 * pl->prof_kind.size();
+  if (int rc = mv_remote(cx, u, f, stages)) return rc;
+  pl->last_launches += cx.launches;
+  return 0;
+}
+
+int htlr_matvec_contract(htlr_plan* pl, const double* u, int64_t nrhs, void* stream) {
+  return matvec_stage(pl, u, nullptr, nrhs, stream, 1);
+}
+
+int htlr_matvec_expand(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  return matvec_stage(pl, u, f, nrhs, stream, 2);
 }
 
 int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,

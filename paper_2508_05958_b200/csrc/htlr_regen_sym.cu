@@ -36,8 +36,9 @@ namespace htlr {
 template <int PP, int KIND, int NS, int MINB>
 __global__ void __launch_bounds__(PP * PP * 8 + 32, MINB)
     regen_sym_kernel(KernelParams kp, int level, const double* __restrict__ ax, const int* __restrict__ order,
-                     const int64_t* __restrict__ uptr, const int* __restrict__ ucols, const double* __restrict__ V,
-                     int64_t vstride, double* __restrict__ OUT, int64_t ostride, double coef) {
+                     int64_t t0, const int64_t* __restrict__ uptr, const int* __restrict__ ucols,
+                     const double* __restrict__ V, int64_t vstride, double* __restrict__ OUT, int64_t ostride,
+                     double coef) {
   constexpr int P = PP * PP * PP, HALF = PP / 2, U = PP * PP / 4;
   constexpr int NCT = PP * PP * 8, NCW = NCT / 32;   // consumer threads / warps
   constexpr int SE = P + 3 * PP;                     // staged doubles per source: V then 3 x PP coordinates
@@ -53,10 +54,11 @@ __global__ void __launch_bounds__(PP * PP * 8 + 32, MINB)
   uint64_t* empty = ready + NS;
   int* sig = reinterpret_cast<int*>(empty + NS);
   const double nid = -1.0 / kp.denom;
-  const int tau = order[blockIdx.x];
+  const int row = order[blockIdx.x];   // own row (longest lists first)
+  const int64_t tau = t0 + row;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int64_t e0 = uptr[tau];
-  const int ns = (int)(uptr[tau + 1] - e0);
+  const int64_t e0 = uptr[row];
+  const int ns = (int)(uptr[row + 1] - e0);
 
   if (t == 0) {
     for (int q = 0; q < NS; ++q) {
@@ -219,7 +221,7 @@ __global__ void near_weight_kernel(int sL, int L, const double* __restrict__ wid
 bool regen_sym_supported(int d, int pp) { return d == 3 && (pp == 4 || pp == 6); }
 
 template <int PP, int KIND, int NS, int MINB>
-static void sym_k(KernelParams kp, int level, const double* ax, const int* order, int64_t nrows,
+static void sym_k(KernelParams kp, int level, const double* ax, const int* order, int64_t nrows, int64_t t0,
                   const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                   int64_t ostride, double coef, cudaStream_t st) {
   constexpr int P = PP * PP * PP, NCT = PP * PP * 8;
@@ -227,31 +229,31 @@ static void sym_k(KernelParams kp, int level, const double* ax, const int* order
                                         (size_t)(PP * PP / 4) * (PP / 2) * NCT) +
                       3 * NS * sizeof(uint64_t) + NS * sizeof(int);
   cudaFuncSetAttribute(regen_sym_kernel<PP, KIND, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  regen_sym_kernel<PP, KIND, NS, MINB><<<(unsigned)nrows, NCT + 32, smem, st>>>(kp, level, ax, order, uptr, ucols, V,
-                                                                          vstride, OUT, ostride, coef);
+  regen_sym_kernel<PP, KIND, NS, MINB><<<(unsigned)nrows, NCT + 32, smem, st>>>(kp, level, ax, order, t0, uptr, ucols,
+                                                                          V, vstride, OUT, ostride, coef);
 }
 
 template <int PP>
-static void sym_p(KernelParams kp, int level, const double* ax, const int* order, int64_t nrows,
+static void sym_p(KernelParams kp, int level, const double* ax, const int* order, int64_t nrows, int64_t t0,
                   const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                   int64_t ostride, cudaStream_t st) {
   const double coef = kernel_coef(kp);
   // 12-source ring, two CTAs per SM (the Gaussian's exp needs the
   // registers of one)
   if (kp.kind == 0)
-    sym_k<PP, 0, 12, 1>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
+    sym_k<PP, 0, 12, 1>(kp, level, ax, order, nrows, t0, uptr, ucols, V, vstride, OUT, ostride, coef, st);
   else
-    sym_k<PP, 2, 12, 2>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, coef, st);
+    sym_k<PP, 2, 12, 2>(kp, level, ax, order, nrows, t0, uptr, ucols, V, vstride, OUT, ostride, coef, st);
 }
 
 void launch_regen_sym(const KernelParams& kp, int pp, int level, const double* ax, const int* order, int64_t nrows,
-                      const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
+                      int64_t t0, const int64_t* uptr, const int* ucols, const double* V, int64_t vstride, double* OUT,
                       int64_t ostride, cudaStream_t st) {
   if (nrows <= 0) return;
   if (pp == 4)
-    sym_p<4>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, st);
+    sym_p<4>(kp, level, ax, order, nrows, t0, uptr, ucols, V, vstride, OUT, ostride, st);
   else
-    sym_p<6>(kp, level, ax, order, nrows, uptr, ucols, V, vstride, OUT, ostride, st);
+    sym_p<6>(kp, level, ax, order, nrows, t0, uptr, ucols, V, vstride, OUT, ostride, st);
 }
 
 void launch_near_weight(int sL, int L, const double* widths, const double* ub, int K_pad, double* V, int64_t nleaf,

@@ -10,7 +10,11 @@ each other, so the work per shard is identical).  Per matvec each shard
   2. exchange: all-gathers those buffers over NCCL / NVLink (each shard's part
               is a contiguous 1/world chunk of each buffer);
   3. remote : runs the gathered GEMMs of its own targets and the fused
-              downward pass, writing the f rows of its own leaf boxes.
+              downward pass, writing the f rows of its own leaf boxes.  On a
+              mapped grid with the symmetric regeneration every unordered
+              block pair is evaluated by one shard, whose column sums land in
+              other shards' rows: the full-size accumulators are
+              sum-reduce-scattered between the contract and the expand half.
 
 The reference has no parallel matvec; the exchange volume is
 |u| + sum_l |W_l| (19 MB for config 4), against milliseconds of fp64 GEMM.
@@ -46,6 +50,24 @@ def allgather_chunks(bufs, rank: int, world: int, group=None) -> None:
             dist.all_gather(outs, mine.clone(), group=group)
 
 
+def reduce_scatter_chunks(bufs, rank: int, world: int, group=None) -> None:
+    """In-place sum-reduce-scatter of each 1-D tensor: afterwards chunk
+    `rank` holds the sum over all ranks' buffers (other chunks are scratch).
+    NCCL uses reduce_scatter_tensor; other backends an all-reduce."""
+    import torch.distributed as dist
+    for b in bufs:
+        n = b.numel()
+        if n % world:
+            raise ValueError("reduce buffer not divisible by the world size")
+        c = n // world
+        if b.is_cuda and dist.get_backend(group) == "nccl":
+            out = b.new_empty(c)
+            dist.reduce_scatter_tensor(out, b, op=dist.ReduceOp.SUM, group=group)
+            b[rank * c:(rank + 1) * c].copy_(out)
+        else:
+            dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+
+
 def shard_ranges(M: int, rank: int, world: int):
     """Owned cluster id range of a level with M clusters."""
     if M % world:
@@ -75,6 +97,7 @@ class ShardedOperator:
             _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
         self.local = op
         self._xbufs = {}
+        self._rbufs = {}
 
     # exchange buffers are torch tensors so torch.distributed can move them
     def exchange_buffers(self, R: int):
@@ -92,6 +115,26 @@ class ShardedOperator:
         _lib.check(_lib.lib().htlr_bind_exchange(self.local._plan, R, ptrs, len(bufs)))
         return bufs
 
+    def reduce_buffers(self, R: int):
+        """Full-size accumulators the shards sum between the contract and the
+        expand half of the remote phase (mapped grid, symmetric
+        regeneration); empty for every other plan."""
+        import torch
+        if R not in self._rbufs:
+            L = _lib.lib()
+            cnt = ctypes.c_int64()
+            _lib.check(L.htlr_reduce_info(self.local._plan, R, ctypes.byref(cnt), None, 0))
+            sizes = np.zeros(max(1, cnt.value), dtype=np.int64)
+            _lib.check(L.htlr_reduce_info(self.local._plan, R, ctypes.byref(cnt), sizes.ctypes.data, cnt.value))
+            bufs = [torch.zeros(int(b) // 8, dtype=torch.float64, device=f"cuda:{self.device}")
+                    for b in sizes[:cnt.value]]
+            self._rbufs[R] = bufs
+        bufs = self._rbufs[R]
+        if bufs:
+            ptrs = (ctypes.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+            _lib.check(_lib.lib().htlr_bind_reduce(self.local._plan, R, ptrs, len(bufs)))
+        return bufs
+
     def shard_info(self) -> dict:
         lo, hi, pairs, fl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
         _lib.check(_lib.lib().htlr_shard_info(self.local._plan, ctypes.byref(lo), ctypes.byref(hi),
@@ -107,14 +150,38 @@ class ShardedOperator:
             _lib.check(_lib.lib().htlr_matvec_local(self.local._plan, ctypes.c_void_p(ud.data_ptr()), R, st))
         return bufs
 
-    def remote_phase(self, ud, fd, R: int):
-        """GEMMs of the own targets + downward of the own leaf boxes."""
+    def contract_phase(self, ud, R: int):
+        """GEMMs / regenerated blocks of the own targets into the
+        accumulators; returns the buffers to sum over the shards (maybe [])."""
         import torch
         self.exchange_buffers(R)
+        rbufs = self.reduce_buffers(R)
         with torch.cuda.device(self.device):
             st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-            _lib.check(_lib.lib().htlr_matvec_remote(self.local._plan, ctypes.c_void_p(ud.data_ptr()),
+            _lib.check(_lib.lib().htlr_matvec_contract(self.local._plan, ctypes.c_void_p(ud.data_ptr()), R, st))
+        return rbufs
+
+    def expand_phase(self, ud, fd, R: int):
+        """Downward pass of the own leaf boxes into fd."""
+        import torch
+        self.exchange_buffers(R)
+        self.reduce_buffers(R)
+        with torch.cuda.device(self.device):
+            st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            _lib.check(_lib.lib().htlr_matvec_expand(self.local._plan, ctypes.c_void_p(ud.data_ptr()),
                                                      ctypes.c_void_p(fd.data_ptr()), R, st))
+
+    def remote_phase(self, ud, fd, R: int, reduce=None):
+        """GEMMs of the own targets + downward of the own leaf boxes.  A
+        sharded symmetric plan sums its accumulators over the shards in
+        between: NCCL reduce-scatter, or `reduce(self, bufs)` (tests)."""
+        rbufs = self.contract_phase(ud, R)
+        if rbufs:
+            if reduce is not None:
+                reduce(self, rbufs)
+            else:
+                reduce_scatter_chunks(rbufs, self.rank, self.world, self.group)
+        self.expand_phase(ud, fd, R)
 
     def matmat(self, U, exchange=None):
         """F rows of this shard's leaf boxes (other rows 0).  `exchange`
@@ -138,8 +205,7 @@ class ShardedOperator:
                 exchange(self, bufs)
             elif self.world > 1:
                 allgather_chunks(bufs, self.rank, self.world, self.group)
-            _lib.check(L.htlr_matvec_remote(self.local._plan, ctypes.c_void_p(ud.data_ptr()),
-                                            ctypes.c_void_p(fd.data_ptr()), R, st))
+        self.remote_phase(ud, fd, R)
         out = fd.reshape(-1) if vec else fd
         return out.cpu() if host else out
 

@@ -77,27 +77,39 @@ def test_mapped_blocks_vs_oracle():
         assert rel(H.materialize(blk), ref) <= TOL
 
 
-def test_mapped_sharded_equals_single():
+@pytest.mark.parametrize("R", [1, 2])
+def test_mapped_sharded_equals_single(R):
+    """Eight shards on one GPU, the NCCL all-gather and reduce-scatter replayed
+    as device copies: R = 1 runs the symmetric regeneration (every unordered
+    pair on one shard, full-size accumulators summed between the contract and
+    the expand half), R = 2 the one-sided kernels."""
     cfg, grid, pb, _ = problem(0)
     single = H.construct(cfg, grid)
-    u = np.random.default_rng(7).standard_normal(grid.num_points)
-    ref = H.matvec(single, u)
+    U = np.random.default_rng(7).standard_normal((grid.num_points, R))
+    ref = H.matmat(single, U)
     world = 8
     ops = [ShardedOperator(cfg, grid, r, world, device=0) for r in range(world)]
-    ud = torch.from_numpy(u).cuda().reshape(-1, 1)
-    bufs = [op.local_phase(ud, 1) for op in ops]
+    ud = torch.from_numpy(U).cuda().contiguous()
+    bufs = [op.local_phase(ud, R) for op in ops]
     for i in range(len(bufs[0])):
         c = bufs[0][i].numel() // world
         for r in range(world):
             for q in range(world):
                 if q != r:
                     bufs[q][i][r * c:(r + 1) * c].copy_(bufs[r][i][r * c:(r + 1) * c])
+    rb = [op.contract_phase(ud, R) for op in ops]
+    assert bool(rb[0]) == (R == 1)
+    for i in range(len(rb[0])):
+        tot = sum(b[i] for b in rb)
+        c = tot.numel() // world
+        for r in range(world):
+            rb[r][i][r * c:(r + 1) * c].copy_(tot[r * c:(r + 1) * c])
     total = torch.zeros_like(ud)
     for op in ops:
         fd = torch.zeros_like(ud)
-        op.remote_phase(ud, fd, 1)
+        op.expand_phase(ud, fd, R)
         total += fd
-    assert rel(total.cpu().numpy().ravel(), ref) <= 1e-13
+    assert rel(total.cpu().numpy(), ref) <= 1e-13
 
 
 def test_cfg5_runs_and_is_symmetric():

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the sharded path's host
 logic: shard ownership from the C++ plan (host-only, no device), balance and
-coverage of the target lists, and the all-gather exchange of Morton-contiguous
-chunks used between the local and remote phases."""
+coverage of the target lists, the all-gather exchange of Morton-contiguous
+chunks used between the local and remote phases, and the sum-reduce-scatter
+of the symmetric mapped path."""
 
 import ctypes
 import os
@@ -51,7 +52,7 @@ def worker(rank, world, port, out):
     import sys
     sys.path.insert(0, ROOT)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2508_05958_b200.multi import allgather_chunks
+    from paper_2508_05958_b200.multi import allgather_chunks, reduce_scatter_chunks
     lo, hi, pairs, fl, sizes = host_shard(rank, world)
     # exchange: every rank fills its own chunk, the all-gather completes the rest
     bufs = [torch.full((int(b) // 8,), -1.0, dtype=torch.float64) for b in sizes]
@@ -64,6 +65,15 @@ def worker(rank, world, port, out):
         c = b.numel() // world
         for r in range(world):
             ok &= bool(torch.equal(b[r * c:(r + 1) * c], torch.arange(c, dtype=torch.float64) + 1000.0 * r))
+    # reduction of the symmetric mapped path: every rank adds into all rows,
+    # afterwards its own chunk holds the sum over the ranks
+    red = [torch.arange(12 * world, dtype=torch.float64) * (rank + 1) for _ in range(2)]
+    reduce_scatter_chunks(red, rank, world)
+    tot = sum(r + 1 for r in range(world))
+    for b in red:
+        c = b.numel() // world
+        ok &= bool(torch.equal(b[rank * c:(rank + 1) * c],
+                               torch.arange(rank * c, (rank + 1) * c, dtype=torch.float64) * tot))
     t = torch.tensor([lo, hi, pairs, fl, float(ok)], dtype=torch.float64)
     gathered = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(gathered, t)

@@ -1,3 +1,3 @@
-for w in cfg1 cfg2 cfg3 cfg4 cfg5; do python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/bench_$w.json 2>gpurun_out/bench_$w.err; done
-python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_cfg4.json 2>gpurun_out/bench_ref.err
-python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err
+python -m pytest tests/test_gpu_mapped.py tests/test_gpu_multi.py -x -q 2>&1 | tail -2
+PYTHONPATH=. python tools/quick_time.py cfg5
+python bench.py --workload cfg5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b5.json 2>gpurun_out/b5.err
