@@ -295,7 +295,7 @@ __device__ __forceinline__ void mma8x8x4(double (&c)[2], double a, double b) {
 // units keep every SM sub-partition equally busy for P = 216, which the
 // 128-row tiles of the wide kernel cannot (216 = 128 + 88).
 // ---------------------------------------------------------------------------
-template <int M8, int STAGES, int CW>
+template <int M8, int STAGES, int CW, int TN>
 __global__ void __launch_bounds__(9 * 32, 1)
     gemm_thin_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                      double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(9 * 32, 1)
   // and all M8 row tiles (64 columns per item); CW = 2 / 1 (16 / 8 columns
   // per item, for passes with few pairs per matrix) split the row tiles
   // round-robin over 4 / 8 warps so every warp has work
-  constexpr int MP = 8 * M8, NT = 8 * CW, KC = kKC, BST = KC + 4, NCW = 8;
+  // TN n8 column tiles per warp (TN = 2: each A fragment feeds two DMMAs)
+  constexpr int MP = 8 * M8, NT = 8 * CW * TN, KC = kKC, BST = KC + 4, NCW = 8;
   constexpr int RG = 8 / CW, MJ = (M8 + RG - 1) / RG;
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;                      // STAGES x MP*KC
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     return;
   }
   const int g8 = lane >> 2, t = lane & 3;
-  const int n0 = (warp % CW) * 8, rw = warp / CW;
+  const int n0 = (warp % CW) * 8 * TN, rw = warp / CW;
   uint32_t g = 0;
   ItemInfo itn{};
   if (blockIdx.x < nitems) itn = item_info(tasks, blockIdx.x, 1, R, Rc, NT);
@@ -380,19 +381,23 @@ __global__ void __launch_bounds__(9 * 32, 1)
     const ItemInfo it = itn;
     if (item + (int)gridDim.x < nitems) itn = item_info(tasks, item + gridDim.x, 1, R, Rc, NT);
     const bool active = n0 < it.ncols;
-    int64_t cbase[2];
+    int64_t cbase[TN][2];
 #pragma unroll
-    for (int cix = 0; cix < 2; ++cix) {
-      const int n = n0 + 2 * t + cix;
-      cbase[cix] = -1;
-      if (n < it.ncols) {
-        const int j = n / Rc, r = it.r0 + n % Rc;
-        cbase[cix] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
+    for (int ni = 0; ni < TN; ++ni)
+#pragma unroll
+      for (int cix = 0; cix < 2; ++cix) {
+        const int n = n0 + ni * 8 + 2 * t + cix;
+        cbase[ni][cix] = -1;
+        if (n < it.ncols) {
+          const int j = n / Rc, r = it.r0 + n % Rc;
+          cbase[ni][cix] = ((int64_t)pairs[it.pair_begin + j].x * R + r) * ldc;
+        }
       }
-    }
-    double acc[MJ][2];
+    double acc[MJ][TN][2];
 #pragma unroll
-    for (int i = 0; i < MJ; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int i = 0; i < MJ; ++i)
+#pragma unroll
+      for (int ni = 0; ni < TN; ++ni) acc[i][ni][0] = acc[i][ni][1] = 0.0;
     const int nstage = it.nkc * kKC / KC;
     for (int kc = 0; kc < nstage; ++kc, ++g) {
       const int s = g % STAGES;
@@ -402,11 +407,17 @@ __global__ void __launch_bounds__(9 * 32, 1)
         const double* cB = sB + s * NT * BST + (n0 + g8) * BST + t;
 #pragma unroll
         for (int k4 = 0; k4 < KC / 4; ++k4) {
-          const double b = cB[k4 * 4];
+          double b[TN];
+#pragma unroll
+          for (int ni = 0; ni < TN; ++ni) b[ni] = cB[ni * 8 * BST + k4 * 4];
           const double* pa = cA + k4 * (M8 * 32) + lane;
 #pragma unroll
           for (int i = 0; i < MJ; ++i)
-            if (rw + RG * i < M8) mma8x8x4(acc[i], pa[(rw + RG * i) * 32], b);
+            if (rw + RG * i < M8) {
+              const double a = pa[(rw + RG * i) * 32];
+#pragma unroll
+              for (int ni = 0; ni < TN; ++ni) mma8x8x4(acc[i][ni], a, b[ni]);
+            }
         }
       }
       __syncwarp();
@@ -414,32 +425,35 @@ __global__ void __launch_bounds__(9 * 32, 1)
     }
     if (!active) continue;
 #pragma unroll
-    for (int cix = 0; cix < 2; ++cix) {
-      if (cbase[cix] < 0) continue;
-      double* cc = C + cbase[cix];
+    for (int ni = 0; ni < TN; ++ni)
 #pragma unroll
-      for (int i = 0; i < MJ; ++i) {
-        const int m = (rw + RG * i) * 8 + g8;
-        if (rw + RG * i < M8 && m < M_valid) atomicAdd(cc + m, acc[i][cix]);
+      for (int cix = 0; cix < 2; ++cix) {
+        if (cbase[ni][cix] < 0) continue;
+        double* cc = C + cbase[ni][cix];
+#pragma unroll
+        for (int i = 0; i < MJ; ++i) {
+          const int m = (rw + RG * i) * 8 + g8;
+          if (rw + RG * i < M8 && m < M_valid) atomicAdd(cc + m, acc[i][ni][cix]);
+        }
       }
-    }
   }
 }
 
-template <int M8, int STAGES, int CW>
+template <int M8, int STAGES, int CW, int TN = 1>
 static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, double* C, const GemmTask* tasks,
                           int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
                           cudaStream_t st) {
   constexpr int MP = 8 * M8, KC = kKC;
   const size_t smem =
-      sizeof(double) * STAGES * (size_t)(MP * KC + 8 * CW * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      sizeof(double) * STAGES * (size_t)(MP * KC + 8 * CW * TN * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
+  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES, CW, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
   if (ntasks == 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = ntasks < sms ? ntasks : sms;
-  gemm_thin_kernel<M8, STAGES, CW><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
+  gemm_thin_kernel<M8, STAGES, CW, TN><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
                                                             K_pad, M_valid, ldc);
 }
 
@@ -455,6 +469,17 @@ int gemm_stage_chunks(int MT, int K_pad) {
 
 int thin_m8_supported(int m8) { return m8 == 5 || m8 == 8 || m8 == 16 || m8 == 27; }
 
+// 64-column thin items: 4 column warps x 2 n8 tiles (each A fragment feeds
+// two DMMAs; measured cfg 3 coupling pass -2%) or 8 x 1 (HTLR_THIN_TN=1)
+static int thin_tn() {
+  static int tn = -1;
+  if (tn < 0) {
+    const char* e = std::getenv("HTLR_THIN_TN");
+    tn = (e && e[0] == '1') ? 1 : 2;
+  }
+  return tn;
+}
+
 template <int M8, int STAGES>
 static void launch_thin_cw(int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                            const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
@@ -463,6 +488,8 @@ static void launch_thin_cw(int NT, const double* A, int64_t mat_stride, const do
     launch_thin_t<M8, STAGES, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
   else if (NT == 16)
     launch_thin_t<M8, STAGES, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
+  else if (thin_tn() == 2)
+    launch_thin_t<M8, STAGES, 4, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
   else
     launch_thin_t<M8, STAGES, 8>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
 }
