@@ -287,6 +287,26 @@ __device__ __forceinline__ void mma8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// One pipeline stage of a thin-kernel warp: row tiles rw, rw + RG, ... (NJ of
+// them) x TN n8 column tiles, K = KC in m8n8k4 steps.
+template <int NJ, int MJ, int TN, int KC, int M8, int BST>
+__device__ __forceinline__ void thin_stage(double (&acc)[MJ][TN][2], const double* cA, const double* cB, int lane,
+                                           int rw, int RG) {
+#pragma unroll
+  for (int k4 = 0; k4 < KC / 4; ++k4) {
+    double b[TN];
+#pragma unroll
+    for (int ni = 0; ni < TN; ++ni) b[ni] = cB[ni * 8 * BST + k4 * 4];
+    const double* pa = cA + k4 * (M8 * 32) + lane;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+      const double a = pa[(rw + RG * i) * 32];
+#pragma unroll
+      for (int ni = 0; ni < TN; ++ni) mma8x8x4(acc[i][ni], a, b[ni]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // "thin" variant for matrices of at most 256 rows (p^d = 216, 64, 36, ...):
 // one item covers ALL rows of its matrix (M_pad = 8*M8, no row-tile padding
@@ -405,20 +425,13 @@ __global__ void __launch_bounds__(9 * 32, 1)
       if (active) {
         const double* cA = sA + s * MP * KC;
         const double* cB = sB + s * NT * BST + (n0 + g8) * BST + t;
-#pragma unroll
-        for (int k4 = 0; k4 < KC / 4; ++k4) {
-          double b[TN];
-#pragma unroll
-          for (int ni = 0; ni < TN; ++ni) b[ni] = cB[ni * 8 * BST + k4 * 4];
-          const double* pa = cA + k4 * (M8 * 32) + lane;
-#pragma unroll
-          for (int i = 0; i < MJ; ++i)
-            if (rw + RG * i < M8) {
-              const double a = pa[(rw + RG * i) * 32];
-#pragma unroll
-              for (int ni = 0; ni < TN; ++ni) mma8x8x4(acc[i][ni], a, b[ni]);
-            }
-        }
+        // warps whose last round-robin row tile is past M8 take the MJ - 1
+        // body (warp-uniform branch: a predicated-off DMMA would still
+        // occupy the tensor pipe)
+        if (rw + RG * (MJ - 1) < M8)
+          thin_stage<MJ, MJ, TN, KC, M8, BST>(acc, cA, cB, lane, rw, RG);
+        else
+          thin_stage<MJ - 1, MJ, TN, KC, M8, BST>(acc, cA, cB, lane, rw, RG);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
