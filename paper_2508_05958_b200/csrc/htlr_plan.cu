@@ -1309,9 +1309,12 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     const int Rc = std::min(R, NT);
     const double* B = ps.from_ub ? cx.ub : cx.W[i];
     double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
-    // algorithmic work: 2 P^2 per (pair, rhs); bytes: every unique matrix once + B gather + C
+    // algorithmic work: 2 P^2 per (pair, rhs); HBM bytes: every unique
+    // matrix once + the level's source vectors B and accumulators C once (the
+    // per-pair gathers of B are L2 traffic)
+    const double ncl = (double)pl->levels[ps.level].nclusters;
     double flops = 2.0 * (double)ps.P * ps.P * (double)ps.npairs * R;
-    double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ps.npairs;
+    double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ncl;
     if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, NT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
                       slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st);
