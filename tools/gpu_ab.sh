@@ -1,3 +1,2 @@
-python -m pytest tests/test_gpu_edge.py tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-python bench.py --workload cfg3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b3.json 2>gpurun_out/b3.err
-python bench.py --workload cfg2 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b2.json 2>gpurun_out/b2.err
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for v in 0 1; do HTLR_PDL=$v PYTHONPATH=. python tools/quick_time.py cfg1 cfg2 cfg3 cfg4 cfg5; done
