@@ -12,6 +12,69 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
   return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
+// fp32 seed (MUFU.RSQ on the rounded argument) widened by integer ops, one
+// Newton step in fp64 on the half argument: 6 fp64 pipe ops per entry with
+// the two sums, relative error <= 1.5 (1.6e-7)^2 ~ 4e-14 (biased low)
+__device__ __forceinline__ double rsqrt_newton_half(double hx) {
+  float yf;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(__double2float_rn(hx)));
+  yf *= 0.70710678118654752f;   // rsqrt(2 hx)
+  const unsigned b = __float_as_uint(yf);
+  const double y0 = __hiloint2double((int)((b >> 3) + (896u << 20)), (int)(b << 29));
+  return y0 * fma(-hx, y0 * y0, 1.5);
+}
+
+template <int R, int C, int MODE>
+__global__ void probe2(const double* in, double* out, int iters) {
+  double dx[R][C], vc[C], wt[R], ra[R], ca[C];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    wt[r] = in[(t + r) & 1023];
+    ra[r] = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) dx[r][c] = 1.0 + in[(t + r * C + c) & 1023];
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    vc[c] = in[(t * 3 + c) & 1023];
+    ca[c] = 0;
+  }
+  double yz = 0.5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double kv;
+        if (MODE == 0) kv = rsqrt_pos(dx[r][c] + yz);
+        else kv = rsqrt_newton_half(dx[r][c] + yz);
+        ra[r] = fma(kv, vc[c], ra[r]);
+        ca[c] = fma(kv, wt[r], ca[c]);
+      }
+    yz += 1e-3;
+  }
+  double s = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) s += ra[r];
+#pragma unroll
+  for (int c = 0; c < C; ++c) s += ca[c];
+  out[t] = s;
+}
+
+__global__ void accuracy(double* out) {
+  // max relative error of rsqrt_newton_half(x/2) against 1/sqrt(x) over a sweep
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double worst = 0;
+  for (int i = 0; i < 4096; ++i) {
+    const double x = 1e-6 + (double)(t * 4096 + i) * 3.0 / (256.0 * 256 * 4096);
+    const double ref = 1.0 / sqrt(x);
+    const double e = fabs(rsqrt_newton_half(0.5 * x) - ref) / ref;
+    worst = fmax(worst, e);
+  }
+  out[t] = worst;
+}
+
 template <int R, int C>
 __global__ void probe(const double* in, double* out, int iters) {
   double dx[R][C], vc[C], wt[R], ra[R], ca[C];
@@ -66,6 +129,24 @@ void run(int blocks, int threads, const double* in, double* out) {
          "\"dp_ops_per_entry\": 8}\n", R, C, blocks, threads, ent / (ms * 1e-3));
 }
 
+template <int MODE>
+void run2(int blocks, int threads, const double* in, double* out) {
+  const int iters = 2000;
+  probe2<3, 6, MODE><<<blocks, threads>>>(in, out, 10);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  probe2<3, 6, MODE><<<blocks, threads>>>(in, out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double ent = (double)blocks * threads * iters * 18;
+  printf("{\"probe\": \"regen_entry_%s\", \"blocks\": %d, \"threads\": %d, \"entries_per_s\": %.4e}\n",
+         MODE == 0 ? "rsq64h_3rd_order" : "f32_seed_newton", blocks, threads, ent / (ms * 1e-3));
+}
+
 int main() {
   double *in, *out;
   cudaMalloc(&in, 1024 * sizeof(double));
@@ -78,5 +159,16 @@ int main() {
   run<3, 6>(148 * 4, 288, in, out);
   run<6, 6>(148 * 4, 256, in, out);
   run<2, 6>(148 * 4, 256, in, out);
+  for (int m = 0; m < 2; ++m)
+    for (int bpsm : {2, 4, 8}) {
+      if (m == 0) run2<0>(148 * bpsm, 288, in, out);
+      else run2<1>(148 * bpsm, 288, in, out);
+    }
+  accuracy<<<256, 256>>>(out);
+  double h[65536];
+  cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+  double w = 0;
+  for (double v : h) w = v > w ? v : w;
+  printf("{\"probe\": \"rsqrt_newton_half_max_rel_error\", \"value\": %.3e}\n", w);
   return 0;
 }
