@@ -46,7 +46,7 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + headers):
-            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-c", s, "-o", o])
+            jobs.append(["g++", "-O2", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-c", s, "-o", o])
         objs.append(o)
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
@@ -63,7 +63,7 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> str:
         for fut in [ex.submit(_run, j) for j in jobs]:
             fut.result()
     if force or _stale(OUT, objs):
-        _run([NVCC, "-shared", *ARCH, "-o", OUT, *objs, "-lcudart"])
+        _run([NVCC, "-shared", *ARCH, "-o", OUT, *objs, "-lcudart", "-Xcompiler", "-pthread"])
     return OUT
 
 

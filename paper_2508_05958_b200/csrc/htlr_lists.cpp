@@ -17,6 +17,10 @@
 #include "htlr_lists.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
+
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -113,11 +117,17 @@ namespace {
 
 struct Builder {
   const TreeSpec& spec;
-  Tree& tree;
+  const Tree& tree;
+  std::vector<LeafRec>* out;   // append here, or ...
+  LeafRec* dst = nullptr;      // ... write here (exact size known), or only count
+  size_t count = 0;
   int combos[8][3];
   int ncombo;
+  // split > 0: stop the recursion at that level and record the pending
+  // subtree (kind -1) instead, in DFS position
+  int split = -1;
 
-  explicit Builder(const TreeSpec& s, Tree& t) : spec(s), tree(t) {
+  Builder(const TreeSpec& s, const Tree& t, std::vector<LeafRec>* o) : spec(s), tree(t), out(o) {
     // np.ndindex(*([2] * d)): last dimension varies fastest
     ncombo = 1 << spec.d;
     for (int i = 0; i < ncombo; ++i) {
@@ -145,6 +155,10 @@ struct Builder {
       push(1, level, tc, sc);
       return;
     }
+    if (level == split) {
+      push(-1, level, tc, sc);
+      return;
+    }
     int tk[3], sk[3];
     for (int si = 0; si < ncombo; ++si) {
       for (int a = 0; a < spec.d; ++a) sk[a] = 2 * sc[a] + combos[si][a];
@@ -155,7 +169,23 @@ struct Builder {
     }
   }
 
+  // the children of a pending subtree (its own node was visited already)
+  void expand(const LeafRec& r) {
+    int tk[3], sk[3];
+    for (int si = 0; si < ncombo; ++si) {
+      for (int a = 0; a < spec.d; ++a) sk[a] = 2 * r.sc[a] + combos[si][a];
+      for (int ti = 0; ti < ncombo; ++ti) {
+        for (int a = 0; a < spec.d; ++a) tk[a] = 2 * r.tc[a] + combos[ti][a];
+        visit(tk, sk, r.level + 1);
+      }
+    }
+  }
+
   void push(int kind, int level, const int* tc, const int* sc) {
+    if (!out && !dst) {
+      ++count;
+      return;
+    }
     LeafRec r;
     r.kind = kind;
     r.level = level;
@@ -163,11 +193,10 @@ struct Builder {
       r.tc[a] = a < spec.d ? tc[a] : 0;
       r.sc[a] = a < spec.d ? sc[a] : 0;
     }
-    tree.leaves.push_back(r);
-    if (kind == 0)
-      ++tree.num_adm;
+    if (dst)
+      dst[count++] = r;
     else
-      ++tree.num_near;
+      out->push_back(r);
   }
 };
 
@@ -214,9 +243,61 @@ int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
   int depth = 0;
   for (int s = spec.n; s > side; s /= 2) ++depth;
   out.depth = depth;
-  Builder b(spec, out);
+  // DFS down to a split level sequentially (the recursion's order), then the
+  // pending subtrees in parallel, concatenated in DFS position: the same
+  // leaf list as one sequential recursion
+  std::vector<LeafRec> top;
+  Builder b(spec, out, &top);
+  b.split = depth >= 3 ? 2 : (depth >= 2 ? 1 : -1);
   int root[3] = {0, 0, 0};
   b.visit(root, root, 0);
+  std::vector<size_t> pend;
+  for (size_t i = 0; i < top.size(); ++i)
+    if (top[i].kind < 0) pend.push_back(i);
+  // two parallel passes over the pending subtrees: count their leaves, then
+  // write them straight into their slots of the final array (no per-subtree
+  // vectors: their growth and the concatenation cost more than the walk)
+  std::vector<size_t> cnt(pend.size(), 0);
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const unsigned nthreads = (unsigned)std::max<size_t>(1, std::min<size_t>(hw, pend.size()));
+  auto parallel = [&](auto&& body) {
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t k = next++; k < pend.size(); k = next++) body(k);
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nthreads; ++t) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+  };
+  parallel([&](size_t k) {
+    Builder w(spec, out, nullptr);
+    w.expand(top[pend[k]]);
+    cnt[k] = w.count;
+  });
+  std::vector<size_t> pos(top.size() + 1, 0);
+  {
+    size_t k = 0, acc = 0;
+    for (size_t i = 0; i < top.size(); ++i) {
+      pos[i] = acc;
+      acc += top[i].kind >= 0 ? 1 : cnt[k++];
+    }
+    pos[top.size()] = acc;
+  }
+  out.leaves.resize(pos[top.size()]);
+  for (size_t i = 0; i < top.size(); ++i)
+    if (top[i].kind >= 0) out.leaves[pos[i]] = top[i];
+  parallel([&](size_t k) {
+    Builder w(spec, out, nullptr);
+    w.dst = out.leaves.data() + pos[pend[k]];
+    w.expand(top[pend[k]]);
+  });
+  for (const auto& r : out.leaves) {
+    if (r.kind == 0)
+      ++out.num_adm;
+    else
+      ++out.num_near;
+  }
   return 0;
 }
 

@@ -11,6 +11,8 @@
 //   permute_in -> upward (per level) -> gathered GEMM passes -> fused downward
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -87,8 +89,24 @@ struct Pass {
   bool to_y = false;       // C accumulator = Y (else H of `level`)
 };
 
+// Run body(i) for i in [0, n) on the host's cores (independent items).
+template <typename F>
+void parallel_for(size_t n, F&& body) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(hw, n));
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t i = next++; i < n; i = next++) body(i);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+}
+
 struct OffsetTable {
-  std::unordered_map<int64_t, int> id;   // packed offset -> id
+  std::unordered_map<int64_t, int> id;   // packed offset -> id (large levels)
+  std::vector<int> dense;                // packed offset -> id + 1 (0: none), when (2m+1)^d is small
   std::vector<std::array<int, 6>> rep;    // representative (tc, sc)
   std::vector<std::vector<std::pair<int, int>>> members;   // (tgt, src) per id
 };
@@ -452,21 +470,34 @@ int htlr_build_lists(htlr_plan* pl) {
   }
   if (pl->own_lo[pl->L] < 0)
     return fail(-1, "the leaf level has fewer boxes than shards (or not a multiple of them)");
+  auto key_range = [&](int m) {
+    int64_t r = 1;
+    for (int a = 0; a < d; ++a) r *= 2 * m + 1;
+    return r;
+  };
+  for (int l = 0; l <= pl->L; ++l)
+    if (key_range(pl->levels[l].m) <= (1 << 22)) pl->levels[l].adm.dense.assign(key_range(pl->levels[l].m), 0);
+  if (key_range(pl->levels[pl->L].m) <= (1 << 22)) pl->near.dense.assign(key_range(pl->levels[pl->L].m), 0);
   for (const auto& lf : tr.leaves) {
     OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
     const int m = pl->levels[lf.level].m;
-    int64_t key = pack_offset(lf.tc, lf.sc, d, m);
-    auto it = tab.id.find(key);
-    int id;
-    if (it == tab.id.end()) {
+    const int64_t key = pack_offset(lf.tc, lf.sc, d, m);
+    int id = -1;
+    if (!tab.dense.empty()) {
+      id = tab.dense[key] - 1;
+    } else {
+      auto it = tab.id.find(key);
+      if (it != tab.id.end()) id = it->second;
+    }
+    if (id < 0) {
       id = (int)tab.rep.size();
-      tab.id.emplace(key, id);
+      if (!tab.dense.empty())
+        tab.dense[key] = id + 1;
+      else
+        tab.id.emplace(key, id);
       tab.rep.push_back({lf.tc[0], lf.tc[1], lf.tc[2], lf.sc[0], lf.sc[1], lf.sc[2]});
       tab.members.emplace_back();
-    } else {
-      id = it->second;
     }
-    (void)m;
     const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
     const int64_t sl = htlr::morton_encode(lf.sc, d, lf.level);
     if (world > 1) {
@@ -539,15 +570,20 @@ int htlr_build_lists(htlr_plan* pl) {
     ps.RT = ps.MT < 0 ? 1 : ps.M_pad / ps.MT;
     ps.mat_stride = (int64_t)ps.M_pad * ps.K_pad;
     ps.seg.assign(1, 0);
-    std::vector<int2> pr;
-    for (const OffsetTable* tab : tabs) {
+    std::vector<const std::vector<std::pair<int, int>>*> mems;
+    for (const OffsetTable* tab : tabs)
       for (const auto& mem : tab->members) {
-        std::vector<std::pair<int, int>> v = mem;
-        std::sort(v.begin(), v.end());
-        for (auto& q : v) pr.push_back(make_int2(q.first, q.second));
-        ps.seg.push_back((int)pr.size());
+        mems.push_back(&mem);
+        ps.seg.push_back(ps.seg.back() + (int)mem.size());
       }
-    }
+    // every matrix's pairs sorted by (target, source), matrices in parallel
+    std::vector<int2> pr((size_t)ps.seg.back());
+    parallel_for(mems.size(), [&](size_t i) {
+      std::vector<std::pair<int, int>> v = *mems[i];
+      std::sort(v.begin(), v.end());
+      int2* o = pr.data() + ps.seg[i];
+      for (size_t k = 0; k < v.size(); ++k) o[k] = make_int2(v[k].first, v[k].second);
+    });
     ps.nmats = (int)ps.seg.size() - 1;
     ps.npairs = (int)pr.size();
     ps.pairs_host.swap(pr);
@@ -1767,8 +1803,9 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   const int d = pl->d, p = pl->p;
   const Level& lv = pl->levels[lf.level];
   const OffsetTable& tab = lf.kind == 0 ? lv.adm : pl->near;
-  int64_t key = pack_offset(lf.tc, lf.sc, d, lv.m);
-  int id = tab.id.at(key);
+  const int64_t key = pack_offset(lf.tc, lf.sc, d, lv.m);
+  const int id = tab.dense.empty() ? tab.id.at(key) : tab.dense[key] - 1;
+  if (id < 0) return fail(2, "leaf offset missing from the plan's tables");
   const Pass* ps = nullptr;
   int mat = id;
   if (lf.kind == 0) {
