@@ -73,46 +73,62 @@ __global__ void mapped_factor_kernel(const MappedFactorJob* __restrict__ jobs, i
 // ---------------------------------------------------------------------------
 // per-point cell integral of k(x_i, .) (the Nystrom diagonal)
 // ---------------------------------------------------------------------------
-__global__ void mapped_diag_kernel(KernelParams kp, int d, int n, int q, const double* __restrict__ gx,
-                                   const double* __restrict__ gw, const double* __restrict__ bounds,
+template <int KIND, int Q>
+__global__ void mapped_diag_kernel(KernelParams kp, int d, int n, int q_rt, const double* __restrict__ gx_g,
+                                   const double* __restrict__ gw_g, const double* __restrict__ bounds,
                                    const double* __restrict__ coords, double* __restrict__ out, int64_t npts) {
-  __shared__ double red[256];
-  for (int64_t pt = blockIdx.x; pt < npts; pt += gridDim.x) {
+  // one warp per point: 2^d corner boxes x d Duffy pyramids (warp-uniform
+  // loops) x q^d Gauss points of the radially graded rule (lanes), shuffle
+  // reduction; k = coef * shape(r^2) with the division-free shapes of the
+  // regeneration kernels.  Q = q as a constant turns the Gauss-index splits
+  // into multiplies (0: runtime q).
+  const int q = Q ? Q : q_rt;
+  __shared__ double gx[64], gw[64];
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    gx[i] = gx_g[i];
+    gw[i] = gw_g[i];
+  }
+  __syncthreads();
+  const double nid = -1.0 / kp.denom;
+  const double coef = kernel_coef(kp);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int qd = (d == 2) ? q * q : q * q * q;
+  const int ncorner = 1 << d;
+  for (int64_t pt = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pt < npts; pt += warps) {
     int idx[3] = {(int)(pt % n), (int)((pt / n) % n), d == 3 ? (int)(pt / ((int64_t)n * n)) : 0};
-    double lo_e[3], hi_e[3];
+    double lo_e[3] = {0, 0, 0}, hi_e[3] = {0, 0, 0};
     for (int a = 0; a < d; ++a) {
       const double x = coords[idx[a]];
       lo_e[a] = x - bounds[idx[a]];
       hi_e[a] = bounds[idx[a] + 1] - x;
     }
-    const int qd = (d == 2) ? q * q : q * q * q;
-    const int ncorner = 1 << d;
-    const int total = ncorner * d * qd;
     double acc = 0.0;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int pidx = e % qd, axis = (e / qd) % d, corner = e / (qd * d);
-      const int ii[3] = {pidx % q, (pidx / q) % q, pidx / (q * q)};
-      const double tt = gx[ii[axis]];
-      const double t = tt * tt * tt;
-      double w = 1.0, vol = 1.0;
-      double pt3[3] = {0, 0, 0}, zero[3] = {0, 0, 0};
+    for (int corner = 0; corner < ncorner; ++corner) {
+      double ext[3] = {0, 0, 0}, vol = 1.0;
       for (int a = 0; a < d; ++a) {
-        const double ext = ((corner >> (d - 1 - a)) & 1) ? hi_e[a] : lo_e[a];
-        vol = vol * ext;
-        pt3[a] = (a == axis) ? ext * t : ext * t * gx[ii[a]];
-        w = w * ((a == axis) ? 3.0 * (tt * tt) * gw[ii[a]] : gw[ii[a]]);
+        ext[a] = ((corner >> (d - 1 - a)) & 1) ? hi_e[a] : lo_e[a];
+        vol = vol * ext[a];
       }
-      const double jac = vol * ((d == 2) ? t : t * t);
-      acc += kernel_from_r2(kp, r2_of(d, zero, pt3)) * (jac * w);
+      for (int axis = 0; axis < d; ++axis) {
+        for (int pidx = lane; pidx < qd; pidx += 32) {
+          const int ii[3] = {pidx % q, (pidx / q) % q, pidx / (q * q)};
+          const double tt = gx[ii[axis]];
+          const double t = tt * tt * tt;
+          double w = 1.0, r2 = 0.0;
+          for (int a = 0; a < d; ++a) {
+            const double c = (a == axis) ? ext[a] * t : ext[a] * t * gx[ii[a]];
+            r2 = __dadd_rn(r2, __dmul_rn(c, c));
+            w = w * ((a == axis) ? 3.0 * (tt * tt) * gw[ii[a]] : gw[ii[a]]);
+          }
+          const double jac = vol * ((d == 2) ? t : t * t);
+          acc += kernel_shape<KIND>(r2, nid) * (jac * w);
+        }
+      }
     }
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-      if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) out[pt] = red[0];
-    __syncthreads();
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) out[pt] = coef * acc;
   }
 }
 
@@ -367,10 +383,90 @@ void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_int
   mapped_factor_kernel<<<(total_intervals + 63) / 64, 64, 0, st>>>(jobs, njobs, bounds, coords, widths, p);
 }
 
+// 3-D fast path (q = Q): the point-independent factors of every (pyramid
+// axis, Gauss point) pair -- the graded coordinate factors f_a and the weight
+// t^2 * prod(w) -- are tabulated once per CTA in shared memory, so an
+// evaluation is r^2 = sum (ext_a f_a)^2, one shape evaluation and one FMA.
+template <int KIND, int Q>
+__global__ void __launch_bounds__(256) mapped_diag3_kernel(KernelParams kp, int n, const double* __restrict__ gx_g,
+                                                          const double* __restrict__ gw_g,
+                                                          const double* __restrict__ bounds,
+                                                          const double* __restrict__ coords,
+                                                          double* __restrict__ out, int64_t npts) {
+  constexpr int QD = Q * Q * Q;
+  extern __shared__ double tab[];   // [axis][pidx] x {f0, f1, f2, wt}
+  for (int e = threadIdx.x; e < 3 * QD; e += blockDim.x) {
+    const int axis = e / QD, pidx = e % QD;
+    const int ii[3] = {pidx % Q, (pidx / Q) % Q, pidx / (Q * Q)};
+    const double tt = gx_g[ii[axis]];
+    const double t = tt * tt * tt;
+    double w = 1.0;
+    for (int a = 0; a < 3; ++a) {
+      tab[e * 4 + a] = (a == axis) ? t : t * gx_g[ii[a]];
+      w = w * ((a == axis) ? 3.0 * (tt * tt) * gw_g[ii[a]] : gw_g[ii[a]]);
+    }
+    tab[e * 4 + 3] = (t * t) * w;
+  }
+  __syncthreads();
+  const double nid = -1.0 / kp.denom;
+  const double coef = kernel_coef(kp);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t pt = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pt < npts; pt += warps) {
+    const int idx[3] = {(int)(pt % n), (int)((pt / n) % n), (int)(pt / ((int64_t)n * n))};
+    double lo_e[3], hi_e[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double x = coords[idx[a]];
+      lo_e[a] = x - bounds[idx[a]];
+      hi_e[a] = bounds[idx[a] + 1] - x;
+    }
+    double acc = 0.0;
+#pragma unroll 1
+    for (int corner = 0; corner < 8; ++corner) {
+      const double e0 = (corner & 4) ? hi_e[0] : lo_e[0];
+      const double e1 = (corner & 2) ? hi_e[1] : lo_e[1];
+      const double e2 = (corner & 1) ? hi_e[2] : lo_e[2];
+      const double vol = (e0 * e1) * e2;
+      for (int e = lane; e < 3 * QD; e += 32) {
+        const double2 f01 = *reinterpret_cast<const double2*>(tab + e * 4);
+        const double2 f2w = *reinterpret_cast<const double2*>(tab + e * 4 + 2);
+        const double c0 = e0 * f01.x, c1 = e1 * f01.y, c2 = e2 * f2w.x;
+        double r2 = __dmul_rn(c0, c0);
+        r2 = __dadd_rn(r2, __dmul_rn(c1, c1));
+        r2 = __dadd_rn(r2, __dmul_rn(c2, c2));
+        acc = fma(kernel_shape<KIND>(r2, nid), vol * f2w.y, acc);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) out[pt] = coef * acc;
+  }
+}
+
+template <int KIND>
+static void mapped_diag_k(const KernelParams& kp, int d, int n, int q, const double* gx, const double* gw,
+                          const double* bounds, const double* coords, double* out, int64_t npts, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((npts + 7) / 8, 148 * 16);
+  if (q == 10 && d == 3) {
+    const size_t smem = sizeof(double) * 4 * 3 * 1000;
+    cudaFuncSetAttribute(mapped_diag3_kernel<KIND, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    mapped_diag3_kernel<KIND, 10><<<std::min(grid, 148 * 2), 256, smem, st>>>(kp, n, gx, gw, bounds, coords, out,
+                                                                             npts);
+  } else if (q == 10)
+    mapped_diag_kernel<KIND, 10><<<grid, 256, 0, st>>>(kp, d, n, q, gx, gw, bounds, coords, out, npts);
+  else
+    mapped_diag_kernel<KIND, 0><<<grid, 256, 0, st>>>(kp, d, n, q, gx, gw, bounds, coords, out, npts);
+}
+
 void launch_mapped_diag(const KernelParams& kp, int d, int n, int q, const double* gx, const double* gw,
                         const double* bounds, const double* coords, double* out, int64_t npts, cudaStream_t st) {
-  int grid = (int)std::min<int64_t>(npts, 148 * 16);
-  mapped_diag_kernel<<<grid, 256, 0, st>>>(kp, d, n, q, gx, gw, bounds, coords, out, npts);
+  if (kp.kind == 0)
+    mapped_diag_k<0>(kp, d, n, q, gx, gw, bounds, coords, out, npts, st);
+  else if (kp.kind == 1)
+    mapped_diag_k<1>(kp, d, n, q, gx, gw, bounds, coords, out, npts, st);
+  else
+    mapped_diag_k<2>(kp, d, n, q, gx, gw, bounds, coords, out, npts, st);
 }
 
 static int regen_threads(int P) { return ((P + 31) / 32) * 32; }

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <chrono>
 #include <thread>
 #include <cmath>
 #include <cstdio>
@@ -87,6 +88,33 @@ struct Pass {
   std::map<int, int> task_nt;                     // columns per item of the R slot's tasks
   bool from_ub = false;    // B operand = leaf-box-major u (else W of `level`)
   bool to_y = false;       // C accumulator = Y (else H of `level`)
+};
+
+// HTLR_TIMING=1: wall-clock split of list building / construction on stderr
+// (synchronises the stream at each mark; development aid)
+struct PhaseTimer {
+  bool on = false;
+  bool sync = false;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t;
+  PhaseTimer() {
+    const char* e = std::getenv("HTLR_TIMING");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  explicit PhaseTimer(cudaStream_t s) : sync(true), st(s) {
+    const char* e = std::getenv("HTLR_TIMING");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[htlr timing] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
 };
 
 // Run body(i) for i in [0, n) on the host's cores (independent items).
@@ -440,7 +468,9 @@ int htlr_build_lists(htlr_plan* pl) {
   ts.eta = pl->desc.eta;
   if (pl->mapped) ts.bounds = pl->mb;
   std::string err;
+  PhaseTimer tm;
   if (htlr::build_tree(ts, pl->tree, err)) return fail(-1, err);
+  tm.mark("lists: tree (DFS)");
   const Tree& tr = pl->tree;
   pl->L = tr.depth;
   pl->sL = tr.leaf_side;
@@ -478,7 +508,15 @@ int htlr_build_lists(htlr_plan* pl) {
   for (int l = 0; l <= pl->L; ++l)
     if (key_range(pl->levels[l].m) <= (1 << 22)) pl->levels[l].adm.dense.assign(key_range(pl->levels[l].m), 0);
   if (key_range(pl->levels[pl->L].m) <= (1 << 22)) pl->near.dense.assign(key_range(pl->levels[pl->L].m), 0);
-  for (const auto& lf : tr.leaves) {
+  // pass 1 (sequential, DFS order): the unique offset of every leaf (ids in
+  // order of first appearance) and the own pairs per offset; pass 2 (all
+  // cores): the (target, source) Morton ids into pre-sized member lists.
+  // The order inside a member list is not kept: every consumer sorts it.
+  const size_t nlf = tr.leaves.size();
+  std::vector<int> lid(nlf);
+  std::vector<char> own(nlf, 1);
+  for (size_t i = 0; i < nlf; ++i) {
+    const auto& lf = tr.leaves[i];
     OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
     const int m = pl->levels[lf.level].m;
     const int64_t key = pack_offset(lf.tc, lf.sc, d, m);
@@ -498,25 +536,43 @@ int htlr_build_lists(htlr_plan* pl) {
       tab.rep.push_back({lf.tc[0], lf.tc[1], lf.tc[2], lf.sc[0], lf.sc[1], lf.sc[2]});
       tab.members.emplace_back();
     }
-    const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
-    const int64_t sl = htlr::morton_encode(lf.sc, d, lf.level);
-    if (world > 1) {
-      if (pl->own_lo[lf.level] < 0)
-        return fail(-1, "admissible blocks on a level with fewer clusters than shards");
-      if (tl < pl->own_lo[lf.level] || tl >= pl->own_hi[lf.level]) {
-        if (lf.kind == 0)
-          pl->levels[lf.level].num_adm++;
-        else
-          pl->num_near++;
-        continue;   // another shard's target
-      }
-    }
-    tab.members[id].emplace_back((int)tl, (int)sl);
+    lid[i] = id;
     if (lf.kind == 0)
       pl->levels[lf.level].num_adm++;
     else
       pl->num_near++;
+    if (world > 1) {
+      if (pl->own_lo[lf.level] < 0)
+        return fail(-1, "admissible blocks on a level with fewer clusters than shards");
+      const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
+      own[i] = tl >= pl->own_lo[lf.level] && tl < pl->own_hi[lf.level];
+    }
+    if (own[i]) tab.members[id].emplace_back(0, 0);   // counted now, filled in pass 2
   }
+  {
+    std::vector<OffsetTable*> tabs;
+    for (auto& lv : pl->levels) tabs.push_back(&lv.adm);
+    tabs.push_back(&pl->near);
+    std::vector<std::vector<std::atomic<int>>> cur(tabs.size());
+    for (size_t t = 0; t < tabs.size(); ++t) {
+      std::vector<std::atomic<int>> v(tabs[t]->members.size());
+      for (auto& a : v) a.store(0);
+      cur[t].swap(v);
+    }
+    const size_t chunk = 1 << 16;
+    parallel_for((nlf + chunk - 1) / chunk, [&](size_t c) {
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i) {
+        if (!own[i]) continue;
+        const auto& lf = tr.leaves[i];
+        const size_t t = lf.kind == 0 ? (size_t)lf.level : tabs.size() - 1;
+        const int pos = cur[t][lid[i]].fetch_add(1, std::memory_order_relaxed);
+        tabs[t]->members[lid[i]][pos] = std::make_pair((int)htlr::morton_encode(lf.tc, d, lf.level),
+                                                        (int)htlr::morton_encode(lf.sc, d, lf.level));
+      }
+    });
+  }
+  tm.mark("lists: offset tables");
   // validation the reference performs at build time (tensor.py:112-113 via
   // blocks.py:160): admissible blocks need box side >= rank
   for (const auto& lv : pl->levels) {
@@ -534,17 +590,16 @@ int htlr_build_lists(htlr_plan* pl) {
   if (pl->mapped) {
     // CSR of the own targets per level (sources sorted by Morton id)
     auto csr = [&](const OffsetTable& tab, int level, std::vector<int64_t>& ptr, std::vector<int>& cols) {
-      std::vector<std::pair<int, int>> all;
-      for (const auto& mem : tab.members) all.insert(all.end(), mem.begin(), mem.end());
-      std::sort(all.begin(), all.end());
       const int64_t lo = pl->own_lo[level], hi = pl->own_hi[level];
       ptr.assign(hi - lo + 1, 0);
-      cols.clear();
-      size_t k = 0;
-      for (int64_t tgt = lo; tgt < hi; ++tgt) {
-        while (k < all.size() && all[k].first == tgt) cols.push_back(all[k++].second);
-        ptr[tgt - lo + 1] = (int64_t)cols.size();
-      }
+      for (const auto& mem : tab.members)
+        for (const auto& q : mem) ptr[q.first - lo + 1]++;
+      for (int64_t r = 0; r < hi - lo; ++r) ptr[r + 1] += ptr[r];
+      cols.assign((size_t)ptr[hi - lo], 0);
+      std::vector<int64_t> fillp(ptr.begin(), ptr.end() - 1);
+      for (const auto& mem : tab.members)
+        for (const auto& q : mem) cols[fillp[q.first - lo]++] = q.second;
+      parallel_for((size_t)(hi - lo), [&](size_t r) { std::sort(cols.begin() + ptr[r], cols.begin() + ptr[r + 1]); });
     };
     for (int l = 0; l <= pl->L; ++l) {
       Level& lv = pl->levels[l];
@@ -555,6 +610,7 @@ int htlr_build_lists(htlr_plan* pl) {
       }
     }
     csr(pl->near, pl->L, pl->near_ptr, pl->near_cols);
+    tm.mark("lists: mapped CSR");
     if (pl->sL > 16) return fail(-1, "mapped grids support leaf sides up to 16");
     pl->merged = false;
     pl->lists_built = true;
@@ -787,28 +843,50 @@ static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& co
                      SymList& out, std::vector<int64_t>* self_ptr, std::vector<int>* self_cols) {
   out.release();
   const int64_t nrows = (int64_t)ptr.size() - 1;
-  std::vector<int64_t> up(nrows + 1, 0);
-  std::vector<int> uc;
-  if (self_ptr) self_ptr->assign(nrows + 1, 0);
-  if (self_cols) self_cols->clear();
-  for (int64_t r = 0; r < nrows; ++r) {
-    const int64_t t = t0 + r;
+  // pass 1 (rows in parallel): owned / self counts, symmetry check
+  std::vector<int64_t> up(nrows + 1, 0), sp(nrows + 1, 0);
+  std::atomic<bool> ok{true};
+  parallel_for((size_t)nrows, [&](size_t r) {
+    const int64_t t = t0 + (int64_t)r;
+    int64_t nu = 0, ns = 0;
     for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
       const int sg = cols[e];
       if (full) {   // symmetry: tau must appear in sigma's (sorted) list
-        if (sg < 0 || sg >= nrows) return 0;
-        if (!std::binary_search(cols.begin() + ptr[sg], cols.begin() + ptr[sg + 1], (int)t)) return 0;
+        if (sg < 0 || sg >= nrows ||
+            !std::binary_search(cols.begin() + ptr[sg], cols.begin() + ptr[sg + 1], (int)t)) {
+          ok = false;
+          return;
+        }
       }
-      if (sg == t) {
-        if (!self_cols) return 0;
-        self_cols->push_back(sg);
-      } else if (pair_owner_is_row(t, sg)) {
-        uc.push_back(sg);
-      }
+      if (sg == t)
+        ++ns;
+      else if (pair_owner_is_row(t, sg))
+        ++nu;
     }
-    up[r + 1] = (int64_t)uc.size();
-    if (self_ptr) (*self_ptr)[r + 1] = (int64_t)self_cols->size();
+    up[r + 1] = nu;
+    sp[r + 1] = ns;
+  });
+  if (!ok) return 0;
+  for (int64_t r = 0; r < nrows; ++r) {
+    up[r + 1] += up[r];
+    sp[r + 1] += sp[r];
   }
+  if (sp[nrows] > 0 && !self_cols) return 0;
+  std::vector<int> uc((size_t)up[nrows]);
+  if (self_ptr) *self_ptr = sp;
+  if (self_cols) self_cols->assign((size_t)sp[nrows], 0);
+  // pass 2: fill (sources stay in CSR order)
+  parallel_for((size_t)nrows, [&](size_t r) {
+    const int64_t t = t0 + (int64_t)r;
+    int64_t ku = up[r], ks = sp[r];
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+      const int sg = cols[e];
+      if (sg == t)
+        (*self_cols)[ks++] = sg;
+      else if (pair_owner_is_row(t, sg))
+        uc[ku++] = sg;
+    }
+  });
   std::vector<int> order(nrows);
   for (int64_t r = 0; r < nrows; ++r) order[r] = (int)r;
   std::stable_sort(order.begin(), order.end(),
@@ -834,6 +912,7 @@ static bool regen_sym_enabled() {
 // raw factors, per-point diagonal cell integrals, CSR lists of own targets.
 static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
   const int d = pl->d, p = pl->p, n = pl->n;
+  PhaseTimer tm(st);
   if (upload(pl->d_mb, pl->mb.data(), pl->mb.size() * sizeof(double))) return 1;
   if (upload(pl->d_mx, pl->mx.data(), pl->mx.size() * sizeof(double))) return 1;
   if (upload(pl->d_mc, pl->mc.data(), pl->mc.size() * sizeof(double))) return 1;
@@ -872,12 +951,14 @@ static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
       }
     }
   }
+  tm.mark("construct: CSR upload + sym lists");
   DevBuf djobs;
   if (!jobs.empty()) {
     if (upload(djobs, jobs.data(), jobs.size() * sizeof(htlr::MappedFactorJob))) return 1;
     htlr::launch_mapped_factors((const htlr::MappedFactorJob*)djobs.ptr, (int)jobs.size(), total, pl->d_mb.d(),
                                 pl->d_mx.d(), pl->d_mc.d(), p, st);
   }
+  tm.mark("construct: factors");
   // Nystrom diagonal: integral of k(x_i, .) over each point's cell
   std::vector<double> gx, gw;
   gauss01(pl->desc.quad_q, gx, gw);
@@ -887,11 +968,13 @@ static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
   pl->device_scalars += pl->N;
   htlr::launch_mapped_diag(pl->kp, d, n, pl->desc.quad_q, pl->gl.d(), pl->gl.d() + pl->desc.quad_q, pl->d_mb.d(),
                            pl->d_mx.d(), pl->dvec.d(), pl->N, st);
+  tm.mark("construct: per-point diagonal");
   if (pl->diag.alloc(sizeof(double))) return 1;
   CUDA_TRY(cudaMemsetAsync(pl->diag.ptr, 0, sizeof(double), st));
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
   djobs.release();
+  tm.mark("construct: finish");
   pl->constructed = true;
   return 0;
 }
