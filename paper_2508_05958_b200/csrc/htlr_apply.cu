@@ -396,13 +396,14 @@ static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, 
 
 void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                 int M_valid, int ldc, int RT, cudaStream_t st) {
+                 int M_valid, int ldc, int RT, cudaStream_t st, const double* gen) {
   if (MT < 0) {
     launch_gemm_thin(-MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
     return;
   }
   if (gemm_use_persistent()) {
-    launch_gemm_persistent(MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+    launch_gemm_persistent(MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st,
+                           gen);
     return;
   }
   if (MT == 64)

@@ -277,6 +277,37 @@ __global__ void near_block_kernel(const NearJob* __restrict__ jobs, int d, int s
 }
 
 // ---------------------------------------------------------------------------
+// Toeplitz generators of the near blocks (3-D, leaf side 8, dyadic h): block
+// delta has A[i][j] = G[(j - i) + 7 per axis], exactly (the coordinates
+// (c + 1/2) h are exact, so r^2 only depends on the index difference).  G is
+// read back from the tiled block itself, so the generated operand equals the
+// stored one bit for bit.
+// ---------------------------------------------------------------------------
+__global__ void near_gen_kernel(const double* __restrict__ table, int64_t mat_stride, int nmats, int MT, int K_pad,
+                                double* __restrict__ gen) {
+  const int total = kGenSide * kGenSide * kGenSide;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)nmats * total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(e / total), u = (int)(e % total);
+    const int uu[3] = {u % kGenSide, (u / kGenSide) % kGenSide, u / (kGenSide * kGenSide)};
+    int row = 0, col = 0, mul = 1;
+    for (int a = 0; a < 3; ++a) {
+      const int i = uu[a] <= 7 ? 7 - uu[a] : 0, j = uu[a] <= 7 ? 0 : uu[a] - 7;
+      row += i * mul;
+      col += j * mul;
+      mul *= 8;
+    }
+    gen[(int64_t)m * kGenStride + u] = table[(int64_t)m * mat_stride + tiled_offset(row, col, MT, K_pad)];
+  }
+}
+
+void launch_near_gen(const double* table, int64_t mat_stride, int nmats, int MT, int K_pad, double* gen,
+                     cudaStream_t st) {
+  if (nmats <= 0) return;
+  near_gen_kernel<<<148 * 4, 256, 0, st>>>(table, mat_stride, nmats, MT, K_pad, gen);
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 void launch_diag(const KernelParams& kp, int d, double h, int q, const double* gx, const double* gw,

@@ -92,12 +92,45 @@ __device__ __forceinline__ void stage_mma(double (&acc)[MI][4][4], const double*
   }
 }
 
-template <int WM, int WN, int STAGES, int KCS, int MI = 2>
+// Narrow-item stage with the A fragments generated from a near block's
+// Toeplitz generator G (3-D, leaf side 8): A[i][j] = G[bi(i) + kb(j)] with
+// bi(i) = sum (7 - i_a) 15^a, kb(j) = sum j_a 15^a.  kabs = first K index of
+// the stage (a multiple of 32), bia / bib = bi of the thread's rows g8, g8 + 8.
+template <int NTL, int KC, int BST>
+__device__ __forceinline__ void stage_mma_gen(double (&acc)[1][4][4], const double* G, const double* cB, int bia,
+                                              int bib, int kabs, int wn, int g8, int t) {
+#pragma unroll
+  for (int ks = 0; ks < KC / 8; ++ks) {
+    const int kk = kabs + ks * 8;
+    const int kb = t + kGenSide * ((kk >> 3) & 7) + kGenSide * kGenSide * (kk >> 6);
+    double a[4];
+    a[0] = G[bia + kb];
+    a[1] = G[bib + kb];
+    a[2] = G[bia + kb + 4];
+    a[3] = G[bib + kb + 4];
+    double b[NTL][2];
+#pragma unroll
+    for (int ni = 0; ni < NTL; ++ni) {
+      const double* pb = cB + (wn * 32 + ni * 8 + g8) * BST + ks * 8 + t;
+      b[ni][0] = pb[0];
+      b[ni][1] = pb[4];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int ni = 0; ni < NTL; ++ni) {
+        mma8x8x4_pair(acc[0][ni][0], acc[0][ni][1], a[2 * h], b[ni][h]);
+        mma8x8x4_pair(acc[0][ni][2], acc[0][ni][3], a[2 * h + 1], b[ni][h]);
+      }
+  }
+}
+
+template <int WM, int WN, int STAGES, int KCS, int MI = 2, bool GEN = false>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_persistent_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                            double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
                            const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
-                           int RT) {
+                           int RT, const double* __restrict__ gen) {
   // a pipeline stage covers KCS = 32 or 64 of K (one or two tiled 32-chunks,
   // adjacent in the A layout); fewer, larger stages halve the mbarrier
   // round trips per unit of tensor work
@@ -105,10 +138,15 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   // of 32 columns for passes with few pairs per matrix)
   constexpr int MT = 16 * MI * WM, NT = 32 * WN, KC = KCS, BST = KC + 4;
   constexpr int NCW = WM * WN;   // consumer warps
+  // GEN: no A stages; the item's Toeplitz generator goes to one of two
+  // slots instead (an item spans more stages than the ring, so the slot of
+  // item i - 1 is free when item i + 1's first stage is issued)
+  constexpr int ASTAGE = GEN ? 0 : MT * KC;
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;                                  // STAGES x MT*KC
-  double* sB = smem + STAGES * MT * KC;               // STAGES x NT*BST
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * NT * BST);
+  double* sB = smem + STAGES * ASTAGE;                // STAGES x NT*BST
+  double* sG = sB + STAGES * NT * BST;                // GEN: 2 x kGenStride
+  uint64_t* full = reinterpret_cast<uint64_t*>(sG + (GEN ? 2 * kGenStride : 0));
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -145,7 +183,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       it = item_info(tasks, item, RT, R, Rc, NT);
       load_cols(it, cb);
     }
-    for (; item < nitems; item += gridDim.x) {
+    for (int ci = 0; item < nitems; item += gridDim.x, ++ci) {
       const int nxt = item + gridDim.x;
       ItemInfo itn{};
       int64_t cbn[NT / 32];
@@ -154,14 +192,21 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         load_cols(itn, cbn);
       }
       const double* Ablk = A + (int64_t)it.mat * mat_stride + (int64_t)it.rt * MT * K_pad;
-      const unsigned bytes = (unsigned)(MT * KC * 8 + it.ncols * KC * 8);
+      const unsigned bytes = (unsigned)(ASTAGE * 8 + it.ncols * KC * 8);
       const int kbeg = it.kc0 * kKC / KC, kend = kbeg + it.nkc * kKC / KC;   // stage units
       for (int kc = kbeg; kc < kend; ++kc, ++g) {
         const int s = g % STAGES;
         if (g >= (uint32_t)STAGES) mbar_wait(&empty[s], ((g / STAGES) - 1) & 1);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[s], bytes);
-          bulk_g2s(sA + s * MT * KC, Ablk + (int64_t)kc * MT * KC, MT * KC * 8, &full[s]);
+          if constexpr (GEN) {
+            const bool first = kc == kbeg;
+            mbar_arrive_expect_tx(&full[s], bytes + (first ? kGenStride * 8u : 0u));
+            if (first)
+              bulk_g2s(sG + (ci & 1) * kGenStride, gen + (int64_t)it.mat * kGenStride, kGenStride * 8, &full[s]);
+          } else {
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(sA + s * MT * KC, Ablk + (int64_t)kc * MT * KC, MT * KC * 8, &full[s]);
+          }
         }
         __syncwarp();
 #pragma unroll
@@ -183,11 +228,17 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   uint32_t g = 0;
   ItemInfo itn{};
   if (blockIdx.x < nitems) itn = item_info(tasks, blockIdx.x, RT, R, Rc, NT);
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  for (int item = blockIdx.x, ci = 0; item < nitems; item += gridDim.x, ++ci) {
     const ItemInfo it = itn;
     if (item + (int)gridDim.x < nitems) itn = item_info(tasks, item + gridDim.x, RT, R, Rc, NT);
     const int n_tiles = max(0, min(4, (it.ncols - wn * 32 + 7) >> 3));
     const int row0 = it.rt * MT + wm * 16 * MI;
+    // GEN: generator slot and the row halves of the Toeplitz index
+    const double* gslot = sG + (ci & 1) * kGenStride;
+    auto gen_row = [](int r) {
+      return (7 - (r & 7)) + kGenSide * (7 - ((r >> 3) & 7)) + kGenSide * kGenSide * (7 - (r >> 6));
+    };
+    const int bia = gen_row(row0 + g8), bib = gen_row(row0 + g8 + 8);
     const int m_tiles = max(0, min(MI, (M_valid - row0 + 15) >> 4));
     // epilogue targets of this thread's 8 columns, fetched now so the pair
     // loads' latency hides under the K loop
@@ -220,7 +271,17 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       // still occupies the tensor pipe (measured 1.45x the issued work on
       // cfg 2's leaf pass).  The wide variants keep one specialised body:
       // four of them cost more in instruction-cache misses (cfg 3: +48%).
-      if (m_tiles == MI && n_tiles == 4)
+      if constexpr (GEN) {
+        const int kabs = (it.kc0 * kKC / KC + kc) * KC;
+        if (n_tiles == 4)
+          stage_mma_gen<4, KC, BST>(acc, gslot, cB, bia, bib, kabs, wn, g8, t);
+        else if (n_tiles == 3)
+          stage_mma_gen<3, KC, BST>(acc, gslot, cB, bia, bib, kabs, wn, g8, t);
+        else if (n_tiles == 2)
+          stage_mma_gen<2, KC, BST>(acc, gslot, cB, bia, bib, kabs, wn, g8, t);
+        else if (n_tiles == 1)
+          stage_mma_gen<1, KC, BST>(acc, gslot, cB, bia, bib, kabs, wn, g8, t);
+      } else if (m_tiles == MI && n_tiles == 4)
         stage_mma<4, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
       else if (MI == 1 && m_tiles == MI && n_tiles == 3)
         stage_mma<3, MI, KC, MT, BST>(acc, cA, cB, wm, wn, lane, g8, t);
@@ -532,27 +593,34 @@ bool gemm_use_persistent() {
   return mode == 1;
 }
 
-template <int WM, int WN, int STAGES, int KCS, int MI = 2, int CPS = 1>
+template <int WM, int WN, int STAGES, int KCS, int MI = 2, int CPS = 1, bool GEN = false>
 static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
                                 const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                                int M_valid, int ldc, int RT, cudaStream_t st) {
+                                int M_valid, int ldc, int RT, cudaStream_t st, const double* gen = nullptr) {
   constexpr int MT = 16 * MI * WM, NT = 32 * WN, KC = KCS;
-  const size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_persistent_kernel<WM, WN, STAGES, KCS, MI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  const size_t smem = sizeof(double) * (STAGES * (size_t)((GEN ? 0 : MT * KC) + NT * (KC + 4)) +
+                                        (GEN ? 2 * kGenStride : 0)) +
+                      2 * STAGES * sizeof(uint64_t);
+  auto kern = gemm_persistent_kernel<WM, WN, STAGES, KCS, MI, GEN>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nitems = ntasks * RT;
   if (nitems == 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = nitems < CPS * sms ? nitems : CPS * sms;   // CPS resident CTAs per SM
-  gemm_persistent_kernel<WM, WN, STAGES, KCS, MI><<<grid, (WM * WN + 1) * 32, smem, st>>>(
-      A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid, ldc, RT);
+  kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(A, mat_stride, B, C, tasks, nitems, pairs, R, Rc, K_pad, M_valid,
+                                               ldc, RT, gen);
 }
 
 void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                            int M_valid, int ldc, int RT, cudaStream_t st) {
+                            int M_valid, int ldc, int RT, cudaStream_t st, const double* gen) {
+  if (MT == 128 && NT == 32 && gen) {   // narrow items, A generated from Toeplitz generators
+    launch_persistent_t<8, 1, 4, 32, 1, 2, true>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid,
+                                                 ldc, RT, st, gen);
+    return;
+  }
   if (MT == 128 && NT == 32) {   // narrow items: 8 warps x (16 rows x 32 columns)
     // two CTAs per SM, two stages each (measured: cfg 2 leaf pass -7%
     // against one CTA with four stages; HTLR_NARROW_CPS=1 for the latter)

@@ -76,6 +76,12 @@ void launch_factor_qr(int nlev, const FactorJob* jobs, double h, int p, cudaStre
 void launch_core_batch(const CoreJob* jobs, int nbatch, int d, int p, double h, double hd,
                        const KernelParams& kp, double* buf0, double* buf1, int MT, int M_pad, int K_pad,
                        cudaStream_t st);
+// Toeplitz generators of 3-D near blocks with leaf side 8: (2*8-1)^3 values
+// each, padded to a 16-byte multiple
+constexpr int kGenSide = 15;
+constexpr int kGenStride = kGenSide * kGenSide * kGenSide + 1;
+void launch_near_gen(const double* table, int64_t mat_stride, int nmats, int MT, int K_pad, double* gen,
+                     cudaStream_t st);
 void launch_near_blocks(const NearJob* jobs, int njobs, int d, int s, double h, double hd,
                         const KernelParams& kp, const double* diag, int MT, int M_pad, int K_pad,
                         cudaStream_t st);
@@ -88,9 +94,12 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
+// gen: Toeplitz generators of the pass's matrices (near-only 3-D leaf pass
+// with leaf side 8) or nullptr; the narrow items then build their A
+// fragments from them instead of streaming the stored blocks
 void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                 int M_valid, int ldc, int RT, cudaStream_t st);
+                 int M_valid, int ldc, int RT, cudaStream_t st, const double* gen = nullptr);
 int gemm_nt(int MT);
 int gemm_wide_wn();   // warps along N of the wide persistent kernel (default 3: 96 columns; HTLR_GEMM_WN=2: 64)
 // persistent warp-specialised variant (htlr_gemm.cu); HTLR_GEMM=legacy selects
@@ -103,7 +112,7 @@ void launch_gemm_thin(int M_pad, int NT, const double* A, int64_t mat_stride, co
                       int ldc, cudaStream_t st);
 void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                             const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                            int M_valid, int ldc, int RT, cudaStream_t st);
+                            int M_valid, int ldc, int RT, cudaStream_t st, const double* gen = nullptr);
 void launch_downward(const double* u, double* f, const double* Y, int ldy, const double* a_vec,
                      double a_const, const double* dvec, int d, int n, int sL, int L, int R, int p,
                      const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st);

@@ -86,6 +86,7 @@ struct Pass {
   int npairs = 0;
   std::map<int, std::pair<DevBuf, int>> tasks;   // per R
   std::map<int, int> task_nt;                     // columns per item of the R slot's tasks
+  DevBuf gen;                                     // Toeplitz generators of the matrices (near-only leaf pass)
   bool from_ub = false;    // B operand = leaf-box-major u (else W of `level`)
   bool to_y = false;       // C accumulator = Y (else H of `level`)
 };
@@ -446,6 +447,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
     ps.table.release();
     ps.pairs.release();
     for (auto& kv : ps.tasks) kv.second.first.release();
+    ps.gen.release();
   }
   pl->diag.release();
   pl->coeff.release();
@@ -899,6 +901,16 @@ static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& co
   return 0;
 }
 
+// HTLR_NEAR_GEN=0: stream the stored near blocks instead of generating them
+static bool near_gen_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("HTLR_NEAR_GEN");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 static bool regen_sym_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -1121,6 +1133,14 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       CUDA_TRY(cudaStreamSynchronize(st));
     }
     njobs.release();
+    // Toeplitz generators for a near-only leaf pass of 3-D side-8 leaves
+    // (n = 8 * 2^L, so h is dyadic and every near block is exactly Toeplitz)
+    if (near_gen_enabled() && d == 3 && pl->sL == 8 && !pl->merged && ps.MT == 128 && ps.K_pad == 512 &&
+        ps.nmats == (int)pl->near.rep.size() && ps.nmats > 0) {
+      if (ps.gen.alloc((size_t)ps.nmats * htlr::kGenStride * sizeof(double))) return 1;
+      htlr::launch_near_gen(ps.table.d(), ps.mat_stride, ps.nmats, ps.MT, ps.K_pad, ps.gen.d(), st);
+      pl->device_scalars += (int64_t)ps.nmats * htlr::kGenStride;
+    }
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   CUDA_TRY(cudaGetLastError());
@@ -1436,7 +1456,8 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ncl;
     if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, NT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
-                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st);
+                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st,
+                      ps.gen.ptr ? ps.gen.d() : nullptr);
     if (cx.prof_end()) return 1;
   }
   htlr::DownParams dp{};

@@ -1,2 +1,1 @@
-timeout 1500 python -m pytest tests/test_gpu_mapped.py tests/test_gpu_blocks_api.py -x -q 2>&1 | tail -2
-HTLR_TIMING=1 PYTHONPATH=. python tools/construct_split.py cfg5 cfg4 2>&1 | tail -20
+for v in 0 1; do HTLR_SPLITK=$v python bench.py --workload cfg2 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b2_$v.json 2>gpurun_out/b2_$v.err; done
