@@ -1452,8 +1452,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     // matrix once + the level's source vectors B and accumulators C once (the
     // per-pair gathers of B are L2 traffic)
     const double ncl = (double)pl->levels[ps.level].nclusters;
+    const bool gen = ps.gen.ptr && ps.MT == 128 && NT == 32;   // A generated from Toeplitz generators
+    const double mat_bytes = gen ? 8.0 * htlr::kGenStride : 8.0 * (double)ps.P * ps.P;
     double flops = 2.0 * (double)ps.P * ps.P * (double)ps.npairs * R;
-    double bytes = 8.0 * (double)ps.P * ps.P * ps.nmats + 2.0 * R8 * (double)ps.P * ncl;
+    double bytes = mat_bytes * ps.nmats + 2.0 * R8 * (double)ps.P * ncl;
     if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, NT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
                       slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st,
