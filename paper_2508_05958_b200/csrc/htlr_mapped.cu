@@ -31,7 +31,8 @@ __device__ __forceinline__ double cheb_node_m(double lo, double hi, int t1, int 
   return __dadd_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(hi, -lo)), cos(arg)), __dmul_rn(0.5, __dadd_rn(hi, lo)));
 }
 
-__global__ void mapped_factor_kernel(const MappedFactorJob* __restrict__ jobs, int njobs, const double* __restrict__ bounds,
+__global__ void mapped_factor_kernel(const MappedFactorJob* __restrict__ jobs, int njobs,
+                                     const double* __restrict__ bounds,
                                      const double* __restrict__ coords, const double* __restrict__ widths, int p) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   int acc = 0, ji = -1, j = 0;

@@ -1874,7 +1874,8 @@ static int export_block_mapped(htlr_plan* pl, const htlr::LeafRec& lf, double* o
   bool self = true;
   for (int a = 0; a < d; ++a) self = self && lf.tc[a] == lf.sc[a];
   if (upload(tmp, geo.data(), geo.size() * 8) || dout.alloc((size_t)P * P * 8)) return 1;
-  htlr::launch_mapped_near_export(pl->kp, d, sL, tmp.d(), tmp.d() + 3 * sL, tmp.d() + 6 * sL, self ? 1 : 0, dout.d(), 0);
+  htlr::launch_mapped_near_export(pl->kp, d, sL, tmp.d(), tmp.d() + 3 * sL, tmp.d() + 6 * sL, self ? 1 : 0,
+                                  dout.d(), 0);
   CUDA_TRY(cudaMemcpy(out, dout.ptr, (size_t)P * P * 8, cudaMemcpyDeviceToHost));
   if (self) {
     std::vector<double> dv((size_t)pl->N), av;
@@ -1936,7 +1937,8 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   if (lf.kind == 0) {
     // core tensor, F-order with target modes first: element (m, k) at m + P*k
     for (int k = 0; k < P; ++k)
-      for (int m = 0; m < P; ++m) core_or_dense[m + (int64_t)P * k] = tiled[htlr::tiled_offset(m, k, ps->MT, ps->K_pad)];
+      for (int m = 0; m < P; ++m)
+        core_or_dense[m + (int64_t)P * k] = tiled[htlr::tiled_offset(m, k, ps->MT, ps->K_pad)];
     if (pl->lowrank) {
       // LowRankBlock(u, g, v): g = core as a P x P matrix (row-major), u = v =
       // dense Kronecker factor (identity where the side equals p)
@@ -1963,7 +1965,8 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
       CUDA_TRY(cudaMemcpy(q.data(), lv.Q.ptr, q.size() * sizeof(double), cudaMemcpyDeviceToHost));
       int64_t need = (int64_t)2 * d * lv.side * p;
       if (!factors || factor_cap < need) return fail(-1, "factor buffer too small");
-      for (int f = 0; f < 2 * d; ++f) std::memcpy(factors + (int64_t)f * lv.side * p, q.data(), q.size() * sizeof(double));
+      for (int f = 0; f < 2 * d; ++f)
+        std::memcpy(factors + (int64_t)f * lv.side * p, q.data(), q.size() * sizeof(double));
       shapes[3] = (int32_t)need;
       shapes[1] = ipow(lv.side, d);
       shapes[2] = ipow(lv.side, d);
@@ -1971,7 +1974,8 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   } else {
     // dense rows x cols, row-major, with a(x_i) on the tau == sigma diagonal
     for (int i = 0; i < P; ++i)
-      for (int j = 0; j < P; ++j) core_or_dense[(int64_t)i * P + j] = tiled[htlr::tiled_offset(i, j, ps->MT, ps->K_pad)];
+      for (int j = 0; j < P; ++j)
+        core_or_dense[(int64_t)i * P + j] = tiled[htlr::tiled_offset(i, j, ps->MT, ps->K_pad)];
     bool self = true;
     for (int a = 0; a < d; ++a)
       if (lf.tc[a] != lf.sc[a]) self = false;
