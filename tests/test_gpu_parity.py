@@ -192,6 +192,22 @@ def test_identity_operator():
     assert np.abs(H.matvec(op, u) - u).max() <= 1e-14
 
 
+def test_single_leaf_is_the_dense_block():
+    """n <= leaf side: the root is one inadmissible leaf (test_operators.py:
+    112-120 / 148-164), so the matvec is that dense block -- K h^d with the
+    cell-average diagonal, plus a -- applied to u."""
+    for d, n, kd, ko in ((2, 8, H.neg_log_2d(), O.Kernel("slp2d", scale=2 * np.pi)),
+                         (3, 8, H.inv_r_3d(), O.Kernel("slp3d", scale=4 * np.pi))):
+        cfg = H.BuildConfig(rank=4, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=kd,
+                            coeff=H.CoefficientFn.constant(0.25))
+        op = H.construct(cfg, H.UniformGrid(d, n))
+        pb = O.Problem(d=d, n=n, rank=4, leaf_side_max=8, kernel=ko, coeff=O.constant_coeff(0.25))
+        full = tuple((0, n) for _ in range(d))
+        A = O.dense_block(pb.kernel, pb.coeff, n, full, full, pb.diag())
+        u = np.random.default_rng(40 + d).standard_normal(n ** d)
+        assert rel(H.matvec(op, u), A @ u) <= 1e-14
+
+
 def test_zero_input_gives_exact_zero():
     grid = H.UniformGrid(3, 16)
     cfg = H.BuildConfig(rank=4, leaf_side=4, rule=H.AdmissibilityRule.strong(1.0),

@@ -1,4 +1,2 @@
-python -m paper_2508_05958_b200.cli bench-uniform --dim 3 --kernel slp3d --n 32 --p 6 --leaf 8 --adm strong --eta 1 --baseline --out gpurun_out/cli_u32.csv
-python -m paper_2508_05958_b200.cli bench-uniform --dim 3 --kernel gaussian --n 64 --p 8 --leaf 8 --adm strong --eta 1 --baseline --out gpurun_out/cli_u64g.csv
-python -m paper_2508_05958_b200.cli bench-uniform --dim 2 --kernel slp2d --n 256 --p 8 --leaf 16 --adm strong --eta 1 --baseline --out gpurun_out/cli_u2d.csv
-python -m paper_2508_05958_b200.cli bench-quasi --kernel slp2d --n 20000 --p 8 --leaf 16 --adm strong --eta 1 --rho 2 --rho 4 --out gpurun_out/cli_q.csv
+for v in 0 1; do HTLR_MT224=$v python bench.py --workload cfg3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b3_$v.json 2>gpurun_out/b3_$v.err; done
+HTLR_MT224=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "cfg3 or small or random" 2>&1 | tail -2
