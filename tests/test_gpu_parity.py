@@ -322,3 +322,16 @@ def test_estimate_rel_error_cfg4_scale():
     err = H.estimate_rel_error_random(op, ev, w.input(), sample_size=1000, seed=1)
     print("cfg4 sampled relative error", err)
     assert err < 1e-3
+
+
+def test_randomised_parity_sweep():
+    """tools/fuzz_parity.py: random dimension / grid (uniform or mapped) /
+    leaf side / rank / admissibility / kernel / coefficient / RHS count
+    against the oracle's full matvec, all within 1e-12."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "tools/fuzz_parity.py", "2", "12"], cwd=root, capture_output=True,
+                         text=True, timeout=1200)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
