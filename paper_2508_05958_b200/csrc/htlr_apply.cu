@@ -23,7 +23,17 @@ namespace htlr {
 // permute: ub[(b*R + r)*K_pad + k] = u[(global point of (b, k))*R + r]
 // ---------------------------------------------------------------------------
 __global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
-                                  int s, int bits, int R, int K_pad, int64_t b0) {
+                                  int s, int bits, int R, int K_pad, int64_t b0, int64_t nb, ZeroList zero) {
+  if (blockIdx.x >= nb) {
+    // the extra CTAs zero the accumulators of the coming GEMM passes
+    const int64_t stride = (int64_t)(gridDim.x - nb) * blockDim.x;
+    const int64_t first = (int64_t)(blockIdx.x - nb) * blockDim.x + threadIdx.x;
+    for (int q = 0; q < zero.cnt; ++q) {
+      double* z = zero.p[q];
+      for (int64_t e = first; e < zero.n[q]; e += stride) z[e] = 0.0;
+    }
+    return;
+  }
   const int64_t b = b0 + blockIdx.x;   // leaf box, Morton id
   int bc[3];
   morton_decode(b, d, bits, bc);
@@ -42,10 +52,18 @@ __global__ void permute_in_kernel(const double* __restrict__ u, double* __restri
 }
 
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
-                       int64_t nb, cudaStream_t st) {
+                       int64_t nb, cudaStream_t st, const ZeroList* zero) {
   int bits = 0;
   while ((s << bits) < n) ++bits;
-  if (nb > 0) permute_in_kernel<<<(unsigned)nb, 256, 0, st>>>(u, ub, d, n, s, bits, R, K_pad, b0);
+  ZeroList z;
+  int64_t words = 0;
+  if (zero) {
+    z = *zero;
+    for (int q = 0; q < z.cnt; ++q) words += z.n[q];
+  }
+  const int64_t zblocks = std::min<int64_t>((words + 2047) / 2048, 4 * 148);
+  if (nb > 0 || zblocks > 0)
+    permute_in_kernel<<<(unsigned)(nb + zblocks), 256, 0, st>>>(u, ub, d, n, s, bits, R, K_pad, b0, nb, z);
 }
 
 // ---------------------------------------------------------------------------

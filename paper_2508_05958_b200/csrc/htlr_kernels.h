@@ -88,8 +88,15 @@ void launch_near_blocks(const NearJob* jobs, int njobs, int d, int s, double h, 
 
 // matvec kernels (htlr_apply.cu)
 // index ranges are Morton ids (see htlr_device.cuh)
+// accumulators the permute launch also zeroes (saves the memset nodes of an
+// unsharded matvec graph)
+struct ZeroList {
+  double* p[kMaxLevels + 2];
+  int64_t n[kMaxLevels + 2];
+  int cnt = 0;
+};
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
-                       int64_t nb, cudaStream_t st);
+                       int64_t nb, cudaStream_t st, const ZeroList* zero = nullptr);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)

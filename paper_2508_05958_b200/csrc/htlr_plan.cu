@@ -1197,6 +1197,7 @@ namespace {
 struct MvCtx {
   htlr_plan* pl;
   cudaStream_t st;
+  bool zeroed = false;      // the permute launch zeroed the remote phase's accumulators
   int R, d, p, P;
   double* ub;
   std::vector<double*> W;   // per pass (nullptr for the leaf pass)
@@ -1283,8 +1284,17 @@ int mv_local_mapped(MvCtx& cx, const double* u) {
   const int PL = ipow(pl->sL, d);
   const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
+  htlr::ZeroList zl;
+  if (pl->shard_world == 1 && R == 1) {   // the symmetric levels accumulate with RED
+    for (const auto& lv : pl->levels)
+      if (lv.needs_up && lv.sym.on) {
+        zl.p[zl.cnt] = lv.H.d();
+        zl.n[zl.cnt++] = lv.nclusters * P;
+      }
+    cx.zeroed = true;
+  }
   if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
-  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, PL, b0, nb, cx.st);
+  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, PL, b0, nb, cx.st, cx.zeroed ? &zl : nullptr);
   if (cx.prof_end()) return 1;
   for (auto& lv : pl->levels) {
     if (!lv.needs_up) continue;
@@ -1353,7 +1363,7 @@ int mv_remote_mapped(MvCtx& cx, const double* u, double* f, int stages) {
     const double evals = sym ? 0.5 : 1.0;
     if (cx.prof_begin(5, lv.level, npair * P * P * (10.0 * evals + 2.0 * R), R8 * npair * P)) return 1;
     if (sym) {
-      CUDA_TRY(cudaMemsetAsync(Hl[lv.level], 0, (size_t)lv.nclusters * P * sizeof(double), cx.st));
+      if (!cx.zeroed) CUDA_TRY(cudaMemsetAsync(Hl[lv.level], 0, (size_t)lv.nclusters * P * sizeof(double), cx.st));
       htlr::launch_regen_sym(pl->kp, p, lv.level, lv.nodes.d(), (const int*)lv.sym.order.ptr, lv.sym.nrows, t0,
                              (const int64_t*)lv.sym.uptr.ptr, (const int*)lv.sym.ucols.ptr, cx.Wl[lv.level], P,
                              Hl[lv.level], P, cx.st);
@@ -1405,8 +1415,22 @@ int mv_local(MvCtx& cx, const double* u) {
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int64_t b0 = pl->own_lo[pl->L], nb = pl->own_hi[pl->L] - b0;
   const double frac = (double)nb / (double)pl->levels[pl->L].nclusters;
+  // unsharded plans: the permute launch also zeroes H_l and Y (one launch
+  // instead of permute + a memset node per accumulator)
+  htlr::ZeroList zl;
+  if (pl->shard_world == 1) {
+    for (const auto& ps : pl->passes) {
+      if (ps.to_y) continue;
+      const Level& lv = pl->levels[ps.level];
+      zl.p[zl.cnt] = lv.H.d();
+      zl.n[zl.cnt++] = lv.nclusters * R * P;
+    }
+    zl.p[zl.cnt] = pl->Y.d();
+    zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
+    cx.zeroed = zl.cnt <= htlr::kMaxLevels + 2;
+  }
   if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
-  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st);
+  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, cx.zeroed ? &zl : nullptr);
   if (cx.prof_end()) return 1;
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
@@ -1434,12 +1458,13 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int64_t nleaf = pl->levels[pl->L].nclusters;
   for (auto& ps : pl->passes) {
-    if (!(stages & 1)) break;
+    if (!(stages & 1) || cx.zeroed) break;
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), cx.st));
   }
-  if (stages & 1) CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
+  if ((stages & 1) && !cx.zeroed)
+    CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     auto& slot = ps.tasks[R];
