@@ -22,19 +22,20 @@ namespace htlr {
 // ---------------------------------------------------------------------------
 // permute: ub[(b*R + r)*K_pad + k] = u[(global point of (b, k))*R + r]
 // ---------------------------------------------------------------------------
-__global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
-                                  int s, int bits, int R, int K_pad, int64_t b0, int64_t nb, ZeroList zero) {
-  if (blockIdx.x >= nb) {
+__device__ __forceinline__ void permute_body(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
+                                             int s, int bits, int R, int K_pad, int64_t b0, int64_t nb,
+                                             const ZeroList& zero, int64_t blk, int64_t nblk) {
+  if (blk >= nb) {
     // the extra CTAs zero the accumulators of the coming GEMM passes
-    const int64_t stride = (int64_t)(gridDim.x - nb) * blockDim.x;
-    const int64_t first = (int64_t)(blockIdx.x - nb) * blockDim.x + threadIdx.x;
+    const int64_t stride = (nblk - nb) * blockDim.x;
+    const int64_t first = (blk - nb) * blockDim.x + threadIdx.x;
     for (int q = 0; q < zero.cnt; ++q) {
       double* z = zero.p[q];
       for (int64_t e = first; e < zero.n[q]; e += stride) z[e] = 0.0;
     }
     return;
   }
-  const int64_t b = b0 + blockIdx.x;   // leaf box, Morton id
+  const int64_t b = b0 + blk;   // leaf box, Morton id
   int bc[3];
   morton_decode(b, d, bits, bc);
   const int P = (d == 2) ? s * s : s * s * s;
@@ -49,6 +50,11 @@ __global__ void permute_in_kernel(const double* __restrict__ u, double* __restri
     }
     ub[((int64_t)b * R + r) * K_pad + k] = v;
   }
+}
+
+__global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
+                                  int s, int bits, int R, int K_pad, int64_t b0, int64_t nb, ZeroList zero) {
+  permute_body(u, ub, d, n, s, bits, R, K_pad, b0, nb, zero, blockIdx.x, gridDim.x);
 }
 
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
@@ -74,15 +80,12 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
 //   T2[a1, a2, z] = sum_y Qy[y][a2] T1[a1, y, z]
 //   W[a1, a2, a3] = sum_z Qz[z][a3] T2[a1, a2, z]
 // ---------------------------------------------------------------------------
-__global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
-                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
-                              int64_t c0) {
-  extern __shared__ double sm[];
+__device__ __forceinline__ void upward_body(const double* __restrict__ u, double* __restrict__ W, int d, int n,
+                                            int s, int p, int bits, int R, int K_pad, const double* __restrict__ Q,
+                                            int64_t qstride, int64_t c, int r, double* sm) {
   double* sQ = sm;                          // d x s*p (factor of each dimension)
   double* T1 = sQ + d * s * p;              // p*s*s (3-D) / p*s (2-D)
   double* T2 = T1 + p * s * (d == 3 ? s : 1);   // p*p*s (3-D)
-  const int64_t c = c0 + blockIdx.x;   // cluster, Morton id
-  const int r = blockIdx.y;
   int cc[3];
   morton_decode(c, d, bits, cc);
   for (int i = threadIdx.x; i < d * s * p; i += blockDim.x) {
@@ -131,6 +134,39 @@ __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__
       for (int z = 0; z < s; ++z) v += sQz[z * p + a3] * T2[a12 + p * p * z];
     }
     dst[i] = v;
+  }
+}
+
+__global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
+                              int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
+                              int64_t c0) {
+  extern __shared__ double sm[];
+  upward_body(u, W, d, n, s, p, bits, R, K_pad, Q, qstride, c0 + blockIdx.x, blockIdx.y, sm);
+}
+
+// ---------------------------------------------------------------------------
+// prologue of an unsharded matvec in one launch: the permute CTAs, the CTAs
+// zeroing the accumulators, and the upward CTAs of every compressed level
+// (all three only read u), instead of 1 + levels launches and memset nodes
+// ---------------------------------------------------------------------------
+__global__ void prologue_kernel(PrologueParams pp) {
+  extern __shared__ double sm[];
+  const int64_t b = blockIdx.x;
+  if (b < pp.nb_perm + pp.nb_zero) {
+    permute_body(pp.u, pp.ub, pp.d, pp.n, pp.sL, pp.bits_L, pp.R, pp.K_pad_leaf, pp.b0, pp.nb_perm, pp.zero, b,
+                 pp.nb_perm + pp.nb_zero);
+    return;
+  }
+  int64_t rest = b - pp.nb_perm - pp.nb_zero;
+  for (int li = 0; li < pp.nlev; ++li) {
+    const UpLevel& lv = pp.lev[li];
+    const int64_t cnt = lv.nc * pp.R;
+    if (rest < cnt) {
+      upward_body(pp.u, lv.W, pp.d, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,
+                  lv.c0 + rest / pp.R, (int)(rest % pp.R), sm);
+      return;
+    }
+    rest -= cnt;
   }
 }
 
@@ -197,11 +233,32 @@ __global__ void upward_slab_kernel(const double* __restrict__ u, double* __restr
   for (int i = threadIdx.x; i < K_pad; i += blockDim.x) dst[i] = i < P ? acc[i] : 0.0;
 }
 
+size_t upward_smem_words(int d, int side, int p) {
+  return (size_t)d * side * p + (size_t)p * side * (d == 3 ? side : 1) + (d == 3 ? (size_t)p * p * side : 0);
+}
+
+void launch_prologue(const PrologueParams& pp_in, cudaStream_t st) {
+  PrologueParams pp = pp_in;
+  int64_t words = 0;
+  for (int q = 0; q < pp.zero.cnt; ++q) words += pp.zero.n[q];
+  pp.nb_zero = std::min<int64_t>((words + 2047) / 2048, 4 * 148);
+  int bits = 0;
+  while ((pp.sL << bits) < pp.n) ++bits;
+  pp.bits_L = bits;
+  size_t smem_words = 0;
+  int64_t blocks = pp.nb_perm + pp.nb_zero;
+  for (int li = 0; li < pp.nlev; ++li) {
+    smem_words = std::max(smem_words, upward_smem_words(pp.d, pp.lev[li].side, pp.p));
+    blocks += pp.lev[li].nc * pp.R;
+  }
+  const size_t smem = smem_words * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (blocks > 0) prologue_kernel<<<(unsigned)blocks, 256, smem, st>>>(pp);
+}
+
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st) {
-  const size_t words = (size_t)d * side * p + (size_t)p * side * (d == 3 ? side : 1) +
-                       (d == 3 ? (size_t)p * p * side : 0);
-  const size_t smem = sizeof(double) * words;
+  const size_t smem = sizeof(double) * upward_smem_words(d, side, p);
   if (nc <= 0) return;
   static int force_slab = -1;   // HTLR_UPWARD_SLAB=1: slab kernel for every box (tests)
   if (force_slab < 0) {

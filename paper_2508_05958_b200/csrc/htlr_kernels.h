@@ -97,6 +97,25 @@ struct ZeroList {
 };
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
                        int64_t nb, cudaStream_t st, const ZeroList* zero = nullptr);
+// one launch for permute + zeroing + the upward pass of every compressed
+// level (unsharded matvec); nb_zero and bits_L are filled in by the launcher
+struct UpLevel {
+  double* W;
+  const double* Q;
+  int64_t qstride, c0, nc;
+  int side, bits, K_pad;
+};
+struct PrologueParams {
+  const double* u;
+  double* ub;
+  int d, n, p, sL, R, K_pad_leaf, bits_L;
+  int64_t b0, nb_perm, nb_zero;
+  ZeroList zero;
+  int nlev;
+  UpLevel lev[kMaxLevels];
+};
+size_t upward_smem_words(int d, int side, int p);
+void launch_prologue(const PrologueParams& pp, cudaStream_t st);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
 // MT selects the tile config (64 or 128)

@@ -1293,6 +1293,35 @@ int mv_local_mapped(MvCtx& cx, const double* u) {
       }
     cx.zeroed = true;
   }
+  if (cx.zeroed && !pl->profiling) {   // one launch, as in mv_local
+    htlr::PrologueParams pp{};
+    pp.u = u;
+    pp.ub = cx.ub;
+    pp.d = d;
+    pp.n = pl->n;
+    pp.p = p;
+    pp.sL = pl->sL;
+    pp.R = R;
+    pp.K_pad_leaf = PL;
+    pp.b0 = b0;
+    pp.nb_perm = nb;
+    pp.zero = zl;
+    bool fused = true;
+    for (auto& lv : pl->levels) {
+      if (!lv.needs_up) continue;
+      if (pp.nlev >= htlr::kMaxLevels || htlr::upward_smem_words(d, lv.side, p) * sizeof(double) > 200 * 1024) {
+        fused = false;
+        break;
+      }
+      pp.lev[pp.nlev++] = htlr::UpLevel{cx.Wl[lv.level], lv.WLm.d(), (int64_t)lv.side * p, pl->own_lo[lv.level],
+                                        pl->own_hi[lv.level] - pl->own_lo[lv.level], lv.side, lv.level, P};
+    }
+    if (fused) {
+      htlr::launch_prologue(pp, cx.st);
+      ++cx.launches;
+      return 0;
+    }
+  }
   if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
   htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, PL, b0, nb, cx.st, cx.zeroed ? &zl : nullptr);
   if (cx.prof_end()) return 1;
@@ -1428,6 +1457,40 @@ int mv_local(MvCtx& cx, const double* u) {
     zl.p[zl.cnt] = pl->Y.d();
     zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
     cx.zeroed = zl.cnt <= htlr::kMaxLevels + 2;
+  }
+  // unprofiled unsharded matvec: permute + zeroing + every level's upward in
+  // one launch (profiling keeps them apart so each phase is timed)
+  if (cx.zeroed && !pl->profiling) {
+    htlr::PrologueParams pp{};
+    pp.u = u;
+    pp.ub = cx.ub;
+    pp.d = d;
+    pp.n = pl->n;
+    pp.p = p;
+    pp.sL = pl->sL;
+    pp.R = R;
+    pp.K_pad_leaf = lp.K_pad;
+    pp.b0 = b0;
+    pp.nb_perm = nb;
+    pp.zero = zl;
+    bool fused = true;
+    for (size_t i = 0; i < pl->passes.size() && fused; ++i) {
+      const Pass& ps = pl->passes[i];
+      if (ps.to_y) continue;
+      const Level& lv = pl->levels[ps.level];
+      if (lv.Kron.ptr || pp.nlev >= htlr::kMaxLevels ||
+          htlr::upward_smem_words(d, lv.side, p) * sizeof(double) > 200 * 1024) {
+        fused = false;
+        break;
+      }
+      pp.lev[pp.nlev++] = htlr::UpLevel{cx.W[i], lv.Q.d(), 0, pl->own_lo[ps.level],
+                                        pl->own_hi[ps.level] - pl->own_lo[ps.level], lv.side, lv.level, ps.K_pad};
+    }
+    if (fused) {
+      htlr::launch_prologue(pp, cx.st);
+      ++cx.launches;
+      return 0;
+    }
   }
   if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
   htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, cx.zeroed ? &zl : nullptr);
