@@ -403,6 +403,7 @@ def run_b200(args):
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
+    launches_per_step = base_op.last_launch_count()   # of the timed (unprofiled) matvec
     # per-kernel device times: the same K steps again with every launch
     # bracketed by CUDA events on its stream (kept out of the timed pass so
     # the event nodes do not inflate the small configs' step time)
@@ -422,7 +423,6 @@ def run_b200(args):
         prof_step_ms.append(e0.elapsed_time(e1))
         prof.append(base_op.profile_read())
     base_op.profile(False)
-    launches_per_step = base_op.last_launch_count()
     total_ms = sum(step_ms)
     if dist is not None:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
