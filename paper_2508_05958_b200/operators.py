@@ -13,13 +13,13 @@ from __future__ import annotations
 import ctypes
 import warnings
 from dataclasses import dataclass, field
-from typing import Callable, Optional
+from typing import Optional
 
 import numpy as np
 
 from . import _lib
 from .blocks import DenseBlock, LowRankBlock, TuckerBlock
-from .grids import (ADMISSIBLE, AdmissibilityRule, BlockClusterTree, UniformGrid,
+from .grids import (AdmissibilityRule, BlockClusterTree, UniformGrid,
                     build_cluster_tree, export_leaf_array, grid_kind)
 from .kernels import CoefficientFn, KernelSpec, QuadratureConfig, singular_rule
 

@@ -5,7 +5,6 @@ lists bit for bit (golden fixtures from the reference).  No device work."""
 import hashlib
 import os
 import re
-import warnings
 
 import numpy as np
 import pytest
