@@ -1205,6 +1205,14 @@ struct MvCtx {
   size_t ev_used = 0;
   int64_t launches = 0;
 
+  // inside a graph capture the event must be an external record node; on a
+  // direct launch (sharded plans, graphs off) a plain record
+  cudaError_t record(cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, st);
+  }
   int prof_begin(int kind, int level, double flops, double bytes) {
     if (!pl->profiling) return 0;
     while (pl->prof_ev.size() < ev_used + 2) {
@@ -1212,7 +1220,7 @@ struct MvCtx {
       CUDA_TRY(cudaEventCreate(&e));
       pl->prof_ev.push_back(e);
     }
-    CUDA_TRY(cudaEventRecordWithFlags(pl->prof_ev[ev_used], st, cudaEventRecordExternal));
+    CUDA_TRY(record(pl->prof_ev[ev_used]));
     pl->prof_kind.push_back(kind);
     pl->prof_level.push_back(level);
     pl->prof_flops.push_back(flops);
@@ -1222,7 +1230,7 @@ struct MvCtx {
   int prof_end() {
     ++launches;
     if (!pl->profiling) return 0;
-    CUDA_TRY(cudaEventRecordWithFlags(pl->prof_ev[ev_used + 1], st, cudaEventRecordExternal));
+    CUDA_TRY(record(pl->prof_ev[ev_used + 1]));
     ev_used += 2;
     return 0;
   }

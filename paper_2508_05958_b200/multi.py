@@ -45,6 +45,11 @@ def allgather_chunks(bufs, rank: int, world: int, group=None) -> None:
         mine = b[rank * c:(rank + 1) * c]
         if b.is_cuda and dist.get_backend(group) == "nccl":
             dist.all_gather_into_tensor(b, mine, group=group)
+        elif b.is_cuda:   # gloo harness runs: staged through host memory
+            h = b.cpu()
+            outs = [h[r * c:(r + 1) * c] for r in range(world)]
+            dist.all_gather(outs, h[rank * c:(rank + 1) * c].clone(), group=group)
+            b.copy_(h)
         else:
             outs = [b[r * c:(r + 1) * c] for r in range(world)]
             dist.all_gather(outs, mine.clone(), group=group)
@@ -64,6 +69,10 @@ def reduce_scatter_chunks(bufs, rank: int, world: int, group=None) -> None:
             out = b.new_empty(c)
             dist.reduce_scatter_tensor(out, b, op=dist.ReduceOp.SUM, group=group)
             b[rank * c:(rank + 1) * c].copy_(out)
+        elif b.is_cuda:   # gloo harness runs: staged through host memory
+            h = b.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            b.copy_(h)
         else:
             dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
 

@@ -61,3 +61,26 @@ def test_sharded_2d_weak_rejects_uneven_levels():
                         kernel=H.gaussian(1.0), coeff=H.CoefficientFn.constant(0.0))
     with pytest.raises(ValueError):
         ShardedOperator(cfg, grid, 0, 8, device=0)
+
+
+def test_profiling_on_direct_launches():
+    """Per-launch profiling works where the matvec is launched directly (a
+    sharded plan's local / remote phases, or graphs switched off), not only
+    inside graph capture: the harness of `bench.py --gpus N` profiles that
+    way."""
+    w = WORKLOADS["cfg2"]
+    cfg, grid = w.build_config(), w.grid
+    op = ShardedOperator(cfg, grid, 0, 2, device=0)
+    ud = torch.from_numpy(np.ascontiguousarray(w.input())).cuda().reshape(grid.num_points, 1)
+    op.local.profile(True)
+    op.local_phase(ud, 1)
+    fd = torch.zeros_like(ud)
+    op.remote_phase(ud, fd, 1)
+    recs = op.local.profile_read()
+    op.local.profile(False)
+    assert recs and all(r["ms"] >= 0 for r in recs)
+    single = H.construct(cfg, grid)
+    H._lib.check(H._lib.lib().htlr_set_graphs(single._plan, 0))
+    single.profile(True)
+    H.matvec(single, w.input())
+    assert single.profile_read()
