@@ -403,6 +403,10 @@ int htlr_plan_create(const htlr_desc* desc, int device, htlr_plan** out) {
   }
   pl->mapped = desc->grid_kind == 1;
   if (pl->mapped) htlr::mapped_tables(desc->n, desc->amplitude, pl->mb, pl->mx, pl->mc);
+  {
+    const char* e = std::getenv("HTLR_GRAPHS");   // HTLR_GRAPHS=0: direct launches (tests)
+    pl->graphs = !(e && e[0] == '0');
+  }
   pl->kp.kind = desc->kernel;
   pl->kp.denom = (2.0 * desc->sigma) * desc->sigma;
   pl->kp.scale = desc->scale;

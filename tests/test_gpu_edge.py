@@ -107,14 +107,15 @@ np.save(sys.argv[1], H.matmat(op, U))
 @pytest.mark.parametrize("env", [{"HTLR_GEMM_NARROW": "0"}, {"HTLR_GEMM_NARROW": "1"},
                                  {"HTLR_GEMM_NARROW": "1", "HTLR_NEAR_GEN": "0"},
                                  {"HTLR_GEMM_WN": "2"}, {"HTLR_GEMM": "legacy"},
-                                 {"HTLR_UPWARD_SLAB": "1", "HTLR_NARROW_CPS": "1"}, {"HTLR_THIN_TN": "1"}])
+                                 {"HTLR_UPWARD_SLAB": "1", "HTLR_NARROW_CPS": "1"}, {"HTLR_THIN_TN": "1"},
+                                 {"HTLR_GRAPHS": "0"}])
 def test_gemm_variants_match_oracle(tmp_path, env, rank):
     """Every GEMM variant, forced per process, against the oracle with two
     right-hand sides: wide 96/64-column and narrow 32-column persistent items
     (P = 512, one or two CTAs per SM; near blocks generated from their
     Toeplitz generators or streamed), thin 64/8-column items (p = 6: P = 216
-    coupling passes), the legacy per-task blocks, and the slab-wise upward
-    kernel that large boxes use."""
+    coupling passes), the legacy per-task blocks, the slab-wise upward
+    kernel that large boxes use, and direct launches instead of the graph."""
     import os
     import subprocess
     import sys
