@@ -84,10 +84,14 @@ constexpr int kKC = 32;
 // i.e. the mma.m8n8k4 A fragment of every 8x4 sub-block is 256 contiguous bytes.
 __host__ __device__ __forceinline__ int64_t tiled_offset(int m, int k, int MT, int K_pad) {
   if (MT < 0) {
+    // thin layout: [k chunk][k4 pair][m8 tile][lane][2] -- a lane's operands
+    // of two consecutive k4 steps are adjacent (one 16-byte shared load)
     const int M_pad = -MT;
     const int kc = k / kKC, kk = k % kKC;
     const int lane = (m & 7) * 4 + (kk & 3);
-    return ((int64_t)kc * (kKC / 4) + (kk >> 2)) * (int64_t)(M_pad / 8 * 32) + (int64_t)((m >> 3) * 32 + lane);
+    const int k4 = kk >> 2;
+    return ((int64_t)kc * (kKC / 8) + (k4 >> 1)) * (int64_t)(M_pad / 8 * 64) + (int64_t)((m >> 3) * 32 + lane) * 2 +
+           (k4 & 1);
   }
   int rt = m / MT, mm = m % MT;
   int kc = k / kKC, kk = k % kKC;

@@ -350,20 +350,33 @@ __device__ __forceinline__ void mma8x8x4(double (&c)[2], double a, double b) {
 
 // One pipeline stage of a thin-kernel warp: row tiles rw, rw + RG, ... (NJ of
 // them) x TN n8 column tiles, K = KC in m8n8k4 steps.
-template <int NJ, int MJ, int TN, int KC, int M8, int BST>
+template <int NJ, int MJ, int TN, int KC, int M8, int BST, int G = 3>
 __device__ __forceinline__ void thin_stage(double (&acc)[MJ][TN][2], const double* cA, const double* cB, int lane,
                                            int rw, int RG) {
+  // two k4 steps per 16-byte A load; row tiles in groups of G so the two
+  // DMMAs of one accumulator are G * TN instructions apart (G = 3 measured
+  // best on config 3's coupling pass: 6.01 ms against 6.16 / 6.32 for 4 / 2)
 #pragma unroll
-  for (int k4 = 0; k4 < KC / 4; ++k4) {
-    double b[TN];
+  for (int j = 0; j < KC / 8; ++j) {
+    double b[2][TN];
 #pragma unroll
-    for (int ni = 0; ni < TN; ++ni) b[ni] = cB[ni * 8 * BST + k4 * 4];
-    const double* pa = cA + k4 * (M8 * 32) + lane;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int i = 0; i < NJ; ++i) {
-      const double a = pa[(rw + RG * i) * 32];
+      for (int ni = 0; ni < TN; ++ni) b[h][ni] = cB[ni * 8 * BST + (2 * j + h) * 4];
+    const double* pa = cA + j * (M8 * 64) + lane * 2;
 #pragma unroll
-      for (int ni = 0; ni < TN; ++ni) mma8x8x4(acc[i][ni], a, b[ni]);
+    for (int i0 = 0; i0 < NJ; i0 += G) {
+      double2 a[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (i0 + g < NJ) a[g] = *reinterpret_cast<const double2*>(pa + (rw + RG * (i0 + g)) * 64);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (i0 + g < NJ)
+#pragma unroll
+            for (int ni = 0; ni < TN; ++ni) mma8x8x4(acc[i0 + g][ni], h ? a[g].y : a[g].x, b[h][ni]);
     }
   }
 }
@@ -376,7 +389,7 @@ __device__ __forceinline__ void thin_stage(double (&acc)[MJ][TN][2], const doubl
 // units keep every SM sub-partition equally busy for P = 216, which the
 // 128-row tiles of the wide kernel cannot (216 = 128 + 88).
 // ---------------------------------------------------------------------------
-template <int M8, int STAGES, int CW, int TN>
+template <int M8, int STAGES, int CW, int TN, int G = 3>
 __global__ void __launch_bounds__(9 * 32, 1)
     gemm_thin_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
                      double* __restrict__ C, const GemmTask* __restrict__ tasks, int nitems,
@@ -490,9 +503,9 @@ __global__ void __launch_bounds__(9 * 32, 1)
         // body (warp-uniform branch: a predicated-off DMMA would still
         // occupy the tensor pipe)
         if (rw + RG * (MJ - 1) < M8)
-          thin_stage<MJ, MJ, TN, KC, M8, BST>(acc, cA, cB, lane, rw, RG);
+          thin_stage<MJ, MJ, TN, KC, M8, BST, G>(acc, cA, cB, lane, rw, RG);
         else
-          thin_stage<MJ - 1, MJ, TN, KC, M8, BST>(acc, cA, cB, lane, rw, RG);
+          thin_stage<MJ - 1, MJ, TN, KC, M8, BST, G>(acc, cA, cB, lane, rw, RG);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -513,21 +526,21 @@ __global__ void __launch_bounds__(9 * 32, 1)
   }
 }
 
-template <int M8, int STAGES, int CW, int TN = 1>
+template <int M8, int STAGES, int CW, int TN = 1, int G = 3>
 static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, double* C, const GemmTask* tasks,
                           int ntasks, const int2* pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
                           cudaStream_t st) {
   constexpr int MP = 8 * M8, KC = kKC;
   const size_t smem =
       sizeof(double) * STAGES * (size_t)(MP * KC + 8 * CW * TN * (KC + 4)) + 2 * STAGES * sizeof(uint64_t);
-  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES, CW, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm_thin_kernel<M8, STAGES, CW, TN, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   if (ntasks == 0) return;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = ntasks < sms ? ntasks : sms;
-  gemm_thin_kernel<M8, STAGES, CW, TN><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
+  gemm_thin_kernel<M8, STAGES, CW, TN, G><<<grid, 9 * 32, smem, st>>>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc,
                                                             K_pad, M_valid, ldc);
 }
 
