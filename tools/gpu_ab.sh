@@ -1,1 +1,2 @@
-for g in 4 2 3; do HTLR_THIN_G=$g python bench.py --workload cfg3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b3_$g.json 2>gpurun_out/b3_$g.err; done
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for w in cfg2 cfg3; do python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/bench_$w.json 2>gpurun_out/bench_$w.err; done
