@@ -657,7 +657,7 @@ void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride,
   }
   if (MT == 64)
     launch_persistent_t<2, 2, 6, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
-  else if (gemm_wide_wn() == 3)
+  else if (NT == 96)
     launch_persistent_t<4, 3, 3, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
   else if (kcs == 64 && K_pad % 64 == 0)
     launch_persistent_t<4, 2, 2, 64>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);

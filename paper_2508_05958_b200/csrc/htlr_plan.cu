@@ -323,9 +323,23 @@ int choose_nt(const Pass& ps, int R) {
     if (force == 1 || cols <= 8.0) return 8;
     return cols <= 16.0 ? 16 : NT;
   }
-  if (ps.MT != 128 || NT != 96) return NT;
+  if (ps.MT != 128 || !htlr::gemm_use_persistent()) return NT;
   if (force >= 0) return force ? 32 : NT;
-  return cols < 48.0 ? 32 : NT;
+  if (cols < 48.0) return 32;
+  if (std::getenv("HTLR_GEMM_WN")) return NT;   // forced 64 / 96
+  // 64 or 96 columns per item: whichever wastes fewer column slots on the
+  // pass's per-matrix pair counts (ties go to the 12-warp 96-column CTA)
+  auto eff = [&](int nt) {
+    const int rc = std::min(R, nt), npt = std::max(1, nt / rc);
+    double useful = 0.0, cap = 0.0;
+    for (int m = 0; m < ps.nmats; ++m) {
+      const int cnt = ps.seg[m + 1] - ps.seg[m];
+      useful += (double)cnt * R;
+      cap += (double)((cnt + npt - 1) / npt) * ((R + rc - 1) / rc) * nt;
+    }
+    return cap > 0 ? useful / cap : 1.0;
+  };
+  return eff(64) > eff(96) + 0.005 ? 64 : 96;
 }
 
 int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
