@@ -1,2 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_integration_stub.py -x -q 2>&1 | tail -5
-python bench.py --workload cfg5 --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['construction'], d['config']['l2'])"
+# Scratch A/B script shipped to the GPU box with gpurun (dev aid; the content
+# changes from experiment to experiment).  Example:
+#   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
+for w in cfg2 cfg4; do
+  python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b_$w.json 2> gpurun_out/b_$w.err
+done
