@@ -308,6 +308,8 @@ PHASE_KERNELS = {
     "gemm_level": "gemm_persistent_kernel / gemm_thin_kernel (coupling cores, fp64 DMMA)",
     "regen_level": "regen_sym_kernel (cores regenerated + contracted, fp64 CUDA cores)",
     "regen_near": "regen_sym_kernel (near blocks regenerated, fp64 CUDA cores)",
+    "sep_level": "sep_apply_kernel (separable coupling cores: per-axis mode products, fp64 DMMA)",
+    "sep_leaf": "sep_apply_kernel (separable near + leaf-level cores: per-axis mode products, fp64 DMMA)",
     "upward": "upward_kernel", "downward": "downward_kernel", "permute": "permute_in_kernel",
 }
 

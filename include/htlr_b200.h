@@ -176,6 +176,15 @@ int htlr_diag_value(htlr_plan* plan, double* out);
 int htlr_export_block(htlr_plan* plan, int64_t leaf_id, double* core_or_dense, int64_t cap,
                       double* factors, int64_t factor_cap, int32_t* shapes);
 
+/* How the constructed plan applies its blocks: 0 = dense deduplicated cores
+ * and near blocks (fp64 tensor-core GEMM passes); 1 = separable cores (a
+ * tensor-product kernel -- the Gaussian -- on a uniform 3-D grid with
+ * p = leaf side = 8: every block is the Kronecker product of three 8 x 8
+ * per-axis factors, applied as mode products; HTLR_SEPARABLE=0 forces 0);
+ * 2 = regenerated cores (mapped grid).  Same operator in every case
+ * (blocks.py:126-227); negative on error. */
+int htlr_formulation(const htlr_plan* plan);
+
 /* storage_report equivalent (operators.py:175-197): scalars the reference
  * would store: [dense, factor, core, total]; plus what this plan stores
  * on the device after deduplication in out[4]. */

@@ -82,16 +82,6 @@ __global__ void diag_kernel(KernelParams kp, int d, double h, int q, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// Chebyshev node of a domain interval (chebyshev.py:36-37), numpy's order.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double cheb_node(double lo, double hi, int t1, int p) {
-  double arg = __ddiv_rn(__dmul_rn((double)(2 * t1 - 1), 3.141592653589793), (double)(2 * p));
-  double c = cos(arg);
-  return __dadd_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(hi, -lo)), c),
-                   __dmul_rn(0.5, __dadd_rn(hi, lo)));
-}
-
-// ---------------------------------------------------------------------------
 // Per-level Lagrange factor of the representative box [0, s) and its thin
 // Householder QR with LAPACK's dlarfg sign convention (dgeqr2 + dorg2r), so
 // Q matches numpy.linalg.qr column signs.  s == p: R := raw factor, Q := I

@@ -70,6 +70,16 @@ __device__ __forceinline__ double r2_of(int d, const double* x, const double* y)
 }
 
 // ---------------------------------------------------------------------------
+// Chebyshev node of a domain interval (chebyshev.py:36-37), numpy's order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double cheb_node(double lo, double hi, int t1, int p) {
+  double arg = __ddiv_rn(__dmul_rn((double)(2 * t1 - 1), 3.141592653589793), (double)(2 * p));
+  double c = cos(arg);
+  return __dadd_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(hi, -lo)), c),
+                   __dmul_rn(0.5, __dadd_rn(hi, lo)));
+}
+
+// ---------------------------------------------------------------------------
 // GEMM A-operand tiling.  Every deduplicated core / near block is stored
 // pre-tiled for mma.sync.m16n8k8.f64 so a CTA stage (MT rows x KC cols) is one
 // contiguous chunk and each lane's fragment (a0..a3) is 32 contiguous bytes:

@@ -143,6 +143,34 @@ void launch_downward(const double* u, double* f, const double* Y, int ldy, const
                      double a_const, const double* dvec, int d, int n, int sL, int L, int R, int p,
                      const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st);
 
+// separable-core formulation (htlr_sep.cu): tensor-product kernels (the
+// Gaussian) on uniform grids with p = leaf side = 8 in 3-D
+constexpr int kSepP = 8;
+constexpr int kSepSlot = 256;       // doubles per (kind, offset) table slot in HBM
+constexpr int kSepSlotSmem = 192;   // the part the apply kernel stages in shared memory
+constexpr int kSepWarps = 8;
+constexpr int kSepMaxNO = 15;       // per-axis offsets -7..7 (4-bit codes)
+struct SepJob {
+  int kind;          // 0 admissible core factor, 1 near-block factor
+  int o;             // per-axis box offset (source - target)
+  int t0;            // representative target box index (t0 and t0 + o inside the domain)
+  int side;          // box side at the pass's level
+  const double* R;   // level factor (p x p row-major), admissible only
+  double* dst;       // kSepSlot doubles
+};
+// a warp's work: pairs [begin, begin + count) of target `tgt`; flags bit 0:
+// the run holds the self pair (near-field diagonal correction)
+struct SepItem {
+  int tgt, begin, count, flags;
+};
+void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
+                       const double* diag, double hd, double* corr_out, cudaStream_t st);
+size_t sep_smem_bytes(int nslots);
+// pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
+// (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
+void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st);
+
 // mapped grid (htlr_mapped.cu)
 void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,
                            const double* coords, const double* widths, int p, cudaStream_t st);

@@ -89,6 +89,11 @@ struct Pass {
   DevBuf gen;                                     // Toeplitz generators of the matrices (near-only leaf pass)
   bool from_ub = false;    // B operand = leaf-box-major u (else W of `level`)
   bool to_y = false;       // C accumulator = Y (else H of `level`)
+  // separable-core formulation (htlr_sep.cu): per-target pair runs sorted by
+  // (kind, o_x, o_y, o_z), warp work items, 1-D factor tables
+  DevBuf sep_tab, sep_pairs, sep_items;
+  int sep_nitems = 0, sep_NO = 0;
+  int64_t sep_groups = 0;
 };
 
 // HTLR_TIMING=1: wall-clock split of list building / construction on stderr
@@ -195,6 +200,8 @@ struct htlr_plan {
   int leaf_pass = -1;
   int near_mats = 0;          // leaf pass: matrices [0, near_mats) are near blocks
   bool merged = false;        // leaf-level admissible cores live in the leaf pass
+  bool sep = false;           // separable-core formulation (tensor-product kernel, htlr_sep.cu)
+  DevBuf sep_corr;            // self-block diagonal correction of the separable near field
   DevBuf diag, coeff, gl, ub, Y;
   DevBuf u_stage, f_stage;   // graph-replay staging vectors
   bool has_coeff = false;
@@ -466,7 +473,11 @@ int htlr_plan_destroy(htlr_plan* pl) {
     ps.pairs.release();
     for (auto& kv : ps.tasks) kv.second.first.release();
     ps.gen.release();
+    ps.sep_tab.release();
+    ps.sep_pairs.release();
+    ps.sep_items.release();
   }
+  pl->sep_corr.release();
   pl->diag.release();
   pl->coeff.release();
   pl->gl.release();
@@ -938,6 +949,135 @@ static bool regen_sym_enabled() {
   return on == 1;
 }
 
+static int upload_sep(Pass& ps, const std::vector<int2>& ent, const std::vector<htlr::SepItem>& items) {
+  if (ps.sep_pairs.alloc(std::max<size_t>(1, ent.size()) * sizeof(int2))) return 1;
+  if (!ent.empty()) CUDA_TRY(cudaMemcpy(ps.sep_pairs.ptr, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  if (ps.sep_items.alloc(std::max<size_t>(1, items.size()) * sizeof(htlr::SepItem))) return 1;
+  if (!items.empty())
+    CUDA_TRY(cudaMemcpy(ps.sep_items.ptr, items.data(), items.size() * sizeof(htlr::SepItem), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// Separable-core formulation (htlr_sep.cu): a tensor-product kernel (the
+// Gaussian) on a uniform 3-D grid with p = leaf side = 8.  HTLR_SEPARABLE=0
+// keeps the dense-core GEMM path for A/B runs.
+static bool sep_wanted(const htlr_plan* pl) {
+  const char* e = std::getenv("HTLR_SEPARABLE");
+  if (e && e[0] == '0') return false;
+  return !pl->mapped && !pl->lowrank && pl->kp.kind == HTLR_KERNEL_GAUSSIAN && pl->d == 3 && pl->p == htlr::kSepP &&
+         pl->sL == htlr::kSepP;
+}
+
+// Work items of at most this many pairs (split at group boundaries), so the
+// warps of a pass finish together; HTLR_SEP_CHUNK overrides.
+static int sep_chunk() {
+  const char* e = std::getenv("HTLR_SEP_CHUNK");
+  const int v = e ? std::atoi(e) : 0;
+  return v > 0 ? v : 128;
+}
+
+// Per-target pair runs of one pass: (source, code) sorted by code, where code
+// packs (kind, o_x, o_y, o_z); returns 1 (and leaves the pass untouched) when
+// an axis offset does not fit the 4-bit code.
+static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) {
+  const int d = pl->d;
+  const bool leaf = ps.to_y;
+  const Level& lv = pl->levels[ps.level];
+  std::vector<std::array<int, 4>> mo((size_t)ps.nmats);   // kind, o_x, o_y, o_z
+  int OR = 0;
+  for (int m = 0; m < ps.nmats; ++m) {
+    const bool near = leaf && m < pl->near_mats;
+    const auto& rp = near ? pl->near.rep[m] : lv.adm.rep[m - (leaf ? pl->near_mats : 0)];
+    mo[m][0] = near ? 1 : 0;
+    for (int a = 0; a < d; ++a) {
+      mo[m][1 + a] = rp[3 + a] - rp[a];
+      OR = std::max(OR, std::abs(mo[m][1 + a]));
+    }
+  }
+  const int NO = 2 * OR + 1;
+  if (NO > htlr::kSepMaxNO) {
+    fits = false;
+    return 0;
+  }
+  fits = true;
+  // counting sort by target, then each target's run by (code, source)
+  const int64_t t0 = pl->own_lo[ps.level], nt = pl->own_hi[ps.level] - t0;
+  std::vector<int64_t> ptr((size_t)nt + 1, 0);
+  for (const int2& q : ps.pairs_host) ptr[q.x - t0 + 1]++;
+  for (int64_t t = 0; t < nt; ++t) ptr[t + 1] += ptr[t];
+  std::vector<int2> ent(ps.pairs_host.size());
+  {
+    std::vector<int64_t> fillp(ptr.begin(), ptr.end() - 1);
+    for (int m = 0; m < ps.nmats; ++m) {
+      const int code = (mo[m][0] << 12) | ((mo[m][1] + OR) << 8) | ((mo[m][2] + OR) << 4) | (mo[m][3] + OR);
+      for (int k = ps.seg[m]; k < ps.seg[m + 1]; ++k) {
+        const int2 q = ps.pairs_host[k];
+        ent[fillp[q.x - t0]++] = make_int2(q.y, code);
+      }
+    }
+  }
+  parallel_for((size_t)nt, [&](size_t t) {
+    std::sort(ent.begin() + ptr[t], ent.begin() + ptr[t + 1],
+              [](const int2& a, const int2& b) { return a.y != b.y ? a.y < b.y : a.x < b.x; });
+  });
+  const int selfcode = (1 << 12) | (OR << 8) | (OR << 4) | OR;
+  const int chunk = sep_chunk();
+  std::vector<htlr::SepItem> items;
+  int64_t groups = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t b = ptr[t];
+    const int64_t e = ptr[t + 1];
+    while (b < e) {
+      // extend by whole groups while the item stays within `chunk` pairs
+      int64_t c = b;
+      int flags = 0;
+      while (c < e) {
+        int64_t g = c;
+        while (g < e && (ent[g].y >> 4) == (ent[c].y >> 4)) ++g;
+        if (c > b && g - b > chunk) break;
+        for (int64_t k = c; k < g; ++k)
+          if (ent[k].y == selfcode && ent[k].x == (int)(t0 + t)) flags |= 1;
+        ++groups;
+        c = g;
+      }
+      items.push_back(htlr::SepItem{(int)(t0 + t), (int)b, (int)(c - b), flags});
+      b = c;
+    }
+  }
+  ps.sep_NO = NO;
+  ps.sep_groups = groups;
+  ps.sep_nitems = (int)items.size();
+  if (upload_sep(ps, ent, items)) return 1;
+  // factor tables: kind 0 (admissible, level factor folded) and kind 1 (near)
+  const int nslots = 2 * NO;
+  if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;
+  CUDA_TRY(cudaMemsetAsync(ps.sep_tab.ptr, 0, (size_t)nslots * htlr::kSepSlot * sizeof(double), st));
+  std::vector<htlr::SepJob> jobs;
+  for (int kind = 0; kind < 2; ++kind) {
+    if (kind == 0 && !lv.R.ptr) continue;
+    if (kind == 1 && !leaf) continue;
+    for (int o = -OR; o <= OR; ++o) {
+      htlr::SepJob j;
+      j.kind = kind;
+      j.o = o;
+      j.t0 = std::max(0, -o);
+      j.side = kind == 0 ? lv.side : pl->sL;
+      j.R = kind == 0 ? lv.R.d() : nullptr;
+      j.dst = ps.sep_tab.d() + (int64_t)(kind * NO + o + OR) * htlr::kSepSlot;
+      jobs.push_back(j);
+    }
+  }
+  DevBuf jb;
+  if (jb.alloc(std::max<size_t>(1, jobs.size()) * sizeof(htlr::SepJob))) return 1;
+  CUDA_TRY(cudaMemcpyAsync(jb.ptr, jobs.data(), jobs.size() * sizeof(htlr::SepJob), cudaMemcpyHostToDevice, st));
+  htlr::launch_sep_tables((const htlr::SepJob*)jb.ptr, (int)jobs.size(), pl->p, pl->sL, pl->h, pl->kp, pl->diag.d(),
+                          pl->hd, leaf ? pl->sep_corr.d() : nullptr, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  pl->device_scalars += (int64_t)nslots * htlr::kSepSlot;
+  return 0;
+}
+
 // Mapped grid construction: geometry tables, per (level, interval) nodes and
 // raw factors, per-point diagonal cell integrals, CSR lists of own targets.
 static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
@@ -1076,6 +1216,35 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       htlr::launch_kron_factor(lv.Q.d(), d, lv.side, p, lv.Kron.d(), st);
       pl->device_scalars += S * P;
     }
+  }
+  // separable-core formulation: 1-D factor tables instead of dense cores
+  pl->sep = false;
+  if (sep_wanted(pl)) {
+    if (pl->sep_corr.alloc(sizeof(double))) return 1;
+    bool all = true;
+    for (auto& ps : pl->passes) {
+      bool fits = false;
+      if (build_sep_pass(pl, ps, fits, st)) return 1;
+      if (!fits) {
+        all = false;
+        break;
+      }
+    }
+    if (all) {
+      CUDA_TRY(cudaStreamSynchronize(st));
+      CUDA_TRY(cudaGetLastError());
+      scratch.release();
+      jobsbuf.release();
+      pl->sep = true;
+      pl->constructed = true;
+      return 0;
+    }
+    for (auto& ps : pl->passes) {   // an offset outside the 4-bit codes: dense cores
+      ps.sep_tab.release();
+      ps.sep_pairs.release();
+      ps.sep_items.release();
+    }
+    pl->device_scalars = 0;
   }
   // tables
   for (auto& ps : pl->passes) {
@@ -1268,7 +1437,7 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   cx.P = ipow(pl->p, pl->d);
   if (ensure_workspace(pl, cx.R)) return 1;
   for (auto& ps : pl->passes) {
-    if (ps.tasks.count(cx.R)) continue;
+    if (pl->sep || ps.tasks.count(cx.R)) continue;
     std::vector<htlr::GemmTask> tv;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
@@ -1556,6 +1725,24 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
+    if (pl->sep) {
+      if (ps.sep_nitems == 0) continue;
+      const double* B = ps.from_ub ? cx.ub : cx.W[i];
+      double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
+      // algorithmic work: 8^4 MAC per pair (mode z) + 2 * 8^4 per group
+      // (modes x, y); HBM bytes: the level's source vectors and accumulators
+      // once (the per-pair gathers are L2 traffic) + the factor tables
+      const double ncl = (double)pl->levels[ps.level].nclusters;
+      const double m4 = 4096.0;
+      const double flops = 2.0 * m4 * ((double)ps.npairs + 2.0 * (double)ps.sep_groups) * R;
+      const double bytes = 2.0 * R8 * (double)ps.P * ncl + 8.0 * 2 * ps.sep_NO * htlr::kSepSlot;
+      if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, flops, bytes)) return 1;
+      htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
+                             ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
+                             pl->sep_corr.d(), cx.st);
+      if (cx.prof_end()) return 1;
+      continue;
+    }
     auto& slot = ps.tasks[R];
     if (slot.second == 0) continue;
     const int NT = ps.task_nt[R];
@@ -2012,6 +2199,81 @@ static int export_block_mapped(htlr_plan* pl, const htlr::LeafRec& lf, double* o
   return 0;
 }
 
+// Separable plan export: the Kronecker product of the pass's device-built 1-D
+// factors (the operator the apply kernel uses), in the dense path's formats.
+static int export_block_sep(htlr_plan* pl, const htlr::LeafRec& lf, double* out, int64_t cap, double* factors,
+                            int64_t factor_cap, int32_t* shapes) {
+  const int d = pl->d, p = pl->p, s = htlr::kSepP;
+  const Level& lv = pl->levels[lf.level];
+  const Pass* ps = nullptr;
+  for (auto& q : pl->passes)
+    if (lf.kind == 0 ? (!q.to_y && q.level == lf.level) : q.to_y) ps = &q;
+  if (!ps && lf.kind == 0) ps = &pl->passes[pl->leaf_pass];   // leaf-level cores live in the leaf pass
+  const int NO = ps->sep_NO, OR = (NO - 1) / 2;
+  std::vector<double> tab((size_t)2 * NO * htlr::kSepSlot);
+  CUDA_TRY(cudaMemcpy(tab.data(), ps->sep_tab.ptr, tab.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  const double* M[3];
+  const int kind = lf.kind == 0 ? 0 : 1;
+  for (int a = 0; a < d; ++a) {
+    const int o = lf.sc[a] - lf.tc[a];
+    if (std::abs(o) > OR) return fail(2, "leaf offset outside the separable tables");
+    M[a] = tab.data() + (int64_t)(kind * NO + o + OR) * htlr::kSepSlot + 192;
+  }
+  const int P = s * s * s;
+  if ((int64_t)P * P > cap) return fail(-1, "block buffer too small");
+  const double scale = pl->kp.scale;
+  auto entry = [&](int m, int k) {
+    return (scale * M[0][(m % s) * s + k % s]) * M[1][((m / s) % s) * s + (k / s) % s] *
+           M[2][(m / (s * s)) * s + k / (s * s)];
+  };
+  shapes[0] = lf.kind;
+  shapes[1] = P;
+  shapes[2] = P;
+  shapes[3] = 0;
+  if (lf.kind == 0) {
+    for (int k = 0; k < P; ++k)
+      for (int m = 0; m < P; ++m) out[m + (int64_t)P * k] = entry(m, k);
+    if (lv.side != p) {
+      std::vector<double> q((size_t)lv.side * p);
+      CUDA_TRY(cudaMemcpy(q.data(), lv.Q.ptr, q.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      const int64_t need = (int64_t)2 * d * lv.side * p;
+      if (!factors || factor_cap < need) return fail(-1, "factor buffer too small");
+      for (int f = 0; f < 2 * d; ++f) std::memcpy(factors + (int64_t)f * lv.side * p, q.data(), q.size() * sizeof(double));
+      shapes[3] = (int32_t)need;
+      shapes[1] = ipow(lv.side, d);
+      shapes[2] = ipow(lv.side, d);
+    }
+    return 0;
+  }
+  for (int i = 0; i < P; ++i)
+    for (int j = 0; j < P; ++j) out[(int64_t)i * P + j] = entry(i, j);
+  bool self = true;
+  for (int a = 0; a < d; ++a)
+    if (lf.tc[a] != lf.sc[a]) self = false;
+  if (self) {
+    double dv = 0.0;
+    CUDA_TRY(cudaMemcpy(&dv, pl->diag.ptr, sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> a(P, pl->desc.coeff_const);
+    if (pl->has_coeff) {
+      std::vector<double> all((size_t)pl->N);
+      CUDA_TRY(cudaMemcpy(all.data(), pl->coeff.ptr, all.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < P; ++k) {
+        const int x = k % s, y = (k / s) % s, z = k / (s * s);
+        a[k] = all[(int64_t)(lf.tc[0] * s + x) + (int64_t)pl->n * (lf.tc[1] * s + y) +
+                   (int64_t)pl->n * pl->n * (lf.tc[2] * s + z)];
+      }
+    }
+    for (int i = 0; i < P; ++i) out[(int64_t)i * P + i] = dv * pl->hd + a[i];
+  }
+  return 0;
+}
+
+int htlr_formulation(const htlr_plan* pl) {
+  if (!pl) return fail(-1, "null plan");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  return pl->mapped ? 2 : pl->sep ? 1 : 0;
+}
+
 int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int64_t cap, double* factors,
                       int64_t factor_cap, int32_t* shapes) {
   if (!pl || !core_or_dense || !shapes) return fail(-1, "null argument");
@@ -2027,6 +2289,7 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   const int64_t key = pack_offset(lf.tc, lf.sc, d, lv.m);
   const int id = tab.dense.empty() ? tab.id.at(key) : tab.dense[key] - 1;
   if (id < 0) return fail(2, "leaf offset missing from the plan's tables");
+  if (pl->sep) return export_block_sep(pl, lf, core_or_dense, cap, factors, factor_cap, shapes);
   const Pass* ps = nullptr;
   int mat = id;
   if (lf.kind == 0) {

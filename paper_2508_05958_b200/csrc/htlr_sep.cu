@@ -1,0 +1,241 @@
+// Separable-core formulation of the HTLR coupling and near-field passes
+// (sm_100a), for tensor-product kernels on uniform grids (the Gaussian,
+// kernels.py:90-92: exp(-|x-y|^2 / (2 s^2)) = prod_a exp(-(x_a-y_a)^2 / (2 s^2))).
+//
+// The reference's admissible block (blocks.py:126-164) is
+//   (U_1 x U_2 x U_3) . core . (V_1 x V_2 x V_3)^T,
+//   core = multi_mode_apply(h^d G, [R_u1, R_v1, R_u2, R_v2, ...]),
+//   G[t, s] = k(xi_t, eta_s) on the tensor Chebyshev grids (chebyshev.py:69-85).
+// For a tensor-product kernel G = G_1 (x) G_2 (x) G_3 with 1-D samples
+// G_a[t, s] = g(xi_t^a - eta_s^a), and every mode product acts on one factor,
+// so the core is exactly the Kronecker product of three p x p matrices
+//   C_a(o_a) = h R G_a(o_a) R^T
+// (R = the level's QR factor, or the raw Lagrange factor when side == p,
+// blocks.py:155-162), each depending only on the per-axis box offset o_a on a
+// uniform grid.  Likewise the near block (blocks.py:190-227) is
+// (x)_a E(o_a), E[i, j] = h g(x_i - y_j), except for the tau == sigma
+// diagonal, which the reference replaces by the cell average (kernels.py:
+// 120-149): a rank-one-per-entry correction (corr * u_tau) added by the item
+// that owns the self pair.  So every (target, source) pair of a pass applies
+//   Y_tau += (C(o_z) (x) C(o_y) (x) C(o_x)) X_sigma      (F-order vectors)
+// -- three 8 x 8 mode products (3 * 8^4 MAC) instead of one 512 x 512 GEMV
+// (8^6 MAC): the same operator, 85x fewer flops.
+//
+// sep_apply_kernel: one warp per work item = (target, run of its pairs, rhs).
+// Pairs of a target are sorted by (kind, o_x, o_y, o_z); the mode-z product
+// runs per pair on the fp64 tensor pipe (mma.m8n8k4, 16 DMMA), accumulating
+// Z over a run of equal (kind, o_x, o_y) ("group"); at a group boundary the
+// mode-x product (16 DMMA, the C fragment of mode z is reused as the B
+// operand with a permuted k order, no shuffles) and the mode-y product
+// (128 DFMA per lane) fold Z into the target's accumulator Y (registers).  The
+// item ends with an fp64 RED of Y into the pass's accumulator (H_l or the
+// leaf-level Y), which the matvec prologue zeroed.
+//
+// Fragment layouts (mma.m8n8k4.row.col.f64): A: lane holds A[lane/4][lane%4];
+// B: lane holds B[lane%4][lane/4]; C: lane holds C[lane/4][2(lane%4) + j].
+//   X (source tensor X[a,b,c] at a + 8b + 64c): B operand of tile t = b,
+//     k-step ks: X[a = lane/4, b = t, c = 4 ks + lane%4]
+//   Z_t[k', a] (C fragment)      = sum_c Mz[k', c] X[a, t, c]
+//   T_t[i, k'] (C fragment)      = sum_a Mx[i, a] Z_t[k', a]
+//   Y[i, j, k'] (lane: i = lane/4, k' = 2(lane%4) + jj)
+//                               += sum_t My[j, t] T_t[i, k']
+#include "htlr_device.cuh"
+#include "htlr_kernels.h"
+
+namespace htlr {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 1-D factor of the Gaussian: g(delta) = exp(-delta^2 / (2 s^2))
+__device__ __forceinline__ double gauss1d(double delta, double denom) {
+  return exp(-__dmul_rn(delta, delta) / denom);
+}
+
+// One table slot per (kind, per-axis offset): the 8 x 8 matrix M in the three
+// fragment orders the apply kernel reads, plus row-major for export.
+__global__ void sep_tables_kernel(const SepJob* __restrict__ jobs, int p, int sL, double h, KernelParams kp,
+                                  const double* __restrict__ diag, double hd, double* __restrict__ corr_out) {
+  const SepJob jb = jobs[blockIdx.x];
+  __shared__ double G[kSepP * kSepP], T[kSepP * kSepP], M[kSepP * kSepP];
+  const int tid = threadIdx.x;   // 64 threads: one entry each
+  const int i = tid / kSepP, j = tid % kSepP;
+  if (jb.kind == 1) {
+    // near block factor (blocks.py:225-226): x_i = (t0 sL + i + 1/2) h, y_j likewise
+    const double x = __dmul_rn(__dadd_rn((double)(jb.t0 * sL + i), 0.5), h);
+    const double y = __dmul_rn(__dadd_rn((double)((jb.t0 + jb.o) * sL + j), 0.5), h);
+    M[tid] = __dmul_rn(h, gauss1d(__dadd_rn(x, -y), kp.denom));
+  } else {
+    // Chebyshev nodes of the target box [t0 s h, (t0+1) s h) and the source box
+    const double tlo = (double)(jb.t0 * jb.side) * h, thi = (double)((jb.t0 + 1) * jb.side) * h;
+    const double slo = (double)((jb.t0 + jb.o) * jb.side) * h, shi = (double)((jb.t0 + jb.o + 1) * jb.side) * h;
+    const double xi = cheb_node(tlo, thi, i + 1, p), eta = cheb_node(slo, shi, j + 1, p);
+    G[tid] = __dmul_rn(h, gauss1d(__dadd_rn(xi, -eta), kp.denom));
+    __syncthreads();
+    // T = R G (target mode), M = T R^T (source mode); R row-major p x p
+    double acc = 0.0;
+    for (int k = 0; k < p; ++k) acc += jb.R[i * p + k] * G[k * kSepP + j];
+    T[tid] = acc;
+    __syncthreads();
+    acc = 0.0;
+    for (int k = 0; k < p; ++k) acc += T[i * kSepP + k] * jb.R[j * p + k];
+    M[tid] = acc;
+  }
+  __syncthreads();
+  double* dst = jb.dst;
+  // [0, 64): mode-z A fragments, [ks][lane] = M[lane/4][4 ks + lane%4]
+  // [64, 128): mode-x A fragments, [ks][lane] = M[lane/4][2 (lane%4) + ks]
+  // [128, 192): mode-y scalars, [t][j] = scale * M[j][t]
+  // [192, 256): M row-major (unscaled; block export)
+  {
+    const int ks = tid / 32, lane = tid % 32;
+    dst[tid] = M[(lane >> 2) * kSepP + 4 * ks + (lane & 3)];
+    dst[64 + tid] = M[(lane >> 2) * kSepP + 2 * (lane & 3) + ks];
+    dst[128 + tid] = kp.scale * M[j * kSepP + i];   // tid = t * 8 + j with t = i
+    dst[192 + tid] = M[tid];
+  }
+  if (jb.kind == 1 && jb.o == 0 && tid == 0 && corr_out) {
+    // self block diagonal: reference value hd * cell average, Kronecker value
+    // scale * E(0)[0][0]^3 (the product the apply kernel forms)
+    const double e = M[0];
+    corr_out[0] = hd * diag[0] - (kp.scale * e) * e * e;
+  }
+}
+
+template <bool kSelfCorr>
+__device__ __forceinline__ void sep_item(const double* __restrict__ tab, const SepItem& it, const int2* __restrict__ pr,
+                                         const double* __restrict__ B, int ldb, double* __restrict__ C, int ldc, int R,
+                                         int r, double corr, int NO, int lane) {
+  double y[kSepP][2];
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
+  double z[kSepP][2];
+#pragma unroll
+  for (int t = 0; t < kSepP; ++t) z[t][0] = z[t][1] = 0.0;
+  const int boff = (lane >> 2) + 64 * (lane & 3);
+  auto load = [&](double (&x)[kSepP][2], int src) {
+    const double* s = B + ((int64_t)src * R + r) * ldb + boff;
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      x[t][0] = __ldg(s + 8 * t);
+      x[t][1] = __ldg(s + 8 * t + 256);
+    }
+  };
+  int2 cur = pr[0];
+  double xb[kSepP][2];
+  load(xb, cur.x);
+  for (int q = 0; q < it.count; ++q) {
+    const bool more = q + 1 < it.count;
+    const int2 nxt = more ? pr[q + 1] : cur;
+    double xn[kSepP][2];
+    if (more) load(xn, nxt.x);
+    // mode z (per pair): Z_t += Mz(o_z) X_t
+    {
+      const int code = cur.y;
+      const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
+      const double a0 = az[lane], a1 = az[32 + lane];
+#pragma unroll
+      for (int t = 0; t < kSepP; ++t) {
+        dmma(z[t][0], z[t][1], a0, xb[t][0]);
+        dmma(z[t][0], z[t][1], a1, xb[t][1]);
+      }
+    }
+    const int g = cur.y >> 4;
+    if (!more || (nxt.y >> 4) != g) {
+      // group flush: Y += My(o_y) . (Mx(o_x) . Z)
+      const int kind = g >> 8, ox = (g >> 4) & 15, oy = g & 15;
+      const double* ax = tab + (kind * NO + ox) * kSepSlotSmem + 64;
+      const double b0 = ax[lane], b1 = ax[32 + lane];
+      const double* my = tab + (kind * NO + oy) * kSepSlotSmem + 128;
+#pragma unroll
+      for (int t = 0; t < kSepP; ++t) {
+        double t0 = 0.0, t1 = 0.0;
+        dmma(t0, t1, b0, z[t][0]);
+        dmma(t0, t1, b1, z[t][1]);
+        const double2* mv = reinterpret_cast<const double2*>(my + t * kSepP);
+#pragma unroll
+        for (int jp = 0; jp < kSepP / 2; ++jp) {
+          const double2 m = mv[jp];
+          y[2 * jp][0] = fma(m.x, t0, y[2 * jp][0]);
+          y[2 * jp][1] = fma(m.x, t1, y[2 * jp][1]);
+          y[2 * jp + 1][0] = fma(m.y, t0, y[2 * jp + 1][0]);
+          y[2 * jp + 1][1] = fma(m.y, t1, y[2 * jp + 1][1]);
+        }
+        z[t][0] = z[t][1] = 0.0;
+      }
+    }
+    if (more) {
+#pragma unroll
+      for (int t = 0; t < kSepP; ++t) {
+        xb[t][0] = xn[t][0];
+        xb[t][1] = xn[t][1];
+      }
+      cur = nxt;
+    }
+  }
+  const int yoff = (lane >> 2) + 128 * (lane & 3);   // i + 64 k', k' = 2 (lane % 4) + jj
+  if (kSelfCorr) {
+    const double* s = B + ((int64_t)it.tgt * R + r) * ldb + yoff;
+#pragma unroll
+    for (int j = 0; j < kSepP; ++j) {
+      y[j][0] = fma(corr, __ldg(s + 8 * j), y[j][0]);
+      y[j][1] = fma(corr, __ldg(s + 8 * j + 64), y[j][1]);
+    }
+  }
+  double* o = C + ((int64_t)it.tgt * R + r) * ldc + yoff;
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) {
+    atomicAdd(o + 8 * j, y[j][0]);
+    atomicAdd(o + 8 * j + 64, y[j][1]);
+  }
+}
+
+__global__ void __launch_bounds__(kSepWarps * 32)
+    sep_apply_kernel(const double* __restrict__ tables, int nslots, int NO, const SepItem* __restrict__ items,
+                     int nitems, const int2* __restrict__ pairs, const double* __restrict__ B, int ldb,
+                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr) {
+  extern __shared__ double tab[];
+  for (int e = threadIdx.x; e < nslots * kSepSlotSmem; e += blockDim.x)
+    tab[e] = tables[(e / kSepSlotSmem) * kSepSlot + e % kSepSlotSmem];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kSepWarps + (threadIdx.x >> 5);
+  if (item >= nitems) return;
+  const SepItem it = items[item];
+  const int r = blockIdx.y;
+  if (it.flags & 1)
+    sep_item<true>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, corr_ptr[0], NO, lane);
+  else
+    sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane);
+}
+
+}  // namespace
+
+void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
+                       const double* diag, double hd, double* corr_out, cudaStream_t st) {
+  if (njobs <= 0) return;
+  sep_tables_kernel<<<njobs, kSepP * kSepP, 0, st>>>(jobs, p, sL, h, kp, diag, hd, corr_out);
+}
+
+size_t sep_smem_bytes(int nslots) { return (size_t)nslots * kSepSlotSmem * sizeof(double); }
+
+void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st) {
+  if (nitems <= 0) return;
+  const size_t smem = sep_smem_bytes(nslots);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sep_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  dim3 grid((nitems + kSepWarps - 1) / kSepWarps, R);
+  sep_apply_kernel<<<grid, kSepWarps * 32, smem, st>>>(tables, nslots, NO, items, nitems, pairs, B, ldb, C, ldc, R,
+                                                       corr);
+}
+
+}  // namespace htlr

@@ -169,10 +169,22 @@ class HTLRMatrix:
         mats = [fac[i * s * p:(i + 1) * s * p].reshape(s, p).copy() for i in range(2 * d)]
         return TuckerBlock(core=core, u_factors=mats[:d], v_factors=mats[d:])
 
+    FORMULATIONS = ("dense", "separable", "regenerated")
+
+    def formulation(self) -> str:
+        """How the device applies the blocks (same operator in every case):
+        "dense" deduplicated cores, "separable" Kronecker per-axis factors
+        (Gaussian kernel, p = leaf side = 8, 3-D), or "regenerated" (mapped grid)."""
+        rc = _lib.lib().htlr_formulation(self._plan)
+        if rc < 0:
+            _lib.check(rc)
+        return self.FORMULATIONS[rc]
+
     def last_launch_count(self) -> int:
         return int(_lib.lib().htlr_last_launch_count(self._plan))
 
-    PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward", "regen_level", "regen_near")
+    PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward", "regen_level", "regen_near", "sep_level",
+              "sep_leaf")
 
     def profile(self, on: bool = True) -> None:
         """Bracket every kernel launch of later matvecs with CUDA events."""

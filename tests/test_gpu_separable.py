@@ -1,0 +1,155 @@
+"""GPU parity of the separable-core formulation (htlr_sep.cu): a Gaussian
+kernel on a uniform 3-D grid with p = leaf side = 8 applies every block as
+the Kronecker product of three 8 x 8 per-axis factors.  Same operator as the
+reference's dense cores (blocks.py:126-227), so the bar is the same: relative
+2-norm error <= 1e-12 against the oracle / the reference's fixtures (the
+config-4 fixture is checked in test_gpu_parity.py), and against the
+dense-core GEMM path of this package (HTLR_SEPARABLE=0)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2508_05958_b200 as H
+from oracle import htlr_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def make(n, sigma=0.1, scale=1.0, a=0.0):
+    cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0),
+                        kernel=H.gaussian(sigma, scale=scale), coeff=H.CoefficientFn.constant(a))
+    return H.construct(cfg, H.UniformGrid(3, n))
+
+
+def problem(n, sigma=0.1, scale=1.0, a=0.0):
+    return O.Problem(d=3, n=n, rank=8, leaf_side_max=8, kernel=O.Kernel("gaussian", sigma=sigma, scale=scale),
+                     coeff=O.constant_coeff(a))
+
+
+BOXES = {
+    32: [((0, 8), (0, 8), (0, 8)), ((8, 16), (16, 24), (24, 32)), ((16, 24), (8, 16), (8, 16))],
+    64: [((0, 8), (0, 8), (0, 8)), ((24, 32), (40, 48), (56, 64)), ((32, 40), (32, 40), (24, 32))],
+}
+
+
+@pytest.mark.parametrize("n,sigma,scale,a", [(32, 0.15, 1.3, 0.7), (64, 0.1, 1.0, 0.0)])
+def test_separable_sampled_rows_vs_oracle(n, sigma, scale, a):
+    """Corner, edge and interior leaf boxes (every kind: near blocks with the
+    self-block diagonal correction, leaf-level square cores, and at n = 64 the
+    QR-factored level-2 cores) with two right-hand sides."""
+    op = make(n, sigma, scale, a)
+    assert op.formulation() == "separable"
+    U = np.random.default_rng(n).standard_normal((n ** 3, 2))
+    F = H.matmat(op, U)
+    rows = O.sampled_matvec(problem(n, sigma, scale, a), U, BOXES[n])
+    for i, bx in enumerate(BOXES[n]):
+        assert rel(F[O.box_linear_indices(n, bx)], rows[i]) <= TOL
+
+
+def test_separable_blocks_vs_oracle():
+    """Construction parity: the exported separable blocks (Kronecker products
+    of the device-built per-axis factors) against the oracle's Tucker / dense
+    blocks, per (kind, level), after QR sign normalisation."""
+    n = 64
+    op = make(n, 0.1, 1.0, 0.25)
+    pb = problem(n, 0.1, 1.0, 0.25)
+    leaves = O.block_leaves(n, 3, 8)
+    diag = pb.diag()
+    picked = {}
+    for lf in leaves:
+        key = (lf.kind, lf.tau[0][1] - lf.tau[0][0])
+        picked.setdefault(key, []).append(lf)
+    rng = np.random.default_rng(5)
+    chosen = []
+    for key, lst in sorted(picked.items()):
+        for j in rng.choice(len(lst), size=min(3, len(lst)), replace=False):
+            chosen.append(lst[int(j)])
+    selfs = [lf for lf in leaves if lf.kind != O.ADM and lf.tau == lf.sigma][:2]
+    assert len(chosen) >= 6
+    for lf in chosen + selfs:
+        got = op.payloads[lf.leaf_id]
+        ref = O.build_payload(pb, lf, diag)
+        if isinstance(ref, O.Tucker):
+            assert rel(H.materialize(got), O.materialize_tucker(ref)) <= TOL
+        else:
+            assert rel(got.matrix, ref) <= TOL
+
+
+_DENSE_SCRIPT = r"""
+import sys
+import numpy as np
+import paper_2508_05958_b200 as H
+from paper_2508_05958_b200.configs import WORKLOADS
+w = WORKLOADS["cfg4"]
+op = H.construct(w.build_config(), w.grid)
+np.save(sys.argv[1], H.matvec(op, w.input()))
+print(op.formulation())
+"""
+
+
+def test_cfg4_separable_equals_dense_cores(tmp_path):
+    """BASELINE config 4 through both formulations: the separable default and
+    the dense-core GEMM path (HTLR_SEPARABLE=0, its own process)."""
+    from paper_2508_05958_b200.configs import WORKLOADS
+    w = WORKLOADS["cfg4"]
+    op = H.construct(w.build_config(), w.grid)
+    assert op.formulation() == "separable"
+    f = H.matvec(op, w.input())
+    out = tmp_path / "f.npy"
+    r = subprocess.run([sys.executable, "-c", _DENSE_SCRIPT, str(out)], check=True, cwd=ROOT, capture_output=True,
+                       text=True, env={**os.environ, "PYTHONPATH": ROOT, "HTLR_SEPARABLE": "0"}, timeout=900)
+    assert r.stdout.strip().splitlines()[-1] == "dense"
+    err = rel(f, np.load(out))
+    print("cfg4 separable vs dense cores", err)
+    assert err <= 1e-13
+
+
+_CHUNK_SCRIPT = r"""
+import sys
+import numpy as np
+import paper_2508_05958_b200 as H
+cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.gaussian(0.1),
+                    coeff=H.CoefficientFn.constant(0.0))
+op = H.construct(cfg, H.UniformGrid(3, 64))
+assert op.formulation() == "separable"
+U = np.random.default_rng(64).standard_normal((64 ** 3, 2))
+np.save(sys.argv[1], H.matmat(op, U))
+"""
+
+
+@pytest.mark.parametrize("env", [{"HTLR_SEP_CHUNK": "1"}, {"HTLR_SEP_CHUNK": "9"}, {"HTLR_SEP_CHUNK": "100000"},
+                                 {"HTLR_GRAPHS": "0"}])
+def test_separable_item_splits(tmp_path, env):
+    """Work items cut at every group (chunk 1), at a few groups, or one item
+    per target list, and direct launches: identical operator."""
+    out = tmp_path / "f.npy"
+    subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT, str(out)], check=True, cwd=ROOT,
+                   env={**os.environ, "PYTHONPATH": ROOT, **env}, timeout=600)
+    F = np.load(out)
+    U = np.random.default_rng(64).standard_normal((64 ** 3, 2))
+    bx = BOXES[64]
+    rows = O.sampled_matvec(problem(64), U, bx)
+    for i, b in enumerate(bx):
+        assert rel(F[O.box_linear_indices(64, b)], rows[i]) <= TOL
+
+
+def test_non_separable_configs_keep_dense_cores():
+    """1/r kernels, p != 8 and 2-D problems keep the dense-core path."""
+    cfg = H.BuildConfig(rank=6, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.gaussian(0.1),
+                        coeff=H.CoefficientFn.constant(0.0))
+    assert H.construct(cfg, H.UniformGrid(3, 32)).formulation() == "dense"
+    cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
+                        coeff=H.CoefficientFn.constant(0.0))
+    assert H.construct(cfg, H.UniformGrid(3, 32)).formulation() == "dense"
