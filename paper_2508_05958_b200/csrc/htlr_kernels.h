@@ -163,6 +163,25 @@ struct SepJob {
 struct SepItem {
   int tgt, begin, count, flags;
 };
+// cooperative leaf-pass variant (sep_block_kernel): one CTA per (parent
+// cluster, part of its source columns); warp w applies the blocks of child
+// target tgt0 + w, the source boxes of a column (equal x, y box coordinates)
+// are staged once per CTA by bulk copies and shared by the 8 warps
+constexpr int kSepColMax = 10;      // source boxes per column
+constexpr int kSepBoxSmem = 8 * 68; // staged box: 8 z-planes of 64 doubles, padded (bank-conflict-free fragments)
+constexpr int kSepRing = 3;         // column slots in flight
+struct SepCol {
+  int n;                                   // boxes in the column
+  int src[kSepColMax];                     // source ids, ascending z
+  unsigned short code[kSepColMax][8];      // per (box, warp): pair code, 0xFFFF = not in that target's list
+  int pad;
+};
+struct SepBlock {
+  int tgt0, col_begin, col_count, corr_mask;   // corr_mask bit w: warp w's self pair is in this part
+};
+size_t sep_block_smem_bytes(int nslots);
+void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st);
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
                        const double* diag, double hd, double* corr_out, cudaStream_t st);
 size_t sep_smem_bytes(int nslots);

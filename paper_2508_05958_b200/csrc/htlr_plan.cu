@@ -92,7 +92,8 @@ struct Pass {
   // separable-core formulation (htlr_sep.cu): per-target pair runs sorted by
   // (kind, o_x, o_y, o_z), warp work items, 1-D factor tables
   DevBuf sep_tab, sep_pairs, sep_items;
-  int sep_nitems = 0, sep_NO = 0;
+  DevBuf sep_blocks, sep_cols;   // cooperative leaf-pass layout (sep_block_kernel), if built
+  int sep_nitems = 0, sep_NO = 0, sep_nblocks = 0;
   int64_t sep_groups = 0;
 };
 
@@ -476,6 +477,8 @@ int htlr_plan_destroy(htlr_plan* pl) {
     ps.sep_tab.release();
     ps.sep_pairs.release();
     ps.sep_items.release();
+    ps.sep_blocks.release();
+    ps.sep_cols.release();
   }
   pl->sep_corr.release();
   pl->diag.release();
@@ -949,6 +952,124 @@ static bool regen_sym_enabled() {
   return on == 1;
 }
 
+// HTLR_SEP_BLOCK=0: leaf pass by per-warp items instead of the cooperative
+// per-parent CTAs (A/B runs, tests)
+static bool sep_block_enabled() {
+  const char* e = std::getenv("HTLR_SEP_BLOCK");
+  return !(e && e[0] == '0');
+}
+
+// Cooperative leaf-pass layout: per parent cluster (8 consecutive Morton
+// targets), the union of its children's sources grouped into columns of equal
+// (x, y) box coordinates, each box with the pair code of every child (or
+// 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default 34) per CTA,
+// CTAs ordered by decreasing work.  Leaves the pass on per-warp items when a
+// column is longer than kSepColMax or the own range is not whole parents.
+static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>& ptr, const std::vector<int2>& ent) {
+  const int L = ps.level;
+  const int64_t t0 = pl->own_lo[L], nt = pl->own_hi[L] - t0;
+  if (t0 % 8 || nt % 8 || pl->d != 3) return 0;
+  const char* e = std::getenv("HTLR_SEP_COLS");
+  const int per_part = (e && std::atoi(e) > 0) ? std::atoi(e) : 34;
+  const int64_t npar = nt / 8;
+  std::vector<std::vector<htlr::SepCol>> pcols((size_t)npar);
+  std::vector<std::vector<int>> pself((size_t)npar);
+  std::atomic<bool> ok{true};
+  parallel_for((size_t)npar, [&](size_t P) {
+    // (source coords, source id) -> per-child codes
+    struct Src {
+      int x, y, z, id;
+      unsigned short code[8];
+    };
+    std::vector<Src> v;
+    std::unordered_map<int, int> at;
+    for (int w = 0; w < 8; ++w) {
+      const int64_t t = (int64_t)P * 8 + w;
+      for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k) {
+        const int src = ent[k].x;
+        auto it = at.find(src);
+        int idx;
+        if (it == at.end()) {
+          idx = (int)v.size();
+          at.emplace(src, idx);
+          Src s{};
+          int c[3];
+          htlr::morton_decode(src, 3, L, c);
+          s.x = c[0];
+          s.y = c[1];
+          s.z = c[2];
+          s.id = src;
+          for (auto& q : s.code) q = 0xFFFF;
+          v.push_back(s);
+        } else {
+          idx = it->second;
+        }
+        v[idx].code[w] = (unsigned short)ent[k].y;
+      }
+    }
+    std::sort(v.begin(), v.end(), [](const Src& a, const Src& b) {
+      return a.x != b.x ? a.x < b.x : a.y != b.y ? a.y < b.y : a.z < b.z;
+    });
+    auto& cols = pcols[P];
+    int self_col[8];
+    for (auto& q : self_col) q = -1;
+    for (size_t i = 0; i < v.size();) {
+      size_t j = i;
+      while (j < v.size() && v[j].x == v[i].x && v[j].y == v[i].y) ++j;
+      if (j - i > (size_t)htlr::kSepColMax) {
+        ok = false;
+        return;
+      }
+      htlr::SepCol c{};
+      c.n = (int)(j - i);
+      for (size_t k = i; k < j; ++k) {
+        c.src[k - i] = v[k].id;
+        for (int w = 0; w < 8; ++w) {
+          c.code[k - i][w] = v[k].code[w];
+          if (v[k].id == (int)(t0 + (int64_t)P * 8 + w)) self_col[w] = (int)cols.size();
+        }
+      }
+      cols.push_back(c);
+      i = j;
+    }
+    pself[P].assign(self_col, self_col + 8);
+  });
+  if (!ok) return 0;
+  struct Part {
+    htlr::SepBlock b;
+    int64_t work;
+  };
+  std::vector<Part> parts;
+  std::vector<htlr::SepCol> all;
+  for (int64_t P = 0; P < npar; ++P) {
+    const auto& cols = pcols[P];
+    for (size_t c0 = 0; c0 < cols.size(); c0 += per_part) {
+      const size_t c1 = std::min(cols.size(), c0 + per_part);
+      Part pt;
+      pt.b.tgt0 = (int)(t0 + P * 8);
+      pt.b.col_begin = (int)(all.size() + (c0));
+      pt.b.col_count = (int)(c1 - c0);
+      pt.b.corr_mask = 0;
+      pt.work = 0;
+      for (size_t c = c0; c < c1; ++c) pt.work += cols[c].n;
+      for (int w = 0; w < 8; ++w)
+        if (pself[P][w] >= (int)c0 && pself[P][w] < (int)c1) pt.b.corr_mask |= 1 << w;
+      parts.push_back(pt);
+    }
+    all.insert(all.end(), cols.begin(), cols.end());
+  }
+  std::stable_sort(parts.begin(), parts.end(), [](const Part& a, const Part& b) { return a.work > b.work; });
+  std::vector<htlr::SepBlock> blocks;
+  for (const auto& pt : parts) blocks.push_back(pt.b);
+  if (ps.sep_cols.alloc(std::max<size_t>(1, all.size()) * sizeof(htlr::SepCol))) return 1;
+  if (!all.empty()) CUDA_TRY(cudaMemcpy(ps.sep_cols.ptr, all.data(), all.size() * sizeof(htlr::SepCol), cudaMemcpyHostToDevice));
+  if (ps.sep_blocks.alloc(std::max<size_t>(1, blocks.size()) * sizeof(htlr::SepBlock))) return 1;
+  if (!blocks.empty())
+    CUDA_TRY(cudaMemcpy(ps.sep_blocks.ptr, blocks.data(), blocks.size() * sizeof(htlr::SepBlock), cudaMemcpyHostToDevice));
+  ps.sep_nblocks = (int)blocks.size();
+  return 0;
+}
+
 static int upload_sep(Pass& ps, const std::vector<int2>& ent, const std::vector<htlr::SepItem>& items) {
   if (ps.sep_pairs.alloc(std::max<size_t>(1, ent.size()) * sizeof(int2))) return 1;
   if (!ent.empty()) CUDA_TRY(cudaMemcpy(ps.sep_pairs.ptr, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -1048,6 +1169,8 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   ps.sep_groups = groups;
   ps.sep_nitems = (int)items.size();
   if (upload_sep(ps, ent, items)) return 1;
+  ps.sep_nblocks = 0;
+  if (leaf && sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
   // factor tables: kind 0 (admissible, level factor folded) and kind 1 (near)
   const int nslots = 2 * NO;
   if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;
@@ -1243,6 +1366,8 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       ps.sep_tab.release();
       ps.sep_pairs.release();
       ps.sep_items.release();
+      ps.sep_blocks.release();
+      ps.sep_cols.release();
     }
     pl->device_scalars = 0;
   }
@@ -1737,9 +1862,14 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       const double flops = 2.0 * m4 * ((double)ps.npairs + 2.0 * (double)ps.sep_groups) * R;
       const double bytes = 2.0 * R8 * (double)ps.P * ncl + 8.0 * 2 * ps.sep_NO * htlr::kSepSlot;
       if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, flops, bytes)) return 1;
-      htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
-                             ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
-                             pl->sep_corr.d(), cx.st);
+      if (ps.sep_nblocks > 0)
+        htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
+                               ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, B, ps.K_pad, C, ps.P, R,
+                               pl->sep_corr.d(), cx.st);
+      else
+        htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
+                               ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
+                               pl->sep_corr.d(), cx.st);
       if (cx.prof_end()) return 1;
       continue;
     }

@@ -41,6 +41,7 @@
 //                               += sum_t My[j, t] T_t[i, k']
 #include "htlr_device.cuh"
 #include "htlr_kernels.h"
+#include "htlr_mbarrier.cuh"
 
 namespace htlr {
 
@@ -107,6 +108,31 @@ __global__ void sep_tables_kernel(const SepJob* __restrict__ jobs, int p, int sL
   }
 }
 
+// Group flush shared by both apply kernels: Y += My(o_y) . (Mx(o_x) . Z).
+__device__ __forceinline__ void sep_flush(const double* __restrict__ tab, int g, int NO, int lane,
+                                          double (&z)[kSepP][2], double (&y)[kSepP][2]) {
+  const int kind = g >> 8, ox = (g >> 4) & 15, oy = g & 15;
+  const double* ax = tab + (kind * NO + ox) * kSepSlotSmem + 64;
+  const double b0 = ax[lane], b1 = ax[32 + lane];
+  const double* my = tab + (kind * NO + oy) * kSepSlotSmem + 128;
+#pragma unroll
+  for (int t = 0; t < kSepP; ++t) {
+    double t0 = 0.0, t1 = 0.0;
+    dmma(t0, t1, b0, z[t][0]);
+    dmma(t0, t1, b1, z[t][1]);
+    const double2* mv = reinterpret_cast<const double2*>(my + t * kSepP);
+#pragma unroll
+    for (int jp = 0; jp < kSepP / 2; ++jp) {
+      const double2 m = mv[jp];
+      y[2 * jp][0] = fma(m.x, t0, y[2 * jp][0]);
+      y[2 * jp][1] = fma(m.x, t1, y[2 * jp][1]);
+      y[2 * jp + 1][0] = fma(m.y, t0, y[2 * jp + 1][0]);
+      y[2 * jp + 1][1] = fma(m.y, t1, y[2 * jp + 1][1]);
+    }
+    z[t][0] = z[t][1] = 0.0;
+  }
+}
+
 template <bool kSelfCorr>
 __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const SepItem& it, const int2* __restrict__ pr,
                                          const double* __restrict__ B, int ldb, double* __restrict__ C, int ldc, int R,
@@ -147,27 +173,7 @@ __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const S
     }
     const int g = cur.y >> 4;
     if (!more || (nxt.y >> 4) != g) {
-      // group flush: Y += My(o_y) . (Mx(o_x) . Z)
-      const int kind = g >> 8, ox = (g >> 4) & 15, oy = g & 15;
-      const double* ax = tab + (kind * NO + ox) * kSepSlotSmem + 64;
-      const double b0 = ax[lane], b1 = ax[32 + lane];
-      const double* my = tab + (kind * NO + oy) * kSepSlotSmem + 128;
-#pragma unroll
-      for (int t = 0; t < kSepP; ++t) {
-        double t0 = 0.0, t1 = 0.0;
-        dmma(t0, t1, b0, z[t][0]);
-        dmma(t0, t1, b1, z[t][1]);
-        const double2* mv = reinterpret_cast<const double2*>(my + t * kSepP);
-#pragma unroll
-        for (int jp = 0; jp < kSepP / 2; ++jp) {
-          const double2 m = mv[jp];
-          y[2 * jp][0] = fma(m.x, t0, y[2 * jp][0]);
-          y[2 * jp][1] = fma(m.x, t1, y[2 * jp][1]);
-          y[2 * jp + 1][0] = fma(m.y, t0, y[2 * jp + 1][0]);
-          y[2 * jp + 1][1] = fma(m.y, t1, y[2 * jp + 1][1]);
-        }
-        z[t][0] = z[t][1] = 0.0;
-      }
+      sep_flush(tab, g, NO, lane, z, y);
     }
     if (more) {
 #pragma unroll
@@ -214,7 +220,138 @@ __global__ void __launch_bounds__(kSepWarps * 32)
     sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane);
 }
 
+// Cooperative leaf pass: CTA = (parent cluster, part of the source columns
+// of its 8 children), 8 consumer warps (warp w = child target tgt0 + w) and a
+// producer warp that bulk-copies every source box of a column once, as 8
+// z-planes at a 68-double pitch (so the mode-z B fragments -- lanes
+// a = lane/4, c = 4 ks + lane%4 -- hit 32 distinct banks), into a ring of
+// kSepRing column slots (full / empty mbarriers).  A column has fixed
+// (o_x, o_y) for every warp, so each warp flushes its Z accumulators (one per
+// block kind) once per column.
+__global__ void __launch_bounds__(9 * 32, 1)
+    sep_block_kernel(const double* __restrict__ tables, int nslots, int NO, const SepBlock* __restrict__ blocks,
+                     const SepCol* __restrict__ cols, const double* __restrict__ B, int ldb, double* __restrict__ C,
+                     int ldc, int R, const double* __restrict__ corr_ptr) {
+  constexpr int NS = kSepRing, SLOT = kSepColMax * kSepBoxSmem;
+  extern __shared__ __align__(16) double sm[];
+  double* tab = sm;
+  double* ring = tab + nslots * kSepSlotSmem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * SLOT);
+  uint64_t* empty = full + NS;
+  const SepBlock bk = blocks[blockIdx.x];
+  const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int e = threadIdx.x; e < nslots * kSepSlotSmem; e += blockDim.x)
+    tab[e] = tables[(e / kSepSlotSmem) * kSepSlot + e % kSepSlotSmem];
+  __syncthreads();
+  const SepCol* cl = cols + bk.col_begin;
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    for (int c = 0; c < bk.col_count; ++c) {
+      const int slot = c % NS;
+      if (c >= NS) mbar_wait(&empty[slot], (unsigned)(((c / NS) - 1) & 1));
+      const int n = cl[c].n;
+      if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * 512 * 8));
+      __syncwarp();
+      double* dst = ring + slot * SLOT;
+      for (int e = lane; e < n * 8; e += 32) {
+        const int k = e >> 3, pl = e & 7;
+        bulk_g2s(dst + k * kSepBoxSmem + pl * 68, B + ((int64_t)cl[c].src[k] * R + r) * ldb + pl * 64, 64 * 8,
+                 &full[slot]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------- consumers
+  double y[kSepP][2];
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
+  const int xoff = (lane >> 2) + 68 * (lane & 3);
+  for (int c = 0; c < bk.col_count; ++c) {
+    const int slot = c % NS;
+    const int n = cl[c].n;
+    double za[kSepP][2], zn[kSepP][2];
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) za[t][0] = za[t][1] = zn[t][0] = zn[t][1] = 0.0;
+    int ga = -1, gn = -1;
+    mbar_wait(&full[slot], (unsigned)((c / NS) & 1));
+    const double* xs = ring + slot * SLOT + xoff;
+    for (int k = 0; k < n; ++k) {
+      const int code = cl[c].code[k][warp];
+      if (code == 0xFFFF) continue;
+      double xv[kSepP][2];
+#pragma unroll
+      for (int t = 0; t < kSepP; ++t) {
+        xv[t][0] = xs[k * kSepBoxSmem + 8 * t];
+        xv[t][1] = xs[k * kSepBoxSmem + 8 * t + 272];
+      }
+      const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
+      const double a0 = az[lane], a1 = az[32 + lane];
+      if (code >> 12) {
+        gn = code >> 4;
+#pragma unroll
+        for (int t = 0; t < kSepP; ++t) {
+          dmma(zn[t][0], zn[t][1], a0, xv[t][0]);
+          dmma(zn[t][0], zn[t][1], a1, xv[t][1]);
+        }
+      } else {
+        ga = code >> 4;
+#pragma unroll
+        for (int t = 0; t < kSepP; ++t) {
+          dmma(za[t][0], za[t][1], a0, xv[t][0]);
+          dmma(za[t][0], za[t][1], a1, xv[t][1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (ga >= 0) sep_flush(tab, ga, NO, lane, za, y);
+    if (gn >= 0) sep_flush(tab, gn, NO, lane, zn, y);
+  }
+  const int tgt = bk.tgt0 + warp;
+  const int yoff = (lane >> 2) + 128 * (lane & 3);
+  if ((bk.corr_mask >> warp) & 1) {
+    const double corr = corr_ptr[0];
+    const double* s = B + ((int64_t)tgt * R + r) * ldb + yoff;
+#pragma unroll
+    for (int j = 0; j < kSepP; ++j) {
+      y[j][0] = fma(corr, __ldg(s + 8 * j), y[j][0]);
+      y[j][1] = fma(corr, __ldg(s + 8 * j + 64), y[j][1]);
+    }
+  }
+  double* o = C + ((int64_t)tgt * R + r) * ldc + yoff;
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) {
+    atomicAdd(o + 8 * j, y[j][0]);
+    atomicAdd(o + 8 * j + 64, y[j][1]);
+  }
+}
+
 }  // namespace
+
+size_t sep_block_smem_bytes(int nslots) {
+  return ((size_t)nslots * kSepSlotSmem + (size_t)kSepRing * kSepColMax * kSepBoxSmem) * sizeof(double) +
+         2 * kSepRing * sizeof(uint64_t);
+}
+
+void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st) {
+  if (nblocks <= 0) return;
+  const size_t smem = sep_block_smem_bytes(nslots);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sep_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  sep_block_kernel<<<dim3(nblocks, R), 9 * 32, smem, st>>>(tables, nslots, NO, blocks, cols, B, ldb, C, ldc, R, corr);
+}
 
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
                        const double* diag, double hd, double* corr_out, cudaStream_t st) {

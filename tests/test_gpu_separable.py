@@ -129,11 +129,15 @@ np.save(sys.argv[1], H.matmat(op, U))
 """
 
 
-@pytest.mark.parametrize("env", [{"HTLR_SEP_CHUNK": "1"}, {"HTLR_SEP_CHUNK": "9"}, {"HTLR_SEP_CHUNK": "100000"},
+@pytest.mark.parametrize("env", [{"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "1"},
+                                 {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "9"},
+                                 {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "100000"},
+                                 {"HTLR_SEP_COLS": "1"}, {"HTLR_SEP_COLS": "7"}, {"HTLR_SEP_COLS": "1000"},
                                  {"HTLR_GRAPHS": "0"}])
 def test_separable_item_splits(tmp_path, env):
-    """Work items cut at every group (chunk 1), at a few groups, or one item
-    per target list, and direct launches: identical operator."""
+    """Leaf pass by per-warp items (cut at every group, at a few groups, or
+    one item per target list) or by cooperative per-parent CTAs (one column,
+    a few, or all columns per CTA), and direct launches: identical operator."""
     out = tmp_path / "f.npy"
     subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT, str(out)], check=True, cwd=ROOT,
                    env={**os.environ, "PYTHONPATH": ROOT, **env}, timeout=600)
