@@ -169,7 +169,9 @@ struct SepItem {
 // are staged once per CTA by bulk copies and shared by the 8 warps
 constexpr int kSepColMax = 10;      // source boxes per column
 constexpr int kSepBoxSmem = 8 * 68; // staged box: 8 z-planes of 64 doubles, padded (bank-conflict-free fragments)
-constexpr int kSepRing = 3;         // column slots in flight
+// column slots in flight for NG consumer warp groups
+__host__ __device__ constexpr int sep_ring_slots(int NG) { return NG == 1 ? 3 : 4; }
+int sep_block_groups();
 struct SepCol {
   int n;                                   // boxes in the column
   int src[kSepColMax];                     // source ids, ascending z

@@ -952,25 +952,23 @@ static bool regen_sym_enabled() {
   return on == 1;
 }
 
-// HTLR_SEP_BLOCK=0: leaf pass by per-warp items instead of the cooperative
+// HTLR_SEP_BLOCK=0: passes by per-warp items instead of the cooperative
 // per-parent CTAs (A/B runs, tests)
 static bool sep_block_enabled() {
   const char* e = std::getenv("HTLR_SEP_BLOCK");
   return !(e && e[0] == '0');
 }
 
-// Cooperative leaf-pass layout: per parent cluster (8 consecutive Morton
+// Cooperative layout of a pass: per parent cluster (8 consecutive Morton
 // targets), the union of its children's sources grouped into columns of equal
 // (x, y) box coordinates, each box with the pair code of every child (or
-// 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default 34) per CTA,
+// 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default: ~8 waves of CTAs, <= 34 columns) per CTA,
 // CTAs ordered by decreasing work.  Leaves the pass on per-warp items when a
 // column is longer than kSepColMax or the own range is not whole parents.
 static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>& ptr, const std::vector<int2>& ent) {
   const int L = ps.level;
   const int64_t t0 = pl->own_lo[L], nt = pl->own_hi[L] - t0;
   if (t0 % 8 || nt % 8 || pl->d != 3) return 0;
-  const char* e = std::getenv("HTLR_SEP_COLS");
-  const int per_part = (e && std::atoi(e) > 0) ? std::atoi(e) : 34;
   const int64_t npar = nt / 8;
   std::vector<std::vector<htlr::SepCol>> pcols((size_t)npar);
   std::vector<std::vector<int>> pself((size_t)npar);
@@ -1035,6 +1033,17 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     pself[P].assign(self_col, self_col + 8);
   });
   if (!ok) return 0;
+  // columns per CTA: enough CTAs for ~8 waves, at most 34 columns each
+  int per_part = 34;
+  {
+    int64_t total = 0;
+    for (const auto& v : pcols) total += (int64_t)v.size();
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
+    per_part = (int)std::max<int64_t>(2, std::min<int64_t>(34, (total + 8 * sms - 1) / (8 * sms)));
+    const char* e = std::getenv("HTLR_SEP_COLS");
+    if (e && std::atoi(e) > 0) per_part = std::atoi(e);
+  }
   struct Part {
     htlr::SepBlock b;
     int64_t work;
@@ -1170,7 +1179,7 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   ps.sep_nitems = (int)items.size();
   if (upload_sep(ps, ent, items)) return 1;
   ps.sep_nblocks = 0;
-  if (leaf && sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
+  if (sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
   // factor tables: kind 0 (admissible, level factor folded) and kind 1 (near)
   const int nslots = 2 * NO;
   if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;

@@ -43,6 +43,8 @@
 #include "htlr_kernels.h"
 #include "htlr_mbarrier.cuh"
 
+#include <cstdlib>
+
 namespace htlr {
 
 namespace {
@@ -220,19 +222,22 @@ __global__ void __launch_bounds__(kSepWarps * 32)
     sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane);
 }
 
-// Cooperative leaf pass: CTA = (parent cluster, part of the source columns
-// of its 8 children), 8 consumer warps (warp w = child target tgt0 + w) and a
+// Cooperative pass: CTA = (parent cluster, part of the source columns of its
+// 8 children), NG groups of 8 consumer warps (warp w applies the blocks of
+// child target tgt0 + w % 8; group w / 8 takes every NG-th column) and a
 // producer warp that bulk-copies every source box of a column once, as 8
 // z-planes at a 68-double pitch (so the mode-z B fragments -- lanes
 // a = lane/4, c = 4 ks + lane%4 -- hit 32 distinct banks), into a ring of
-// kSepRing column slots (full / empty mbarriers).  A column has fixed
-// (o_x, o_y) for every warp, so each warp flushes its Z accumulators (one per
-// block kind) once per column.
-__global__ void __launch_bounds__(9 * 32, 1)
+// NS = ring_slots(NG) column slots (full / empty mbarriers).  A column has
+// fixed (o_x, o_y) for every warp, so a warp flushes its Z accumulator when
+// the block kind changes along the column and at its end (one flush for the
+// far columns, at most three where near blocks sit between admissible ones).
+template <int NG>
+__global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
     sep_block_kernel(const double* __restrict__ tables, int nslots, int NO, const SepBlock* __restrict__ blocks,
                      const SepCol* __restrict__ cols, const double* __restrict__ B, int ldb, double* __restrict__ C,
                      int ldc, int R, const double* __restrict__ corr_ptr) {
-  constexpr int NS = kSepRing, SLOT = kSepColMax * kSepBoxSmem;
+  constexpr int NS = sep_ring_slots(NG), SLOT = kSepColMax * kSepBoxSmem, NCW = 8 * NG;
   extern __shared__ __align__(16) double sm[];
   double* tab = sm;
   double* ring = tab + nslots * kSepSlotSmem;
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     tab[e] = tables[(e / kSepSlotSmem) * kSepSlot + e % kSepSlotSmem];
   __syncthreads();
   const SepCol* cl = cols + bk.col_begin;
-  if (warp == 8) {
+  if (warp == NCW) {
     // ------------------------------------------------------------ producer
     for (int c = 0; c < bk.col_count; ++c) {
       const int slot = c % NS;
@@ -270,22 +275,26 @@ __global__ void __launch_bounds__(9 * 32, 1)
     return;
   }
   // ------------------------------------------------------------- consumers
-  double y[kSepP][2];
+  const int tw = warp & 7, grp = warp >> 3;
+  double y[kSepP][2], z[kSepP][2];
 #pragma unroll
-  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
+  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = z[j][0] = z[j][1] = 0.0;
   const int xoff = (lane >> 2) + 68 * (lane & 3);
-  for (int c = 0; c < bk.col_count; ++c) {
+  for (int c = grp; c < bk.col_count; c += NG) {
     const int slot = c % NS;
     const int n = cl[c].n;
-    double za[kSepP][2], zn[kSepP][2];
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) za[t][0] = za[t][1] = zn[t][0] = zn[t][1] = 0.0;
-    int ga = -1, gn = -1;
+    // the column's pair codes of this warp's target, one per lane
+    const int mycode = lane < n ? (int)cl[c].code[lane][tw] : 0xFFFF;
     mbar_wait(&full[slot], (unsigned)((c / NS) & 1));
     const double* xs = ring + slot * SLOT + xoff;
+    int g = -1;
     for (int k = 0; k < n; ++k) {
-      const int code = cl[c].code[k][warp];
+      const int code = __shfl_sync(0xffffffffu, mycode, k);
       if (code == 0xFFFF) continue;
+      if ((code >> 4) != g) {   // kind change inside the column (o_x, o_y fixed)
+        if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
+        g = code >> 4;
+      }
       double xv[kSepP][2];
 #pragma unroll
       for (int t = 0; t < kSepP; ++t) {
@@ -294,30 +303,19 @@ __global__ void __launch_bounds__(9 * 32, 1)
       }
       const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
       const double a0 = az[lane], a1 = az[32 + lane];
-      if (code >> 12) {
-        gn = code >> 4;
 #pragma unroll
-        for (int t = 0; t < kSepP; ++t) {
-          dmma(zn[t][0], zn[t][1], a0, xv[t][0]);
-          dmma(zn[t][0], zn[t][1], a1, xv[t][1]);
-        }
-      } else {
-        ga = code >> 4;
-#pragma unroll
-        for (int t = 0; t < kSepP; ++t) {
-          dmma(za[t][0], za[t][1], a0, xv[t][0]);
-          dmma(za[t][0], za[t][1], a1, xv[t][1]);
-        }
+      for (int t = 0; t < kSepP; ++t) {
+        dmma(z[t][0], z[t][1], a0, xv[t][0]);
+        dmma(z[t][0], z[t][1], a1, xv[t][1]);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
-    if (ga >= 0) sep_flush(tab, ga, NO, lane, za, y);
-    if (gn >= 0) sep_flush(tab, gn, NO, lane, zn, y);
+    if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
   }
-  const int tgt = bk.tgt0 + warp;
+  const int tgt = bk.tgt0 + tw;
   const int yoff = (lane >> 2) + 128 * (lane & 3);
-  if ((bk.corr_mask >> warp) & 1) {
+  if (grp == 0 && ((bk.corr_mask >> tw) & 1)) {
     const double corr = corr_ptr[0];
     const double* s = B + ((int64_t)tgt * R + r) * ldb + yoff;
 #pragma unroll
@@ -336,21 +334,42 @@ __global__ void __launch_bounds__(9 * 32, 1)
 
 }  // namespace
 
+// HTLR_SEP_GROUPS=1|2: consumer warp groups of the cooperative kernel
+int sep_block_groups() {
+  static int g = 0;
+  if (!g) {
+    const char* e = std::getenv("HTLR_SEP_GROUPS");
+    g = (e && e[0] == '1') ? 1 : 2;
+  }
+  return g;
+}
+
 size_t sep_block_smem_bytes(int nslots) {
-  return ((size_t)nslots * kSepSlotSmem + (size_t)kSepRing * kSepColMax * kSepBoxSmem) * sizeof(double) +
-         2 * kSepRing * sizeof(uint64_t);
+  const int NS = sep_ring_slots(sep_block_groups());
+  return ((size_t)nslots * kSepSlotSmem + (size_t)NS * kSepColMax * kSepBoxSmem) * sizeof(double) +
+         2 * NS * sizeof(uint64_t);
+}
+
+template <int NG>
+static void launch_sep_block_t(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks,
+                               const SepCol* cols, const double* B, int ldb, double* C, int ldc, int R,
+                               const double* corr, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sep_block_kernel<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  sep_block_kernel<NG><<<dim3(nblocks, R), (8 * NG + 1) * 32, sep_block_smem_bytes(nslots), st>>>(
+      tables, nslots, NO, blocks, cols, B, ldb, C, ldc, R, corr);
 }
 
 void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
                       const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st) {
   if (nblocks <= 0) return;
-  const size_t smem = sep_block_smem_bytes(nslots);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sep_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  sep_block_kernel<<<dim3(nblocks, R), 9 * 32, smem, st>>>(tables, nslots, NO, blocks, cols, B, ldb, C, ldc, R, corr);
+  if (sep_block_groups() == 1)
+    launch_sep_block_t<1>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, st);
+  else
+    launch_sep_block_t<2>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, st);
 }
 
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,

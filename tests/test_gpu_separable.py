@@ -133,6 +133,7 @@ np.save(sys.argv[1], H.matmat(op, U))
                                  {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "9"},
                                  {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "100000"},
                                  {"HTLR_SEP_COLS": "1"}, {"HTLR_SEP_COLS": "7"}, {"HTLR_SEP_COLS": "1000"},
+                                 {"HTLR_SEP_GROUPS": "1"},
                                  {"HTLR_GRAPHS": "0"}])
 def test_separable_item_splits(tmp_path, env):
     """Leaf pass by per-warp items (cut at every group, at a few groups, or
