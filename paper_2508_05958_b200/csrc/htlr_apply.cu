@@ -137,6 +137,101 @@ __device__ __forceinline__ void upward_body(const double* __restrict__ u, double
   }
 }
 
+// Split variant for levels with few clusters (3-D): CTA (cluster, rhs, slab)
+// runs the three mode products on its side / nslab z-planes only, writes the
+// partial W (the mode-3 sum over its planes), and the last of the nslab CTAs
+// of the cluster (arrival counter, gpu-scope fences) sums the partials into W
+// and resets the counter.
+__device__ __forceinline__ void upward_split_body(const double* __restrict__ u, double* __restrict__ W, int n, int s,
+                                                  int p, int bits, int R, int K_pad, const double* __restrict__ Q,
+                                                  int64_t qstride, int64_t c, int64_t c0, int r, int slab, int nslab,
+                                                  double* __restrict__ scratch, int* __restrict__ counters,
+                                                  double* sm) {
+  const int zs = s / nslab, z0 = slab * zs;
+  double* sQ = sm;                 // 3 x s*p
+  double* T1 = sQ + 3 * s * p;     // p*s*zs
+  double* T2 = T1 + p * s * zs;    // p*p*zs
+  __shared__ int last;
+  int cc[3];
+  morton_decode(c, 3, bits, cc);
+  for (int i = threadIdx.x; i < 3 * s * p; i += blockDim.x) {
+    const int a = i / (s * p);
+    sQ[i] = Q[(qstride ? cc[a] * qstride : 0) + i % (s * p)];
+  }
+  const double* sQx = sQ;
+  const double* sQy = sQ + s * p;
+  const double* sQz = sQ + 2 * s * p;
+  const int P = p * p * p;
+  __syncthreads();
+  for (int i = threadIdx.x; i < p * s * zs; i += blockDim.x) {
+    const int a1 = i % p, y = (i / p) % s, z = z0 + i / (p * s);
+    const int64_t g = (int64_t)cc[0] * s + (int64_t)n * (cc[1] * s + y) + (int64_t)n * n * (cc[2] * s + z);
+    double v = 0.0;
+    for (int x = 0; x < s; ++x) v += sQx[x * p + a1] * u[(g + x) * R + r];
+    T1[i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < p * p * zs; i += blockDim.x) {
+    const int a1 = i % p, a2 = (i / p) % p, z = i / (p * p);
+    const double* t1 = T1 + a1 + p * s * z;
+    double v = 0.0;
+    for (int y = 0; y < s; ++y) v += sQy[y * p + a2] * t1[p * y];
+    T2[i] = v;
+  }
+  __syncthreads();
+  const int64_t cr = (c - c0) * R + r;
+  double* part = scratch + (cr * nslab + slab) * P;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const int a12 = i % (p * p), a3 = i / (p * p);
+    double v = 0.0;
+    for (int z = 0; z < zs; ++z) v += sQz[(z0 + z) * p + a3] * T2[a12 + p * p * z];
+    part[i] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counters + cr, 1) == nslab - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double* p0 = scratch + cr * nslab * P;
+  double* dst = W + ((int64_t)c * R + r) * K_pad;
+  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) {
+    double v = 0.0;
+    if (i < P)
+      for (int q = 0; q < nslab; ++q) v += __ldcg(p0 + q * P + i);
+    dst[i] = v;
+  }
+  if (threadIdx.x == 0) counters[cr] = 0;
+}
+
+size_t upward_split_smem_words(int side, int p, int nslab) {
+  const int zs = side / nslab;
+  return (size_t)3 * side * p + (size_t)p * side * zs + (size_t)p * p * zs;
+}
+
+int upward_nslab(int d, int side, int64_t nc, int R) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = std::getenv("HTLR_UPWARD_SPLIT");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  if (off || d != 3) return 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int ns = 1;
+  while (nc * R * ns < 2 * sms && side % (2 * ns) == 0 && side / (2 * ns) >= 2) ns *= 2;
+  return ns;
+}
+
+__global__ void upward_split_kernel(const double* __restrict__ u, double* __restrict__ W, int n, int s, int p,
+                                    int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
+                                    int64_t c0, int nslab, double* __restrict__ scratch, int* __restrict__ counters) {
+  extern __shared__ double sm[];
+  upward_split_body(u, W, n, s, p, bits, R, K_pad, Q, qstride, c0 + blockIdx.x / nslab, c0, blockIdx.y,
+                    (int)(blockIdx.x % nslab), nslab, scratch, counters, sm);
+}
+
 __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
                               int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
                               int64_t c0) {
@@ -160,8 +255,16 @@ __global__ void prologue_kernel(PrologueParams pp) {
   int64_t rest = b - pp.nb_perm - pp.nb_zero;
   for (int li = 0; li < pp.nlev; ++li) {
     const UpLevel& lv = pp.lev[li];
-    const int64_t cnt = lv.nc * pp.R;
+    const int ns = lv.nslab > 1 ? lv.nslab : 1;
+    const int64_t cnt = lv.nc * pp.R * ns;
     if (rest < cnt) {
+      if (ns > 1) {
+        const int64_t cr = rest / ns;
+        upward_split_body(pp.u, lv.W, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,
+                          lv.c0 + cr / pp.R, lv.c0, (int)(cr % pp.R), (int)(rest % ns), ns, lv.scratch, lv.counters,
+                          sm);
+        return;
+      }
       upward_body(pp.u, lv.W, pp.d, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,
                   lv.c0 + rest / pp.R, (int)(rest % pp.R), sm);
       return;
@@ -248,8 +351,11 @@ void launch_prologue(const PrologueParams& pp_in, cudaStream_t st) {
   size_t smem_words = 0;
   int64_t blocks = pp.nb_perm + pp.nb_zero;
   for (int li = 0; li < pp.nlev; ++li) {
-    smem_words = std::max(smem_words, upward_smem_words(pp.d, pp.lev[li].side, pp.p));
-    blocks += pp.lev[li].nc * pp.R;
+    const UpLevel& lv = pp.lev[li];
+    const int ns = lv.nslab > 1 ? lv.nslab : 1;
+    smem_words = std::max(smem_words, ns > 1 ? upward_split_smem_words(lv.side, pp.p, ns)
+                                             : upward_smem_words(pp.d, lv.side, pp.p));
+    blocks += lv.nc * pp.R * ns;
   }
   const size_t smem = smem_words * sizeof(double);
   if (smem > 48 * 1024) cudaFuncSetAttribute(prologue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -257,9 +363,18 @@ void launch_prologue(const PrologueParams& pp_in, cudaStream_t st) {
 }
 
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st) {
+                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st,
+                   int nslab, double* scratch, int* counters) {
   const size_t smem = sizeof(double) * upward_smem_words(d, side, p);
   if (nc <= 0) return;
+  if (nslab > 1 && d == 3) {
+    const size_t sm2 = sizeof(double) * upward_split_smem_words(side, p, nslab);
+    if (sm2 > 48 * 1024)
+      cudaFuncSetAttribute(upward_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    upward_split_kernel<<<dim3((unsigned)(nc * nslab), R), 256, sm2, st>>>(u, W, n, side, p, level, R, K_pad, Q,
+                                                                          qstride, c0, nslab, scratch, counters);
+    return;
+  }
   static int force_slab = -1;   // HTLR_UPWARD_SLAB=1: slab kernel for every box (tests)
   if (force_slab < 0) {
     const char* e = std::getenv("HTLR_UPWARD_SLAB");

@@ -104,7 +104,16 @@ struct UpLevel {
   const double* Q;
   int64_t qstride, c0, nc;
   int side, bits, K_pad;
+  // nslab > 1 (3-D): each (cluster, rhs) is split over nslab CTAs of
+  // side / nslab z-planes; their partial W land in `scratch` and the last CTA
+  // to arrive (per-(cluster, rhs) counter, reset by it) sums them into W
+  int nslab;
+  double* scratch;   // [cluster - c0][rhs][nslab][p^3]
+  int* counters;     // [cluster - c0][rhs], zero between launches
 };
+// z-slabs per cluster for a level of nc clusters x R right-hand sides (1: whole
+// boxes); HTLR_UPWARD_SPLIT=0 disables the split
+int upward_nslab(int d, int side, int64_t nc, int R);
 struct PrologueParams {
   const double* u;
   double* ub;
@@ -117,7 +126,8 @@ struct PrologueParams {
 size_t upward_smem_words(int d, int side, int p);
 void launch_prologue(const PrologueParams& pp, cudaStream_t st);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
-                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st);
+                   int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st,
+                   int nslab = 1, double* scratch = nullptr, int* counters = nullptr);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
 // gen: Toeplitz generators of the pass's matrices (near-only 3-D leaf pass
@@ -191,6 +201,12 @@ size_t sep_smem_bytes(int nslots);
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
                       const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st);
+
+// downward pass by per-warp mode products when p = leaf side = 8 in 3-D on a
+// uniform grid (HTLR_DOWN8=0 keeps downward_kernel)
+bool downward8_supported(int d, int p, int sL, const DownParams& dp);
+void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
+                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st);
 
 // mapped grid (htlr_mapped.cu)
 void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,

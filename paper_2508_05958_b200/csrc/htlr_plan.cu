@@ -181,6 +181,10 @@ struct Level {
   std::vector<int> csr_cols;
   DevBuf d_ptr, d_cols;
   SymList sym;             // sources sigma > tau for the symmetric regeneration
+  // split upward pass (few large clusters): z-slabs per cluster for the
+  // current nrhs, partial-W scratch and per-(cluster, rhs) arrival counters
+  int up_ns = 1;
+  DevBuf up_scratch, up_count;
 };
 
 }  // namespace
@@ -458,6 +462,8 @@ int htlr_plan_destroy(htlr_plan* pl) {
     lv.d_ptr.release();
     lv.d_cols.release();
     lv.sym.release();
+    lv.up_scratch.release();
+    lv.up_count.release();
   }
   pl->d_mb.release();
   pl->d_mx.release();
@@ -1570,6 +1576,23 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   cx.p = pl->p;
   cx.P = ipow(pl->p, pl->d);
   if (ensure_workspace(pl, cx.R)) return 1;
+  if (!pl->mapped) {
+    // split upward of levels with few clusters (outside any graph capture:
+    // a grown scratch invalidates the captured graphs)
+    for (auto& ps : pl->passes) {
+      if (ps.to_y) continue;
+      Level& lv = pl->levels[ps.level];
+      const int64_t nc = pl->own_hi[ps.level] - pl->own_lo[ps.level];
+      lv.up_ns = lv.Kron.ptr ? 1 : htlr::upward_nslab(cx.d, lv.side, nc, cx.R);
+      if (lv.up_ns <= 1) continue;
+      const size_t sb = (size_t)nc * cx.R * lv.up_ns * cx.P * sizeof(double), cb = (size_t)nc * cx.R * sizeof(int);
+      if (lv.up_scratch.bytes < sb || lv.up_count.bytes < cb) {
+        drop_graphs(pl);
+        if (lv.up_scratch.alloc(sb) || lv.up_count.alloc(cb)) return 1;
+        CUDA_TRY(cudaMemset(lv.up_count.ptr, 0, lv.up_count.bytes));
+      }
+    }
+  }
   for (auto& ps : pl->passes) {
     if (pl->sep || ps.tasks.count(cx.R)) continue;
     std::vector<htlr::GemmTask> tv;
@@ -1812,8 +1835,11 @@ int mv_local(MvCtx& cx, const double* u) {
         fused = false;
         break;
       }
-      pp.lev[pp.nlev++] = htlr::UpLevel{cx.W[i], lv.Q.d(), 0, pl->own_lo[ps.level],
-                                        pl->own_hi[ps.level] - pl->own_lo[ps.level], lv.side, lv.level, ps.K_pad};
+      pp.lev[pp.nlev++] = htlr::UpLevel{cx.W[i],       lv.Q.d(),      0,
+                                        pl->own_lo[ps.level], pl->own_hi[ps.level] - pl->own_lo[ps.level],
+                                        lv.side,         lv.level,      ps.K_pad,
+                                        lv.up_ns,        lv.up_ns > 1 ? lv.up_scratch.d() : nullptr,
+                                        lv.up_ns > 1 ? (int*)lv.up_count.ptr : nullptr};
     }
     if (fused) {
       htlr::launch_prologue(pp, cx.st);
@@ -1836,7 +1862,8 @@ int mv_local(MvCtx& cx, const double* u) {
     if (lv.Kron.ptr)
       htlr::launch_dense_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Kron.d(), c0, nc, cx.st);
     else
-      htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st);
+      htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st,
+                          lv.up_ns, lv.up_scratch.d(), (int*)lv.up_count.ptr);
     if (cx.prof_end()) return 1;
   }
   return 0;
@@ -1917,8 +1944,12 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   const double frac = (double)nb / (double)nleaf;
   if (!(stages & 2)) return 0;
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
-  htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
-                        nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
+  if (lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && htlr::downward8_supported(d, p, pl->sL, dp))
+    htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
+                           pl->L, R, dp, b0, nb, cx.st);
+  else
+    htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
+                          nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
   if (cx.prof_end()) return 1;
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -332,7 +332,96 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
   }
 }
 
+// Downward pass + epilogue for p = leaf side = 8 in 3-D (any kernel): one warp
+// per (leaf box, rhs), no shared memory or barriers.  For each compressed
+// level the box's 8 x 8 slices of the level factor (rows of its position in
+// the ancestor box, blocks.py:251-258) are the per-axis matrices of the same
+// mode-product chain as the separable passes (mode z, mode x on the tensor
+// pipe, mode y on DFMA), applied to H[ancestor]; then f = acc + Y + a u,
+// written back in F-order (operators.py:153-156).
+__global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict__ u, double* __restrict__ f,
+                                                         const double* __restrict__ Y, const double* __restrict__ avec,
+                                                         double aconst, int n, int L, int R, DownParams dp, int64_t b0,
+                                                         int64_t nb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wi >= nb * R) return;
+  const int64_t b = b0 + wi / R;
+  const int r = (int)(wi % R);
+  int bc[3];
+  morton_decode(b, 3, L, bc);
+  double y[kSepP][2], z[kSepP][2];
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = z[j][0] = z[j][1] = 0.0;
+  const int g = lane >> 2, q = lane & 3;
+  for (int li = 0; li < dp.nlev; ++li) {
+    const DownLevel lv = dp.lev[li];
+    const int shift = L - lv.level;
+    const int64_t anc = b >> (3 * shift);
+    const double* Qx = lv.Q + (int64_t)((bc[0] & ((1 << shift) - 1)) * kSepP) * kSepP;
+    const double* Qy = lv.Q + (int64_t)((bc[1] & ((1 << shift) - 1)) * kSepP) * kSepP;
+    const double* Qz = lv.Q + (int64_t)((bc[2] & ((1 << shift) - 1)) * kSepP) * kSepP;
+    const double* hs = lv.H + (anc * R + r) * (int64_t)lv.P + g + 64 * q;
+    // mode z: Z_t[k', a] = sum_c Qz[k', c] H[a, t, c]
+    const double az0 = Qz[g * kSepP + q], az1 = Qz[g * kSepP + 4 + q];
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      dmma(z[t][0], z[t][1], az0, __ldg(hs + 8 * t));
+      dmma(z[t][0], z[t][1], az1, __ldg(hs + 8 * t + 256));
+    }
+    // mode x then mode y into the accumulator
+    const double bx0 = Qx[g * kSepP + 2 * q], bx1 = Qx[g * kSepP + 2 * q + 1];
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      double t0 = 0.0, t1 = 0.0;
+      dmma(t0, t1, bx0, z[t][0]);
+      dmma(t0, t1, bx1, z[t][1]);
+#pragma unroll
+      for (int j = 0; j < kSepP; ++j) {
+        const double m = __ldg(Qy + j * kSepP + t);
+        y[j][0] = fma(m, t0, y[j][0]);
+        y[j][1] = fma(m, t1, y[j][1]);
+      }
+      z[t][0] = z[t][1] = 0.0;
+    }
+  }
+  // epilogue: lane holds (i = g, j, k' = 2 q + jj)
+  const double* yb = Y ? Y + (b * R + r) * (int64_t)(kSepP * kSepP * kSepP) + g + 128 * q : nullptr;
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int k = 2 * q + jj;
+      const int64_t gi =
+          (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP + j) + (int64_t)n * n * (bc[2] * kSepP + k);
+      double v = y[j][jj];
+      if (yb) v += __ldg(yb + 8 * j + 64 * jj);
+      const double a = avec ? __ldg(avec + gi) : aconst;
+      if (a != 0.0) v = fma(a, __ldg(u + gi * R + r), v);
+      f[gi * R + r] = v;
+    }
+}
+
 }  // namespace
+
+bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = std::getenv("HTLR_DOWN8");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  if (off || d != 3 || p != kSepP || sL != kSepP) return false;
+  for (int i = 0; i < dp.nlev; ++i)
+    if (dp.lev[i].K || dp.lev[i].qstride || dp.lev[i].P != kSepP * kSepP * kSepP) return false;
+  return true;
+}
+
+void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
+                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st) {
+  const int64_t warps = nb * R;
+  if (warps <= 0) return;
+  downward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0, nb);
+}
 
 // HTLR_SEP_GROUPS=1|2: consumer warp groups of the cooperative kernel
 int sep_block_groups() {
