@@ -220,7 +220,7 @@ int upward_nslab(int d, int side, int64_t nc, int R) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int ns = 1;
-  while (nc * R * ns < 2 * sms && side % (2 * ns) == 0 && side / (2 * ns) >= 2) ns *= 2;
+  while (nc * R * ns < 2 * sms && side % (2 * ns) == 0 && side / (2 * ns) >= 4) ns *= 2;
   return ns;
 }
 

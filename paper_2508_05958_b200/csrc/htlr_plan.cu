@@ -968,8 +968,8 @@ static bool sep_block_enabled() {
 // Cooperative layout of a pass: per parent cluster (8 consecutive Morton
 // targets), the union of its children's sources grouped into columns of equal
 // (x, y) box coordinates, each box with the pair code of every child (or
-// 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default: ~8 waves of CTAs, <= 34 columns) per CTA,
-// CTAs ordered by decreasing work.  Leaves the pass on per-warp items when a
+// 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default: ~16 parts
+// per SM, <= 34 columns), parts ordered by decreasing work.  Leaves the pass on per-warp items when a
 // column is longer than kSepColMax or the own range is not whole parents.
 static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>& ptr, const std::vector<int2>& ent) {
   const int L = ps.level;
@@ -1039,14 +1039,15 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     pself[P].assign(self_col, self_col + 8);
   });
   if (!ok) return 0;
-  // columns per CTA: enough CTAs for ~8 waves, at most 34 columns each
+  // columns per part: ~16 parts per SM for the persistent CTAs' round robin
+  // (parts sorted longest first), at most 34 columns each
   int per_part = 34;
   {
     int64_t total = 0;
     for (const auto& v : pcols) total += (int64_t)v.size();
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
-    per_part = (int)std::max<int64_t>(2, std::min<int64_t>(34, (total + 8 * sms - 1) / (8 * sms)));
+    per_part = (int)std::max<int64_t>(2, std::min<int64_t>(34, (total + 16 * sms - 1) / (16 * sms)));
     const char* e = std::getenv("HTLR_SEP_COLS");
     if (e && std::atoi(e) > 0) per_part = std::atoi(e);
   }

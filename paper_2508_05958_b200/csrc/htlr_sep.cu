@@ -49,10 +49,12 @@ namespace htlr {
 
 namespace {
 
+// not volatile: pure register op, so the compiler may interleave independent
+// accumulator chains
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
 // 1-D factor of the Gaussian: g(delta) = exp(-delta^2 / (2 s^2))
@@ -117,19 +119,25 @@ __device__ __forceinline__ void sep_flush(const double* __restrict__ tab, int g,
   const double* ax = tab + (kind * NO + ox) * kSepSlotSmem + 64;
   const double b0 = ax[lane], b1 = ax[32 + lane];
   const double* my = tab + (kind * NO + oy) * kSepSlotSmem + 128;
+  // mode x for every t (k-step 0 of all tiles, then k-step 1: dependent DMMAs
+  // 8 apart), then mode y
+  double tt[kSepP][2];
+#pragma unroll
+  for (int t = 0; t < kSepP; ++t) tt[t][0] = tt[t][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < kSepP; ++t) dmma(tt[t][0], tt[t][1], b0, z[t][0]);
+#pragma unroll
+  for (int t = 0; t < kSepP; ++t) dmma(tt[t][0], tt[t][1], b1, z[t][1]);
 #pragma unroll
   for (int t = 0; t < kSepP; ++t) {
-    double t0 = 0.0, t1 = 0.0;
-    dmma(t0, t1, b0, z[t][0]);
-    dmma(t0, t1, b1, z[t][1]);
     const double2* mv = reinterpret_cast<const double2*>(my + t * kSepP);
 #pragma unroll
     for (int jp = 0; jp < kSepP / 2; ++jp) {
       const double2 m = mv[jp];
-      y[2 * jp][0] = fma(m.x, t0, y[2 * jp][0]);
-      y[2 * jp][1] = fma(m.x, t1, y[2 * jp][1]);
-      y[2 * jp + 1][0] = fma(m.y, t0, y[2 * jp + 1][0]);
-      y[2 * jp + 1][1] = fma(m.y, t1, y[2 * jp + 1][1]);
+      y[2 * jp][0] = fma(m.x, tt[t][0], y[2 * jp][0]);
+      y[2 * jp][1] = fma(m.x, tt[t][1], y[2 * jp][1]);
+      y[2 * jp + 1][0] = fma(m.y, tt[t][0], y[2 * jp + 1][0]);
+      y[2 * jp + 1][1] = fma(m.y, tt[t][1], y[2 * jp + 1][1]);
     }
     z[t][0] = z[t][1] = 0.0;
   }
@@ -168,10 +176,9 @@ __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const S
       const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
       const double a0 = az[lane], a1 = az[32 + lane];
 #pragma unroll
-      for (int t = 0; t < kSepP; ++t) {
-        dmma(z[t][0], z[t][1], a0, xb[t][0]);
-        dmma(z[t][0], z[t][1], a1, xb[t][1]);
-      }
+      for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], a0, xb[t][0]);
+#pragma unroll
+      for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], a1, xb[t][1]);
     }
     const int g = cur.y >> 4;
     if (!more || (nxt.y >> 4) != g) {
@@ -222,28 +229,31 @@ __global__ void __launch_bounds__(kSepWarps * 32)
     sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane);
 }
 
-// Cooperative pass: CTA = (parent cluster, part of the source columns of its
-// 8 children), NG groups of 8 consumer warps (warp w applies the blocks of
-// child target tgt0 + w % 8; group w / 8 takes every NG-th column) and a
-// producer warp that bulk-copies every source box of a column once, as 8
-// z-planes at a 68-double pitch (so the mode-z B fragments -- lanes
-// a = lane/4, c = 4 ks + lane%4 -- hit 32 distinct banks), into a ring of
-// NS = ring_slots(NG) column slots (full / empty mbarriers).  A column has
-// fixed (o_x, o_y) for every warp, so a warp flushes its Z accumulator when
-// the block kind changes along the column and at its end (one flush for the
-// far columns, at most three where near blocks sit between admissible ones).
+// Cooperative pass, persistent: CTA i walks the parts i, i + grid, ... (a
+// part = a parent cluster and a run of the source columns of its 8 children;
+// parts sorted longest first).  NG groups of 8 consumer warps (warp w applies
+// the blocks of child target tgt0 + w % 8; group w / 8 takes every NG-th
+// column of the CTA's column sequence) and a producer warp that bulk-copies
+// every source box of a column once, as 8 z-planes at a 68-double pitch (so
+// the mode-z B fragments -- lanes a = lane/4, c = 4 ks + lane%4 -- hit 32
+// distinct banks), into a ring of NS = sep_ring_slots(NG) column slots (full /
+// empty mbarriers); the ring runs across part boundaries, so the next part's
+// columns load while the current one finishes.  A column has fixed (o_x, o_y)
+// for every warp, so a warp flushes its Z accumulator when the block kind
+// changes along the column and at its end (one flush for the far columns, at
+// most three where near blocks sit between admissible ones).  At the end of a
+// part each group adds its partial Y into C (fp64 RED).
 template <int NG>
 __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
     sep_block_kernel(const double* __restrict__ tables, int nslots, int NO, const SepBlock* __restrict__ blocks,
-                     const SepCol* __restrict__ cols, const double* __restrict__ B, int ldb, double* __restrict__ C,
-                     int ldc, int R, const double* __restrict__ corr_ptr) {
+                     int nblocks, const SepCol* __restrict__ cols, const double* __restrict__ B, int ldb,
+                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr) {
   constexpr int NS = sep_ring_slots(NG), SLOT = kSepColMax * kSepBoxSmem, NCW = 8 * NG;
   extern __shared__ __align__(16) double sm[];
   double* tab = sm;
   double* ring = tab + nslots * kSepSlotSmem;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * SLOT);
   uint64_t* empty = full + NS;
-  const SepBlock bk = blocks[blockIdx.x];
   const int r = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -256,79 +266,97 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
   for (int e = threadIdx.x; e < nslots * kSepSlotSmem; e += blockDim.x)
     tab[e] = tables[(e / kSepSlotSmem) * kSepSlot + e % kSepSlotSmem];
   __syncthreads();
-  const SepCol* cl = cols + bk.col_begin;
   if (warp == NCW) {
     // ------------------------------------------------------------ producer
-    for (int c = 0; c < bk.col_count; ++c) {
-      const int slot = c % NS;
-      if (c >= NS) mbar_wait(&empty[slot], (unsigned)(((c / NS) - 1) & 1));
-      const int n = cl[c].n;
-      if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * 512 * 8));
-      __syncwarp();
-      double* dst = ring + slot * SLOT;
-      for (int e = lane; e < n * 8; e += 32) {
-        const int k = e >> 3, pl = e & 7;
-        bulk_g2s(dst + k * kSepBoxSmem + pl * 68, B + ((int64_t)cl[c].src[k] * R + r) * ldb + pl * 64, 64 * 8,
-                 &full[slot]);
+    int gc = 0;   // column index in this CTA's sequence (ring position)
+    for (int part = blockIdx.x; part < nblocks; part += gridDim.x) {
+      const SepBlock bk = blocks[part];
+      const SepCol* cl = cols + bk.col_begin;
+      for (int c = 0; c < bk.col_count; ++c, ++gc) {
+        const int slot = gc % NS;
+        if (gc >= NS) mbar_wait(&empty[slot], (unsigned)(((gc / NS) - 1) & 1));
+        const int n = cl[c].n;
+        if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * 512 * 8));
+        __syncwarp();
+        double* dst = ring + slot * SLOT;
+        for (int e = lane; e < n * 8; e += 32) {
+          const int k = e >> 3, pl = e & 7;
+          bulk_g2s(dst + k * kSepBoxSmem + pl * 68, B + ((int64_t)cl[c].src[k] * R + r) * ldb + pl * 64, 64 * 8,
+                   &full[slot]);
+        }
       }
     }
     return;
   }
   // ------------------------------------------------------------- consumers
   const int tw = warp & 7, grp = warp >> 3;
+  const int xoff = (lane >> 2) + 68 * (lane & 3);
+  const int yoff = (lane >> 2) + 128 * (lane & 3);
   double y[kSepP][2], z[kSepP][2];
 #pragma unroll
   for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = z[j][0] = z[j][1] = 0.0;
-  const int xoff = (lane >> 2) + 68 * (lane & 3);
-  for (int c = grp; c < bk.col_count; c += NG) {
-    const int slot = c % NS;
-    const int n = cl[c].n;
-    // the column's pair codes of this warp's target, one per lane
-    const int mycode = lane < n ? (int)cl[c].code[lane][tw] : 0xFFFF;
-    mbar_wait(&full[slot], (unsigned)((c / NS) & 1));
-    const double* xs = ring + slot * SLOT + xoff;
-    int g = -1;
-    for (int k = 0; k < n; ++k) {
-      const int code = __shfl_sync(0xffffffffu, mycode, k);
-      if (code == 0xFFFF) continue;
-      if ((code >> 4) != g) {   // kind change inside the column (o_x, o_y fixed)
-        if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
-        g = code >> 4;
-      }
-      double xv[kSepP][2];
+  int gc0 = 0;   // first ring position of the current part
+  for (int part = blockIdx.x; part < nblocks; part += gridDim.x) {
+    const SepBlock bk = blocks[part];
+    const SepCol* cl = cols + bk.col_begin;
+    // this group's first column of the part
+    int c = ((grp - gc0) % NG + NG) % NG;
+    const bool mine = c < bk.col_count;
+    for (; c < bk.col_count; c += NG) {
+      const int gc = gc0 + c;
+      const int slot = gc % NS;
+      const int n = cl[c].n;
+      // the column's pair codes of this warp's target, one per lane
+      const int mycode = lane < n ? (int)cl[c].code[lane][tw] : 0xFFFF;
+      mbar_wait(&full[slot], (unsigned)((gc / NS) & 1));
+      const double* xs = ring + slot * SLOT + xoff;
+      int g = -1;
+      for (int k = 0; k < n; ++k) {
+        const int code = __shfl_sync(0xffffffffu, mycode, k);
+        if (code == 0xFFFF) continue;
+        if ((code >> 4) != g) {   // kind change inside the column (o_x, o_y fixed)
+          if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
+          g = code >> 4;
+        }
+        double xv[kSepP][2];
 #pragma unroll
-      for (int t = 0; t < kSepP; ++t) {
-        xv[t][0] = xs[k * kSepBoxSmem + 8 * t];
-        xv[t][1] = xs[k * kSepBoxSmem + 8 * t + 272];
-      }
-      const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
-      const double a0 = az[lane], a1 = az[32 + lane];
+        for (int t = 0; t < kSepP; ++t) {
+          xv[t][0] = xs[k * kSepBoxSmem + 8 * t];
+          xv[t][1] = xs[k * kSepBoxSmem + 8 * t + 272];
+        }
+        const double* az = tab + ((code >> 12) * NO + (code & 15)) * kSepSlotSmem;
+        const double a0 = az[lane], a1 = az[32 + lane];
 #pragma unroll
-      for (int t = 0; t < kSepP; ++t) {
-        dmma(z[t][0], z[t][1], a0, xv[t][0]);
-        dmma(z[t][0], z[t][1], a1, xv[t][1]);
+        for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], a0, xv[t][0]);
+#pragma unroll
+        for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], a1, xv[t][1]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
+    }
+    // the group that owns the part's column 0 adds the self-block correction
+    const int tgt = bk.tgt0 + tw;
+    const bool corr = (gc0 % NG) == grp && ((bk.corr_mask >> tw) & 1);
+    if (corr) {
+      const double cv = corr_ptr[0];
+      const double* s = B + ((int64_t)tgt * R + r) * ldb + yoff;
+#pragma unroll
+      for (int j = 0; j < kSepP; ++j) {
+        y[j][0] = fma(cv, __ldg(s + 8 * j), y[j][0]);
+        y[j][1] = fma(cv, __ldg(s + 8 * j + 64), y[j][1]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (g >= 0) sep_flush(tab, g, NO, lane, z, y);
-  }
-  const int tgt = bk.tgt0 + tw;
-  const int yoff = (lane >> 2) + 128 * (lane & 3);
-  if (grp == 0 && ((bk.corr_mask >> tw) & 1)) {
-    const double corr = corr_ptr[0];
-    const double* s = B + ((int64_t)tgt * R + r) * ldb + yoff;
+    if (mine || corr) {
+      double* o = C + ((int64_t)tgt * R + r) * ldc + yoff;
 #pragma unroll
-    for (int j = 0; j < kSepP; ++j) {
-      y[j][0] = fma(corr, __ldg(s + 8 * j), y[j][0]);
-      y[j][1] = fma(corr, __ldg(s + 8 * j + 64), y[j][1]);
+      for (int j = 0; j < kSepP; ++j) {
+        atomicAdd(o + 8 * j, y[j][0]);
+        atomicAdd(o + 8 * j + 64, y[j][1]);
+        y[j][0] = y[j][1] = 0.0;
+      }
     }
-  }
-  double* o = C + ((int64_t)tgt * R + r) * ldc + yoff;
-#pragma unroll
-  for (int j = 0; j < kSepP; ++j) {
-    atomicAdd(o + 8 * j, y[j][0]);
-    atomicAdd(o + 8 * j + 64, y[j][1]);
+    gc0 += bk.col_count;
   }
 }
 
@@ -365,10 +393,9 @@ __global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict
     // mode z: Z_t[k', a] = sum_c Qz[k', c] H[a, t, c]
     const double az0 = Qz[g * kSepP + q], az1 = Qz[g * kSepP + 4 + q];
 #pragma unroll
-    for (int t = 0; t < kSepP; ++t) {
-      dmma(z[t][0], z[t][1], az0, __ldg(hs + 8 * t));
-      dmma(z[t][0], z[t][1], az1, __ldg(hs + 8 * t + 256));
-    }
+    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az0, __ldg(hs + 8 * t));
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az1, __ldg(hs + 8 * t + 256));
     // mode x then mode y into the accumulator
     const double bx0 = Qx[g * kSepP + 2 * q], bx1 = Qx[g * kSepP + 2 * q + 1];
 #pragma unroll
@@ -448,8 +475,12 @@ static void launch_sep_block_t(const double* tables, int nslots, int NO, const S
     cudaFuncSetAttribute(sep_block_kernel<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  sep_block_kernel<NG><<<dim3(nblocks, R), (8 * NG + 1) * 32, sep_block_smem_bytes(nslots), st>>>(
-      tables, nslots, NO, blocks, cols, B, ldb, C, ldc, R, corr);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = nblocks < sms ? nblocks : sms;   // persistent: one CTA per SM
+  sep_block_kernel<NG><<<dim3(grid, R), (8 * NG + 1) * 32, sep_block_smem_bytes(nslots), st>>>(
+      tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr);
 }
 
 void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
