@@ -308,8 +308,8 @@ PHASE_KERNELS = {
     "gemm_level": "gemm_persistent_kernel / gemm_thin_kernel (coupling cores, fp64 DMMA)",
     "regen_level": "regen_sym_kernel (cores regenerated + contracted, fp64 CUDA cores)",
     "regen_near": "regen_sym_kernel (near blocks regenerated, fp64 CUDA cores)",
-    "sep_level": "sep_apply_kernel (separable coupling cores: per-axis mode products, fp64 DMMA)",
-    "sep_leaf": "sep_apply_kernel (separable near + leaf-level cores: per-axis mode products, fp64 DMMA)",
+    "sep_level": "sep_block_kernel (separable coupling cores: per-axis mode products, fp64 DMMA)",
+    "sep_leaf": "sep_block_kernel (separable near + leaf-level cores: per-axis mode products, fp64 DMMA)",
     "upward": "upward_kernel", "downward": "downward_kernel", "permute": "permute_in_kernel",
 }
 
@@ -471,8 +471,12 @@ def run_b200(args):
 
     # e2e through the public API from pinned host memory
     u_pin = torch.from_numpy(np.ascontiguousarray(u_host)).pin_memory()
-    e2e_apply = apply
-    for _ in range(2):
+    f_pin = torch.empty(u_pin.shape, dtype=torch.float64).pin_memory()
+    if world > 1:
+        e2e_apply = apply
+    else:
+        e2e_apply = (lambda x: H.matmat(op, x, out=f_pin)) if R > 1 else (lambda x: H.matvec(op, x, out=f_pin))
+    for _ in range(max(3, args.warmup)):
         e2e_apply(u_pin)
     torch.cuda.synchronize()
     if dist is not None:
@@ -509,6 +513,7 @@ def run_b200(args):
                    "nrhs": R, "l2": "flushed (512 MiB write) before every step, outside the timed bracket; "
                                    f"operator tables {rep.device_scalars * 8 / 1e9:.2f} GB "
                                    f"({'>' if rep.device_scalars * 8 > 126e6 else '<'} the 126 MB L2)",
+                   "formulation": base_op.formulation(),
                    "construct_s": construct_s, "parallelism": f"target subtrees x{world}" if world > 1 else "1 GPU",
                    "reference_storage_GB": rep.total_scalars * 8 / 1e9,
                    "device_storage_GB": rep.device_scalars * 8 / 1e9},

@@ -276,7 +276,7 @@ def _all_points(grid: UniformGrid) -> np.ndarray:
     return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
 
 
-def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int]):
+def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int], out=None):
     import torch
     is_torch = isinstance(u, torch.Tensor)
     if is_torch:
@@ -303,29 +303,41 @@ def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int]):
         stream = torch.cuda.current_stream(op.device).cuda_stream
         _lib.check(_lib.lib().htlr_matvec(op._plan, ctypes.c_void_p(ud.data_ptr()),
                                           ctypes.c_void_p(fd.data_ptr()), R, ctypes.c_void_p(stream)))
-    out = fd.reshape(-1) if nrhs_expected == 1 else fd
+    res_d = fd.reshape(-1) if nrhs_expected == 1 else fd
+    if out is not None:
+        # caller-provided result buffer (host or device), e.g. a reused pinned
+        # tensor: one async copy on the same stream, no allocation
+        if not isinstance(out, torch.Tensor) or tuple(out.shape) != tuple(res_d.shape) or \
+                out.dtype != torch.float64:
+            raise ValueError(f"out must be a float64 tensor of shape {tuple(res_d.shape)}")
+        out.copy_(res_d, non_blocking=True)
+        if out.device.type != "cuda":
+            torch.cuda.current_stream(op.device).synchronize()
+        return out
     if host:
         if is_torch and x.is_pinned():
             # pinned in -> pinned out (torch's caching host allocator), one
             # async D2H copy on the same stream
-            res = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-            res.copy_(out, non_blocking=True)
+            res = torch.empty(res_d.shape, dtype=res_d.dtype, pin_memory=True)
+            res.copy_(res_d, non_blocking=True)
             torch.cuda.current_stream(op.device).synchronize()
             return res
-        res = out.cpu()
+        res = res_d.cpu()
         return res.numpy() if not is_torch else res
-    return out
+    return res_d
 
 
-def matvec(op: HTLRMatrix, u):
+def matvec(op: HTLRMatrix, u, out=None):
     """f = A u (operators.py:159-161).  numpy in -> numpy out; CUDA tensor in
-    -> CUDA tensor out (no host copies)."""
-    return _apply(op, u, 1)
+    -> CUDA tensor out (no host copies).  `out`: optional float64 torch tensor
+    (host, e.g. pinned, or device) that receives f and is returned."""
+    return _apply(op, u, 1, out)
 
 
-def matmat(op: HTLRMatrix, U):
-    """F = A U for a block of right-hand sides U of shape (N, R)."""
-    return _apply(op, U, None)
+def matmat(op: HTLRMatrix, U, out=None):
+    """F = A U for a block of right-hand sides U of shape (N, R); `out` as in
+    matvec."""
+    return _apply(op, U, None, out)
 
 
 def weak_storage_bound(d: int, rank: int, num_points: int) -> float:

@@ -158,3 +158,20 @@ def test_non_separable_configs_keep_dense_cores():
     cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
                         coeff=H.CoefficientFn.constant(0.0))
     assert H.construct(cfg, H.UniformGrid(3, 32)).formulation() == "dense"
+
+
+def test_out_buffer_host_and_device():
+    """matvec / matmat write into a caller's float64 tensor (pinned host or
+    device) and return it; a wrong shape raises ValueError."""
+    import torch
+    op = make(32, 0.15, 1.3, 0.7)
+    u = np.random.default_rng(3).standard_normal(32 ** 3)
+    ref = H.matvec(op, u)
+    pin = torch.empty(32 ** 3, dtype=torch.float64).pin_memory()
+    got = H.matvec(op, torch.from_numpy(u).pin_memory(), out=pin)
+    assert got is pin and np.array_equal(pin.numpy(), ref)
+    dev = torch.empty((32 ** 3, 1), dtype=torch.float64, device="cuda")
+    assert H.matmat(op, torch.from_numpy(u).reshape(-1, 1).cuda(), out=dev) is dev
+    assert np.array_equal(dev.cpu().numpy()[:, 0], ref)
+    with pytest.raises(ValueError):
+        H.matvec(op, u, out=torch.empty(7, dtype=torch.float64))

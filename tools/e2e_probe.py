@@ -16,11 +16,13 @@ up = torch.from_numpy(u).pin_memory()
 ud = up.cuda()
 
 
-def timeit(label, fn, reps=5):
+def timeit(label, fn, reps=10, pre=None):
     fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
+        if pre is not None:
+            pre()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         e0.record()
@@ -37,3 +39,14 @@ out = torch.empty_like(ud)
 timeit("d2h pinned only    ", lambda: torch.empty(out.shape, dtype=out.dtype, pin_memory=True).copy_(out, non_blocking=True))
 timeit("pinned in/out      ", lambda: H.matvec(op, up))
 timeit("numpy in/out       ", lambda: H.matvec(op, u))
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+keep = [None]
+
+
+def kept():
+    keep[0] = H.matvec(op, up)
+
+
+timeit("pinned, result kept ", kept)
+timeit("pinned, L2 flushed  ", lambda: H.matvec(op, up), pre=flush.zero_)
+timeit("kept + flushed      ", kept, pre=flush.zero_)

@@ -2,8 +2,10 @@
 # changes from experiment to experiment).  Example:
 #   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
 export PYTHONPATH=$PWD
-python tools/phases.py cfg4 > gpurun_out/ph.log 2>&1
-HTLR_SEP_GROUPS=1 python tools/phases.py cfg4 >> gpurun_out/ph.log 2>&1
-python tools/phases.py cfg2 >> gpurun_out/ph.log 2>&1
-python -m pytest tests/test_gpu_separable.py -x -q > gpurun_out/t.log 2>&1
-cat gpurun_out/ph.log; tail -n 3 gpurun_out/t.log
+python tools/e2e_probe.py cfg4 > gpurun_out/e2e.log 2>&1
+python bench.py --workload cfg4 --steps 10 --warmup 3 > gpurun_out/b_cfg4.json 2> gpurun_out/b_cfg4.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg4.csv \
+  python tools/prof_cmd.py cfg4 1 > gpurun_out/ncu_l.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sep_block -s 5 -c 1 -f -o gpurun_out/r01_cfg4_sep_leaf \
+  python tools/prof_cmd.py cfg4 1 > gpurun_out/ncu_f.log 2>&1
+cat gpurun_out/e2e.log
