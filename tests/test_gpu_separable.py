@@ -162,16 +162,18 @@ def test_non_separable_configs_keep_dense_cores():
 
 def test_out_buffer_host_and_device():
     """matvec / matmat write into a caller's float64 tensor (pinned host or
-    device) and return it; a wrong shape raises ValueError."""
+    device) and return it; a wrong shape raises ValueError.  (Accumulation
+    order across CTAs is not fixed -- fp64 RED -- so repeated matvecs agree to
+    rounding, not bitwise.)"""
     import torch
     op = make(32, 0.15, 1.3, 0.7)
     u = np.random.default_rng(3).standard_normal(32 ** 3)
     ref = H.matvec(op, u)
     pin = torch.empty(32 ** 3, dtype=torch.float64).pin_memory()
     got = H.matvec(op, torch.from_numpy(u).pin_memory(), out=pin)
-    assert got is pin and np.array_equal(pin.numpy(), ref)
+    assert got is pin and rel(pin.numpy(), ref) <= 1e-14
     dev = torch.empty((32 ** 3, 1), dtype=torch.float64, device="cuda")
     assert H.matmat(op, torch.from_numpy(u).reshape(-1, 1).cuda(), out=dev) is dev
-    assert np.array_equal(dev.cpu().numpy()[:, 0], ref)
+    assert rel(dev.cpu().numpy()[:, 0], ref) <= 1e-14
     with pytest.raises(ValueError):
         H.matvec(op, u, out=torch.empty(7, dtype=torch.float64))
