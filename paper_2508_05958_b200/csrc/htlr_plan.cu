@@ -969,7 +969,7 @@ static bool sep_block_enabled() {
 // targets), the union of its children's sources grouped into columns of equal
 // (x, y) box coordinates, each box with the pair code of every child (or
 // 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default: ~16 parts
-// per SM, <= 34 columns), parts ordered by decreasing work.  Leaves the pass on per-warp items when a
+// per SM, <= 12 columns), parts ordered by decreasing work.  Leaves the pass on per-warp items when a
 // column is longer than kSepColMax or the own range is not whole parents.
 static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>& ptr, const std::vector<int2>& ent) {
   const int L = ps.level;
@@ -980,40 +980,59 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
   std::vector<std::vector<int>> pself((size_t)npar);
   std::atomic<bool> ok{true};
   parallel_for((size_t)npar, [&](size_t P) {
-    // (source coords, source id) -> per-child codes
+    // (source coords, source id) -> per-child codes; sources indexed through a
+    // dense array over their bounding box
     struct Src {
       int x, y, z, id;
       unsigned short code[8];
     };
+    int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {-1, -1, -1};
+    for (int64_t k = ptr[(int64_t)P * 8]; k < ptr[(int64_t)P * 8 + 8]; ++k) {
+      int c[3];
+      htlr::morton_decode(ent[k].x, 3, L, c);
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], c[a]);
+        hi[a] = std::max(hi[a], c[a]);
+      }
+    }
     std::vector<Src> v;
-    std::unordered_map<int, int> at;
+    if (hi[0] < 0) {
+      pself[P].assign(8, -1);
+      return;
+    }
+    const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+    std::vector<int> at((size_t)ex * ey * ez, -1);
     for (int w = 0; w < 8; ++w) {
       const int64_t t = (int64_t)P * 8 + w;
       for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k) {
         const int src = ent[k].x;
-        auto it = at.find(src);
-        int idx;
-        if (it == at.end()) {
-          idx = (int)v.size();
-          at.emplace(src, idx);
-          Src s{};
-          int c[3];
-          htlr::morton_decode(src, 3, L, c);
-          s.x = c[0];
-          s.y = c[1];
-          s.z = c[2];
-          s.id = src;
-          for (auto& q : s.code) q = 0xFFFF;
-          v.push_back(s);
-        } else {
-          idx = it->second;
+        int c[3];
+        htlr::morton_decode(src, 3, L, c);
+        int& slot = at[((size_t)(c[2] - lo[2]) * ey + (c[1] - lo[1])) * ex + (c[0] - lo[0])];
+        if (slot < 0) {
+          slot = (int)v.size();
+          Src sr{};
+          sr.x = c[0];
+          sr.y = c[1];
+          sr.z = c[2];
+          sr.id = src;
+          for (auto& q : sr.code) q = 0xFFFF;
+          v.push_back(sr);
         }
-        v[idx].code[w] = (unsigned short)ent[k].y;
+        v[slot].code[w] = (unsigned short)ent[k].y;
       }
     }
-    std::sort(v.begin(), v.end(), [](const Src& a, const Src& b) {
-      return a.x != b.x ? a.x < b.x : a.y != b.y ? a.y < b.y : a.z < b.z;
-    });
+    {   // (x, y, z) order = a scan of the dense index, x slowest
+      std::vector<Src> sorted;
+      sorted.reserve(v.size());
+      for (int x = 0; x < ex; ++x)
+        for (int y = 0; y < ey; ++y)
+          for (int z = 0; z < ez; ++z) {
+            const int q = at[((size_t)z * ey + y) * ex + x];
+            if (q >= 0) sorted.push_back(v[q]);
+          }
+      v.swap(sorted);
+    }
     auto& cols = pcols[P];
     int self_col[8];
     for (auto& q : self_col) q = -1;
@@ -1040,14 +1059,14 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
   });
   if (!ok) return 0;
   // columns per part: ~16 parts per SM for the persistent CTAs' round robin
-  // (parts sorted longest first), at most 34 columns each
-  int per_part = 34;
+  // (parts sorted longest first), at most 12 columns each
+  int per_part = 12;
   {
     int64_t total = 0;
     for (const auto& v : pcols) total += (int64_t)v.size();
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
-    per_part = (int)std::max<int64_t>(2, std::min<int64_t>(34, (total + 16 * sms - 1) / (16 * sms)));
+    per_part = (int)std::max<int64_t>(2, std::min<int64_t>(12, (total + 16 * sms - 1) / (16 * sms)));
     const char* e = std::getenv("HTLR_SEP_COLS");
     if (e && std::atoi(e) > 0) per_part = std::atoi(e);
   }
@@ -1157,11 +1176,25 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
     std::sort(ent.begin() + ptr[t], ent.begin() + ptr[t + 1],
               [](const int2& a, const int2& b) { return a.y != b.y ? a.y < b.y : a.x < b.x; });
   });
+  // groups = runs of equal (kind, o_x, o_y) per target (algorithmic flop count)
+  std::vector<int64_t> gcount((size_t)nt, 0);
+  parallel_for((size_t)nt, [&](size_t t) {
+    int64_t c = 0;
+    for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k)
+      if (k == ptr[t] || (ent[k].y >> 4) != (ent[k - 1].y >> 4)) ++c;
+    gcount[t] = c;
+  });
+  int64_t groups = 0;
+  for (int64_t c : gcount) groups += c;
+  ps.sep_NO = NO;
+  ps.sep_groups = groups;
+  ps.sep_nblocks = 0;
+  ps.sep_nitems = 0;
+  if (sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
   const int selfcode = (1 << 12) | (OR << 8) | (OR << 4) | OR;
   const int chunk = sep_chunk();
   std::vector<htlr::SepItem> items;
-  int64_t groups = 0;
-  for (int64_t t = 0; t < nt; ++t) {
+  for (int64_t t = 0; t < nt && ps.sep_nblocks == 0; ++t) {
     int64_t b = ptr[t];
     const int64_t e = ptr[t + 1];
     while (b < e) {
@@ -1174,19 +1207,17 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
         if (c > b && g - b > chunk) break;
         for (int64_t k = c; k < g; ++k)
           if (ent[k].y == selfcode && ent[k].x == (int)(t0 + t)) flags |= 1;
-        ++groups;
         c = g;
       }
       items.push_back(htlr::SepItem{(int)(t0 + t), (int)b, (int)(c - b), flags});
       b = c;
     }
   }
-  ps.sep_NO = NO;
-  ps.sep_groups = groups;
-  ps.sep_nitems = (int)items.size();
-  if (upload_sep(ps, ent, items)) return 1;
-  ps.sep_nblocks = 0;
-  if (sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
+  // per-warp items only when the cooperative layout does not apply
+  if (ps.sep_nblocks == 0) {
+    ps.sep_nitems = (int)items.size();
+    if (upload_sep(ps, ent, items)) return 1;
+  }
   // factor tables: kind 0 (admissible, level factor folded) and kind 1 (near)
   const int nslots = 2 * NO;
   if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;
@@ -1297,12 +1328,19 @@ int htlr_construct(htlr_plan* pl, void* stream) {
   }
   CUDA_TRY(cudaSetDevice(pl->device));
   cudaStream_t st = (cudaStream_t)stream;
-  for (auto& ps : pl->passes) {
-    if (ps.pairs.alloc(std::max<size_t>(1, ps.pairs_host.size()) * sizeof(int2))) return 1;
-    if (!ps.pairs_host.empty())
-      CUDA_TRY(cudaMemcpy(ps.pairs.ptr, ps.pairs_host.data(), ps.pairs_host.size() * sizeof(int2),
-                          cudaMemcpyHostToDevice));
-  }
+  PhaseTimer tm(st);
+  // the dense GEMM passes' (target, source) lists (not used by the separable
+  // formulation, uploaded if it does not apply)
+  auto upload_pairs = [&]() -> int {
+    for (auto& ps : pl->passes) {
+      if (ps.pairs.alloc(std::max<size_t>(1, ps.pairs_host.size()) * sizeof(int2))) return 1;
+      if (!ps.pairs_host.empty())
+        CUDA_TRY(cudaMemcpy(ps.pairs.ptr, ps.pairs_host.data(), ps.pairs_host.size() * sizeof(int2),
+                            cudaMemcpyHostToDevice));
+    }
+    return 0;
+  };
+  if (!sep_wanted(pl) && upload_pairs()) return 1;
   if (pl->mapped) return construct_mapped(pl, st);
   const int d = pl->d, p = pl->p;
   // diagonal cell average (operators.py:95-99)
@@ -1345,6 +1383,7 @@ int htlr_construct(htlr_plan* pl, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(jobsbuf.ptr, fj.data(), fj.size() * sizeof(htlr::FactorJob), cudaMemcpyHostToDevice, st));
     htlr::launch_factor_qr((int)fj.size(), (const htlr::FactorJob*)jobsbuf.ptr, pl->h, p, st);
   }
+  tm.mark("construct: diagonal + level factors");
   // H-matrix baseline: dense Kronecker factors of the levels with a factor
   pl->device_scalars = 0;
   if (pl->lowrank) {
@@ -1372,6 +1411,7 @@ int htlr_construct(htlr_plan* pl, void* stream) {
     if (all) {
       CUDA_TRY(cudaStreamSynchronize(st));
       CUDA_TRY(cudaGetLastError());
+      tm.mark("construct: separable lists + factor tables");
       scratch.release();
       jobsbuf.release();
       pl->sep = true;
@@ -1386,6 +1426,7 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       ps.sep_cols.release();
     }
     pl->device_scalars = 0;
+    if (upload_pairs()) return 1;
   }
   // tables
   for (auto& ps : pl->passes) {
@@ -1888,7 +1929,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     if (pl->sep) {
-      if (ps.sep_nitems == 0) continue;
+      if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;
       const double* B = ps.from_ub ? cx.ub : cx.W[i];
       double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
       // algorithmic work: 8^4 MAC per pair (mode z) + 2 * 8^4 per group
