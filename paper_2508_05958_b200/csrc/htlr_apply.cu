@@ -19,12 +19,23 @@
 
 namespace htlr {
 
+// Physical -> logical index of a box vector stored with a z-plane pitch
+// (zpitch == 0: natural layout).  Pitched layout (separable passes): plane z
+// of `plane` doubles starts at z * zpitch, so one bulk copy of the box lands
+// in shared memory with bank-conflict-free mode-z fragments.  Returns a value
+// >= nplanes * plane for padding positions.
+__device__ __forceinline__ int unpitch(int kp, int plane, int nplanes, int zpitch) {
+  if (!zpitch) return kp;
+  const int pl = kp / zpitch, off = kp - pl * zpitch;
+  return (off < plane && pl < nplanes) ? pl * plane + off : nplanes * plane;
+}
+
 // ---------------------------------------------------------------------------
 // permute: ub[(b*R + r)*K_pad + k] = u[(global point of (b, k))*R + r]
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void permute_body(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
                                              int s, int bits, int R, int K_pad, int64_t b0, int64_t nb,
-                                             const ZeroList& zero, int64_t blk, int64_t nblk) {
+                                             const ZeroList& zero, int64_t blk, int64_t nblk, int zpitch = 0) {
   if (blk >= nb) {
     // the extra CTAs zero the accumulators of the coming GEMM passes
     const int64_t stride = (nblk - nb) * blockDim.x;
@@ -40,7 +51,8 @@ __device__ __forceinline__ void permute_body(const double* __restrict__ u, doubl
   morton_decode(b, d, bits, bc);
   const int P = (d == 2) ? s * s : s * s * s;
   for (int idx = threadIdx.x; idx < R * K_pad; idx += blockDim.x) {
-    int r = idx % R, k = idx / R;
+    int r = idx % R, kp = idx / R;
+    const int k = (d == 3) ? unpitch(kp, s * s, s, zpitch) : kp;
     double v = 0.0;
     if (k < P) {
       int x = k % s, y = (k / s) % s, z = k / (s * s);
@@ -48,17 +60,18 @@ __device__ __forceinline__ void permute_body(const double* __restrict__ u, doubl
       if (d == 3) g += (int64_t)n * n * (bc[2] * s + z);
       v = u[g * R + r];
     }
-    ub[((int64_t)b * R + r) * K_pad + k] = v;
+    ub[((int64_t)b * R + r) * K_pad + kp] = v;
   }
 }
 
 __global__ void permute_in_kernel(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
-                                  int s, int bits, int R, int K_pad, int64_t b0, int64_t nb, ZeroList zero) {
-  permute_body(u, ub, d, n, s, bits, R, K_pad, b0, nb, zero, blockIdx.x, gridDim.x);
+                                  int s, int bits, int R, int K_pad, int64_t b0, int64_t nb, ZeroList zero,
+                                  int zpitch) {
+  permute_body(u, ub, d, n, s, bits, R, K_pad, b0, nb, zero, blockIdx.x, gridDim.x, zpitch);
 }
 
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
-                       int64_t nb, cudaStream_t st, const ZeroList* zero) {
+                       int64_t nb, cudaStream_t st, const ZeroList* zero, int zpitch) {
   int bits = 0;
   while ((s << bits) < n) ++bits;
   ZeroList z;
@@ -69,7 +82,7 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
   }
   const int64_t zblocks = std::min<int64_t>((words + 2047) / 2048, 4 * 148);
   if (nb > 0 || zblocks > 0)
-    permute_in_kernel<<<(unsigned)(nb + zblocks), 256, 0, st>>>(u, ub, d, n, s, bits, R, K_pad, b0, nb, z);
+    permute_in_kernel<<<(unsigned)(nb + zblocks), 256, 0, st>>>(u, ub, d, n, s, bits, R, K_pad, b0, nb, z, zpitch);
 }
 
 // ---------------------------------------------------------------------------
@@ -82,7 +95,7 @@ void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void upward_body(const double* __restrict__ u, double* __restrict__ W, int d, int n,
                                             int s, int p, int bits, int R, int K_pad, const double* __restrict__ Q,
-                                            int64_t qstride, int64_t c, int r, double* sm) {
+                                            int64_t qstride, int64_t c, int r, double* sm, int zpitch = 0) {
   double* sQ = sm;                          // d x s*p (factor of each dimension)
   double* T1 = sQ + d * s * p;              // p*s*s (3-D) / p*s (2-D)
   double* T2 = T1 + p * s * (d == 3 ? s : 1);   // p*p*s (3-D)
@@ -127,13 +140,14 @@ __device__ __forceinline__ void upward_body(const double* __restrict__ u, double
     T2[i] = v;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) {
+  for (int ip = threadIdx.x; ip < K_pad; ip += blockDim.x) {
+    const int i = unpitch(ip, p * p, p, zpitch);
     double v = 0.0;
     if (i < P) {
       const int a12 = i % (p * p), a3 = i / (p * p);
       for (int z = 0; z < s; ++z) v += sQz[z * p + a3] * T2[a12 + p * p * z];
     }
-    dst[i] = v;
+    dst[ip] = v;
   }
 }
 
@@ -146,7 +160,7 @@ __device__ __forceinline__ void upward_split_body(const double* __restrict__ u, 
                                                   int p, int bits, int R, int K_pad, const double* __restrict__ Q,
                                                   int64_t qstride, int64_t c, int64_t c0, int r, int slab, int nslab,
                                                   double* __restrict__ scratch, int* __restrict__ counters,
-                                                  double* sm) {
+                                                  double* sm, int zpitch = 0) {
   const int zs = s / nslab, z0 = slab * zs;
   double* sQ = sm;                 // 3 x s*p
   double* T1 = sQ + 3 * s * p;     // p*s*zs
@@ -195,11 +209,12 @@ __device__ __forceinline__ void upward_split_body(const double* __restrict__ u, 
   __threadfence();
   const double* p0 = scratch + cr * nslab * P;
   double* dst = W + ((int64_t)c * R + r) * K_pad;
-  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) {
+  for (int ip = threadIdx.x; ip < K_pad; ip += blockDim.x) {
+    const int i = unpitch(ip, p * p, p, zpitch);
     double v = 0.0;
     if (i < P)
       for (int q = 0; q < nslab; ++q) v += __ldcg(p0 + q * P + i);
-    dst[i] = v;
+    dst[ip] = v;
   }
   if (threadIdx.x == 0) counters[cr] = 0;
 }
@@ -226,17 +241,18 @@ int upward_nslab(int d, int side, int64_t nc, int R) {
 
 __global__ void upward_split_kernel(const double* __restrict__ u, double* __restrict__ W, int n, int s, int p,
                                     int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
-                                    int64_t c0, int nslab, double* __restrict__ scratch, int* __restrict__ counters) {
+                                    int64_t c0, int nslab, double* __restrict__ scratch, int* __restrict__ counters,
+                                    int zpitch) {
   extern __shared__ double sm[];
   upward_split_body(u, W, n, s, p, bits, R, K_pad, Q, qstride, c0 + blockIdx.x / nslab, c0, blockIdx.y,
-                    (int)(blockIdx.x % nslab), nslab, scratch, counters, sm);
+                    (int)(blockIdx.x % nslab), nslab, scratch, counters, sm, zpitch);
 }
 
 __global__ void upward_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
                               int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
-                              int64_t c0) {
+                              int64_t c0, int zpitch) {
   extern __shared__ double sm[];
-  upward_body(u, W, d, n, s, p, bits, R, K_pad, Q, qstride, c0 + blockIdx.x, blockIdx.y, sm);
+  upward_body(u, W, d, n, s, p, bits, R, K_pad, Q, qstride, c0 + blockIdx.x, blockIdx.y, sm, zpitch);
 }
 
 // ---------------------------------------------------------------------------
@@ -249,7 +265,7 @@ __global__ void prologue_kernel(PrologueParams pp) {
   const int64_t b = blockIdx.x;
   if (b < pp.nb_perm + pp.nb_zero) {
     permute_body(pp.u, pp.ub, pp.d, pp.n, pp.sL, pp.bits_L, pp.R, pp.K_pad_leaf, pp.b0, pp.nb_perm, pp.zero, b,
-                 pp.nb_perm + pp.nb_zero);
+                 pp.nb_perm + pp.nb_zero, pp.zpitch_leaf);
     return;
   }
   int64_t rest = b - pp.nb_perm - pp.nb_zero;
@@ -262,11 +278,11 @@ __global__ void prologue_kernel(PrologueParams pp) {
         const int64_t cr = rest / ns;
         upward_split_body(pp.u, lv.W, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,
                           lv.c0 + cr / pp.R, lv.c0, (int)(cr % pp.R), (int)(rest % ns), ns, lv.scratch, lv.counters,
-                          sm);
+                          sm, lv.zpitch);
         return;
       }
       upward_body(pp.u, lv.W, pp.d, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,
-                  lv.c0 + rest / pp.R, (int)(rest % pp.R), sm);
+                  lv.c0 + rest / pp.R, (int)(rest % pp.R), sm, lv.zpitch);
       return;
     }
     rest -= cnt;
@@ -277,7 +293,7 @@ __global__ void prologue_kernel(PrologueParams pp) {
 // per z-slab, the mode-3 product accumulated slab by slab
 __global__ void upward_slab_kernel(const double* __restrict__ u, double* __restrict__ W, int d, int n, int s,
                               int p, int bits, int R, int K_pad, const double* __restrict__ Q, int64_t qstride,
-                              int64_t c0) {
+                              int64_t c0, int zpitch) {
   extern __shared__ double sm[];
   double* sQ = sm;             // d x s*p (factor of each dimension)
   double* T1 = sQ + d * s * p; // p*s
@@ -333,7 +349,10 @@ __global__ void upward_slab_kernel(const double* __restrict__ u, double* __restr
     }
   }
   double* dst = W + ((int64_t)c * R + r) * K_pad;
-  for (int i = threadIdx.x; i < K_pad; i += blockDim.x) dst[i] = i < P ? acc[i] : 0.0;
+  for (int ip = threadIdx.x; ip < K_pad; ip += blockDim.x) {
+    const int i = d == 3 ? unpitch(ip, p * p, p, zpitch) : ip;
+    dst[ip] = i < P ? acc[i] : 0.0;
+  }
 }
 
 size_t upward_smem_words(int d, int side, int p) {
@@ -364,7 +383,7 @@ void launch_prologue(const PrologueParams& pp_in, cudaStream_t st) {
 
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st,
-                   int nslab, double* scratch, int* counters) {
+                   int nslab, double* scratch, int* counters, int zpitch) {
   const size_t smem = sizeof(double) * upward_smem_words(d, side, p);
   if (nc <= 0) return;
   if (nslab > 1 && d == 3) {
@@ -372,7 +391,8 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
     if (sm2 > 48 * 1024)
       cudaFuncSetAttribute(upward_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     upward_split_kernel<<<dim3((unsigned)(nc * nslab), R), 256, sm2, st>>>(u, W, n, side, p, level, R, K_pad, Q,
-                                                                          qstride, c0, nslab, scratch, counters);
+                                                                          qstride, c0, nslab, scratch, counters,
+                                                                          zpitch);
     return;
   }
   static int force_slab = -1;   // HTLR_UPWARD_SLAB=1: slab kernel for every box (tests)
@@ -383,7 +403,8 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
   if (smem <= 200 * 1024 && !force_slab) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(upward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride, c0);
+    upward_kernel<<<dim3((unsigned)nc, R), 256, smem, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride, c0,
+                                                            zpitch);
     return;
   }
   const int P = (d == 2) ? p * p : p * p * p;
@@ -391,7 +412,7 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
   if (smem2 > 48 * 1024)
     cudaFuncSetAttribute(upward_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   upward_slab_kernel<<<dim3((unsigned)nc, R), 256, smem2, st>>>(u, W, d, n, side, p, level, R, K_pad, Q, qstride,
-                                                                c0);
+                                                                c0, zpitch);
 }
 
 // ---------------------------------------------------------------------------

@@ -95,8 +95,11 @@ struct ZeroList {
   int64_t n[kMaxLevels + 2];
   int cnt = 0;
 };
+// zpitch (3-D): doubles between the z-planes of a stored box vector (0 =
+// natural layout; the separable passes use 68 so one bulk copy of a box lands
+// bank-conflict free in shared memory)
 void launch_permute_in(const double* u, double* ub, int d, int n, int s, int R, int K_pad, int64_t b0,
-                       int64_t nb, cudaStream_t st, const ZeroList* zero = nullptr);
+                       int64_t nb, cudaStream_t st, const ZeroList* zero = nullptr, int zpitch = 0);
 // one launch for permute + zeroing + the upward pass of every compressed
 // level (unsharded matvec); nb_zero and bits_L are filled in by the launcher
 struct UpLevel {
@@ -110,6 +113,7 @@ struct UpLevel {
   int nslab;
   double* scratch;   // [cluster - c0][rhs][nslab][p^3]
   int* counters;     // [cluster - c0][rhs], zero between launches
+  int zpitch;        // z-plane pitch of W (0: natural)
 };
 // z-slabs per cluster for a level of nc clusters x R right-hand sides (1: whole
 // boxes); HTLR_UPWARD_SPLIT=0 disables the split
@@ -117,7 +121,7 @@ int upward_nslab(int d, int side, int64_t nc, int R);
 struct PrologueParams {
   const double* u;
   double* ub;
-  int d, n, p, sL, R, K_pad_leaf, bits_L;
+  int d, n, p, sL, R, K_pad_leaf, bits_L, zpitch_leaf;
   int64_t b0, nb_perm, nb_zero;
   ZeroList zero;
   int nlev;
@@ -127,7 +131,7 @@ size_t upward_smem_words(int d, int side, int p);
 void launch_prologue(const PrologueParams& pp, cudaStream_t st);
 void launch_upward(const double* u, double* W, int d, int n, int side, int p, int level, int R,
                    int K_pad, const double* Q, int64_t qstride, int64_t c0, int64_t nc, cudaStream_t st,
-                   int nslab = 1, double* scratch = nullptr, int* counters = nullptr);
+                   int nslab = 1, double* scratch = nullptr, int* counters = nullptr, int zpitch = 0);
 // MT selects the tile config (64 or 128)
 int gemm_mt_for(int P_out);
 // gen: Toeplitz generators of the pass's matrices (near-only 3-D leaf pass
@@ -178,7 +182,8 @@ struct SepItem {
 // target tgt0 + w, the source boxes of a column (equal x, y box coordinates)
 // are staged once per CTA by bulk copies and shared by the 8 warps
 constexpr int kSepColMax = 10;      // source boxes per column
-constexpr int kSepBoxSmem = 8 * 68; // staged box: 8 z-planes of 64 doubles, padded (bank-conflict-free fragments)
+constexpr int kSepZPitch = 68;      // z-plane pitch of staged (and, in separable plans, stored) boxes
+constexpr int kSepBoxSmem = 8 * kSepZPitch; // staged box: 8 z-planes of 64 doubles, padded (bank-conflict-free fragments)
 // column slots in flight for NG consumer warp groups
 __host__ __device__ constexpr int sep_ring_slots(int NG) { return NG == 1 ? 3 : 4; }
 int sep_block_groups();
@@ -193,14 +198,16 @@ struct SepBlock {
 };
 size_t sep_block_smem_bytes(int nslots);
 void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
-                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st);
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st,
+                      int zpitch = 0);
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
                        const double* diag, double hd, double* corr_out, cudaStream_t st);
 size_t sep_smem_bytes(int nslots);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
-                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st);
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st,
+                      int zpitch = 0);
 
 // downward pass by per-warp mode products when p = leaf side = 8 in 3-D on a
 // uniform grid (HTLR_DOWN8=0 keeps downward_kernel)

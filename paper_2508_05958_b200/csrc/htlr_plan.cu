@@ -94,6 +94,7 @@ struct Pass {
   DevBuf sep_tab, sep_pairs, sep_items;
   DevBuf sep_blocks, sep_cols;   // cooperative leaf-pass layout (sep_block_kernel), if built
   int sep_nitems = 0, sep_NO = 0, sep_nblocks = 0;
+  int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
 };
 
@@ -1397,6 +1398,10 @@ int htlr_construct(htlr_plan* pl, void* stream) {
   }
   // separable-core formulation: 1-D factor tables instead of dense cores
   pl->sep = false;
+  for (auto& ps : pl->passes) {   // natural vector layout unless the separable passes apply
+    ps.zpitch = 0;
+    ps.K_pad = round_up(ps.P, htlr::kKC);
+  }
   if (sep_wanted(pl)) {
     if (pl->sep_corr.alloc(sizeof(double))) return 1;
     bool all = true;
@@ -1409,6 +1414,12 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       }
     }
     if (all) {
+      // source vectors (ub, W_l) stored with padded z-planes: one bulk copy
+      // per box into the apply kernel's bank-conflict-free staging layout
+      for (auto& ps : pl->passes) {
+        ps.zpitch = htlr::kSepZPitch;
+        ps.K_pad = htlr::kSepP * htlr::kSepZPitch;
+      }
       CUDA_TRY(cudaStreamSynchronize(st));
       CUDA_TRY(cudaGetLastError());
       tm.mark("construct: separable lists + factor tables");
@@ -1864,6 +1875,7 @@ int mv_local(MvCtx& cx, const double* u) {
     pp.sL = pl->sL;
     pp.R = R;
     pp.K_pad_leaf = lp.K_pad;
+    pp.zpitch_leaf = lp.zpitch;
     pp.b0 = b0;
     pp.nb_perm = nb;
     pp.zero = zl;
@@ -1881,7 +1893,7 @@ int mv_local(MvCtx& cx, const double* u) {
                                         pl->own_lo[ps.level], pl->own_hi[ps.level] - pl->own_lo[ps.level],
                                         lv.side,         lv.level,      ps.K_pad,
                                         lv.up_ns,        lv.up_ns > 1 ? lv.up_scratch.d() : nullptr,
-                                        lv.up_ns > 1 ? (int*)lv.up_count.ptr : nullptr};
+                                        lv.up_ns > 1 ? (int*)lv.up_count.ptr : nullptr, ps.zpitch};
     }
     if (fused) {
       htlr::launch_prologue(pp, cx.st);
@@ -1890,7 +1902,8 @@ int mv_local(MvCtx& cx, const double* u) {
     }
   }
   if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N * frac)) return 1;
-  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, cx.zeroed ? &zl : nullptr);
+  htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, cx.zeroed ? &zl : nullptr,
+                          lp.zpitch);
   if (cx.prof_end()) return 1;
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
@@ -1905,7 +1918,7 @@ int mv_local(MvCtx& cx, const double* u) {
       htlr::launch_dense_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Kron.d(), c0, nc, cx.st);
     else
       htlr::launch_upward(u, cx.W[i], d, pl->n, lv.side, p, lv.level, R, ps.K_pad, lv.Q.d(), 0, c0, nc, cx.st,
-                          lv.up_ns, lv.up_scratch.d(), (int*)lv.up_count.ptr);
+                          lv.up_ns, lv.up_scratch.d(), (int*)lv.up_count.ptr, ps.zpitch);
     if (cx.prof_end()) return 1;
   }
   return 0;
@@ -1943,11 +1956,11 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       if (ps.sep_nblocks > 0)
         htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
                                ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, B, ps.K_pad, C, ps.P, R,
-                               pl->sep_corr.d(), cx.st);
+                               pl->sep_corr.d(), cx.st, ps.zpitch);
       else
         htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
                                ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
-                               pl->sep_corr.d(), cx.st);
+                               pl->sep_corr.d(), cx.st, ps.zpitch);
       if (cx.prof_end()) return 1;
       continue;
     }

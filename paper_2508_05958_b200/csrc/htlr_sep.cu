@@ -146,20 +146,20 @@ __device__ __forceinline__ void sep_flush(const double* __restrict__ tab, int g,
 template <bool kSelfCorr>
 __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const SepItem& it, const int2* __restrict__ pr,
                                          const double* __restrict__ B, int ldb, double* __restrict__ C, int ldc, int R,
-                                         int r, double corr, int NO, int lane) {
+                                         int r, double corr, int NO, int lane, int zp) {
   double y[kSepP][2];
 #pragma unroll
   for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
   double z[kSepP][2];
 #pragma unroll
   for (int t = 0; t < kSepP; ++t) z[t][0] = z[t][1] = 0.0;
-  const int boff = (lane >> 2) + 64 * (lane & 3);
+  const int boff = (lane >> 2) + zp * (lane & 3);
   auto load = [&](double (&x)[kSepP][2], int src) {
     const double* s = B + ((int64_t)src * R + r) * ldb + boff;
 #pragma unroll
     for (int t = 0; t < kSepP; ++t) {
       x[t][0] = __ldg(s + 8 * t);
-      x[t][1] = __ldg(s + 8 * t + 256);
+      x[t][1] = __ldg(s + 8 * t + 4 * zp);
     }
   };
   int2 cur = pr[0];
@@ -195,11 +195,11 @@ __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const S
   }
   const int yoff = (lane >> 2) + 128 * (lane & 3);   // i + 64 k', k' = 2 (lane % 4) + jj
   if (kSelfCorr) {
-    const double* s = B + ((int64_t)it.tgt * R + r) * ldb + yoff;
+    const double* s = B + ((int64_t)it.tgt * R + r) * ldb + (lane >> 2) + 2 * zp * (lane & 3);
 #pragma unroll
     for (int j = 0; j < kSepP; ++j) {
       y[j][0] = fma(corr, __ldg(s + 8 * j), y[j][0]);
-      y[j][1] = fma(corr, __ldg(s + 8 * j + 64), y[j][1]);
+      y[j][1] = fma(corr, __ldg(s + 8 * j + zp), y[j][1]);
     }
   }
   double* o = C + ((int64_t)it.tgt * R + r) * ldc + yoff;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void sep_item(const double* __restrict__ tab, const S
 __global__ void __launch_bounds__(kSepWarps * 32)
     sep_apply_kernel(const double* __restrict__ tables, int nslots, int NO, const SepItem* __restrict__ items,
                      int nitems, const int2* __restrict__ pairs, const double* __restrict__ B, int ldb,
-                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr) {
+                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr, int zp) {
   extern __shared__ double tab[];
   for (int e = threadIdx.x; e < nslots * kSepSlotSmem; e += blockDim.x)
     tab[e] = tables[(e / kSepSlotSmem) * kSepSlot + e % kSepSlotSmem];
@@ -224,9 +224,9 @@ __global__ void __launch_bounds__(kSepWarps * 32)
   const SepItem it = items[item];
   const int r = blockIdx.y;
   if (it.flags & 1)
-    sep_item<true>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, corr_ptr[0], NO, lane);
+    sep_item<true>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, corr_ptr[0], NO, lane, zp);
   else
-    sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane);
+    sep_item<false>(tab, it, pairs + it.begin, B, ldb, C, ldc, R, r, 0.0, NO, lane, zp);
 }
 
 // Cooperative pass, persistent: CTA i walks the parts i, i + grid, ... (a
@@ -247,7 +247,7 @@ template <int NG>
 __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
     sep_block_kernel(const double* __restrict__ tables, int nslots, int NO, const SepBlock* __restrict__ blocks,
                      int nblocks, const SepCol* __restrict__ cols, const double* __restrict__ B, int ldb,
-                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr) {
+                     double* __restrict__ C, int ldc, int R, const double* __restrict__ corr_ptr, int zp) {
   constexpr int NS = sep_ring_slots(NG), SLOT = kSepColMax * kSepBoxSmem, NCW = 8 * NG;
   extern __shared__ __align__(16) double sm[];
   double* tab = sm;
@@ -276,13 +276,23 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
         const int slot = gc % NS;
         if (gc >= NS) mbar_wait(&empty[slot], (unsigned)(((gc / NS) - 1) & 1));
         const int n = cl[c].n;
-        if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * 512 * 8));
-        __syncwarp();
         double* dst = ring + slot * SLOT;
-        for (int e = lane; e < n * 8; e += 32) {
-          const int k = e >> 3, pl = e & 7;
-          bulk_g2s(dst + k * kSepBoxSmem + pl * 68, B + ((int64_t)cl[c].src[k] * R + r) * ldb + pl * 64, 64 * 8,
-                   &full[slot]);
+        if (zp == kSepZPitch) {
+          // boxes stored pitched: one bulk copy per box
+          if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * kSepBoxSmem * 8));
+          __syncwarp();
+          if (lane < n)
+            bulk_g2s(dst + lane * kSepBoxSmem, B + ((int64_t)cl[c].src[lane] * R + r) * ldb, kSepBoxSmem * 8,
+                     &full[slot]);
+        } else {
+          // natural layout: 8 plane copies per box into the padded slots
+          if (lane == 0) mbar_arrive_expect_tx(&full[slot], (unsigned)(n * 512 * 8));
+          __syncwarp();
+          for (int e = lane; e < n * 8; e += 32) {
+            const int k = e >> 3, pl = e & 7;
+            bulk_g2s(dst + k * kSepBoxSmem + pl * 68, B + ((int64_t)cl[c].src[k] * R + r) * ldb + pl * 64, 64 * 8,
+                     &full[slot]);
+          }
         }
       }
     }
@@ -340,11 +350,11 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
     const bool corr = (gc0 % NG) == grp && ((bk.corr_mask >> tw) & 1);
     if (corr) {
       const double cv = corr_ptr[0];
-      const double* s = B + ((int64_t)tgt * R + r) * ldb + yoff;
+      const double* s = B + ((int64_t)tgt * R + r) * ldb + (lane >> 2) + 2 * zp * (lane & 3);
 #pragma unroll
       for (int j = 0; j < kSepP; ++j) {
         y[j][0] = fma(cv, __ldg(s + 8 * j), y[j][0]);
-        y[j][1] = fma(cv, __ldg(s + 8 * j + 64), y[j][1]);
+        y[j][1] = fma(cv, __ldg(s + 8 * j + zp), y[j][1]);
       }
     }
     if (mine || corr) {
@@ -469,7 +479,7 @@ size_t sep_block_smem_bytes(int nslots) {
 template <int NG>
 static void launch_sep_block_t(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks,
                                const SepCol* cols, const double* B, int ldb, double* C, int ldc, int R,
-                               const double* corr, cudaStream_t st) {
+                               const double* corr, int zpitch, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(sep_block_kernel<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -480,16 +490,17 @@ static void launch_sep_block_t(const double* tables, int nslots, int NO, const S
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = nblocks < sms ? nblocks : sms;   // persistent: one CTA per SM
   sep_block_kernel<NG><<<dim3(grid, R), (8 * NG + 1) * 32, sep_block_smem_bytes(nslots), st>>>(
-      tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr);
+      tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, zpitch ? zpitch : 64);
 }
 
 void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* blocks, int nblocks, const SepCol* cols,
-                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st) {
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st,
+                      int zpitch) {
   if (nblocks <= 0) return;
   if (sep_block_groups() == 1)
-    launch_sep_block_t<1>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, st);
+    launch_sep_block_t<1>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, zpitch, st);
   else
-    launch_sep_block_t<2>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, st);
+    launch_sep_block_t<2>(tables, nslots, NO, blocks, nblocks, cols, B, ldb, C, ldc, R, corr, zpitch, st);
 }
 
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
@@ -501,7 +512,8 @@ void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, c
 size_t sep_smem_bytes(int nslots) { return (size_t)nslots * kSepSlotSmem * sizeof(double); }
 
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
-                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st) {
+                      const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st,
+                      int zpitch) {
   if (nitems <= 0) return;
   const size_t smem = sep_smem_bytes(nslots);
   static bool attr = false;
@@ -511,7 +523,7 @@ void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* i
   }
   dim3 grid((nitems + kSepWarps - 1) / kSepWarps, R);
   sep_apply_kernel<<<grid, kSepWarps * 32, smem, st>>>(tables, nslots, NO, items, nitems, pairs, B, ldb, C, ldc, R,
-                                                       corr);
+                                                       corr, zpitch ? zpitch : 64);
 }
 
 }  // namespace htlr
