@@ -176,6 +176,15 @@ int htlr_diag_value(htlr_plan* plan, double* out);
 int htlr_export_block(htlr_plan* plan, int64_t leaf_id, double* core_or_dense, int64_t cap,
                       double* factors, int64_t factor_cap, int32_t* shapes);
 
+/* f = A u with u and f in page-locked HOST memory (the reference's matvec
+ * takes host numpy arrays, operators.py:159-161): the plan copies u in and f
+ * out on the stream itself.  For separable plans the copies are overlapped
+ * with the device work (z halves of the vectors, two streams, one CUDA graph
+ * per (nrhs, u, f)); otherwise H2D, htlr_matvec, D2H.  Asynchronous on
+ * `stream`; negative if a vector is not page-locked (cudaHostAlloc /
+ * cudaHostRegister / pinned torch tensors) or the plan is sharded. */
+int htlr_matvec_host(htlr_plan* plan, const double* u_host, double* f_host, int64_t nrhs, void* stream);
+
 /* How the constructed plan applies its blocks: 0 = dense deduplicated cores
  * and near blocks (fp64 tensor-core GEMM passes); 1 = separable cores (a
  * tensor-product kernel -- the Gaussian -- on a uniform 3-D grid with

@@ -35,7 +35,8 @@ __device__ __forceinline__ int unpitch(int kp, int plane, int nplanes, int zpitc
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void permute_body(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
                                              int s, int bits, int R, int K_pad, int64_t b0, int64_t nb,
-                                             const ZeroList& zero, int64_t blk, int64_t nblk, int zpitch = 0) {
+                                             const ZeroList& zero, int64_t blk, int64_t nblk, int zpitch = 0,
+                                             int zsel = 0) {
   if (blk >= nb) {
     // the extra CTAs zero the accumulators of the coming GEMM passes
     const int64_t stride = (nblk - nb) * blockDim.x;
@@ -49,6 +50,7 @@ __device__ __forceinline__ void permute_body(const double* __restrict__ u, doubl
   const int64_t b = b0 + blk;   // leaf box, Morton id
   int bc[3];
   morton_decode(b, d, bits, bc);
+  if (zsel > 0 && (bc[2] >= (1 << bits) / 2 ? 2 : 1) != zsel) return;
   const int P = (d == 2) ? s * s : s * s * s;
   for (int idx = threadIdx.x; idx < R * K_pad; idx += blockDim.x) {
     int r = idx % R, kp = idx / R;
@@ -265,7 +267,7 @@ __global__ void prologue_kernel(PrologueParams pp) {
   const int64_t b = blockIdx.x;
   if (b < pp.nb_perm + pp.nb_zero) {
     permute_body(pp.u, pp.ub, pp.d, pp.n, pp.sL, pp.bits_L, pp.R, pp.K_pad_leaf, pp.b0, pp.nb_perm, pp.zero, b,
-                 pp.nb_perm + pp.nb_zero, pp.zpitch_leaf);
+                 pp.nb_perm + pp.nb_zero, pp.zpitch_leaf, pp.perm_zsel);
     return;
   }
   int64_t rest = b - pp.nb_perm - pp.nb_zero;

@@ -122,6 +122,9 @@ struct PrologueParams {
   const double* u;
   double* ub;
   int d, n, p, sL, R, K_pad_leaf, bits_L, zpitch_leaf;
+  // permute only the leaf boxes of one z half of the domain (1: z < n/2,
+  // 2: z >= n/2; 0: all) -- the overlapped host-vector matvec
+  int perm_zsel;
   int64_t b0, nb_perm, nb_zero;
   ZeroList zero;
   int nlev;
@@ -212,8 +215,11 @@ void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* i
 // downward pass by per-warp mode products when p = leaf side = 8 in 3-D on a
 // uniform grid (HTLR_DOWN8=0 keeps downward_kernel)
 bool downward8_supported(int d, int p, int sL, const DownParams& dp);
+// [zlo, zhi): leaf-box z range written (the overlapped host-vector matvec
+// writes f by z halves)
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
-                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st);
+                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st, int zlo = 0,
+                      int zhi = 1 << 30);
 
 // mapped grid (htlr_mapped.cu)
 void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,

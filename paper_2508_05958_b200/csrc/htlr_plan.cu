@@ -93,6 +93,11 @@ struct Pass {
   // (kind, o_x, o_y, o_z), warp work items, 1-D factor tables
   DevBuf sep_tab, sep_pairs, sep_items;
   DevBuf sep_blocks, sep_cols;   // cooperative leaf-pass layout (sep_block_kernel), if built
+  // leaf pass of an unsharded plan, for the overlapped host-vector matvec:
+  // columns cut at the domain's z midplane, parts grouped as (sources z < n/2),
+  // (sources z >= n/2, targets z < n/2), (both >= n/2)
+  DevBuf sep_gblocks, sep_gcols;
+  int sep_gcount[3] = {0, 0, 0};
   int sep_nitems = 0, sep_NO = 0, sep_nblocks = 0;
   int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
@@ -255,6 +260,11 @@ struct htlr_plan {
     int64_t launches;
   };
   std::vector<GraphEntry> graph_cache;
+  // overlapped host-vector matvec (htlr_matvec_host): its graphs (keyed by the
+  // host pointers), a copy stream and the fork / join events
+  std::vector<GraphEntry> host_graphs;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ov_ev[6] = {};
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
   std::vector<int32_t> prof_level;
@@ -451,6 +461,9 @@ int htlr_plan_destroy(htlr_plan* pl) {
   for (auto e : pl->prof_ev) cudaEventDestroy(e);
   for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
+  if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
+  for (auto& e : pl->ov_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& lv : pl->levels) {
     lv.Q.release();
     lv.R.release();
@@ -486,6 +499,8 @@ int htlr_plan_destroy(htlr_plan* pl) {
     ps.sep_items.release();
     ps.sep_blocks.release();
     ps.sep_cols.release();
+    ps.sep_gblocks.release();
+    ps.sep_gcols.release();
   }
   pl->sep_corr.release();
   pl->diag.release();
@@ -1075,34 +1090,87 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     htlr::SepBlock b;
     int64_t work;
   };
-  std::vector<Part> parts;
-  std::vector<htlr::SepCol> all;
-  for (int64_t P = 0; P < npar; ++P) {
-    const auto& cols = pcols[P];
+  // parts of <= per_part columns of one parent; selfc[w] = index of the column
+  // holding warp w's self pair (or -1)
+  auto emit = [&](const std::vector<htlr::SepCol>& cols, const int* selfc, int64_t P, std::vector<Part>& parts,
+                  std::vector<htlr::SepCol>& all) {
     for (size_t c0 = 0; c0 < cols.size(); c0 += per_part) {
       const size_t c1 = std::min(cols.size(), c0 + per_part);
       Part pt;
       pt.b.tgt0 = (int)(t0 + P * 8);
-      pt.b.col_begin = (int)(all.size() + (c0));
+      pt.b.col_begin = (int)(all.size() + c0);
       pt.b.col_count = (int)(c1 - c0);
       pt.b.corr_mask = 0;
       pt.work = 0;
       for (size_t c = c0; c < c1; ++c) pt.work += cols[c].n;
       for (int w = 0; w < 8; ++w)
-        if (pself[P][w] >= (int)c0 && pself[P][w] < (int)c1) pt.b.corr_mask |= 1 << w;
+        if (selfc[w] >= (int)c0 && selfc[w] < (int)c1) pt.b.corr_mask |= 1 << w;
       parts.push_back(pt);
     }
     all.insert(all.end(), cols.begin(), cols.end());
+  };
+  auto by_work = [](const Part& a, const Part& b) { return a.work > b.work; };
+  auto upload = [&](const std::vector<htlr::SepCol>& all, const std::vector<Part>& parts, DevBuf& dc,
+                    DevBuf& db) -> int {
+    std::vector<htlr::SepBlock> blocks;
+    for (const auto& pt : parts) blocks.push_back(pt.b);
+    if (dc.alloc(std::max<size_t>(1, all.size()) * sizeof(htlr::SepCol))) return 1;
+    if (!all.empty()) CUDA_TRY(cudaMemcpy(dc.ptr, all.data(), all.size() * sizeof(htlr::SepCol), cudaMemcpyHostToDevice));
+    if (db.alloc(std::max<size_t>(1, blocks.size()) * sizeof(htlr::SepBlock))) return 1;
+    if (!blocks.empty())
+      CUDA_TRY(cudaMemcpy(db.ptr, blocks.data(), blocks.size() * sizeof(htlr::SepBlock), cudaMemcpyHostToDevice));
+    return 0;
+  };
+  {
+    std::vector<Part> parts;
+    std::vector<htlr::SepCol> all;
+    for (int64_t P = 0; P < npar; ++P) emit(pcols[P], pself[P].data(), P, parts, all);
+    std::stable_sort(parts.begin(), parts.end(), by_work);
+    if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
+    ps.sep_nblocks = (int)parts.size();
   }
-  std::stable_sort(parts.begin(), parts.end(), [](const Part& a, const Part& b) { return a.work > b.work; });
-  std::vector<htlr::SepBlock> blocks;
-  for (const auto& pt : parts) blocks.push_back(pt.b);
-  if (ps.sep_cols.alloc(std::max<size_t>(1, all.size()) * sizeof(htlr::SepCol))) return 1;
-  if (!all.empty()) CUDA_TRY(cudaMemcpy(ps.sep_cols.ptr, all.data(), all.size() * sizeof(htlr::SepCol), cudaMemcpyHostToDevice));
-  if (ps.sep_blocks.alloc(std::max<size_t>(1, blocks.size()) * sizeof(htlr::SepBlock))) return 1;
-  if (!blocks.empty())
-    CUDA_TRY(cudaMemcpy(ps.sep_blocks.ptr, blocks.data(), blocks.size() * sizeof(htlr::SepBlock), cudaMemcpyHostToDevice));
-  ps.sep_nblocks = (int)blocks.size();
+  // z-midplane groups of the leaf pass (unsharded plans with an even number of
+  // leaf boxes per axis)
+  ps.sep_gcount[0] = ps.sep_gcount[1] = ps.sep_gcount[2] = 0;
+  const int mz = pl->levels[L].m;
+  if (ps.to_y && pl->shard_world == 1 && mz % 2 == 0) {
+    const int half = mz / 2;
+    std::vector<Part> grp[3];
+    std::vector<htlr::SepCol> all;
+    for (int64_t P = 0; P < npar; ++P) {
+      int tc[3];
+      htlr::morton_decode(t0 + P * 8, 3, L, tc);
+      const int th = tc[2] >= half ? 1 : 0;   // the 8 children share the parent's z half
+      for (int sh = 0; sh < 2; ++sh) {
+        std::vector<htlr::SepCol> cols;
+        int selfc[8];
+        for (auto& q : selfc) q = -1;
+        for (const auto& c : pcols[P]) {
+          htlr::SepCol h{};
+          for (int k = 0; k < c.n; ++k) {
+            int sc[3];
+            htlr::morton_decode(c.src[k], 3, L, sc);
+            if ((sc[2] >= half ? 1 : 0) != sh) continue;
+            h.src[h.n] = c.src[k];
+            for (int w = 0; w < 8; ++w) {
+              h.code[h.n][w] = c.code[k][w];
+              if (c.src[k] == (int)(t0 + P * 8 + w)) selfc[w] = (int)cols.size();
+            }
+            ++h.n;
+          }
+          if (h.n > 0) cols.push_back(h);
+        }
+        emit(cols, selfc, P, grp[sh == 0 ? 0 : 1 + th], all);
+      }
+    }
+    std::vector<Part> parts;
+    for (int g = 0; g < 3; ++g) {
+      std::stable_sort(grp[g].begin(), grp[g].end(), by_work);
+      ps.sep_gcount[g] = (int)grp[g].size();
+      parts.insert(parts.end(), grp[g].begin(), grp[g].end());
+    }
+    if (upload(all, parts, ps.sep_gcols, ps.sep_gblocks)) return 1;
+  }
   return 0;
 }
 
@@ -1841,6 +1909,40 @@ int mv_remote_mapped(MvCtx& cx, const double* u, double* f, int stages) {
   return 0;
 }
 
+// Parameters of the fused prologue launch (permute + zeroing + every level's
+// upward pass) of a uniform plan; false if a level cannot be fused.
+bool prologue_params(MvCtx& cx, const double* u, const htlr::ZeroList& zl, htlr::PrologueParams& pp) {
+  htlr_plan* pl = cx.pl;
+  const int d = cx.d, p = cx.p;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  pp.u = u;
+  pp.ub = cx.ub;
+  pp.d = d;
+  pp.n = pl->n;
+  pp.p = p;
+  pp.sL = pl->sL;
+  pp.R = cx.R;
+  pp.K_pad_leaf = lp.K_pad;
+  pp.zpitch_leaf = lp.zpitch;
+  pp.b0 = pl->own_lo[pl->L];
+  pp.nb_perm = pl->own_hi[pl->L] - pp.b0;
+  pp.zero = zl;
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    const Pass& ps = pl->passes[i];
+    if (ps.to_y) continue;
+    const Level& lv = pl->levels[ps.level];
+    if (lv.Kron.ptr || pp.nlev >= htlr::kMaxLevels ||
+        htlr::upward_smem_words(d, lv.side, p) * sizeof(double) > 200 * 1024)
+      return false;
+    pp.lev[pp.nlev++] = htlr::UpLevel{cx.W[i],       lv.Q.d(),      0,
+                                      pl->own_lo[ps.level], pl->own_hi[ps.level] - pl->own_lo[ps.level],
+                                      lv.side,         lv.level,      ps.K_pad,
+                                      lv.up_ns,        lv.up_ns > 1 ? lv.up_scratch.d() : nullptr,
+                                      lv.up_ns > 1 ? (int*)lv.up_count.ptr : nullptr, ps.zpitch};
+  }
+  return true;
+}
+
 int mv_local(MvCtx& cx, const double* u) {
   htlr_plan* pl = cx.pl;
   if (pl->mapped) return mv_local_mapped(cx, u);
@@ -1867,35 +1969,7 @@ int mv_local(MvCtx& cx, const double* u) {
   // one launch (profiling keeps them apart so each phase is timed)
   if (cx.zeroed && !pl->profiling) {
     htlr::PrologueParams pp{};
-    pp.u = u;
-    pp.ub = cx.ub;
-    pp.d = d;
-    pp.n = pl->n;
-    pp.p = p;
-    pp.sL = pl->sL;
-    pp.R = R;
-    pp.K_pad_leaf = lp.K_pad;
-    pp.zpitch_leaf = lp.zpitch;
-    pp.b0 = b0;
-    pp.nb_perm = nb;
-    pp.zero = zl;
-    bool fused = true;
-    for (size_t i = 0; i < pl->passes.size() && fused; ++i) {
-      const Pass& ps = pl->passes[i];
-      if (ps.to_y) continue;
-      const Level& lv = pl->levels[ps.level];
-      if (lv.Kron.ptr || pp.nlev >= htlr::kMaxLevels ||
-          htlr::upward_smem_words(d, lv.side, p) * sizeof(double) > 200 * 1024) {
-        fused = false;
-        break;
-      }
-      pp.lev[pp.nlev++] = htlr::UpLevel{cx.W[i],       lv.Q.d(),      0,
-                                        pl->own_lo[ps.level], pl->own_hi[ps.level] - pl->own_lo[ps.level],
-                                        lv.side,         lv.level,      ps.K_pad,
-                                        lv.up_ns,        lv.up_ns > 1 ? lv.up_scratch.d() : nullptr,
-                                        lv.up_ns > 1 ? (int*)lv.up_count.ptr : nullptr, ps.zpitch};
-    }
-    if (fused) {
+    if (prologue_params(cx, u, zl, pp)) {
       htlr::launch_prologue(pp, cx.st);
       ++cx.launches;
       return 0;
@@ -2015,6 +2089,8 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
 static void drop_graphs(htlr_plan* pl) {
   for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
   pl->graph_cache.clear();
+  for (auto& g : pl->host_graphs) cudaGraphExecDestroy(g.exec);
+  pl->host_graphs.clear();
 }
 
 int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
@@ -2038,9 +2114,9 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
         pl->prof_level = g.level;
         pl->prof_flops = g.flops;
         pl->prof_bytes = g.bytes;
-        CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
+        if (u != us) CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         CUDA_TRY(cudaGraphLaunch(g.exec, cx.st));
-        CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
+        if (f != fs) CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         pl->last_launches = g.launches;
         return 0;
       }
@@ -2060,9 +2136,9 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
       if (pl->graph_cache.size() >= 8) drop_graphs(pl);
       pl->graph_cache.push_back({cx.R, us, fs, pl->profiling, exec, pl->prof_kind, pl->prof_level, pl->prof_flops,
                                  pl->prof_bytes, cc.launches});
-      CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
+      if (u != us) CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
       CUDA_TRY(cudaGraphLaunch(exec, cx.st));
-      CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
+      if (f != fs) CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
       pl->last_launches = cc.launches;
       return 0;
     }
@@ -2076,6 +2152,167 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
   if (int rc = mv_local(cx, u)) return rc;
   if (int rc = mv_remote(cx, u, f)) return rc;
   pl->last_launches = cx.launches;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Host-vector matvec with the PCIe copies overlapped (unsharded separable
+// plans): the z < n/2 half of u goes first (F-order halves are contiguous);
+// its boxes are permuted and the leaf pass over its sources runs while the
+// other half is copied; then the rest of the prologue, the level passes, the
+// leaf pass over the upper sources for the lower targets, the lower half of
+// f (copied back while the leaf pass for the upper targets runs), the upper
+// half.  Captured once per (nrhs, host pointers) into a two-stream graph.
+// HTLR_OVERLAP=0: plain H2D, device matvec, D2H.
+// ---------------------------------------------------------------------------
+static bool overlap_ok(const htlr_plan* pl) {
+  const char* e = std::getenv("HTLR_OVERLAP");
+  if ((e && e[0] == '0') || !pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
+  if (pl->N % 2) return false;
+  for (const auto& ps : pl->passes) {
+    if (ps.sep_nblocks == 0) return false;
+    if (ps.to_y && ps.sep_gcount[0] + ps.sep_gcount[1] + ps.sep_gcount[2] == 0) return false;
+  }
+  return true;
+}
+
+namespace {
+
+int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
+  htlr_plan* pl = cx.pl;
+  const int R = cx.R, P = cx.P;
+  const int64_t Nh = pl->N / 2;   // points with z < n/2: the first half in F-order
+  const size_t hb = (size_t)Nh * R * sizeof(double);
+  double* us = pl->u_stage.d();
+  double* fs = pl->f_stage.d();
+  cudaEvent_t* ev = pl->ov_ev;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int hz = pl->levels[pl->L].m / 2;   // leaf boxes below the midplane
+  CUDA_TRY(cudaEventRecord(ev[0], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev[0], 0));
+  CUDA_TRY(cudaMemcpyAsync(us, uh, hb, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(ev[1], cs));
+  CUDA_TRY(cudaMemcpyAsync(us + Nh * R, uh + Nh * R, hb, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(ev[2], cs));
+  htlr::ZeroList zl;
+  for (const auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    const Level& lv = pl->levels[ps.level];
+    zl.p[zl.cnt] = lv.H.d();
+    zl.n[zl.cnt++] = lv.nclusters * R * P;
+  }
+  zl.p[zl.cnt] = pl->Y.d();
+  zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
+  // lower half in: permute its boxes, zero the accumulators, leaf pass over
+  // the lower sources (every target)
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[1], 0));
+  htlr::PrologueParams pa{};
+  if (!prologue_params(cx, us, zl, pa)) return fail(2, "overlapped matvec: prologue not fusable");
+  pa.nlev = 0;
+  pa.perm_zsel = 1;
+  htlr::launch_prologue(pa, cx.st);
+  auto leaf_group = [&](int g) {
+    int off = 0;
+    for (int q = 0; q < g; ++q) off += lp.sep_gcount[q];
+    htlr::launch_sep_block(lp.sep_tab.d(), 2 * lp.sep_NO, lp.sep_NO, (const htlr::SepBlock*)lp.sep_gblocks.ptr + off,
+                           lp.sep_gcount[g], (const htlr::SepCol*)lp.sep_gcols.ptr, cx.ub, lp.K_pad, pl->Y.d(), lp.P,
+                           R, pl->sep_corr.d(), cx.st, lp.zpitch);
+  };
+  leaf_group(0);
+  // upper half in: its boxes, every level's upward pass, the level passes
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2], 0));
+  htlr::PrologueParams pb{};
+  prologue_params(cx, us, htlr::ZeroList(), pb);
+  pb.perm_zsel = 2;
+  htlr::launch_prologue(pb, cx.st);
+  htlr::DownParams dp{};
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    const Pass& ps = pl->passes[i];
+    if (ps.to_y) continue;
+    Level& lv = pl->levels[ps.level];
+    htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
+                           ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, cx.W[i], ps.K_pad, lv.H.d(), ps.P, R,
+                           pl->sep_corr.d(), cx.st, ps.zpitch);
+    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0, nullptr};
+  }
+  if (!htlr::downward8_supported(3, cx.p, pl->sL, dp)) return fail(2, "overlapped matvec: downward not supported");
+  const int64_t nb = pl->levels[pl->L].nclusters;
+  const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
+  // lower targets: upper sources, downward, copy out while the upper targets run
+  leaf_group(1);
+  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, 0, hz);
+  CUDA_TRY(cudaEventRecord(ev[3], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev[3], 0));
+  CUDA_TRY(cudaMemcpyAsync(fh, fs, hb, cudaMemcpyDeviceToHost, cs));
+  leaf_group(2);
+  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, hz, 1 << 30);
+  CUDA_TRY(cudaEventRecord(ev[4], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev[4], 0));
+  CUDA_TRY(cudaMemcpyAsync(fh + Nh * R, fs + Nh * R, hb, cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaEventRecord(ev[5], cs));
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[5], 0));
+  cx.launches += 6 + dp.nlev;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+bool page_locked(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  MvCtx cx;
+  if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
+  if (!u || !f) return fail(-1, "null vector");
+  if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
+  if (!page_locked(u) || !page_locked(f)) return fail(-1, "host vectors must be page-locked (pinned or registered)");
+  const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
+  if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;
+  if (!overlap_ok(pl) || pl->profiling) {
+    CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyHostToDevice, cx.st));
+    if (int rc = htlr_matvec(pl, pl->u_stage.d(), pl->f_stage.d(), nrhs, stream)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(f, pl->f_stage.ptr, vbytes, cudaMemcpyDeviceToHost, cx.st));
+    return 0;
+  }
+  for (auto& g : pl->host_graphs) {
+    if (g.R == cx.R && g.u == u && g.f == f) {
+      CUDA_TRY(cudaGraphLaunch(g.exec, cx.st));
+      pl->last_launches = g.launches;
+      return 0;
+    }
+  }
+  if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  if (!pl->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : pl->ov_ev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  MvCtx cc = cx;
+  cc.st = pl->cap_stream;
+  cc.launches = 0;
+  CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
+  int rc = mv_overlap(cc, u, f, pl->copy_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (rc || ce != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return rc ? rc : fail(2, std::string("overlapped matvec capture failed: ") + cudaGetErrorString(ce));
+  }
+  cudaGraphDestroy(graph);
+  if (pl->host_graphs.size() >= 8) {
+    for (auto& g : pl->host_graphs) cudaGraphExecDestroy(g.exec);
+    pl->host_graphs.clear();
+  }
+  pl->host_graphs.push_back({cx.R, u, f, false, exec, {}, {}, {}, {}, cc.launches});
+  CUDA_TRY(cudaGraphLaunch(exec, cx.st));
+  pl->last_launches = cc.launches;
   return 0;
 }
 

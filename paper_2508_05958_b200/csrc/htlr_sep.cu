@@ -380,7 +380,7 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
 __global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict__ u, double* __restrict__ f,
                                                          const double* __restrict__ Y, const double* __restrict__ avec,
                                                          double aconst, int n, int L, int R, DownParams dp, int64_t b0,
-                                                         int64_t nb) {
+                                                         int64_t nb, int zlo, int zhi) {
   const int lane = threadIdx.x & 31;
   const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wi >= nb * R) return;
@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict
   const int r = (int)(wi % R);
   int bc[3];
   morton_decode(b, 3, L, bc);
+  if (bc[2] < zlo || bc[2] >= zhi) return;
   double y[kSepP][2], z[kSepP][2];
 #pragma unroll
   for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = z[j][0] = z[j][1] = 0.0;
@@ -454,10 +455,11 @@ bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
 }
 
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
-                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st) {
+                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st, int zlo, int zhi) {
   const int64_t warps = nb * R;
   if (warps <= 0) return;
-  downward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0, nb);
+  downward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0, nb, zlo,
+                                                                zhi);
 }
 
 // HTLR_SEP_GROUPS=1|2: consumer warp groups of the cooperative kernel

@@ -297,6 +297,27 @@ def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int], out=None):
         x2 = x
     R = int(x2.shape[1])
     dev = torch.device("cuda", op.device)
+    if host and is_torch and x2.is_pinned() and x2.is_contiguous():
+        # page-locked host vectors: the plan copies them itself, overlapped
+        # with the device work where the formulation allows (htlr_matvec_host)
+        shape = (n_pts,) if nrhs_expected == 1 else (n_pts, R)
+        if out is not None:
+            if not isinstance(out, torch.Tensor) or tuple(out.shape) != shape or out.dtype != torch.float64:
+                raise ValueError(f"out must be a float64 tensor of shape {shape}")
+        if out is not None and out.device.type == "cpu" and out.is_pinned() and out.is_contiguous():
+            res = out
+        else:
+            res = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        with torch.cuda.device(op.device):
+            stream = torch.cuda.current_stream(op.device)
+            _lib.check(_lib.lib().htlr_matvec_host(op._plan, ctypes.c_void_p(x2.data_ptr()),
+                                                   ctypes.c_void_p(res.data_ptr()), R,
+                                                   ctypes.c_void_p(stream.cuda_stream)))
+            stream.synchronize()
+        if out is not None and res is not out:
+            out.copy_(res)
+            return out
+        return res
     ud = x2.to(dev, non_blocking=True).contiguous()
     fd = torch.empty_like(ud)
     with torch.cuda.device(op.device):

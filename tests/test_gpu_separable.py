@@ -177,3 +177,42 @@ def test_out_buffer_host_and_device():
     assert rel(dev.cpu().numpy()[:, 0], ref) <= 1e-14
     with pytest.raises(ValueError):
         H.matvec(op, u, out=torch.empty(7, dtype=torch.float64))
+
+
+@pytest.mark.parametrize("n,a,R", [(64, 0.0, 1), (64, 0.4, 2), (128, 0.0, 1)])
+def test_host_vector_path_matches_device(n, a, R):
+    """Pinned host vectors go through htlr_matvec_host: for separable plans
+    the PCIe copies are overlapped with the device work (z halves, two
+    streams); the result equals the device-vector matvec (to rounding: RED
+    accumulation order), on repeated calls (graph replay) and for R > 1."""
+    import torch
+    op = make(n, 0.1, 1.0, a)
+    U = np.random.default_rng(n + R).standard_normal((n ** 3, R))
+    ref = H.matmat(op, torch.from_numpy(U).cuda()).cpu().numpy()
+    up = torch.from_numpy(U if R > 1 else U[:, 0].copy()).pin_memory()
+    out = torch.empty(up.shape, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        got = (H.matmat if R > 1 else H.matvec)(op, up, out=out)
+        assert got is out
+        assert rel(got.numpy().reshape(-1, R), ref) <= 1e-14
+    got2 = (H.matmat if R > 1 else H.matvec)(op, up)   # fresh pinned result (another graph)
+    assert got2.is_pinned() and rel(got2.numpy().reshape(-1, R), ref) <= 1e-14
+
+
+def test_host_vector_path_dense_plan_and_unpinned_rejected():
+    """A dense-core plan takes the plain H2D / matvec / D2H route; the C ABI
+    rejects pageable host pointers with a ValueError."""
+    import ctypes
+    import torch
+    from paper_2508_05958_b200 import _lib
+    cfg = H.BuildConfig(rank=6, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
+                        coeff=H.CoefficientFn.constant(0.0))
+    op = H.construct(cfg, H.UniformGrid(3, 32))
+    u = np.random.default_rng(9).uniform(-1, 1, 32 ** 3)
+    ref = H.matvec(op, torch.from_numpy(u).cuda()).cpu().numpy()
+    got = H.matvec(op, torch.from_numpy(u).pin_memory())
+    assert rel(got.numpy(), ref) <= 1e-14
+    f = np.zeros_like(u)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.lib().htlr_matvec_host(op._plan, ctypes.c_void_p(u.ctypes.data),
+                                               ctypes.c_void_p(f.ctypes.data), 1, None))

@@ -2,7 +2,8 @@
 # changes from experiment to experiment).  Example:
 #   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
 export PYTHONPATH=$PWD
-HTLR_TIMING=1 python tools/phases.py cfg4 > gpurun_out/ph.log 2>&1
-python tools/quick_time.py cfg4 cfg4 >> gpurun_out/ph.log 2>&1
-python -m pytest tests/test_gpu_separable.py tests/test_gpu_multi.py -x -q > gpurun_out/t.log 2>&1
-cat gpurun_out/ph.log; tail -n 2 gpurun_out/t.log
+python -m pytest tests/test_gpu_separable.py -x -q -k "host" > gpurun_out/t.log 2>&1
+python tools/e2e_probe.py cfg4 > gpurun_out/e2e.log 2>&1
+HTLR_OVERLAP=0 python tools/e2e_probe.py cfg4 >> gpurun_out/e2e.log 2>&1
+python tools/phases.py cfg4 >> gpurun_out/e2e.log 2>&1
+tail -n 15 gpurun_out/t.log; cat gpurun_out/e2e.log
