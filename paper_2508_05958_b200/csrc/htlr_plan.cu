@@ -564,18 +564,44 @@ int htlr_build_lists(htlr_plan* pl) {
   for (int l = 0; l <= pl->L; ++l)
     if (key_range(pl->levels[l].m) <= (1 << 22)) pl->levels[l].adm.dense.assign(key_range(pl->levels[l].m), 0);
   if (key_range(pl->levels[pl->L].m) <= (1 << 22)) pl->near.dense.assign(key_range(pl->levels[pl->L].m), 0);
-  // pass 1 (sequential, DFS order): the unique offset of every leaf (ids in
-  // order of first appearance) and the own pairs per offset; pass 2 (all
-  // cores): the (target, source) Morton ids into pre-sized member lists.
-  // The order inside a member list is not kept: every consumer sorts it.
+  // Offset tables.  (1, all cores) per leaf: its packed offset key and, for
+  // sharded plans, whether its target is owned; (2, sequential, DFS order)
+  // offset ids in order of first appearance -- the only order-dependent step,
+  // a tight loop over the keys; (3, all cores) per-chunk counts per id, then
+  // every chunk writes its (target, source) Morton ids at precomputed
+  // positions of the pre-sized member lists (no shared counters).  The order
+  // inside a member list is not kept: every consumer sorts it.
   const size_t nlf = tr.leaves.size();
+  const size_t ntab = pl->levels.size() + 1;   // adm per level, then near
+  std::vector<OffsetTable*> tabs;
+  for (auto& lv : pl->levels) tabs.push_back(&lv.adm);
+  tabs.push_back(&pl->near);
+  std::vector<int64_t> keys(nlf);
   std::vector<int> lid(nlf);
   std::vector<char> own(nlf, 1);
+  const size_t chunk = 1 << 15;
+  const size_t nchunks = (nlf + chunk - 1) / chunk;
+  std::atomic<bool> bad_level{false};
+  parallel_for(nchunks, [&](size_t c) {
+    const size_t e = std::min(nlf, (c + 1) * chunk);
+    for (size_t i = c * chunk; i < e; ++i) {
+      const auto& lf = tr.leaves[i];
+      keys[i] = pack_offset(lf.tc, lf.sc, d, pl->levels[lf.level].m);
+      if (world > 1) {
+        if (pl->own_lo[lf.level] < 0) {
+          bad_level = true;
+          continue;
+        }
+        const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
+        own[i] = tl >= pl->own_lo[lf.level] && tl < pl->own_hi[lf.level];
+      }
+    }
+  });
+  if (bad_level) return fail(-1, "admissible blocks on a level with fewer clusters than shards");
   for (size_t i = 0; i < nlf; ++i) {
     const auto& lf = tr.leaves[i];
     OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
-    const int m = pl->levels[lf.level].m;
-    const int64_t key = pack_offset(lf.tc, lf.sc, d, m);
+    const int64_t key = keys[i];
     int id = -1;
     if (!tab.dense.empty()) {
       id = tab.dense[key] - 1;
@@ -590,41 +616,53 @@ int htlr_build_lists(htlr_plan* pl) {
       else
         tab.id.emplace(key, id);
       tab.rep.push_back({lf.tc[0], lf.tc[1], lf.tc[2], lf.sc[0], lf.sc[1], lf.sc[2]});
-      tab.members.emplace_back();
     }
     lid[i] = id;
     if (lf.kind == 0)
       pl->levels[lf.level].num_adm++;
     else
       pl->num_near++;
-    if (world > 1) {
-      if (pl->own_lo[lf.level] < 0)
-        return fail(-1, "admissible blocks on a level with fewer clusters than shards");
-      const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
-      own[i] = tl >= pl->own_lo[lf.level] && tl < pl->own_hi[lf.level];
-    }
-    if (own[i]) tab.members[id].emplace_back(0, 0);   // counted now, filled in pass 2
   }
   {
-    std::vector<OffsetTable*> tabs;
-    for (auto& lv : pl->levels) tabs.push_back(&lv.adm);
-    tabs.push_back(&pl->near);
-    std::vector<std::vector<std::atomic<int>>> cur(tabs.size());
-    for (size_t t = 0; t < tabs.size(); ++t) {
-      std::vector<std::atomic<int>> v(tabs[t]->members.size());
-      for (auto& a : v) a.store(0);
-      cur[t].swap(v);
+    // global id = base[table] + id
+    std::vector<int> base(ntab + 1, 0);
+    for (size_t t = 0; t < ntab; ++t) base[t + 1] = base[t] + (int)tabs[t]->rep.size();
+    const int nid = base[ntab];
+    auto gid = [&](size_t i) {
+      const auto& lf = tr.leaves[i];
+      return base[lf.kind == 0 ? (size_t)lf.level : ntab - 1] + lid[i];
+    };
+    std::vector<std::vector<int>> cnt(nchunks, std::vector<int>(nid, 0));
+    parallel_for(nchunks, [&](size_t c) {
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i)
+        if (own[i]) cnt[c][gid(i)]++;
+    });
+    // exclusive prefix over chunks, per id; sizes of the member lists
+    std::vector<int> total(nid, 0);
+    for (size_t c = 0; c < nchunks; ++c)
+      for (int g = 0; g < nid; ++g) {
+        const int v = cnt[c][g];
+        cnt[c][g] = total[g];
+        total[g] += v;
+      }
+    std::vector<std::pair<int, int>*> dst(nid);
+    for (size_t t = 0; t < ntab; ++t) {
+      tabs[t]->members.assign(tabs[t]->rep.size(), {});
+      for (size_t k = 0; k < tabs[t]->rep.size(); ++k) {
+        auto& m = tabs[t]->members[k];
+        m.resize((size_t)total[base[t] + (int)k]);
+        dst[base[t] + (int)k] = m.data();
+      }
     }
-    const size_t chunk = 1 << 16;
-    parallel_for((nlf + chunk - 1) / chunk, [&](size_t c) {
+    parallel_for(nchunks, [&](size_t c) {
       const size_t e = std::min(nlf, (c + 1) * chunk);
       for (size_t i = c * chunk; i < e; ++i) {
         if (!own[i]) continue;
         const auto& lf = tr.leaves[i];
-        const size_t t = lf.kind == 0 ? (size_t)lf.level : tabs.size() - 1;
-        const int pos = cur[t][lid[i]].fetch_add(1, std::memory_order_relaxed);
-        tabs[t]->members[lid[i]][pos] = std::make_pair((int)htlr::morton_encode(lf.tc, d, lf.level),
-                                                        (int)htlr::morton_encode(lf.sc, d, lf.level));
+        const int g = gid(i);
+        dst[g][cnt[c][g]++] = std::make_pair((int)htlr::morton_encode(lf.tc, d, lf.level),
+                                             (int)htlr::morton_encode(lf.sc, d, lf.level));
       }
     });
   }
@@ -726,6 +764,7 @@ int htlr_build_lists(htlr_plan* pl) {
     pl->near_mats = (int)pl->near.members.size();
     if (fill_pass(ps, tabs)) return 1;
   }
+  tm.mark("lists: passes (sorted pairs)");
   pl->lists_built = true;
   pl->constructed = false;
   return 0;
