@@ -216,3 +216,23 @@ def test_host_vector_path_dense_plan_and_unpinned_rejected():
     with pytest.raises(ValueError):
         _lib.check(_lib.lib().htlr_matvec_host(op._plan, ctypes.c_void_p(u.ctypes.data),
                                                ctypes.c_void_p(f.ctypes.data), 1, None))
+
+
+@pytest.mark.parametrize("rule,eta", [("weak", None), ("strong", 2.0), ("strong", 0.7)])
+def test_separable_other_admissibility(rule, eta):
+    """Other admissibility rules change the offset sets and column lengths:
+    the plan stays separable where the 4-bit offset codes fit (falling back to
+    per-warp items when a column exceeds the cooperative layout) or keeps the
+    dense cores; either way the oracle's rows are reproduced."""
+    n = 32
+    adm = H.AdmissibilityRule.weak() if rule == "weak" else H.AdmissibilityRule.strong(eta)
+    cfg = H.BuildConfig(rank=8, leaf_side=8, rule=adm, kernel=H.gaussian(0.12), coeff=H.CoefficientFn.constant(0.3))
+    op = H.construct(cfg, H.UniformGrid(3, n))
+    print(rule, eta, op.formulation())
+    U = np.random.default_rng(21).standard_normal((n ** 3, 2))
+    F = H.matmat(op, U)
+    pb = O.Problem(d=3, n=n, rank=8, leaf_side_max=8, kernel=O.Kernel("gaussian", sigma=0.12),
+                   coeff=O.constant_coeff(0.3), rule=rule, eta=eta)
+    rows = O.sampled_matvec(pb, U, BOXES[32])
+    for i, bx in enumerate(BOXES[32]):
+        assert rel(F[O.box_linear_indices(n, bx)], rows[i]) <= TOL
