@@ -179,7 +179,7 @@ int htlr_export_block(htlr_plan* plan, int64_t leaf_id, double* core_or_dense, i
 /* f = A u with u and f in page-locked HOST memory (the reference's matvec
  * takes host numpy arrays, operators.py:159-161): the plan copies u in and f
  * out on the stream itself.  For separable plans the copies are overlapped
- * with the device work (z halves of the vectors, two streams, one CUDA graph
+ * with the device work (z-slabs of the vectors, two streams, one CUDA graph
  * per (nrhs, u, f)); otherwise H2D, htlr_matvec, D2H.  Asynchronous on
  * `stream`; negative if a vector is not page-locked (cudaHostAlloc /
  * cudaHostRegister / pinned torch tensors) or the plan is sharded. */

@@ -36,7 +36,7 @@ __device__ __forceinline__ int unpitch(int kp, int plane, int nplanes, int zpitc
 __device__ __forceinline__ void permute_body(const double* __restrict__ u, double* __restrict__ ub, int d, int n,
                                              int s, int bits, int R, int K_pad, int64_t b0, int64_t nb,
                                              const ZeroList& zero, int64_t blk, int64_t nblk, int zpitch = 0,
-                                             int zsel = 0) {
+                                             int zlo = 0, int zhi = 0) {
   if (blk >= nb) {
     // the extra CTAs zero the accumulators of the coming GEMM passes
     const int64_t stride = (nblk - nb) * blockDim.x;
@@ -50,7 +50,7 @@ __device__ __forceinline__ void permute_body(const double* __restrict__ u, doubl
   const int64_t b = b0 + blk;   // leaf box, Morton id
   int bc[3];
   morton_decode(b, d, bits, bc);
-  if (zsel > 0 && (bc[2] >= (1 << bits) / 2 ? 2 : 1) != zsel) return;
+  if (zhi > 0 && (bc[2] < zlo || bc[2] >= zhi)) return;
   const int P = (d == 2) ? s * s : s * s * s;
   for (int idx = threadIdx.x; idx < R * K_pad; idx += blockDim.x) {
     int r = idx % R, kp = idx / R;
@@ -267,7 +267,7 @@ __global__ void prologue_kernel(PrologueParams pp) {
   const int64_t b = blockIdx.x;
   if (b < pp.nb_perm + pp.nb_zero) {
     permute_body(pp.u, pp.ub, pp.d, pp.n, pp.sL, pp.bits_L, pp.R, pp.K_pad_leaf, pp.b0, pp.nb_perm, pp.zero, b,
-                 pp.nb_perm + pp.nb_zero, pp.zpitch_leaf, pp.perm_zsel);
+                 pp.nb_perm + pp.nb_zero, pp.zpitch_leaf, pp.zlo, pp.zhi);
     return;
   }
   int64_t rest = b - pp.nb_perm - pp.nb_zero;
@@ -276,6 +276,13 @@ __global__ void prologue_kernel(PrologueParams pp) {
     const int ns = lv.nslab > 1 ? lv.nslab : 1;
     const int64_t cnt = lv.nc * pp.R * ns;
     if (rest < cnt) {
+      if (pp.zhi > 0) {   // cluster filter: its last leaf-box z index in [zlo, zhi)
+        int cc[3];
+        morton_decode(lv.c0 + rest / ((int64_t)pp.R * ns), 3, lv.bits, cc);
+        const int span = 1 << (pp.bits_L - lv.bits);
+        const int zl = cc[2] * span + span - 1;
+        if (zl < pp.zlo || zl >= pp.zhi) return;
+      }
       if (ns > 1) {
         const int64_t cr = rest / ns;
         upward_split_body(pp.u, lv.W, pp.n, lv.side, pp.p, lv.bits, pp.R, lv.K_pad, lv.Q, lv.qstride,

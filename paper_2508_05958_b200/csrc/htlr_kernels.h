@@ -122,9 +122,10 @@ struct PrologueParams {
   const double* u;
   double* ub;
   int d, n, p, sL, R, K_pad_leaf, bits_L, zpitch_leaf;
-  // permute only the leaf boxes of one z half of the domain (1: z < n/2,
-  // 2: z >= n/2; 0: all) -- the overlapped host-vector matvec
-  int perm_zsel;
+  // overlapped host-vector matvec: only the leaf boxes whose z index lies in
+  // [zlo, zhi), and the upward pass only of the clusters whose last leaf-box
+  // z index does (zhi == 0: everything)
+  int zlo, zhi;
   int64_t b0, nb_perm, nb_zero;
   ZeroList zero;
   int nlev;

@@ -94,10 +94,12 @@ struct Pass {
   DevBuf sep_tab, sep_pairs, sep_items;
   DevBuf sep_blocks, sep_cols;   // cooperative leaf-pass layout (sep_block_kernel), if built
   // leaf pass of an unsharded plan, for the overlapped host-vector matvec:
-  // columns cut at the domain's z midplane, parts grouped as (sources z < n/2),
-  // (sources z >= n/2, targets z < n/2), (both >= n/2)
+  // the domain cut into sep_slabs z-slabs of leaf boxes, columns cut at the
+  // slab boundaries, parts grouped by (source slab s, target slab t), group
+  // s * sep_slabs + t holding sep_gcount[s * sep_slabs + t] parts
   DevBuf sep_gblocks, sep_gcols;
-  int sep_gcount[3] = {0, 0, 0};
+  int sep_slabs = 0;
+  std::vector<int> sep_gcount;
   int sep_nitems = 0, sep_NO = 0, sep_nblocks = 0;
   int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
@@ -264,7 +266,7 @@ struct htlr_plan {
   // host pointers), a copy stream and the fork / join events
   std::vector<GraphEntry> host_graphs;
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ov_ev[6] = {};
+  std::vector<cudaEvent_t> ov_ev;
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
   std::vector<int32_t> prof_level;
@@ -462,8 +464,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
   for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
-  for (auto& e : pl->ov_ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& e : pl->ov_ev) cudaEventDestroy(e);
   for (auto& lv : pl->levels) {
     lv.Q.release();
     lv.R.release();
@@ -1168,19 +1169,25 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
     ps.sep_nblocks = (int)parts.size();
   }
-  // z-midplane groups of the leaf pass (unsharded plans with an even number of
-  // leaf boxes per axis)
-  ps.sep_gcount[0] = ps.sep_gcount[1] = ps.sep_gcount[2] = 0;
+  // z-slab groups of the leaf pass (unsharded plans): HTLR_OVERLAP_SLABS
+  // (default 2; 4 measured slower on config 4: the extra launches cost more
+  // than the shorter exposed copies) slabs of an even number of leaf boxes
+  // each (so siblings share a slab)
+  ps.sep_slabs = 0;
+  ps.sep_gcount.clear();
   const int mz = pl->levels[L].m;
-  if (ps.to_y && pl->shard_world == 1 && mz % 2 == 0) {
-    const int half = mz / 2;
-    std::vector<Part> grp[3];
+  int S = 2;
+  if (const char* e = std::getenv("HTLR_OVERLAP_SLABS")) S = std::max(1, std::atoi(e));
+  if (mz % (2 * S) != 0) S = (mz % 4 == 0) ? 2 : 0;
+  if (ps.to_y && pl->shard_world == 1 && S > 0) {
+    const int zs = mz / S;   // leaf boxes per slab
+    std::vector<std::vector<Part>> grp((size_t)S * S);
     std::vector<htlr::SepCol> all;
     for (int64_t P = 0; P < npar; ++P) {
       int tc[3];
       htlr::morton_decode(t0 + P * 8, 3, L, tc);
-      const int th = tc[2] >= half ? 1 : 0;   // the 8 children share the parent's z half
-      for (int sh = 0; sh < 2; ++sh) {
+      const int th = tc[2] / zs;   // the 8 children share the parent's slab (zs is even)
+      for (int sh = 0; sh < S; ++sh) {
         std::vector<htlr::SepCol> cols;
         int selfc[8];
         for (auto& q : selfc) q = -1;
@@ -1189,7 +1196,7 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
           for (int k = 0; k < c.n; ++k) {
             int sc[3];
             htlr::morton_decode(c.src[k], 3, L, sc);
-            if ((sc[2] >= half ? 1 : 0) != sh) continue;
+            if (sc[2] / zs != sh) continue;
             h.src[h.n] = c.src[k];
             for (int w = 0; w < 8; ++w) {
               h.code[h.n][w] = c.code[k][w];
@@ -1199,16 +1206,17 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
           }
           if (h.n > 0) cols.push_back(h);
         }
-        emit(cols, selfc, P, grp[sh == 0 ? 0 : 1 + th], all);
+        if (!cols.empty()) emit(cols, selfc, P, grp[(size_t)sh * S + th], all);
       }
     }
     std::vector<Part> parts;
-    for (int g = 0; g < 3; ++g) {
-      std::stable_sort(grp[g].begin(), grp[g].end(), by_work);
-      ps.sep_gcount[g] = (int)grp[g].size();
-      parts.insert(parts.end(), grp[g].begin(), grp[g].end());
+    for (auto& g : grp) {
+      std::stable_sort(g.begin(), g.end(), by_work);
+      ps.sep_gcount.push_back((int)g.size());
+      parts.insert(parts.end(), g.begin(), g.end());
     }
     if (upload(all, parts, ps.sep_gcols, ps.sep_gblocks)) return 1;
+    ps.sep_slabs = S;
   }
   return 0;
 }
@@ -2196,21 +2204,22 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
 
 // ---------------------------------------------------------------------------
 // Host-vector matvec with the PCIe copies overlapped (unsharded separable
-// plans): the z < n/2 half of u goes first (F-order halves are contiguous);
-// its boxes are permuted and the leaf pass over its sources runs while the
-// other half is copied; then the rest of the prologue, the level passes, the
-// leaf pass over the upper sources for the lower targets, the lower half of
-// f (copied back while the leaf pass for the upper targets runs), the upper
-// half.  Captured once per (nrhs, host pointers) into a two-stream graph.
-// HTLR_OVERLAP=0: plain H2D, device matvec, D2H.
+// plans).  u and f are cut into S z-slabs of leaf boxes (contiguous in
+// F-order); slab s is copied in on a copy stream while the device permutes the
+// boxes of the slabs already there, runs the upward pass of the clusters they
+// complete and the leaf pass over their sources (parts grouped by (source
+// slab, target slab)); after the last slab and the level passes, each target
+// slab gets its last leaf group and its downward pass and is copied out while
+// the next one runs.  Captured once per (nrhs, host pointers) into a
+// two-stream graph.  HTLR_OVERLAP=0: plain H2D, device matvec, D2H.
 // ---------------------------------------------------------------------------
 static bool overlap_ok(const htlr_plan* pl) {
   const char* e = std::getenv("HTLR_OVERLAP");
   if ((e && e[0] == '0') || !pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
-  if (pl->N % 2) return false;
+
   for (const auto& ps : pl->passes) {
     if (ps.sep_nblocks == 0) return false;
-    if (ps.to_y && ps.sep_gcount[0] + ps.sep_gcount[1] + ps.sep_gcount[2] == 0) return false;
+    if (ps.to_y && ps.sep_slabs == 0) return false;
   }
   return true;
 }
@@ -2220,19 +2229,21 @@ namespace {
 int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   htlr_plan* pl = cx.pl;
   const int R = cx.R, P = cx.P;
-  const int64_t Nh = pl->N / 2;   // points with z < n/2: the first half in F-order
-  const size_t hb = (size_t)Nh * R * sizeof(double);
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int S = lp.sep_slabs;
+  const int zs = pl->levels[pl->L].m / S;         // leaf boxes per z-slab
+  const int64_t Ns = pl->N / S;                     // points per slab (contiguous in F-order)
+  const size_t sb = (size_t)Ns * R * sizeof(double);
   double* us = pl->u_stage.d();
   double* fs = pl->f_stage.d();
-  cudaEvent_t* ev = pl->ov_ev;
-  const Pass& lp = pl->passes[pl->leaf_pass];
-  const int hz = pl->levels[pl->L].m / 2;   // leaf boxes below the midplane
+  if ((int)pl->ov_ev.size() < 2 * S + 2) return fail(2, "overlapped matvec: events missing");
+  cudaEvent_t* ev = pl->ov_ev.data();   // [0] fork, [1..S] slab in, [S+1..2S] slab out ready, [2S+1] join
   CUDA_TRY(cudaEventRecord(ev[0], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[0], 0));
-  CUDA_TRY(cudaMemcpyAsync(us, uh, hb, cudaMemcpyHostToDevice, cs));
-  CUDA_TRY(cudaEventRecord(ev[1], cs));
-  CUDA_TRY(cudaMemcpyAsync(us + Nh * R, uh + Nh * R, hb, cudaMemcpyHostToDevice, cs));
-  CUDA_TRY(cudaEventRecord(ev[2], cs));
+  for (int q = 0; q < S; ++q) {
+    CUDA_TRY(cudaMemcpyAsync(us + q * Ns * R, uh + q * Ns * R, sb, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaEventRecord(ev[1 + q], cs));
+  }
   htlr::ZeroList zl;
   for (const auto& ps : pl->passes) {
     if (ps.to_y) continue;
@@ -2242,28 +2253,33 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   }
   zl.p[zl.cnt] = pl->Y.d();
   zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
-  // lower half in: permute its boxes, zero the accumulators, leaf pass over
-  // the lower sources (every target)
-  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[1], 0));
-  htlr::PrologueParams pa{};
-  if (!prologue_params(cx, us, zl, pa)) return fail(2, "overlapped matvec: prologue not fusable");
-  pa.nlev = 0;
-  pa.perm_zsel = 1;
-  htlr::launch_prologue(pa, cx.st);
-  auto leaf_group = [&](int g) {
-    int off = 0;
-    for (int q = 0; q < g; ++q) off += lp.sep_gcount[q];
-    htlr::launch_sep_block(lp.sep_tab.d(), 2 * lp.sep_NO, lp.sep_NO, (const htlr::SepBlock*)lp.sep_gblocks.ptr + off,
-                           lp.sep_gcount[g], (const htlr::SepCol*)lp.sep_gcols.ptr, cx.ub, lp.K_pad, pl->Y.d(), lp.P,
-                           R, pl->sep_corr.d(), cx.st, lp.zpitch);
+  std::vector<int> goff(lp.sep_gcount.size() + 1, 0);
+  for (size_t g = 0; g < lp.sep_gcount.size(); ++g) goff[g + 1] = goff[g] + lp.sep_gcount[g];
+  auto leaf_group = [&](int s, int t) {
+    const int g = s * S + t;
+    if (lp.sep_gcount[g] == 0) return;
+    htlr::launch_sep_block(lp.sep_tab.d(), 2 * lp.sep_NO, lp.sep_NO,
+                           (const htlr::SepBlock*)lp.sep_gblocks.ptr + goff[g], lp.sep_gcount[g],
+                           (const htlr::SepCol*)lp.sep_gcols.ptr, cx.ub, lp.K_pad, pl->Y.d(), lp.P, R,
+                           pl->sep_corr.d(), cx.st, lp.zpitch);
+    ++cx.launches;
   };
-  leaf_group(0);
-  // upper half in: its boxes, every level's upward pass, the level passes
-  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2], 0));
-  htlr::PrologueParams pb{};
-  prologue_params(cx, us, htlr::ZeroList(), pb);
-  pb.perm_zsel = 2;
-  htlr::launch_prologue(pb, cx.st);
+  // slab s in: permute its boxes (zeroing the accumulators with the first),
+  // the upward pass of the clusters it completes, the leaf pass over its
+  // sources for every target slab
+  for (int q = 0; q < S; ++q) {
+    CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[1 + q], 0));
+    htlr::PrologueParams pp{};
+    if (!prologue_params(cx, us, q == 0 ? zl : htlr::ZeroList(), pp))
+      return fail(2, "overlapped matvec: prologue not fusable");
+    pp.zlo = q * zs;
+    pp.zhi = (q + 1) * zs;
+    htlr::launch_prologue(pp, cx.st);
+    ++cx.launches;
+    if (q < S - 1)
+      for (int t = 0; t < S; ++t) leaf_group(q, t);
+  }
+  // every W is complete: the level passes
   htlr::DownParams dp{};
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
@@ -2272,25 +2288,25 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
     htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
                            ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, cx.W[i], ps.K_pad, lv.H.d(), ps.P, R,
                            pl->sep_corr.d(), cx.st, ps.zpitch);
+    ++cx.launches;
     dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0, nullptr};
   }
   if (!htlr::downward8_supported(3, cx.p, pl->sL, dp)) return fail(2, "overlapped matvec: downward not supported");
   const int64_t nb = pl->levels[pl->L].nclusters;
   const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
-  // lower targets: upper sources, downward, copy out while the upper targets run
-  leaf_group(1);
-  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, 0, hz);
-  CUDA_TRY(cudaEventRecord(ev[3], cx.st));
-  CUDA_TRY(cudaStreamWaitEvent(cs, ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(fh, fs, hb, cudaMemcpyDeviceToHost, cs));
-  leaf_group(2);
-  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, hz, 1 << 30);
-  CUDA_TRY(cudaEventRecord(ev[4], cx.st));
-  CUDA_TRY(cudaStreamWaitEvent(cs, ev[4], 0));
-  CUDA_TRY(cudaMemcpyAsync(fh + Nh * R, fs + Nh * R, hb, cudaMemcpyDeviceToHost, cs));
-  CUDA_TRY(cudaEventRecord(ev[5], cs));
-  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[5], 0));
-  cx.launches += 6 + dp.nlev;
+  // last slab's sources per target slab; each finished target slab is
+  // expanded and copied out while the next one runs
+  for (int t = 0; t < S; ++t) {
+    leaf_group(S - 1, t);
+    htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, t * zs,
+                           (t + 1) * zs);
+    ++cx.launches;
+    CUDA_TRY(cudaEventRecord(ev[S + 1 + t], cx.st));
+    CUDA_TRY(cudaStreamWaitEvent(cs, ev[S + 1 + t], 0));
+    CUDA_TRY(cudaMemcpyAsync(fh + t * Ns * R, fs + t * Ns * R, sb, cudaMemcpyDeviceToHost, cs));
+  }
+  CUDA_TRY(cudaEventRecord(ev[2 * S + 1], cs));
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2 * S + 1], 0));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -2329,8 +2345,11 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   }
   if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   if (!pl->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
-  for (auto& e : pl->ov_ev)
-    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  while (pl->ov_ev.size() < 2 * (size_t)pl->passes[pl->leaf_pass].sep_slabs + 2) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pl->ov_ev.push_back(e);
+  }
   MvCtx cc = cx;
   cc.st = pl->cap_stream;
   cc.launches = 0;

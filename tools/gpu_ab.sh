@@ -2,8 +2,9 @@
 # changes from experiment to experiment).  Example:
 #   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
 export PYTHONPATH=$PWD
+python tools/e2e_probe.py cfg4 2>&1 | grep pinned > gpurun_out/e2e.log
+HTLR_OVERLAP_SLABS=4 python tools/e2e_probe.py cfg4 2>&1 | grep pinned >> gpurun_out/e2e.log
+HTLR_OVERLAP=0 python tools/e2e_probe.py cfg4 2>&1 | grep pinned >> gpurun_out/e2e.log
 python -m pytest tests/test_gpu_separable.py -x -q -k "host" > gpurun_out/t.log 2>&1
-python tools/e2e_probe.py cfg4 > gpurun_out/e2e.log 2>&1
-HTLR_OVERLAP=0 python tools/e2e_probe.py cfg4 >> gpurun_out/e2e.log 2>&1
-python tools/phases.py cfg4 >> gpurun_out/e2e.log 2>&1
-tail -n 15 gpurun_out/t.log; cat gpurun_out/e2e.log
+HTLR_OVERLAP_SLABS=4 python -m pytest tests/test_gpu_separable.py -x -q -k "host" >> gpurun_out/t.log 2>&1
+cat gpurun_out/e2e.log; grep passed gpurun_out/t.log
