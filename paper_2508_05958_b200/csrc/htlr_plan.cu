@@ -266,6 +266,9 @@ struct htlr_plan {
   // host pointers), a copy stream and the fork / join events
   std::vector<GraphEntry> host_graphs;
   cudaStream_t copy_stream = nullptr;
+  // concurrent level passes (mv_remote): side stream + fork / join events
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ov_ev;
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
@@ -464,6 +467,9 @@ int htlr_plan_destroy(htlr_plan* pl) {
   for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
   if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
+  if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
+  for (auto& e : pl->side_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : pl->ov_ev) cudaEventDestroy(e);
   for (auto& lv : pl->levels) {
     lv.Q.release();
@@ -2060,8 +2066,27 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   }
   if ((stages & 1) && !cx.zeroed)
     CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
+  // The level passes (-> H_l) and the leaf pass (-> Y) are independent: the
+  // level passes go to a side stream (a parallel branch of the graph), so
+  // they fill the SMs the leaf pass leaves idle (its tail rounds).  Serial
+  // when profiling (per-launch events on one stream) or HTLR_CONCURRENT=0.
+  bool fork = false;
+  if ((stages & 1) && !pl->profiling) {
+    const char* e = std::getenv("HTLR_CONCURRENT");
+    int nlev = 0;
+    for (const auto& ps : pl->passes) nlev += ps.to_y ? 0 : 1;
+    fork = nlev > 0 && !(e && e[0] == '0');
+  }
+  if (fork) {
+    if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
+    for (auto& ev : pl->side_ev)
+      if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
+    CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
+  }
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
+    const cudaStream_t sst = (fork && !ps.to_y) ? pl->side_stream : cx.st;
     if (pl->sep) {
       if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;
       const double* B = ps.from_ub ? cx.ub : cx.W[i];
@@ -2077,11 +2102,11 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       if (ps.sep_nblocks > 0)
         htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
                                ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, B, ps.K_pad, C, ps.P, R,
-                               pl->sep_corr.d(), cx.st, ps.zpitch);
+                               pl->sep_corr.d(), sst, ps.zpitch);
       else
         htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
                                ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
-                               pl->sep_corr.d(), cx.st, ps.zpitch);
+                               pl->sep_corr.d(), sst, ps.zpitch);
       if (cx.prof_end()) return 1;
       continue;
     }
@@ -2101,9 +2126,13 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     double bytes = mat_bytes * ps.nmats + 2.0 * R8 * (double)ps.P * ncl;
     if (cx.prof_begin(ps.to_y ? 3 : 2, ps.level, flops, bytes)) return 1;
     htlr::launch_gemm(ps.MT, NT, ps.table.d(), ps.mat_stride, B, C, (const htlr::GemmTask*)slot.first.ptr,
-                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, cx.st,
+                      slot.second, (const int2*)ps.pairs.ptr, R, Rc, ps.K_pad, ps.P, ps.P, ps.RT, sst,
                       ps.gen.ptr ? ps.gen.d() : nullptr);
     if (cx.prof_end()) return 1;
+  }
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
+    CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
   }
   htlr::DownParams dp{};
   dp.nlev = 0;
@@ -2220,6 +2249,9 @@ static bool overlap_ok(const htlr_plan* pl) {
   for (const auto& ps : pl->passes) {
     if (ps.sep_nblocks == 0) return false;
     if (ps.to_y && ps.sep_slabs == 0) return false;
+    // the slab prologues are launches of the fused prologue kernel
+    if (!ps.to_y && htlr::upward_smem_words(pl->d, pl->levels[ps.level].side, pl->p) * sizeof(double) > 200 * 1024)
+      return false;
   }
   return true;
 }
