@@ -95,8 +95,9 @@ struct Pass {
   DevBuf sep_blocks, sep_cols;   // cooperative leaf-pass layout (sep_block_kernel), if built
   // leaf pass of an unsharded plan, for the overlapped host-vector matvec:
   // the domain cut into sep_slabs z-slabs of leaf boxes, columns cut at the
-  // slab boundaries, parts grouped by (source slab s, target slab t), group
-  // s * sep_slabs + t holding sep_gcount[s * sep_slabs + t] parts
+  // slab boundaries, parts in three ranges of sep_gcount[0..2] parts: sources
+  // in the first slab (every target); later sources, targets before the last
+  // slab; later sources, targets in the last slab
   DevBuf sep_gblocks, sep_gcols;
   int sep_slabs = 0;
   std::vector<int> sep_gcount;
@@ -1175,25 +1176,28 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
     ps.sep_nblocks = (int)parts.size();
   }
-  // z-slab groups of the leaf pass (unsharded plans): HTLR_OVERLAP_SLABS
-  // (default 2; 4 measured slower on config 4: the extra launches cost more
-  // than the shorter exposed copies) slabs of an even number of leaf boxes
-  // each (so siblings share a slab)
+  // z-slab groups of the leaf pass (unsharded plans): 4 slabs of an even
+  // number of leaf boxes (siblings share a slab), else 2 (HTLR_OVERLAP_SLABS
+  // overrides).  With 4, the first quarter of u goes in alone and the leaf work
+  // over its sources (~1/4) covers the copy of the rest; the last quarter of f
+  // is the only copy-out left exposed.
   ps.sep_slabs = 0;
   ps.sep_gcount.clear();
   const int mz = pl->levels[L].m;
-  int S = 2;
-  if (const char* e = std::getenv("HTLR_OVERLAP_SLABS")) S = std::max(1, std::atoi(e));
+  int S = (mz % 8 == 0) ? 4 : 2;
+  if (const char* e = std::getenv("HTLR_OVERLAP_SLABS")) S = std::max(2, std::atoi(e));
   if (mz % (2 * S) != 0) S = (mz % 4 == 0) ? 2 : 0;
   if (ps.to_y && pl->shard_world == 1 && S > 0) {
     const int zs = mz / S;   // leaf boxes per slab
-    std::vector<std::vector<Part>> grp((size_t)S * S);
+    std::vector<std::vector<Part>> grp(3);
     std::vector<htlr::SepCol> all;
     for (int64_t P = 0; P < npar; ++P) {
       int tc[3];
       htlr::morton_decode(t0 + P * 8, 3, L, tc);
       const int th = tc[2] / zs;   // the 8 children share the parent's slab (zs is even)
-      for (int sh = 0; sh < S; ++sh) {
+      // sources in the first slab vs the rest: the columns are cut only there
+      // (each cut adds a mode-x / mode-y flush per target)
+      for (int sh = 0; sh < 2; ++sh) {
         std::vector<htlr::SepCol> cols;
         int selfc[8];
         for (auto& q : selfc) q = -1;
@@ -1202,7 +1206,7 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
           for (int k = 0; k < c.n; ++k) {
             int sc[3];
             htlr::morton_decode(c.src[k], 3, L, sc);
-            if (sc[2] / zs != sh) continue;
+            if ((sc[2] >= zs ? 1 : 0) != sh) continue;
             h.src[h.n] = c.src[k];
             for (int w = 0; w < 8; ++w) {
               h.code[h.n][w] = c.code[k][w];
@@ -1212,7 +1216,8 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
           }
           if (h.n > 0) cols.push_back(h);
         }
-        if (!cols.empty()) emit(cols, selfc, P, grp[(size_t)sh * S + th], all);
+        const int range = sh == 0 ? 0 : (th < S - 1 ? 1 : 2);
+        if (!cols.empty()) emit(cols, selfc, P, grp[range], all);
       }
     }
     std::vector<Part> parts;
@@ -2233,14 +2238,15 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
 
 // ---------------------------------------------------------------------------
 // Host-vector matvec with the PCIe copies overlapped (unsharded separable
-// plans).  u and f are cut into S z-slabs of leaf boxes (contiguous in
-// F-order); slab s is copied in on a copy stream while the device permutes the
-// boxes of the slabs already there, runs the upward pass of the clusters they
-// complete and the leaf pass over their sources (parts grouped by (source
-// slab, target slab)); after the last slab and the level passes, each target
-// slab gets its last leaf group and its downward pass and is copied out while
-// the next one runs.  Captured once per (nrhs, host pointers) into a
-// two-stream graph.  HTLR_OVERLAP=0: plain H2D, device matvec, D2H.
+// plans).  u and f are cut at z-slab boundaries of leaf boxes (contiguous in
+// F-order, S = 4 slabs): the first slab of u is copied in alone; the device
+// permutes its boxes and runs the leaf pass over its sources (~1/S of the
+// work) while the rest of u is copied on a copy stream; then the remaining
+// prologue, the level passes, the leaf pass for the targets before the last
+// slab and their downward pass; their f is copied out while the last slab's
+// targets run; the last slab of f goes last.  Captured once per (nrhs, host
+// pointers) into a two-stream graph.  HTLR_OVERLAP=0: plain H2D, device
+// matvec, D2H.
 // ---------------------------------------------------------------------------
 static bool overlap_ok(const htlr_plan* pl) {
   const char* e = std::getenv("HTLR_OVERLAP");
@@ -2263,19 +2269,21 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   const int R = cx.R, P = cx.P;
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int S = lp.sep_slabs;
-  const int zs = pl->levels[pl->L].m / S;         // leaf boxes per z-slab
-  const int64_t Ns = pl->N / S;                     // points per slab (contiguous in F-order)
-  const size_t sb = (size_t)Ns * R * sizeof(double);
+  const int mz = pl->levels[pl->L].m, zs = mz / S;   // leaf boxes per axis / per slab
+  const int64_t Ns = pl->N / S;                      // points per slab (contiguous in F-order)
   double* us = pl->u_stage.d();
   double* fs = pl->f_stage.d();
-  if ((int)pl->ov_ev.size() < 2 * S + 2) return fail(2, "overlapped matvec: events missing");
-  cudaEvent_t* ev = pl->ov_ev.data();   // [0] fork, [1..S] slab in, [S+1..2S] slab out ready, [2S+1] join
+  if (pl->ov_ev.size() < 6 || lp.sep_gcount.size() != 3) return fail(2, "overlapped matvec: not prepared");
+  cudaEvent_t* ev = pl->ov_ev.data();
+  const size_t first = (size_t)Ns * R, rest = (size_t)(pl->N - Ns) * R, last = first;
+  const size_t lead = (size_t)(pl->N - Ns) * R;     // points before the last slab
+  // u: the first slab, then the rest, on the copy stream
   CUDA_TRY(cudaEventRecord(ev[0], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[0], 0));
-  for (int q = 0; q < S; ++q) {
-    CUDA_TRY(cudaMemcpyAsync(us + q * Ns * R, uh + q * Ns * R, sb, cudaMemcpyHostToDevice, cs));
-    CUDA_TRY(cudaEventRecord(ev[1 + q], cs));
-  }
+  CUDA_TRY(cudaMemcpyAsync(us, uh, first * sizeof(double), cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(ev[1], cs));
+  CUDA_TRY(cudaMemcpyAsync(us + first, uh + first, rest * sizeof(double), cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaEventRecord(ev[2], cs));
   htlr::ZeroList zl;
   for (const auto& ps : pl->passes) {
     if (ps.to_y) continue;
@@ -2285,33 +2293,34 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   }
   zl.p[zl.cnt] = pl->Y.d();
   zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
-  std::vector<int> goff(lp.sep_gcount.size() + 1, 0);
-  for (size_t g = 0; g < lp.sep_gcount.size(); ++g) goff[g + 1] = goff[g] + lp.sep_gcount[g];
-  auto leaf_group = [&](int s, int t) {
-    const int g = s * S + t;
+  auto leaf_range = [&](int g) {
+    int off = 0;
+    for (int q = 0; q < g; ++q) off += lp.sep_gcount[q];
     if (lp.sep_gcount[g] == 0) return;
-    htlr::launch_sep_block(lp.sep_tab.d(), 2 * lp.sep_NO, lp.sep_NO,
-                           (const htlr::SepBlock*)lp.sep_gblocks.ptr + goff[g], lp.sep_gcount[g],
-                           (const htlr::SepCol*)lp.sep_gcols.ptr, cx.ub, lp.K_pad, pl->Y.d(), lp.P, R,
-                           pl->sep_corr.d(), cx.st, lp.zpitch);
+    htlr::launch_sep_block(lp.sep_tab.d(), 2 * lp.sep_NO, lp.sep_NO, (const htlr::SepBlock*)lp.sep_gblocks.ptr + off,
+                           lp.sep_gcount[g], (const htlr::SepCol*)lp.sep_gcols.ptr, cx.ub, lp.K_pad, pl->Y.d(), lp.P,
+                           R, pl->sep_corr.d(), cx.st, lp.zpitch);
     ++cx.launches;
   };
-  // slab s in: permute its boxes (zeroing the accumulators with the first),
-  // the upward pass of the clusters it completes, the leaf pass over its
-  // sources for every target slab
-  for (int q = 0; q < S; ++q) {
-    CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[1 + q], 0));
+  auto prologue = [&](int zlo, int zhi, const htlr::ZeroList& z) -> int {
     htlr::PrologueParams pp{};
-    if (!prologue_params(cx, us, q == 0 ? zl : htlr::ZeroList(), pp))
-      return fail(2, "overlapped matvec: prologue not fusable");
-    pp.zlo = q * zs;
-    pp.zhi = (q + 1) * zs;
+    if (!prologue_params(cx, us, z, pp)) return fail(2, "overlapped matvec: prologue not fusable");
+    pp.zlo = zlo;
+    pp.zhi = zhi;
     htlr::launch_prologue(pp, cx.st);
     ++cx.launches;
-    if (q < S - 1)
-      for (int t = 0; t < S; ++t) leaf_group(q, t);
-  }
-  // every W is complete: the level passes
+    return 0;
+  };
+  // first slab: its boxes (and the accumulators zeroed), the clusters it
+  // completes, the leaf pass over its sources while the rest is copied
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[1], 0));
+  if (prologue(0, zs, zl)) return 1;
+  leaf_range(0);
+  // the rest: boxes, upward passes, level passes, the leaf pass for the
+  // targets before the last slab, their f copied out while the last slab's
+  // targets run
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2], 0));
+  if (prologue(zs, mz, htlr::ZeroList())) return 1;
   htlr::DownParams dp{};
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
@@ -2326,19 +2335,22 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   if (!htlr::downward8_supported(3, cx.p, pl->sL, dp)) return fail(2, "overlapped matvec: downward not supported");
   const int64_t nb = pl->levels[pl->L].nclusters;
   const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
-  // last slab's sources per target slab; each finished target slab is
-  // expanded and copied out while the next one runs
-  for (int t = 0; t < S; ++t) {
-    leaf_group(S - 1, t);
-    htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, t * zs,
-                           (t + 1) * zs);
-    ++cx.launches;
-    CUDA_TRY(cudaEventRecord(ev[S + 1 + t], cx.st));
-    CUDA_TRY(cudaStreamWaitEvent(cs, ev[S + 1 + t], 0));
-    CUDA_TRY(cudaMemcpyAsync(fh + t * Ns * R, fs + t * Ns * R, sb, cudaMemcpyDeviceToHost, cs));
-  }
-  CUDA_TRY(cudaEventRecord(ev[2 * S + 1], cs));
-  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2 * S + 1], 0));
+  leaf_range(1);
+  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, 0,
+                         mz - zs);
+  ++cx.launches;
+  CUDA_TRY(cudaEventRecord(ev[3], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev[3], 0));
+  CUDA_TRY(cudaMemcpyAsync(fh, fs, lead * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  leaf_range(2);
+  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, mz - zs,
+                         mz);
+  ++cx.launches;
+  CUDA_TRY(cudaEventRecord(ev[4], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, ev[4], 0));
+  CUDA_TRY(cudaMemcpyAsync(fh + lead, fs + lead, last * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaEventRecord(ev[5], cs));
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[5], 0));
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -2377,7 +2389,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   }
   if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   if (!pl->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
-  while (pl->ov_ev.size() < 2 * (size_t)pl->passes[pl->leaf_pass].sep_slabs + 2) {
+  while (pl->ov_ev.size() < 6) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pl->ov_ev.push_back(e);

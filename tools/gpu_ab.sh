@@ -2,9 +2,9 @@
 # changes from experiment to experiment).  Example:
 #   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
 export PYTHONPATH=$PWD
-for w in cfg1 cfg2 cfg3 cfg4; do
-  python tools/phases.py $w 20 2>&1 | head -1 >> gpurun_out/ab.log
-  HTLR_CONCURRENT=0 python tools/phases.py $w 20 2>&1 | head -1 | sed 's/^/serial /' >> gpurun_out/ab.log
-done
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -x -q > gpurun_out/t.log 2>&1
-cat gpurun_out/ab.log; tail -n 2 gpurun_out/t.log
+python tools/e2e_probe.py cfg4 2>&1 | grep -E "pinned|h2d" > gpurun_out/e2e.log
+HTLR_OVERLAP_SLABS=2 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned in" >> gpurun_out/e2e.log
+HTLR_OVERLAP=0 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned in" >> gpurun_out/e2e.log
+python -m pytest tests/test_gpu_separable.py -x -q -k "host" > gpurun_out/t.log 2>&1
+HTLR_OVERLAP_SLABS=2 python -m pytest tests/test_gpu_separable.py -x -q -k "host" >> gpurun_out/t.log 2>&1
+cat gpurun_out/e2e.log; grep passed gpurun_out/t.log
