@@ -2321,6 +2321,13 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   // targets run
   CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[2], 0));
   if (prologue(zs, mz, htlr::ZeroList())) return 1;
+  // level passes on the side stream, next to the leaf pass (joined before the
+  // downward passes)
+  if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
+  for (auto& e : pl->side_ev)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
   htlr::DownParams dp{};
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
@@ -2328,14 +2335,16 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
     Level& lv = pl->levels[ps.level];
     htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
                            ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, cx.W[i], ps.K_pad, lv.H.d(), ps.P, R,
-                           pl->sep_corr.d(), cx.st, ps.zpitch);
+                           pl->sep_corr.d(), pl->side_stream, ps.zpitch);
     ++cx.launches;
     dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0, nullptr};
   }
+  CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
   if (!htlr::downward8_supported(3, cx.p, pl->sL, dp)) return fail(2, "overlapped matvec: downward not supported");
   const int64_t nb = pl->levels[pl->L].nclusters;
   const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
   leaf_range(1);
+  CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
   htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, 0,
                          mz - zs);
   ++cx.launches;
