@@ -162,6 +162,15 @@ int htlr_bind_reduce(htlr_plan* plan, int64_t nrhs, void* const* ptrs, int64_t c
 int htlr_matvec_contract(htlr_plan* plan, const double* u, int64_t nrhs, void* stream);
 int htlr_matvec_expand(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
 
+/* The remote phase split around the exchange, so the all-gather overlaps
+ * device work: _begin zeroes the accumulators and (separable plans) applies
+ * the blocks whose sources this shard owns -- it reads only the own chunk of
+ * the exchange buffers; _finish, after the exchange, applies the rest and runs
+ * the downward pass.  begin + finish == htlr_matvec_remote (not for the
+ * mapped symmetric plans, which use contract / reduce / expand). */
+int htlr_matvec_remote_begin(htlr_plan* plan, const double* u, int64_t nrhs, void* stream);
+int htlr_matvec_remote_finish(htlr_plan* plan, const double* u, double* f, int64_t nrhs, void* stream);
+
 /* Diagonal cell average used by the inadmissible tau == sigma blocks
  * (operators.py:95-99).  Synchronises. */
 int htlr_diag_value(htlr_plan* plan, double* out);

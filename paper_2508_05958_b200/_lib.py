@@ -56,6 +56,8 @@ SYMBOLS = [
     ("htlr_construct", ctypes.c_int, [_P, _P]),
     ("htlr_matvec", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("htlr_matvec_host", ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    ("htlr_matvec_remote_begin", ctypes.c_int, [_P, _P, _I64, _P]),
+    ("htlr_matvec_remote_finish", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("htlr_set_lowrank", ctypes.c_int, [_P, _I32]),
     ("htlr_set_shard", ctypes.c_int, [_P, _I32, _I32]),
     ("htlr_shard_info", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),

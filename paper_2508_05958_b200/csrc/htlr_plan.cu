@@ -102,6 +102,8 @@ struct Pass {
   int sep_slabs = 0;
   std::vector<int> sep_gcount;
   int sep_nitems = 0, sep_NO = 0, sep_nblocks = 0;
+  int sep_own_nb = 0;            // sharded plans: parts [0, sep_own_nb) read only own sources
+  double sep_own_frac = 1.0;     // their share of the pass's (pair, box) work
   int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
 };
@@ -1168,13 +1170,53 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
       CUDA_TRY(cudaMemcpy(db.ptr, blocks.data(), blocks.size() * sizeof(htlr::SepBlock), cudaMemcpyHostToDevice));
     return 0;
   };
-  {
+  if (pl->shard_world == 1) {
     std::vector<Part> parts;
     std::vector<htlr::SepCol> all;
     for (int64_t P = 0; P < npar; ++P) emit(pcols[P], pself[P].data(), P, parts, all);
     std::stable_sort(parts.begin(), parts.end(), by_work);
     if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
+    ps.sep_nblocks = ps.sep_own_nb = (int)parts.size();
+  } else {
+    // sharded: columns cut where the sources change owner; the parts over own
+    // sources first (they run while the exchange is in flight), then the rest
+    const int64_t olo = pl->own_lo[L], ohi = pl->own_hi[L];
+    std::vector<Part> grp[2];
+    std::vector<htlr::SepCol> all;
+    for (int64_t P = 0; P < npar; ++P) {
+      for (int side = 0; side < 2; ++side) {
+        std::vector<htlr::SepCol> cols;
+        int selfc[8];
+        for (auto& q : selfc) q = -1;
+        for (const auto& c : pcols[P]) {
+          htlr::SepCol h{};
+          for (int k = 0; k < c.n; ++k) {
+            const bool own = c.src[k] >= olo && c.src[k] < ohi;
+            if (own != (side == 0)) continue;
+            h.src[h.n] = c.src[k];
+            for (int w = 0; w < 8; ++w) {
+              h.code[h.n][w] = c.code[k][w];
+              if (c.src[k] == (int)(t0 + P * 8 + w)) selfc[w] = (int)cols.size();
+            }
+            ++h.n;
+          }
+          if (h.n > 0) cols.push_back(h);
+        }
+        if (!cols.empty()) emit(cols, selfc, P, grp[side], all);
+      }
+    }
+    std::vector<Part> parts;
+    for (auto& g : grp) {
+      std::stable_sort(g.begin(), g.end(), by_work);
+      parts.insert(parts.end(), g.begin(), g.end());
+    }
+    if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
     ps.sep_nblocks = (int)parts.size();
+    ps.sep_own_nb = (int)grp[0].size();
+    double w0 = 0, w1 = 0;
+    for (const auto& pt : grp[0]) w0 += (double)pt.work;
+    for (const auto& pt : grp[1]) w1 += (double)pt.work;
+    ps.sep_own_frac = (w0 + w1) > 0 ? w0 / (w0 + w1) : 1.0;
   }
   // z-slab groups of the leaf pass (unsharded plans): 4 slabs of an even
   // number of leaf boxes (siblings share a slab), else 2 (HTLR_OVERLAP_SLABS
@@ -2063,13 +2105,17 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   const double R8 = 8.0 * R;
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int64_t nleaf = pl->levels[pl->L].nclusters;
+  // stages: 1 contract, 2 expand; 4 = contract only the separable parts over
+  // own sources (+ the zeroing), 8 = contract the rest without zeroing
+  // (htlr_matvec_remote_begin / _finish: the exchange overlaps the first)
+  const bool own_only = (stages & 4) != 0, rest_only = (stages & 8) != 0;
   for (auto& ps : pl->passes) {
-    if (!(stages & 1) || cx.zeroed) break;
+    if (!(stages & 1) || cx.zeroed || rest_only) break;
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
     CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), cx.st));
   }
-  if ((stages & 1) && !cx.zeroed)
+  if ((stages & 1) && !cx.zeroed && !rest_only)
     CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
   // The level passes (-> H_l) and the leaf pass (-> Y) are independent: the
   // level passes go to a side stream (a parallel branch of the graph), so
@@ -2092,8 +2138,18 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     const cudaStream_t sst = (fork && !ps.to_y) ? pl->side_stream : cx.st;
+    if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
       if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;
+      // part range of this stage (per-warp items: everything in the rest stage)
+      int b0 = 0, nbk = ps.sep_nblocks;
+      if (own_only) nbk = ps.sep_nblocks > 0 ? ps.sep_own_nb : 0;
+      if (rest_only) {
+        b0 = ps.sep_nblocks > 0 ? ps.sep_own_nb : 0;
+        nbk = ps.sep_nblocks - b0;
+      }
+      if (ps.sep_nblocks > 0 && nbk == 0) continue;
+      if (ps.sep_nblocks == 0 && own_only) continue;
       const double* B = ps.from_ub ? cx.ub : cx.W[i];
       double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
       // algorithmic work: 8^4 MAC per pair (mode z) + 2 * 8^4 per group
@@ -2101,13 +2157,16 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       // once (the per-pair gathers are L2 traffic) + the factor tables
       const double ncl = (double)pl->levels[ps.level].nclusters;
       const double m4 = 4096.0;
-      const double flops = 2.0 * m4 * ((double)ps.npairs + 2.0 * (double)ps.sep_groups) * R;
+      const double share =
+          own_only ? ps.sep_own_frac : (rest_only && ps.sep_nblocks > 0) ? 1.0 - ps.sep_own_frac : 1.0;
+      const double flops = share * 2.0 * m4 * ((double)ps.npairs + 2.0 * (double)ps.sep_groups) * R;
       const double bytes = 2.0 * R8 * (double)ps.P * ncl + 8.0 * 2 * ps.sep_NO * htlr::kSepSlot;
       if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, flops, bytes)) return 1;
       if (ps.sep_nblocks > 0)
-        htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepBlock*)ps.sep_blocks.ptr,
-                               ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, B, ps.K_pad, C, ps.P, R,
-                               pl->sep_corr.d(), sst, ps.zpitch);
+        htlr::launch_sep_block(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO,
+                               (const htlr::SepBlock*)ps.sep_blocks.ptr + b0, nbk,
+                               (const htlr::SepCol*)ps.sep_cols.ptr, B, ps.K_pad, C, ps.P, R, pl->sep_corr.d(), sst,
+                               ps.zpitch);
       else
         htlr::launch_sep_apply(ps.sep_tab.d(), 2 * ps.sep_NO, ps.sep_NO, (const htlr::SepItem*)ps.sep_items.ptr,
                                ps.sep_nitems, (const int2*)ps.sep_pairs.ptr, B, ps.K_pad, C, ps.P, R,
@@ -2529,6 +2588,14 @@ int htlr_matvec_contract(htlr_plan* pl, const double* u, int64_t nrhs, void* str
 
 int htlr_matvec_expand(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
   return matvec_stage(pl, u, f, nrhs, stream, 2);
+}
+
+int htlr_matvec_remote_begin(htlr_plan* pl, const double* u, int64_t nrhs, void* stream) {
+  return matvec_stage(pl, u, nullptr, nrhs, stream, 1 | 4);
+}
+
+int htlr_matvec_remote_finish(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* stream) {
+  return matvec_stage(pl, u, f, nrhs, stream, 1 | 2 | 8);
 }
 
 int htlr_cell_average(int32_t kernel, double sigma, double scale, int32_t d, double h, int32_t q,

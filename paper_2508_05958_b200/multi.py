@@ -55,6 +55,21 @@ def allgather_chunks(bufs, rank: int, world: int, group=None) -> None:
             dist.all_gather(outs, mine.clone(), group=group)
 
 
+def allgather_chunks_async(bufs, rank: int, world: int, group=None):
+    """NCCL all-gather of the exchange buffers issued asynchronously (one
+    work handle per buffer); the caller enqueues device work that reads only
+    its own chunks, then waits (the current stream waits on the collective)."""
+    import torch.distributed as dist
+    works = []
+    for b in bufs:
+        n = b.numel()
+        if n % world:
+            raise ValueError("exchange buffer not divisible by the world size")
+        c = n // world
+        works.append(dist.all_gather_into_tensor(b, b[rank * c:(rank + 1) * c], group=group, async_op=True))
+    return works
+
+
 def reduce_scatter_chunks(bufs, rank: int, world: int, group=None) -> None:
     """In-place sum-reduce-scatter of each 1-D tensor: afterwards chunk
     `rank` holds the sum over all ranks' buffers (other chunks are scratch).
@@ -180,6 +195,25 @@ class ShardedOperator:
             _lib.check(_lib.lib().htlr_matvec_expand(self.local._plan, ctypes.c_void_p(ud.data_ptr()),
                                                      ctypes.c_void_p(fd.data_ptr()), R, st))
 
+    def remote_begin(self, ud, R: int):
+        """Zero the accumulators and apply the blocks whose sources this shard
+        owns (separable plans): reads only the own chunks of the exchange
+        buffers, so it runs while the all-gather is in flight."""
+        import torch
+        self.exchange_buffers(R)
+        with torch.cuda.device(self.device):
+            st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            _lib.check(_lib.lib().htlr_matvec_remote_begin(self.local._plan, ctypes.c_void_p(ud.data_ptr()), R, st))
+
+    def remote_finish(self, ud, fd, R: int):
+        """After the exchange: the remaining blocks and the downward pass."""
+        import torch
+        self.exchange_buffers(R)
+        with torch.cuda.device(self.device):
+            st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            _lib.check(_lib.lib().htlr_matvec_remote_finish(self.local._plan, ctypes.c_void_p(ud.data_ptr()),
+                                                            ctypes.c_void_p(fd.data_ptr()), R, st))
+
     def remote_phase(self, ud, fd, R: int, reduce=None):
         """GEMMs of the own targets + downward of the own leaf boxes.  A
         sharded symmetric plan sums its accumulators over the shards in
@@ -207,14 +241,26 @@ class ShardedOperator:
         fd = torch.zeros_like(ud)
         bufs = self.exchange_buffers(R)
         L = _lib.lib()
+        import torch.distributed as dist
+        overlap = (exchange is None and self.world > 1 and not self.reduce_buffers(R) and
+                   dist.get_backend(self.group) == "nccl")
         with torch.cuda.device(self.device):
             st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
             _lib.check(L.htlr_matvec_local(self.local._plan, ctypes.c_void_p(ud.data_ptr()), R, st))
-            if exchange is not None:
-                exchange(self, bufs)
-            elif self.world > 1:
-                allgather_chunks(bufs, self.rank, self.world, self.group)
-        self.remote_phase(ud, fd, R)
+            if overlap:
+                # the all-gather overlaps the blocks over own sources
+                works = allgather_chunks_async(bufs, self.rank, self.world, self.group)
+                self.remote_begin(ud, R)
+                for w in works:
+                    w.wait()
+                self.remote_finish(ud, fd, R)
+            else:
+                if exchange is not None:
+                    exchange(self, bufs)
+                elif self.world > 1:
+                    allgather_chunks(bufs, self.rank, self.world, self.group)
+        if not overlap:
+            self.remote_phase(ud, fd, R)
         out = fd.reshape(-1) if vec else fd
         return out.cpu() if host else out
 

@@ -2,9 +2,8 @@
 # changes from experiment to experiment).  Example:
 #   gpurun --timeout 1200 -- 'mkdir -p gpurun_out; bash tools/gpu_ab.sh'
 export PYTHONPATH=$PWD
-python tools/e2e_probe.py cfg4 2>&1 | grep -E "pinned|h2d" > gpurun_out/e2e.log
-HTLR_OVERLAP_SLABS=2 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned in" >> gpurun_out/e2e.log
-HTLR_OVERLAP=0 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned in" >> gpurun_out/e2e.log
-python -m pytest tests/test_gpu_separable.py -x -q -k "host" > gpurun_out/t.log 2>&1
-HTLR_OVERLAP_SLABS=2 python -m pytest tests/test_gpu_separable.py -x -q -k "host" >> gpurun_out/t.log 2>&1
-cat gpurun_out/e2e.log; grep passed gpurun_out/t.log
+python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/t.log 2>&1
+HTLR_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+  --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b_w2.json 2> gpurun_out/b_w2.err
+python tools/phases.py cfg4 > gpurun_out/ph.log 2>&1
+tail -n 3 gpurun_out/t.log; tail -c 300 gpurun_out/b_w2.json; head -3 gpurun_out/ph.log
