@@ -1025,9 +1025,12 @@ static bool regen_sym_enabled() {
 
 // HTLR_SEP_BLOCK=0: passes by per-warp items instead of the cooperative
 // per-parent CTAs (A/B runs, tests)
-static bool sep_block_enabled() {
+static bool sep_block_enabled(bool leaf) {
   const char* e = std::getenv("HTLR_SEP_BLOCK");
-  return !(e && e[0] == '0');
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == 'l') return leaf;     // "leaf": cooperative leaf pass only
+  if (e && e[0] == 'v') return !leaf;    // "levels": cooperative level passes only
+  return true;
 }
 
 // Cooperative layout of a pass: per parent cluster (8 consecutive Morton
@@ -1036,6 +1039,11 @@ static bool sep_block_enabled() {
 // 0xFFFF); columns split into parts of <= HTLR_SEP_COLS (default: ~16 parts
 // per SM, <= 12 columns), parts ordered by decreasing work.  Leaves the pass on per-warp items when a
 // column is longer than kSepColMax or the own range is not whole parents.
+// The self pair of a target is its near-field (kind 1) pair with itself.  The
+// target can also be another sibling's source (e.g. weak admissibility makes
+// adjacent siblings admissible), with no pair of its own -- code 0xFFFF.
+static bool is_self_code(unsigned short code) { return code != 0xFFFF && (code >> 12) == 1; }
+
 static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>& ptr, const std::vector<int2>& ent) {
   const int L = ps.level;
   const int64_t t0 = pl->own_lo[L], nt = pl->own_hi[L] - t0;
@@ -1114,7 +1122,7 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
         c.src[k - i] = v[k].id;
         for (int w = 0; w < 8; ++w) {
           c.code[k - i][w] = v[k].code[w];
-          if (v[k].id == (int)(t0 + (int64_t)P * 8 + w)) self_col[w] = (int)cols.size();
+          if (v[k].id == (int)(t0 + (int64_t)P * 8 + w) && is_self_code(v[k].code[w])) self_col[w] = (int)cols.size();
         }
       }
       cols.push_back(c);
@@ -1175,6 +1183,21 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     std::vector<htlr::SepCol> all;
     for (int64_t P = 0; P < npar; ++P) emit(pcols[P], pself[P].data(), P, parts, all);
     std::stable_sort(parts.begin(), parts.end(), by_work);
+    if (std::getenv("HTLR_SEP_DUMP") && npar <= 2) {
+      for (const auto& pt : parts) {
+        std::fprintf(stderr, "[sep dump] level %d part tgt0 %d cols %d..%d corr %x\n", L, pt.b.tgt0, pt.b.col_begin,
+                     pt.b.col_begin + pt.b.col_count, pt.b.corr_mask);
+        for (int c = pt.b.col_begin; c < pt.b.col_begin + pt.b.col_count; ++c) {
+          std::fprintf(stderr, "   col %d n=%d:", c, all[c].n);
+          for (int k = 0; k < all[c].n; ++k) {
+            std::fprintf(stderr, " src %d [", all[c].src[k]);
+            for (int w = 0; w < 8; ++w) std::fprintf(stderr, "%x ", all[c].code[k][w]);
+            std::fprintf(stderr, "]");
+          }
+          std::fprintf(stderr, "\n");
+        }
+      }
+    }
     if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
     ps.sep_nblocks = ps.sep_own_nb = (int)parts.size();
   } else {
@@ -1196,7 +1219,7 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
             h.src[h.n] = c.src[k];
             for (int w = 0; w < 8; ++w) {
               h.code[h.n][w] = c.code[k][w];
-              if (c.src[k] == (int)(t0 + P * 8 + w)) selfc[w] = (int)cols.size();
+              if (c.src[k] == (int)(t0 + P * 8 + w) && is_self_code(c.code[k][w])) selfc[w] = (int)cols.size();
             }
             ++h.n;
           }
@@ -1252,7 +1275,7 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
             h.src[h.n] = c.src[k];
             for (int w = 0; w < 8; ++w) {
               h.code[h.n][w] = c.code[k][w];
-              if (c.src[k] == (int)(t0 + P * 8 + w)) selfc[w] = (int)cols.size();
+              if (c.src[k] == (int)(t0 + P * 8 + w) && is_self_code(c.code[k][w])) selfc[w] = (int)cols.size();
             }
             ++h.n;
           }
@@ -1359,7 +1382,7 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   ps.sep_groups = groups;
   ps.sep_nblocks = 0;
   ps.sep_nitems = 0;
-  if (sep_block_enabled() && build_sep_blocks(pl, ps, ptr, ent)) return 1;
+  if (sep_block_enabled(ps.to_y) && build_sep_blocks(pl, ps, ptr, ent)) return 1;
   const int selfcode = (1 << 12) | (OR << 8) | (OR << 4) | OR;
   const int chunk = sep_chunk();
   std::vector<htlr::SepItem> items;
