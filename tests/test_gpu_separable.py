@@ -236,3 +236,37 @@ def test_separable_other_admissibility(rule, eta):
     rows = O.sampled_matvec(pb, U, BOXES[32])
     for i, bx in enumerate(BOXES[32]):
         assert rel(F[O.box_linear_indices(n, bx)], rows[i]) <= TOL
+
+
+def test_separable_random_sweep():
+    """Random separable-eligible problems (3-D Gaussian, p = leaf side = 8):
+    grid size, admissibility rule and eta, sigma, kernel scale, coefficient
+    and RHS count drawn at random; rows of random leaf boxes against the
+    oracle.  (The weak rule once exposed a self-correction bug that the
+    BASELINE configs could not.)"""
+    rng = np.random.default_rng(2024)
+    for case in range(8):
+        n = int(rng.choice([16, 32, 32]))
+        rule = str(rng.choice(["weak", "strong"]))
+        eta = float(rng.choice([0.5, 0.7, 1.0, 1.5, 2.0, 3.0])) if rule == "strong" else None
+        sig = float(rng.choice([0.05, 0.1, 0.3]))
+        scale = float(rng.choice([1.0, 0.7]))
+        a = float(rng.choice([0.0, 0.4]))
+        R = int(rng.choice([1, 2, 3]))
+        adm = H.AdmissibilityRule.weak() if rule == "weak" else H.AdmissibilityRule.strong(eta)
+        cfg = H.BuildConfig(rank=8, leaf_side=8, rule=adm, kernel=H.gaussian(sig, scale=scale),
+                            coeff=H.CoefficientFn.constant(a))
+        op = H.construct(cfg, H.UniformGrid(3, n))
+        U = rng.standard_normal((n ** 3, R))
+        F = H.matmat(op, U)
+        pb = O.Problem(d=3, n=n, rank=8, leaf_side_max=8, kernel=O.Kernel("gaussian", sigma=sig, scale=scale),
+                       coeff=O.constant_coeff(a), rule=rule, eta=eta)
+        m = n // 8
+        boxes = []
+        for _ in range(2):
+            c = rng.integers(0, m, size=3)
+            boxes.append(tuple((int(8 * q), int(8 * q + 8)) for q in c))
+        rows = O.sampled_matvec(pb, U, boxes)
+        for i, bx in enumerate(boxes):
+            err = rel(F[O.box_linear_indices(n, bx)], rows[i])
+            assert err <= TOL, (case, n, rule, eta, sig, scale, a, R, op.formulation(), err)
