@@ -1,4 +1,6 @@
 export PYTHONPATH=$PWD
-python -m pytest tests/test_gpu_separable.py -x -q -k "random" > gpurun_out/t.log 2>&1
-HTLR_SEP_BLOCK=0 python -m pytest tests/test_gpu_separable.py -x -q -k "random" >> gpurun_out/t.log 2>&1
-cat gpurun_out/t.log | tail -20
+export HTLR_GRAPHS=0
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_small.py > gpurun_out/memcheck.log 2>&1
+timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 20 python tools/sanitize_small.py > gpurun_out/racecheck.log 2>&1
+timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python tools/sanitize_small.py > gpurun_out/synccheck.log 2>&1
+tail -n 4 gpurun_out/memcheck.log gpurun_out/racecheck.log gpurun_out/synccheck.log
