@@ -2146,10 +2146,13 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   // when profiling (per-launch events on one stream) or HTLR_CONCURRENT=0.
   bool fork = false;
   if ((stages & 1) && !pl->profiling) {
-    const char* e = std::getenv("HTLR_CONCURRENT");
+    static const bool concurrent = [] {
+      const char* e = std::getenv("HTLR_CONCURRENT");
+      return !(e && e[0] == '0');
+    }();
     int nlev = 0;
     for (const auto& ps : pl->passes) nlev += ps.to_y ? 0 : 1;
-    fork = nlev > 0 && !(e && e[0] == '0');
+    fork = nlev > 0 && concurrent;
   }
   if (fork) {
     if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
@@ -2331,8 +2334,11 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
 // matvec, D2H.
 // ---------------------------------------------------------------------------
 static bool overlap_ok(const htlr_plan* pl) {
-  const char* e = std::getenv("HTLR_OVERLAP");
-  if ((e && e[0] == '0') || !pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
+  static const bool off = [] {
+    const char* e = std::getenv("HTLR_OVERLAP");
+    return e && e[0] == '0';
+  }();
+  if (off || !pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
 
   for (const auto& ps : pl->passes) {
     if (ps.sep_nblocks == 0) return false;
