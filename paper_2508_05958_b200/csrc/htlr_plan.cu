@@ -608,7 +608,57 @@ int htlr_build_lists(htlr_plan* pl) {
     }
   });
   if (bad_level) return fail(-1, "admissible blocks on a level with fewer clusters than shards");
-  for (size_t i = 0; i < nlf; ++i) {
+  tm.mark("lists: offset keys");
+  bool all_dense = true;
+  for (auto* t : tabs) all_dense = all_dense && !t->dense.empty();
+  if (all_dense) {
+    // (2) in parallel: every chunk lists its leaves whose key is new to the
+    // chunk (bitmaps per table), in index order; merged chunk by chunk, the
+    // first occurrence of every key gets the next id -- the same ids as the
+    // sequential pass; then lid[] and the per-level counts in parallel.
+    auto tab_of = [&](size_t i) {
+      const auto& lf = tr.leaves[i];
+      return lf.kind == 0 ? (size_t)lf.level : ntab - 1;
+    };
+    std::vector<std::vector<size_t>> cand(nchunks);
+    parallel_for(nchunks, [&](size_t c) {
+      std::vector<std::vector<char>> seen(ntab);
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i) {
+        const size_t t = tab_of(i);
+        if (seen[t].empty()) seen[t].assign(tabs[t]->dense.size(), 0);
+        char& f = seen[t][keys[i]];
+        if (!f) {
+          f = 1;
+          cand[c].push_back(i);
+        }
+      }
+    });
+    for (size_t c = 0; c < nchunks; ++c)
+      for (size_t i : cand[c]) {
+        OffsetTable& tab = *tabs[tab_of(i)];
+        int& slot = tab.dense[keys[i]];
+        if (slot == 0) {
+          slot = (int)tab.rep.size() + 1;
+          const auto& lf = tr.leaves[i];
+          tab.rep.push_back({lf.tc[0], lf.tc[1], lf.tc[2], lf.sc[0], lf.sc[1], lf.sc[2]});
+        }
+      }
+    std::vector<std::vector<int64_t>> lcount(nchunks, std::vector<int64_t>(ntab, 0));
+    parallel_for(nchunks, [&](size_t c) {
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i) {
+        const size_t t = tab_of(i);
+        lid[i] = tabs[t]->dense[keys[i]] - 1;
+        lcount[c][t]++;
+      }
+    });
+    for (size_t c = 0; c < nchunks; ++c) {
+      for (size_t t = 0; t + 1 < ntab; ++t) pl->levels[t].num_adm += lcount[c][t];
+      pl->num_near += lcount[c][ntab - 1];
+    }
+  }
+  for (size_t i = 0; i < nlf && !all_dense; ++i) {
     const auto& lf = tr.leaves[i];
     OffsetTable& tab = lf.kind == 0 ? pl->levels[lf.level].adm : pl->near;
     const int64_t key = keys[i];
@@ -633,6 +683,7 @@ int htlr_build_lists(htlr_plan* pl) {
     else
       pl->num_near++;
   }
+  tm.mark("lists: offset ids");
   {
     // global id = base[table] + id
     std::vector<int> base(ntab + 1, 0);
@@ -1256,35 +1307,47 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     const int zs = mz / S;   // leaf boxes per slab
     std::vector<std::vector<Part>> grp(3);
     std::vector<htlr::SepCol> all;
-    for (int64_t P = 0; P < npar; ++P) {
+    // per parent (all cores): its columns split by source slab class --
+    // sources in the first slab vs the rest; the columns are cut only there
+    // (each cut adds a mode-x / mode-y flush per target)
+    struct Split {
+      std::vector<htlr::SepCol> cols[2];
+      int selfc[2][8];
+      int th = 0;
+    };
+    std::vector<Split> split((size_t)npar);
+    parallel_for((size_t)npar, [&](size_t P) {
+      Split& sp = split[P];
       int tc[3];
-      htlr::morton_decode(t0 + P * 8, 3, L, tc);
-      const int th = tc[2] / zs;   // the 8 children share the parent's slab (zs is even)
-      // sources in the first slab vs the rest: the columns are cut only there
-      // (each cut adds a mode-x / mode-y flush per target)
-      for (int sh = 0; sh < 2; ++sh) {
-        std::vector<htlr::SepCol> cols;
-        int selfc[8];
-        for (auto& q : selfc) q = -1;
-        for (const auto& c : pcols[P]) {
-          htlr::SepCol h{};
-          for (int k = 0; k < c.n; ++k) {
-            int sc[3];
-            htlr::morton_decode(c.src[k], 3, L, sc);
-            if ((sc[2] >= zs ? 1 : 0) != sh) continue;
-            h.src[h.n] = c.src[k];
-            for (int w = 0; w < 8; ++w) {
-              h.code[h.n][w] = c.code[k][w];
-              if (c.src[k] == (int)(t0 + P * 8 + w) && is_self_code(c.code[k][w])) selfc[w] = (int)cols.size();
-            }
-            ++h.n;
+      htlr::morton_decode(t0 + (int64_t)P * 8, 3, L, tc);
+      sp.th = tc[2] / zs;   // the 8 children share the parent's slab (zs is even)
+      for (int sh = 0; sh < 2; ++sh)
+        for (auto& q : sp.selfc[sh]) q = -1;
+      for (const auto& c : pcols[P]) {
+        htlr::SepCol h[2] = {};
+        for (int k = 0; k < c.n; ++k) {
+          int sc[3];
+          htlr::morton_decode(c.src[k], 3, L, sc);
+          const int sh = sc[2] >= zs ? 1 : 0;
+          htlr::SepCol& o = h[sh];
+          o.src[o.n] = c.src[k];
+          for (int w = 0; w < 8; ++w) {
+            o.code[o.n][w] = c.code[k][w];
+            if (c.src[k] == (int)(t0 + (int64_t)P * 8 + w) && is_self_code(c.code[k][w]))
+              sp.selfc[sh][w] = (int)sp.cols[sh].size();
           }
-          if (h.n > 0) cols.push_back(h);
+          ++o.n;
         }
-        const int range = sh == 0 ? 0 : (th < S - 1 ? 1 : 2);
-        if (!cols.empty()) emit(cols, selfc, P, grp[range], all);
+        for (int sh = 0; sh < 2; ++sh)
+          if (h[sh].n > 0) sp.cols[sh].push_back(h[sh]);
       }
-    }
+    });
+    for (int64_t P = 0; P < npar; ++P)
+      for (int sh = 0; sh < 2; ++sh) {
+        const Split& sp = split[P];
+        const int range = sh == 0 ? 0 : (sp.th < S - 1 ? 1 : 2);
+        if (!sp.cols[sh].empty()) emit(sp.cols[sh], sp.selfc[sh], P, grp[range], all);
+      }
     std::vector<Part> parts;
     for (auto& g : grp) {
       std::stable_sort(g.begin(), g.end(), by_work);
@@ -1348,21 +1411,45 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
     return 0;
   }
   fits = true;
+  PhaseTimer tm;
   // counting sort by target, then each target's run by (code, source)
   const int64_t t0 = pl->own_lo[ps.level], nt = pl->own_hi[ps.level] - t0;
   std::vector<int64_t> ptr((size_t)nt + 1, 0);
-  for (const int2& q : ps.pairs_host) ptr[q.x - t0 + 1]++;
-  for (int64_t t = 0; t < nt; ++t) ptr[t + 1] += ptr[t];
   std::vector<int2> ent(ps.pairs_host.size());
   {
-    std::vector<int64_t> fillp(ptr.begin(), ptr.end() - 1);
-    for (int m = 0; m < ps.nmats; ++m) {
-      const int code = (mo[m][0] << 12) | ((mo[m][1] + OR) << 8) | ((mo[m][2] + OR) << 4) | (mo[m][3] + OR);
-      for (int k = ps.seg[m]; k < ps.seg[m + 1]; ++k) {
-        const int2 q = ps.pairs_host[k];
-        ent[fillp[q.x - t0]++] = make_int2(q.y, code);
+    // per-chunk counts per target, exclusive prefix over (target, chunk), then
+    // every chunk writes its pairs at its own positions (all cores, no atomics)
+    const size_t np = ps.pairs_host.size(), chunk = 1 << 16, nch = (np + chunk - 1) / chunk;
+    std::vector<int> code_of(ps.nmats);
+    std::vector<int> mat_of_chunk(nch + 1, 0);
+    for (int m = 0; m < ps.nmats; ++m)
+      code_of[m] = (mo[m][0] << 12) | ((mo[m][1] + OR) << 8) | ((mo[m][2] + OR) << 4) | (mo[m][3] + OR);
+    for (size_t c = 0; c < nch; ++c)
+      mat_of_chunk[c] = (int)(std::upper_bound(ps.seg.begin(), ps.seg.end(), (int)(c * chunk)) - ps.seg.begin()) - 1;
+    std::vector<std::vector<int64_t>> cnt(nch, std::vector<int64_t>((size_t)nt, 0));
+    parallel_for(nch, [&](size_t c) {
+      const size_t e = std::min(np, (c + 1) * chunk);
+      for (size_t k = c * chunk; k < e; ++k) cnt[c][ps.pairs_host[k].x - t0]++;
+    });
+    int64_t acc = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+      ptr[t] = acc;
+      for (size_t c = 0; c < nch; ++c) {
+        const int64_t v = cnt[c][t];
+        cnt[c][t] = acc;
+        acc += v;
       }
     }
+    ptr[nt] = acc;
+    parallel_for(nch, [&](size_t c) {
+      const size_t e = std::min(np, (c + 1) * chunk);
+      int m = mat_of_chunk[c];
+      for (size_t k = c * chunk; k < e; ++k) {
+        while ((int)k >= ps.seg[m + 1]) ++m;
+        const int2 q = ps.pairs_host[k];
+        ent[cnt[c][q.x - t0]++] = make_int2(q.y, code_of[m]);
+      }
+    });
   }
   parallel_for((size_t)nt, [&](size_t t) {
     std::sort(ent.begin() + ptr[t], ent.begin() + ptr[t + 1],
@@ -1378,11 +1465,13 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   });
   int64_t groups = 0;
   for (int64_t c : gcount) groups += c;
+  tm.mark("  separable: per-target runs");
   ps.sep_NO = NO;
   ps.sep_groups = groups;
   ps.sep_nblocks = 0;
   ps.sep_nitems = 0;
   if (sep_block_enabled(ps.to_y) && build_sep_blocks(pl, ps, ptr, ent)) return 1;
+  tm.mark("  separable: columns + parts");
   const int selfcode = (1 << 12) | (OR << 8) | (OR << 4) | OR;
   const int chunk = sep_chunk();
   std::vector<htlr::SepItem> items;

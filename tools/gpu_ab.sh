@@ -1,6 +1,4 @@
 export PYTHONPATH=$PWD
-export HTLR_GRAPHS=0
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_small.py > gpurun_out/memcheck.log 2>&1
-timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 20 python tools/sanitize_small.py > gpurun_out/racecheck.log 2>&1
-timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python tools/sanitize_small.py > gpurun_out/synccheck.log 2>&1
-tail -n 4 gpurun_out/memcheck.log gpurun_out/racecheck.log gpurun_out/synccheck.log
+HTLR_TIMING=1 python tools/quick_time.py cfg4 cfg5 cfg3 > gpurun_out/qt.log 2>&1
+python -m pytest tests/test_gpu_separable.py tests/test_gpu_parity.py tests/test_gpu_multi.py -x -q > gpurun_out/t.log 2>&1
+cat gpurun_out/qt.log | grep -v "^\[htlr timing\]   sep" ; tail -n 2 gpurun_out/t.log
