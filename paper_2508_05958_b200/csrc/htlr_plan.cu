@@ -2457,9 +2457,9 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   // u: the first slab, then the rest, on the copy stream
   CUDA_TRY(cudaEventRecord(ev[0], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[0], 0));
-  CUDA_TRY(cudaMemcpyAsync(us, uh, first * sizeof(double), cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaMemcpyAsync(us, uh, first * sizeof(double), cudaMemcpyDefault, cs));
   CUDA_TRY(cudaEventRecord(ev[1], cs));
-  CUDA_TRY(cudaMemcpyAsync(us + first, uh + first, rest * sizeof(double), cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaMemcpyAsync(us + first, uh + first, rest * sizeof(double), cudaMemcpyDefault, cs));
   CUDA_TRY(cudaEventRecord(ev[2], cs));
   htlr::ZeroList zl;
   for (const auto& ps : pl->passes) {
@@ -2527,14 +2527,14 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   ++cx.launches;
   CUDA_TRY(cudaEventRecord(ev[3], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(fh, fs, lead * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaMemcpyAsync(fh, fs, lead * sizeof(double), cudaMemcpyDefault, cs));
   leaf_range(2);
   htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, mz - zs,
                          mz);
   ++cx.launches;
   CUDA_TRY(cudaEventRecord(ev[4], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[4], 0));
-  CUDA_TRY(cudaMemcpyAsync(fh + lead, fs + lead, last * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CUDA_TRY(cudaMemcpyAsync(fh + lead, fs + lead, last * sizeof(double), cudaMemcpyDefault, cs));
   CUDA_TRY(cudaEventRecord(ev[5], cs));
   CUDA_TRY(cudaStreamWaitEvent(cx.st, ev[5], 0));
   CUDA_TRY(cudaGetLastError());
@@ -2557,13 +2557,17 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
   if (!u || !f) return fail(-1, "null vector");
   if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
-  if (!page_locked(u) || !page_locked(f)) return fail(-1, "host vectors must be page-locked (pinned or registered)");
+  // HTLR_HOST_DEVICE_OK=1 (timing experiments): device vectors through the
+  // same overlapped schedule
+  static const bool dev_ok = std::getenv("HTLR_HOST_DEVICE_OK") != nullptr;
+  if (!dev_ok && (!page_locked(u) || !page_locked(f)))
+    return fail(-1, "host vectors must be page-locked (pinned or registered)");
   const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
   if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;
   if (!overlap_ok(pl) || pl->profiling) {
-    CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyHostToDevice, cx.st));
+    CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDefault, cx.st));
     if (int rc = htlr_matvec(pl, pl->u_stage.d(), pl->f_stage.d(), nrhs, stream)) return rc;
-    CUDA_TRY(cudaMemcpyAsync(f, pl->f_stage.ptr, vbytes, cudaMemcpyDeviceToHost, cx.st));
+    CUDA_TRY(cudaMemcpyAsync(f, pl->f_stage.ptr, vbytes, cudaMemcpyDefault, cx.st));
     return 0;
   }
   for (auto& g : pl->host_graphs) {
