@@ -242,17 +242,23 @@ class ShardedOperator:
         bufs = self.exchange_buffers(R)
         L = _lib.lib()
         import torch.distributed as dist
-        overlap = (exchange is None and self.world > 1 and not self.reduce_buffers(R) and
-                   dist.get_backend(self.group) == "nccl")
+        overlap = exchange is None and self.world > 1 and not self.reduce_buffers(R)
         with torch.cuda.device(self.device):
             st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
             _lib.check(L.htlr_matvec_local(self.local._plan, ctypes.c_void_p(ud.data_ptr()), R, st))
             if overlap:
-                # the all-gather overlaps the blocks over own sources
-                works = allgather_chunks_async(bufs, self.rank, self.world, self.group)
-                self.remote_begin(ud, R)
-                for w in works:
-                    w.wait()
+                # the all-gather overlaps the blocks over own sources (NCCL:
+                # asynchronous collective; other backends: the same order,
+                # exchange in between -- the gloo harness runs this flow)
+                if dist.get_backend(self.group) == "nccl":
+                    works = allgather_chunks_async(bufs, self.rank, self.world, self.group)
+                    self.remote_begin(ud, R)
+                    for w in works:
+                        w.wait()
+                else:
+                    self.remote_begin(ud, R)
+                    torch.cuda.current_stream().synchronize()
+                    allgather_chunks(bufs, self.rank, self.world, self.group)
                 self.remote_finish(ud, fd, R)
             else:
                 if exchange is not None:
