@@ -314,6 +314,17 @@ PHASE_KERNELS = {
 }
 
 
+FORMULATION_NOTES = {
+    "separable": "tensor-product kernel (Gaussian): every reference block (Tucker core with its factors, or "
+                 "near block) is exactly a Kronecker product of three 8x8 per-axis factors and is applied as mode "
+                 "products -- the same operator as the reference's dense cores (1.5e-15 apart); "
+                 "HTLR_SEPARABLE=0 runs the dense-core GEMM path instead",
+    "dense": "deduplicated dense cores per (level, offset) and near blocks per offset, gathered fp64 "
+             "tensor-core GEMMs",
+    "regenerated": "mapped grid: cores and near blocks regenerated from the kernel inside the contraction",
+}
+
+
 def phase_roofline(key: str, flops: float, nbytes: float, ms: float) -> dict:
     """Roofline of one phase's launch: the binding resource is the larger of
     the compute time at the fp64 peak of the pipe the kernel runs on (DMMA
@@ -514,6 +525,7 @@ def run_b200(args):
                                    f"operator tables {rep.device_scalars * 8 / 1e9:.2f} GB "
                                    f"({'>' if rep.device_scalars * 8 > 126e6 else '<'} the 126 MB L2)",
                    "formulation": base_op.formulation(),
+                   "formulation_note": FORMULATION_NOTES.get(base_op.formulation(), ""),
                    "construct_s": construct_s, "parallelism": f"target subtrees x{world}" if world > 1 else "1 GPU",
                    "reference_storage_GB": rep.total_scalars * 8 / 1e9,
                    "device_storage_GB": rep.device_scalars * 8 / 1e9},
