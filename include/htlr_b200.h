@@ -203,6 +203,13 @@ int htlr_matvec_host(htlr_plan* plan, const double* u_host, double* f_host, int6
  * (blocks.py:126-227); negative on error. */
 int htlr_formulation(const htlr_plan* plan);
 
+/* Leaf-level pass of a separable plan: 0 = not separable (dense GEMM or
+ * regenerated passes), 1 = per-warp pair runs, 2 = cooperative per-parent
+ * CTAs, 3 = banded line sweeps (eta = 1 strong admissibility: the leaf lists'
+ * product-set structure, checked against the lists at construction).  All
+ * apply the reference's blocks (blocks.py:126-227); negative on error. */
+int htlr_leaf_pass(const htlr_plan* plan);
+
 /* storage_report equivalent (operators.py:175-197): scalars the reference
  * would store: [dense, factor, core, total]; plus what this plan stores
  * on the device after deduplication in out[4]. */

@@ -74,6 +74,7 @@ SYMBOLS = [
     ("htlr_export_block", ctypes.c_int, [_P, _I64, _P, _I64, _P, _I64, _P]),
     ("htlr_storage", ctypes.c_int, [_P, _P]),
     ("htlr_formulation", ctypes.c_int, [_P]),
+    ("htlr_leaf_pass", ctypes.c_int, [_P]),
     ("htlr_cell_average", ctypes.c_int, [_I32, _D, _D, _I32, _D, _I32, _I32, ctypes.c_int, ctypes.POINTER(_D)]),
     ("htlr_exact_rows", ctypes.c_int, [_P, _P, _I64, _P, _P, _P]),
     ("htlr_set_graphs", ctypes.c_int, [_P, _I32]),

@@ -207,6 +207,13 @@ void launch_sep_block(const double* tables, int nslots, int NO, const SepBlock* 
 void launch_sep_tables(const SepJob* jobs, int njobs, int p, int sL, double h, const KernelParams& kp,
                        const double* diag, double hd, double* corr_out, cudaStream_t st);
 size_t sep_smem_bytes(int nslots);
+// banded leaf pass (eta = 1 strong admissibility, htlr_sep.cu): three line
+// sweeps (sweep 0: z, ub -> six term buffers; 1: y, in place; 2: x, Y +=)
+size_t sep_band_smem_bytes(int NO, int L);
+int64_t sep_band_workspace(int L, int R);   // doubles
+cudaError_t sep_band_init(int NO, int L);
+void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
+                     double* ws, double* Y, const double* corr, double scale, cudaStream_t st);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,

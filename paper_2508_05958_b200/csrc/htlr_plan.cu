@@ -106,6 +106,8 @@ struct Pass {
   double sep_own_frac = 1.0;     // their share of the pass's (pair, box) work
   int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
+  bool band = false;             // leaf pass as banded line sweeps (sep_band_kernel)
+  double band_flops = 0;         // its algorithmic flop count per rhs (mode products it runs)
 };
 
 // HTLR_TIMING=1: wall-clock split of list building / construction on stderr
@@ -218,6 +220,7 @@ struct htlr_plan {
   bool merged = false;        // leaf-level admissible cores live in the leaf pass
   bool sep = false;           // separable-core formulation (tensor-product kernel, htlr_sep.cu)
   DevBuf sep_corr;            // self-block diagonal correction of the separable near field
+  DevBuf band_ws;             // banded leaf pass: six term buffers [term][leaf box][rhs][512]
   DevBuf diag, coeff, gl, ub, Y;
   DevBuf u_stage, f_stage;   // graph-replay staging vectors
   bool has_coeff = false;
@@ -513,6 +516,7 @@ int htlr_plan_destroy(htlr_plan* pl) {
     ps.sep_gcols.release();
   }
   pl->sep_corr.release();
+  pl->band_ws.release();
   pl->diag.release();
   pl->coeff.release();
   pl->gl.release();
@@ -1387,6 +1391,78 @@ static int sep_chunk() {
   return v > 0 ? v : 128;
 }
 
+// Banded leaf pass (sep_band_kernel, htlr_sep.cu): enabled only when every
+// leaf target's list (kind, offset) equals the product-set structure the
+// sweeps apply -- per axis R10 = {-4-c..5-c} minus the corner parents'
+// children A4^3, near = {-2..2}^3 minus {+-2}^3, inside the domain -- so the
+// sweeps apply exactly the listed blocks.  HTLR_SEP_BAND=0 keeps the
+// cooperative pass.
+static bool band_check(const htlr_plan* pl, const Pass& ps, int OR, const std::vector<int64_t>& ptr,
+                       const std::vector<int2>& ent, double& flops) {
+  const char* e = std::getenv("HTLR_SEP_BAND");
+  if (e && e[0] == '0') return false;
+  const int L = ps.level;
+  if (!ps.to_y || pl->shard_world != 1 || pl->d != 3 || L < 2 || L > 4) return false;
+  const int nb = 1 << L;
+  if (OR < std::min(5, nb - 1)) return false;   // the sweeps' in-domain offsets need table slots
+  const int64_t nt = (int64_t)ptr.size() - 1;
+  if (pl->own_lo[L] != 0 || nt != ((int64_t)1 << (3 * L))) return false;
+  std::atomic<bool> ok{true};
+  parallel_for((size_t)nt, [&](size_t t) {
+    if (!ok.load(std::memory_order_relaxed)) return;
+    int tc[3];
+    htlr::morton_decode((int64_t)t, 3, L, tc);
+    std::vector<int2> want;
+    for (int oz = -5; oz <= 5; ++oz)
+      for (int oy = -5; oy <= 5; ++oy)
+        for (int ox = -5; ox <= 5; ++ox) {
+          const int o[3] = {ox, oy, oz};
+          bool in10 = true, inA4 = true, in5 = true, corner = true;
+          int sc[3];
+          for (int a = 0; a < 3; ++a) {
+            const int c = tc[a] & 1;
+            sc[a] = tc[a] + o[a];
+            in10 = in10 && o[a] >= -4 - c && o[a] <= 5 - c;
+            inA4 = inA4 && (o[a] <= -3 - c || o[a] >= 4 - c);
+            in5 = in5 && o[a] >= -2 && o[a] <= 2;
+            corner = corner && (o[a] == -2 || o[a] == 2);
+          }
+          if (!in10 || inA4) continue;
+          if (sc[0] < 0 || sc[0] >= nb || sc[1] < 0 || sc[1] >= nb || sc[2] < 0 || sc[2] >= nb) continue;
+          const int kind = (in5 && !corner) ? 1 : 0;
+          const int code = (kind << 12) | ((ox + OR) << 8) | ((oy + OR) << 4) | (oz + OR);
+          want.push_back(make_int2((int)htlr::morton_encode(sc, 3, L), code));
+        }
+    std::vector<int2> got(ent.begin() + ptr[t], ent.begin() + ptr[t + 1]);
+    auto lt = [](const int2& a, const int2& b) { return a.y != b.y ? a.y < b.y : a.x < b.x; };
+    std::sort(want.begin(), want.end(), lt);
+    std::sort(got.begin(), got.end(), lt);
+    bool same = want.size() == got.size();
+    for (size_t k = 0; same && k < want.size(); ++k) same = want[k].x == got[k].x && want[k].y == got[k].y;
+    if (!same) ok.store(false);
+  });
+  if (!ok.load()) return false;
+  // mode products the three sweeps run (per rhs): per axis and box position q,
+  // the in-domain offsets of the six terms
+  const int cnt_lo[6] = {-4, -4, -2, -2, -2, -2};
+  (void)cnt_lo;
+  double per_line = 0;
+  for (int q = 0; q < nb; ++q) {
+    const int c = q & 1;
+    auto in = [&](int o) { return q + o >= 0 && q + o < nb; };
+    int k = 0;
+    for (int o = -4 - c; o <= 5 - c; ++o) k += in(o);
+    for (int o : {-4 - c, -3 - c, 4 - c, 5 - c}) k += in(o);
+    for (int rep = 0; rep < 2; ++rep) {
+      for (int o = -2; o <= 2; ++o) k += in(o);
+      for (int o : {-2, 2}) k += in(o);
+    }
+    per_line += k;
+  }
+  flops = 3.0 * (double)nb * nb * per_line * 2.0 * 4096.0;
+  return true;
+}
+
 // Per-target pair runs of one pass: (source, code) sorted by code, where code
 // packs (kind, o_x, o_y, o_z); returns 1 (and leaves the pass untouched) when
 // an axis offset does not fit the 4-bit code.
@@ -1470,6 +1546,8 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   ps.sep_groups = groups;
   ps.sep_nblocks = 0;
   ps.sep_nitems = 0;
+  ps.band = band_check(pl, ps, OR, ptr, ent, ps.band_flops);
+  tm.mark("  separable: banded-pass check");
   if (sep_block_enabled(ps.to_y) && build_sep_blocks(pl, ps, ptr, ent)) return 1;
   tm.mark("  separable: columns + parts");
   const int selfcode = (1 << 12) | (OR << 8) | (OR << 4) | OR;
@@ -1838,6 +1916,10 @@ static int ensure_workspace(htlr_plan* pl, int R) {
   const int64_t nleaf = pl->levels[pl->L].nclusters;
   if (pl->ub.alloc((size_t)nleaf * R * lp.K_pad * sizeof(double))) return 1;
   if (pl->Y.alloc((size_t)nleaf * R * lp.P * sizeof(double))) return 1;
+  if (pl->sep && lp.band) {
+    if (pl->band_ws.alloc((size_t)htlr::sep_band_workspace(lp.level, R) * sizeof(double))) return 1;
+    CUDA_TRY(htlr::sep_band_init(lp.sep_NO, lp.level));   // kernel attributes, outside any graph capture
+  }
   for (auto& ps : pl->passes) {
     if (ps.to_y) continue;
     Level& lv = pl->levels[ps.level];
@@ -2267,6 +2349,18 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       if (ps.sep_nblocks == 0 && own_only) continue;
       const double* B = ps.from_ub ? cx.ub : cx.W[i];
       double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
+      if (ps.band && !own_only && !rest_only) {
+        // banded leaf pass: three line sweeps; algorithmic work = the mode
+        // products they run; HBM bytes: ub, six term buffers written, read
+        // and rewritten, read, Y read and written
+        const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
+        if (cx.prof_begin(8, ps.level, ps.band_flops * R, nv * (2.0 + 6.0 * 4.0 + 2.0))) return 1;
+        for (int sw = 0; sw < 3; ++sw)
+          htlr::launch_sep_band(sw, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch,
+                                pl->band_ws.d(), C, pl->sep_corr.d(), pl->kp.scale, sst);
+        if (cx.prof_end()) return 1;
+        continue;
+      }
       // algorithmic work: 8^4 MAC per pair (mode z) + 2 * 8^4 per group
       // (modes x, y); HBM bytes: the level's source vectors and accumulators
       // once (the per-pair gathers are L2 traffic) + the factor tables
@@ -2432,6 +2526,7 @@ static bool overlap_ok(const htlr_plan* pl) {
   for (const auto& ps : pl->passes) {
     if (ps.sep_nblocks == 0) return false;
     if (ps.to_y && ps.sep_slabs == 0) return false;
+    if (ps.band) return false;   // the banded sweeps read whole lines of boxes
     // the slab prologues are launches of the fused prologue kernel
     if (!ps.to_y && htlr::upward_smem_words(pl->d, pl->levels[ps.level].side, pl->p) * sizeof(double) > 200 * 1024)
       return false;
@@ -3034,6 +3129,14 @@ int htlr_formulation(const htlr_plan* pl) {
   if (!pl) return fail(-1, "null plan");
   if (!pl->constructed) return fail(-1, "plan not constructed");
   return pl->mapped ? 2 : pl->sep ? 1 : 0;
+}
+
+int htlr_leaf_pass(const htlr_plan* pl) {
+  if (!pl) return fail(-1, "null plan");
+  if (!pl->constructed) return fail(-1, "plan not constructed");
+  if (!pl->sep || pl->mapped) return 0;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  return lp.band ? 3 : lp.sep_nblocks > 0 ? 2 : 1;
 }
 
 int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int64_t cap, double* factors,

@@ -440,6 +440,184 @@ __global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict
     }
 }
 
+// Banded leaf pass (strong admissibility, eta = 1, uniform grid): at the leaf
+// level every (target, source) pair is a child pair of an inadmissible parent
+// pair, so the offsets o = sigma - tau a target tau meets form product sets:
+// per axis o_a = 2 po_a + c'_a - c_a (po = parent offset in {-2..2}^3 minus the
+// 8 corners {+-2}^3, c / c' = child positions).  Per axis, with c = tau's
+// coordinate parity:
+//   all children of the parents:  R10 = {-4-c, ..., 5-c}   (minus the corner
+//                                  parents' children: A4 = {-4-c,-3-c,4-c,5-c})
+//   leaf near field:               R5  = {-2, ..., 2}        (minus {+-2}^3)
+// so, with K_S = sum_{o in S} M(o) shift(o) along one axis (M = the level's
+// admissible factor C or the near factor E, htlr_sep.cu header),
+//   Y = C10^3 - C4^3 - C5^3 + C2^3 + E5^3 - E2^3   (+ the self-block diagonal
+//       correction), X^3 = X_x X_y X_z.
+// Every term is a Kronecker product of three block-banded 1-D operators, so
+// the pass is three line sweeps (z, then y, then x) over lines of leaf boxes;
+// the same blocks as the reference's list (every pair's C(o_x) C(o_y) C(o_z) or
+// E(...)), summed in a different order.  The plan checks the leaf lists
+// against this structure before it enables the banded pass.
+//
+// sep_band_kernel<A, MODE>: one CTA per (line of nb boxes along axis A, rhs);
+// the line is staged in shared memory as [box][k = coordinate along A][n =
+// the other two, pitch 68] (B fragments bank-conflict free), warp w computes
+// boxes q = w, w + 16, ...: out[m][n] = sum_{b in S(q)} M(b - q)[m][k]
+// X_b[k][n] as 16 DMMA m8n8k4 per (q, b).  MODE 0: in = ub, out = the six
+// term buffers; MODE 1: term buffers in place; MODE 2: Y += scale * sum_t
+// sign_t term_t + corr * ub.
+__device__ __forceinline__ int band_count(int t) { return t == 0 ? 10 : (t == 1 || t == 3 || t == 5) ? ((t == 1) ? 4 : 2) : 5; }
+__device__ __forceinline__ int band_off(int t, int c, int i) {
+  switch (t) {
+    case 0: return -4 - c + i;
+    case 1: return i < 2 ? -4 - c + i : 2 - c + i;   // -4-c, -3-c, 4-c, 5-c
+    case 3:
+    case 5: return i ? 2 : -2;
+    default: return i - 2;                           // 2, 4: -2..2
+  }
+}
+
+constexpr int kBandTerms = 6;
+constexpr int kBandWarps = 16;
+
+// element e = x + 8 y + 64 z of a box -> (k, n) for a sweep along axis A
+template <int A>
+__device__ __forceinline__ int band_kn(int x, int y, int z) {
+  if (A == 2) return z * kSepZPitch + x + 8 * y;
+  if (A == 1) return y * kSepZPitch + x + 8 * z;
+  return x * kSepZPitch + y + 8 * z;
+}
+// output (m, n) -> natural element index
+template <int A>
+__device__ __forceinline__ int band_elem(int m, int n) {
+  if (A == 2) return n + 64 * m;
+  if (A == 1) return (n & 7) + 8 * m + 64 * (n >> 3);
+  return m + 8 * n;
+}
+
+template <int A, int MODE>
+__global__ void __launch_bounds__(kBandWarps * 32, 2)
+    sep_band_kernel(const double* __restrict__ tables, int NO, int L, int R, const double* __restrict__ ub,
+                    int ldub, int zpub, double* __restrict__ ws, int64_t term_stride, double* __restrict__ Y,
+                    const double* __restrict__ corr_ptr, double scale) {
+  extern __shared__ __align__(16) double sm[];
+  const int nb = 1 << L;
+  double* tab = sm;                          // [kind][offset] A fragments (64 doubles)
+  double* line = sm + 2 * NO * 64;           // [box][8][68]
+  const int r = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int OR = (NO - 1) / 2;
+  int lc[3];
+  {
+    const int l = blockIdx.x;
+    const int a1 = A == 0 ? 1 : 0, a2 = A == 2 ? 1 : 2;
+    lc[a1] = l % nb;
+    lc[a2] = l / nb;
+    lc[A] = 0;
+  }
+  for (int e = threadIdx.x; e < 2 * NO * 64; e += blockDim.x) tab[e] = tables[(e >> 6) * kSepSlot + (e & 63)];
+  __shared__ int64_t bids[16];
+  if (threadIdx.x < nb) {
+    int c[3] = {lc[0], lc[1], lc[2]};
+    c[A] = threadIdx.x;
+    bids[threadIdx.x] = morton_encode(c, 3, L);
+  }
+  __syncthreads();
+  auto box_id = [&](int q) { return bids[q]; };
+  auto stage = [&](const double* src, int64_t stride_box, int zp) {
+    for (int e = threadIdx.x; e < nb * 512; e += blockDim.x) {
+      const int q = e >> 9, i = e & 511;
+      const int x = i & 7, y = (i >> 3) & 7, z = i >> 6;
+      line[q * kSepBoxSmem + band_kn<A>(x, y, z)] = src[(box_id(q) * R + r) * stride_box + x + 8 * y + zp * z];
+    }
+  };
+  // one term's band product for box q into acc
+  auto apply = [&](int t, int q, double (&acc)[kSepP][2], double sg) {
+    const int kind = t >= 4 ? 1 : 0, c = q & 1, cnt = band_count(t);
+    const double* xs = line + (lane & 3) * kSepZPitch + (lane >> 2);
+    for (int i = 0; i < cnt; ++i) {
+      const int o = band_off(t, c, i), b = q + o;
+      if (b < 0 || b >= nb) continue;
+      const double* az = tab + (kind * NO + o + OR) * 64;
+      const double a0 = sg * az[lane], a1 = sg * az[32 + lane];
+      const double* xb = xs + b * kSepBoxSmem;
+      double xv[kSepP][2];
+#pragma unroll
+      for (int t8 = 0; t8 < kSepP; ++t8) {
+        xv[t8][0] = xb[8 * t8];
+        xv[t8][1] = xb[8 * t8 + 4 * kSepZPitch];
+      }
+#pragma unroll
+      for (int t8 = 0; t8 < kSepP; ++t8) dmma(acc[t8][0], acc[t8][1], a0, xv[t8][0]);
+#pragma unroll
+      for (int t8 = 0; t8 < kSepP; ++t8) dmma(acc[t8][0], acc[t8][1], a1, xv[t8][1]);
+    }
+  };
+  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  if (MODE == 0) {
+    stage(ub, ldub, zpub);
+    __syncthreads();
+    for (int q = warp; q < nb; q += kBandWarps) {
+      const int64_t ob = (box_id(q) * R + r) * 512;
+      for (int t = 0; t < kBandTerms; ++t) {
+        double acc[kSepP][2];
+#pragma unroll
+        for (int t8 = 0; t8 < kSepP; ++t8) acc[t8][0] = acc[t8][1] = 0.0;
+        apply(t, q, acc, 1.0);
+        double* o = ws + t * term_stride + ob;
+#pragma unroll
+        for (int t8 = 0; t8 < kSepP; ++t8) {
+          o[band_elem<A>(m, 8 * t8 + n0)] = acc[t8][0];
+          o[band_elem<A>(m, 8 * t8 + n0 + 1)] = acc[t8][1];
+        }
+      }
+    }
+    return;
+  }
+  double ya[(MODE == 2) ? 1 : 1][kSepP][2];
+  // MODE 2 keeps one accumulator per warp box; nb <= 16 boxes per line -> one box per warp
+  for (int q0 = 0; q0 < nb; q0 += kBandWarps) {
+    const int q = q0 + warp;
+#pragma unroll
+    for (int t8 = 0; t8 < kSepP; ++t8) ya[0][t8][0] = ya[0][t8][1] = 0.0;
+    for (int t = 0; t < kBandTerms; ++t) {
+      __syncthreads();   // previous term's readers are done with the line
+      stage(ws + t * term_stride, 512, 64);
+      __syncthreads();
+      if (q >= nb) continue;
+      if (MODE == 1) {
+        double acc[kSepP][2];
+#pragma unroll
+        for (int t8 = 0; t8 < kSepP; ++t8) acc[t8][0] = acc[t8][1] = 0.0;
+        apply(t, q, acc, 1.0);
+        double* o = ws + t * term_stride + (box_id(q) * R + r) * 512;
+#pragma unroll
+        for (int t8 = 0; t8 < kSepP; ++t8) {
+          o[band_elem<A>(m, 8 * t8 + n0)] = acc[t8][0];
+          o[band_elem<A>(m, 8 * t8 + n0 + 1)] = acc[t8][1];
+        }
+      } else {
+        // the term's sign folded into the A fragments: accumulate in place
+        apply(t, q, ya[0], (t == 1 || t == 2 || t == 5) ? -1.0 : 1.0);
+      }
+    }
+    if (MODE == 2 && q < nb) {
+      const int64_t bid = box_id(q);
+      double* o = Y + (bid * R + r) * 512;
+      const double* us = ub + (bid * R + r) * ldub;
+      const double cv = corr_ptr[0];
+#pragma unroll
+      for (int t8 = 0; t8 < kSepP; ++t8)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int e = band_elem<A>(m, 8 * t8 + n0 + jj);
+          const int x = e & 7, y = (e >> 3) & 7, z = e >> 6;
+          o[e] += fma(scale, ya[0][t8][jj], cv * __ldg(us + x + 8 * y + zpub * z));
+        }
+    }
+  }
+}
+
 }  // namespace
 
 bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
@@ -526,6 +704,42 @@ void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* i
   dim3 grid((nitems + kSepWarps - 1) / kSepWarps, R);
   sep_apply_kernel<<<grid, kSepWarps * 32, smem, st>>>(tables, nslots, NO, items, nitems, pairs, B, ldb, C, ldc, R,
                                                        corr, zpitch ? zpitch : 64);
+}
+
+
+size_t sep_band_smem_bytes(int NO, int L) {
+  return ((size_t)2 * NO * 64 + (size_t)(1 << L) * kSepBoxSmem) * sizeof(double);
+}
+
+int64_t sep_band_workspace(int L, int R) { return (int64_t)kBandTerms * ((int64_t)1 << (3 * L)) * R * 512; }
+
+cudaError_t sep_band_init(int NO, int L) {
+  const int smem = (int)sep_band_smem_bytes(NO, L);
+  cudaError_t e = cudaFuncSetAttribute(sep_band_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sep_band_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sep_band_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
+}
+
+template <int A, int MODE>
+static void launch_band_t(const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
+                          double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
+  const size_t smem = sep_band_smem_bytes(NO, L);
+  const int64_t tstride = ((int64_t)1 << (3 * L)) * R * 512;
+  sep_band_kernel<A, MODE><<<dim3(1u << (2 * L), R), kBandWarps * 32, smem, st>>>(tables, NO, L, R, ub, ldub, zpub,
+                                                                                   ws, tstride, Y, corr, scale);
+}
+
+void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
+                     double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
+  if (sweep == 0)
+    launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
+  else if (sweep == 1)
+    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
+  else
+    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
 }
 
 }  // namespace htlr

@@ -180,6 +180,17 @@ class HTLRMatrix:
             _lib.check(rc)
         return self.FORMULATIONS[rc]
 
+    LEAF_PASSES = ("gemm", "items", "cooperative", "banded")
+
+    def leaf_pass(self) -> str:
+        """How a separable plan runs its leaf level: "items" (per-warp pair
+        runs), "cooperative" (per-parent CTAs) or "banded" (three line sweeps
+        over the leaf grid, eta = 1); "gemm" for the other formulations."""
+        rc = _lib.lib().htlr_leaf_pass(self._plan)
+        if rc < 0:
+            _lib.check(rc)
+        return self.LEAF_PASSES[rc]
+
     def last_launch_count(self) -> int:
         return int(_lib.lib().htlr_last_launch_count(self._plan))
 

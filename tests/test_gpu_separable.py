@@ -129,11 +129,16 @@ np.save(sys.argv[1], H.matmat(op, U))
 """
 
 
-@pytest.mark.parametrize("env", [{"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "1"},
-                                 {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "9"},
-                                 {"HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "100000"},
-                                 {"HTLR_SEP_COLS": "1"}, {"HTLR_SEP_COLS": "7"}, {"HTLR_SEP_COLS": "1000"},
-                                 {"HTLR_SEP_GROUPS": "1"},
+_NB = {"HTLR_SEP_BAND": "0"}   # the cooperative / per-warp leaf passes instead of the banded sweeps
+
+
+@pytest.mark.parametrize("env", [{**_NB, "HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "1"},
+                                 {**_NB, "HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "9"},
+                                 {**_NB, "HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "100000"},
+                                 {**_NB, "HTLR_SEP_COLS": "1"}, {**_NB, "HTLR_SEP_COLS": "7"},
+                                 {**_NB, "HTLR_SEP_COLS": "1000"},
+                                 {**_NB, "HTLR_SEP_GROUPS": "1"},
+                                 {**_NB},
                                  {"HTLR_GRAPHS": "0"}])
 def test_separable_item_splits(tmp_path, env):
     """Leaf pass by per-warp items (cut at every group, at a few groups, or
@@ -270,3 +275,49 @@ def test_separable_random_sweep():
         for i, bx in enumerate(boxes):
             err = rel(F[O.box_linear_indices(n, bx)], rows[i])
             assert err <= TOL, (case, n, rule, eta, sig, scale, a, R, op.formulation(), err)
+
+
+_BAND_SCRIPT = r"""
+import sys
+import numpy as np
+import paper_2508_05958_b200 as H
+n, R, a = int(sys.argv[2]), int(sys.argv[3]), float(sys.argv[4])
+cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(1.0), kernel=H.gaussian(0.1, scale=1.3),
+                    coeff=H.CoefficientFn.constant(a))
+op = H.construct(cfg, H.UniformGrid(3, n))
+print(op.leaf_pass())
+U = np.random.default_rng(n + R).standard_normal((n ** 3, R))
+np.save(sys.argv[1], H.matmat(op, U))
+"""
+
+
+@pytest.mark.parametrize("n,R,a", [(32, 1, 0.5), (64, 3, 0.25), (128, 1, 0.0)])
+def test_banded_leaf_pass_equals_cooperative(tmp_path, n, R, a):
+    """The banded leaf pass (three line sweeps over the leaf grid: C10^3 -
+    C4^3 - C5^3 + C2^3 + E5^3 - E2^3, htlr_sep.cu) against the cooperative
+    per-pair pass (HTLR_SEP_BAND=0), each in its own process: the same blocks
+    summed in another order, so equal to rounding."""
+    outs = {}
+    for band in ("1", "0"):
+        out = tmp_path / f"f{band}.npy"
+        r = subprocess.run([sys.executable, "-c", _BAND_SCRIPT, str(out), str(n), str(R), str(a)], check=True,
+                           cwd=ROOT, capture_output=True, text=True,
+                           env={**os.environ, "PYTHONPATH": ROOT, "HTLR_SEP_BAND": band}, timeout=900)
+        kind = r.stdout.strip().splitlines()[-1]
+        assert kind == ("banded" if band == "1" else "cooperative")
+        outs[band] = np.load(out)
+    err = rel(outs["1"], outs["0"])
+    print(f"n={n} R={R} banded vs cooperative", err)
+    assert err <= 1e-13
+
+
+def test_banded_only_for_eta_one():
+    """Other admissibility rules break the product-set structure: the plan's
+    list check keeps the cooperative pass."""
+    for rule in (H.AdmissibilityRule.strong(2.0), H.AdmissibilityRule.weak()):
+        cfg = H.BuildConfig(rank=8, leaf_side=8, rule=rule, kernel=H.gaussian(0.1),
+                            coeff=H.CoefficientFn.constant(0.0))
+        op = H.construct(cfg, H.UniformGrid(3, 64))
+        assert op.leaf_pass() != "banded"
+    op = make(64)
+    assert op.leaf_pass() == "banded"
