@@ -211,9 +211,11 @@ size_t sep_smem_bytes(int nslots);
 // sweeps (sweep 0: z, ub -> six term buffers; 1: y, in place; 2: x, Y +=)
 size_t sep_band_smem_bytes(int NO, int L);
 int64_t sep_band_workspace(int L, int R);   // doubles
-cudaError_t sep_band_init(int NO, int L);
+cudaError_t sep_band_init();
+// nterms: 6 at the leaf level (admissible + near terms), 4 at a coupling
+// level (admissible terms only); corr may be null (no self-block correction)
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                     double* ws, double* Y, const double* corr, double scale, cudaStream_t st);
+                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,

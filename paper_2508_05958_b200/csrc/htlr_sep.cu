@@ -499,7 +499,7 @@ template <int A, int MODE>
 __global__ void __launch_bounds__(kBandWarps * 32, 2)
     sep_band_kernel(const double* __restrict__ tables, int NO, int L, int R, const double* __restrict__ ub,
                     int ldub, int zpub, double* __restrict__ ws, int64_t term_stride, double* __restrict__ Y,
-                    const double* __restrict__ corr_ptr, double scale) {
+                    const double* __restrict__ corr_ptr, double scale, int nterms) {
   extern __shared__ __align__(16) double sm[];
   const int nb = 1 << L;
   double* tab = sm;                          // [kind][offset] A fragments (64 doubles)
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
     __syncthreads();
     for (int q = warp; q < nb; q += kBandWarps) {
       const int64_t ob = (box_id(q) * R + r) * 512;
-      for (int t = 0; t < kBandTerms; ++t) {
+      for (int t = 0; t < nterms; ++t) {
         double acc[kSepP][2];
 #pragma unroll
         for (int t8 = 0; t8 < kSepP; ++t8) acc[t8][0] = acc[t8][1] = 0.0;
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
     const int q = q0 + warp;
 #pragma unroll
     for (int t8 = 0; t8 < kSepP; ++t8) ya[0][t8][0] = ya[0][t8][1] = 0.0;
-    for (int t = 0; t < kBandTerms; ++t) {
+    for (int t = 0; t < nterms; ++t) {
       __syncthreads();   // previous term's readers are done with the line
       stage(ws + t * term_stride, 512, 64);
       __syncthreads();
@@ -605,15 +605,125 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
       const int64_t bid = box_id(q);
       double* o = Y + (bid * R + r) * 512;
       const double* us = ub + (bid * R + r) * ldub;
-      const double cv = corr_ptr[0];
+      const double cv = corr_ptr ? corr_ptr[0] : 0.0;
 #pragma unroll
       for (int t8 = 0; t8 < kSepP; ++t8)
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
           const int e = band_elem<A>(m, 8 * t8 + n0 + jj);
           const int x = e & 7, y = (e >> 3) & 7, z = e >> 6;
-          o[e] += fma(scale, ya[0][t8][jj], cv * __ldg(us + x + 8 * y + zpub * z));
+          o[e] += corr_ptr ? fma(scale, ya[0][t8][jj], cv * __ldg(us + x + 8 * y + zpub * z)) : scale * ya[0][t8][jj];
         }
+    }
+  }
+}
+
+// sweeps y and x fused (sep_band_xy_kernel<NB>): the mode-y and mode-x
+// products mix only x and y, so one CTA per (z-point plane, rhs) stages the
+// plane of a term (NB^2 box cells of 8 x 8 points, [y][x] at a pitch of
+// 8 NB + 4 doubles: B fragments bank-conflict free along both axes), runs the
+// y sweep into registers (2 DMMA per (cell, source box)), writes it back in
+// place, runs the x sweep into the Y accumulator (term sign folded into the A
+// fragments) and moves to the next term; at the end Y += scale * acc +
+// corr * u.  NB = 16 at the leaf level of config 4: 128 CTAs of 32 warps, 8
+// cells per warp (16 registers per lane for each of the two accumulators).
+template <int NB>
+__host__ __device__ constexpr int band_xy_warps() { return NB >= 16 ? 32 : kBandWarps; }
+
+template <int NB>
+__global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
+    sep_band_xy_kernel(const double* __restrict__ tables, int NO, int L, int R, const double* __restrict__ ub,
+                       int ldub, int zpub, const double* __restrict__ ws, int64_t term_stride, double* __restrict__ Y,
+                       const double* __restrict__ corr_ptr, double scale, int nterms) {
+  constexpr int NW = band_xy_warps<NB>();
+  constexpr int CPW = NB * NB / NW;   // cells per warp (one row / column segment)
+  constexpr int SEG = NB / CPW;        // segments per row
+  constexpr int PITCH = 8 * NB + 4;
+  extern __shared__ __align__(16) double sm[];
+  double* tab = sm;
+  double* P = sm + 2 * NO * 64;
+  __shared__ int64_t bids[NB * NB];
+  const int r = blockIdx.y, zl = blockIdx.x & 7, bz = blockIdx.x >> 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int OR = (NO - 1) / 2;
+  for (int e = threadIdx.x; e < 2 * NO * 64; e += blockDim.x) tab[e] = tables[(e >> 6) * kSepSlot + (e & 63)];
+  for (int c = threadIdx.x; c < NB * NB; c += blockDim.x) {
+    const int cc[3] = {c % NB, c / NB, bz};
+    bids[c] = morton_encode(cc, 3, L);
+  }
+  double yacc[CPW][2];
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) yacc[i][0] = yacc[i][1] = 0.0;
+  const int kq = lane & 3, nq = lane >> 2;
+  for (int t = 0; t < nterms; ++t) {
+    __syncthreads();
+    {
+      const double* src = ws + t * term_stride + 64 * zl;
+#pragma unroll 4
+      for (int e = threadIdx.x; e < NB * NB * 64; e += blockDim.x) {
+        const int c = e >> 6, i = e & 63;
+        P[(8 * (c / NB) + (i >> 3)) * PITCH + 8 * (c % NB) + (i & 7)] = src[(bids[c] * R + r) * 512 + i];
+      }
+    }
+    __syncthreads();
+    const int kind = t >= 4 ? 1 : 0, cnt = band_count(t);
+    // y sweep: acc[y'][x] = sum_o My(o)[y'][y] T[8 (by + o) + y][8 bx + x];
+    // the warp's cells share by (a row segment), so one A fragment per offset
+    double acc[CPW][2];
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) acc[i][0] = acc[i][1] = 0.0;
+    {
+      const int by = warp / SEG, bx0 = (warp % SEG) * CPW;
+      const double* xb0 = P + kq * PITCH + 8 * bx0 + nq;
+      for (int j = 0; j < cnt; ++j) {
+        const int o = band_off(t, by & 1, j), b = by + o;
+        if (b < 0 || b >= NB) continue;
+        const double* az = tab + (kind * NO + o + OR) * 64;
+        const double a0 = az[lane], a1 = az[32 + lane];
+        const double* xb = xb0 + 8 * b * PITCH;
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) dmma(acc[i][0], acc[i][1], a0, xb[8 * i]);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) dmma(acc[i][0], acc[i][1], a1, xb[8 * i + 4 * PITCH]);
+      }
+      __syncthreads();
+      double* wb = P + (8 * by + nq) * PITCH + 8 * bx0 + 2 * kq;
+#pragma unroll
+      for (int i = 0; i < CPW; ++i) *reinterpret_cast<double2*>(wb + 8 * i) = make_double2(acc[i][0], acc[i][1]);
+    }
+    __syncthreads();
+    // x sweep: yacc[x'][y] += sg * sum_o Mx(o)[x'][x] U[8 by + y][8 (bx + o) + x];
+    // the warp's cells share bx (a column segment)
+    {
+      const double sg = (t == 1 || t == 2 || t == 5) ? -1.0 : 1.0;
+      const int bx = warp / SEG, by0 = (warp % SEG) * CPW;
+      const double* xb0 = P + (8 * by0 + nq) * PITCH + kq;
+      for (int j = 0; j < cnt; ++j) {
+        const int o = band_off(t, bx & 1, j), b = bx + o;
+        if (b < 0 || b >= NB) continue;
+        const double* az = tab + (kind * NO + o + OR) * 64;
+        const double a0 = sg * az[lane], a1 = sg * az[32 + lane];
+        const double* xb = xb0 + 8 * b;
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) dmma(yacc[i][0], yacc[i][1], a0, xb[8 * i * PITCH]);
+#pragma unroll
+        for (int i = 0; i < CPW; ++i) dmma(yacc[i][0], yacc[i][1], a1, xb[8 * i * PITCH + 4]);
+      }
+    }
+  }
+  // epilogue: lane holds (x' = nq, y = 2 kq + jj) of each cell (bx, by0 + i)
+  const double cv = corr_ptr ? corr_ptr[0] : 0.0;
+  const int bx = warp / SEG, by0 = (warp % SEG) * CPW;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int64_t bid = bids[(by0 + i) * NB + bx];
+    double* o = Y + (bid * R + r) * 512 + 64 * zl + nq + 16 * kq;
+    const double* us = ub + (bid * R + r) * ldub + zpub * zl + nq + 16 * kq;
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      double v = scale * yacc[i][jj];
+      if (corr_ptr) v = fma(cv, __ldg(us + 8 * jj), v);
+      o[8 * jj] += v;
     }
   }
 }
@@ -713,33 +823,68 @@ size_t sep_band_smem_bytes(int NO, int L) {
 
 int64_t sep_band_workspace(int L, int R) { return (int64_t)kBandTerms * ((int64_t)1 << (3 * L)) * R * 512; }
 
-cudaError_t sep_band_init(int NO, int L) {
-  const int smem = (int)sep_band_smem_bytes(NO, L);
-  cudaError_t e = cudaFuncSetAttribute(sep_band_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sep_band_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sep_band_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  return e;
-}
 
 template <int A, int MODE>
 static void launch_band_t(const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                          double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
+                          double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st) {
   const size_t smem = sep_band_smem_bytes(NO, L);
   const int64_t tstride = ((int64_t)1 << (3 * L)) * R * 512;
   sep_band_kernel<A, MODE><<<dim3(1u << (2 * L), R), kBandWarps * 32, smem, st>>>(tables, NO, L, R, ub, ldub, zpub,
-                                                                                   ws, tstride, Y, corr, scale);
+                                                                                   ws, tstride, Y, corr, scale,
+                                                                                   nterms);
+}
+
+size_t sep_band_xy_smem_bytes(int NO, int L) {
+  const int nb = 1 << L;
+  return ((size_t)2 * NO * 64 + (size_t)(8 * nb) * (8 * nb + 4)) * sizeof(double);
+}
+
+
+template <int NB>
+static void launch_band_xy_t(const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
+                             const double* ws, double* Y, const double* corr, double scale, int nterms,
+                             cudaStream_t st) {
+  const int64_t tstride = ((int64_t)1 << (3 * L)) * R * 512;
+  sep_band_xy_kernel<NB><<<dim3(8 * NB, R), band_xy_warps<NB>() * 32, sep_band_xy_smem_bytes(NO, L), st>>>(
+      tables, NO, L, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, nterms);
+}
+
+// HTLR_BAND_XY=0: separate y and x sweeps (sep_band_kernel modes 1, 2)
+static bool band_xy_fused() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HTLR_BAND_XY");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                     double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
-  if (sweep == 0)
-    launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
-  else if (sweep == 1)
-    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
-  else
-    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub ? zpub : 64, ws, Y, corr, scale, st);
+                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st) {
+  zpub = zpub ? zpub : 64;
+  if (sweep == 0) {
+    launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+  } else if (band_xy_fused()) {
+    if (sweep == 2) return;   // done by the fused launch of sweep 1
+    if (L == 4) launch_band_xy_t<16>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+    else if (L == 3) launch_band_xy_t<8>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+    else launch_band_xy_t<4>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+  } else if (sweep == 1) {
+    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+  } else {
+    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+  }
+}
+
+cudaError_t sep_band_init() {
+  const int smem = 200 * 1024;   // an upper bound (<= 227 KB minus static): occupancy follows each launch
+  cudaError_t e = cudaFuncSetAttribute(sep_band_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
 }
 
 }  // namespace htlr
