@@ -312,6 +312,12 @@ PHASE_KERNELS = {
     "sep_leaf": "sep_block_kernel (separable near + leaf-level cores: per-axis mode products, fp64 DMMA)",
     "upward": "upward_kernel", "downward": "downward_kernel", "permute": "permute_in_kernel",
 }
+# separable plans whose passes run as banded line sweeps (op.leaf_pass() == "banded")
+BANDED_KERNELS = {
+    "sep_leaf": "sep_band_kernel<z> + sep_band_xy_kernel (banded leaf pass: near + leaf-level cores as "
+                "C10^3 - C4^3 - C5^3 + C2^3 + E5^3 - E2^3 line sweeps, fp64 DMMA)",
+    "sep_level": "sep_band_kernel<z> + sep_band_xy_kernel (banded coupling pass, fp64 DMMA)",
+}
 
 
 FORMULATION_NOTES = {
@@ -469,6 +475,8 @@ def run_b200(args):
     flops_per_launch = dom["flops"] / dom["launches"]
     bytes_per_launch = dom["bytes"] / dom["launches"]
     peak = fp64_peak()
+    if base_op.formulation() == "separable" and base_op.leaf_pass() == "banded":
+        PHASE_KERNELS.update(BANDED_KERNELS)
     roofline = phase_roofline(dom_key, flops_per_launch, bytes_per_launch, avg_ms)
     roofline.update({
         "traffic": ncu_traffic(args.workload), "algorithmic_flops_per_launch": flops_per_launch,
@@ -524,7 +532,7 @@ def run_b200(args):
                    "nrhs": R, "l2": "flushed (512 MiB write) before every step, outside the timed bracket; "
                                    f"operator tables {rep.device_scalars * 8 / 1e9:.2f} GB "
                                    f"({'>' if rep.device_scalars * 8 > 126e6 else '<'} the 126 MB L2)",
-                   "formulation": base_op.formulation(),
+                   "formulation": base_op.formulation(), "leaf_pass": base_op.leaf_pass(),
                    "formulation_note": FORMULATION_NOTES.get(base_op.formulation(), ""),
                    "construct_s": construct_s, "parallelism": f"target subtrees x{world}" if world > 1 else "1 GPU",
                    "reference_storage_GB": rep.total_scalars * 8 / 1e9,

@@ -224,6 +224,22 @@ void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* i
 
 // downward pass by per-warp mode products when p = leaf side = 8 in 3-D on a
 // uniform grid (HTLR_DOWN8=0 keeps downward_kernel)
+// upward pass from the leaf boxes for p = leaf side = 8 in 3-D (htlr_sep.cu):
+// one warp per (leaf box, rhs), 8 x 8 factor slices per compressed level,
+// fp64 RED into W_l (zeroed beforehand); unsharded plans
+struct UpLevel8 {
+  int level;
+  const double* Q;   // side x 8 row-major
+  double* W;         // [cluster][R][K_pad], pitched z-planes
+  int K_pad, zpitch;
+};
+struct UpParams {
+  int nlev;
+  UpLevel8 lev[kMaxLevels];
+};
+bool upward8_supported(int d, int p, int sL);
+void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
+                    cudaStream_t st);
 bool downward8_supported(int d, int p, int sL, const DownParams& dp);
 // [zlo, zhi): leaf-box z range written (the overlapped host-vector matvec
 // writes f by z halves)

@@ -2261,6 +2261,38 @@ int mv_local(MvCtx& cx, const double* u) {
     zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
     cx.zeroed = zl.cnt <= htlr::kMaxLevels + 2;
   }
+  // separable plans (p = leaf side = 8): permute (+ zeroing, W_l included),
+  // then the upward pass of every level from the leaf boxes (upward8)
+  if (pl->shard_world == 1 && pl->sep && cx.zeroed && htlr::upward8_supported(d, p, pl->sL)) {
+    htlr::UpParams up{};
+    bool ok = true;
+    for (size_t i = 0; i < pl->passes.size() && ok; ++i) {
+      const Pass& ps = pl->passes[i];
+      if (ps.to_y) continue;
+      const Level& lv = pl->levels[ps.level];
+      if (lv.Kron.ptr || up.nlev >= htlr::kMaxLevels || zl.cnt >= htlr::kMaxLevels + 2 || ps.zpitch == 0) {
+        ok = false;
+        break;
+      }
+      up.lev[up.nlev++] = htlr::UpLevel8{lv.level, lv.Q.d(), cx.W[i], ps.K_pad, ps.zpitch};
+    }
+    if (ok && zl.cnt + up.nlev <= htlr::kMaxLevels + 2) {
+      for (int li = 0; li < up.nlev; ++li) {
+        zl.p[zl.cnt] = up.lev[li].W;
+        zl.n[zl.cnt++] = pl->levels[up.lev[li].level].nclusters * R * up.lev[li].K_pad;
+      }
+      if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N)) return 1;
+      htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, &zl, lp.zpitch);
+      if (cx.prof_end()) return 1;
+      // algorithmic work per (leaf box, level): 3 mode products of 8^4 MAC
+      const double flops = 2.0 * 3.0 * 4096.0 * (double)nb * R * up.nlev;
+      if (cx.prof_begin(1, pl->L - 1, flops, R8 * 512.0 * (double)nb)) return 1;
+      htlr::launch_upward8(cx.ub, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st);
+      if (cx.prof_end()) return 1;
+      cx.launches += 2;
+      return 0;
+    }
+  }
   // unprofiled unsharded matvec: permute + zeroing + every level's upward in
   // one launch (profiling keeps them apart so each phase is timed)
   if (cx.zeroed && !pl->profiling) {

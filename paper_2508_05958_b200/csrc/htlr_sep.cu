@@ -728,6 +728,79 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
   }
 }
 
+// Upward pass for p = leaf side = 8 in 3-D (the mirror of downward8): one
+// warp per (leaf box, rhs) reads the box from ub (pitched z-planes, the
+// layout the permute wrote) and, for every compressed level, applies the
+// transposed 8 x 8 slices of the level factor at the box's position in its
+// ancestor (W_l = (Q_z (x) Q_y (x) Q_x)^T u over the cluster's points,
+// upward_body / blocks.py:239-247, split over the ancestor's leaf boxes):
+// mode z and mode x on the tensor pipe, mode y on DFMA, then one fp64 RED per
+// entry into W_l[ancestor] (zeroed by the permute launch).
+__global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L, int R,
+                                                       UpParams up, int64_t nb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wi >= nb * R) return;
+  const int64_t b = wi / R;
+  const int r = (int)(wi % R);
+  int bc[3];
+  morton_decode(b, 3, L, bc);
+  const int g = lane >> 2, q = lane & 3;
+  // B fragments of mode z: X[a = g, t, c = 4 ks + q]
+  double xv[kSepP][2];
+  {
+    const double* s = ub + (b * R + r) * (int64_t)ldub + g + zpub * q;
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      xv[t][0] = __ldg(s + 8 * t);
+      xv[t][1] = __ldg(s + 8 * t + 4 * zpub);
+    }
+  }
+  for (int li = 0; li < up.nlev; ++li) {
+    const UpLevel8 lv = up.lev[li];
+    const int shift = L - lv.level, mask = (1 << shift) - 1;
+    const int64_t anc = b >> (3 * shift);
+    const double* Qx = lv.Q + (int64_t)((bc[0] & mask) * kSepP) * kSepP;
+    const double* Qy = lv.Q + (int64_t)((bc[1] & mask) * kSepP) * kSepP;
+    const double* Qz = lv.Q + (int64_t)((bc[2] & mask) * kSepP) * kSepP;
+    // mode z: Z_t[k', a] = sum_c Qz[c][k'] X[a, t, c]  (A[m = k'][k = c] = Qz[c][k'])
+    double z[kSepP][2];
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) z[t][0] = z[t][1] = 0.0;
+    const double az0 = __ldg(Qz + q * kSepP + g), az1 = __ldg(Qz + (4 + q) * kSepP + g);
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az0, xv[t][0]);
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az1, xv[t][1]);
+    // mode x (C fragment reused as B, k order permuted): T_t[i, k'] =
+    // sum_a Qx[a][i] Z_t[k', a], A[m = i][k = 2 q + ks] = Qx[2 q + ks][i]
+    const double bx0 = __ldg(Qx + (2 * q) * kSepP + g), bx1 = __ldg(Qx + (2 * q + 1) * kSepP + g);
+    double y[kSepP][2];
+#pragma unroll
+    for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      double t0 = 0.0, t1 = 0.0;
+      dmma(t0, t1, bx0, z[t][0]);
+      dmma(t0, t1, bx1, z[t][1]);
+      // mode y: W[i, j, k'] += Qy[t][j] T_t[i, k']
+#pragma unroll
+      for (int j = 0; j < kSepP; ++j) {
+        const double m = __ldg(Qy + t * kSepP + j);
+        y[j][0] = fma(m, t0, y[j][0]);
+        y[j][1] = fma(m, t1, y[j][1]);
+      }
+    }
+    // lane holds (i = g, j, k' = 2 q + jj)
+    double* o = lv.W + (anc * R + r) * (int64_t)lv.K_pad + g + lv.zpitch * 2 * q;
+#pragma unroll
+    for (int j = 0; j < kSepP; ++j) {
+      atomicAdd(o + 8 * j, y[j][0]);
+      atomicAdd(o + 8 * j + lv.zpitch, y[j][1]);
+    }
+  }
+}
+
 }  // namespace
 
 bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
@@ -740,6 +813,22 @@ bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
   for (int i = 0; i < dp.nlev; ++i)
     if (dp.lev[i].K || dp.lev[i].qstride || dp.lev[i].P != kSepP * kSepP * kSepP) return false;
   return true;
+}
+
+bool upward8_supported(int d, int p, int sL) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = std::getenv("HTLR_UP8");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  return !off && d == 3 && p == kSepP && sL == kSepP;
+}
+
+void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
+                    cudaStream_t st) {
+  const int64_t warps = nb * R;
+  if (warps <= 0 || up.nlev == 0) return;
+  upward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb);
 }
 
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
