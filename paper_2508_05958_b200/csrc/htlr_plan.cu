@@ -2277,19 +2277,30 @@ int mv_local(MvCtx& cx, const double* u) {
       up.lev[up.nlev++] = htlr::UpLevel8{lv.level, lv.Q.d(), cx.W[i], ps.K_pad, ps.zpitch};
     }
     if (ok && zl.cnt + up.nlev <= htlr::kMaxLevels + 2) {
+      // accumulators: W_l (RED targets of upward8) and those of the passes
+      // that accumulate (the banded passes store every entry)
+      htlr::ZeroList z2;
       for (int li = 0; li < up.nlev; ++li) {
-        zl.p[zl.cnt] = up.lev[li].W;
-        zl.n[zl.cnt++] = pl->levels[up.lev[li].level].nclusters * R * up.lev[li].K_pad;
+        z2.p[z2.cnt] = up.lev[li].W;
+        z2.n[z2.cnt++] = pl->levels[up.lev[li].level].nclusters * R * up.lev[li].K_pad;
       }
-      if (cx.prof_begin(0, pl->L, 0.0, 2.0 * R8 * (double)pl->N)) return 1;
-      htlr::launch_permute_in(u, cx.ub, d, pl->n, pl->sL, R, lp.K_pad, b0, nb, cx.st, &zl, lp.zpitch);
-      if (cx.prof_end()) return 1;
-      // algorithmic work per (leaf box, level): 3 mode products of 8^4 MAC
+      {
+        int q = 0;
+        for (const auto& ps : pl->passes) {
+          if (ps.to_y) continue;
+          if (!ps.band) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
+          ++q;
+        }
+        if (!lp.band) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
+      }
+      for (int q = 0; q < z2.cnt; ++q) CUDA_TRY(cudaMemsetAsync(z2.p[q], 0, (size_t)z2.n[q] * sizeof(double), cx.st));
+      // permute fused into the upward launch: algorithmic work per (leaf box,
+      // level) 3 mode products of 8^4 MAC; bytes u read + ub written
       const double flops = 2.0 * 3.0 * 4096.0 * (double)nb * R * up.nlev;
-      if (cx.prof_begin(1, pl->L - 1, flops, R8 * 512.0 * (double)nb)) return 1;
-      htlr::launch_upward8(cx.ub, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st);
+      if (cx.prof_begin(1, pl->L - 1, flops, 2.0 * R8 * (double)pl->N)) return 1;
+      htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n);
       if (cx.prof_end()) return 1;
-      cx.launches += 2;
+      cx.launches += 1;
       return 0;
     }
   }

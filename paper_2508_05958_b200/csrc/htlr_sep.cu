@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
         for (int jj = 0; jj < 2; ++jj) {
           const int e = band_elem<A>(m, 8 * t8 + n0 + jj);
           const int x = e & 7, y = (e >> 3) & 7, z = e >> 6;
-          o[e] += corr_ptr ? fma(scale, ya[0][t8][jj], cv * __ldg(us + x + 8 * y + zpub * z)) : scale * ya[0][t8][jj];
+          o[e] = corr_ptr ? fma(scale, ya[0][t8][jj], cv * __ldg(us + x + 8 * y + zpub * z)) : scale * ya[0][t8][jj];
         }
     }
   }
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
     for (int jj = 0; jj < 2; ++jj) {
       double v = scale * yacc[i][jj];
       if (corr_ptr) v = fma(cv, __ldg(us + 8 * jj), v);
-      o[8 * jj] += v;
+      o[8 * jj] = v;   // every entry of the level's accumulator is written here once
     }
   }
 }
@@ -737,7 +737,8 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
 // mode z and mode x on the tensor pipe, mode y on DFMA, then one fp64 RED per
 // entry into W_l[ancestor] (zeroed by the permute launch).
 __global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L, int R,
-                                                       UpParams up, int64_t nb) {
+                                                       UpParams up, int64_t nb, const double* __restrict__ u,
+                                                       double* __restrict__ ub_out, int n) {
   const int lane = threadIdx.x & 31;
   const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wi >= nb * R) return;
@@ -748,7 +749,19 @@ __global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__
   const int g = lane >> 2, q = lane & 3;
   // B fragments of mode z: X[a = g, t, c = 4 ks + q]
   double xv[kSepP][2];
-  {
+  if (u) {
+    // fused permute: the box's points from the F-order vector, written to ub
+    const int64_t g0 = (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP) +
+                       (int64_t)n * n * (bc[2] * kSepP + q);
+    double* d = ub_out + (b * R + r) * (int64_t)ldub + g + zpub * q;
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) {
+      xv[t][0] = __ldg(u + (g0 + (int64_t)n * t) * R + r);
+      xv[t][1] = __ldg(u + (g0 + (int64_t)n * t + (int64_t)n * n * 4) * R + r);
+      d[8 * t] = xv[t][0];
+      d[8 * t + 4 * zpub] = xv[t][1];
+    }
+  } else {
     const double* s = ub + (b * R + r) * (int64_t)ldub + g + zpub * q;
 #pragma unroll
     for (int t = 0; t < kSepP; ++t) {
@@ -825,10 +838,11 @@ bool upward8_supported(int d, int p, int sL) {
 }
 
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
-                    cudaStream_t st) {
+                    cudaStream_t st, const double* u, double* ub_out, int n) {
   const int64_t warps = nb * R;
-  if (warps <= 0 || up.nlev == 0) return;
-  upward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb);
+  if (warps <= 0 || (up.nlev == 0 && !u)) return;
+  upward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb, u, ub_out,
+                                                               n);
 }
 
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
