@@ -555,7 +555,19 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
   };
   const int m = lane >> 2, n0 = 2 * (lane & 3);
   if (MODE == 0) {
-    stage(ub, ldub, zpub);
+    if (A == 2 && zpub == kSepZPitch && ldub == kSepBoxSmem) {
+      // pitched boxes are already in the z-sweep's staging layout: 16-byte
+      // asynchronous copies of the whole box
+      for (int e = threadIdx.x; e < nb * (kSepBoxSmem / 2); e += blockDim.x) {
+        const int q = e / (kSepBoxSmem / 2), i = 2 * (e % (kSepBoxSmem / 2));
+        const double* g = ub + (box_id(q) * R + r) * (int64_t)ldub + i;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(line + q * kSepBoxSmem + i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g) : "memory");
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else {
+      stage(ub, ldub, zpub);
+    }
     __syncthreads();
     for (int q = warp; q < nb; q += kBandWarps) {
       const int64_t ob = (box_id(q) * R + r) * 512;
@@ -567,8 +579,12 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
         double* o = ws + t * term_stride + ob;
 #pragma unroll
         for (int t8 = 0; t8 < kSepP; ++t8) {
-          o[band_elem<A>(m, 8 * t8 + n0)] = acc[t8][0];
-          o[band_elem<A>(m, 8 * t8 + n0 + 1)] = acc[t8][1];
+          if (A == 2) {   // n, n + 1 adjacent in memory
+            *reinterpret_cast<double2*>(o + band_elem<A>(m, 8 * t8 + n0)) = make_double2(acc[t8][0], acc[t8][1]);
+          } else {
+            o[band_elem<A>(m, 8 * t8 + n0)] = acc[t8][0];
+            o[band_elem<A>(m, 8 * t8 + n0 + 1)] = acc[t8][1];
+          }
         }
       }
     }
@@ -658,12 +674,15 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
   for (int t = 0; t < nterms; ++t) {
     __syncthreads();
     {
+      // asynchronous 16-byte copies: every load of the plane in flight at once
       const double* src = ws + t * term_stride + 64 * zl;
-#pragma unroll 4
-      for (int e = threadIdx.x; e < NB * NB * 64; e += blockDim.x) {
-        const int c = e >> 6, i = e & 63;
-        P[(8 * (c / NB) + (i >> 3)) * PITCH + 8 * (c % NB) + (i & 7)] = src[(bids[c] * R + r) * 512 + i];
+      for (int e = threadIdx.x; e < NB * NB * 32; e += blockDim.x) {
+        const int c = e >> 5, i = 2 * (e & 31);
+        const double* g = src + (bids[c] * R + r) * 512 + i;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(P + (8 * (c / NB) + (i >> 3)) * PITCH + 8 * (c % NB) + (i & 7));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g) : "memory");
       }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
     __syncthreads();
     const int kind = t >= 4 ? 1 : 0, cnt = band_count(t);
