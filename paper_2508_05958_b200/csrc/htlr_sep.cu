@@ -758,17 +758,26 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
 __global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L, int R,
                                                        UpParams up, int64_t nb, const double* __restrict__ u,
                                                        double* __restrict__ ub_out, int n) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wi >= nb * R) return;
-  const int64_t b = wi / R;
-  const int r = (int)(wi % R);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  // rhs-major: the CTA's 8 warps are the 8 leaf boxes of one parent (Morton
+  // order) for one rhs, so their contributions are summed in shared memory
+  // and each W_l entry gets one RED per CTA instead of eight
+  const bool valid = wi < nb * R;
+  const int64_t b = valid ? wi % nb : 0;
+  const int r = valid ? (int)(wi / nb) : 0;
+  __shared__ double red[8][512];
+  const bool cta_red = (nb % 8) == 0 && blockDim.x == 256;
+  if (!valid && !cta_red) return;
   int bc[3];
   morton_decode(b, 3, L, bc);
   const int g = lane >> 2, q = lane & 3;
   // B fragments of mode z: X[a = g, t, c = 4 ks + q]
   double xv[kSepP][2];
-  if (u) {
+  if (!valid) {
+#pragma unroll
+    for (int t = 0; t < kSepP; ++t) xv[t][0] = xv[t][1] = 0.0;
+  } else if (u) {
     // fused permute: the box's points from the F-order vector, written to ub
     const int64_t g0 = (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP) +
                        (int64_t)n * n * (bc[2] * kSepP + q);
@@ -824,11 +833,29 @@ __global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__
       }
     }
     // lane holds (i = g, j, k' = 2 q + jj)
-    double* o = lv.W + (anc * R + r) * (int64_t)lv.K_pad + g + lv.zpitch * 2 * q;
+    if (cta_red) {
+      __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kSepP; ++j) {
-      atomicAdd(o + 8 * j, y[j][0]);
-      atomicAdd(o + 8 * j + lv.zpitch, y[j][1]);
+      for (int j = 0; j < kSepP; ++j) {
+        red[warp][g + 8 * j + 128 * q] = y[j][0];
+        red[warp][g + 8 * j + 128 * q + 64] = y[j][1];
+      }
+      __syncthreads();
+      const int64_t b0 = (wi - warp) % nb;   // the CTA's first box (same parent)
+      const int64_t anc0 = b0 >> (3 * shift);
+      for (int e = threadIdx.x; e < 512; e += blockDim.x) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[w][e];
+        atomicAdd(lv.W + (anc0 * R + r) * (int64_t)lv.K_pad + (e & 63) + lv.zpitch * (e >> 6), v);
+      }
+    } else {
+      double* o = lv.W + (anc * R + r) * (int64_t)lv.K_pad + g + lv.zpitch * 2 * q;
+#pragma unroll
+      for (int j = 0; j < kSepP; ++j) {
+        atomicAdd(o + 8 * j, y[j][0]);
+        atomicAdd(o + 8 * j + lv.zpitch, y[j][1]);
+      }
     }
   }
 }
