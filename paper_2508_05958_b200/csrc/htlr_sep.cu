@@ -377,7 +377,7 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
 // mode-product chain as the separable passes (mode z, mode x on the tensor
 // pipe, mode y on DFMA), applied to H[ancestor]; then f = acc + Y + a u,
 // written back in F-order (operators.py:153-156).
-__global__ void __launch_bounds__(256) downward8_kernel(const double* __restrict__ u, double* __restrict__ f,
+__global__ void __launch_bounds__(256, 4) downward8_kernel(const double* __restrict__ u, double* __restrict__ f,
                                                          const double* __restrict__ Y, const double* __restrict__ avec,
                                                          double aconst, int n, int L, int R, DownParams dp, int64_t b0,
                                                          int64_t nb, int zlo, int zhi) {
