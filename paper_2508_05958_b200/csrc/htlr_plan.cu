@@ -2374,6 +2374,24 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
     for (auto& ev : pl->side_ev)
       if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  // banded leaf pass (HTLR_BAND_LATE_FORK, default on): its z sweep first,
+  // then the fork, so the level passes fill the SMs the y-x sweep leaves idle
+  // (128 planes on 148 SMs) instead of delaying the z sweep
+  bool leaf_z_done = false;
+  if (fork && !own_only && !rest_only) {
+    static const bool late = [] {
+      const char* e = std::getenv("HTLR_BAND_LATE_FORK");
+      return !(e && e[0] == '0');
+    }();
+    const Pass& lq = pl->passes[pl->leaf_pass];
+    if (late && pl->sep && lq.band) {
+      htlr::launch_sep_band(0, lq.sep_tab.d(), lq.sep_NO, lq.level, R, cx.ub, lq.K_pad, lq.zpitch, lq.band_ws.d(),
+                            pl->Y.d(), pl->sep_corr.d(), pl->kp.scale, 6, cx.st);
+      leaf_z_done = true;
+    }
+  }
+  if (fork) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
     CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
   }
@@ -2401,7 +2419,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
         const double nterm = ps.to_y ? 6.0 : 4.0;
         if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, ps.band_flops * R, nv * (1.0 + 2.0 * nterm + 2.0))) return 1;
-        for (int sw = 0; sw < 3; ++sw)
+        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw)
           htlr::launch_sep_band(sw, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C,
                                 ps.to_y ? pl->sep_corr.d() : nullptr, pl->kp.scale, ps.to_y ? 6 : 4, sst);
         if (cx.prof_end()) return 1;
