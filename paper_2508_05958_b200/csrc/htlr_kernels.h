@@ -214,8 +214,12 @@ int64_t sep_band_workspace(int L, int R);   // doubles
 cudaError_t sep_band_init();
 // nterms: 6 at the leaf level (admissible + near terms), 4 at a coupling
 // level (admissible terms only); corr may be null (no self-block correction)
+// lo / hi: the own target boxes (a box region; the whole level unsharded):
+// the z sweep runs the lines within 5 boxes of it in x and y and outputs its
+// z range, the y-x sweep its z planes, storing only its cells
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st);
+                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
+                     const int* lo, const int* hi);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
@@ -232,6 +236,9 @@ struct UpLevel8 {
   const double* Q;   // side x 8 row-major
   double* W;         // [cluster][R][K_pad], pitched z-planes
   int K_pad, zpitch;
+};
+struct BandRegion {
+  int lo[3], hi[3];
 };
 struct UpParams {
   int nlev;

@@ -109,6 +109,7 @@ struct Pass {
   bool band = false;             // pass as banded line sweeps (sep_band_kernel)
   DevBuf band_ws;                // its term buffers [term][box][rhs][512]
   double band_flops = 0;         // its algorithmic flop count per rhs (mode products it runs)
+  int band_lo[3] = {0, 0, 0}, band_hi[3] = {0, 0, 0};   // own target boxes (a box region of the level)
 };
 
 // HTLR_TIMING=1: wall-clock split of list building / construction on stderr
@@ -1397,22 +1398,33 @@ static int sep_chunk() {
 // children A4^3, near = {-2..2}^3 minus {+-2}^3, inside the domain -- so the
 // sweeps apply exactly the listed blocks.  HTLR_SEP_BAND=0 keeps the
 // cooperative pass.
-static bool band_check(const htlr_plan* pl, const Pass& ps, int OR, const std::vector<int64_t>& ptr,
+static bool band_check(const htlr_plan* pl, Pass& ps, int OR, const std::vector<int64_t>& ptr,
                        const std::vector<int2>& ent, double& flops) {
   const char* e = std::getenv("HTLR_SEP_BAND");
   if (e && e[0] == '0') return false;
   const int L = ps.level;
   // L >= 3: on coarser grids the cooperative pass is faster (n = 32: 0.05 vs 0.07 ms)
-  if (pl->shard_world != 1 || pl->d != 3 || L < 3 || L > 4) return false;
+  if (pl->d != 3 || L < 3 || L > 4) return false;
   const int nb = 1 << L;
   if (OR < std::min(5, nb - 1)) return false;   // the sweeps' in-domain offsets need table slots
-  const int64_t nt = (int64_t)ptr.size() - 1;
-  if (pl->own_lo[L] != 0 || nt != ((int64_t)1 << (3 * L))) return false;
+  const int64_t nt = (int64_t)ptr.size() - 1, t0 = pl->own_lo[L];
+  if (nt <= 0) return false;
+  // own targets (sharded plans: Morton subtrees) must form a box region
+  int lo[3] = {nb, nb, nb}, hi[3] = {0, 0, 0};
+  for (int64_t t = 0; t < nt; ++t) {
+    int tc[3];
+    htlr::morton_decode(t0 + t, 3, L, tc);
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], tc[a]);
+      hi[a] = std::max(hi[a], tc[a] + 1);
+    }
+  }
+  if ((int64_t)(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]) != nt) return false;
   std::atomic<bool> ok{true};
   parallel_for((size_t)nt, [&](size_t t) {
     if (!ok.load(std::memory_order_relaxed)) return;
     int tc[3];
-    htlr::morton_decode((int64_t)t, 3, L, tc);
+    htlr::morton_decode(t0 + (int64_t)t, 3, L, tc);
     std::vector<int2> want;
     for (int oz = -5; oz <= 5; ++oz)
       for (int oy = -5; oy <= 5; ++oy)
@@ -1460,7 +1472,12 @@ static bool band_check(const htlr_plan* pl, const Pass& ps, int OR, const std::v
     }
     per_line += k;
   }
-  flops = 3.0 * (double)nb * nb * per_line * 2.0 * 4096.0;
+  // per rhs, the region's share of the sweeps (halo lines of the z sweep not counted)
+  flops = 3.0 * (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * L));
+  for (int a = 0; a < 3; ++a) {
+    ps.band_lo[a] = lo[a];
+    ps.band_hi[a] = hi[a];
+  }
   return true;
 }
 
@@ -2387,7 +2404,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     const Pass& lq = pl->passes[pl->leaf_pass];
     if (late && pl->sep && lq.band) {
       htlr::launch_sep_band(0, lq.sep_tab.d(), lq.sep_NO, lq.level, R, cx.ub, lq.K_pad, lq.zpitch, lq.band_ws.d(),
-                            pl->Y.d(), pl->sep_corr.d(), pl->kp.scale, 6, cx.st);
+                            pl->Y.d(), pl->sep_corr.d(), pl->kp.scale, 6, cx.st, lq.band_lo, lq.band_hi);
       leaf_z_done = true;
     }
   }
@@ -2400,6 +2417,24 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     const cudaStream_t sst = (fork && !ps.to_y) ? pl->side_stream : cx.st;
     if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
+      if (ps.band && own_only) continue;   // the sweeps need every (gathered) source box
+      if (ps.band) {
+        const double* B = cx.ub;   // the banded passes are built for the leaf level and level passes alike
+        if (!ps.from_ub) B = cx.W[i];
+        double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
+        // banded pass: a z sweep and the fused y-x sweep; algorithmic work =
+        // the mode products they run; HBM bytes: the source vectors, the term
+        // buffers written and read back, the accumulator read and written
+        const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
+        const double nterm = ps.to_y ? 6.0 : 4.0;
+        if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, ps.band_flops * R, nv * (1.0 + 2.0 * nterm + 2.0))) return 1;
+        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw)
+          htlr::launch_sep_band(sw, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C,
+                                ps.to_y ? pl->sep_corr.d() : nullptr, pl->kp.scale, ps.to_y ? 6 : 4, sst,
+                                ps.band_lo, ps.band_hi);
+        if (cx.prof_end()) return 1;
+        continue;
+      }
       if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;
       // part range of this stage (per-warp items: everything in the rest stage)
       int b0 = 0, nbk = ps.sep_nblocks;
@@ -2412,19 +2447,6 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       if (ps.sep_nblocks == 0 && own_only) continue;
       const double* B = ps.from_ub ? cx.ub : cx.W[i];
       double* C = ps.to_y ? pl->Y.d() : pl->levels[ps.level].H.d();
-      if (ps.band && !own_only && !rest_only) {
-        // banded pass: a z sweep and the fused y-x sweep; algorithmic work =
-        // the mode products they run; HBM bytes: the source vectors, the term
-        // buffers written and read back, the accumulator read and written
-        const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
-        const double nterm = ps.to_y ? 6.0 : 4.0;
-        if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, ps.band_flops * R, nv * (1.0 + 2.0 * nterm + 2.0))) return 1;
-        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw)
-          htlr::launch_sep_band(sw, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C,
-                                ps.to_y ? pl->sep_corr.d() : nullptr, pl->kp.scale, ps.to_y ? 6 : 4, sst);
-        if (cx.prof_end()) return 1;
-        continue;
-      }
       // algorithmic work: 8^4 MAC per pair (mode z) + 2 * 8^4 per group
       // (modes x, y); HBM bytes: the level's source vectors and accumulators
       // once (the per-pair gathers are L2 traffic) + the factor tables

@@ -499,7 +499,7 @@ template <int A, int MODE>
 __global__ void __launch_bounds__(kBandWarps * 32, 2)
     sep_band_kernel(const double* __restrict__ tables, int NO, int L, int R, const double* __restrict__ ub,
                     int ldub, int zpub, double* __restrict__ ws, int64_t term_stride, double* __restrict__ Y,
-                    const double* __restrict__ corr_ptr, double scale, int nterms) {
+                    const double* __restrict__ corr_ptr, double scale, int nterms, BandRegion rg) {
   extern __shared__ __align__(16) double sm[];
   const int nb = 1 << L;
   double* tab = sm;                          // [kind][offset] A fragments (64 doubles)
@@ -514,6 +514,10 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
     lc[a1] = l % nb;
     lc[a2] = l / nb;
     lc[A] = 0;
+    // sharded plans: only the lines within 5 boxes of the own region matter
+    if (MODE == 0 && (lc[a1] < rg.lo[a1] - 5 || lc[a1] >= rg.hi[a1] + 5 || lc[a2] < rg.lo[a2] - 5 ||
+                      lc[a2] >= rg.hi[a2] + 5))
+      return;
   }
   for (int e = threadIdx.x; e < 2 * NO * 64; e += blockDim.x) tab[e] = tables[(e >> 6) * kSepSlot + (e & 63)];
   __shared__ int64_t bids[16];
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(kBandWarps * 32, 2)
       stage(ub, ldub, zpub);
     }
     __syncthreads();
-    for (int q = warp; q < nb; q += kBandWarps) {
+    for (int q = rg.lo[A] + warp; q < rg.hi[A]; q += kBandWarps) {
       const int64_t ob = (box_id(q) * R + r) * 512;
       for (int t = 0; t < nterms; ++t) {
         double acc[kSepP][2];
@@ -650,7 +654,7 @@ template <int NB>
 __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
     sep_band_xy_kernel(const double* __restrict__ tables, int NO, int L, int R, const double* __restrict__ ub,
                        int ldub, int zpub, const double* __restrict__ ws, int64_t term_stride, double* __restrict__ Y,
-                       const double* __restrict__ corr_ptr, double scale, int nterms) {
+                       const double* __restrict__ corr_ptr, double scale, int nterms, BandRegion rg) {
   constexpr int NW = band_xy_warps<NB>();
   constexpr int CPW = NB * NB / NW;   // cells per warp (one row / column segment)
   constexpr int SEG = NB / CPW;        // segments per row
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
   double* tab = sm;
   double* P = sm + 2 * NO * 64;
   __shared__ int64_t bids[NB * NB];
-  const int r = blockIdx.y, zl = blockIdx.x & 7, bz = blockIdx.x >> 3;
+  const int r = blockIdx.y, zl = blockIdx.x & 7, bz = rg.lo[2] + (blockIdx.x >> 3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int OR = (NO - 1) / 2;
   for (int e = threadIdx.x; e < 2 * NO * 64; e += blockDim.x) tab[e] = tables[(e >> 6) * kSepSlot + (e & 63)];
@@ -694,7 +698,9 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
     {
       const int by = warp / SEG, bx0 = (warp % SEG) * CPW;
       const double* xb0 = P + kq * PITCH + 8 * bx0 + nq;
-      for (int j = 0; j < cnt; ++j) {
+      // sharded plans: only the rows of the own region, columns within 5 boxes of it
+      const bool need = by >= rg.lo[1] && by < rg.hi[1] && bx0 < rg.hi[0] + 5 && bx0 + CPW > rg.lo[0] - 5;
+      for (int j = 0; j < (need ? cnt : 0); ++j) {
         const int o = band_off(t, by & 1, j), b = by + o;
         if (b < 0 || b >= NB) continue;
         const double* az = tab + (kind * NO + o + OR) * 64;
@@ -717,7 +723,8 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
       const double sg = (t == 1 || t == 2 || t == 5) ? -1.0 : 1.0;
       const int bx = warp / SEG, by0 = (warp % SEG) * CPW;
       const double* xb0 = P + (8 * by0 + nq) * PITCH + kq;
-      for (int j = 0; j < cnt; ++j) {
+      const bool need = bx >= rg.lo[0] && bx < rg.hi[0] && by0 < rg.hi[1] && by0 + CPW > rg.lo[1];
+      for (int j = 0; j < (need ? cnt : 0); ++j) {
         const int o = band_off(t, bx & 1, j), b = bx + o;
         if (b < 0 || b >= NB) continue;
         const double* az = tab + (kind * NO + o + OR) * 64;
@@ -735,6 +742,8 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
   const int bx = warp / SEG, by0 = (warp % SEG) * CPW;
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
+    // sharded plans: only the own cells (the rest saw partial halo data)
+    if (bx < rg.lo[0] || bx >= rg.hi[0] || by0 + i < rg.lo[1] || by0 + i >= rg.hi[1]) continue;
     const int64_t bid = bids[(by0 + i) * NB + bx];
     double* o = Y + (bid * R + r) * 512 + 64 * zl + nq + 16 * kq;
     const double* us = ub + (bid * R + r) * ldub + zpub * zl + nq + 16 * kq;
@@ -975,12 +984,13 @@ int64_t sep_band_workspace(int L, int R) { return (int64_t)kBandTerms * ((int64_
 
 template <int A, int MODE>
 static void launch_band_t(const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                          double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st) {
+                          double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
+                          const BandRegion& rg) {
   const size_t smem = sep_band_smem_bytes(NO, L);
   const int64_t tstride = ((int64_t)1 << (3 * L)) * R * 512;
   sep_band_kernel<A, MODE><<<dim3(1u << (2 * L), R), kBandWarps * 32, smem, st>>>(tables, NO, L, R, ub, ldub, zpub,
                                                                                    ws, tstride, Y, corr, scale,
-                                                                                   nterms);
+                                                                                   nterms, rg);
 }
 
 size_t sep_band_xy_smem_bytes(int NO, int L) {
@@ -992,10 +1002,12 @@ size_t sep_band_xy_smem_bytes(int NO, int L) {
 template <int NB>
 static void launch_band_xy_t(const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
                              const double* ws, double* Y, const double* corr, double scale, int nterms,
-                             cudaStream_t st) {
+                             cudaStream_t st, const BandRegion& rg) {
   const int64_t tstride = ((int64_t)1 << (3 * L)) * R * 512;
-  sep_band_xy_kernel<NB><<<dim3(8 * NB, R), band_xy_warps<NB>() * 32, sep_band_xy_smem_bytes(NO, L), st>>>(
-      tables, NO, L, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, nterms);
+  const int planes = 8 * (rg.hi[2] - rg.lo[2]);
+  if (planes <= 0) return;
+  sep_band_xy_kernel<NB><<<dim3(planes, R), band_xy_warps<NB>() * 32, sep_band_xy_smem_bytes(NO, L), st>>>(
+      tables, NO, L, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, nterms, rg);
 }
 
 // HTLR_BAND_XY=0: separate y and x sweeps (sep_band_kernel modes 1, 2)
@@ -1009,19 +1021,28 @@ static bool band_xy_fused() {
 }
 
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
-                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st) {
+                     double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
+                     const int* lo, const int* hi) {
   zpub = zpub ? zpub : 64;
+  const int nb = 1 << L;
+  BandRegion rg;
+  bool full = true;
+  for (int a = 0; a < 3; ++a) {
+    rg.lo[a] = lo ? lo[a] : 0;
+    rg.hi[a] = hi ? hi[a] : nb;
+    full = full && rg.lo[a] == 0 && rg.hi[a] == nb;
+  }
   if (sweep == 0) {
-    launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
-  } else if (band_xy_fused()) {
+    launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
+  } else if (band_xy_fused() || !full) {   // the separate sweeps handle whole levels only
     if (sweep == 2) return;   // done by the fused launch of sweep 1
-    if (L == 4) launch_band_xy_t<16>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
-    else if (L == 3) launch_band_xy_t<8>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
-    else launch_band_xy_t<4>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+    if (L == 4) launch_band_xy_t<16>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
+    else if (L == 3) launch_band_xy_t<8>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
+    else launch_band_xy_t<4>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
   } else if (sweep == 1) {
-    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
   } else {
-    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st);
+    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
   }
 }
 

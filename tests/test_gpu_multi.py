@@ -87,7 +87,7 @@ def test_sharded_overlapped_exchange(name, world):
     assert err <= 1e-13, err
 
 
-@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 8), ("cfg3", 4), ("cfg4", 8)])
+@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 8), ("cfg3", 4), ("cfg4", 8), ("cfg4", 2), ("cfg4", 4)])
 def test_sharded_equals_single(name, world):
     w = WORKLOADS[name]
     cfg, grid = w.build_config(), w.grid
