@@ -1,0 +1,446 @@
+// Banded passes as register-resident line sweeps (sm_100a).
+//
+// At strong admissibility eta = 1 on a uniform grid the pairs a target box
+// meets form product sets (htlr_sep.cu, "Banded leaf pass"), so a separable
+// pass is
+//   Y = C10^3 - C4^3 - C5^3 + C2^3 + E5^3 - E2^3   (+ self correction),
+// X^3 = X_x (x) X_y (x) X_z, every X_S = sum_{o in S} M(o) shift(o) a 1-D
+// block-banded operator over the boxes of one axis.  Each term is applied as
+// three line sweeps, z first, then y, then x.  The reference's blocks
+// (grids.py:268-296, blocks.py:126-259) are all applied, in a different order.
+//
+// The unit of work is a *line*: 8 points across x one axis of boxes long
+// (NB boxes x 8 points x 8 points = 64 NB doubles, 2 NB registers per lane)
+// in the m8n8k4 B-fragment layout, lane (g = lane/4, q = lane%4) holding
+// points (k = q, n = g) and (k = q + 4, n = g) of every box, k running along
+// the sweep axis.  A warp applies a term's band to its line entirely in
+// registers: for target box b the sum over the band's source boxes s = b + o
+// of A(o) B_s, 2 DMMA per (b, o), the box and offset loops unrolled so every
+// register index is static (the band of box b depends only on b's parent
+// b >> 1 and the term).  No source box is staged or re-read: each is loaded
+// once by the one warp whose line holds it.
+//
+// band_line_kernel (z sweep): one warp per z line (box column (bx, by), point
+// row y): reads the line of ub once and writes all NT terms' z-swept lines
+// to the term buffers ([term][box][rhs][512], z-plane pitch 64).
+//
+// band_plane_kernel (y then x sweep): one CTA per z-point plane; per term,
+// warp w loads the y line of box column bx = w from the term buffer (the
+// next term's line is loaded while the current x sweep runs), sweeps y in
+// registers and writes its C fragments to shared memory cell (by, bx) in
+// lane order; after a barrier warp w reads box row by = w from shared memory
+// as x-sweep B fragments (the y sweep's C fragment is the x sweep's B
+// fragment with the k order permuted, the tables' mode-x A fragments use the
+// same permutation) and accumulates sign_t * X_x(t) into its registers.  The
+// last term ends in Y = scale * acc + corr * ub (self pairs).  128 KB of
+// shared memory (NB = 16): the transposition buffer of one term, no staging.
+#include "htlr_device.cuh"
+#include "htlr_kernels.h"
+
+#include <algorithm>
+#include <type_traits>
+
+namespace htlr {
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// shared-memory load the compiler may not merge with an earlier one (the
+// factor fragments of an offset recur in several terms; keeping them all live
+// would cost 32+ registers)
+__device__ __forceinline__ double lds(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+__device__ __forceinline__ double2 lds2(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+// Tensor memory as the plane kernel's Y accumulator (128 KB per plane, which
+// the register file cannot hold next to the sweep lines): warp w owns 64
+// columns of lane quarter w % 4; a double is two 32-bit columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, double (&v)[4][2]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) v[c][j] = __hiloint2double((int)r[4 * c + 2 * j + 1], (int)r[4 * c + 2 * j]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const double (&v)[4][2]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      r[4 * c + 2 * j] = (uint32_t)__double2loint(v[c][j]);
+      r[4 * c + 2 * j + 1] = (uint32_t)__double2hiint(v[c][j]);
+    }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+      ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ double neg(double v) {
+  return __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull);
+}
+
+// band of term T (htlr_sep.cu band_count / band_off): count and the i-th
+// per-axis offset for a target of coordinate parity c
+template <int T>
+__host__ __device__ constexpr int bcount() {
+  return T == 0 ? 10 : T == 1 ? 4 : (T == 3 || T == 5) ? 2 : 5;
+}
+template <int T>
+__host__ __device__ constexpr int boff(int c, int i) {
+  return T == 0 ? -4 - c + i
+       : T == 1 ? (i < 2 ? -4 - c + i : 2 - c + i)
+       : (T == 3 || T == 5) ? (i ? 2 : -2)
+       : i - 2;
+}
+template <int T>
+__host__ __device__ constexpr bool bneg() { return T == 1 || T == 2 || T == 5; }
+
+// spread the 4 low bits of v to every third bit (Morton interleave)
+__host__ __device__ constexpr int spread3(int v) {
+  return (v & 1) | ((v & 2) << 2) | ((v & 4) << 4) | ((v & 8) << 6) | ((v & 16) << 8);
+}
+// Morton id of box (x, y, z): x the most significant bit of each triple
+// (htlr_device.cuh morton_encode with d = 3)
+__device__ __forceinline__ int64_t morton3(int x, int y, int z) {
+  return (int64_t)((spread3(x) << 2) | (spread3(y) << 1) | spread3(z));
+}
+
+// shared-memory copy of a pass's factor tables: per (kind, offset) slot the
+// standard A fragments [0, 64) and the mode-x (permuted k) ones [64, 128)
+constexpr int kTabSlot = 128;
+// TMEM columns of a plane CTA: NB warps x 4 NB columns over 4 lane quarters
+// (a power of two >= 32)
+__host__ __device__ constexpr int plane_tmem_cols(int NB) { return NB == 16 ? 256 : NB == 8 ? 64 : 32; }
+__device__ __forceinline__ void stage_tables(double* __restrict__ dst, const double* __restrict__ tables, int NO,
+                                             int nval) {
+  for (int e = threadIdx.x; e < 2 * NO * nval; e += blockDim.x)
+    dst[(e / nval) * kTabSlot + e % nval] = tables[(int64_t)(e / nval) * kSepSlot + e % nval];
+}
+
+// One term's band over a register line: acc[b] (+)= sum_o A(o) in[b + o].
+// SLOT 0: standard A fragments, 64: the mode-x (permuted k) ones.
+template <int NB, int T, int SLOT, bool SIGN, int B0 = 0, int B1 = NB>
+__device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO, int lane, const double (&in)[NB][2],
+                                          double (&acc)[NB][2]) {
+  constexpr int kind = T >= 4 ? 1 : 0;
+  const int OR = (NO - 1) / 2;
+#pragma unroll
+  for (int i = 0; i < bcount<T>(); ++i) {
+    const double* p0 = tab + (kind * NO + boff<T>(0, i) + OR) * kTabSlot + SLOT;
+    const double* p1 = tab + (kind * NO + boff<T>(1, i) + OR) * kTabSlot + SLOT;
+    double a00 = lds(p0 + lane), a01 = lds(p0 + 32 + lane);
+    double a10 = lds(p1 + lane), a11 = lds(p1 + 32 + lane);
+    if (SIGN && bneg<T>()) {
+      a00 = neg(a00); a01 = neg(a01); a10 = neg(a10); a11 = neg(a11);
+    }
+#pragma unroll
+    for (int b = B0; b < B1; ++b) {
+      const int s = b + boff<T>(b & 1, i);
+      if (s >= 0 && s < NB) dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, in[s][0]);
+    }
+#pragma unroll
+    for (int b = B0; b < B1; ++b) {
+      const int s = b + boff<T>(b & 1, i);
+      if (s >= 0 && s < NB) dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, in[s][1]);
+    }
+  }
+}
+
+// The same band with the B fragments read from shared memory cells
+// (cell s of the warp's row: a double2 per lane, lane order).
+template <int NB, int T, int B0, int B1>
+__device__ __forceinline__ void band_smem(const double* __restrict__ tab, int NO, int lane,
+                                          const double2* __restrict__ row, double (&acc)[NB][2]) {
+  constexpr int kind = T >= 4 ? 1 : 0;
+  const int OR = (NO - 1) / 2;
+#pragma unroll
+  for (int i = 0; i < bcount<T>(); ++i) {
+    const double* p0 = tab + (kind * NO + boff<T>(0, i) + OR) * kTabSlot + 64;
+    const double* p1 = tab + (kind * NO + boff<T>(1, i) + OR) * kTabSlot + 64;
+    double a00 = lds(p0 + lane), a01 = lds(p0 + 32 + lane);
+    double a10 = lds(p1 + lane), a11 = lds(p1 + 32 + lane);
+    if (bneg<T>()) {
+      a00 = neg(a00); a01 = neg(a01); a10 = neg(a10); a11 = neg(a11);
+    }
+#pragma unroll
+    for (int b = B0; b < B1; ++b) {
+      const int s = b + boff<T>(b & 1, i);
+      if (s >= 0 && s < NB) {
+        const double2 v = lds2(row + s * 32);
+        dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, v.x);
+        dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, v.y);
+      }
+    }
+  }
+}
+
+template <int NB>
+__device__ __forceinline__ void zero(double (&a)[NB][2]) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) a[b][0] = a[b][1] = 0.0;
+}
+
+// z sweep: warp = z line (bx, by, point row y, rhs r); CTA c of G takes lines
+// c + G w', so every SM gets the same number of lines
+constexpr int kLineWarps = 8;
+template <int NB, int NT, bool R1>
+__global__ void __launch_bounds__(kLineWarps * 32, 2) band_line_kernel(const double* __restrict__ tables, int NO,
+                                                                      int R_, const double* __restrict__ ub, int ldub,
+                                                                      int zpub, double* __restrict__ ws,
+                                                                      int64_t tstride) {
+  const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
+  __shared__ double tab[2 * 15 * kTabSlot];
+  stage_tables(tab, tables, NO, 64);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nlines = NB * NB * 8 * R;
+  const int g = lane >> 2, q = lane & 3;
+  for (int line = blockIdx.x + gridDim.x * (threadIdx.x >> 5); line < nlines; line += gridDim.x * kLineWarps) {
+    const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
+    const int bx = col % NB, by = col / NB;
+    // box (bx, by, b): Morton id m0 + spread3(b) (z the least significant bit)
+    const int64_t m0 = morton3(bx, by, 0) * R + r, bstride = (int64_t)R;
+    double in[NB][2];
+    {
+      const double* s = ub + m0 * ldub + 8 * y + g + zpub * q;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const double* sb = s + spread3(b) * bstride * ldub;
+        in[b][0] = __ldg(sb);
+        in[b][1] = __ldg(sb + 4 * zpub);
+      }
+    }
+    // lane's C fragment: (z' = g, x = 2q + j) of every box
+    double* const ob = ws + m0 * 512 + 64 * g + 8 * y + 2 * q;
+    // a term's targets in halves (16 accumulator registers at a time)
+    auto term = [&](auto tc) {
+      constexpr int T = decltype(tc)::value;
+      constexpr int H = NB / 2;
+      double* o = ob + T * tstride;
+      double acc[NB][2];
+      zero(acc);
+      band_regs<NB, T, 0, false, 0, H>(tab, NO, lane, in, acc);
+#pragma unroll
+      for (int b = 0; b < H; ++b)
+        *reinterpret_cast<double2*>(o + spread3(b) * bstride * 512) = make_double2(acc[b][0], acc[b][1]);
+      band_regs<NB, T, 0, false, H, NB>(tab, NO, lane, in, acc);
+#pragma unroll
+      for (int b = H; b < NB; ++b)
+        *reinterpret_cast<double2*>(o + spread3(b) * bstride * 512) = make_double2(acc[b][0], acc[b][1]);
+    };
+    // a runtime loop over the terms: the compiler cannot interleave (and keep
+    // live) several terms' accumulators
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+      switch (t) {
+        case 0: term(std::integral_constant<int, 0>{}); break;
+        case 1: term(std::integral_constant<int, 1>{}); break;
+        case 2: term(std::integral_constant<int, 2>{}); break;
+        case 3: term(std::integral_constant<int, 3>{}); break;
+        case 4: term(std::integral_constant<int, 4>{}); break;
+        default: term(std::integral_constant<int, 5>{}); break;
+      }
+    }
+  }
+}
+
+// y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
+template <int NB, int NT, bool R1>
+__global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __restrict__ tables, int NO, int R_,
+                                                                const double* __restrict__ ub, int ldub, int zpub,
+                                                                const double* __restrict__ ws, int64_t tstride,
+                                                                double* __restrict__ Y,
+                                                                const double* __restrict__ corr_ptr, double scale) {
+  constexpr int NQ = NB / 4;   // quarters of a row of cells (4 cells = 16 TMEM columns)
+  const int R = R1 ? 1 : R_;
+  extern __shared__ __align__(16) double smp[];
+  double2* cell = reinterpret_cast<double2*>(smp);   // [by][bx][lane]
+  double* tab = smp + NB * NB * 64;
+  __shared__ uint32_t tmem_sh;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tmem_sh)),
+                 "n"(plane_tmem_cols(NB)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  stage_tables(tab, tables, NO, 128);
+  const int zl = blockIdx.x & 7, bz = blockIdx.x >> 3, r = blockIdx.y;
+  const int g = lane >> 2, q = lane & 3;
+  // y line of box column bx = w: element (y = q (+4), x = g) of z plane zl;
+  // box (w, b, bz) has Morton id morton3(w, 0, bz) + 2 spread3(b)
+  const int64_t yb = (morton3(w, 0, bz) * R + r) * 512 + 64 * zl + 8 * q + g, ystride = (int64_t)R * 512 * 2;
+  double in[NB][2];
+  auto load = [&](int t) {
+    const double* s = ws + t * tstride + yb;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      in[b][0] = __ldg(s + spread3(b) * ystride);
+      in[b][1] = __ldg(s + spread3(b) * ystride + 32);
+    }
+  };
+  const double2* row = cell + w * NB * 32 + lane;
+  double2* mine = cell + w * 32 + lane;   // column bx = w, row b at + b * NB * 32
+  load(0);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tm = tmem_sh + ((uint32_t)(32 * (w & 3)) << 16) + 16 * NQ * (w >> 2);
+  auto term = [&](auto tc) {
+    constexpr int T = decltype(tc)::value;
+    constexpr int H = NB / 2;
+    {
+      double acc[NB][2];
+      zero(acc);
+      band_regs<NB, T, 0, false, 0, H>(tab, NO, lane, in, acc);
+#pragma unroll
+      for (int b = 0; b < H; ++b) mine[b * NB * 32] = make_double2(acc[b][0], acc[b][1]);
+      band_regs<NB, T, 0, false, H, NB>(tab, NO, lane, in, acc);
+#pragma unroll
+      for (int b = H; b < NB; ++b) mine[b * NB * 32] = make_double2(acc[b][0], acc[b][1]);
+    }
+    __syncthreads();
+    if (T + 1 < NT) load(T + 1);   // in flight during the x sweep
+    // x sweep of the warp's row, four cells at a time, added to the TMEM accumulator
+    auto quarter = [&](auto qc) {
+      constexpr int Q = decltype(qc)::value;
+      double acc[NB][2];
+      zero(acc);
+      band_smem<NB, T, 4 * Q, 4 * Q + 4>(tab, NO, lane, row, acc);
+      double v[4][2];
+      if (T > 0) {
+        tmem_ld16(tm + 16 * Q, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c][0] += acc[4 * Q + c][0], v[c][1] += acc[4 * Q + c][1];
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c][0] = acc[4 * Q + c][0], v[c][1] = acc[4 * Q + c][1];
+      }
+      tmem_st16(tm + 16 * Q, v);
+    };
+    quarter(std::integral_constant<int, 0>{});
+    if (NQ > 1) quarter(std::integral_constant<int, (NQ > 1 ? 1 : 0)>{});
+    if (NQ > 2) quarter(std::integral_constant<int, (NQ > 2 ? 2 : 0)>{});
+    if (NQ > 3) quarter(std::integral_constant<int, (NQ > 3 ? 3 : 0)>{});
+    __syncthreads();
+  };
+#pragma unroll 1
+  for (int t = 0; t < NT; ++t) {
+    switch (t) {
+      case 0: term(std::integral_constant<int, 0>{}); break;
+      case 1: term(std::integral_constant<int, 1>{}); break;
+      case 2: term(std::integral_constant<int, 2>{}); break;
+      case 3: term(std::integral_constant<int, 3>{}); break;
+      case 4: term(std::integral_constant<int, 4>{}); break;
+      default: term(std::integral_constant<int, 5>{}); break;
+    }
+  }
+  // lane holds (x' = g, y = 2q + j) of cells (bx = b, by = w)
+  const double cv = corr_ptr ? corr_ptr[0] : 0.0;
+  const int64_t mw = morton3(0, w, bz) * R + r;
+#pragma unroll
+  for (int Q = 0; Q < NQ; ++Q) {
+    double v[4][2];
+    tmem_ld16(tm + 16 * Q, v);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t m = mw + (int64_t)(spread3(4 * Q + c) << 2) * R;
+      double* o = Y + m * 512 + 64 * zl + 16 * q + g;
+      const double* us = ub + m * ldub + zpub * zl + 16 * q + g;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double val = scale * v[c][j];
+        if (corr_ptr) val = fma(cv, __ldg(us + 8 * j), val);
+        o[8 * j] = val;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_sh), "n"(plane_tmem_cols(NB)));
+}
+
+template <int NB, int NT>
+void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, double* ws,
+                    cudaStream_t st) {
+  const int64_t lines = (int64_t)NB * NB * 8 * R;
+  const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(2 * sms, (lines + kLineWarps - 1) / kLineWarps);
+  if (R == 1)
+    band_line_kernel<NB, NT, true><<<(unsigned)grid, kLineWarps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+  else
+    band_line_kernel<NB, NT, false><<<(unsigned)grid, kLineWarps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+}
+
+template <int NB, int NT>
+void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, const double* ws,
+                     double* Y, const double* corr, double scale, cudaStream_t st) {
+  const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
+  const size_t smem = (size_t)NB * NB * 32 * sizeof(double2) + (size_t)2 * NO * kTabSlot * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (R == 1)
+    band_plane_kernel<NB, NT, true><<<dim3(8 * NB, R), NB * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride,
+                                                                            Y, corr, scale);
+  else
+    band_plane_kernel<NB, NT, false><<<dim3(8 * NB, R), NB * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride,
+                                                                             Y, corr, scale);
+}
+
+}  // namespace
+
+bool band_lines_supported(int L) { return L >= 2 && L <= 4; }
+
+void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
+                       double* ws, cudaStream_t st) {
+  zpub = zpub ? zpub : 64;
+  if (L == 4) nterms == 6 ? launch_lines_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
+                          : launch_lines_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
+  else if (L == 3) nterms == 6 ? launch_lines_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
+                               : launch_lines_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
+  else nterms == 6 ? launch_lines_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
+                   : launch_lines_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
+}
+
+void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
+                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
+  zpub = zpub ? zpub : 64;
+  if (L == 4) nterms == 6 ? launch_planes_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
+                          : launch_planes_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
+  else if (L == 3) nterms == 6 ? launch_planes_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
+                               : launch_planes_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
+  else nterms == 6 ? launch_planes_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
+                   : launch_planes_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
+}
+
+}  // namespace htlr

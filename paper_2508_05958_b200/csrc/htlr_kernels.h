@@ -220,6 +220,13 @@ cudaError_t sep_band_init();
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
                      double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
                      const int* lo, const int* hi);
+// register-line sweeps (htlr_band.cu): z sweep (ub -> term buffers) and the
+// fused y-x sweep of every z-point plane (term buffers -> Y), whole levels
+bool band_lines_supported(int L);
+void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
+                       double* ws, cudaStream_t st);
+void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
+                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,

@@ -1032,6 +1032,15 @@ void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, cons
     rg.hi[a] = hi ? hi[a] : nb;
     full = full && rg.lo[a] == 0 && rg.hi[a] == nb;
   }
+  static const bool v1 = [] {
+    const char* e = std::getenv("HTLR_BAND_V1");
+    return e && e[0] == '1';
+  }();
+  if (full && !v1 && band_lines_supported(L)) {
+    if (sweep == 0) launch_band_lines(L, nterms, tables, NO, R, ub, ldub, zpub, ws, st);
+    else if (sweep == 1) launch_band_planes(L, nterms, tables, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
+    return;
+  }
   if (sweep == 0) {
     launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
   } else if (band_xy_fused() || !full) {   // the separate sweeps handle whole levels only
