@@ -134,10 +134,10 @@ constexpr int kTabSlot = 128;
 // TMEM columns of a plane CTA: NB warps x 4 NB columns over 4 lane quarters
 // (a power of two >= 32)
 __host__ __device__ constexpr int plane_tmem_cols(int NB) { return NB == 16 ? 256 : NB == 8 ? 64 : 32; }
-__device__ __forceinline__ void stage_tables(double* __restrict__ dst, const double* __restrict__ tables, int NO,
-                                             int nval) {
-  for (int e = threadIdx.x; e < 2 * NO * nval; e += blockDim.x)
-    dst[(e / nval) * kTabSlot + e % nval] = tables[(int64_t)(e / nval) * kSepSlot + e % nval];
+template <int NVAL>
+__device__ __forceinline__ void stage_tables(double* __restrict__ dst, const double* __restrict__ tables, int NO) {
+  for (int e = threadIdx.x; e < 2 * NO * NVAL; e += blockDim.x)
+    dst[(e / NVAL) * kTabSlot + e % NVAL] = __ldg(tables + (e / NVAL) * kSepSlot + e % NVAL);
 }
 
 // One term's band over a register line: acc[b] (+)= sum_o A(o) in[b + o].
@@ -203,36 +203,42 @@ __device__ __forceinline__ void zero(double (&a)[NB][2]) {
   for (int b = 0; b < NB; ++b) a[b][0] = a[b][1] = 0.0;
 }
 
-// z sweep: warp = z line (bx, by, point row y, rhs r); CTA c of G takes lines
-// c + G w', so every SM gets the same number of lines
-constexpr int kLineWarps = 8;
+// z sweep: warp = z line (bx, by, point row y, rhs r); one CTA per SM, CTA c
+// of G takes lines c + G w' (w' < blockDim / 32), so every SM gets the same
+// number of lines to within one
+constexpr int kLineWarps = 16;   // at most
 template <int NB, int NT, bool R1>
-__global__ void __launch_bounds__(kLineWarps * 32, 2) band_line_kernel(const double* __restrict__ tables, int NO,
+__global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
                                                                       int R_, const double* __restrict__ ub, int ldub,
                                                                       int zpub, double* __restrict__ ws,
                                                                       int64_t tstride) {
   const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
   __shared__ double tab[2 * 15 * kTabSlot];
-  stage_tables(tab, tables, NO, 64);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nlines = NB * NB * 8 * R;
   const int g = lane >> 2, q = lane & 3;
-  for (int line = blockIdx.x + gridDim.x * (threadIdx.x >> 5); line < nlines; line += gridDim.x * kLineWarps) {
+  const int64_t bstride = (int64_t)R;
+  double in[NB][2];
+  auto load = [&](int line) {
+    const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
+    const double* s = ub + (morton3(col % NB, col / NB, 0) * R + r) * ldub + 8 * y + g + zpub * q;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double* sb = s + spread3(b) * bstride * ldub;
+      in[b][0] = __ldg(sb);
+      in[b][1] = __ldg(sb + 4 * zpub);
+    }
+  };
+  int line = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
+  if (line < nlines) load(line);   // in flight while the tables are staged
+  stage_tables<64>(tab, tables, NO);
+  __syncthreads();
+  for (; line < nlines; line += gridDim.x * (blockDim.x >> 5)) {
+    if (line >= blockIdx.x + gridDim.x * (threadIdx.x >> 5) + 1) load(line);
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
     const int bx = col % NB, by = col / NB;
     // box (bx, by, b): Morton id m0 + spread3(b) (z the least significant bit)
-    const int64_t m0 = morton3(bx, by, 0) * R + r, bstride = (int64_t)R;
-    double in[NB][2];
-    {
-      const double* s = ub + m0 * ldub + 8 * y + g + zpub * q;
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const double* sb = s + spread3(b) * bstride * ldub;
-        in[b][0] = __ldg(sb);
-        in[b][1] = __ldg(sb + 4 * zpub);
-      }
-    }
+    const int64_t m0 = morton3(bx, by, 0) * R + r;
     // lane's C fragment: (z' = g, x = 2q + j) of every box
     double* const ob = ws + m0 * 512 + 64 * g + 8 * y + 2 * q;
     // a term's targets in halves (16 accumulator registers at a time)
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
                  "n"(plane_tmem_cols(NB)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  stage_tables(tab, tables, NO, 128);
+  stage_tables<128>(tab, tables, NO);
   const int zl = blockIdx.x & 7, bz = blockIdx.x >> 3, r = blockIdx.y;
   const int g = lane >> 2, q = lane & 3;
   // y line of box column bx = w: element (y = q (+4), x = g) of z plane zl;
@@ -391,11 +397,13 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = std::min<int64_t>(2 * sms, (lines + kLineWarps - 1) / kLineWarps);
+  // one CTA per SM with ceil(lines / SMs) warps (at most 16, then they loop)
+  const int64_t grid = std::min<int64_t>(sms, lines);
+  const int warps = (int)std::min<int64_t>(kLineWarps, (lines + grid - 1) / grid);
   if (R == 1)
-    band_line_kernel<NB, NT, true><<<(unsigned)grid, kLineWarps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+    band_line_kernel<NB, NT, true><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
   else
-    band_line_kernel<NB, NT, false><<<(unsigned)grid, kLineWarps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+    band_line_kernel<NB, NT, false><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
 }
 
 template <int NB, int NT>
