@@ -14,10 +14,12 @@ Multi-GPU (torchrun) shards target boxes by cluster subtrees (strong
 scaling); `e2e` repeats the step through the public API from
 pinned host memory with the result copied back.
 
-`--impl reference` times the reference algorithm's CPU path (the oracle
-port, oracle/htlr_oracle.py -- /root/reference does not exist on the GPU
-box) on a bounded sample of leaf blocks per (level, kind), extrapolated to
-the full leaf counts; rank 0 only.
+`--impl reference` times the reference's CPU matvec on the host cores (the
+reference is pure Python and absent on the GPU box: its leaf loop restated
+call for call, oracle/htlr_oracle.py rl_*): the whole loop per step for
+configs 1-2, a stratified leaf sample extrapolated to all leaves (stated in
+the line) for configs 3-5; rank 0 only, no product code imported.  `--gpus N`
+without torchrun starts N ranks itself.
 """
 
 from __future__ import annotations
@@ -112,68 +114,96 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# --------------------------------------------------------------------------- CPU path
+# --------------------------------------------------------------------------- workloads
+
+# BASELINE.json configs[0..4] as plain data, shared by both arms so their
+# `config` objects are identical.  The reference arm must not import the
+# product package (its __init__ loads _htlr_b200.so); tests/test_bench_contract.py
+# checks this table against paper_2508_05958_b200/configs.py.
+#   name: (d, n, leaf_side_max, rank, (oracle kernel, sigma, scale), a, nrhs, seed, amplitude, description)
+TWO_PI, FOUR_PI = 2.0 * 3.141592653589793, 4.0 * 3.141592653589793
+WORKLOADS_PLAIN = {
+    "cfg1": (2, 64, 8, 8, ("slp2d", None, TWO_PI), 1.0, 1, 0, None,
+             "2D n=64 -log|x-y| a=1 leaf 8 eta=1 p=8, 1 matvec"),
+    "cfg2": (3, 32, 8, 6, ("slp3d", None, FOUR_PI), 0.0, 1, 1, None,
+             "3D n=32 1/|x-y| leaf 8 eta=1 p=6, construct + 10 matvecs"),
+    "cfg3": (3, 64, 8, 6, ("slp3d", None, FOUR_PI), 0.0, 16, 2, None,
+             "3D n=64 1/|x-y| leaf 8 eta=1 p=6, 16 RHS batched matvec"),
+    "cfg4": (3, 128, 8, 8, ("gaussian", 0.1 / 2.0 ** 0.5, 1.0), 0.0, 1, 3, None,
+             "3D n=128 exp(-|x-y|^2/0.01) leaf 8 eta=1 p=8, matvec"),
+    "cfg5": (3, 96, 8, 6, ("slp3d", None, FOUR_PI), 0.0, 1, 4, 0.05,
+             "3D mapped quasi-uniform n=96 (x=t+0.05 sin(2 pi t)/(2 pi)) 1/|x-y| leaf 8 (side 6) "
+             "eta=1 p=6, construct + matvec"),
+}
+L2_NOTE = ("inputs re-read from HBM every step: the GPU arm writes a 512 MiB buffer (> the 126 MB L2) before "
+           "every step, outside the timed bracket; the reference arm runs on the host CPU")
+
+
+def workload_config(name: str) -> dict:
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    d, n, _, _, _, _, nrhs, _, _, desc = WORKLOADS_PLAIN[name]
+    return {"workload": name, "description": desc, "points": n ** d, "nrhs": nrhs, "l2": L2_NOTE}
+
+
+def workload_input(name: str):
+    """BASELINE.json's seeded input in the reference's F-order linearisation
+    (same recipe as paper_2508_05958_b200/configs.py Workload.input)."""
+    import numpy as np
+    d, n, _, _, _, _, nrhs, seed, _, _ = WORKLOADS_PLAIN[name]
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((n ** d, nrhs)) if nrhs > 1 else rng.uniform(-1, 1, n ** d)
+
+
+# --------------------------------------------------------------------------- CPU path (reference algorithm)
 
 
 def oracle_problem(name):
     from oracle import htlr_oracle as O
-    import math
-    from paper_2508_05958_b200.configs import WORKLOADS
-    w = WORKLOADS[name]
-    kern = {
-        "cfg1": O.Kernel("slp2d", scale=2 * math.pi),
-        "cfg2": O.Kernel("slp3d", scale=4 * math.pi),
-        "cfg3": O.Kernel("slp3d", scale=4 * math.pi),
-        "cfg4": O.Kernel("gaussian", sigma=0.1 / math.sqrt(2.0)),
-        "cfg5": O.Kernel("slp3d", scale=4 * math.pi),
-    }[name]
-    if w.amplitude >= 0:
-        return w, O.MappedProblem(d=w.d, geo=O.MappedGeometry(w.n, w.amplitude), rank=w.rank,
-                                  leaf_side_max=w.leaf, kernel=kern, coeff=O.constant_coeff(w.a))
-    return w, O.Problem(d=w.d, n=w.n, rank=w.rank, leaf_side_max=w.leaf, kernel=kern,
-                        coeff=O.constant_coeff(w.a))
+    d, n, leaf, rank, (kind, sigma, scale), a, _, _, amp, _ = WORKLOADS_PLAIN[name]
+    kern = O.Kernel(kind, sigma=sigma, scale=scale) if sigma is not None else O.Kernel(kind, scale=scale)
+    if amp is not None:
+        return O.MappedProblem(d=d, geo=O.MappedGeometry(n, amp), rank=rank, leaf_side_max=leaf, kernel=kern,
+                               coeff=O.constant_coeff(a))
+    return O.Problem(d=d, n=n, rank=rank, leaf_side_max=leaf, kernel=kern, coeff=O.constant_coeff(a))
 
 
-def leaf_groups(name):
-    """Leaf rows grouped by (level, kind), from the (bit-exact) host list
-    builder -- used only to choose and count the sampled blocks."""
-    import numpy as np
-    import paper_2508_05958_b200 as H
-    from paper_2508_05958_b200.configs import WORKLOADS
-    w = WORKLOADS[name]
-    grid = w.grid
-    bt = H.build_block_cluster_tree(H.build_cluster_tree(grid, w.leaf), H.AdmissibilityRule.strong(1.0))
-    arr = bt.leaf_array
-    groups = {}
-    for lvl in np.unique(arr[:, 2]):
-        for kind in (0, 1):
-            rows = arr[(arr[:, 2] == lvl) & (arr[:, 1] == kind)]
-            if len(rows):
-                groups[(int(lvl), kind)] = rows
-    return groups
+FULL_REFERENCE = ("cfg1", "cfg2")   # the whole leaf loop per step; larger configs: stratified samples
+SAMPLES_FILE = os.path.join(ROOT, "tests", "golden", "bench_samples.npz")
 
 
-class CpuSample:
-    """Reference matvec inner loop (operators.py:146-155) on a bounded sample
-    of leaves per (level, kind), payloads built beforehand (untimed)."""
+class ReferenceLoop:
+    """The reference's matvec (operators.py:138-156 with blocks.py:230-259,
+    restated call for call in oracle/htlr_oracle.py `rl_*`) on the host CPU.
 
-    def __init__(self, name: str, per_group: int, seed: int = 0):
+    Configs 1-2: one step is the whole DFS leaf loop over every leaf (payloads
+    built beforehand, untimed, one block object per distinct (kind, level,
+    offset): equal values).  Configs 3-5 (0.17-2.7 M leaves, 0.1-5 TB of
+    payloads): one step applies a stratified sample -- the leaves of
+    tests/golden/bench_samples.npz, 32 per (level, kind) stratum -- and the full
+    matvec time is extrapolated as sum over strata of count / sampled x the
+    stratum's measured time, x the RHS count."""
+
+    def __init__(self, name: str):
         import numpy as np
         from oracle import htlr_oracle as O
-        self.O = O
-        self.w, self.pb = oracle_problem(name)
-        groups = leaf_groups(name)
-        rng = np.random.default_rng(seed)
-        d = self.w.d
+        self.O, self.name = O, name
+        self.pb = oracle_problem(name)
+        d, n, leaf, rank = WORKLOADS_PLAIN[name][:4]
+        self.d, self.n, self.nrhs = d, n, WORKLOADS_PLAIN[name][6]
+        self.full = name in FULL_REFERENCE
         mapped = isinstance(self.pb, O.MappedProblem)
-        diag = None if mapped else self.pb.diag()
-        self.items = []      # (group, leaf, payload)
-        self.counts = {}
-        for key, rows in groups.items():
-            self.counts[key] = len(rows)
-            pick = rng.choice(len(rows), size=min(per_group, len(rows)), replace=False)
-            for i in pick:
-                r = rows[i]
+        if self.full:
+            self.leaves = O.block_leaves(n, d, leaf)
+            self.payloads = O.shared_payloads(self.pb, self.leaves)
+            self.strata = None
+        else:
+            smp = np.load(SAMPLES_FILE)
+            counts, rows = smp[f"{name}_counts"], smp[f"{name}_rows"]
+            self.counts = {(int(l), int(k)): int(c) for l, k, c in counts}
+            self.leaves, self.payloads, self.strata = [], [], []
+            diag = None if mapped else self.pb.diag()
+            cache = {}
+            for r in rows:
                 lf = O.Leaf(int(r[0]), int(r[1]), int(r[2]),
                             tuple((int(r[3 + 2 * a]), int(r[4 + 2 * a])) for a in range(d)),
                             tuple((int(r[3 + 2 * d + 2 * a]), int(r[4 + 2 * d + 2 * a])) for a in range(d)))
@@ -182,87 +212,104 @@ class CpuSample:
                           if lf.kind == O.ADM else
                           O.mapped_dense_block(self.pb.kernel, self.pb.coeff, self.pb.geo, lf.tau, lf.sigma))
                 else:
-                    pl = O.build_payload(self.pb, lf, diag)
-                self.items.append((key, lf, pl))
-        u = self.w.input()
-        self.R = 1 if u.ndim == 1 else u.shape[1]
-        shape = (self.w.n,) * d
-        self.u = u.reshape(self.w.grid.num_points, -1)[:, 0].reshape(shape, order="F")
-        self.f = np.zeros(shape)
+                    key = O.leaf_key(lf)
+                    if key not in cache:
+                        cache[key] = O.build_payload(self.pb, lf, diag)
+                    pl = cache[key]
+                self.leaves.append(lf)
+                self.payloads.append(pl)
+                self.strata.append((lf.level, lf.kind))
+        u = workload_input(name)
+        self.u = u.reshape(n ** d, -1)[:, 0].reshape((n,) * d, order="F")
+        self.f = np.zeros((n,) * d)
+
+    @property
+    def sample(self) -> str:
+        if self.full:
+            return (f"the whole reference leaf loop (operators.py:146-155, {len(self.leaves)} leaves, "
+                    f"rl_* restatement in oracle/htlr_oracle.py) per step")
+        return (f"{len(self.leaves)} leaves per step ({len(self.leaves) // max(1, len(self.counts))} per (level, kind) "
+                f"stratum, tests/golden/bench_samples.npz) through the reference leaf loop (rl_* restatement), "
+                f"extrapolated to all {sum(self.counts.values())} leaves x {self.nrhs} RHS")
 
     def step(self):
-        """Apply every sampled block once; returns (estimated full matvec
-        seconds for all R right-hand sides, sampled seconds)."""
+        """One step; returns (elapsed seconds, seconds of one full matvec of
+        all RHS: measured for the full loop, else extrapolated)."""
         O = self.O
+        t_start = time.perf_counter()
+        if self.full:
+            self.f[...] = 0.0
+            for lf, pl in zip(self.leaves, self.payloads):
+                O.rl_leaf(self.u, self.f, lf, pl)
+            el = time.perf_counter() - t_start
+            return el, el * self.nrhs
         per = {}
-        t_all = 0.0
-        for key, lf, pl in self.items:
+        for lf, pl, key in zip(self.leaves, self.payloads, self.strata):
             t0 = time.perf_counter()
-            seg = self.u[O._slices(lf.sigma)].ravel(order="F")
-            out = O.apply_payload(pl, seg)
-            self.f[O._slices(lf.tau)] += out.reshape([hi - lo for lo, hi in lf.tau], order="F")
-            dt = time.perf_counter() - t0
-            t_all += dt
+            O.rl_leaf(self.u, self.f, lf, pl)
             s, c = per.get(key, (0.0, 0))
-            per[key] = (s + dt, c + 1)
-        est = sum(self.counts[k] * s / c for k, (s, c) in per.items()) * self.R
-        return est, t_all
+            per[key] = (s + time.perf_counter() - t0, c + 1)
+        el = time.perf_counter() - t_start
+        est = sum(self.counts[k] * s / c for k, (s, c) in per.items()) * self.nrhs
+        return el, est
 
 
-def blas_threads() -> int:
+def host_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
         n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
         return max(n) if n else 1
     except Exception:
-        return 1
+        return os.cpu_count() or 1
 
 
 def cpu_baseline(name: str, budget_s: float) -> dict:
-    per_group = 12
-    smp = CpuSample(name, per_group)
+    """The reference arm's loop, bounded to about `budget_s` seconds."""
+    loop = ReferenceLoop(name)
     t_start = time.perf_counter()
     ests = []
     while time.perf_counter() - t_start < budget_s or not ests:
-        est, _ = smp.step()
-        ests.append(est)
+        ests.append(loop.step()[1])
     est = statistics.median(ests)
-    npts = smp.w.grid.num_points * smp.R
-    return {"value": npts / est, "unit": "points/s", "cores": blas_threads(), "kind": "port",
-            "sample": (f"oracle port of the reference matvec loop (operators.py:146-155) on {len(smp.items)} "
-                       f"leaves ({per_group} per (level, kind)), {len(ests)} passes, extrapolated to the full "
-                       f"{sum(smp.counts.values())} leaves; est. full matvec {est:.2f} s")}
+    npts = loop.n ** loop.d * loop.nrhs
+    return {"value": npts / est, "unit": "points/s", "cores": host_threads(), "kind": "port",
+            "sample": f"{loop.sample}; {len(ests)} steps in {time.perf_counter() - t_start:.1f} s; "
+                      f"full matvec {est:.3f} s"}
 
 
 def run_reference(args):
+    """`--impl reference`: the reference's CPU matvec (oracle port; the
+    reference is pure Python, not installable on the GPU box), rank 0 only,
+    with the BLAS threads of every host core, on the B200 arm's config."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2508_05958_b200.configs import WORKLOADS
-    w = WORKLOADS[args.workload]
-    smp = CpuSample(args.workload, per_group=8)
+    loop = ReferenceLoop(args.workload)
     for _ in range(args.warmup):
-        smp.step()
-    ests = []
+        loop.step()
+    els, ests = [], []
     for _ in range(args.steps):
-        est, _ = smp.step()
+        el, est = loop.step()
+        els.append(el)
         ests.append(est)
+    ms_per_step = statistics.mean(els) * 1e3
     est = statistics.mean(ests)
-    npts = w.grid.num_points * w.nrhs
+    npts = loop.n ** loop.d * loop.nrhs
     value = npts / est
     line = {
         "metric": "HTLR matvec points/s", "value": value, "unit": "points/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json seeds)",
-        "config": {"workload": args.workload, "description": w.description, "points": w.grid.num_points,
-                   "nrhs": w.nrhs},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": blas_threads(), "kind": "port",
-                         "sample": (f"oracle port (oracle/htlr_oracle.py) of the reference matvec loop on "
-                                    f"{len(smp.items)} sampled leaves per step, extrapolated to "
-                                    f"{sum(smp.counts.values())} leaves")},
+        "config": workload_config(args.workload),
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": host_threads(), "kind": "port",
+                         "sample": loop.sample},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not loop.full:
+        line["extrapolated"] = {"ms_per_step_is": "the measured time of the sampled leaves",
+                                "full_matvec_s_est": est, "sampled_leaves": len(loop.leaves),
+                                "leaves": sum(loop.counts.values())}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -370,6 +417,9 @@ def run_b200(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks with torchrun, or "
+                         f"run without WORLD_SIZE and bench.py starts them)")
     # HTLR_DIST_BACKEND=gloo: a harness check of the multi-rank flow on fewer
     # GPUs than ranks (exchange staged through host memory; not a measurement)
     backend = os.environ.get("HTLR_DIST_BACKEND", "nccl")
@@ -397,7 +447,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     construct_s = time.perf_counter() - t0
 
-    u_host = w.input()
+    u_host = workload_input(args.workload)
     R = 1 if u_host.ndim == 1 else u_host.shape[1]
     ud = torch.from_numpy(np.ascontiguousarray(u_host)).cuda()
     if world > 1:
@@ -451,10 +501,13 @@ def run_b200(args):
         prof.append(base_op.profile_read())
     base_op.profile(False)
     total_ms = sum(step_ms)
+    rank_ms = [total_ms / args.steps]
     if dist is not None:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        t = torch.zeros(world, dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        t[rank] = total_ms
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        rank_ms = [float(v) / args.steps for v in t.tolist()]
+        total_ms = max(float(v) for v in t.tolist())
     ms_per_step = total_ms / args.steps
     npts = grid.num_points * R
     value = npts / (ms_per_step / 1e3)
@@ -524,19 +577,20 @@ def run_b200(args):
         cpu = cpu_baseline(args.workload, args.cpu_seconds)
 
     rep = H.storage_report(base_op)
+    xbytes = 0
+    if world > 1:
+        xbytes = sum(b.numel() * 8 for b in op.exchange_buffers(R)) * (world - 1) // world
     line = {
         "metric": "HTLR matvec points/s", "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json seeds)",
-        "config": {"workload": args.workload, "description": w.description, "points": grid.num_points,
-                   "nrhs": R, "l2": "flushed (512 MiB write) before every step, outside the timed bracket; "
-                                   f"operator tables {rep.device_scalars * 8 / 1e9:.2f} GB "
-                                   f"({'>' if rep.device_scalars * 8 > 126e6 else '<'} the 126 MB L2)",
-                   "formulation": base_op.formulation(), "leaf_pass": base_op.leaf_pass(),
-                   "formulation_note": FORMULATION_NOTES.get(base_op.formulation(), ""),
-                   "construct_s": construct_s, "parallelism": f"target subtrees x{world}" if world > 1 else "1 GPU",
-                   "reference_storage_GB": rep.total_scalars * 8 / 1e9,
-                   "device_storage_GB": rep.device_scalars * 8 / 1e9},
+        "config": workload_config(args.workload),
+        "plan": {"formulation": base_op.formulation(), "leaf_pass": base_op.leaf_pass(),
+                 "formulation_note": FORMULATION_NOTES.get(base_op.formulation(), ""),
+                 "construct_s": construct_s, "parallelism": f"target subtrees x{world}" if world > 1 else "1 GPU",
+                 "operator_tables_GB": rep.device_scalars * 8 / 1e9,
+                 "reference_storage_GB": rep.total_scalars * 8 / 1e9,
+                 "rank_ms_per_step": rank_ms, "exchange_bytes_per_rank_per_step": xbytes},
         "roofline": roofline,
         "whole_step": whole,
         "construction": {"seconds": construct_s, "points_per_s": grid.num_points / construct_s,
@@ -556,8 +610,25 @@ def run_b200(args):
     return 0
 
 
+def self_launch(args) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks of this
+    script (torch.distributed.run, one process per GPU, 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

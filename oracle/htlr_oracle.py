@@ -782,8 +782,163 @@ def mapped_matvec(pb: MappedProblem, u: np.ndarray, leaves: Optional[list] = Non
     return out.reshape(u.shape)
 
 
+def mapped_sampled_matvec(pb: MappedProblem, u: np.ndarray, targets: Sequence[Ranges],
+                          leaves: Optional[list] = None) -> np.ndarray:
+    """`sampled_matvec` on the mapped grid: rows of the target leaf boxes
+    only, from the leaves whose tau contains one, in DFS order (the same
+    restriction of operators.py:146-155).  Returns (len(targets), points, R)."""
+    u = np.asarray(u, dtype=np.float64)
+    cols = u.reshape(pb.num_points, -1)
+    if leaves is None:
+        leaves = mapped_block_leaves(pb.geo, pb.d, pb.leaf_side_max, pb.rule, pb.eta)
+    shape = (pb.n,) * pb.d
+    R = cols.shape[1]
+    uts = [cols[:, r].reshape(shape, order="F") for r in range(R)]
+    acc = {}
+    for lf in leaves:
+        hit = [i for i, tb in enumerate(targets) if _contains(lf.tau, tb)]
+        if not hit:
+            continue
+        if lf.kind == ADM:
+            pl = mapped_tucker_block(pb.kernel, pb.geo, lf.tau, lf.sigma, pb.rank)
+        else:
+            pl = mapped_dense_block(pb.kernel, pb.coeff, pb.geo, lf.tau, lf.sigma, pb.q)
+        tsz = [hi - lo for lo, hi in lf.tau]
+        for r in range(R):
+            res = apply_payload(pl, uts[r][_slices(lf.sigma)].ravel(order="F")).reshape(tsz, order="F")
+            for i in hit:
+                sub = tuple(slice(lo - tlo, hi - tlo) for (lo, hi), (tlo, _) in zip(targets[i], lf.tau))
+                acc.setdefault((i, r), np.zeros([hi - lo for lo, hi in targets[i]]))
+                acc[(i, r)] += res[sub]
+    npts = int(np.prod([hi - lo for lo, hi in targets[0]]))
+    out = np.zeros((len(targets), npts, R))
+    for (i, r), v in acc.items():
+        out[i, :, r] = v.ravel(order="F")
+    return out
+
+
 def mapped_dense_matrix(pb: MappedProblem) -> np.ndarray:
     """Full Nystrom matrix on the mapped grid (small n; exactness check of the
     compressed operator)."""
     full = tuple((0, pb.n) for _ in range(pb.d))
     return mapped_dense_block(pb.kernel, pb.coeff, pb.geo, full, full, pb.q)
+
+
+# --------------------------------------------------------------------------
+# The reference's matvec *call structure*, operation for operation -- what the
+# `bench.py --impl reference` arm times (the reference is pure Python and
+# cannot travel to the GPU box).  `tucker_apply` / `matvec` above compute the
+# same values with fewer wrapper layers; these keep every conversion,
+# validation and axis move of the reference's per-leaf path, so the Python
+# overhead per block is the reference's:
+#   tensor.mode_product / contract / reshape / multi_mode_apply
+#       (tensor.py:27-32, 35-52, 55-86, 89-104, 118-132),
+#   blocks.tlr_apply (blocks.py:230-259),
+#   operators._hierarchical_matvec (operators.py:138-156).
+# --------------------------------------------------------------------------
+
+
+def _rl_array(t) -> np.ndarray:
+    arr = np.asarray(t, dtype=np.float64)                  # tensor.py:27-32
+    if arr.ndim == 0:
+        raise ValueError("tensor must have order >= 1")
+    return arr
+
+
+def rl_mode_product(t, m, mode: int) -> np.ndarray:
+    """tensor.py:35-52: validated tensordot over `mode`, new axis moved back."""
+    t = _rl_array(t)
+    m = np.asarray(m, dtype=np.float64)
+    if m.ndim != 2 or not 1 <= mode <= t.ndim or m.shape[1] != t.shape[mode - 1]:
+        raise ValueError("mode_product: bad factor or mode")
+    return np.moveaxis(np.tensordot(m, t, axes=([1], [mode - 1])), 0, mode - 1)
+
+
+def rl_contract(a, b, dims_a, dims_b) -> np.ndarray:
+    """tensor.py:55-86: validated tensordot over 1-based dimension lists."""
+    a, b = _rl_array(a), _rl_array(b)
+    dims_a, dims_b = list(dims_a), list(dims_b)
+    if len(dims_a) != len(dims_b) or len(set(dims_a)) != len(dims_a) or len(set(dims_b)) != len(dims_b):
+        raise ValueError("contract: bad dimension lists")
+    for da, db in zip(dims_a, dims_b):
+        if not (1 <= da <= a.ndim and 1 <= db <= b.ndim) or a.shape[da - 1] != b.shape[db - 1]:
+            raise ValueError("contract: extent mismatch")
+    return np.tensordot(a, b, axes=([x - 1 for x in dims_a], [x - 1 for x in dims_b]))
+
+
+def rl_vec_to_tensor(v, shape) -> np.ndarray:
+    """tensor.py:89-100: F-order reshape after a float64 ravel."""
+    flat = _rl_array(np.asarray(v, dtype=np.float64).ravel(order="F"))
+    shape = tuple(int(s) for s in shape)
+    if int(np.prod(shape)) != flat.size:
+        raise ValueError("reshape: size mismatch")
+    return np.reshape(flat, shape, order="F")
+
+
+def rl_multi_mode_apply(t, factors) -> np.ndarray:
+    """tensor.py:118-132: sequential mode products over distinct modes."""
+    if len({mode for _, mode in factors}) != len(factors):
+        raise ValueError("multi_mode_apply requires distinct modes")
+    out = _rl_array(t)
+    for m, mode in factors:
+        out = rl_mode_product(out, m, mode)
+    return out
+
+
+def rl_tlr_apply(b: Tucker, seg) -> np.ndarray:
+    """blocks.py:230-259: V^T mode products (square factors skipped), core
+    contraction over the source modes, U mode products, F-order flatten."""
+    seg = np.asarray(seg, dtype=np.float64).ravel(order="F")
+    d = len(b.ufac)
+    cols = [f.shape[0] if f is not None else b.core.shape[d + a] for a, f in enumerate(b.vfac)]
+    if seg.size != int(np.prod(cols)):
+        raise ValueError("segment length does not match the block")
+    w = rl_vec_to_tensor(seg, cols)
+    w = rl_multi_mode_apply(w, [(f.T, a + 1) for a, f in enumerate(b.vfac) if f is not None])
+    hh = rl_contract(b.core, w, list(range(d + 1, 2 * d + 1)), list(range(1, d + 1)))
+    ff = rl_multi_mode_apply(hh, [(f, a + 1) for a, f in enumerate(b.ufac) if f is not None])
+    return _rl_array(ff).ravel(order="F")
+
+
+def rl_leaf(u_tensor: np.ndarray, f_tensor: np.ndarray, lf: Leaf, payload) -> None:
+    """One iteration of the leaf loop of operators.py:146-155."""
+    seg = u_tensor[_slices(lf.sigma)].ravel(order="F")
+    out = payload @ seg if not isinstance(payload, Tucker) else rl_tlr_apply(payload, seg)
+    f_tensor[_slices(lf.tau)] += out.reshape([hi - lo for lo, hi in lf.tau], order="F")
+
+
+def rl_matvec(n: int, d: int, leaves: list, payloads, u) -> np.ndarray:
+    """operators.py:138-156: F-order u -> (n,)*d tensor, the DFS leaf loop,
+    F-order f.  `payloads[i]` belongs to `leaves[i]`."""
+    u = np.asarray(u, dtype=np.float64).ravel(order="F")
+    if u.size != n ** d:
+        raise ValueError(f"vector length {u.size} != {n ** d}")
+    ut = u.reshape((n,) * d, order="F")
+    ft = np.zeros((n,) * d)
+    for lf, pl in zip(leaves, payloads):
+        rl_leaf(ut, ft, lf, pl)
+    return ft.ravel(order="F")
+
+
+def leaf_key(lf: Leaf) -> tuple:
+    """Payload identity on a uniform grid with a translation-invariant kernel:
+    (kind, level, box sizes, source - target offset) -- equal keys give equal
+    blocks (the factors depend on the box size only, the core and the dense
+    block on the offset; the tau == sigma diagonal is the same cell average)."""
+    return (lf.kind, lf.level, tuple(hi - lo for lo, hi in lf.tau), tuple(hi - lo for lo, hi in lf.sigma),
+            tuple(s[0] - t[0] for t, s in zip(lf.tau, lf.sigma)))
+
+
+def shared_payloads(pb: Problem, leaves: list) -> list:
+    """Payload per leaf, one object per leaf_key (uniform grids): the
+    reference builds every leaf's block separately; the loop applies the same
+    values, and configs 2-4 would not fit in host memory otherwise."""
+    diag = pb.diag()
+    cache: dict = {}
+    out = []
+    for lf in leaves:
+        key = leaf_key(lf)
+        if key not in cache:
+            cache[key] = build_payload(pb, lf, diag)
+        out.append(cache[key])
+    return out

@@ -41,8 +41,8 @@ struct GemmTask {
   int pair_begin;
   int pair_count;
   int r0;
-  int kc0;   // K range of the item in 32-wide chunks: split-K for passes with
-  int nkc;   // too few items to fill the GPU (partial sums meet in the RED epilogue)
+  int kc0;   // K range of the item in 32-wide chunks (the whole K extent:
+  int nkc;   // kc0 = 0, nkc = K_pad / 32)
 };
 
 // coarse-level contribution gathered by the fused downward kernel

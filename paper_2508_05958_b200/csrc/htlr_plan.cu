@@ -272,6 +272,9 @@ struct htlr_plan {
   // overlapped host-vector matvec (htlr_matvec_host): its graphs (keyed by the
   // host pointers), a copy stream and the fork / join events
   std::vector<GraphEntry> host_graphs;
+  // staging vectors the host graphs were captured with (a reallocation of
+  // u_stage / f_stage by another path invalidates every host graph)
+  void* host_graph_stage[2] = {nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;
   // concurrent level passes (mv_remote): side stream + fork / join events
   cudaStream_t side_stream = nullptr;
@@ -377,41 +380,20 @@ int choose_nt(const Pass& ps, int R) {
   return eff(64) > eff(96) + 0.005 ? 64 : 96;
 }
 
-int make_tasks(Pass& ps, int R, int sms, std::vector<htlr::GemmTask>& out) {
+int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
   const int NT = choose_nt(ps, R);
   ps.task_nt[R] = NT;
   const int Rc = std::min(R, NT);
   const int npt = std::max(1, NT / Rc);
   const int nk = ps.K_pad / htlr::kKC;
-  // split K until the pass has ~8 work items per SM (small passes are
-  // otherwise a few waves of long, memory-bound items on part of the GPU)
-  int64_t base = 0;
-  for (int mat = 0; mat < ps.nmats; ++mat) {
-    const int64_t np = ps.seg[mat + 1] - ps.seg[mat];
-    base += ((np + npt - 1) / npt) * ((R + Rc - 1) / Rc);
-  }
-  const int64_t items = base * ps.RT;
-  const int64_t want = 8LL * sms;
-  const int kstep = htlr::gemm_stage_chunks(ps.MT, ps.K_pad);   // split granularity (chunks per stage)
-  // measured: no gain for the small configs (their items are bound by the
-  // few active consumer warps, not by load balance), so split-K is opt-in
-  static int splitk = -1;
-  if (splitk < 0) {
-    const char* e = std::getenv("HTLR_SPLITK");
-    splitk = (e && e[0] == '1') ? 1 : 0;
-  }
-  int ksplit = 1;
-  while (splitk && items * ksplit < want && ksplit * 2 * kstep <= nk) ksplit *= 2;
-  const int nunits = nk / kstep;
+  // one item = the whole K extent of its matrix (split-K items measured no
+  // gain and would break the generated near blocks' two-slot generator ring,
+  // which assumes every item spans >= STAGES ring stages)
   out.clear();
   for (int mat = 0; mat < ps.nmats; ++mat) {
     for (int b = ps.seg[mat]; b < ps.seg[mat + 1]; b += npt) {
       int cnt = std::min(npt, ps.seg[mat + 1] - b);
-      for (int r0 = 0; r0 < R; r0 += Rc)
-        for (int k = 0; k < ksplit; ++k) {
-          const int u0 = (int)((int64_t)k * nunits / ksplit), u1 = (int)((int64_t)(k + 1) * nunits / ksplit);
-          out.push_back({mat, b, cnt, r0, u0 * kstep, (u1 - u0) * kstep});
-        }
+      for (int r0 = 0; r0 < R; r0 += Rc) out.push_back({mat, b, cnt, r0, 0, nk});
     }
   }
   return 0;
@@ -2030,9 +2012,7 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   for (auto& ps : pl->passes) {
     if (pl->sep || ps.tasks.count(cx.R)) continue;
     std::vector<htlr::GemmTask> tv;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
-    make_tasks(ps, cx.R, sms, tv);
+    make_tasks(ps, cx.R, tv);
     auto& slot = ps.tasks[cx.R];
     if (slot.first.alloc(std::max<size_t>(1, tv.size()) * sizeof(htlr::GemmTask))) return 1;
     if (!tv.empty())
@@ -2750,6 +2730,12 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
     if (int rc = htlr_matvec(pl, pl->u_stage.d(), pl->f_stage.d(), nrhs, stream)) return rc;
     CUDA_TRY(cudaMemcpyAsync(f, pl->f_stage.ptr, vbytes, cudaMemcpyDefault, cx.st));
     return 0;
+  }
+  if (pl->host_graph_stage[0] != pl->u_stage.ptr || pl->host_graph_stage[1] != pl->f_stage.ptr) {
+    for (auto& g : pl->host_graphs) cudaGraphExecDestroy(g.exec);
+    pl->host_graphs.clear();
+    pl->host_graph_stage[0] = pl->u_stage.ptr;
+    pl->host_graph_stage[1] = pl->f_stage.ptr;
   }
   for (auto& g : pl->host_graphs) {
     if (g.R == cx.R && g.u == u && g.f == f) {

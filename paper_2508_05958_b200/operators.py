@@ -298,7 +298,9 @@ def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int], out=None):
         host = True
     n_pts = op.num_points
     if nrhs_expected == 1:
-        flat = x.reshape(-1)
+        # the reference flattens in F order (operators.py:139 u.ravel(order="F")):
+        # an (n,)*d field's first index runs fastest
+        flat = x.permute(*reversed(range(x.dim()))).reshape(-1) if x.dim() > 1 else x.reshape(-1)
         if flat.numel() != n_pts:
             raise ValueError(f"vector length {flat.numel()} != {n_pts}")
         x2 = flat.reshape(n_pts, 1)

@@ -77,17 +77,10 @@ def test_mapped_blocks_vs_oracle():
         assert rel(H.materialize(blk), ref) <= TOL
 
 
-@pytest.mark.parametrize("R", [1, 2])
-def test_mapped_sharded_equals_single(R):
-    """Eight shards on one GPU, the NCCL all-gather and reduce-scatter replayed
-    as device copies: R = 1 runs the symmetric regeneration (every unordered
-    pair on one shard, full-size accumulators summed between the contract and
-    the expand half), R = 2 the one-sided kernels."""
-    cfg, grid, pb, _ = problem(0)
-    single = H.construct(cfg, grid)
-    U = np.random.default_rng(7).standard_normal((grid.num_points, R))
-    ref = H.matmat(single, U)
-    world = 8
+def emulated_shards(cfg, grid, U, world):
+    """The sharded matvec with `world` shards on one GPU: the NCCL all-gather
+    and reduce-scatter replayed as device copies between the shards' plans."""
+    R = U.shape[1]
     ops = [ShardedOperator(cfg, grid, r, world, device=0) for r in range(world)]
     ud = torch.from_numpy(U).cuda().contiguous()
     bufs = [op.local_phase(ud, R) for op in ops]
@@ -98,7 +91,6 @@ def test_mapped_sharded_equals_single(R):
                 if q != r:
                     bufs[q][i][r * c:(r + 1) * c].copy_(bufs[r][i][r * c:(r + 1) * c])
     rb = [op.contract_phase(ud, R) for op in ops]
-    assert bool(rb[0]) == (R == 1)
     for i in range(len(rb[0])):
         tot = sum(b[i] for b in rb)
         c = tot.numel() // world
@@ -109,7 +101,64 @@ def test_mapped_sharded_equals_single(R):
         fd = torch.zeros_like(ud)
         op.expand_phase(ud, fd, R)
         total += fd
-    assert rel(total.cpu().numpy(), ref) <= 1e-13
+    return total.cpu().numpy(), rb
+
+
+def _mapped_fixture():
+    return np.load(os.path.join(GOLD, "mapped.npz"))
+
+
+def _box_rows(f, n, boxes):
+    return [f[O.box_linear_indices(n, tuple(map(tuple, b)))] for b in boxes]
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_cfg5_sampled_rows_vs_oracle(world):
+    """BASELINE config 5 at its own size (n = 96, side-6 leaves, p = 6, 1/r,
+    seed-4 input): rows of corner, face, interior and octant-boundary leaf
+    boxes against the oracle's mapped restatement (tests/golden/mapped.npz:
+    per-block QR Tucker payloads with the 24 x 6 and 12 x 6 factors of levels
+    2 and 3, per-point rectangular-cell diagonal, kernels.py:222-249
+    generalised), on one plan and on 8 emulated shards (the octant planes run
+    through the last box)."""
+    g = _mapped_fixture()
+    w = WORKLOADS["cfg5"]
+    u = w.input()
+    if world == 1:
+        f = H.matvec(H.construct(w.build_config(), w.grid), u)
+    else:
+        f, _ = emulated_shards(w.build_config(), w.grid, u.reshape(-1, 1), world)
+        f = f[:, 0]
+    for got, ref in zip(_box_rows(f, 96, g["cfg5_boxes"]), g["cfg5_rows"]):
+        assert rel(got, ref[:, 0]) <= TOL
+
+
+def test_mapped_48_nonsquare_factors_vs_oracle():
+    """A 3-D 1/r mapped case whose level-2 blocks have non-square 12 x 6
+    factors (n = 48, leaf 6, p = 6) against the oracle's sampled rows."""
+    g = _mapped_fixture()
+    cfg = H.BuildConfig(rank=6, leaf_side=6, rule=H.AdmissibilityRule.strong(1.0), kernel=H.inv_r_3d(),
+                        coeff=H.CoefficientFn.constant(0.0))
+    op = H.construct(cfg, H.MappedGrid(3, 48, 0.05))
+    u = np.random.default_rng(48).standard_normal(48 ** 3)
+    f = H.matvec(op, u)
+    for got, ref in zip(_box_rows(f, 48, g["m48_boxes"]), g["m48_rows"]):
+        assert rel(got, ref[:, 0]) <= TOL
+
+
+@pytest.mark.parametrize("R", [1, 2])
+def test_mapped_sharded_equals_single(R):
+    """Eight shards on one GPU, the NCCL all-gather and reduce-scatter replayed
+    as device copies: R = 1 runs the symmetric regeneration (every unordered
+    pair on one shard, full-size accumulators summed between the contract and
+    the expand half), R = 2 the one-sided kernels."""
+    cfg, grid, pb, _ = problem(0)
+    single = H.construct(cfg, grid)
+    U = np.random.default_rng(7).standard_normal((grid.num_points, R))
+    ref = H.matmat(single, U)
+    total, rb = emulated_shards(cfg, grid, U, 8)
+    assert bool(rb[0]) == (R == 1)
+    assert rel(total, ref) <= 1e-13
 
 
 def test_cfg5_runs_and_is_symmetric():

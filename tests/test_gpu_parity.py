@@ -335,3 +335,20 @@ def test_randomised_parity_sweep():
     out = subprocess.run([sys.executable, "tools/fuzz_parity.py", "2", "12"], cwd=root, capture_output=True,
                          text=True, timeout=1200)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+
+
+def test_field_shaped_input_flattens_in_fortran_order():
+    """matvec accepts the grid field as an (n,)*d array and flattens it like
+    the reference, u.ravel(order="F") (operators.py:139): first index fastest.
+    numpy and torch (host and device) inputs, against the reference fixture."""
+    import torch
+    w = WORKLOADS["cfg1"]
+    op = H.construct(w.build_config(), w.grid)
+    u = w.input()
+    gold = load("cfg1_matvec")["f"]
+    field = u.reshape((64, 64), order="F")
+    for x in (field, torch.from_numpy(field), torch.from_numpy(field).cuda()):
+        f = H.matvec(op, x)
+        f = f.cpu().numpy() if isinstance(f, torch.Tensor) else np.asarray(f)
+        assert f.shape == (4096,)
+        assert rel(f, gold) <= TOL

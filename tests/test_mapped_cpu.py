@@ -67,3 +67,23 @@ def test_rectangular_cell_quadrature_converges():
     g0 = O.MappedGeometry(12, 0.0)
     c = O.mapped_cell_integral(k, g0, idx, q=10)
     assert abs(c - O.cell_average(k, 3, 1 / 12) / 12 ** 3) <= 1e-13 * abs(c)
+
+
+def test_cfg5_lists_bit_exact_vs_oracle_fixture():
+    """BASELINE config 5 at its own size (n = 96, leaf_side 8 -> side-6
+    leaves, 2.65 M leaves): the C++ builder's DFS list equals the oracle's
+    mapped restatement bit for bit (sha256 of the whole list, the
+    (level, kind) histogram, strided rows; tests/golden/make_mapped_fixtures.py).
+    Ties of the predicate on the non-dyadic mapped domains (grids.py:153-165)
+    are where the two could part."""
+    import hashlib
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "mapped.npz"))
+    grid = H.MappedGrid(3, 96, 0.05)
+    arr = H.build_block_cluster_tree(H.build_cluster_tree(grid, 8), H.AdmissibilityRule.strong(1.0)).leaf_array
+    hist = np.zeros((16, 2), dtype=np.int64)
+    np.add.at(hist, (arr[:, 2], arr[:, 1]), 1)
+    assert np.array_equal(hist, g["cfg5_hist"])
+    assert np.array_equal(arr[g["cfg5_spotidx"]], g["cfg5_spot"])
+    sha = hashlib.sha256(np.ascontiguousarray(arr, dtype=np.int32).tobytes()).digest()
+    assert sha == bytes(g["cfg5_sha"])
