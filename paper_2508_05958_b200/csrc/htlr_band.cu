@@ -203,59 +203,49 @@ __device__ __forceinline__ void zero(double (&a)[NB][2]) {
   for (int b = 0; b < NB; ++b) a[b][0] = a[b][1] = 0.0;
 }
 
-// z sweep: warp = z line (bx, by, point row y, rhs r); one CTA per SM, CTA c
-// of G takes lines c + G w' (w' < blockDim / 32), so every SM gets the same
-// number of lines to within one
-constexpr int kLineWarps = 16;   // at most
-template <int NB, int NT, bool R1>
-__global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
-                                                                      int R_, const double* __restrict__ ub, int ldub,
-                                                                      int zpub, double* __restrict__ ws,
-                                                                      int64_t tstride) {
-  const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
-  __shared__ double tab[2 * 15 * kTabSlot];
-  const int lane = threadIdx.x & 31;
-  const int nlines = NB * NB * 8 * R;
-  const int g = lane >> 2, q = lane & 3;
-  const int64_t bstride = (int64_t)R;
-  double in[NB][2];
-  auto load = [&](int line) {
+// z sweep.  Work unit = half a z line: (box column (bx, by), point row y,
+// rhs r, half h) -- the targets [H h, H h + H) (H = NB / 2) and the source
+// boxes within 5 of them (13 of 16 at NB = 16).  One CTA per SM; warp gw
+// takes units gw, gw + S, gw + 2S, ... (S = grid x warps, even, so a warp
+// keeps its half): every SM sub-partition gets the same number of units to
+// within one (a single warp with two accumulator chains already saturates
+// its sub-partition's DMMA pipe, 1 DMMA.8x8x4 per 16 cycles, dependent
+// latency 26 cycles: tools/dmma_latency.cu), and each unit's source boxes are
+// loaded while the previous unit computes (two register buffers).
+constexpr int kLineWarps = 12;
+template <int NB, int NT, bool R1, int HALF>
+__device__ __forceinline__ void line_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
+                                           const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
+                                           int u0, int ustride, int nunits) {
+  constexpr int H = NB / 2;
+  constexpr int S0 = HALF ? (H - 5 > 0 ? H - 5 : 0) : 0;         // loaded source boxes [S0, S1)
+  constexpr int S1 = HALF ? NB : (H + 5 < NB ? H + 5 : NB);
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  auto load = [&](int u, double(&in)[NB][2]) {
+    const int line = u >> 1;
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
     const double* s = ub + (morton3(col % NB, col / NB, 0) * R + r) * ldub + 8 * y + g + zpub * q;
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const double* sb = s + spread3(b) * bstride * ldub;
+    for (int b = S0; b < S1; ++b) {
+      const double* sb = s + spread3(b) * (int64_t)R * ldub;
       in[b][0] = __ldg(sb);
       in[b][1] = __ldg(sb + 4 * zpub);
     }
   };
-  int line = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
-  if (line < nlines) load(line);   // in flight while the tables are staged
-  stage_tables<64>(tab, tables, NO);
-  __syncthreads();
-  for (; line < nlines; line += gridDim.x * (blockDim.x >> 5)) {
-    if (line >= blockIdx.x + gridDim.x * (threadIdx.x >> 5) + 1) load(line);
+  auto compute = [&](int u, const double(&in)[NB][2]) {
+    const int line = u >> 1;
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
-    const int bx = col % NB, by = col / NB;
-    // box (bx, by, b): Morton id m0 + spread3(b) (z the least significant bit)
-    const int64_t m0 = morton3(bx, by, 0) * R + r;
-    // lane's C fragment: (z' = g, x = 2q + j) of every box
-    double* const ob = ws + m0 * 512 + 64 * g + 8 * y + 2 * q;
-    // a term's targets in halves (16 accumulator registers at a time)
+    // lane's C fragment: (z' = g, x = 2q + j) of every target box
+    double* const ob = ws + (morton3(col % NB, col / NB, 0) * R + r) * 512 + 64 * g + 8 * y + 2 * q;
     auto term = [&](auto tc) {
       constexpr int T = decltype(tc)::value;
-      constexpr int H = NB / 2;
-      double* o = ob + T * tstride;
       double acc[NB][2];
       zero(acc);
-      band_regs<NB, T, 0, false, 0, H>(tab, NO, lane, in, acc);
+      band_regs<NB, T, 0, false, HALF * H, HALF * H + H>(tab, NO, lane, in, acc);
+      double* o = ob + T * tstride;
 #pragma unroll
-      for (int b = 0; b < H; ++b)
-        *reinterpret_cast<double2*>(o + spread3(b) * bstride * 512) = make_double2(acc[b][0], acc[b][1]);
-      band_regs<NB, T, 0, false, H, NB>(tab, NO, lane, in, acc);
-#pragma unroll
-      for (int b = H; b < NB; ++b)
-        *reinterpret_cast<double2*>(o + spread3(b) * bstride * 512) = make_double2(acc[b][0], acc[b][1]);
+      for (int b = HALF * H; b < HALF * H + H; ++b)
+        *reinterpret_cast<double2*>(o + spread3(b) * (int64_t)R * 512) = make_double2(acc[b][0], acc[b][1]);
     };
     // a runtime loop over the terms: the compiler cannot interleave (and keep
     // live) several terms' accumulators
@@ -270,7 +260,38 @@ __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const dou
         default: term(std::integral_constant<int, 5>{}); break;
       }
     }
+  };
+  double a[NB][2], b[NB][2];
+  int u = u0;
+  if (u < nunits) load(u, a);
+  __syncthreads();   // the tables (staged by the caller) are in place
+  while (u < nunits) {
+    const int un = u + ustride;
+    if (un < nunits) load(un, b);
+    compute(u, a);
+    if (un >= nunits) break;
+    const int unn = un + ustride;
+    if (unn < nunits) load(unn, a);
+    compute(un, b);
+    u = unn;
   }
+}
+
+template <int NB, int NT, bool R1>
+__global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
+                                                                      int R_, const double* __restrict__ ub, int ldub,
+                                                                      int zpub, double* __restrict__ ws,
+                                                                      int64_t tstride) {
+  const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
+  __shared__ double tab[2 * 15 * kTabSlot];
+  stage_tables<64>(tab, tables, NO);   // line_units syncs after issuing its first loads
+  const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
+  const int ustride = gridDim.x * (blockDim.x >> 5);
+  const int nunits = 2 * NB * NB * 8 * R;
+  if (gw & 1)
+    line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nunits);
+  else
+    line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nunits);
 }
 
 // y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
@@ -397,9 +418,10 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one CTA per SM with ceil(lines / SMs) warps (at most 16, then they loop)
-  const int64_t grid = std::min<int64_t>(sms, lines);
-  const int warps = (int)std::min<int64_t>(kLineWarps, (lines + grid - 1) / grid);
+  // one CTA of kLineWarps warps per SM (the stride over the 2 x lines
+  // half-line units must be even: a warp keeps its half)
+  const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
+  const int warps = kLineWarps;
   if (R == 1)
     band_line_kernel<NB, NT, true><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
   else

@@ -256,6 +256,7 @@ bool upward8_supported(int d, int p, int sL);
 // an n^3 grid and written to ub_out, then the upward from registers)
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
                     cudaStream_t st, const double* u = nullptr, double* ub_out = nullptr, int n = 0);
+constexpr int kMaxDown8 = 4;   // compressed levels the cooperative downward8 stages (config 4: 2)
 bool downward8_supported(int d, int p, int sL, const DownParams& dp);
 // [zlo, zhi): leaf-box z range written (the overlapped host-vector matvec
 // writes f by z halves)

@@ -43,6 +43,7 @@
 #include "htlr_kernels.h"
 #include "htlr_mbarrier.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace htlr {
@@ -381,50 +382,73 @@ __global__ void __launch_bounds__(256, 4) downward8_kernel(const double* __restr
                                                          const double* __restrict__ Y, const double* __restrict__ avec,
                                                          double aconst, int n, int L, int R, DownParams dp, int64_t b0,
                                                          int64_t nb, int zlo, int zhi) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wi >= nb * R) return;
-  const int64_t b = b0 + wi / R;
-  const int r = (int)(wi % R);
+  // CTA = the 8 sibling leaf boxes of one parent cluster (Morton ids
+  // b0 + 8 blockIdx.x + w) for rhs blockIdx.y: every level's ancestor
+  // coefficients are shared by the 8 warps, so they and the boxes' Y slices
+  // are copied into shared memory up front (16-byte cp.async, all in flight),
+  // and each warp's chain of mode products reads them with shared-memory
+  // latency; one wave of 4 CTAs per SM covers config 4.
+  constexpr int HP = kSepZPitch;   // H staged as [c][t][a] at a z pitch of 68 (B fragments conflict free)
+  constexpr int YP = 66;           // Y staged at a z pitch of 66 (epilogue reads conflict free)
+  extern __shared__ __align__(16) double smd[];
+  const int nlev = dp.nlev < kMaxDown8 ? dp.nlev : kMaxDown8;
+  double* sh = smd;                                              // [level][c][t][a]
+  double(*sy)[kSepP * YP] = reinterpret_cast<double(*)[kSepP * YP]>(smd + nlev * kSepP * HP);   // [box][k][j][i]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int64_t bb = b0 + 8 * (int64_t)blockIdx.x;   // first box of the sibling group
+  auto cp16 = [](double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+  };
+  for (int li = 0; li < nlev; ++li) {
+    const DownLevel lv = dp.lev[li];
+    const int64_t anc = bb >> (3 * (L - lv.level));
+    const double* hs = lv.H + (anc * R + r) * (int64_t)lv.P;
+    for (int e = threadIdx.x; e < 256; e += blockDim.x) cp16(sh + li * kSepP * HP + (e >> 5) * HP + 2 * (e & 31), hs + 2 * e);
+  }
+  if (Y) {
+    const double* ys = Y + ((bb + w) * R + r) * 512;
+    for (int e = lane; e < 256; e += 32) cp16(&sy[w][(e >> 5) * YP + 2 * (e & 31)], ys + 2 * e);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  const int64_t b = bb + w;
+  if (b >= b0 + nb) return;
   int bc[3];
   morton_decode(b, 3, L, bc);
   if (bc[2] < zlo || bc[2] >= zhi) return;
-  double y[kSepP][2], z[kSepP][2];
-#pragma unroll
-  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = z[j][0] = z[j][1] = 0.0;
   const int g = lane >> 2, q = lane & 3;
-  for (int li = 0; li < dp.nlev; ++li) {
+  double y[kSepP][2];
+#pragma unroll
+  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
+  for (int li = 0; li < nlev; ++li) {
     const DownLevel lv = dp.lev[li];
     const int shift = L - lv.level;
-    const int64_t anc = b >> (3 * shift);
     const double* Qx = lv.Q + (int64_t)((bc[0] & ((1 << shift) - 1)) * kSepP) * kSepP;
     const double* Qy = lv.Q + (int64_t)((bc[1] & ((1 << shift) - 1)) * kSepP) * kSepP;
     const double* Qz = lv.Q + (int64_t)((bc[2] & ((1 << shift) - 1)) * kSepP) * kSepP;
-    const double* hs = lv.H + (anc * R + r) * (int64_t)lv.P + g + 64 * q;
-    // mode z: Z_t[k', a] = sum_c Qz[k', c] H[a, t, c]
-    const double az0 = Qz[g * kSepP + q], az1 = Qz[g * kSepP + 4 + q];
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az0, __ldg(hs + 8 * t));
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az1, __ldg(hs + 8 * t + 256));
-    // mode x then mode y into the accumulator
-    const double bx0 = Qx[g * kSepP + 2 * q], bx1 = Qx[g * kSepP + 2 * q + 1];
+    const double* hs = sh + li * kSepP * HP + g + HP * q;
+    // mode z: Z_t[k', a] = sum_c Qz[k', c] H[a, t, c]; mode x, then mode y
+    // into the accumulator, one t at a time (8 registers of chain state)
+    const double az0 = __ldg(Qz + g * kSepP + q), az1 = __ldg(Qz + g * kSepP + 4 + q);
+    const double bx0 = __ldg(Qx + g * kSepP + 2 * q), bx1 = __ldg(Qx + g * kSepP + 2 * q + 1);
 #pragma unroll
     for (int t = 0; t < kSepP; ++t) {
-      double t0 = 0.0, t1 = 0.0;
-      dmma(t0, t1, bx0, z[t][0]);
-      dmma(t0, t1, bx1, z[t][1]);
+      double z0 = 0.0, z1 = 0.0, t0 = 0.0, t1 = 0.0;
+      dmma(z0, z1, az0, hs[8 * t]);
+      dmma(z0, z1, az1, hs[8 * t + 4 * HP]);
+      dmma(t0, t1, bx0, z0);
+      dmma(t0, t1, bx1, z1);
 #pragma unroll
       for (int j = 0; j < kSepP; ++j) {
         const double m = __ldg(Qy + j * kSepP + t);
         y[j][0] = fma(m, t0, y[j][0]);
         y[j][1] = fma(m, t1, y[j][1]);
       }
-      z[t][0] = z[t][1] = 0.0;
     }
   }
   // epilogue: lane holds (i = g, j, k' = 2 q + jj)
-  const double* yb = Y ? Y + (b * R + r) * (int64_t)(kSepP * kSepP * kSepP) + g + 128 * q : nullptr;
 #pragma unroll
   for (int j = 0; j < kSepP; ++j)
 #pragma unroll
@@ -433,7 +457,7 @@ __global__ void __launch_bounds__(256, 4) downward8_kernel(const double* __restr
       const int64_t gi =
           (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP + j) + (int64_t)n * n * (bc[2] * kSepP + k);
       double v = y[j][jj];
-      if (yb) v += __ldg(yb + 8 * j + 64 * jj);
+      if (Y) v += sy[w][g + 8 * j + YP * k];
       const double a = avec ? __ldg(avec + gi) : aconst;
       if (a != 0.0) v = fma(a, __ldg(u + gi * R + r), v);
       f[gi * R + r] = v;
@@ -764,76 +788,86 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
 // upward_body / blocks.py:239-247, split over the ancestor's leaf boxes):
 // mode z and mode x on the tensor pipe, mode y on DFMA, then one fp64 RED per
 // entry into W_l[ancestor] (zeroed by the permute launch).
-__global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L, int R,
-                                                       UpParams up, int64_t nb, const double* __restrict__ u,
-                                                       double* __restrict__ ub_out, int n) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  // rhs-major: the CTA's 8 warps are the 8 leaf boxes of one parent (Morton
-  // order) for one rhs, so their contributions are summed in shared memory
-  // and each W_l entry gets one RED per CTA instead of eight
-  const bool valid = wi < nb * R;
-  const int64_t b = valid ? wi % nb : 0;
-  const int r = valid ? (int)(wi / nb) : 0;
-  __shared__ double red[8][512];
-  const bool cta_red = (nb % 8) == 0 && blockDim.x == 256;
-  if (!valid && !cta_red) return;
-  int bc[3];
-  morton_decode(b, 3, L, bc);
-  const int g = lane >> 2, q = lane & 3;
-  // B fragments of mode z: X[a = g, t, c = 4 ks + q]
-  double xv[kSepP][2];
-  if (!valid) {
+__global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L,
+                                                          int R, UpParams up, int64_t nb, const double* __restrict__ u,
+                                                          double* __restrict__ ub_out, int n) {
+  // CTA = the 8 sibling leaf boxes of one parent cluster (Morton ids
+  // 8 blockIdx.x + w) for rhs blockIdx.y.  The 16^3-point cube is read once
+  // (rows of 16 contiguous points of the F-order u, or the boxes of ub) into
+  // shared memory at the pitched box layout, written to ub, and every level's
+  // mode products read it from there; the 8 boxes' W contributions are summed
+  // in shared memory (two halves) before one RED per W entry.
+  constexpr int BP = kSepBoxSmem;   // 8 z-planes at a pitch of 68: mode-z B fragments conflict free
+  extern __shared__ __align__(16) double smu[];
+  double* box = smu;                // [8][BP]
+  double* red = smu + 8 * BP;       // [8][256]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int64_t bb = 8 * (int64_t)blockIdx.x;
+  if (bb >= nb) return;
+  int c0[3];
+  morton_decode(bb, 3, L, c0);   // even coordinates: the cube origin in boxes
+  if (u) {
+    // row (yy, zz) of the cube: 16 points along x (boxes x = 0, 1); 256
+    // threads x 8 double2 each, every load in flight before the first store
+    double2 v[8];
+    const int xx2 = threadIdx.x & 7, xx = 2 * xx2;
 #pragma unroll
-    for (int t = 0; t < kSepP; ++t) xv[t][0] = xv[t][1] = 0.0;
-  } else if (u) {
-    // fused permute: the box's points from the F-order vector, written to ub
-    const int64_t g0 = (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP) +
-                       (int64_t)n * n * (bc[2] * kSepP + q);
-    double* d = ub_out + (b * R + r) * (int64_t)ldub + g + zpub * q;
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) {
-      xv[t][0] = __ldg(u + (g0 + (int64_t)n * t) * R + r);
-      xv[t][1] = __ldg(u + (g0 + (int64_t)n * t + (int64_t)n * n * 4) * R + r);
-      d[8 * t] = xv[t][0];
-      d[8 * t + 4 * zpub] = xv[t][1];
+    for (int it = 0; it < 8; ++it) {
+      const int row = (threadIdx.x >> 3) + 32 * it, yy = row & 15, zz = row >> 4;
+      const int64_t gi = (int64_t)(c0[0] * kSepP + xx) + (int64_t)n * (c0[1] * kSepP + yy) +
+                         (int64_t)n * n * (c0[2] * kSepP + zz);
+      if (R == 1) {
+        v[it] = __ldg(reinterpret_cast<const double2*>(u + gi));
+      } else {
+        v[it].x = __ldg(u + gi * R + r);
+        v[it].y = __ldg(u + (gi + 1) * R + r);
+      }
     }
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int row = (threadIdx.x >> 3) + 32 * it, yy = row & 15, zz = row >> 4;
+      const int wb = ((xx >> 3) << 2) | ((yy >> 3) << 1) | (zz >> 3);   // sibling (Morton child order)
+      double* d = box + wb * BP + (xx & 7) + 8 * (yy & 7) + zpub * (zz & 7);
+      d[0] = v[it].x;
+      d[1] = v[it].y;
+    }
+    __syncthreads();
+    // the permute: every box to ub, pitched as staged
+    double* o = ub_out + ((bb + w) * R + r) * (int64_t)ldub;
+    for (int e = lane; e < BP / 2; e += 32)
+      reinterpret_cast<double2*>(o)[e] = reinterpret_cast<const double2*>(box + w * BP)[e];
   } else {
-    const double* s = ub + (b * R + r) * (int64_t)ldub + g + zpub * q;
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) {
-      xv[t][0] = __ldg(s + 8 * t);
-      xv[t][1] = __ldg(s + 8 * t + 4 * zpub);
-    }
+    const double* sbx = ub + ((bb + w) * R + r) * (int64_t)ldub;
+    for (int e = lane; e < BP / 2; e += 32)
+      reinterpret_cast<double2*>(box + w * BP)[e] = __ldg(reinterpret_cast<const double2*>(sbx) + e);
+    __syncthreads();
   }
+  int bc[3];
+  morton_decode(bb + w, 3, L, bc);
+  const int g = lane >> 2, q = lane & 3;
+  const double* xs = box + w * BP + g + zpub * q;
   for (int li = 0; li < up.nlev; ++li) {
     const UpLevel8 lv = up.lev[li];
     const int shift = L - lv.level, mask = (1 << shift) - 1;
-    const int64_t anc = b >> (3 * shift);
     const double* Qx = lv.Q + (int64_t)((bc[0] & mask) * kSepP) * kSepP;
     const double* Qy = lv.Q + (int64_t)((bc[1] & mask) * kSepP) * kSepP;
     const double* Qz = lv.Q + (int64_t)((bc[2] & mask) * kSepP) * kSepP;
-    // mode z: Z_t[k', a] = sum_c Qz[c][k'] X[a, t, c]  (A[m = k'][k = c] = Qz[c][k'])
-    double z[kSepP][2];
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) z[t][0] = z[t][1] = 0.0;
+    // mode z: Z_t[k', a] = sum_c Qz[c][k'] X[a, t, c]; mode x: T_t[i, k'] =
+    // sum_a Qx[a][i] Z_t[k', a] (the C fragment reused as B, k order
+    // permuted); mode y: W[i, j, k'] += Qy[t][j] T_t[i, k'] -- one t at a time
     const double az0 = __ldg(Qz + q * kSepP + g), az1 = __ldg(Qz + (4 + q) * kSepP + g);
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az0, xv[t][0]);
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) dmma(z[t][0], z[t][1], az1, xv[t][1]);
-    // mode x (C fragment reused as B, k order permuted): T_t[i, k'] =
-    // sum_a Qx[a][i] Z_t[k', a], A[m = i][k = 2 q + ks] = Qx[2 q + ks][i]
     const double bx0 = __ldg(Qx + (2 * q) * kSepP + g), bx1 = __ldg(Qx + (2 * q + 1) * kSepP + g);
     double y[kSepP][2];
 #pragma unroll
     for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
 #pragma unroll
     for (int t = 0; t < kSepP; ++t) {
-      double t0 = 0.0, t1 = 0.0;
-      dmma(t0, t1, bx0, z[t][0]);
-      dmma(t0, t1, bx1, z[t][1]);
-      // mode y: W[i, j, k'] += Qy[t][j] T_t[i, k']
+      double z0 = 0.0, z1 = 0.0, t0 = 0.0, t1 = 0.0;
+      dmma(z0, z1, az0, xs[8 * t]);
+      dmma(z0, z1, az1, xs[8 * t + 4 * zpub]);
+      dmma(t0, t1, bx0, z0);
+      dmma(t0, t1, bx1, z1);
 #pragma unroll
       for (int j = 0; j < kSepP; ++j) {
         const double m = __ldg(Qy + t * kSepP + j);
@@ -841,29 +875,25 @@ __global__ void __launch_bounds__(256) upward8_kernel(const double* __restrict__
         y[j][1] = fma(m, t1, y[j][1]);
       }
     }
-    // lane holds (i = g, j, k' = 2 q + jj)
-    if (cta_red) {
+    // lane holds (i = g, j, k' = 2 q + jj); sum the 8 boxes, half the j at a time
+    const int64_t anc = bb >> (3 * shift);
+    double* W = lv.W + (anc * R + r) * (int64_t)lv.K_pad;
+#pragma unroll
+    for (int hj = 0; hj < 2; ++hj) {
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < kSepP; ++j) {
-        red[warp][g + 8 * j + 128 * q] = y[j][0];
-        red[warp][g + 8 * j + 128 * q + 64] = y[j][1];
+      for (int j = 0; j < 4; ++j) {
+        red[w * 256 + g + 8 * j + 64 * q] = y[4 * hj + j][0];
+        red[w * 256 + g + 8 * j + 64 * q + 32] = y[4 * hj + j][1];
       }
       __syncthreads();
-      const int64_t b0 = (wi - warp) % nb;   // the CTA's first box (same parent)
-      const int64_t anc0 = b0 >> (3 * shift);
-      for (int e = threadIdx.x; e < 512; e += blockDim.x) {
+      {
+        const int e = threadIdx.x;   // 256 entries: (i, j', k') = (e & 7, (e >> 3) & 3, 2 (e >> 6) + ((e >> 5) & 1))
         double v = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) v += red[w][e];
-        atomicAdd(lv.W + (anc0 * R + r) * (int64_t)lv.K_pad + (e & 63) + lv.zpitch * (e >> 6), v);
-      }
-    } else {
-      double* o = lv.W + (anc * R + r) * (int64_t)lv.K_pad + g + lv.zpitch * 2 * q;
-#pragma unroll
-      for (int j = 0; j < kSepP; ++j) {
-        atomicAdd(o + 8 * j, y[j][0]);
-        atomicAdd(o + 8 * j + lv.zpitch, y[j][1]);
+        for (int ww = 0; ww < 8; ++ww) v += red[ww * 256 + e];
+        const int i = e & 7, jl = (e >> 3) & 3, kk = 2 * (e >> 6) + ((e >> 5) & 1);
+        atomicAdd(W + i + 8 * (4 * hj + jl) + lv.zpitch * kk, v);
       }
     }
   }
@@ -877,7 +907,7 @@ bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
     const char* e = std::getenv("HTLR_DOWN8");
     off = (e && e[0] == '0') ? 1 : 0;
   }
-  if (off || d != 3 || p != kSepP || sL != kSepP) return false;
+  if (off || d != 3 || p != kSepP || sL != kSepP || dp.nlev > kMaxDown8) return false;
   for (int i = 0; i < dp.nlev; ++i)
     if (dp.lev[i].K || dp.lev[i].qstride || dp.lev[i].P != kSepP * kSepP * kSepP) return false;
   return true;
@@ -894,18 +924,32 @@ bool upward8_supported(int d, int p, int sL) {
 
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
                     cudaStream_t st, const double* u, double* ub_out, int n) {
-  const int64_t warps = nb * R;
-  if (warps <= 0 || (up.nlev == 0 && !u)) return;
-  upward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb, u, ub_out,
-                                                               n);
+  if (nb <= 0 || (up.nlev == 0 && !u)) return;
+  // sibling groups of 8 boxes; the pitched box layout is what every caller
+  // passes (zpub = kSepZPitch, ldub >= 8 zpub)
+  const size_t smem = (size_t)(8 * kSepBoxSmem + 8 * 256) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(upward8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  upward8_kernel<<<dim3((unsigned)((nb + 7) / 8), R), 256, smem, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb, u,
+                                                                       ub_out, n);
 }
 
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
                       int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st, int zlo, int zhi) {
-  const int64_t warps = nb * R;
-  if (warps <= 0) return;
-  downward8_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0, nb, zlo,
-                                                                zhi);
+  if (nb <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(downward8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((kMaxDown8 * kSepP * kSepZPitch + 8 * kSepP * 66) * sizeof(double)));
+    attr = true;
+  }
+  const size_t smem = ((size_t)std::min(dp.nlev, kMaxDown8) * kSepP * kSepZPitch + 8 * kSepP * 66) * sizeof(double);
+  // sibling groups of 8 (b0 and nb are whole subtrees of the Morton order)
+  downward8_kernel<<<dim3((unsigned)((nb + 7) / 8), R), 256, smem, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0,
+                                                                         nb, zlo, zhi);
 }
 
 // HTLR_SEP_GROUPS=1|2: consumer warp groups of the cooperative kernel
