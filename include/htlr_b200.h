@@ -128,6 +128,21 @@ int htlr_set_lowrank(htlr_plan* plan, int32_t on);
  * target rows, its leaf boxes and its source clusters' upward data.
  * Call htlr_set_shard before htlr_build_lists / htlr_construct. */
 int htlr_set_shard(htlr_plan* plan, int32_t rank, int32_t world);
+/* z-slab shards of a banded separable plan (3-D Gaussian, eta = 1, p = leaf
+ * side = 8; BASELINE config 4), set after htlr_construct on an unsharded plan:
+ * shard `rank` of `world` owns the leaf boxes with z in
+ * [rank, rank+1) * 2^L / world.  Every shard holds the whole input u; the
+ * local phase adds the own boxes' upward contributions into the W_l exchange
+ * buffers, which the caller then SUM-reduces across shards (all-reduce, see
+ * htlr_exchange_kind); the remote phase runs the banded passes over the z
+ * range of each level that holds the own boxes (the z sweep reads the halo
+ * from u itself, so there is no other exchange), the downward pass, and
+ * writes the f rows of the own boxes -- a contiguous block of the F-order f.
+ * world = 1 restores the whole plan.  No reference counterpart. */
+int htlr_set_zslab(htlr_plan* plan, int32_t rank, int32_t world);
+/* How the exchange buffers are combined across shards: 0 all-gather (shard
+ * r's chunk is the r-th 1/world of each buffer), 1 sum (all-reduce). */
+int htlr_exchange_kind(const htlr_plan* plan);
 /* Owned leaf-box range (Morton ids), owned (target, source) pairs and their
  * GEMM flops per right-hand side. */
 int htlr_shard_info(const htlr_plan* plan, int64_t* own_leaf_lo, int64_t* own_leaf_hi,

@@ -60,6 +60,8 @@ SYMBOLS = [
     ("htlr_matvec_remote_finish", ctypes.c_int, [_P, _P, _P, _I64, _P]),
     ("htlr_set_lowrank", ctypes.c_int, [_P, _I32]),
     ("htlr_set_shard", ctypes.c_int, [_P, _I32, _I32]),
+    ("htlr_set_zslab", ctypes.c_int, [_P, _I32, _I32]),
+    ("htlr_exchange_kind", ctypes.c_int, [_P]),
     ("htlr_shard_info", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                        ctypes.POINTER(_D)]),
     ("htlr_exchange_info", ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), _P, _I64]),

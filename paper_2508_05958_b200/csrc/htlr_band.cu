@@ -144,7 +144,7 @@ __device__ __forceinline__ void stage_tables(double* __restrict__ dst, const dou
 // SLOT 0: standard A fragments, 64: the mode-x (permuted k) ones.
 template <int NB, int T, int SLOT, bool SIGN, int B0 = 0, int B1 = NB>
 __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO, int lane, const double (&in)[NB][2],
-                                          double (&acc)[NB][2]) {
+                                          double (&acc)[NB][2], int tlo = 0, int thi = NB) {
   constexpr int kind = T >= 4 ? 1 : 0;
   const int OR = (NO - 1) / 2;
 #pragma unroll
@@ -159,12 +159,12 @@ __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO
 #pragma unroll
     for (int b = B0; b < B1; ++b) {
       const int s = b + boff<T>(b & 1, i);
-      if (s >= 0 && s < NB) dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, in[s][0]);
+      if (s >= 0 && s < NB && b >= tlo && b < thi) dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, in[s][0]);
     }
 #pragma unroll
     for (int b = B0; b < B1; ++b) {
       const int s = b + boff<T>(b & 1, i);
-      if (s >= 0 && s < NB) dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, in[s][1]);
+      if (s >= 0 && s < NB && b >= tlo && b < thi) dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, in[s][1]);
     }
   }
 }
@@ -216,14 +216,28 @@ constexpr int kLineWarps = 12;
 template <int NB, int NT, bool R1, int HALF>
 __device__ __forceinline__ void line_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
                                            const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
-                                           int u0, int ustride, int nunits) {
+                                           int u0, int ustride, int nunits, int usel, int n, int zlo, int zhi) {
   constexpr int H = NB / 2;
   constexpr int S0 = HALF ? (H - 5 > 0 ? H - 5 : 0) : 0;         // loaded source boxes [S0, S1)
   constexpr int S1 = HALF ? NB : (H + 5 < NB ? H + 5 : NB);
   const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  // unit -> line: both halves active: u >> 1; one half: u
+  auto line_of = [&](int u) { return usel ? u : (u >> 1); };
   auto load = [&](int u, double(&in)[NB][2]) {
-    const int line = u >> 1;
+    const int line = line_of(u);
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
+    if (n) {
+      // straight from the F-order grid vector: box (bx, by, b), point
+      // (x = g, y, z = q (+4)) at (8 bx + g) + n (8 by + y) + n^2 (8 b + q)
+      const int64_t n2 = (int64_t)n * n;
+      const double* s = ub + ((int64_t)(8 * (col % NB) + g) + (int64_t)n * (8 * (col / NB) + y) + n2 * q) * R + r;
+#pragma unroll
+      for (int b = S0; b < S1; ++b) {
+        in[b][0] = __ldg(s + 8 * b * n2 * R);
+        in[b][1] = __ldg(s + (8 * b + 4) * n2 * R);
+      }
+      return;
+    }
     const double* s = ub + (morton3(col % NB, col / NB, 0) * R + r) * ldub + 8 * y + g + zpub * q;
 #pragma unroll
     for (int b = S0; b < S1; ++b) {
@@ -233,7 +247,7 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
     }
   };
   auto compute = [&](int u, const double(&in)[NB][2]) {
-    const int line = u >> 1;
+    const int line = line_of(u);
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
     // lane's C fragment: (z' = g, x = 2q + j) of every target box
     double* const ob = ws + (morton3(col % NB, col / NB, 0) * R + r) * 512 + 64 * g + 8 * y + 2 * q;
@@ -241,11 +255,12 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
       constexpr int T = decltype(tc)::value;
       double acc[NB][2];
       zero(acc);
-      band_regs<NB, T, 0, false, HALF * H, HALF * H + H>(tab, NO, lane, in, acc);
+      band_regs<NB, T, 0, false, HALF * H, HALF * H + H>(tab, NO, lane, in, acc, zlo, zhi);
       double* o = ob + T * tstride;
 #pragma unroll
       for (int b = HALF * H; b < HALF * H + H; ++b)
-        *reinterpret_cast<double2*>(o + spread3(b) * (int64_t)R * 512) = make_double2(acc[b][0], acc[b][1]);
+        if (b >= zlo && b < zhi)
+          *reinterpret_cast<double2*>(o + spread3(b) * (int64_t)R * 512) = make_double2(acc[b][0], acc[b][1]);
     };
     // a runtime loop over the terms: the compiler cannot interleave (and keep
     // live) several terms' accumulators
@@ -277,21 +292,131 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
   }
 }
 
+// Pair units (z-slab shards narrower than half a line): unit = (line, own
+// sibling pair p): targets 2p, 2p + 1 and the 12 source boxes 2p - 5 ...
+// 2p + 6, indexed relative to the pair so every register index is static
+// (boxes outside the level are loaded as zeros and contribute nothing).
+// Restricting a half-line unit's targets by a runtime test would not save
+// the work: predicated-off DMMAs still occupy the tensor pipe.
+template <int NB, int T>
+__device__ __forceinline__ void band_pair(const double* __restrict__ tab, int NO, int lane, const double (&in)[12][2],
+                                          double (&acc)[2][2]) {
+  constexpr int kind = T >= 4 ? 1 : 0;
+  const int OR = (NO - 1) / 2;
+#pragma unroll
+  for (int i = 0; i < bcount<T>(); ++i) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const double* p0 = tab + (kind * NO + boff<T>(0, i) + OR) * kTabSlot;
+    const double* p1 = tab + (kind * NO + boff<T>(1, i) + OR) * kTabSlot;
+    const double a00 = lds(p0 + lane), a01 = lds(p0 + 32 + lane);
+    const double a10 = lds(p1 + lane), a11 = lds(p1 + 32 + lane);
+    const int s0 = boff<T>(0, i) + 5, s1 = boff<T>(1, i) + 6;   // relative source boxes of 2p, 2p + 1
+    dmma(acc[0][0], acc[0][1], a00, in[s0][0]);
+    dmma(acc[1][0], acc[1][1], a10, in[s1][0]);
+    dmma(acc[0][0], acc[0][1], a01, in[s0][1]);
+    dmma(acc[1][0], acc[1][1], a11, in[s1][1]);
+  }
+}
+
+template <int NB, int NT, bool R1>
+__device__ __forceinline__ void pair_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
+                                           const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
+                                           int u0, int ustride, int n, int zlo, int zhi) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int npairs = (zhi - zlo) >> 1;
+  const int nunits = NB * NB * 8 * R * npairs;
+  auto load = [&](int u, double(&in)[12][2]) {
+    const int line = u / npairs, p = (zlo >> 1) + u % npairs;
+    const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
+    const int64_t n2 = (int64_t)n * n;
+    const double* sf = ub + ((int64_t)(8 * (col % NB) + g) + (int64_t)n * (8 * (col / NB) + y) + n2 * q) * R + r;
+    const double* sb = ub + (morton3(col % NB, col / NB, 0) * R + r) * ldub + 8 * y + g + zpub * q;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int b = 2 * p - 5 + i;
+      if (b < 0 || b >= NB) {
+        in[i][0] = in[i][1] = 0.0;
+      } else if (n) {
+        in[i][0] = __ldg(sf + 8 * b * n2 * R);
+        in[i][1] = __ldg(sf + (8 * b + 4) * n2 * R);
+      } else {
+        const double* s = sb + spread3(b) * (int64_t)R * ldub;
+        in[i][0] = __ldg(s);
+        in[i][1] = __ldg(s + 4 * zpub);
+      }
+    }
+  };
+  auto compute = [&](int u, const double(&in)[12][2]) {
+    const int line = u / npairs, p = (zlo >> 1) + u % npairs;
+    const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
+    // boxes 2p, 2p + 1: Morton ids m(bx, by, 0) + spread3(2p) (+ 1)
+    double* const ob = ws + ((morton3(col % NB, col / NB, 0) + spread3(2 * p)) * R + r) * 512 + 64 * g + 8 * y + 2 * q;
+    auto term = [&](auto tc) {
+      constexpr int T = decltype(tc)::value;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      band_pair<NB, T>(tab, NO, lane, in, acc);
+      double* o = ob + T * tstride;
+      *reinterpret_cast<double2*>(o) = make_double2(acc[0][0], acc[0][1]);
+      *reinterpret_cast<double2*>(o + (int64_t)R * 512) = make_double2(acc[1][0], acc[1][1]);
+    };
+#pragma unroll 1
+    for (int t = 0; t < NT; ++t) {
+      switch (t) {
+        case 0: term(std::integral_constant<int, 0>{}); break;
+        case 1: term(std::integral_constant<int, 1>{}); break;
+        case 2: term(std::integral_constant<int, 2>{}); break;
+        case 3: term(std::integral_constant<int, 3>{}); break;
+        case 4: term(std::integral_constant<int, 4>{}); break;
+        default: term(std::integral_constant<int, 5>{}); break;
+      }
+    }
+  };
+  double a[12][2], b[12][2];
+  int u = u0;
+  if (u < nunits) load(u, a);
+  __syncthreads();
+  while (u < nunits) {
+    const int un = u + ustride;
+    if (un < nunits) load(un, b);
+    compute(u, a);
+    if (un >= nunits) break;
+    const int unn = un + ustride;
+    if (unn < nunits) load(unn, a);
+    compute(un, b);
+    u = unn;
+  }
+}
+
+// src: the level's boxes [box][rhs][ldub] (z pitch zpub), or with n > 0 the
+// F-order grid vector u[N][R] of an n^3 grid (the leaf pass reads u itself:
+// no permuted copy).  Targets are written for z boxes [zlo, zhi) only (a
+// z-slab shard); halves without an own box are skipped.
 template <int NB, int NT, bool R1>
 __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
                                                                       int R_, const double* __restrict__ ub, int ldub,
                                                                       int zpub, double* __restrict__ ws,
-                                                                      int64_t tstride) {
+                                                                      int64_t tstride, int n, int zlo, int zhi) {
   const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
   __shared__ double tab[2 * 15 * kTabSlot];
   stage_tables<64>(tab, tables, NO);   // line_units syncs after issuing its first loads
   const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
   const int ustride = gridDim.x * (blockDim.x >> 5);
-  const int nunits = 2 * NB * NB * 8 * R;
-  if (gw & 1)
-    line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nunits);
-  else
-    line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nunits);
+  const int nlines = NB * NB * 8 * R;
+  const bool h0 = zlo < NB / 2, h1 = zhi > NB / 2;
+  const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
+  if (!halves) {   // a z-slab shard narrower than a half line: whole sibling pairs
+    pair_units<NB, NT, R1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, n, zlo & ~1, (zhi + 1) & ~1);
+  } else if (h0 && h1) {   // both halves: the parity of the (even-strided) unit picks the half
+    if (gw & 1)
+      line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+    else
+      line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+  } else if (h1) {
+    line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+  } else {
+    line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+  }
 }
 
 // y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
@@ -300,7 +425,8 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
                                                                 const double* __restrict__ ub, int ldub, int zpub,
                                                                 const double* __restrict__ ws, int64_t tstride,
                                                                 double* __restrict__ Y,
-                                                                const double* __restrict__ corr_ptr, double scale) {
+                                                                const double* __restrict__ corr_ptr, double scale,
+                                                                int n, int zlo) {
   constexpr int NQ = NB / 4;   // quarters of a row of cells (4 cells = 16 TMEM columns)
   const int R = R1 ? 1 : R_;
   extern __shared__ __align__(16) double smp[];
@@ -315,7 +441,7 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   stage_tables<128>(tab, tables, NO);
-  const int zl = blockIdx.x & 7, bz = blockIdx.x >> 3, r = blockIdx.y;
+  const int zl = blockIdx.x & 7, bz = zlo + (blockIdx.x >> 3), r = blockIdx.y;
   const int g = lane >> 2, q = lane & 3;
   // y line of box column bx = w: element (y = q (+4), x = g) of z plane zl;
   // box (w, b, bz) has Morton id morton3(w, 0, bz) + 2 spread3(b)
@@ -396,11 +522,15 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
     for (int c = 0; c < 4; ++c) {
       const int64_t m = mw + (int64_t)(spread3(4 * Q + c) << 2) * R;
       double* o = Y + m * 512 + 64 * zl + 16 * q + g;
-      const double* us = ub + m * ldub + zpub * zl + 16 * q + g;
+      // the self pair's point: box (4Q + c, w, bz), element (x = g, y = 2q + j, zl)
+      const double* us = n ? ub + ((int64_t)(8 * (4 * Q + c) + g) + (int64_t)n * (8 * w + 2 * q) +
+                                   (int64_t)n * n * (8 * bz + zl)) * R + r
+                           : ub + m * ldub + zpub * zl + 16 * q + g;
+      const int64_t ustep = n ? (int64_t)n * R : 8;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         double val = scale * v[c][j];
-        if (corr_ptr) val = fma(cv, __ldg(us + 8 * j), val);
+        if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
         o[8 * j] = val;
       }
     }
@@ -410,9 +540,222 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_sh), "n"(plane_tmem_cols(NB)));
 }
 
+// The y and x sweeps as line kernels (the plane kernel's alternative for
+// z-slab shards, whose few planes would occupy few SMs): every unit is a half
+// line of one z-point plane, so a slab's sweeps spread over all SMs, and the
+// slab's term buffers (1/world of the level's) stay in L2 between them.
+//
+// band_yline_kernel: unit = (term t, box column bx, z box bz, z point zl,
+// half): the y line of z-swept term t (ws, [term][box][rhs][512], element
+// 64 zl + 8 y + x) -> y-swept cells in the x sweep's B-fragment order (ws2,
+// [term][box][rhs][zl][lane][2]).
+template <int NB, int NT, bool R1, int HALF>
+__device__ __forceinline__ void yline_units(const double* __restrict__ tab, int NO, int R, const double* __restrict__ ws,
+                                            double* __restrict__ ws2, int64_t tstride, int u0, int ustride,
+                                            int nunits, int zlo, int nz) {
+  constexpr int H = NB / 2;
+  constexpr int S0 = HALF ? (H - 5 > 0 ? H - 5 : 0) : 0;
+  constexpr int S1 = HALF ? NB : (H + 5 < NB ? H + 5 : NB);
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  // unit u: half = u & 1 (the warp's), then bx, zl, bz, r, t (slowest)
+  struct Line {
+    int t, bx, bz, zl, r;
+  };
+  auto decode = [&](int u) {
+    int v = u >> 1;
+    Line l;
+    l.bx = v % NB;
+    v /= NB;
+    l.zl = v & 7;
+    v >>= 3;
+    l.bz = zlo + v % nz;
+    v /= nz;
+    l.r = v % R;
+    l.t = v / R;
+    return l;
+  };
+  auto base = [&](const Line& l) {   // box (bx, by = 0, bz): Morton id + 2 spread3(by) per by
+    return (morton3(l.bx, 0, l.bz) * R + l.r) * 512;
+  };
+  auto load = [&](int u, double(&in)[NB][2]) {
+    const Line l = decode(u);
+    const double* s = ws + l.t * tstride + base(l) + 64 * l.zl + 8 * q + g;
+#pragma unroll
+    for (int b = S0; b < S1; ++b) {
+      const double* sb = s + (int64_t)(2 * spread3(b)) * R * 512;
+      in[b][0] = __ldg(sb);
+      in[b][1] = __ldg(sb + 32);
+    }
+  };
+  auto compute = [&](int u, const double(&in)[NB][2]) {
+    const Line l = decode(u);
+    double* o = ws2 + l.t * tstride + base(l) + 64 * l.zl + 2 * lane;
+    auto term = [&](auto tc) {
+      constexpr int T = decltype(tc)::value;
+      double acc[NB][2];
+      zero(acc);
+      band_regs<NB, T, 0, false, HALF * H, HALF * H + H>(tab, NO, lane, in, acc);
+#pragma unroll
+      for (int b = HALF * H; b < HALF * H + H; ++b)
+        *reinterpret_cast<double2*>(o + (int64_t)(2 * spread3(b)) * R * 512) = make_double2(acc[b][0], acc[b][1]);
+    };
+    switch (l.t) {
+      case 0: term(std::integral_constant<int, 0>{}); break;
+      case 1: term(std::integral_constant<int, 1>{}); break;
+      case 2: term(std::integral_constant<int, 2>{}); break;
+      case 3: term(std::integral_constant<int, 3>{}); break;
+      case 4: if (NT > 4) term(std::integral_constant<int, 4>{}); break;
+      default: if (NT > 4) term(std::integral_constant<int, 5>{}); break;
+    }
+  };
+  double a[NB][2], b[NB][2];
+  int u = u0;
+  if (u < nunits) load(u, a);
+  __syncthreads();
+  while (u < nunits) {
+    const int un = u + ustride;
+    if (un < nunits) load(un, b);
+    compute(u, a);
+    if (un >= nunits) break;
+    const int unn = un + ustride;
+    if (unn < nunits) load(unn, a);
+    compute(un, b);
+    u = unn;
+  }
+}
+
+template <int NB, int NT, bool R1>
+__global__ void __launch_bounds__(kLineWarps * 32, 1) band_yline_kernel(const double* __restrict__ tables, int NO,
+                                                                       int R_, const double* __restrict__ ws,
+                                                                       double* __restrict__ ws2, int64_t tstride,
+                                                                       int zlo, int nz) {
+  const int R = R1 ? 1 : R_;
+  __shared__ double tab[2 * 15 * kTabSlot];
+  stage_tables<64>(tab, tables, NO);
+  const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
+  const int ustride = gridDim.x * (blockDim.x >> 5);
+  const int nunits = 2 * NT * R * nz * 8 * NB;
+  if (gw & 1)
+    yline_units<NB, NT, R1, 1>(tab, NO, R, ws, ws2, tstride, gw, ustride, nunits, zlo, nz);
+  else
+    yline_units<NB, NT, R1, 0>(tab, NO, R, ws, ws2, tstride, gw, ustride, nunits, zlo, nz);
+}
+
+// band_xline_kernel: unit = (box row by, z box bz, z point zl, half): the x
+// line of every term's y-swept cells (ws2), the term's sign folded into the
+// mode-x A fragments, summed in registers (the next term's line loads while
+// the current one computes); Y = scale * sum + corr * u (self pairs).
+template <int NB, int NT, bool R1, int HALF>
+__device__ __forceinline__ void xline_units(const double* __restrict__ tab, int NO, int R, const double* __restrict__ ws2,
+                                            int64_t tstride, double* __restrict__ Y, const double* __restrict__ src,
+                                            int ldub, int zpub, int n, const double* __restrict__ corr_ptr,
+                                            double scale, int u0, int ustride, int nunits, int zlo, int nz) {
+  constexpr int H = NB / 2;
+  constexpr int S0 = HALF ? (H - 5 > 0 ? H - 5 : 0) : 0;
+  constexpr int S1 = HALF ? NB : (H + 5 < NB ? H + 5 : NB);
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const double cv = corr_ptr ? corr_ptr[0] : 0.0;
+  for (int u = u0; u < nunits; u += ustride) {
+    int v = u >> 1;
+    const int by = v % NB;
+    v /= NB;
+    const int zl = v & 7;
+    v >>= 3;
+    const int bz = zlo + v % nz, r = v / nz;
+    // cell (bx, by, bz): Morton id morton3(0, by, bz) + 4 spread3(bx)
+    const int64_t m0 = morton3(0, by, bz) * R + r;
+    const double* s = ws2 + m0 * 512 + 64 * zl + 2 * lane;
+    double bufa[NB][2], bufb[NB][2], acc[NB][2];
+    zero(acc);
+    auto load = [&](int t, double(&in)[NB][2]) {
+      const double* st = s + t * tstride;
+#pragma unroll
+      for (int b = S0; b < S1; ++b) {
+        const double2 w2 = __ldg(reinterpret_cast<const double2*>(st + (int64_t)(4 * spread3(b)) * R * 512));
+        in[b][0] = w2.x;
+        in[b][1] = w2.y;
+      }
+    };
+    load(0, bufa);
+    load(1, bufb);
+    band_regs<NB, 0, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+    load(2, bufa);
+    band_regs<NB, 1, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+    load(3, bufb);
+    band_regs<NB, 2, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+    if (NT > 4) load(4, bufa);
+    band_regs<NB, 3, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+    if (NT > 4) {
+      load(5, bufb);
+      band_regs<NB, 4, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+      band_regs<NB, 5, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+    }
+    // lane holds (x' = g, y = 2q + j) of target cells bx in the half
+#pragma unroll
+    for (int bx = HALF * H; bx < HALF * H + H; ++bx) {
+      const int64_t m = m0 + (int64_t)(4 * spread3(bx)) * R;
+      double* o = Y + m * 512 + 64 * zl + 16 * q + g;
+      const double* us = n ? src + ((int64_t)(8 * bx + g) + (int64_t)n * (8 * by + 2 * q) +
+                                    (int64_t)n * n * (8 * bz + zl)) * R + r
+                           : src + m * ldub + zpub * zl + 16 * q + g;
+      const int64_t ustep = n ? (int64_t)n * R : 8;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double val = scale * acc[bx][j];
+        if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
+        o[8 * j] = val;
+      }
+    }
+  }
+}
+
+template <int NB, int NT, bool R1>
+__global__ void __launch_bounds__(kLineWarps * 32, 1) band_xline_kernel(const double* __restrict__ tables, int NO,
+                                                                       int R_, const double* __restrict__ ws2,
+                                                                       int64_t tstride, double* __restrict__ Y,
+                                                                       const double* __restrict__ src, int ldub,
+                                                                       int zpub, int n,
+                                                                       const double* __restrict__ corr_ptr,
+                                                                       double scale, int zlo, int nz) {
+  const int R = R1 ? 1 : R_;
+  __shared__ double tab[2 * 15 * kTabSlot];
+  stage_tables<128>(tab, tables, NO);
+  __syncthreads();
+  const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
+  const int ustride = gridDim.x * (blockDim.x >> 5);
+  const int nunits = 2 * R * nz * 8 * NB;
+  if (gw & 1)
+    xline_units<NB, NT, R1, 1>(tab, NO, R, ws2, tstride, Y, src, ldub, zpub, n, corr_ptr, scale, gw, ustride, nunits,
+                               zlo, nz);
+  else
+    xline_units<NB, NT, R1, 0>(tab, NO, R, ws2, tstride, Y, src, ldub, zpub, n, corr_ptr, scale, gw, ustride, nunits,
+                               zlo, nz);
+}
+
+template <int NB, int NT>
+void launch_ylines_t(const double* tab, int NO, int R, const double* ws, double* ws2, double* Y, const double* src,
+                     int ldub, int zpub, int n, const double* corr, double scale, cudaStream_t st, int zlo, int zhi) {
+  const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nz = zhi - zlo;
+  const int64_t yunits = 2LL * NT * R * nz * 8 * NB;
+  const int gy = (int)std::min<int64_t>(sms, std::max<int64_t>(1, yunits / (2 * kLineWarps)));
+  if (R == 1) {
+    band_yline_kernel<NB, NT, true><<<gy, kLineWarps * 32, 0, st>>>(tab, NO, R, ws, ws2, tstride, zlo, nz);
+    band_xline_kernel<NB, NT, true><<<sms, kLineWarps * 32, 0, st>>>(tab, NO, R, ws2, tstride, Y, src, ldub, zpub, n,
+                                                                     corr, scale, zlo, nz);
+  } else {
+    band_yline_kernel<NB, NT, false><<<gy, kLineWarps * 32, 0, st>>>(tab, NO, R, ws, ws2, tstride, zlo, nz);
+    band_xline_kernel<NB, NT, false><<<sms, kLineWarps * 32, 0, st>>>(tab, NO, R, ws2, tstride, Y, src, ldub, zpub,
+                                                                      n, corr, scale, zlo, nz);
+  }
+}
+
 template <int NB, int NT>
 void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, double* ws,
-                    cudaStream_t st) {
+                    cudaStream_t st, int n, int zlo, int zhi) {
   const int64_t lines = (int64_t)NB * NB * 8 * R;
   const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
   int dev = 0, sms = 148;
@@ -423,14 +766,17 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
   const int warps = kLineWarps;
   if (R == 1)
-    band_line_kernel<NB, NT, true><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+    band_line_kernel<NB, NT, true><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n,
+                                                                           zlo, zhi);
   else
-    band_line_kernel<NB, NT, false><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride);
+    band_line_kernel<NB, NT, false><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n,
+                                                                            zlo, zhi);
 }
 
 template <int NB, int NT>
 void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, const double* ws,
-                     double* Y, const double* corr, double scale, cudaStream_t st) {
+                     double* Y, const double* corr, double scale, cudaStream_t st, int n, int zlo, int zhi) {
+  if (zhi <= zlo) return;
   const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
   const size_t smem = (size_t)NB * NB * 32 * sizeof(double2) + (size_t)2 * NO * kTabSlot * sizeof(double);
   static bool attr = false;
@@ -440,11 +786,11 @@ void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldu
     attr = true;
   }
   if (R == 1)
-    band_plane_kernel<NB, NT, true><<<dim3(8 * NB, R), NB * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride,
-                                                                            Y, corr, scale);
+    band_plane_kernel<NB, NT, true><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
+        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo);
   else
-    band_plane_kernel<NB, NT, false><<<dim3(8 * NB, R), NB * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride,
-                                                                             Y, corr, scale);
+    band_plane_kernel<NB, NT, false><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
+        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo);
 }
 
 }  // namespace
@@ -452,25 +798,45 @@ void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldu
 bool band_lines_supported(int L) { return L >= 2 && L <= 4; }
 
 void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                       double* ws, cudaStream_t st) {
+                       double* ws, cudaStream_t st, int n, int zlo, int zhi) {
   zpub = zpub ? zpub : 64;
-  if (L == 4) nterms == 6 ? launch_lines_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
-                          : launch_lines_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
-  else if (L == 3) nterms == 6 ? launch_lines_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
-                               : launch_lines_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
-  else nterms == 6 ? launch_lines_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, st)
-                   : launch_lines_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, st);
+  const int nb = 1 << L;
+  zhi = std::min(zhi, nb);
+  if (zhi <= zlo) return;
+  if (L == 4) nterms == 6 ? launch_lines_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
+                          : launch_lines_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
+  else if (L == 3) nterms == 6 ? launch_lines_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
+                               : launch_lines_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
+  else nterms == 6 ? launch_lines_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
+                   : launch_lines_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
 }
 
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st) {
+                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st, int n,
+                        int zlo, int zhi) {
   zpub = zpub ? zpub : 64;
-  if (L == 4) nterms == 6 ? launch_planes_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
-                          : launch_planes_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
-  else if (L == 3) nterms == 6 ? launch_planes_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
-                               : launch_planes_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
-  else nterms == 6 ? launch_planes_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st)
-                   : launch_planes_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
+  zhi = std::min(zhi, 1 << L);
+  if (L == 4) nterms == 6 ? launch_planes_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
+                          : launch_planes_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
+  else if (L == 3) nterms == 6 ? launch_planes_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
+                               : launch_planes_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
+  else nterms == 6 ? launch_planes_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
+                   : launch_planes_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
+}
+
+void launch_band_ylines(int L, int nterms, const double* tab, int NO, int R, const double* ws, double* ws2, double* Y,
+                        const double* src, int ldub, int zpub, int n, const double* corr, double scale,
+                        cudaStream_t st, int zlo, int zhi) {
+  zpub = zpub ? zpub : 64;
+  zhi = std::min(zhi, 1 << L);
+  if (zhi <= zlo) return;
+  if (L == 4) nterms == 6 ? launch_ylines_t<16, 6>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi)
+                          : launch_ylines_t<16, 4>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi);
+  else if (L == 3)
+    nterms == 6 ? launch_ylines_t<8, 6>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi)
+                : launch_ylines_t<8, 4>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi);
+  else nterms == 6 ? launch_ylines_t<4, 6>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi)
+                   : launch_ylines_t<4, 4>(tab, NO, R, ws, ws2, Y, src, ldub, zpub, n, corr, scale, st, zlo, zhi);
 }
 
 }  // namespace htlr

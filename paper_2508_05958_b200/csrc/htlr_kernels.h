@@ -220,13 +220,22 @@ cudaError_t sep_band_init();
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
                      double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
                      const int* lo, const int* hi);
-// register-line sweeps (htlr_band.cu): z sweep (ub -> term buffers) and the
-// fused y-x sweep of every z-point plane (term buffers -> Y), whole levels
+// register-line sweeps (htlr_band.cu): z sweep (source -> term buffers) and
+// the fused y-x sweep of every z-point plane (term buffers -> Y), for the
+// target z boxes [zlo, zhi) of the level (a z-slab shard; 0, 1 << L whole).
+// n > 0: the source (and the self-correction's u) is the F-order grid vector
+// u[N][R] of an n^3 grid instead of the level's boxes [box][R][ldub].
 bool band_lines_supported(int L);
 void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                       double* ws, cudaStream_t st);
+                       double* ws, cudaStream_t st, int n = 0, int zlo = 0, int zhi = 1 << 30);
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st);
+                        const double* ws, double* Y, const double* corr, double scale, cudaStream_t st, int n = 0,
+                        int zlo = 0, int zhi = 1 << 30);
+// the y-x sweep as two line kernels over all SMs (z-slab shards: a slab has
+// few planes): ws (z-swept terms) -> ws2 (y-swept, B-fragment order) -> Y
+void launch_band_ylines(int L, int nterms, const double* tab, int NO, int R, const double* ws, double* ws2, double* Y,
+                        const double* src, int ldub, int zpub, int n, const double* corr, double scale,
+                        cudaStream_t st, int zlo, int zhi);
 // pairs: int2 (source id, code), code = kind << 12 | ix << 8 | iy << 4 | iz
 // (per-axis offset + (NO - 1) / 2); table slot of (kind, i) = kind * NO + i
 void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* items, int nitems, const int2* pairs,
@@ -254,8 +263,10 @@ struct UpParams {
 bool upward8_supported(int d, int p, int sL);
 // u != null: the permute fused in (the box read from the F-order u[N][R] of
 // an n^3 grid and written to ub_out, then the upward from registers)
+// [zlo, zhi): leaf-box z range (a z-slab shard: the own boxes' contributions)
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
-                    cudaStream_t st, const double* u = nullptr, double* ub_out = nullptr, int n = 0);
+                    cudaStream_t st, const double* u = nullptr, double* ub_out = nullptr, int n = 0, int zlo = 0,
+                    int zhi = 1 << 30);
 constexpr int kMaxDown8 = 4;   // compressed levels the cooperative downward8 stages (config 4: 2)
 bool downward8_supported(int d, int p, int sL, const DownParams& dp);
 // [zlo, zhi): leaf-box z range written (the overlapped host-vector matvec

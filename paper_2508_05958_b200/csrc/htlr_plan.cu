@@ -108,6 +108,7 @@ struct Pass {
   int64_t sep_groups = 0;
   bool band = false;             // pass as banded line sweeps (sep_band_kernel)
   DevBuf band_ws;                // its term buffers [term][box][rhs][512]
+  DevBuf band_ws2;               // y-swept terms of the line-kernel y-x sweep (z-slab shards)
   double band_flops = 0;         // its algorithmic flop count per rhs (mode products it runs)
   int band_lo[3] = {0, 0, 0}, band_hi[3] = {0, 0, 0};   // own target boxes (a box region of the level)
 };
@@ -245,6 +246,12 @@ struct htlr_plan {
   // of leaf boxes [own_lo[L], own_hi[L]) and the upward data of its own
   // source clusters; every level's own range is a contiguous Morton range
   int shard_rank = 0, shard_world = 1;
+  // z-slab shards of a banded separable plan (htlr_set_zslab): the plan keeps
+  // the whole lists; the matvec covers the leaf boxes with z in [zs_lo, zs_hi)
+  // (upward contributions, banded passes over the z range of each level,
+  // downward, f rows), and the W_l are summed over the shards
+  bool zslab = false;
+  int zs_rank = 0, zs_world = 1, zs_lo = 0, zs_hi = 0;
   std::vector<int64_t> own_lo, own_hi;
   // caller-bound exchange buffers (ub, then W of each level pass), per R
   int ext_R = 0;
@@ -378,6 +385,17 @@ int choose_nt(const Pass& ps, int R) {
     return cap > 0 ? useful / cap : 1.0;
   };
   return eff(64) > eff(96) + 0.005 ? 64 : 96;
+}
+
+// y-x sweep of the banded passes as two line kernels (all SMs) instead of the
+// plane kernel (one SM per z-point plane): z-slab shards, whose slab has few
+// planes (HTLR_BAND_XY_LINES=1 forces it for measurements)
+static bool band_xy_lines(const htlr_plan* pl) {
+  static const int forced = [] {
+    const char* e = std::getenv("HTLR_BAND_XY_LINES");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return forced >= 0 ? forced == 1 : pl->zslab;
 }
 
 int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
@@ -837,6 +855,42 @@ int htlr_set_shard(htlr_plan* pl, int32_t rank, int32_t world) {
   return 0;
 }
 
+static void drop_graphs(htlr_plan* pl);
+
+int htlr_set_zslab(htlr_plan* pl, int32_t rank, int32_t world) {
+  if (!pl) return fail(-1, "null plan");
+  if (world < 1 || rank < 0 || rank >= world) return fail(-1, "invalid shard rank/world");
+  if (!pl->constructed) return fail(-1, "construct the plan before setting its z-slab");
+  if (pl->shard_world != 1) return fail(-1, "z-slab shards need an unsharded plan (no htlr_set_shard)");
+  if (!pl->sep || pl->d != 3 || !pl->passes[pl->leaf_pass].band)
+    return fail(-1, "z-slab shards need the banded separable formulation (3-D Gaussian, eta = 1, p = leaf side = 8)");
+  const int M = 1 << pl->L;
+  if (M % world || (M / world) % 2) return fail(-1, "z-slab shards: 2^L / world must be even");
+  drop_graphs(pl);
+  pl->zslab = world > 1;
+  pl->zs_rank = rank;
+  pl->zs_world = world;
+  pl->zs_lo = M / world * rank;
+  pl->zs_hi = M / world * (rank + 1);
+  // each banded pass covers the z range of its level that holds the own leaf
+  // boxes (coarse levels shared by several shards are computed by each)
+  for (auto& ps : pl->passes) {
+    if (!ps.band) continue;
+    const int s = pl->L - ps.level, nb = 1 << ps.level;
+    for (int a = 0; a < 3; ++a) ps.band_lo[a] = 0, ps.band_hi[a] = nb;
+    if (world > 1) {
+      ps.band_lo[2] = pl->zs_lo >> s;
+      ps.band_hi[2] = (pl->zs_hi + (1 << s) - 1) >> s;
+    }
+  }
+  return 0;
+}
+
+int htlr_exchange_kind(const htlr_plan* pl) {
+  if (!pl) return fail(-1, "null plan");
+  return pl->zslab ? 1 : 0;
+}
+
 int htlr_shard_info(const htlr_plan* pl, int64_t* own_leaf_lo, int64_t* own_leaf_hi, int64_t* own_pairs,
                     double* own_flops) {
   if (!pl) return fail(-1, "null plan");
@@ -873,7 +927,8 @@ static void exchange_sizes(const htlr_plan* pl, int R, std::vector<int64_t>& byt
     return;
   }
   const Pass& lp = pl->passes[pl->leaf_pass];
-  bytes.push_back(pl->levels[pl->L].nclusters * (int64_t)R * lp.K_pad * (int64_t)sizeof(double));
+  if (!pl->zslab)   // z-slab shards read u itself: only the W_l are exchanged (summed)
+    bytes.push_back(pl->levels[pl->L].nclusters * (int64_t)R * lp.K_pad * (int64_t)sizeof(double));
   for (const auto& ps : pl->passes) {
     if (ps.to_y) continue;
     bytes.push_back(pl->levels[ps.level].nclusters * (int64_t)R * ps.K_pad * (int64_t)sizeof(double));
@@ -1919,6 +1974,8 @@ static int ensure_workspace(htlr_plan* pl, int R) {
   for (auto& ps : pl->passes) {
     if (!pl->sep || !ps.band) continue;
     if (ps.band_ws.alloc((size_t)htlr::sep_band_workspace(ps.level, R) * sizeof(double))) return 1;
+    if (band_xy_lines(pl) && ps.band_ws2.alloc((size_t)htlr::sep_band_workspace(ps.level, R) * sizeof(double)))
+      return 1;
     CUDA_TRY(htlr::sep_band_init());   // kernel attributes, outside any graph capture
   }
   for (auto& ps : pl->passes) {
@@ -2021,7 +2078,7 @@ int mv_prepare(htlr_plan* pl, int64_t nrhs, void* stream, MvCtx& cx) {
   }
   const bool ext = pl->ext_R == cx.R && !pl->ext_ptrs.empty();
   size_t xi = 0;
-  cx.ub = ext ? pl->ext_ptrs[xi++] : pl->ub.d();
+  cx.ub = (ext && !pl->zslab) ? pl->ext_ptrs[xi++] : pl->ub.d();
   cx.Wl.assign(pl->levels.size(), nullptr);
   if (pl->mapped) {
     for (size_t l = 0; l < pl->levels.size(); ++l)
@@ -2295,7 +2352,8 @@ int mv_local(MvCtx& cx, const double* u) {
       // level) 3 mode products of 8^4 MAC; bytes u read + ub written
       const double flops = 2.0 * 3.0 * 4096.0 * (double)nb * R * up.nlev;
       if (cx.prof_begin(1, pl->L - 1, flops, 2.0 * R8 * (double)pl->N)) return 1;
-      htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n);
+      htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n,
+                           pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
       if (cx.prof_end()) return 1;
       cx.launches += 1;
       return 0;
@@ -2332,6 +2390,40 @@ int mv_local(MvCtx& cx, const double* u) {
     if (cx.prof_end()) return 1;
   }
   return 0;
+}
+
+// One sweep of a banded pass (0: z sweep, 1: the fused y-x sweep; 2: the
+// legacy separate x sweep, a no-op for the line/plane kernels).  Regions that
+// are whole in x and y (unsharded, or a z-slab shard) run the register-line
+// kernels (htlr_band.cu) over the region's z boxes; the leaf pass reads the
+// F-order u itself (no permuted copy).  Octant regions of Morton-sharded
+// plans keep the staged sweeps of htlr_sep.cu.
+static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
+                              cudaStream_t st, const double* u) {
+  const int nb = 1 << ps.level;
+  const bool xy_full = ps.band_lo[0] == 0 && ps.band_lo[1] == 0 && ps.band_hi[0] == nb && ps.band_hi[1] == nb;
+  const double* corr = ps.to_y ? pl->sep_corr.d() : nullptr;
+  const int nterms = ps.to_y ? 6 : 4;
+  if (xy_full && htlr::band_lines_supported(ps.level)) {
+    // sharded plans: u itself (every rank holds it; the permuted copy covers
+    // the own boxes only); unsharded: the permuted boxes upward8 wrote (the
+    // pitched box rows load with fewer address instructions: 108 vs 115 us)
+    const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab);
+    const double* src = fo ? u : B;
+    const int n = fo ? pl->n : 0;
+    if (sweep == 0)
+      htlr::launch_band_lines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
+                              ps.band_ws.d(), st, n, ps.band_lo[2], ps.band_hi[2]);
+    else if (sweep == 1 && band_xy_lines(pl))
+      htlr::launch_band_ylines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, ps.band_ws.d(), ps.band_ws2.d(), C, src,
+                               ps.K_pad, ps.zpitch, n, corr, pl->kp.scale, st, ps.band_lo[2], ps.band_hi[2]);
+    else if (sweep == 1)
+      htlr::launch_band_planes(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
+                               ps.band_ws.d(), C, corr, pl->kp.scale, st, n, ps.band_lo[2], ps.band_hi[2]);
+    return;
+  }
+  htlr::launch_sep_band(sweep, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C, corr,
+                        pl->kp.scale, nterms, st, ps.band_lo, ps.band_hi);
 }
 
 int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
@@ -2383,8 +2475,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     }();
     const Pass& lq = pl->passes[pl->leaf_pass];
     if (late && pl->sep && lq.band) {
-      htlr::launch_sep_band(0, lq.sep_tab.d(), lq.sep_NO, lq.level, R, cx.ub, lq.K_pad, lq.zpitch, lq.band_ws.d(),
-                            pl->Y.d(), pl->sep_corr.d(), pl->kp.scale, 6, cx.st, lq.band_lo, lq.band_hi);
+      launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u);
       leaf_z_done = true;
     }
   }
@@ -2408,10 +2499,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
         const double nterm = ps.to_y ? 6.0 : 4.0;
         if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, ps.band_flops * R, nv * (1.0 + 2.0 * nterm + 2.0))) return 1;
-        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw)
-          htlr::launch_sep_band(sw, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C,
-                                ps.to_y ? pl->sep_corr.d() : nullptr, pl->kp.scale, ps.to_y ? 6 : 4, sst,
-                                ps.band_lo, ps.band_hi);
+        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) launch_band_sweep(pl, ps, sw, B, C, R, sst, u);
         if (cx.prof_end()) return 1;
         continue;
       }
@@ -2490,7 +2578,8 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
   if (lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && htlr::downward8_supported(d, p, pl->sL, dp))
     htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
-                           pl->L, R, dp, b0, nb, cx.st);
+                           pl->L, R, dp, b0, nb, cx.st, pl->zslab ? pl->zs_lo : 0,
+                           pl->zslab ? pl->zs_hi : 1 << 30);
   else
     htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
                           nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
@@ -2512,7 +2601,8 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
   MvCtx cx;
   if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
   if (!u || !f) return fail(-1, "null vector");
-  if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
+  if (pl->shard_world > 1 || (pl->zslab && pl->zs_world > 1))
+    return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
   if (pl->graphs) {
     // replay a captured graph of the whole launch sequence (one CPU call
     // instead of ~10 launches + memsets).  The graph reads/writes plan-owned
@@ -2717,7 +2807,8 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   MvCtx cx;
   if (int rc = mv_prepare(pl, nrhs, stream, cx)) return rc;
   if (!u || !f) return fail(-1, "null vector");
-  if (pl->shard_world > 1) return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
+  if (pl->shard_world > 1 || (pl->zslab && pl->zs_world > 1))
+    return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
   // HTLR_HOST_DEVICE_OK=1 (timing experiments): device vectors through the
   // same overlapped schedule
   static const bool dev_ok = std::getenv("HTLR_HOST_DEVICE_OK") != nullptr;

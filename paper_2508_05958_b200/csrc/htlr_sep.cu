@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
 // entry into W_l[ancestor] (zeroed by the permute launch).
 __global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L,
                                                           int R, UpParams up, int64_t nb, const double* __restrict__ u,
-                                                          double* __restrict__ ub_out, int n) {
+                                                          double* __restrict__ ub_out, int n, int zlo, int zhi) {
   // CTA = the 8 sibling leaf boxes of one parent cluster (Morton ids
   // 8 blockIdx.x + w) for rhs blockIdx.y.  The 16^3-point cube is read once
   // (rows of 16 contiguous points of the F-order u, or the boxes of ub) into
@@ -807,6 +807,7 @@ __global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restric
   if (bb >= nb) return;
   int c0[3];
   morton_decode(bb, 3, L, c0);   // even coordinates: the cube origin in boxes
+  if (c0[2] < zlo || c0[2] >= zhi) return;   // z-slab shards: the own leaf boxes only
   if (u) {
     // row (yy, zz) of the cube: 16 points along x (boxes x = 0, 1); 256
     // threads x 8 double2 each, every load in flight before the first store
@@ -923,7 +924,7 @@ bool upward8_supported(int d, int p, int sL) {
 }
 
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
-                    cudaStream_t st, const double* u, double* ub_out, int n) {
+                    cudaStream_t st, const double* u, double* ub_out, int n, int zlo, int zhi) {
   if (nb <= 0 || (up.nlev == 0 && !u)) return;
   // sibling groups of 8 boxes; the pitched box layout is what every caller
   // passes (zpub = kSepZPitch, ldub >= 8 zpub)
@@ -934,7 +935,7 @@ void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const Up
     attr = true;
   }
   upward8_kernel<<<dim3((unsigned)((nb + 7) / 8), R), 256, smem, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb, u,
-                                                                       ub_out, n);
+                                                                       ub_out, n, zlo, zhi);
 }
 
 void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
@@ -1075,15 +1076,6 @@ void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, cons
     rg.lo[a] = lo ? lo[a] : 0;
     rg.hi[a] = hi ? hi[a] : nb;
     full = full && rg.lo[a] == 0 && rg.hi[a] == nb;
-  }
-  static const bool v1 = [] {
-    const char* e = std::getenv("HTLR_BAND_V1");
-    return e && e[0] == '1';
-  }();
-  if (full && !v1 && band_lines_supported(L)) {
-    if (sweep == 0) launch_band_lines(L, nterms, tables, NO, R, ub, ldub, zpub, ws, st);
-    else if (sweep == 1) launch_band_planes(L, nterms, tables, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st);
-    return;
   }
   if (sweep == 0) {
     launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);

@@ -99,29 +99,109 @@ def shard_ranges(M: int, rank: int, world: int):
     return M // world * rank, M // world * (rank + 1)
 
 
+def allreduce_sum(bufs, group=None) -> None:
+    """In-place sum of each buffer over all ranks (z-slab shards' W_l)."""
+    import torch.distributed as dist
+    for b in bufs:
+        if b.is_cuda and dist.get_backend(group) != "nccl":   # gloo harness runs
+            h = b.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            b.copy_(h)
+        else:
+            dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+
+
 class ShardedOperator:
-    """HTLR operator whose targets are split across `world` GPUs."""
+    """HTLR operator whose targets are split across `world` GPUs.
+
+    mode "subtree": Morton subtrees of every level (the general scheme, module
+    docstring).  mode "zslab" (banded separable plans, BASELINE config 4): the
+    leaf boxes with z in the rank's 1/world slab -- every rank holds the whole
+    u, the only exchange is a sum of the upward coefficients W_l (2.4 MB for
+    config 4), and every banded sweep, the upward and the downward pass run
+    over the own slab (htlr_set_zslab).  mode "auto" picks zslab when the plan
+    is banded."""
 
     def __init__(self, cfg: BuildConfig, grid: UniformGrid, rank: int, world: int,
-                 device: Optional[int] = None, group=None):
+                 device: Optional[int] = None, group=None, mode: str = "auto"):
         import torch
+        if mode not in ("auto", "subtree", "zslab"):
+            raise ValueError(f"unknown shard mode {mode!r}")
         self.grid, self.config = grid, cfg
         self.rank, self.world, self.group = rank, world, group
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
-        op = HTLRMatrix(grid, cfg, self.device)
         L = _lib.lib()
-        _lib.check(L.htlr_set_shard(op._plan, int(rank), int(world)))
-        _lib.check(L.htlr_build_lists(op._plan))
-        if cfg.coeff.constant_value is None:
-            a = np.ascontiguousarray(cfg.coeff(_all_points(grid)), dtype=np.float64)
-            _lib.check(L.htlr_set_coeff(op._plan, a.ctypes.data))
-        with torch.cuda.device(self.device):
-            _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        op = None
+        # the banded formulation: 3-D Gaussian on a uniform grid, p = leaf side = 8, strong eta = 1
+        maybe_banded = (isinstance(grid, UniformGrid) and grid.d == 3 and cfg.kernel.kind == "gaussian"
+                        and cfg.rank == 8 and cfg.leaf_side == 8 and cfg.rule.kind == "strong"
+                        and float(cfg.rule.eta) == 1.0)
+        if mode == "zslab" or (mode == "auto" and maybe_banded):
+            from .operators import construct
+            op = construct(cfg, grid, device=self.device)
+            if op.leaf_pass() == "banded":
+                _lib.check(L.htlr_set_zslab(op._plan, int(rank), int(world)))
+                self.mode = "zslab"
+            elif mode == "zslab":
+                raise ValueError("zslab shards need the banded separable formulation")
+            else:
+                op = None
+        if op is None:
+            op = HTLRMatrix(grid, cfg, self.device)
+            _lib.check(L.htlr_set_shard(op._plan, int(rank), int(world)))
+            _lib.check(L.htlr_build_lists(op._plan))
+            if cfg.coeff.constant_value is None:
+                a = np.ascontiguousarray(cfg.coeff(_all_points(grid)), dtype=np.float64)
+                _lib.check(L.htlr_set_coeff(op._plan, a.ctypes.data))
+            with torch.cuda.device(self.device):
+                _lib.check(L.htlr_construct(op._plan, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            self.mode = "subtree"
         self.local = op
         self._xbufs = {}
         self._rbufs = {}
+
+    graphs = True   # NCCL z-slab matvecs replay one CUDA graph (local, all-reduce, remote)
+
+    def _zslab_graph(self, ud, R: int):
+        """One CUDA graph per RHS count of [local phase, NCCL all-reduce of the
+        W_l, remote phase] over plan-owned staging vectors (the caller's u is
+        copied in, the result returned as a copy): one host call per matvec
+        instead of ~15 launches, so a small shard's device work is not starved
+        by the host."""
+        import torch
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        if R not in self._graphs:
+            u_st = torch.empty_like(ud)
+            f_st = torch.zeros_like(ud)
+            u_st.copy_(ud)
+            bufs = self.exchange_buffers(R)
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):   # warm-up outside the capture (lazy allocations)
+                self.local_phase(u_st, R)
+                if self.world > 1:
+                    allreduce_sum(bufs, self.group)
+                self.remote_phase(u_st, f_st, R)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.local_phase(u_st, R)
+                if self.world > 1:
+                    allreduce_sum(bufs, self.group)
+                self.remote_phase(u_st, f_st, R)
+            self._graphs[R] = (g, u_st, f_st)
+        g, u_st, f_st = self._graphs[R]
+        u_st.copy_(ud)
+        g.replay()
+        return f_st.clone()
+
+    @property
+    def exchange_sums(self) -> bool:
+        """True when the exchange buffers are summed (all-reduce), not gathered."""
+        return _lib.lib().htlr_exchange_kind(self.local._plan) == 1
 
     # exchange buffers are torch tensors so torch.distributed can move them
     def exchange_buffers(self, R: int):
@@ -242,6 +322,28 @@ class ShardedOperator:
         bufs = self.exchange_buffers(R)
         L = _lib.lib()
         import torch.distributed as dist
+        if self.mode == "zslab":
+            # own slab's upward contributions, summed over the ranks, then the
+            # banded passes and the downward pass of the own slab
+            nccl = self.world > 1 and dist.get_backend(self.group) == "nccl"
+            out = None
+            if exchange is None and self.graphs and (nccl or self.world == 1):
+                try:
+                    out = self._zslab_graph(ud, R)
+                except RuntimeError:   # a collective that cannot be captured: direct launches from now on
+                    self.graphs = False
+                    self._graphs = {}
+                    torch.cuda.synchronize(self.device)
+            if out is None:
+                self.local_phase(ud, R)
+                if exchange is not None:
+                    exchange(self, bufs)
+                elif self.world > 1:
+                    allreduce_sum(bufs, self.group)
+                self.remote_phase(ud, fd, R)
+                out = fd
+            out = out.reshape(-1) if vec else out
+            return out.cpu() if host else out
         overlap = exchange is None and self.world > 1 and not self.reduce_buffers(R)
         with torch.cuda.device(self.device):
             st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -15,13 +15,18 @@ from paper_2508_05958_b200.multi import ShardedOperator
 pytestmark = pytest.mark.gpu
 
 
-def emulate(cfg, grid, U, world):
-    ops = [ShardedOperator(cfg, grid, r, world, device=0) for r in range(world)]
+def emulate(cfg, grid, U, world, mode="subtree"):
+    ops = [ShardedOperator(cfg, grid, r, world, device=0, mode=mode) for r in range(world)]
     ud = torch.from_numpy(np.ascontiguousarray(U)).cuda()
     ud2 = ud.reshape(grid.num_points, -1)
     R = ud2.shape[1]
     bufs = [op.local_phase(ud2, R) for op in ops]
     for i in range(len(bufs[0])):
+        if ops[0].exchange_sums:   # z-slab shards: the NCCL all-reduce (sum)
+            tot = sum(b[i] for b in bufs)
+            for r in range(world):
+                bufs[r][i].copy_(tot)
+            continue
         n = bufs[0][i].numel()
         c = n // world
         for r in range(world):
@@ -44,7 +49,7 @@ def emulate_split(cfg, grid, U, world):
     with every non-own chunk of the exchange buffers poisoned with NaN (so it
     provably reads own sources only), then the chunks are exchanged and
     remote_finish completes the matvec."""
-    ops = [ShardedOperator(cfg, grid, r, world, device=0) for r in range(world)]
+    ops = [ShardedOperator(cfg, grid, r, world, device=0, mode="subtree") for r in range(world)]
     ud = torch.from_numpy(np.ascontiguousarray(U)).cuda()
     ud2 = ud.reshape(grid.num_points, -1)
     R = ud2.shape[1]
@@ -103,6 +108,40 @@ def test_sharded_equals_single(name, world):
     assert leaves[0][0] == 0 and all(a[1] == b[0] for a, b in zip(leaves, leaves[1:]))
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_zslab_shards_equal_single(world):
+    """z-slab shards of the banded config-4 plan (htlr_set_zslab): each shard
+    sums its slab's upward contributions into W_l, the W_l are summed over
+    the shards (NCCL all-reduce, replayed here), then each shard runs the
+    banded passes, the downward pass and writes the f rows of its z slab
+    (a contiguous block of the F-order f) -- together the single-GPU matvec."""
+    w = WORKLOADS["cfg4"]
+    cfg, grid = w.build_config(), w.grid
+    U = w.input()
+    single = H.construct(cfg, grid)
+    ref = H.matvec(single, U)
+    ops = [ShardedOperator(cfg, grid, r, world, device=0, mode="zslab") for r in range(world)]
+    assert all(op.mode == "zslab" and op.exchange_sums for op in ops)
+    ud = torch.from_numpy(np.ascontiguousarray(U)).cuda().reshape(-1, 1)
+    bufs = [op.local_phase(ud, 1) for op in ops]
+    for i in range(len(bufs[0])):
+        tot = sum(b[i] for b in bufs)
+        for b in bufs:
+            b[i].copy_(tot)
+    n = grid.n
+    rows = n * n * n // world
+    total = torch.zeros_like(ud)
+    for r, op in enumerate(ops):
+        fd = torch.zeros_like(ud)
+        op.remote_phase(ud, fd, 1)
+        f = fd.reshape(-1)
+        # only the own z slab is written
+        assert float(f[:r * rows].abs().sum()) == 0.0 and float(f[(r + 1) * rows:].abs().sum()) == 0.0
+        total += fd
+    err = np.linalg.norm(total.cpu().numpy().ravel() - ref) / np.linalg.norm(ref)
+    assert err <= 1e-13, err
+
+
 def test_sharded_2d_weak_rejects_uneven_levels():
     grid = H.UniformGrid(2, 32)
     cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.weak(),
@@ -118,7 +157,7 @@ def test_profiling_on_direct_launches():
     way."""
     w = WORKLOADS["cfg2"]
     cfg, grid = w.build_config(), w.grid
-    op = ShardedOperator(cfg, grid, 0, 2, device=0)
+    op = ShardedOperator(cfg, grid, 0, 2, device=0, mode="subtree")
     ud = torch.from_numpy(np.ascontiguousarray(w.input())).cuda().reshape(grid.num_points, 1)
     op.local.profile(True)
     op.local_phase(ud, 1)
@@ -132,3 +171,20 @@ def test_profiling_on_direct_launches():
     single.profile(True)
     H.matvec(single, w.input())
     assert single.profile_read()
+
+
+def test_zslab_graph_replay():
+    """The NCCL z-slab path replays one CUDA graph per RHS count of [local
+    phase, all-reduce, remote phase]; at world 1 (no collective: this run has
+    one GPU) the captured phases equal the plain matvec on capture and on
+    replay, and a new input reaches the graph through its staging copy."""
+    w = WORKLOADS["cfg4"]
+    cfg, grid = w.build_config(), w.grid
+    single = H.construct(cfg, grid)
+    op = ShardedOperator(cfg, grid, 0, 1, device=0, mode="zslab")
+    for seed in (0, 0, 1):
+        u = np.random.default_rng(seed).uniform(-1, 1, grid.num_points)
+        ref = H.matvec(single, u)
+        got = op.matvec(torch.from_numpy(u).cuda()).cpu().numpy()
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    assert op.graphs and 1 in op._graphs
