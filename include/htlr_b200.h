@@ -270,6 +270,23 @@ int htlr_lagrange_matrix(const double* pts_host, int64_t npts, const double* nod
                          double* out_host);
 int htlr_kernel_pairs(int32_t kernel, double sigma, double scale, int32_t d, const double* x_host, int64_t m1,
                       const double* y_host, int64_t m2, double* out_host);
+/* kernels.py:137-149 pairwise_masked_diagonal for one point set (row i and
+ * column i the same point): every coincident pair is kept off the singular
+ * evaluator and entry (i, i) is replaced by diag[i]. */
+int htlr_kernel_pairs_masked(int32_t kernel, double sigma, double scale, int32_t d, const double* x_host, int64_t m,
+                             const double* diag_host, double* out_host);
+/* Per-block tensor building blocks of htlr.tensor / htlr.blocks, computed on
+ * the current device; host arrays, row-major:
+ *   mode_product: out[a][r][b] = sum_k m[r][k] t[a][k][b]  (tensor.py:35-52 with
+ *                 the contracted mode's leading / trailing extents a, b);
+ *   gemm:         c = a (m x k) . b (k x n)               (contract, tensor.py:55-86);
+ *   kron:         numpy.kron(a, b)                       (blocks.py:166-187);
+ *   qr:           thin Householder QR, rows >= cols, LAPACK dgeqr2 / dorg2r
+ *                 sign conventions (tensor.py:107-115). */
+int htlr_mode_product(const double* t, int64_t a, int64_t k, int64_t b, const double* m, int64_t rows, double* out);
+int htlr_gemm(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c);
+int htlr_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc, double* out);
+int htlr_qr(const double* a, int64_t rows, int64_t cols, double* q, double* r);
 
 /* Per-launch profiling of htlr_matvec: when enabled, every kernel launch of
  * a matvec is bracketed by CUDA events on the launching stream.

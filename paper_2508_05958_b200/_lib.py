@@ -61,6 +61,11 @@ SYMBOLS = [
     ("htlr_set_lowrank", ctypes.c_int, [_P, _I32]),
     ("htlr_set_shard", ctypes.c_int, [_P, _I32, _I32]),
     ("htlr_set_zslab", ctypes.c_int, [_P, _I32, _I32]),
+    ("htlr_kernel_pairs_masked", ctypes.c_int, [_I32, ctypes.c_double, ctypes.c_double, _I32, _P, _I64, _P, _P]),
+    ("htlr_mode_product", ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P]),
+    ("htlr_gemm", ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P]),
+    ("htlr_kron", ctypes.c_int, [_P, _I64, _I64, _P, _I64, _I64, _P]),
+    ("htlr_qr", ctypes.c_int, [_P, _I64, _I64, _P, _P]),
     ("htlr_exchange_kind", ctypes.c_int, [_P]),
     ("htlr_shard_info", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                        ctypes.POINTER(_D)]),

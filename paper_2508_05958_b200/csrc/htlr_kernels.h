@@ -226,6 +226,13 @@ void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, cons
 // n > 0: the source (and the self-correction's u) is the F-order grid vector
 // u[N][R] of an n^3 grid instead of the level's boxes [box][R][ldub].
 bool band_lines_supported(int L);
+// per-block drop-in API (htlr_tensor.cu): host arrays, row-major
+cudaError_t tensor_mode_product(const double* t, int64_t A, int64_t K, int64_t B, const double* m, int64_t M,
+                                double* out);
+cudaError_t tensor_gemm(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c);
+cudaError_t tensor_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc,
+                        double* out);
+cudaError_t tensor_qr(const double* a, int64_t rows, int64_t cols, double* q, double* r);
 void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
                        double* ws, cudaStream_t st, int n = 0, int zlo = 0, int zhi = 1 << 30);
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,

@@ -3138,6 +3138,56 @@ int htlr_kernel_pairs(int32_t kernel, double sigma, double scale, int32_t d, con
   return 0;
 }
 
+int htlr_kernel_pairs_masked(int32_t kernel, double sigma, double scale, int32_t d, const double* x_host, int64_t m,
+                             const double* diag_host, double* out_host) {
+  if (!out_host || !diag_host || (!x_host && m)) return fail(-1, "null argument");
+  if (d < 1 || d > 3) return fail(-1, "dimension must be 1..3 for device kernel pairs");
+  if (kernel < 0 || kernel > 2) return fail(-1, "unknown kernel kind");
+  htlr::KernelParams kp;
+  kp.kind = kernel;
+  kp.denom = (2.0 * sigma) * sigma;
+  kp.scale = scale;
+  DevBuf dx, o, flag;
+  if (upload(dx, x_host, m * d * sizeof(double)) || o.alloc(std::max<int64_t>(1, m * m) * sizeof(double)) ||
+      flag.alloc(sizeof(int)))
+    return 1;
+  CUDA_TRY(cudaMemset(flag.ptr, 0, sizeof(int)));
+  // coincident pairs (the diagonal, and any repeated point) are flagged and
+  // zeroed by the pair kernel instead of evaluating the singular kernel there
+  htlr::launch_pairs(kp, d, dx.d(), m, dx.d(), m, o.d(), (int*)flag.ptr, 0);
+  CUDA_TRY(cudaMemcpy(out_host, o.ptr, m * m * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < m; ++i) out_host[i * m + i] = diag_host[i];
+  return 0;
+}
+
+static int tensor_rc(cudaError_t e) {
+  return e == cudaSuccess ? 0 : fail(1, std::string("tensor op: ") + cudaGetErrorString(e));
+}
+
+int htlr_mode_product(const double* t, int64_t a, int64_t k, int64_t b, const double* m, int64_t rows, double* out) {
+  if ((!t && a * k * b) || (!m && rows * k) || (!out && a * rows * b)) return fail(-1, "null argument");
+  if (a < 0 || k < 0 || b < 0 || rows < 0) return fail(-1, "negative extent");
+  return tensor_rc(htlr::tensor_mode_product(t, a, k, b, m, rows, out));
+}
+
+int htlr_gemm(const double* a, const double* b, int64_t m, int64_t k, int64_t n, double* c) {
+  if ((!a && m * k) || (!b && k * n) || (!c && m * n)) return fail(-1, "null argument");
+  if (m < 0 || k < 0 || n < 0) return fail(-1, "negative extent");
+  return tensor_rc(htlr::tensor_gemm(a, b, m, k, n, c));
+}
+
+int htlr_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc, double* out) {
+  if ((!a && ar * ac) || (!b && br * bc) || (!out && ar * ac * br * bc)) return fail(-1, "null argument");
+  return tensor_rc(htlr::tensor_kron(a, ar, ac, b, br, bc, out));
+}
+
+int htlr_qr(const double* a, int64_t rows, int64_t cols, double* q, double* r) {
+  if (!a || !q || !r) return fail(-1, "null argument");
+  if (rows < cols) return fail(-1, "qr requires rows >= cols, got shape (" + std::to_string(rows) + ", " +
+                                       std::to_string(cols) + ")");
+  return tensor_rc(htlr::tensor_qr(a, rows, cols, q, r));
+}
+
 int64_t htlr_last_launch_count(const htlr_plan* pl) { return pl ? pl->last_launches : -1; }
 
 int htlr_diag_value(htlr_plan* pl, double* out) {

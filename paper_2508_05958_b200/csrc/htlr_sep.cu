@@ -834,10 +834,17 @@ __global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restric
       d[1] = v[it].y;
     }
     __syncthreads();
-    // the permute: every box to ub, pitched as staged
-    double* o = ub_out + ((bb + w) * R + r) * (int64_t)ldub;
-    for (int e = lane; e < BP / 2; e += 32)
-      reinterpret_cast<double2*>(o)[e] = reinterpret_cast<const double2*>(box + w * BP)[e];
+    // the permute: every box to ub, pitched as staged (every shared load
+    // issued before the stores)
+    double2* o = reinterpret_cast<double2*>(ub_out + ((bb + w) * R + r) * (int64_t)ldub);
+    const double2* sbox = reinterpret_cast<const double2*>(box + w * BP);
+    double2 c[(BP / 2 + 31) / 32];
+#pragma unroll
+    for (int k = 0; k < (BP / 2 + 31) / 32; ++k)
+      if (lane + 32 * k < BP / 2) c[k] = sbox[lane + 32 * k];
+#pragma unroll
+    for (int k = 0; k < (BP / 2 + 31) / 32; ++k)
+      if (lane + 32 * k < BP / 2) o[lane + 32 * k] = c[k];
   } else {
     const double* sbx = ub + ((bb + w) * R + r) * (int64_t)ldub;
     for (int e = lane; e < BP / 2; e += 32)
