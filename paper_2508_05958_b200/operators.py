@@ -396,3 +396,8 @@ def operation_counts(op: HTLRMatrix) -> dict:
     """operators.py:200-209."""
     _, _, nl, na, nn = op._info()
     return {"dense_leaves": nn, "compressed_leaves": na, "total_leaves": nl}
+
+
+# the reference defines the row-sampling error estimate in operators.py
+# (operators.py:212-260); here it lives in rows.py (device exact rows)
+from .rows import DegenerateErrorEstimate, estimate_rel_error_random, exact_row_evaluator  # noqa: E402,F401
