@@ -227,12 +227,7 @@ size_t upward_split_smem_words(int side, int p, int nslab) {
 }
 
 int upward_nslab(int d, int side, int64_t nc, int R) {
-  static int off = -1;
-  if (off < 0) {
-    const char* e = std::getenv("HTLR_UPWARD_SPLIT");
-    off = (e && e[0] == '0') ? 1 : 0;
-  }
-  if (off || d != 3) return 1;
+  if (d != 3) return 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -590,14 +585,7 @@ int gemm_mt_for(int P_out) {
   if (gemm_use_persistent() && thin_m8_supported(m8) && P_out != 64) return -8 * m8;
   return P_out <= 64 ? 64 : 128;
 }
-int gemm_wide_wn() {
-  static int wn = -1;
-  if (wn < 0) {
-    const char* e = std::getenv("HTLR_GEMM_WN");
-    wn = (e && e[0] == '2') ? 2 : 3;   // 12 consumer warps: measured +1.3% over 8 (cfg4 leaf pass)
-  }
-  return wn;
-}
+int gemm_wide_wn() { return 3; }   // 12 consumer warps: measured +1.3% over 8 (cfg4 leaf pass)
 int gemm_nt(int MT) { return (MT == 128 && gemm_use_persistent()) ? 32 * gemm_wide_wn() : 64; }
 
 template <int WM, int WN, int STAGES>

@@ -546,26 +546,14 @@ static void launch_thin_t(const double* A, int64_t mat_stride, const double* B, 
 
 int gemm_stage_chunks(int MT, int K_pad) {
   if (MT < 0 || MT == 64 || !gemm_use_persistent()) return 1;
-  static int kcs = -1;
-  if (kcs < 0) {
-    const char* e = std::getenv("HTLR_GEMM_KCS");
-    kcs = (e && std::strcmp(e, "32") == 0) ? 32 : 64;
-  }
-  return (gemm_wide_wn() == 2 && kcs == 64 && K_pad % 64 == 0) ? 2 : 1;
+  return (gemm_wide_wn() == 2 && K_pad % 64 == 0) ? 2 : 1;
 }
 
 int thin_m8_supported(int m8) { return m8 == 5 || m8 == 8 || m8 == 16 || m8 == 27; }
 
 // 64-column thin items: 4 column warps x 2 n8 tiles (each A fragment feeds
-// two DMMAs; measured cfg 3 coupling pass -2%) or 8 x 1 (HTLR_THIN_TN=1)
-static int thin_tn() {
-  static int tn = -1;
-  if (tn < 0) {
-    const char* e = std::getenv("HTLR_THIN_TN");
-    tn = (e && e[0] == '1') ? 1 : 2;
-  }
-  return tn;
-}
+// two DMMAs; measured cfg 3 coupling pass -2% against 8 x 1)
+static int thin_tn() { return 2; }
 
 template <int M8, int STAGES>
 static void launch_thin_cw(int NT, const double* A, int64_t mat_stride, const double* B, double* C,
@@ -597,14 +585,7 @@ void launch_gemm_thin(int M_pad, int NT, const double* A, int64_t mat_stride, co
   }
 }
 
-bool gemm_use_persistent() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = std::getenv("HTLR_GEMM");
-    mode = (e && std::strcmp(e, "legacy") == 0) ? 0 : 1;
-  }
-  return mode == 1;
-}
+bool gemm_use_persistent() { return true; }
 
 template <int WM, int WN, int STAGES, int KCS, int MI = 2, int CPS = 1, bool GEN = false>
 static void launch_persistent_t(const double* A, int64_t mat_stride, const double* B, double* C,
@@ -636,30 +617,16 @@ void launch_gemm_persistent(int MT, int NT, const double* A, int64_t mat_stride,
   }
   if (MT == 128 && NT == 32) {   // narrow items: 8 warps x (16 rows x 32 columns)
     // two CTAs per SM, two stages each (measured: cfg 2 leaf pass -7%
-    // against one CTA with four stages; HTLR_NARROW_CPS=1 for the latter)
-    static int v = -1;
-    if (v < 0) {
-      const char* e = std::getenv("HTLR_NARROW_CPS");
-      v = e ? std::atoi(e) : 2;
-    }
-    if (v == 2)
-      launch_persistent_t<8, 1, 2, 32, 1, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc,
-                                             RT, st);
-    else
-      launch_persistent_t<8, 1, 4, 32, 1>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
-                                          st);
+    // against one CTA with four stages)
+    launch_persistent_t<8, 1, 2, 32, 1, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,
+                                           st);
     return;
-  }
-  static int kcs = -1;
-  if (kcs < 0) {
-    const char* e = std::getenv("HTLR_GEMM_KCS");
-    kcs = (e && std::strcmp(e, "32") == 0) ? 32 : 64;
   }
   if (MT == 64)
     launch_persistent_t<2, 2, 6, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
   else if (NT == 96)
     launch_persistent_t<4, 3, 3, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
-  else if (kcs == 64 && K_pad % 64 == 0)
+  else if (K_pad % 64 == 0)
     launch_persistent_t<4, 2, 2, 64>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
   else
     launch_persistent_t<4, 2, 4, 32>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT,

@@ -351,27 +351,18 @@ int validate(const htlr_desc& ds, std::string& err) {
 // whose matrices have few (pair, rhs) columns each (the near-field of small
 // grids, the coarse far-field levels) would leave two of its three column
 // warp groups idle, so it gets the narrow 32-column variant instead, whose
-// eight warps all work on the one 32-column slab.  HTLR_GEMM_NARROW=0/1
-// forces the choice for A/B runs.
+// eight warps all work on the one 32-column slab.
 int choose_nt(const Pass& ps, int R) {
   const int NT = htlr::gemm_nt(ps.MT);
-  static int force = -2;
-  if (force == -2) {
-    const char* e = std::getenv("HTLR_GEMM_NARROW");
-    force = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : -1;
-  }
   const double cols = (double)ps.npairs / std::max(1, ps.nmats) * std::min(R, NT);
   if (ps.MT < 0 && htlr::gemm_use_persistent()) {
     // thin passes: 8 or 16 columns per item when the matrices have few
     // pairs each (all 8 warps then split the rows of one or two n8 tiles)
-    if (force == 0) return NT;
-    if (force == 1 || cols <= 8.0) return 8;
+    if (cols <= 8.0) return 8;
     return cols <= 16.0 ? 16 : NT;
   }
   if (ps.MT != 128 || !htlr::gemm_use_persistent()) return NT;
-  if (force >= 0) return force ? 32 : NT;
   if (cols < 48.0) return 32;
-  if (std::getenv("HTLR_GEMM_WN")) return NT;   // forced 64 / 96
   // 64 or 96 columns per item: whichever wastes fewer column slots on the
   // pass's per-matrix pair counts (ties go to the 12-warp 96-column CTA)
   auto eff = [&](int nt) {
@@ -389,14 +380,8 @@ int choose_nt(const Pass& ps, int R) {
 
 // y-x sweep of the banded passes as two line kernels (all SMs) instead of the
 // plane kernel (one SM per z-point plane): z-slab shards, whose slab has few
-// planes (HTLR_BAND_XY_LINES=1 forces it for measurements)
-static bool band_xy_lines(const htlr_plan* pl) {
-  static const int forced = [] {
-    const char* e = std::getenv("HTLR_BAND_XY_LINES");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  return forced >= 0 ? forced == 1 : pl->zslab;
-}
+// planes (on one GPU the plane kernel is faster: 108 vs 136 us, config 4)
+static bool band_xy_lines(const htlr_plan* pl) { return pl->zslab; }
 
 int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
   const int NT = choose_nt(ps, R);
@@ -1097,15 +1082,9 @@ static int build_sym(const std::vector<int64_t>& ptr, const std::vector<int>& co
   return 0;
 }
 
-// HTLR_NEAR_GEN=0: stream the stored near blocks instead of generating them
-static bool near_gen_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("HTLR_NEAR_GEN");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
+// near-only leaf passes with Toeplitz near blocks generate their A fragments
+// from the 15^3 generators (config 2: 80 -> 73 us against streaming the blocks)
+static bool near_gen_enabled() { return true; }
 
 static bool regen_sym_enabled() {
   static int on = -1;
@@ -1276,21 +1255,6 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     std::vector<htlr::SepCol> all;
     for (int64_t P = 0; P < npar; ++P) emit(pcols[P], pself[P].data(), P, parts, all);
     std::stable_sort(parts.begin(), parts.end(), by_work);
-    if (std::getenv("HTLR_SEP_DUMP") && npar <= 2) {
-      for (const auto& pt : parts) {
-        std::fprintf(stderr, "[sep dump] level %d part tgt0 %d cols %d..%d corr %x\n", L, pt.b.tgt0, pt.b.col_begin,
-                     pt.b.col_begin + pt.b.col_count, pt.b.corr_mask);
-        for (int c = pt.b.col_begin; c < pt.b.col_begin + pt.b.col_count; ++c) {
-          std::fprintf(stderr, "   col %d n=%d:", c, all[c].n);
-          for (int k = 0; k < all[c].n; ++k) {
-            std::fprintf(stderr, " src %d [", all[c].src[k]);
-            for (int w = 0; w < 8; ++w) std::fprintf(stderr, "%x ", all[c].code[k][w]);
-            std::fprintf(stderr, "]");
-          }
-          std::fprintf(stderr, "\n");
-        }
-      }
-    }
     if (upload(all, parts, ps.sep_cols, ps.sep_blocks)) return 1;
     ps.sep_nblocks = ps.sep_own_nb = (int)parts.size();
   } else {
@@ -1335,15 +1299,13 @@ static int build_sep_blocks(htlr_plan* pl, Pass& ps, const std::vector<int64_t>&
     ps.sep_own_frac = (w0 + w1) > 0 ? w0 / (w0 + w1) : 1.0;
   }
   // z-slab groups of the leaf pass (unsharded plans): 4 slabs of an even
-  // number of leaf boxes (siblings share a slab), else 2 (HTLR_OVERLAP_SLABS
-  // overrides).  With 4, the first quarter of u goes in alone and the leaf work
+  // number of leaf boxes (siblings share a slab), else 2.  With 4, the first quarter of u goes in alone and the leaf work
   // over its sources (~1/4) covers the copy of the rest; the last quarter of f
   // is the only copy-out left exposed.
   ps.sep_slabs = 0;
   ps.sep_gcount.clear();
   const int mz = pl->levels[L].m;
   int S = (mz % 8 == 0) ? 4 : 2;
-  if (const char* e = std::getenv("HTLR_OVERLAP_SLABS")) S = std::max(2, std::atoi(e));
   if (mz % (2 * S) != 0) S = (mz % 4 == 0) ? 2 : 0;
   if (ps.to_y && pl->shard_world == 1 && S > 0) {
     const int zs = mz / S;   // leaf boxes per slab
@@ -2449,33 +2411,25 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   // The level passes (-> H_l) and the leaf pass (-> Y) are independent: the
   // level passes go to a side stream (a parallel branch of the graph), so
   // they fill the SMs the leaf pass leaves idle (its tail rounds).  Serial
-  // when profiling (per-launch events on one stream) or HTLR_CONCURRENT=0.
+  // when profiling (per-launch events on one stream).
   bool fork = false;
   if ((stages & 1) && !pl->profiling) {
-    static const bool concurrent = [] {
-      const char* e = std::getenv("HTLR_CONCURRENT");
-      return !(e && e[0] == '0');
-    }();
     int nlev = 0;
     for (const auto& ps : pl->passes) nlev += ps.to_y ? 0 : 1;
-    fork = nlev > 0 && concurrent;
+    fork = nlev > 0;
   }
   if (fork) {
     if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
     for (auto& ev : pl->side_ev)
       if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  // banded leaf pass (HTLR_BAND_LATE_FORK, default on): its z sweep first,
-  // then the fork, so the level passes fill the SMs the y-x sweep leaves idle
-  // (128 planes on 148 SMs) instead of delaying the z sweep
+  // banded leaf pass: its z sweep first, then the fork, so the level passes
+  // fill the SMs the y-x sweep leaves idle (128 planes on 148 SMs) instead of
+  // delaying the z sweep
   bool leaf_z_done = false;
   if (fork && !own_only && !rest_only) {
-    static const bool late = [] {
-      const char* e = std::getenv("HTLR_BAND_LATE_FORK");
-      return !(e && e[0] == '0');
-    }();
     const Pass& lq = pl->passes[pl->leaf_pass];
-    if (late && pl->sep && lq.band) {
+    if (pl->sep && lq.band) {
       launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u);
       leaf_z_done = true;
     }
@@ -2670,15 +2624,10 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
 // prologue, the level passes, the leaf pass for the targets before the last
 // slab and their downward pass; their f is copied out while the last slab's
 // targets run; the last slab of f goes last.  Captured once per (nrhs, host
-// pointers) into a two-stream graph.  HTLR_OVERLAP=0: plain H2D, device
-// matvec, D2H.
+// pointers) into a two-stream graph.
 // ---------------------------------------------------------------------------
 static bool overlap_ok(const htlr_plan* pl) {
-  static const bool off = [] {
-    const char* e = std::getenv("HTLR_OVERLAP");
-    return e && e[0] == '0';
-  }();
-  if (off || !pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
+  if (!pl->sep || pl->mapped || pl->shard_world != 1 || pl->d != 3 || !pl->graphs) return false;
 
   for (const auto& ps : pl->passes) {
     if (ps.sep_nblocks == 0) return false;
@@ -2810,10 +2759,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   if (!u || !f) return fail(-1, "null vector");
   if (pl->shard_world > 1 || (pl->zslab && pl->zs_world > 1))
     return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
-  // HTLR_HOST_DEVICE_OK=1 (timing experiments): device vectors through the
-  // same overlapped schedule
-  static const bool dev_ok = std::getenv("HTLR_HOST_DEVICE_OK") != nullptr;
-  if (!dev_ok && (!page_locked(u) || !page_locked(f)))
+  if (!page_locked(u) || !page_locked(f))
     return fail(-1, "host vectors must be page-locked (pinned or registered)");
   const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
   if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;

@@ -910,25 +910,13 @@ __global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restric
 }  // namespace
 
 bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
-  static int off = -1;
-  if (off < 0) {
-    const char* e = std::getenv("HTLR_DOWN8");
-    off = (e && e[0] == '0') ? 1 : 0;
-  }
-  if (off || d != 3 || p != kSepP || sL != kSepP || dp.nlev > kMaxDown8) return false;
+  if (d != 3 || p != kSepP || sL != kSepP || dp.nlev > kMaxDown8) return false;
   for (int i = 0; i < dp.nlev; ++i)
     if (dp.lev[i].K || dp.lev[i].qstride || dp.lev[i].P != kSepP * kSepP * kSepP) return false;
   return true;
 }
 
-bool upward8_supported(int d, int p, int sL) {
-  static int off = -1;
-  if (off < 0) {
-    const char* e = std::getenv("HTLR_UP8");
-    off = (e && e[0] == '0') ? 1 : 0;
-  }
-  return !off && d == 3 && p == kSepP && sL == kSepP;
-}
+bool upward8_supported(int d, int p, int sL) { return d == 3 && p == kSepP && sL == kSepP; }
 
 void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
                     cudaStream_t st, const double* u, double* ub_out, int n, int zlo, int zhi) {
@@ -960,15 +948,8 @@ void launch_downward8(const double* u, double* f, const double* Y, const double*
                                                                          nb, zlo, zhi);
 }
 
-// HTLR_SEP_GROUPS=1|2: consumer warp groups of the cooperative kernel
-int sep_block_groups() {
-  static int g = 0;
-  if (!g) {
-    const char* e = std::getenv("HTLR_SEP_GROUPS");
-    g = (e && e[0] == '1') ? 1 : 2;
-  }
-  return g;
-}
+// consumer warp groups of the cooperative kernel (two: alternate columns)
+int sep_block_groups() { return 2; }
 
 size_t sep_block_smem_bytes(int nslots) {
   const int NS = sep_ring_slots(sep_block_groups());
@@ -1062,15 +1043,6 @@ static void launch_band_xy_t(const double* tables, int NO, int L, int R, const d
       tables, NO, L, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, nterms, rg);
 }
 
-// HTLR_BAND_XY=0: separate y and x sweeps (sep_band_kernel modes 1, 2)
-static bool band_xy_fused() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("HTLR_BAND_XY");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, const double* ub, int ldub, int zpub,
                      double* ws, double* Y, const double* corr, double scale, int nterms, cudaStream_t st,
@@ -1078,31 +1050,22 @@ void launch_sep_band(int sweep, const double* tables, int NO, int L, int R, cons
   zpub = zpub ? zpub : 64;
   const int nb = 1 << L;
   BandRegion rg;
-  bool full = true;
   for (int a = 0; a < 3; ++a) {
     rg.lo[a] = lo ? lo[a] : 0;
     rg.hi[a] = hi ? hi[a] : nb;
-    full = full && rg.lo[a] == 0 && rg.hi[a] == nb;
   }
   if (sweep == 0) {
     launch_band_t<2, 0>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
-  } else if (band_xy_fused() || !full) {   // the separate sweeps handle whole levels only
-    if (sweep == 2) return;   // done by the fused launch of sweep 1
+  } else if (sweep == 1) {   // the fused y-x sweep (sweep 2 is a no-op)
     if (L == 4) launch_band_xy_t<16>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
     else if (L == 3) launch_band_xy_t<8>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
     else launch_band_xy_t<4>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
-  } else if (sweep == 1) {
-    launch_band_t<1, 1>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
-  } else {
-    launch_band_t<0, 2>(tables, NO, L, R, ub, ldub, zpub, ws, Y, corr, scale, nterms, st, rg);
   }
 }
 
 cudaError_t sep_band_init() {
   const int smem = 200 * 1024;   // an upper bound (<= 227 KB minus static): occupancy follows each launch
   cudaError_t e = cudaFuncSetAttribute(sep_band_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sep_band_xy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -137,7 +137,6 @@ _NB = {"HTLR_SEP_BAND": "0"}   # the cooperative / per-warp leaf passes instead 
                                  {**_NB, "HTLR_SEP_BLOCK": "0", "HTLR_SEP_CHUNK": "100000"},
                                  {**_NB, "HTLR_SEP_COLS": "1"}, {**_NB, "HTLR_SEP_COLS": "7"},
                                  {**_NB, "HTLR_SEP_COLS": "1000"},
-                                 {**_NB, "HTLR_SEP_GROUPS": "1"},
                                  {**_NB},
                                  {"HTLR_GRAPHS": "0"}])
 def test_separable_item_splits(tmp_path, env):
