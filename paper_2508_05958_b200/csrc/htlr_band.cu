@@ -142,7 +142,7 @@ __device__ __forceinline__ void stage_tables(double* __restrict__ dst, const dou
 
 // One term's band over a register line: acc[b] (+)= sum_o A(o) in[b + o].
 // SLOT 0: standard A fragments, 64: the mode-x (permuted k) ones.
-template <int NB, int T, int SLOT, bool SIGN, int B0 = 0, int B1 = NB>
+template <int NB, int T, int SLOT, bool SIGN, int B0 = 0, int B1 = NB, bool CHK = false>
 __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO, int lane, const double (&in)[NB][2],
                                           double (&acc)[NB][2], int tlo = 0, int thi = NB) {
   constexpr int kind = T >= 4 ? 1 : 0;
@@ -159,12 +159,12 @@ __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO
 #pragma unroll
     for (int b = B0; b < B1; ++b) {
       const int s = b + boff<T>(b & 1, i);
-      if (s >= 0 && s < NB && b >= tlo && b < thi) dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, in[s][0]);
+      if (s >= 0 && s < NB && (!CHK || (b >= tlo && b < thi))) dmma(acc[b][0], acc[b][1], (b & 1) ? a10 : a00, in[s][0]);
     }
 #pragma unroll
     for (int b = B0; b < B1; ++b) {
       const int s = b + boff<T>(b & 1, i);
-      if (s >= 0 && s < NB && b >= tlo && b < thi) dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, in[s][1]);
+      if (s >= 0 && s < NB && (!CHK || (b >= tlo && b < thi))) dmma(acc[b][0], acc[b][1], (b & 1) ? a11 : a01, in[s][1]);
     }
   }
 }
@@ -213,7 +213,7 @@ __device__ __forceinline__ void zero(double (&a)[NB][2]) {
 // latency 26 cycles: tools/dmma_latency.cu), and each unit's source boxes are
 // loaded while the previous unit computes (two register buffers).
 constexpr int kLineWarps = 12;
-template <int NB, int NT, bool R1, int HALF>
+template <int NB, int NT, bool R1, int HALF, bool FO = false, bool CHK = false>
 __device__ __forceinline__ void line_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
                                            const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
                                            int u0, int ustride, int nunits, int usel, int n, int zlo, int zhi) {
@@ -226,7 +226,7 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
   auto load = [&](int u, double(&in)[NB][2]) {
     const int line = line_of(u);
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
-    if (n) {
+    if (FO) {
       // straight from the F-order grid vector: box (bx, by, b), point
       // (x = g, y, z = q (+4)) at (8 bx + g) + n (8 by + y) + n^2 (8 b + q)
       const int64_t n2 = (int64_t)n * n;
@@ -255,11 +255,11 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
       constexpr int T = decltype(tc)::value;
       double acc[NB][2];
       zero(acc);
-      band_regs<NB, T, 0, false, HALF * H, HALF * H + H>(tab, NO, lane, in, acc, zlo, zhi);
+      band_regs<NB, T, 0, false, HALF * H, HALF * H + H, CHK>(tab, NO, lane, in, acc, zlo, zhi);
       double* o = ob + T * tstride;
 #pragma unroll
       for (int b = HALF * H; b < HALF * H + H; ++b)
-        if (b >= zlo && b < zhi)
+        if (!CHK || (b >= zlo && b < zhi))
           *reinterpret_cast<double2*>(o + spread3(b) * (int64_t)R * 512) = make_double2(acc[b][0], acc[b][1]);
     };
     // a runtime loop over the terms: the compiler cannot interleave (and keep
@@ -388,6 +388,26 @@ __device__ __forceinline__ void pair_units(const double* __restrict__ tab, int N
   }
 }
 
+// half-line units over the target z range [zlo, zhi), which covers whole
+// halves: both (the parity of the even-strided unit picks the half) or one
+template <int NB, int NT, bool R1, bool FO>
+__device__ __forceinline__ void dispatch_halves(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
+                                                const double* __restrict__ ub, double* __restrict__ ws,
+                                                int64_t tstride, int gw, int ustride, int nlines, int n, int zlo,
+                                                int zhi) {
+  const bool h0 = zlo < NB / 2, h1 = zhi > NB / 2;
+  if (h0 && h1) {
+    if (gw & 1)
+      line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+    else
+      line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+  } else if (h1) {
+    line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+  } else {
+    line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+  }
+}
+
 // src: the level's boxes [box][rhs][ldub] (z pitch zpub), or with n > 0 the
 // F-order grid vector u[N][R] of an n^3 grid (the leaf pass reads u itself:
 // no permuted copy).  Targets are written for z boxes [zlo, zhi) only (a
@@ -403,19 +423,13 @@ __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const dou
   const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
   const int ustride = gridDim.x * (blockDim.x >> 5);
   const int nlines = NB * NB * 8 * R;
-  const bool h0 = zlo < NB / 2, h1 = zhi > NB / 2;
   const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
   if (!halves) {   // a z-slab shard narrower than a half line: whole sibling pairs
     pair_units<NB, NT, R1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, n, zlo & ~1, (zhi + 1) & ~1);
-  } else if (h0 && h1) {   // both halves: the parity of the (even-strided) unit picks the half
-    if (gw & 1)
-      line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
-    else
-      line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
-  } else if (h1) {
-    line_units<NB, NT, R1, 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
-  } else {
-    line_units<NB, NT, R1, 0>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+  } else if (n) {   // straight from the F-order u (z-slab shards of the leaf pass)
+    dispatch_halves<NB, NT, R1, true>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
+  } else {           // the level's boxes (the permuted leaf boxes, or a coupling level's W)
+    dispatch_halves<NB, NT, R1, false>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
   }
 }
 
