@@ -412,25 +412,25 @@ __device__ __forceinline__ void dispatch_halves(const double* __restrict__ tab, 
 // F-order grid vector u[N][R] of an n^3 grid (the leaf pass reads u itself:
 // no permuted copy).  Targets are written for z boxes [zlo, zhi) only (a
 // z-slab shard); halves without an own box are skipped.
-template <int NB, int NT, bool R1>
+// KIND 0: the level's boxes, whole halves; 1: the F-order u, whole halves;
+// 2: sibling pairs of a narrow z slab.  Separate kernels keep the unsharded
+// kernel's code what it was (one kernel with all three bodies measured 33 ->
+// 37 us for config 4's z sweep).
+template <int NB, int NT, bool R1, int KIND>
 __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
                                                                       int R_, const double* __restrict__ ub, int ldub,
                                                                       int zpub, double* __restrict__ ws,
                                                                       int64_t tstride, int n, int zlo, int zhi) {
   const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
   __shared__ double tab[2 * 15 * kTabSlot];
-  stage_tables<64>(tab, tables, NO);   // line_units syncs after issuing its first loads
+  stage_tables<64>(tab, tables, NO);   // the units sync after issuing their first loads
   const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
   const int ustride = gridDim.x * (blockDim.x >> 5);
   const int nlines = NB * NB * 8 * R;
-  const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
-  if (!halves) {   // a z-slab shard narrower than a half line: whole sibling pairs
+  if (KIND == 2)
     pair_units<NB, NT, R1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, n, zlo & ~1, (zhi + 1) & ~1);
-  } else if (n) {   // straight from the F-order u (z-slab shards of the leaf pass)
-    dispatch_halves<NB, NT, R1, true>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
-  } else {           // the level's boxes (the permuted leaf boxes, or a coupling level's W)
-    dispatch_halves<NB, NT, R1, false>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
-  }
+  else
+    dispatch_halves<NB, NT, R1, KIND == 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
 }
 
 // y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
@@ -779,12 +779,19 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   // half-line units must be even: a warp keeps its half)
   const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
   const int warps = kLineWarps;
-  if (R == 1)
-    band_line_kernel<NB, NT, true><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n,
-                                                                           zlo, zhi);
-  else
-    band_line_kernel<NB, NT, false><<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n,
-                                                                            zlo, zhi);
+  const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
+  const int kind = !halves ? 2 : n ? 1 : 0;
+  auto go = [&](auto r1, auto kc) {
+    band_line_kernel<NB, NT, decltype(r1)::value, decltype(kc)::value>
+        <<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n, zlo, zhi);
+  };
+  using T1 = std::true_type;
+  using F1 = std::false_type;
+  using K0 = std::integral_constant<int, 0>;
+  using K1 = std::integral_constant<int, 1>;
+  using K2 = std::integral_constant<int, 2>;
+  if (R == 1) kind == 0 ? go(T1{}, K0{}) : kind == 1 ? go(T1{}, K1{}) : go(T1{}, K2{});
+  else kind == 0 ? go(F1{}, K0{}) : kind == 1 ? go(F1{}, K1{}) : go(F1{}, K2{});
 }
 
 template <int NB, int NT>
