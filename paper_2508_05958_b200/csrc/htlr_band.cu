@@ -769,7 +769,7 @@ void launch_ylines_t(const double* tab, int NO, int R, const double* ws, double*
 
 template <int NB, int NT>
 void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, double* ws,
-                    cudaStream_t st, int n, int zlo, int zhi) {
+                    cudaStream_t st, int n, int zlo, int zhi, int max_ctas) {
   const int64_t lines = (int64_t)NB * NB * 8 * R;
   const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
   int dev = 0, sms = 148;
@@ -777,6 +777,7 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one CTA of kLineWarps warps per SM (the stride over the 2 x lines
   // half-line units must be even: a warp keeps its half)
+  if (max_ctas > 0) sms = std::min(sms, max_ctas);
   const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
   const int warps = kLineWarps;
   const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
@@ -819,17 +820,17 @@ void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldu
 bool band_lines_supported(int L) { return L >= 2 && L <= 4; }
 
 void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                       double* ws, cudaStream_t st, int n, int zlo, int zhi) {
+                       double* ws, cudaStream_t st, int n, int zlo, int zhi, int max_ctas) {
   zpub = zpub ? zpub : 64;
   const int nb = 1 << L;
   zhi = std::min(zhi, nb);
   if (zhi <= zlo) return;
-  if (L == 4) nterms == 6 ? launch_lines_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
-                          : launch_lines_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
-  else if (L == 3) nterms == 6 ? launch_lines_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
-                               : launch_lines_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
-  else nterms == 6 ? launch_lines_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi)
-                   : launch_lines_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi);
+  if (L == 4) nterms == 6 ? launch_lines_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas)
+                          : launch_lines_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas);
+  else if (L == 3) nterms == 6 ? launch_lines_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas)
+                               : launch_lines_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas);
+  else nterms == 6 ? launch_lines_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas)
+                   : launch_lines_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, st, n, zlo, zhi, max_ctas);
 }
 
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,

@@ -233,8 +233,9 @@ cudaError_t tensor_gemm(const double* a, const double* b, int64_t m, int64_t k, 
 cudaError_t tensor_kron(const double* a, int64_t ar, int64_t ac, const double* b, int64_t br, int64_t bc,
                         double* out);
 cudaError_t tensor_qr(const double* a, int64_t rows, int64_t cols, double* q, double* r);
+// max_ctas > 0 caps the z sweep's persistent grid (SMs left to a concurrent stream)
 void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
-                       double* ws, cudaStream_t st, int n = 0, int zlo = 0, int zhi = 1 << 30);
+                       double* ws, cudaStream_t st, int n = 0, int zlo = 0, int zhi = 1 << 30, int max_ctas = 0);
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
                         const double* ws, double* Y, const double* corr, double scale, cudaStream_t st, int n = 0,
                         int zlo = 0, int zhi = 1 << 30);

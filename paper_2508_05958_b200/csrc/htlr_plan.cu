@@ -274,8 +274,10 @@ struct htlr_plan {
     std::vector<int32_t> kind, level;
     std::vector<double> flops, bytes;
     int64_t launches;
+    uint64_t stamp = 0;   // last use (graph_clock)
   };
   std::vector<GraphEntry> graph_cache;
+  uint64_t graph_clock = 0;
   // overlapped host-vector matvec (htlr_matvec_host): its graphs (keyed by the
   // host pointers), a copy stream and the fork / join events
   std::vector<GraphEntry> host_graphs;
@@ -1959,9 +1961,23 @@ static int ensure_workspace(htlr_plan* pl, int R) {
 // multi-GPU caller all-gathers the exchange buffers (contiguous Morton chunks).
 namespace {
 
+// Host-vector pipeline of a banded plan (htlr_matvec_host): u arrives and f
+// leaves in S z slabs of leaf boxes (contiguous in F-order) on a copy stream;
+// upward8 runs per slab as it lands, downward8 per slab before its copy out.
+struct HostPipe {
+  int S = 0;                   // slabs
+  int zu[5] = {}, zf[5] = {};  // slab bounds (leaf boxes along z) of u and of f
+  size_t zrow = 0;             // doubles per leaf-box row along z (points x rhs)
+  const double* uh = nullptr;  // caller's page-locked u / f
+  double* fh = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t* ev = nullptr;   // 2 S + 2: fork, S landed, S written, join
+};
+
 struct MvCtx {
   htlr_plan* pl;
   cudaStream_t st;
+  HostPipe* pipe = nullptr;
   bool zeroed = false;      // the permute launch zeroed the remote phase's accumulators
   int R, d, p, P;
   double* ub;
@@ -2317,6 +2333,16 @@ int mv_local(MvCtx& cx, const double* u) {
       // level) 3 mode products of 8^4 MAC; bytes u read + ub written
       const double flops = 2.0 * 3.0 * 4096.0 * (double)nb * R * up.nlev;
       if (cx.prof_begin(1, pl->L - 1, flops, 2.0 * R8 * (double)pl->N)) return 1;
+      if (HostPipe* hp = cx.pipe) {
+        // one launch per slab of u, each after its copy landed
+        for (int k = 0; k < hp->S; ++k) {
+          CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[1 + k], 0));
+          htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n, hp->zu[k],
+                               hp->zu[k + 1]);
+        }
+        cx.launches += hp->S;
+        return 0;
+      }
       htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n,
                            pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
       if (cx.prof_end()) return 1;
@@ -2324,6 +2350,7 @@ int mv_local(MvCtx& cx, const double* u) {
       return 0;
     }
   }
+  if (cx.pipe) return fail(2, "host pipeline: upward8 not applicable");
   // unprofiled unsharded matvec: permute + zeroing + every level's upward in
   // one launch (profiling keeps them apart so each phase is timed)
   if (cx.zeroed && !pl->profiling) {
@@ -2357,6 +2384,9 @@ int mv_local(MvCtx& cx, const double* u) {
   return 0;
 }
 
+// SMs the leaf z sweep leaves to the level passes running beside it
+static constexpr int kLevelSMs = 20;
+
 // One sweep of a banded pass (0: z sweep, 1: the fused y-x sweep; 2: the
 // legacy separate x sweep, a no-op for the line/plane kernels).  Regions that
 // are whole in x and y (unsharded, or a z-slab shard) run the register-line
@@ -2364,7 +2394,7 @@ int mv_local(MvCtx& cx, const double* u) {
 // F-order u itself (no permuted copy).  Octant regions of Morton-sharded
 // plans keep the staged sweeps of htlr_sep.cu.
 static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
-                              cudaStream_t st, const double* u) {
+                              cudaStream_t st, const double* u, int max_ctas = 0) {
   const int nb = 1 << ps.level;
   const bool xy_full = ps.band_lo[0] == 0 && ps.band_lo[1] == 0 && ps.band_hi[0] == nb && ps.band_hi[1] == nb;
   const double* corr = ps.to_y ? pl->sep_corr.d() : nullptr;
@@ -2378,7 +2408,7 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
     const int n = fo ? pl->n : 0;
     if (sweep == 0)
       htlr::launch_band_lines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
-                              ps.band_ws.d(), st, n, ps.band_lo[2], ps.band_hi[2]);
+                              ps.band_ws.d(), st, n, ps.band_lo[2], ps.band_hi[2], max_ctas);
     else if (sweep == 1 && band_xy_lines(pl))
       htlr::launch_band_ylines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, ps.band_ws.d(), ps.band_ws2.d(), C, src,
                                ps.K_pad, ps.zpitch, n, corr, pl->kp.scale, st, ps.band_lo[2], ps.band_hi[2]);
@@ -2425,20 +2455,22 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     for (auto& ev : pl->side_ev)
       if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  // banded leaf pass: its z sweep first, then the fork, so the level passes
-  // fill the SMs the y-x sweep leaves idle (128 planes on 148 SMs) instead of
-  // delaying the z sweep
+  // banded leaf pass: the fork first, then its z sweep on all but
+  // kLevelSMs SMs, which the level passes (side stream) run on meanwhile; they
+  // go on filling the SMs the y-x sweep leaves idle (128 planes on 148 SMs)
   bool leaf_z_done = false;
-  if (fork && !own_only && !rest_only) {
-    const Pass& lq = pl->passes[pl->leaf_pass];
-    if (pl->sep && lq.band) {
-      launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u);
-      leaf_z_done = true;
-    }
-  }
   if (fork) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
     CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
+  }
+  if (fork && !own_only && !rest_only) {
+    const Pass& lq = pl->passes[pl->leaf_pass];
+    if (pl->sep && lq.band) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
+      launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u, sms - kLevelSMs);
+      leaf_z_done = true;
+    }
   }
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
@@ -2533,7 +2565,25 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   const double frac = (double)nb / (double)nleaf;
   if (!(stages & 2)) return 0;
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
-  if (lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && htlr::downward8_supported(d, p, pl->sL, dp))
+  const bool down8 = lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && htlr::downward8_supported(d, p, pl->sL, dp);
+  if (HostPipe* hp = cx.pipe) {
+    if (!down8) return fail(2, "host pipeline: downward8 not applicable");
+    // one launch per slab of f, each copied out while the next is computed
+    for (int k = 0; k < hp->S; ++k) {
+      htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
+                             pl->L, R, dp, b0, nb, cx.st, hp->zf[k], hp->zf[k + 1]);
+      CUDA_TRY(cudaEventRecord(hp->ev[1 + hp->S + k], cx.st));
+      CUDA_TRY(cudaStreamWaitEvent(hp->cs, hp->ev[1 + hp->S + k], 0));
+      const size_t o = hp->zf[k] * hp->zrow, c = (hp->zf[k + 1] - hp->zf[k]) * hp->zrow;
+      CUDA_TRY(cudaMemcpyAsync(hp->fh + o, f + o, c * sizeof(double), cudaMemcpyDefault, hp->cs));
+    }
+    cx.launches += hp->S;
+    CUDA_TRY(cudaEventRecord(hp->ev[2 * hp->S + 1], hp->cs));
+    CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[2 * hp->S + 1], 0));
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  if (down8)
     htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
                            pl->L, R, dp, b0, nb, cx.st, pl->zslab ? pl->zs_lo : 0,
                            pl->zslab ? pl->zs_hi : 1 << 30);
@@ -2562,23 +2612,21 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     return fail(-1, "sharded plan: use htlr_matvec_local / exchange / htlr_matvec_remote");
   if (pl->graphs) {
     // replay a captured graph of the whole launch sequence (one CPU call
-    // instead of ~10 launches + memsets).  The graph reads/writes plan-owned
-    // staging vectors, so it does not depend on the caller's pointers: the
-    // caller's u / f are copied in and out around the replay (2 N R doubles
-    // each way, D2D).
-    const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
-    if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;
-    const double* us = pl->u_stage.d();
-    double* fs = pl->f_stage.d();
+    // instead of ~10 launches + memsets), keyed by the caller's u / f.  A
+    // miss captures the sequence again; up to kGraphsPerShape graphs of one
+    // shape are kept, beyond that the least recently used one has its
+    // parameters rewritten in place (cudaGraphExecUpdate: pointer changes
+    // only, no re-instantiation) -- callers that rotate many buffers pay one
+    // capture per call, never a D2D copy of u or f.
+    constexpr int kGraphsPerShape = 4;
     for (auto& g : pl->graph_cache) {
-      if (g.R == cx.R && g.u == us && g.f == fs && g.prof == pl->profiling) {
+      if (g.R == cx.R && g.u == u && g.f == f && g.prof == pl->profiling) {
+        g.stamp = ++pl->graph_clock;
         pl->prof_kind = g.kind;
         pl->prof_level = g.level;
         pl->prof_flops = g.flops;
         pl->prof_bytes = g.bytes;
-        if (u != us) CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         CUDA_TRY(cudaGraphLaunch(g.exec, cx.st));
-        if (f != fs) CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
         pl->last_launches = g.launches;
         return 0;
       }
@@ -2588,21 +2636,47 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     cc.st = pl->cap_stream;
     prof_reset(pl);
     CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
-    int rc = mv_local(cc, us);
-    if (!rc) rc = mv_remote(cc, us, fs);
+    int rc = mv_local(cc, u);
+    if (!rc) rc = mv_remote(cc, u, f);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
-    cudaGraphExec_t exec = nullptr;
-    if (!rc && ce == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
-      cudaGraphDestroy(graph);
-      if (pl->graph_cache.size() >= 8) drop_graphs(pl);
-      pl->graph_cache.push_back({cx.R, us, fs, pl->profiling, exec, pl->prof_kind, pl->prof_level, pl->prof_flops,
-                                 pl->prof_bytes, cc.launches});
-      if (u != us) CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDeviceToDevice, cx.st));
-      CUDA_TRY(cudaGraphLaunch(exec, cx.st));
-      if (f != fs) CUDA_TRY(cudaMemcpyAsync(f, fs, vbytes, cudaMemcpyDeviceToDevice, cx.st));
-      pl->last_launches = cc.launches;
-      return 0;
+    if (!rc && ce == cudaSuccess && graph) {
+      htlr_plan::GraphEntry* hit = nullptr;
+      int same = 0;
+      for (auto& g : pl->graph_cache) {
+        if (g.R != cx.R || g.prof != pl->profiling) continue;
+        ++same;
+        if (!hit || g.stamp < hit->stamp) hit = &g;
+      }
+      if (hit && same >= kGraphsPerShape) {
+        cudaGraphExecUpdateResultInfo info{};
+        if (cudaGraphExecUpdate(hit->exec, graph, &info) != cudaSuccess) {
+          cudaGetLastError();
+          hit = nullptr;
+        }
+      } else {
+        hit = nullptr;
+      }
+      cudaGraphExec_t exec = nullptr;
+      if (!hit && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        if (pl->graph_cache.size() >= 8) drop_graphs(pl);
+        pl->graph_cache.push_back({cx.R, u, f, pl->profiling, exec, {}, {}, {}, {}, 0});
+        hit = &pl->graph_cache.back();
+      }
+      if (hit) {
+        cudaGraphDestroy(graph);
+        hit->u = u;
+        hit->f = f;
+        hit->kind = pl->prof_kind;
+        hit->level = pl->prof_level;
+        hit->flops = pl->prof_flops;
+        hit->bytes = pl->prof_bytes;
+        hit->launches = cc.launches;
+        hit->stamp = ++pl->graph_clock;
+        CUDA_TRY(cudaGraphLaunch(hit->exec, cx.st));
+        pl->last_launches = cc.launches;
+        return 0;
+      }
     }
     // capture not possible here: fall back to direct launches from now on
     if (graph) cudaGraphDestroy(graph);
@@ -2744,6 +2818,49 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
   return 0;
 }
 
+// Slabs of the banded host pipeline (0: not applicable): a single-GPU banded
+// separable plan whose upward and downward passes are the per-box-octet
+// kernels, which take z ranges of leaf boxes (even bounds).  Four equal
+// slabs: a slab's upward8 / downward8 lasts about one CTA's latency (12-16
+// us) whatever its size (thinner end slabs measured no faster), the copy of
+// a slab ~80 us, so all but the last upward and the first downward hide.
+int band_pipe_slabs(const htlr_plan* pl, int* zu = nullptr, int* zf = nullptr) {
+  if (!pl->sep || pl->mapped || pl->shard_world != 1 || pl->zslab || pl->d != 3 || !pl->graphs) return 0;
+  if (!pl->passes[pl->leaf_pass].band || !htlr::upward8_supported(pl->d, pl->p, pl->sL)) return 0;
+  const int mz = pl->levels[pl->L].m;
+  for (int S : {4, 2}) {
+    if (mz % (2 * S)) continue;
+    for (int k = 0; zu && k <= S; ++k) zu[k] = zf[k] = k * (mz / S);
+    return S;
+  }
+  return 0;
+}
+
+int mv_band_host(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
+  htlr_plan* pl = cx.pl;
+  HostPipe hp;
+  hp.S = band_pipe_slabs(pl, hp.zu, hp.zf);
+  hp.zrow = (size_t)pl->sL * pl->n * pl->n * cx.R;
+  hp.uh = uh;
+  hp.fh = fh;
+  hp.cs = cs;
+  hp.ev = pl->ov_ev.data();
+  if (hp.S == 0 || pl->ov_ev.size() < (size_t)(2 * hp.S + 2)) return fail(2, "banded host pipeline: not prepared");
+  double* us = pl->u_stage.d();
+  CUDA_TRY(cudaEventRecord(hp.ev[0], cx.st));
+  CUDA_TRY(cudaStreamWaitEvent(cs, hp.ev[0], 0));
+  for (int k = 0; k < hp.S; ++k) {
+    const size_t o = hp.zu[k] * hp.zrow, c = (hp.zu[k + 1] - hp.zu[k]) * hp.zrow;
+    CUDA_TRY(cudaMemcpyAsync(us + o, uh + o, c * sizeof(double), cudaMemcpyDefault, cs));
+    CUDA_TRY(cudaEventRecord(hp.ev[1 + k], cs));
+  }
+  cx.pipe = &hp;
+  int rc = mv_local(cx, us);
+  if (!rc) rc = mv_remote(cx, us, pl->f_stage.d());
+  cx.pipe = nullptr;
+  return rc;
+}
+
 bool page_locked(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -2765,7 +2882,8 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
     return fail(-1, "host vectors must be page-locked (pinned or registered)");
   const size_t vbytes = (size_t)pl->N * cx.R * sizeof(double);
   if (pl->u_stage.alloc(vbytes) || pl->f_stage.alloc(vbytes)) return 1;
-  if (!overlap_ok(pl) || pl->profiling) {
+  const bool banded = band_pipe_slabs(pl) > 0;
+  if ((!banded && !overlap_ok(pl)) || pl->profiling) {
     CUDA_TRY(cudaMemcpyAsync(pl->u_stage.ptr, u, vbytes, cudaMemcpyDefault, cx.st));
     if (int rc = htlr_matvec(pl, pl->u_stage.d(), pl->f_stage.d(), nrhs, stream)) return rc;
     CUDA_TRY(cudaMemcpyAsync(f, pl->f_stage.ptr, vbytes, cudaMemcpyDefault, cx.st));
@@ -2786,7 +2904,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   }
   if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   if (!pl->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
-  while (pl->ov_ev.size() < 6) {
+  while (pl->ov_ev.size() < 10) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pl->ov_ev.push_back(e);
@@ -2795,7 +2913,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   cc.st = pl->cap_stream;
   cc.launches = 0;
   CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
-  int rc = mv_overlap(cc, u, f, pl->copy_stream);
+  int rc = banded ? mv_band_host(cc, u, f, pl->copy_stream) : mv_overlap(cc, u, f, pl->copy_stream);
   cudaGraph_t graph = nullptr;
   cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
   cudaGraphExec_t exec = nullptr;

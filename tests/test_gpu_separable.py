@@ -203,6 +203,42 @@ def test_host_vector_path_matches_device(n, a, R):
     assert got2.is_pinned() and rel(got2.numpy().reshape(-1, R), ref) <= 1e-14
 
 
+def test_host_vector_path_banded_pipeline():
+    """Banded plans (n >= 64) stream u in and f out in z slabs around the
+    per-slab upward / downward launches (htlr_matvec_host, HostPipe): 4 slabs
+    of upward8, the passes, 4 of downward8 -- the result equals the device
+    matvec, for R = 1 and R = 3 (slabs of point-major rows)."""
+    import torch
+    op = make(64, 0.1, 1.0, 0.2)
+    assert op.leaf_pass() == "banded"
+    for R in (1, 3):
+        U = np.random.default_rng(40 + R).standard_normal((64 ** 3, R))
+        ref = H.matmat(op, torch.from_numpy(U).cuda()).cpu().numpy()
+        up = torch.from_numpy(U).pin_memory()
+        out = torch.empty(up.shape, dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            H.matmat(op, up, out=out)
+            assert rel(out.numpy(), ref) <= 1e-14
+        assert op.last_launch_count() >= 8
+
+
+def test_graph_cache_rotating_device_buffers():
+    """Device vectors: graphs are keyed by the caller's (u, f); beyond 4 per
+    shape the least recently used graph is re-pointed (cudaGraphExecUpdate)
+    instead of re-instantiated.  Six rotating buffer pairs, two rounds: every
+    result is the reference's."""
+    import torch
+    op = make(64, 0.1, 1.0, 0.3)
+    rng = np.random.default_rng(11)
+    us = [torch.from_numpy(rng.standard_normal(64 ** 3)).cuda() for _ in range(6)]
+    fs = [torch.empty(64 ** 3, dtype=torch.float64, device="cuda") for _ in range(6)]
+    refs = [H.matvec(op, u.cpu().numpy()) for u in us]
+    for _ in range(2):
+        for u, f, ref in zip(us, fs, refs):
+            H.matvec(op, u, out=f)
+            assert rel(f.cpu().numpy(), ref) <= 1e-13
+
+
 def test_host_vector_path_dense_plan_and_unpinned_rejected():
     """A dense-core plan takes the plain H2D / matvec / D2H route; the C ABI
     rejects pageable host pointers with a ValueError."""
