@@ -287,9 +287,43 @@ def _all_points(grid: UniformGrid) -> np.ndarray:
     return np.stack([m.ravel(order="F") for m in mesh], axis=-1)
 
 
+def _apply_device_fast(op: HTLRMatrix, u, nrhs_expected: Optional[int], out):
+    """Contiguous float64 CUDA input on the plan's device (and a matching
+    contiguous CUDA `out`, if given): straight to htlr_matvec with the
+    caller's buffers -- no reshapes, copies or extra checks (a few us of host
+    time per call, which the small configs' steps are made of).  None when
+    the input needs the general path."""
+    import torch
+    if not (u.is_cuda and u.dtype == torch.float64 and u.is_contiguous() and u.device.index == op.device):
+        return None
+    n_pts = op.num_points
+    if nrhs_expected == 1:
+        if u.dim() != 1 or u.shape[0] != n_pts:
+            return None
+        R = 1
+    else:
+        if u.dim() != 2 or u.shape[0] != n_pts:
+            return None
+        R = u.shape[1]
+    if out is None:
+        f = torch.empty_like(u)
+    elif (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()
+          and out.shape == u.shape and out.device == u.device and out.data_ptr() != u.data_ptr()):
+        f = out
+    else:
+        return None
+    _lib.check(_lib.lib().htlr_matvec(op._plan, u.data_ptr(), f.data_ptr(), R,
+                                      torch.cuda.current_stream(op.device).cuda_stream))
+    return f
+
+
 def _apply(op: HTLRMatrix, u, nrhs_expected: Optional[int], out=None):
     import torch
     is_torch = isinstance(u, torch.Tensor)
+    if is_torch and u.is_cuda:
+        f = _apply_device_fast(op, u, nrhs_expected, out)
+        if f is not None:
+            return f
     if is_torch:
         x = u.to(dtype=torch.float64)
         host = x.device.type != "cuda"
