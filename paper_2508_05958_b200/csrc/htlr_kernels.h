@@ -250,39 +250,35 @@ void launch_sep_apply(const double* tables, int nslots, int NO, const SepItem* i
                       const double* B, int ldb, double* C, int ldc, int R, const double* corr, cudaStream_t st,
                       int zpitch = 0);
 
-// downward pass by per-warp mode products when p = leaf side = 8 in 3-D on a
-// uniform grid (HTLR_DOWN8=0 keeps downward_kernel)
-// upward pass from the leaf boxes for p = leaf side = 8 in 3-D (htlr_sep.cu):
-// one warp per (leaf box, rhs), 8 x 8 factor slices per compressed level,
-// fp64 RED into W_l (zeroed beforehand); unsharded plans
-struct UpLevel8 {
-  int level;
-  const double* Q;   // side x 8 row-major
-  double* W;         // [cluster][R][K_pad], pitched z-planes
-  int K_pad, zpitch;
-};
 struct BandRegion {
   int lo[3], hi[3];
 };
-struct UpParams {
-  int nlev;
-  UpLevel8 lev[kMaxLevels];
+// upward / downward passes over cubes (htlr_cube.cu): the level-(L-1) boxes
+// of separable plans (p = leaf side = 8, 3-D); coarser compressed levels via
+// 8 x 8 transfer matrices M_l = Q_c^T Q_l[cube rows] per axis and sub-position
+constexpr int kMaxCubeCoarse = 4;
+struct CubeLevel {
+  int level;
+  const double* M;   // [2^(L-1-level)][8 x 8], M[a'][a] (a' the cube's coefficient)
+  double* W;         // [cluster][R][K_pad], pitched z-planes (RED target)
+  const double* H;   // [cluster][R][512]
+  int K_pad, zpitch;
 };
-bool upward8_supported(int d, int p, int sL);
-// u != null: the permute fused in (the box read from the F-order u[N][R] of
-// an n^3 grid and written to ub_out, then the upward from registers)
-// [zlo, zhi): leaf-box z range (a z-slab shard: the own boxes' contributions)
-void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
-                    cudaStream_t st, const double* u = nullptr, double* ub_out = nullptr, int n = 0, int zlo = 0,
-                    int zhi = 1 << 30);
-constexpr int kMaxDown8 = 4;   // compressed levels the cooperative downward8 stages (config 4: 2)
-bool downward8_supported(int d, int p, int sL, const DownParams& dp);
-// [zlo, zhi): leaf-box z range written (the overlapped host-vector matvec
-// writes f by z halves)
-void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
-                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st, int zlo = 0,
-                      int zhi = 1 << 30);
-
+struct CubeLevels {
+  const double* Qc;   // level L-1 factor, 16 x 8 row-major; null: no compressed level
+  double* Wc;         // W_{L-1} [cube][R][K_pad_c] (stored, no atomics)
+  const double* Hc;   // H_{L-1} [cube][R][512]
+  int K_pad_c, zpitch_c;
+  int ncoarse;
+  CubeLevel lev[kMaxCubeCoarse];
+};
+bool cube_supported(int d, int p, int sL, int L);
+// [zlo, zhi): leaf-box z range (whole cubes: even bounds)
+void launch_upward_cube(const CubeLevels& cl, int L, int R, int64_t nb, cudaStream_t st, const double* u,
+                        double* ub_out, int ldub, int zpub, int n, int zlo = 0, int zhi = 1 << 30);
+void launch_downward_cube(const CubeLevels& cl, int L, int R, int64_t b0, int64_t nb, cudaStream_t st,
+                          const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n,
+                          int zlo = 0, int zhi = 1 << 30);
 // mapped grid (htlr_mapped.cu)
 void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,
                            const double* coords, const double* widths, int p, cudaStream_t st);

@@ -201,6 +201,9 @@ struct Level {
   // current nrhs, partial-W scratch and per-(cluster, rhs) arrival counters
   int up_ns = 1;
   DevBuf up_scratch, up_count;
+  // separable plans: transfer matrices from the cube level (L - 1) to this
+  // coarser level, [2^(L-1-level)][8 x 8] (htlr_cube.cu)
+  DevBuf Mcube;
 };
 
 }  // namespace
@@ -222,6 +225,7 @@ struct htlr_plan {
   int near_mats = 0;          // leaf pass: matrices [0, near_mats) are near blocks
   bool merged = false;        // leaf-level admissible cores live in the leaf pass
   bool sep = false;           // separable-core formulation (tensor-product kernel, htlr_sep.cu)
+  bool cube_ok = false;       // separable plan whose upward / downward passes run over cubes (htlr_cube.cu)
   DevBuf sep_corr;            // self-block diagonal correction of the separable near field
   DevBuf diag, coeff, gl, ub, Y;
   DevBuf u_stage, f_stage;   // graph-replay staging vectors
@@ -1700,6 +1704,88 @@ static int construct_mapped(htlr_plan* pl, cudaStream_t st) {
   return 0;
 }
 
+// Cube tables of a separable plan (htlr_cube.cu): the upward / downward
+// passes contract 16^3-point cubes (the level-(L-1) boxes) with Q_c = Q_{L-1}
+// and reach every coarser compressed level l through
+//   M_l[s] = Q_c^T Q_l[16 s .. 16 s + 15]   (8 x 8, sub-position s per axis).
+// Q_l's rows over a cube are degree-7 polynomials, which Q_c's columns span,
+// so Q_c M_l[s] = Q_l[cube rows] up to rounding; the residual is checked here
+// and the cube passes are disabled (generic upward / downward) if it is not
+// at rounding level.
+static int build_cube_tables(htlr_plan* pl) {
+  pl->cube_ok = false;
+  const int L = pl->L, lc = L - 1;
+  if (!htlr::cube_supported(pl->d, pl->p, pl->sL, L) || lc < 0) return 0;
+  std::vector<int> coarse;
+  bool has_c = false;
+  for (const auto& ps : pl->passes) {
+    if (ps.to_y) continue;
+    const Level& lv = pl->levels[ps.level];
+    if (lv.Kron.ptr || !lv.Q.ptr) return 0;
+    if (ps.level == lc) has_c = lv.side == 16;
+    else if (ps.level < lc) coarse.push_back(ps.level);
+    else return 0;
+  }
+  if (coarse.empty() && !has_c) {   // no compressed level: the permute only
+    pl->cube_ok = true;
+    return 0;
+  }
+  if (!has_c || (int)coarse.size() > htlr::kMaxCubeCoarse) return 0;
+  const int p = pl->p;
+  std::vector<double> qc(16 * p);
+  CUDA_TRY(cudaMemcpy(qc.data(), pl->levels[lc].Q.ptr, qc.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int l : coarse) {
+    Level& lv = pl->levels[l];
+    std::vector<double> ql((size_t)lv.side * p);
+    CUDA_TRY(cudaMemcpy(ql.data(), lv.Q.ptr, ql.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const int ns = lv.side / 16;
+    std::vector<double> M((size_t)ns * 64);
+    double qmax = 0.0, res = 0.0;
+    for (double v : ql) qmax = std::max(qmax, std::fabs(v));
+    for (int s = 0; s < ns; ++s) {
+      double* Ms = M.data() + 64 * s;
+      for (int a1 = 0; a1 < 8; ++a1)
+        for (int a = 0; a < 8; ++a) {
+          double acc = 0.0;
+          for (int x = 0; x < 16; ++x) acc += qc[x * 8 + a1] * ql[(16 * s + x) * 8 + a];
+          Ms[a1 * 8 + a] = acc;
+        }
+      for (int x = 0; x < 16; ++x)
+        for (int a = 0; a < 8; ++a) {
+          double v = 0.0;
+          for (int a1 = 0; a1 < 8; ++a1) v += qc[x * 8 + a1] * Ms[a1 * 8 + a];
+          res = std::max(res, std::fabs(v - ql[(16 * s + x) * 8 + a]));
+        }
+    }
+    if (!(res <= 1e-13 * std::max(qmax, 1.0))) return 0;
+    if (upload(lv.Mcube, M.data(), M.size() * sizeof(double))) return 1;
+  }
+  pl->cube_ok = true;
+  return 0;
+}
+
+// the cube passes' per-call parameters (false: not applicable to this plan)
+static bool cube_params(const htlr_plan* pl, double* const* W, htlr::CubeLevels& cl) {
+  cl = htlr::CubeLevels{};
+  if (!pl->cube_ok) return false;
+  for (size_t i = 0; i < pl->passes.size(); ++i) {
+    const Pass& ps = pl->passes[i];
+    if (ps.to_y) continue;
+    const Level& lv = pl->levels[ps.level];
+    if (ps.level == pl->L - 1) {
+      cl.Qc = lv.Q.d();
+      cl.Wc = W ? W[i] : nullptr;
+      cl.Hc = lv.H.d();
+      cl.K_pad_c = ps.K_pad;
+      cl.zpitch_c = ps.zpitch;
+    } else {
+      if (cl.ncoarse >= htlr::kMaxCubeCoarse) return false;
+      cl.lev[cl.ncoarse++] = htlr::CubeLevel{ps.level, lv.Mcube.d(), W ? W[i] : nullptr, lv.H.d(), ps.K_pad, ps.zpitch};
+    }
+  }
+  return cl.Qc != nullptr || cl.ncoarse == 0;
+}
+
 int htlr_construct(htlr_plan* pl, void* stream) {
   if (!pl) return fail(-1, "null plan");
   if (pl->device < 0) return fail(-1, "host-only plan: no device work");
@@ -1806,6 +1892,7 @@ int htlr_construct(htlr_plan* pl, void* stream) {
       scratch.release();
       jobsbuf.release();
       pl->sep = true;
+      if (build_cube_tables(pl)) return 1;
       pl->constructed = true;
       return 0;
     }
@@ -1963,7 +2050,7 @@ namespace {
 
 // Host-vector pipeline of a banded plan (htlr_matvec_host): u arrives and f
 // leaves in S z slabs of leaf boxes (contiguous in F-order) on a copy stream;
-// upward8 runs per slab as it lands, downward8 per slab before its copy out.
+// the cube upward runs per slab as it lands, the cube downward per slab before its copy out.
 struct HostPipe {
   int S = 0;                   // slabs
   int zu[5] = {}, zf[5] = {};  // slab bounds (leaf boxes along z) of u and of f
@@ -2296,61 +2383,55 @@ int mv_local(MvCtx& cx, const double* u) {
     zl.n[zl.cnt++] = pl->levels[pl->L].nclusters * R * lp.P;
     cx.zeroed = zl.cnt <= htlr::kMaxLevels + 2;
   }
-  // separable plans (p = leaf side = 8): permute (+ zeroing, W_l included),
-  // then the upward pass of every level from the leaf boxes (upward8)
-  if (pl->shard_world == 1 && pl->sep && cx.zeroed && htlr::upward8_supported(d, p, pl->sL)) {
-    htlr::UpParams up{};
-    bool ok = true;
-    for (size_t i = 0; i < pl->passes.size() && ok; ++i) {
-      const Pass& ps = pl->passes[i];
-      if (ps.to_y) continue;
-      const Level& lv = pl->levels[ps.level];
-      if (lv.Kron.ptr || up.nlev >= htlr::kMaxLevels || zl.cnt >= htlr::kMaxLevels + 2 || ps.zpitch == 0) {
-        ok = false;
-        break;
-      }
-      up.lev[up.nlev++] = htlr::UpLevel8{lv.level, lv.Q.d(), cx.W[i], ps.K_pad, ps.zpitch};
+  // separable plans (p = leaf side = 8): the permute and the upward pass of
+  // every compressed level in one launch over cubes (htlr_cube.cu)
+  htlr::CubeLevels cl;
+  if (pl->shard_world == 1 && pl->sep && cx.zeroed && cube_params(pl, cx.W.data(), cl)) {
+    // accumulators: W_l of the coarser levels (RED targets), W_{L-1} when a
+    // z-slab shard stores only its own cubes (the ranks sum W_l), and those
+    // of the passes that accumulate (the banded passes store every entry)
+    htlr::ZeroList z2;
+    for (int li = 0; li < cl.ncoarse; ++li) {
+      z2.p[z2.cnt] = cl.lev[li].W;
+      z2.n[z2.cnt++] = pl->levels[cl.lev[li].level].nclusters * R * cl.lev[li].K_pad;
     }
-    if (ok && zl.cnt + up.nlev <= htlr::kMaxLevels + 2) {
-      // accumulators: W_l (RED targets of upward8) and those of the passes
-      // that accumulate (the banded passes store every entry)
-      htlr::ZeroList z2;
-      for (int li = 0; li < up.nlev; ++li) {
-        z2.p[z2.cnt] = up.lev[li].W;
-        z2.n[z2.cnt++] = pl->levels[up.lev[li].level].nclusters * R * up.lev[li].K_pad;
+    if (cl.Qc && pl->zslab) {
+      z2.p[z2.cnt] = cl.Wc;
+      z2.n[z2.cnt++] = pl->levels[pl->L - 1].nclusters * R * cl.K_pad_c;
+    }
+    {
+      int q = 0;
+      for (const auto& ps : pl->passes) {
+        if (ps.to_y) continue;
+        if (!ps.band && z2.cnt < htlr::kMaxLevels + 2) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
+        ++q;
       }
-      {
-        int q = 0;
-        for (const auto& ps : pl->passes) {
-          if (ps.to_y) continue;
-          if (!ps.band) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
-          ++q;
-        }
-        if (!lp.band) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
+      if (!lp.band && z2.cnt < htlr::kMaxLevels + 2) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
+    }
+    for (int q = 0; q < z2.cnt; ++q) CUDA_TRY(cudaMemsetAsync(z2.p[q], 0, (size_t)z2.n[q] * sizeof(double), cx.st));
+    // algorithmic work per cube: 16^3 x 8 + 16^2 x 8^2 + 16 x 8^3 MAC (the
+    // three mode products of W_{L-1}) + 3 x 8^4 per coarser level; bytes: u
+    // read + ub written
+    const double ncube = (double)nb / 8.0;
+    const double flops = 2.0 * ncube * R * ((cl.Qc ? 57344.0 : 0.0) + 12288.0 * cl.ncoarse);
+    if (cx.prof_begin(1, pl->L - 1, flops, 2.0 * R8 * (double)pl->N)) return 1;
+    if (HostPipe* hp = cx.pipe) {
+      // one launch per slab of u, each after its copy landed
+      for (int k = 0; k < hp->S; ++k) {
+        CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[1 + k], 0));
+        htlr::launch_upward_cube(cl, pl->L, R, nb, cx.st, u, cx.ub, lp.K_pad, lp.zpitch, pl->n, hp->zu[k],
+                                 hp->zu[k + 1]);
       }
-      for (int q = 0; q < z2.cnt; ++q) CUDA_TRY(cudaMemsetAsync(z2.p[q], 0, (size_t)z2.n[q] * sizeof(double), cx.st));
-      // permute fused into the upward launch: algorithmic work per (leaf box,
-      // level) 3 mode products of 8^4 MAC; bytes u read + ub written
-      const double flops = 2.0 * 3.0 * 4096.0 * (double)nb * R * up.nlev;
-      if (cx.prof_begin(1, pl->L - 1, flops, 2.0 * R8 * (double)pl->N)) return 1;
-      if (HostPipe* hp = cx.pipe) {
-        // one launch per slab of u, each after its copy landed
-        for (int k = 0; k < hp->S; ++k) {
-          CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[1 + k], 0));
-          htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n, hp->zu[k],
-                               hp->zu[k + 1]);
-        }
-        cx.launches += hp->S;
-        return 0;
-      }
-      htlr::launch_upward8(nullptr, lp.K_pad, lp.zpitch, pl->L, R, up, nb, cx.st, u, cx.ub, pl->n,
-                           pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
-      if (cx.prof_end()) return 1;
-      cx.launches += 1;
+      cx.launches += hp->S;
       return 0;
     }
+    htlr::launch_upward_cube(cl, pl->L, R, nb, cx.st, u, cx.ub, lp.K_pad, lp.zpitch, pl->n,
+                             pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
+    if (cx.prof_end()) return 1;
+    cx.launches += 1;
+    return 0;
   }
-  if (cx.pipe) return fail(2, "host pipeline: upward8 not applicable");
+  if (cx.pipe) return fail(2, "host pipeline: cube upward not applicable");
   // unprofiled unsharded matvec: permute + zeroing + every level's upward in
   // one launch (profiling keeps them apart so each phase is timed)
   if (cx.zeroed && !pl->profiling) {
@@ -2401,7 +2482,7 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
   const int nterms = ps.to_y ? 6 : 4;
   if (xy_full && htlr::band_lines_supported(ps.level)) {
     // sharded plans: u itself (every rank holds it; the permuted copy covers
-    // the own boxes only); unsharded: the permuted boxes upward8 wrote (the
+    // the own boxes only); unsharded: the permuted boxes the cube upward wrote (the
     // pitched box rows load with fewer address instructions: 108 vs 115 us)
     const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab);
     const double* src = fo ? u : B;
@@ -2565,13 +2646,15 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   const double frac = (double)nb / (double)nleaf;
   if (!(stages & 2)) return 0;
   if (cx.prof_begin(4, pl->L, 2.0 * down_macs * nb * R, R8 * 3.0 * (double)pl->N * frac)) return 1;
-  const bool down8 = lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && htlr::downward8_supported(d, p, pl->sL, dp);
+  htlr::CubeLevels cl;
+  const bool cube = lp.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && cube_params(pl, nullptr, cl);
+  const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
   if (HostPipe* hp = cx.pipe) {
-    if (!down8) return fail(2, "host pipeline: downward8 not applicable");
+    if (!cube) return fail(2, "host pipeline: cube downward not applicable");
     // one launch per slab of f, each copied out while the next is computed
     for (int k = 0; k < hp->S; ++k) {
-      htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
-                             pl->L, R, dp, b0, nb, cx.st, hp->zf[k], hp->zf[k + 1]);
+      htlr::launch_downward_cube(cl, pl->L, R, b0, nb, cx.st, u, f, pl->Y.d(), av, pl->desc.coeff_const, pl->n,
+                                 hp->zf[k], hp->zf[k + 1]);
       CUDA_TRY(cudaEventRecord(hp->ev[1 + hp->S + k], cx.st));
       CUDA_TRY(cudaStreamWaitEvent(hp->cs, hp->ev[1 + hp->S + k], 0));
       const size_t o = hp->zf[k] * hp->zrow, c = (hp->zf[k + 1] - hp->zf[k]) * hp->zrow;
@@ -2583,10 +2666,9 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
-  if (down8)
-    htlr::launch_downward8(u, f, pl->Y.d(), pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n,
-                           pl->L, R, dp, b0, nb, cx.st, pl->zslab ? pl->zs_lo : 0,
-                           pl->zslab ? pl->zs_hi : 1 << 30);
+  if (cube)
+    htlr::launch_downward_cube(cl, pl->L, R, b0, nb, cx.st, u, f, pl->Y.d(), av, pl->desc.coeff_const, pl->n,
+                               pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
   else
     htlr::launch_downward(u, f, pl->Y.d(), lp.P, pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const,
                           nullptr, d, pl->n, pl->sL, pl->L, R, p, dp, b0, nb, cx.st);
@@ -2782,7 +2864,6 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
     if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
-  htlr::DownParams dp{};
   for (size_t i = 0; i < pl->passes.size(); ++i) {
     const Pass& ps = pl->passes[i];
     if (ps.to_y) continue;
@@ -2791,23 +2872,23 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
                            ps.sep_nblocks, (const htlr::SepCol*)ps.sep_cols.ptr, cx.W[i], ps.K_pad, lv.H.d(), ps.P, R,
                            pl->sep_corr.d(), pl->side_stream, ps.zpitch);
     ++cx.launches;
-    dp.lev[dp.nlev++] = htlr::DownLevel{lv.level, lv.side, P, lv.Q.d(), lv.H.d(), 0, nullptr};
   }
   CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
-  if (!htlr::downward8_supported(3, cx.p, pl->sL, dp)) return fail(2, "overlapped matvec: downward not supported");
+  htlr::CubeLevels cl;
+  if (!cube_params(pl, nullptr, cl)) return fail(2, "overlapped matvec: downward not supported");
   const int64_t nb = pl->levels[pl->L].nclusters;
   const double* av = pl->has_coeff ? pl->coeff.d() : nullptr;
   leaf_range(1);
   CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
-  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, 0,
-                         mz - zs);
+  htlr::launch_downward_cube(cl, pl->L, R, 0, nb, cx.st, us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, 0,
+                             mz - zs);
   ++cx.launches;
   CUDA_TRY(cudaEventRecord(ev[3], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[3], 0));
   CUDA_TRY(cudaMemcpyAsync(fh, fs, lead * sizeof(double), cudaMemcpyDefault, cs));
   leaf_range(2);
-  htlr::launch_downward8(us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n, pl->L, R, dp, 0, nb, cx.st, mz - zs,
-                         mz);
+  htlr::launch_downward_cube(cl, pl->L, R, 0, nb, cx.st, us, fs, pl->Y.d(), av, pl->desc.coeff_const, pl->n,
+                             mz - zs, mz);
   ++cx.launches;
   CUDA_TRY(cudaEventRecord(ev[4], cx.st));
   CUDA_TRY(cudaStreamWaitEvent(cs, ev[4], 0));
@@ -2821,12 +2902,12 @@ int mv_overlap(MvCtx& cx, const double* uh, double* fh, cudaStream_t cs) {
 // Slabs of the banded host pipeline (0: not applicable): a single-GPU banded
 // separable plan whose upward and downward passes are the per-box-octet
 // kernels, which take z ranges of leaf boxes (even bounds).  Four equal
-// slabs: a slab's upward8 / downward8 lasts about one CTA's latency (12-16
+// slabs: a slab's cube upward / downward lasts about one CTA's latency (12-16
 // us) whatever its size (thinner end slabs measured no faster), the copy of
 // a slab ~80 us, so all but the last upward and the first downward hide.
 int band_pipe_slabs(const htlr_plan* pl, int* zu = nullptr, int* zf = nullptr) {
   if (!pl->sep || pl->mapped || pl->shard_world != 1 || pl->zslab || pl->d != 3 || !pl->graphs) return 0;
-  if (!pl->passes[pl->leaf_pass].band || !htlr::upward8_supported(pl->d, pl->p, pl->sL)) return 0;
+  if (!pl->passes[pl->leaf_pass].band || !pl->cube_ok) return 0;
   const int mz = pl->levels[pl->L].m;
   for (int S : {4, 2}) {
     if (mz % (2 * S)) continue;

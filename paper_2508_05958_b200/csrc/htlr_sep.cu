@@ -371,125 +371,6 @@ __global__ void __launch_bounds__((8 * NG + 1) * 32, 1)
   }
 }
 
-// Downward pass + epilogue for p = leaf side = 8 in 3-D (any kernel): one warp
-// per (leaf box, rhs), no shared memory or barriers.  For each compressed
-// level the box's 8 x 8 slices of the level factor (rows of its position in
-// the ancestor box, blocks.py:251-258) are the per-axis matrices of the same
-// mode-product chain as the separable passes (mode z, mode x on the tensor
-// pipe, mode y on DFMA), applied to H[ancestor]; then f = acc + Y + a u,
-// written back in F-order (operators.py:153-156).
-__global__ void __launch_bounds__(256, 4) downward8_kernel(const double* __restrict__ u, double* __restrict__ f,
-                                                         const double* __restrict__ Y, const double* __restrict__ avec,
-                                                         double aconst, int n, int L, int R, DownParams dp, int64_t b0,
-                                                         int64_t nb, int zlo, int zhi) {
-  // CTA = the 8 sibling leaf boxes of one parent cluster (Morton ids
-  // b0 + 8 blockIdx.x + w, sub-positions (px, py, pz) = the child bits of w)
-  // for rhs blockIdx.y.  Per compressed level, f_box += (Qx (x) Qy (x) Qz) H
-  // with the level factor's 8 x 8 slices at the box's position in the
-  // ancestor.  The siblings share slices, so the mode products are shared
-  // (downward of the reference's blocks.py:251-258 per box, regrouped):
-  //   stage 1: Z_pz = H x_z Qz_pz        (2 variants, the t tiles spread over the 8 warps)
-  //   stage 2: X_px,pz = Z_pz x_x Qx_px  (4 variants)
-  //   stage 3: Y_box += X_px,pz x_y Qy_py (each warp its box, DFMA)
-  // 14 mode products per level instead of 24.  H, Z and X live in shared
-  // memory in fragment order (each lane reads back its own 16 bytes).
-  constexpr int HP = kSepZPitch;   // H staged as [c][t][a] at a z pitch of 68 (B fragments conflict free)
-  extern __shared__ __align__(16) double smd[];
-  const int nlev = dp.nlev < kMaxDown8 ? dp.nlev : kMaxDown8;
-  double* sh = smd;                                   // [level][c][t][a]
-  double2* zs = reinterpret_cast<double2*>(smd + nlev * kSepP * HP);   // [pz][t][lane]
-  double2* xs = zs + 2 * kSepP * 32;                                    // [px][pz][t][lane]
-  double* qs = reinterpret_cast<double*>(xs + 4 * kSepP * 32);          // [level][axis][bit][8 x 8]
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.y;
-  const int64_t bb = b0 + 8 * (int64_t)blockIdx.x;   // first box of the sibling group
-  if (bb >= b0 + nb) return;
-  int c0[3];
-  morton_decode(bb, 3, L, c0);   // the group's origin (even coordinates)
-  if (c0[2] < zlo || c0[2] >= zhi) return;   // the group spans z boxes c0z, c0z + 1 (ranges are even)
-  for (int li = 0; li < nlev; ++li) {
-    const DownLevel lv = dp.lev[li];
-    const int64_t anc = bb >> (3 * (L - lv.level));
-    const double* hs = lv.H + (anc * R + r) * (int64_t)lv.P;
-    for (int e = threadIdx.x; e < 256; e += blockDim.x) {
-      const unsigned d = (unsigned)__cvta_generic_to_shared(sh + li * kSepP * HP + (e >> 5) * HP + 2 * (e & 31));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(hs + 2 * e) : "memory");
-    }
-    // the 8 x 8 factor slices of the group's two sub-positions per axis
-    const int mask = (1 << (L - lv.level)) - 1;
-    for (int e = threadIdx.x; e < 3 * 2 * 32; e += blockDim.x) {
-      const int a = e / 64, bit = (e / 32) & 1, k = e & 31;
-      const double* src = lv.Q + (int64_t)(((c0[a] & mask) + bit) * kSepP) * kSepP + 2 * k;
-      const unsigned d = (unsigned)__cvta_generic_to_shared(qs + ((li * 3 + a) * 2 + bit) * 64 + 2 * k);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-    }
-  }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  const int g = lane >> 2, q = lane & 3;
-  const int px = (w >> 2) & 1, py = (w >> 1) & 1, pz = w & 1;
-  double y[kSepP][2];
-#pragma unroll
-  for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
-  for (int li = 0; li < nlev; ++li) {
-    auto slice = [&](int a, int bit) { return qs + ((li * 3 + a) * 2 + bit) * 64; };
-    __syncthreads();   // H staged (first level) / the previous level's Z, X read
-    // stage 1: Z_t[k', a] = sum_c Qz[k'][c] H[a, t, c] for the 2 z slices;
-    // unit = (pz, t): 16 units over 8 warps
-    const double* hsl = sh + li * kSepP * HP + g + HP * q;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int unit = w + 8 * k, vz = unit >> 3, t = unit & 7;
-      const double* Qz = slice(2, vz);
-      double z0 = 0.0, z1 = 0.0;
-      dmma(z0, z1, Qz[g * kSepP + q], hsl[8 * t]);
-      dmma(z0, z1, Qz[g * kSepP + 4 + q], hsl[8 * t + 4 * HP]);
-      zs[(vz * kSepP + t) * 32 + lane] = make_double2(z0, z1);
-    }
-    __syncthreads();
-    // stage 2: T_t[i, k'] = sum_a Qx[i][a] Z_t[k', a] (the C fragment reused
-    // as B with a permuted k order) for the 4 (x, z) slices; 32 units
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int unit = w + 8 * k, vxz = unit >> 3, t = unit & 7;
-      const double* Qx = slice(0, vxz >> 1);
-      const double2 zz = zs[((vxz & 1) * kSepP + t) * 32 + lane];
-      double t0 = 0.0, t1 = 0.0;
-      dmma(t0, t1, Qx[g * kSepP + 2 * q], zz.x);
-      dmma(t0, t1, Qx[g * kSepP + 2 * q + 1], zz.y);
-      xs[(vxz * kSepP + t) * 32 + lane] = make_double2(t0, t1);
-    }
-    __syncthreads();
-    // stage 3: Y[i, j, k'] += sum_t Qy[j][t] T_t[i, k'] of the warp's box
-    const double* Qy = slice(1, py);
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) {
-      const double2 tt = xs[(((px << 1) | pz) * kSepP + t) * 32 + lane];
-#pragma unroll
-      for (int j = 0; j < kSepP; ++j) {
-        const double m = Qy[j * kSepP + t];
-        y[j][0] = fma(m, tt.x, y[j][0]);
-        y[j][1] = fma(m, tt.y, y[j][1]);
-      }
-    }
-  }
-  // epilogue: lane holds (i = g, j, k' = 2 q + jj) of box w
-  const int bc[3] = {c0[0] + px, c0[1] + py, c0[2] + pz};
-  const double* yb = Y ? Y + ((bb + w) * R + r) * 512 + g + 128 * q : nullptr;
-#pragma unroll
-  for (int j = 0; j < kSepP; ++j)
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      const int k = 2 * q + jj;
-      const int64_t gi =
-          (int64_t)(bc[0] * kSepP + g) + (int64_t)n * (bc[1] * kSepP + j) + (int64_t)n * n * (bc[2] * kSepP + k);
-      double v = y[j][jj];
-      if (yb) v += __ldg(yb + 8 * j + 64 * jj);
-      const double a = avec ? __ldg(avec + gi) : aconst;
-      if (a != 0.0) v = fma(a, __ldg(u + gi * R + r), v);
-      f[gi * R + r] = v;
-    }
-}
-
 // Banded leaf pass (strong admissibility, eta = 1, uniform grid): at the leaf
 // level every (target, source) pair is a child pair of an inadmissible parent
 // pair, so the offsets o = sigma - tau a target tau meets form product sets:
@@ -806,184 +687,7 @@ __global__ void __launch_bounds__(band_xy_warps<NB>() * 32, 1)
   }
 }
 
-// Upward pass for p = leaf side = 8 in 3-D (the mirror of downward8): one
-// warp per (leaf box, rhs) reads the box from ub (pitched z-planes, the
-// layout the permute wrote) and, for every compressed level, applies the
-// transposed 8 x 8 slices of the level factor at the box's position in its
-// ancestor (W_l = (Q_z (x) Q_y (x) Q_x)^T u over the cluster's points,
-// upward_body / blocks.py:239-247, split over the ancestor's leaf boxes):
-// mode z and mode x on the tensor pipe, mode y on DFMA, then one fp64 RED per
-// entry into W_l[ancestor] (zeroed by the permute launch).
-__global__ void __launch_bounds__(256, 4) upward8_kernel(const double* __restrict__ ub, int ldub, int zpub, int L,
-                                                          int R, UpParams up, int64_t nb, const double* __restrict__ u,
-                                                          double* __restrict__ ub_out, int n, int zlo, int zhi) {
-  // CTA = the 8 sibling leaf boxes of one parent cluster (Morton ids
-  // 8 blockIdx.x + w) for rhs blockIdx.y.  The 16^3-point cube is read once
-  // (rows of 16 contiguous points of the F-order u, or the boxes of ub) into
-  // shared memory at the pitched box layout, written to ub, and every level's
-  // mode products read it from there; the 8 boxes' W contributions are summed
-  // in shared memory (two halves) before one RED per W entry.
-  constexpr int BP = kSepBoxSmem;   // 8 z-planes at a pitch of 68: mode-z B fragments conflict free
-  extern __shared__ __align__(16) double smu[];
-  double* box = smu;                // [8][BP]
-  double* red = smu + 8 * BP;       // [8][128]
-  double* qs = red + 8 * 128;       // [level][axis][2 sub-positions][8 x 8] factor slices
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.y;
-  const int64_t bb = 8 * (int64_t)blockIdx.x;
-  if (bb >= nb) return;
-  int c0[3];
-  morton_decode(bb, 3, L, c0);   // even coordinates: the cube origin in boxes
-  if (c0[2] < zlo || c0[2] >= zhi) return;   // z-slab shards: the own leaf boxes only
-  if (u) {
-    // row (yy, zz) of the cube: 16 points along x (boxes x = 0, 1); 256
-    // threads x 8 double2 each, every load in flight before the first store
-    double2 v[8];
-    const int xx2 = threadIdx.x & 7, xx = 2 * xx2;
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int row = (threadIdx.x >> 3) + 32 * it, yy = row & 15, zz = row >> 4;
-      const int64_t gi = (int64_t)(c0[0] * kSepP + xx) + (int64_t)n * (c0[1] * kSepP + yy) +
-                         (int64_t)n * n * (c0[2] * kSepP + zz);
-      if (R == 1) {
-        v[it] = __ldg(reinterpret_cast<const double2*>(u + gi));
-      } else {
-        v[it].x = __ldg(u + gi * R + r);
-        v[it].y = __ldg(u + (gi + 1) * R + r);
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int row = (threadIdx.x >> 3) + 32 * it, yy = row & 15, zz = row >> 4;
-      const int wb = ((xx >> 3) << 2) | ((yy >> 3) << 1) | (zz >> 3);   // sibling (Morton child order)
-      double* d = box + wb * BP + (xx & 7) + 8 * (yy & 7) + zpub * (zz & 7);
-      d[0] = v[it].x;
-      d[1] = v[it].y;
-    }
-    __syncthreads();
-    // the permute: every box to ub, pitched as staged (every shared load
-    // issued before the stores)
-    double2* o = reinterpret_cast<double2*>(ub_out + ((bb + w) * R + r) * (int64_t)ldub);
-    const double2* sbox = reinterpret_cast<const double2*>(box + w * BP);
-    double2 c[(BP / 2 + 31) / 32];
-#pragma unroll
-    for (int k = 0; k < (BP / 2 + 31) / 32; ++k)
-      if (lane + 32 * k < BP / 2) c[k] = sbox[lane + 32 * k];
-#pragma unroll
-    for (int k = 0; k < (BP / 2 + 31) / 32; ++k)
-      if (lane + 32 * k < BP / 2) o[lane + 32 * k] = c[k];
-  } else {
-    const double* sbx = ub + ((bb + w) * R + r) * (int64_t)ldub;
-    for (int e = lane; e < BP / 2; e += 32)
-      reinterpret_cast<double2*>(box + w * BP)[e] = __ldg(reinterpret_cast<const double2*>(sbx) + e);
-    __syncthreads();
-  }
-  // the level factors' 8 x 8 slices at the group's two sub-positions per axis
-  for (int li = 0; li < up.nlev; ++li) {
-    const int mask = (1 << (L - up.lev[li].level)) - 1;
-    for (int e = threadIdx.x; e < 3 * 2 * 32; e += blockDim.x) {
-      const int a = e / 64, bit = (e / 32) & 1, kk = e & 31;
-      const double2 v = __ldg(reinterpret_cast<const double2*>(up.lev[li].Q + ((c0[a] & mask) + bit) * kSepP * kSepP) + kk);
-      reinterpret_cast<double2*>(qs + ((li * 3 + a) * 2 + bit) * 64)[kk] = v;
-    }
-  }
-  __syncthreads();
-  int bc[3];
-  morton_decode(bb + w, 3, L, bc);
-  const int g = lane >> 2, q = lane & 3;
-  const double* xs = box + w * BP + g + zpub * q;
-  for (int li = 0; li < up.nlev; ++li) {
-    const UpLevel8 lv = up.lev[li];
-    const int shift = L - lv.level, mask = (1 << shift) - 1;
-    const double* Qx = qs + ((li * 3 + 0) * 2 + ((w >> 2) & 1)) * 64;
-    const double* Qy = qs + ((li * 3 + 1) * 2 + ((w >> 1) & 1)) * 64;
-    const double* Qz = qs + ((li * 3 + 2) * 2 + (w & 1)) * 64;
-    (void)mask;
-    // mode z: Z_t[k', a] = sum_c Qz[c][k'] X[a, t, c]; mode x: T_t[i, k'] =
-    // sum_a Qx[a][i] Z_t[k', a] (the C fragment reused as B, k order
-    // permuted); mode y: W[i, j, k'] += Qy[t][j] T_t[i, k'] -- one t at a time
-    const double az0 = Qz[q * kSepP + g], az1 = Qz[(4 + q) * kSepP + g];
-    const double bx0 = Qx[(2 * q) * kSepP + g], bx1 = Qx[(2 * q + 1) * kSepP + g];
-    double y[kSepP][2];
-#pragma unroll
-    for (int j = 0; j < kSepP; ++j) y[j][0] = y[j][1] = 0.0;
-#pragma unroll
-    for (int t = 0; t < kSepP; ++t) {
-      double z0 = 0.0, z1 = 0.0, t0 = 0.0, t1 = 0.0;
-      dmma(z0, z1, az0, xs[8 * t]);
-      dmma(z0, z1, az1, xs[8 * t + 4 * zpub]);
-      dmma(t0, t1, bx0, z0);
-      dmma(t0, t1, bx1, z1);
-#pragma unroll
-      for (int j = 0; j < kSepP; ++j) {
-        const double m = Qy[t * kSepP + j];
-        y[j][0] = fma(m, t0, y[j][0]);
-        y[j][1] = fma(m, t1, y[j][1]);
-      }
-    }
-    // lane holds (i = g, j, k' = 2 q + jj); sum the 8 boxes, a quarter of
-    // the j at a time (8 KB of shared memory: four CTAs per SM)
-    const int64_t anc = bb >> (3 * shift);
-    double* W = lv.W + (anc * R + r) * (int64_t)lv.K_pad;
-#pragma unroll
-    for (int hj = 0; hj < 4; ++hj) {
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        red[w * 128 + g + 8 * j + 16 * q] = y[2 * hj + j][0];
-        red[w * 128 + g + 8 * j + 16 * q + 64] = y[2 * hj + j][1];
-      }
-      __syncthreads();
-      if (threadIdx.x < 128) {
-        // 128 entries: (i, j', k') = (e & 7, (e >> 3) & 1, 2 ((e >> 4) & 3) + (e >> 6))
-        const int e = threadIdx.x;
-        double v = 0.0;
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) v += red[ww * 128 + e];
-        const int i = e & 7, jl = (e >> 3) & 1, kk = 2 * ((e >> 4) & 3) + (e >> 6);
-        atomicAdd(W + i + 8 * (2 * hj + jl) + lv.zpitch * kk, v);
-      }
-    }
-  }
-}
-
 }  // namespace
-
-bool downward8_supported(int d, int p, int sL, const DownParams& dp) {
-  if (d != 3 || p != kSepP || sL != kSepP || dp.nlev > kMaxDown8) return false;
-  for (int i = 0; i < dp.nlev; ++i)
-    if (dp.lev[i].K || dp.lev[i].qstride || dp.lev[i].P != kSepP * kSepP * kSepP) return false;
-  return true;
-}
-
-bool upward8_supported(int d, int p, int sL) { return d == 3 && p == kSepP && sL == kSepP; }
-
-void launch_upward8(const double* ub, int ldub, int zpub, int L, int R, const UpParams& up, int64_t nb,
-                    cudaStream_t st, const double* u, double* ub_out, int n, int zlo, int zhi) {
-  if (nb <= 0 || (up.nlev == 0 && !u)) return;
-  // sibling groups of 8 boxes; the pitched box layout is what every caller
-  // passes (zpub = kSepZPitch, ldub >= 8 zpub)
-  const size_t smem = (size_t)(8 * kSepBoxSmem + 8 * 128 + up.nlev * 6 * 64) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(upward8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((8 * kSepBoxSmem + 8 * 128 + kMaxLevels * 6 * 64) * sizeof(double)));
-    attr = true;
-  }
-  upward8_kernel<<<dim3((unsigned)((nb + 7) / 8), R), 256, smem, st>>>(ub, ldub, zpub ? zpub : 64, L, R, up, nb, u,
-                                                                       ub_out, n, zlo, zhi);
-}
-
-void launch_downward8(const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n, int L,
-                      int R, const DownParams& dp, int64_t b0, int64_t nb, cudaStream_t st, int zlo, int zhi) {
-  if (nb <= 0) return;
-  // H of every level + the Z (2 x 8 tiles) and X (4 x 8 tiles) fragments
-  const size_t smem =
-      ((size_t)std::min(dp.nlev, kMaxDown8) * (kSepP * kSepZPitch + 6 * 64) + 6 * kSepP * 64) * sizeof(double);
-  // sibling groups of 8 (b0 and nb are whole subtrees of the Morton order)
-  downward8_kernel<<<dim3((unsigned)((nb + 7) / 8), R), 256, smem, st>>>(u, f, Y, a_vec, a_const, n, L, R, dp, b0,
-                                                                         nb, zlo, zhi);
-}
 
 // consumer warp groups of the cooperative kernel (two: alternate columns)
 int sep_block_groups() { return 2; }
