@@ -103,20 +103,30 @@ __device__ __forceinline__ double neg(double v) {
 }
 
 // band of term T (htlr_sep.cu band_count / band_off): count and the i-th
-// per-axis offset for a target of coordinate parity c
+// per-axis offset for a target of coordinate parity c.  T = 0..5 are the six
+// terms (C10, C4, C5, C2, E5, E2); 6..9 are pieces of them, which the first
+// and the last sweep of a pass share between terms:
+//   6: C{-1, 0, 1}   7: C{3 - 6c} (= C10 minus C4 minus C5)   8: E{-1, 0, 1}
+//   9: C4 plus piece 7 (= C10 minus C5)
 template <int T>
 __host__ __device__ constexpr int bcount() {
-  return T == 0 ? 10 : T == 1 ? 4 : (T == 3 || T == 5) ? 2 : 5;
+  return T == 0 ? 10 : T == 1 ? 4 : (T == 3 || T == 5) ? 2 : (T == 6 || T == 8) ? 3 : T == 7 ? 1 : 5;
 }
 template <int T>
 __host__ __device__ constexpr int boff(int c, int i) {
   return T == 0 ? -4 - c + i
        : T == 1 ? (i < 2 ? -4 - c + i : 2 - c + i)
        : (T == 3 || T == 5) ? (i ? 2 : -2)
+       : (T == 6 || T == 8) ? i - 1
+       : T == 7 ? 3 - 6 * c
+       : T == 9 ? (c ? (i < 3 ? -5 + i : i) : (i < 2 ? -4 + i : 1 + i))
        : i - 2;
 }
 template <int T>
 __host__ __device__ constexpr bool bneg() { return T == 1 || T == 2 || T == 5; }
+// factor kind of a term or piece: 0 admissible (C), 1 near (E)
+template <int T>
+__host__ __device__ constexpr int bkind() { return (T == 4 || T == 5 || T == 8) ? 1 : 0; }
 
 // spread the 4 low bits of v to every third bit (Morton interleave)
 __host__ __device__ constexpr int spread3(int v) {
@@ -145,7 +155,7 @@ __device__ __forceinline__ void stage_tables(double* __restrict__ dst, const dou
 template <int NB, int T, int SLOT, bool SIGN, int B0 = 0, int B1 = NB, bool CHK = false>
 __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO, int lane, const double (&in)[NB][2],
                                           double (&acc)[NB][2], int tlo = 0, int thi = NB) {
-  constexpr int kind = T >= 4 ? 1 : 0;
+  constexpr int kind = bkind<T>();
   const int OR = (NO - 1) / 2;
 #pragma unroll
   for (int i = 0; i < bcount<T>(); ++i) {
@@ -170,21 +180,19 @@ __device__ __forceinline__ void band_regs(const double* __restrict__ tab, int NO
 }
 
 // The same band with the B fragments read from shared memory cells
-// (cell s of the warp's row: a double2 per lane, lane order).
+// (cell s of the warp's row: a double2 per lane, lane order); unsigned (the
+// cells carry the terms' signs).
 template <int NB, int T, int B0, int B1>
 __device__ __forceinline__ void band_smem(const double* __restrict__ tab, int NO, int lane,
                                           const double2* __restrict__ row, double (&acc)[NB][2]) {
-  constexpr int kind = T >= 4 ? 1 : 0;
+  constexpr int kind = bkind<T>();
   const int OR = (NO - 1) / 2;
 #pragma unroll
   for (int i = 0; i < bcount<T>(); ++i) {
     const double* p0 = tab + (kind * NO + boff<T>(0, i) + OR) * kTabSlot + 64;
     const double* p1 = tab + (kind * NO + boff<T>(1, i) + OR) * kTabSlot + 64;
-    double a00 = lds(p0 + lane), a01 = lds(p0 + 32 + lane);
-    double a10 = lds(p1 + lane), a11 = lds(p1 + 32 + lane);
-    if (bneg<T>()) {
-      a00 = neg(a00); a01 = neg(a01); a10 = neg(a10); a11 = neg(a11);
-    }
+    const double a00 = lds(p0 + lane), a01 = lds(p0 + 32 + lane);
+    const double a10 = lds(p1 + lane), a11 = lds(p1 + 32 + lane);
 #pragma unroll
     for (int b = B0; b < B1; ++b) {
       const int s = b + boff<T>(b & 1, i);
@@ -216,7 +224,8 @@ constexpr int kLineWarps = 12;
 template <int NB, int NT, bool R1, int HALF, bool FO = false, bool CHK = false>
 __device__ __forceinline__ void line_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
                                            const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
-                                           int u0, int ustride, int nunits, int usel, int n, int zlo, int zhi) {
+                                           int u0, int ustride, int nunits, int usel, int n, int zlo, int zhi,
+                                           double2* __restrict__ spill) {
   constexpr int H = NB / 2;
   constexpr int S0 = HALF ? (H - 5 > 0 ? H - 5 : 0) : 0;         // loaded source boxes [S0, S1)
   constexpr int S1 = HALF ? NB : (H + 5 < NB ? H + 5 : NB);
@@ -251,28 +260,62 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
     const int y = line & 7, col = (line >> 3) % (NB * NB), r = (line >> 3) / (NB * NB);
     // lane's C fragment: (z' = g, x = 2q + j) of every target box
     double* const ob = ws + (morton3(col % NB, col / NB, 0) * R + r) * 512 + 64 * g + 8 * y + 2 * q;
-    auto term = [&](auto tc) {
-      constexpr int T = decltype(tc)::value;
-      double acc[NB][2];
-      zero(acc);
-      band_regs<NB, T, 0, false, HALF * H, HALF * H + H, CHK>(tab, NO, lane, in, acc, zlo, zhi);
+    // The six terms' bands are unions of five pieces (B = C{-2, 2}, M =
+    // C{-1, 0, 1}, P = C{3 - 6c}, A = C4; EB = E{-2, 2}, EM = E{-1, 0, 1}):
+    //   C2 = B, C5 = B + M, C10 = B + M + P + A, C4 = A, E2 = EB, E5 = EB + EM,
+    // so one accumulator chain per kind gives every term with 15 instead of 28
+    // offsets per target box; B + M + P waits in shared memory while A runs.
+    double acc[NB][2];
+    auto band = [&](auto tc) {
+      band_regs<NB, decltype(tc)::value, 0, false, HALF * H, HALF * H + H, CHK>(tab, NO, lane, in, acc, zlo, zhi);
+    };
+    auto put = [&](int T) {
       double* o = ob + T * tstride;
 #pragma unroll
       for (int b = HALF * H; b < HALF * H + H; ++b)
         if (!CHK || (b >= zlo && b < zhi))
           *reinterpret_cast<double2*>(o + spread3(b) * (int64_t)R * 512) = make_double2(acc[b][0], acc[b][1]);
     };
-    // a runtime loop over the terms: the compiler cannot interleave (and keep
-    // live) several terms' accumulators
+    // a runtime loop over the phases: the compiler cannot interleave (and keep
+    // live) several accumulator chains
 #pragma unroll 1
-    for (int t = 0; t < NT; ++t) {
-      switch (t) {
-        case 0: term(std::integral_constant<int, 0>{}); break;
-        case 1: term(std::integral_constant<int, 1>{}); break;
-        case 2: term(std::integral_constant<int, 2>{}); break;
-        case 3: term(std::integral_constant<int, 3>{}); break;
-        case 4: term(std::integral_constant<int, 4>{}); break;
-        default: term(std::integral_constant<int, 5>{}); break;
+    for (int ph = 0; ph < NT; ++ph) {
+      switch (ph) {
+        case 0:
+          zero(acc);
+          band(std::integral_constant<int, 3>{});
+          put(3);
+          break;
+        case 1:
+          band(std::integral_constant<int, 6>{});
+          put(2);
+          break;
+        case 2:
+          band(std::integral_constant<int, 7>{});
+#pragma unroll
+          for (int b = 0; b < H; ++b) spill[b * 32] = make_double2(acc[HALF * H + b][0], acc[HALF * H + b][1]);
+          break;
+        case 3:
+          zero(acc);
+          band(std::integral_constant<int, 1>{});
+          put(1);
+#pragma unroll
+          for (int b = 0; b < H; ++b) {
+            const double2 v = spill[b * 32];
+            acc[HALF * H + b][0] += v.x;
+            acc[HALF * H + b][1] += v.y;
+          }
+          put(0);
+          break;
+        case 4:
+          zero(acc);
+          band(std::integral_constant<int, 5>{});
+          put(5);
+          break;
+        default:
+          band(std::integral_constant<int, 8>{});
+          put(4);
+          break;
       }
     }
   };
@@ -301,7 +344,7 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
 template <int NB, int T>
 __device__ __forceinline__ void band_pair(const double* __restrict__ tab, int NO, int lane, const double (&in)[12][2],
                                           double (&acc)[2][2]) {
-  constexpr int kind = T >= 4 ? 1 : 0;
+  constexpr int kind = bkind<T>();
   const int OR = (NO - 1) / 2;
 #pragma unroll
   for (int i = 0; i < bcount<T>(); ++i) {
@@ -394,17 +437,17 @@ template <int NB, int NT, bool R1, bool FO>
 __device__ __forceinline__ void dispatch_halves(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
                                                 const double* __restrict__ ub, double* __restrict__ ws,
                                                 int64_t tstride, int gw, int ustride, int nlines, int n, int zlo,
-                                                int zhi) {
+                                                int zhi, double2* __restrict__ spill) {
   const bool h0 = zlo < NB / 2, h1 = zhi > NB / 2;
   if (h0 && h1) {
     if (gw & 1)
-      line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+      line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi, spill);
     else
-      line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi);
+      line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, 2 * nlines, 0, n, zlo, zhi, spill);
   } else if (h1) {
-    line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+    line_units<NB, NT, R1, 1, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi, spill);
   } else {
-    line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi);
+    line_units<NB, NT, R1, 0, FO>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, 1, n, zlo, zhi, spill);
   }
 }
 
@@ -423,6 +466,7 @@ __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const dou
                                                                       int64_t tstride, int n, int zlo, int zhi) {
   const int R = R1 ? 1 : R_;   // one rhs: every box offset a compile-time constant
   __shared__ double tab[2 * 15 * kTabSlot];
+  extern __shared__ __align__(16) double2 spill_sm[];   // [warp][target box of the half][lane]
   stage_tables<64>(tab, tables, NO);   // the units sync after issuing their first loads
   const int gw = blockIdx.x + gridDim.x * (threadIdx.x >> 5);
   const int ustride = gridDim.x * (blockDim.x >> 5);
@@ -430,7 +474,8 @@ __global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const dou
   if (KIND == 2)
     pair_units<NB, NT, R1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, n, zlo & ~1, (zhi + 1) & ~1);
   else
-    dispatch_halves<NB, NT, R1, KIND == 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi);
+    dispatch_halves<NB, NT, R1, KIND == 1>(tab, NO, R, ldub, zpub, ub, ws, tstride, gw, ustride, nlines, n, zlo, zhi,
+                                           spill_sm + (threadIdx.x >> 5) * (NB / 2) * 32 + (threadIdx.x & 31));
 }
 
 // y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
@@ -476,29 +521,54 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tm = tmem_sh + ((uint32_t)(32 * (w & 3)) << 16) + 16 * NQ * (w >> 2);
-  auto term = [&](auto tc) {
-    constexpr int T = decltype(tc)::value;
+  // The x sweeps share pieces between the terms (bcount / boff): with the
+  // cells S running through  V10, V10 - V5, V10 - V5 + V2, -V4, W5, W5 - W2
+  // (V_t, W_t the y-swept terms; the y sweep carries the term's sign and adds
+  // to the cells it wrote in the phase before),
+  //   Y = (C4 + P)_x V10 + M_x (V10 - V5) + B_x (V10 - V5 + V2) + C4_x (-V4)
+  //       + EM_x W5 + EB_x (W5 - W2)
+  // -- 19 instead of 28 offsets per target cell.
+  // phase: term T's y sweep (ADD: onto the cells), then x piece XT of the
+  // cells; TN = the next phase's term, whose lines load during the x sweep
+  auto term = [&](auto tc, auto xc, auto addc, auto firstc, int TN) {
+    constexpr int T = decltype(tc)::value, XT = decltype(xc)::value;
+    constexpr bool ADD = decltype(addc)::value, FIRST = decltype(firstc)::value;
     constexpr int H = NB / 2;
     {
       double acc[NB][2];
-      zero(acc);
-      band_regs<NB, T, 0, false, 0, H>(tab, NO, lane, in, acc);
+      if (ADD) {
+#pragma unroll
+        for (int b = 0; b < H; ++b) {
+          const double2 v = mine[b * NB * 32];
+          acc[b][0] = v.x, acc[b][1] = v.y;
+        }
+      } else {
+        zero(acc);
+      }
+      band_regs<NB, T, 0, true, 0, H>(tab, NO, lane, in, acc);
 #pragma unroll
       for (int b = 0; b < H; ++b) mine[b * NB * 32] = make_double2(acc[b][0], acc[b][1]);
-      band_regs<NB, T, 0, false, H, NB>(tab, NO, lane, in, acc);
+      if (ADD) {
+#pragma unroll
+        for (int b = H; b < NB; ++b) {
+          const double2 v = mine[b * NB * 32];
+          acc[b][0] = v.x, acc[b][1] = v.y;
+        }
+      }
+      band_regs<NB, T, 0, true, H, NB>(tab, NO, lane, in, acc);
 #pragma unroll
       for (int b = H; b < NB; ++b) mine[b * NB * 32] = make_double2(acc[b][0], acc[b][1]);
     }
     __syncthreads();
-    if (T + 1 < NT) load(T + 1);   // in flight during the x sweep
+    if (TN >= 0) load(TN);   // in flight during the x sweep
     // x sweep of the warp's row, four cells at a time, added to the TMEM accumulator
     auto quarter = [&](auto qc) {
       constexpr int Q = decltype(qc)::value;
       double acc[NB][2];
       zero(acc);
-      band_smem<NB, T, 4 * Q, 4 * Q + 4>(tab, NO, lane, row, acc);
+      band_smem<NB, XT, 4 * Q, 4 * Q + 4>(tab, NO, lane, row, acc);
       double v[4][2];
-      if (T > 0) {
+      if (!FIRST) {
         tmem_ld16(tm + 16 * Q, v);
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c][0] += acc[4 * Q + c][0], v[c][1] += acc[4 * Q + c][1];
@@ -514,15 +584,17 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
     if (NQ > 3) quarter(std::integral_constant<int, (NQ > 3 ? 3 : 0)>{});
     __syncthreads();
   };
+  using TT = std::true_type;
+  using FF = std::false_type;
 #pragma unroll 1
-  for (int t = 0; t < NT; ++t) {
-    switch (t) {
-      case 0: term(std::integral_constant<int, 0>{}); break;
-      case 1: term(std::integral_constant<int, 1>{}); break;
-      case 2: term(std::integral_constant<int, 2>{}); break;
-      case 3: term(std::integral_constant<int, 3>{}); break;
-      case 4: term(std::integral_constant<int, 4>{}); break;
-      default: term(std::integral_constant<int, 5>{}); break;
+  for (int ph = 0; ph < NT; ++ph) {
+    switch (ph) {
+      case 0: term(std::integral_constant<int, 0>{}, std::integral_constant<int, 9>{}, FF{}, TT{}, 2); break;
+      case 1: term(std::integral_constant<int, 2>{}, std::integral_constant<int, 6>{}, TT{}, FF{}, 3); break;
+      case 2: term(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{}, TT{}, FF{}, 1); break;
+      case 3: term(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}, FF{}, FF{}, NT > 4 ? 4 : -1); break;
+      case 4: term(std::integral_constant<int, 4>{}, std::integral_constant<int, 8>{}, FF{}, FF{}, 5); break;
+      default: term(std::integral_constant<int, 5>{}, std::integral_constant<int, 5>{}, TT{}, FF{}, -1); break;
     }
   }
   // lane holds (x' = g, y = 2q + j) of cells (bx = b, by = w)
@@ -783,8 +855,15 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
   const int kind = !halves ? 2 : n ? 1 : 0;
   auto go = [&](auto r1, auto kc) {
-    band_line_kernel<NB, NT, decltype(r1)::value, decltype(kc)::value>
-        <<<(unsigned)grid, warps * 32, 0, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n, zlo, zhi);
+    auto kern = band_line_kernel<NB, NT, decltype(r1)::value, decltype(kc)::value>;
+    // the whole-half units park one accumulator (NB / 2 boxes) per warp in shared memory
+    const size_t smem = decltype(kc)::value == 2 ? 0 : (size_t)warps * (NB / 2) * 32 * sizeof(double2);
+    static bool attr = false;
+    if (!attr && smem > 16 * 1024) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    kern<<<(unsigned)grid, warps * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n, zlo, zhi);
   };
   using T1 = std::true_type;
   using F1 = std::false_type;
