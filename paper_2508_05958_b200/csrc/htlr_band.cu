@@ -31,13 +31,19 @@
 // lane order; after a barrier warp w reads box row by = w from shared memory
 // as x-sweep B fragments (the y sweep's C fragment is the x sweep's B
 // fragment with the k order permuted, the tables' mode-x A fragments use the
-// same permutation) and accumulates sign_t * X_x(t) into its registers.  The
-// last term ends in Y = scale * acc + corr * ub (self pairs).  128 KB of
-// shared memory (NB = 16): the transposition buffer of one term, no staging.
+// same permutation) and adds its x sweep to the plane's accumulator in tensor
+// memory.  The last term ends in Y = scale * acc + corr * ub (self pairs).
+// 128 KB of shared memory (NB = 16): the transposition buffer, no staging.
+//
+// The first and the last sweep share work between the terms (bcount / boff):
+// the six bands are unions of five pieces, so the z sweep runs 15 instead of
+// 28 offsets per target box, and the x sweep applies each piece once to a
+// running combination of the y-swept terms, 19 instead of 28.
 #include "htlr_device.cuh"
 #include "htlr_kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace htlr {
@@ -218,9 +224,9 @@ __device__ __forceinline__ void zero(double (&a)[NB][2]) {
 // keeps its half): every SM sub-partition gets the same number of units to
 // within one (a single warp with two accumulator chains already saturates
 // its sub-partition's DMMA pipe, 1 DMMA.8x8x4 per 16 cycles, dependent
-// latency 26 cycles: tools/dmma_latency.cu), and each unit's source boxes are
-// loaded while the previous unit computes (two register buffers).
+// latency 26 cycles: tools/dmma_latency.cu).
 constexpr int kLineWarps = 12;
+constexpr int kZWarps = 16;   // z sweep over whole halves (band_line_kernel KIND 0, 1)
 template <int NB, int NT, bool R1, int HALF, bool FO = false, bool CHK = false>
 __device__ __forceinline__ void line_units(const double* __restrict__ tab, int NO, int R, int ldub, int zpub,
                                            const double* __restrict__ ub, double* __restrict__ ws, int64_t tstride,
@@ -319,19 +325,15 @@ __device__ __forceinline__ void line_units(const double* __restrict__ tab, int N
       }
     }
   };
-  double a[NB][2], b[NB][2];
-  int u = u0;
-  if (u < nunits) load(u, a);
+  // one register buffer per warp: the other warps of the sub-partition cover
+  // a unit's loads (a second buffer with 12 warps, or 8 and 20 warps, measured
+  // the same: the sweep is bound by its 117 MB of loads and stores, 19.5 us
+  // without the DMMAs, next to 14 us of DMMA issue)
+  double a[NB][2];
   __syncthreads();   // the tables (staged by the caller) are in place
-  while (u < nunits) {
-    const int un = u + ustride;
-    if (un < nunits) load(un, b);
+  for (int u = u0; u < nunits; u += ustride) {
+    load(u, a);
     compute(u, a);
-    if (un >= nunits) break;
-    const int unn = un + ustride;
-    if (unn < nunits) load(unn, a);
-    compute(un, b);
-    u = unn;
   }
 }
 
@@ -459,8 +461,8 @@ __device__ __forceinline__ void dispatch_halves(const double* __restrict__ tab, 
 // 2: sibling pairs of a narrow z slab.  Separate kernels keep the unsharded
 // kernel's code what it was (one kernel with all three bodies measured 33 ->
 // 37 us for config 4's z sweep).
-template <int NB, int NT, bool R1, int KIND>
-__global__ void __launch_bounds__(kLineWarps * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
+template <int NB, int NT, bool R1, int KIND, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) band_line_kernel(const double* __restrict__ tables, int NO,
                                                                       int R_, const double* __restrict__ ub, int ldub,
                                                                       int zpub, double* __restrict__ ws,
                                                                       int64_t tstride, int n, int zlo, int zhi) {
@@ -762,19 +764,29 @@ __device__ __forceinline__ void xline_units(const double* __restrict__ tab, int 
         in[b][1] = w2.y;
       }
     };
+    // the x pieces shared between the terms (band_plane_kernel): the line S
+    // runs through V10, V10 - V5, V10 - V5 + V2, then V4 (negated band), W5,
+    // W5 - W2 -- 19 instead of 28 offsets per target cell
+    auto axpy = [&](double sgn, double(&s_)[NB][2], const double(&t_)[NB][2]) {
+#pragma unroll
+      for (int b = S0; b < S1; ++b) s_[b][0] = fma(sgn, t_[b][0], s_[b][0]), s_[b][1] = fma(sgn, t_[b][1], s_[b][1]);
+    };
     load(0, bufa);
-    load(1, bufb);
-    band_regs<NB, 0, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
-    load(2, bufa);
-    band_regs<NB, 1, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+    load(2, bufb);
+    band_regs<NB, 9, 64, false, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+    axpy(-1.0, bufa, bufb);
     load(3, bufb);
-    band_regs<NB, 2, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+    band_regs<NB, 6, 64, false, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+    axpy(1.0, bufa, bufb);
+    load(1, bufb);
+    band_regs<NB, 3, 64, false, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
     if (NT > 4) load(4, bufa);
-    band_regs<NB, 3, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+    band_regs<NB, 1, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
     if (NT > 4) {
       load(5, bufb);
-      band_regs<NB, 4, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
-      band_regs<NB, 5, 64, true, HALF * H, HALF * H + H>(tab, NO, lane, bufb, acc);
+      band_regs<NB, 8, 64, false, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
+      axpy(-1.0, bufa, bufb);
+      band_regs<NB, 5, 64, false, HALF * H, HALF * H + H>(tab, NO, lane, bufa, acc);
     }
     // lane holds (x' = g, y = 2q + j) of target cells bx in the half
 #pragma unroll
@@ -850,19 +862,19 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
   // one CTA of kLineWarps warps per SM (the stride over the 2 x lines
   // half-line units must be even: a warp keeps its half)
   if (max_ctas > 0) sms = std::min(sms, max_ctas);
-  const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
-  const int warps = kLineWarps;
   const bool halves = (zlo == 0 || zlo == NB / 2) && (zhi == NB || zhi == NB / 2);
   const int kind = !halves ? 2 : n ? 1 : 0;
   auto go = [&](auto r1, auto kc) {
-    auto kern = band_line_kernel<NB, NT, decltype(r1)::value, decltype(kc)::value>;
-    // the whole-half units park one accumulator (NB / 2 boxes) per warp in shared memory
-    const size_t smem = decltype(kc)::value == 2 ? 0 : (size_t)warps * (NB / 2) * 32 * sizeof(double2);
-    static bool attr = false;
-    if (!attr && smem > 16 * 1024) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    constexpr bool r1v = decltype(r1)::value;
+    constexpr int kv = decltype(kc)::value;
+    // whole-half units: kZWarps warps with one register buffer each, one
+    // accumulator (NB / 2 boxes) per warp parked in shared memory; pair units:
+    // kLineWarps warps, two register buffers
+    constexpr int warps = kv == 2 ? kLineWarps : kZWarps;
+    const size_t smem = kv == 2 ? (size_t)0 : (size_t)warps * (NB / 2) * 32 * sizeof(double2);
+    auto kern = band_line_kernel<NB, NT, r1v, kv, warps>;
+    const int64_t grid = std::min<int64_t>(sms, std::max<int64_t>(1, lines / 4));
+    if (smem > 16 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, warps * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, n, zlo, zhi);
   };
   using T1 = std::true_type;

@@ -127,9 +127,10 @@ __global__ void __launch_bounds__(kCubeThreads, 4)
   }
   if (threadIdx.x < 128 && cl.Qc) qs[threadIdx.x] = __ldg(cl.Qc + threadIdx.x);
   stage_transfers(cl, cc, L, ms);
-  // the permute: every loaded point to its pitched leaf box in ub
+  // the permute: every loaded point to its pitched leaf box in ub (skipped
+  // when the leaf pass reads u itself)
 #pragma unroll
-  for (int yy = 0; yy < 2; ++yy) {
+  for (int yy = 0; yy < 2 && ub_out; ++yy) {
     const int y = 2 * w + yy;
 #pragma unroll
     for (int h = 0; h < 2; ++h)

@@ -1463,23 +1463,25 @@ static bool band_check(const htlr_plan* pl, Pass& ps, int OR, const std::vector<
     if (!same) ok.store(false);
   });
   if (!ok.load()) return false;
-  // mode products the three sweeps run (per rhs): per axis and box position q,
-  // the in-domain offsets of the six terms
+  // mode products the three sweeps run (per rhs), per box position q along a
+  // line: the y sweep applies each term's band (28 offsets away from the
+  // boundary at the leaf level); the z and x sweeps share band pieces between
+  // the terms (htlr_band.cu bcount / boff): z 15 (B, M, P, C4 and EB, EM once
+  // each), x 19 (C4 + P, M, B, C4 and EM, EB)
   double per_line = 0;
   for (int q = 0; q < nb; ++q) {
     const int c = q & 1;
     auto in = [&](int o) { return q + o >= 0 && q + o < nb; };
-    int k = 0;
-    for (int o = -4 - c; o <= 5 - c; ++o) k += in(o);
-    for (int o : {-4 - c, -3 - c, 4 - c, 5 - c}) k += in(o);
-    for (int rep = 0; rep < (ps.to_y ? 2 : 1); ++rep) {
-      for (int o = -2; o <= 2; ++o) k += in(o);
-      for (int o : {-2, 2}) k += in(o);
-    }
-    per_line += k;
+    int A = 0, B = in(-2) + in(2), M = in(-1) + in(0) + in(1), P = in(3 - 6 * c);
+    for (int o : {-4 - c, -3 - c, 4 - c, 5 - c}) A += in(o);
+    const int nk = ps.to_y ? 2 : 1;   // factor kinds with a {-2..2} and a {-2, 2} term
+    const int ysw = (A + B + M + P) + A + nk * ((B + M) + B);
+    const int zsw = A + P + nk * (B + M);
+    const int xsw = (A + P) + A + nk * (M + B);
+    per_line += ysw + zsw + xsw;
   }
   // per rhs, the region's share of the sweeps (halo lines of the z sweep not counted)
-  flops = 3.0 * (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * L));
+  flops = (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * L));
   for (int a = 0; a < 3; ++a) {
     ps.band_lo[a] = lo[a];
     ps.band_hi[a] = hi[a];
@@ -2066,6 +2068,8 @@ struct MvCtx {
   cudaStream_t st;
   HostPipe* pipe = nullptr;
   bool zeroed = false;      // the permute launch zeroed the remote phase's accumulators
+  bool whole = false;       // local and remote phase in one call (htlr_matvec): they may share the side stream
+  bool side_forked = false; // the upward pass already runs on the side stream (mv_local forked it)
   int R, d, p, P;
   double* ub;
   std::vector<double*> W;   // per pass (nullptr for the leaf pass)
@@ -2361,6 +2365,18 @@ bool prologue_params(MvCtx& cx, const double* u, const htlr::ZeroList& zl, htlr:
   return true;
 }
 
+// The banded leaf pass of an unsharded plan reads the F-order u itself (line /
+// plane kernels over whole x-y planes), so nothing on the leaf pass's path
+// waits for the upward pass: that runs on the side stream, before the level
+// passes, beside the leaf z sweep -- and writes no permuted copy of u.
+static bool leaf_from_u(const htlr_plan* pl) {
+  if (!pl->sep || pl->mapped || pl->d != 3 || pl->leaf_pass < 0) return false;
+  const Pass& lp = pl->passes[pl->leaf_pass];
+  const int nb = 1 << lp.level;
+  return lp.band && lp.from_ub && htlr::band_lines_supported(lp.level) && lp.band_lo[0] == 0 && lp.band_lo[1] == 0 &&
+         lp.band_hi[0] == nb && lp.band_hi[1] == nb;
+}
+
 int mv_local(MvCtx& cx, const double* u) {
   htlr_plan* pl = cx.pl;
   if (pl->mapped) return mv_local_mapped(cx, u);
@@ -2408,7 +2424,21 @@ int mv_local(MvCtx& cx, const double* u) {
       }
       if (!lp.band && z2.cnt < htlr::kMaxLevels + 2) z2.p[z2.cnt] = zl.p[q], z2.n[z2.cnt++] = zl.n[q];
     }
-    for (int q = 0; q < z2.cnt; ++q) CUDA_TRY(cudaMemsetAsync(z2.p[q], 0, (size_t)z2.n[q] * sizeof(double), cx.st));
+    // leaf pass reading u itself: no permuted copy, and (unprofiled, outside
+    // the host pipeline) the zeroing and the upward pass go to the side stream
+    const bool from_u = leaf_from_u(pl);
+    double* const ub_out = from_u ? nullptr : cx.ub;
+    cudaStream_t ust = cx.st;
+    if (from_u && cx.whole && !pl->zslab && !pl->profiling && !cx.pipe) {
+      if (!pl->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->side_stream, cudaStreamNonBlocking));
+      for (auto& ev : pl->side_ev)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
+      CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
+      cx.side_forked = true;
+      ust = pl->side_stream;
+    }
+    for (int q = 0; q < z2.cnt; ++q) CUDA_TRY(cudaMemsetAsync(z2.p[q], 0, (size_t)z2.n[q] * sizeof(double), ust));
     // algorithmic work per cube: 16^3 x 8 + 16^2 x 8^2 + 16 x 8^3 MAC (the
     // three mode products of W_{L-1}) + 3 x 8^4 per coarser level; bytes: u
     // read + ub written
@@ -2419,13 +2449,13 @@ int mv_local(MvCtx& cx, const double* u) {
       // one launch per slab of u, each after its copy landed
       for (int k = 0; k < hp->S; ++k) {
         CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[1 + k], 0));
-        htlr::launch_upward_cube(cl, pl->L, R, nb, cx.st, u, cx.ub, lp.K_pad, lp.zpitch, pl->n, hp->zu[k],
+        htlr::launch_upward_cube(cl, pl->L, R, nb, cx.st, u, ub_out, lp.K_pad, lp.zpitch, pl->n, hp->zu[k],
                                  hp->zu[k + 1]);
       }
       cx.launches += hp->S;
       return 0;
     }
-    htlr::launch_upward_cube(cl, pl->L, R, nb, cx.st, u, cx.ub, lp.K_pad, lp.zpitch, pl->n,
+    htlr::launch_upward_cube(cl, pl->L, R, nb, ust, u, ub_out, lp.K_pad, lp.zpitch, pl->n,
                              pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
     if (cx.prof_end()) return 1;
     cx.launches += 1;
@@ -2465,8 +2495,13 @@ int mv_local(MvCtx& cx, const double* u) {
   return 0;
 }
 
-// SMs the leaf z sweep leaves to the level passes running beside it
-static constexpr int kLevelSMs = 20;
+// SMs the leaf z sweep leaves to the passes running beside it on the side
+// stream: the level passes (20), or the upward pass and the level passes
+// (48: the z sweep is bound by its memory traffic, not by its SM count, and
+// the upward pass then ends with it; measured 20 / 40 / 48 / 56 / 64: config
+// 4's step 0.1307 (upward first, on the main stream) / 0.1323 / 0.1280 /
+// 0.1286 / 0.1284 ms)
+static int level_sms(bool with_upward) { return with_upward ? 48 : 20; }
 
 // One sweep of a banded pass (0: z sweep, 1: the fused y-x sweep; 2: the
 // legacy separate x sweep, a no-op for the line/plane kernels).  Regions that
@@ -2484,7 +2519,7 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
     // sharded plans: u itself (every rank holds it; the permuted copy covers
     // the own boxes only); unsharded: the permuted boxes the cube upward wrote (the
     // pitched box rows load with fewer address instructions: 108 vs 115 us)
-    const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab);
+    const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab || leaf_from_u(pl));
     const double* src = fo ? u : B;
     const int n = fo ? pl->n : 0;
     if (sweep == 0)
@@ -2537,10 +2572,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   // banded leaf pass: the fork first, then its z sweep on all but
-  // kLevelSMs SMs, which the level passes (side stream) run on meanwhile; they
+  // level_sms SMs, which the upward and level passes (side stream) run on meanwhile; they
   // go on filling the SMs the y-x sweep leaves idle (128 planes on 148 SMs)
   bool leaf_z_done = false;
-  if (fork) {
+  if (fork && !cx.side_forked) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
     CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
   }
@@ -2549,7 +2584,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     if (pl->sep && lq.band) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
-      launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u, sms - kLevelSMs);
+      launch_band_sweep(pl, lq, 0, cx.ub, pl->Y.d(), R, cx.st, u, sms - level_sms(cx.side_forked));
       leaf_z_done = true;
     }
   }
@@ -2627,7 +2662,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
                       ps.gen.ptr ? ps.gen.d() : nullptr);
     if (cx.prof_end()) return 1;
   }
-  if (fork) {
+  if (fork || cx.side_forked) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
     CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
   }
@@ -2679,6 +2714,16 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
 
 }  // namespace
 
+// The capture stream has the highest priority, the side stream the default
+// (lowest): captured kernel nodes keep their stream's priority, so when the
+// leaf z sweep and the upward pass become ready together the z sweep's CTAs
+// are placed first and the upward pass takes the SMs it leaves.
+static cudaError_t make_cap_stream(cudaStream_t* st) {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, greatest);
+}
+
 static void drop_graphs(htlr_plan* pl) {
   for (auto& g : pl->graph_cache) cudaGraphExecDestroy(g.exec);
   pl->graph_cache.clear();
@@ -2713,9 +2758,10 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
         return 0;
       }
     }
-    if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+    if (!pl->cap_stream) CUDA_TRY(make_cap_stream(&pl->cap_stream));
     MvCtx cc = cx;
     cc.st = pl->cap_stream;
+    cc.whole = true;
     prof_reset(pl);
     CUDA_TRY(cudaStreamBeginCapture(cc.st, cudaStreamCaptureModeThreadLocal));
     int rc = mv_local(cc, u);
@@ -2767,6 +2813,7 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
     if (rc > 0) return rc;
   }
   prof_reset(pl);
+  cx.whole = true;
   if (int rc = mv_local(cx, u)) return rc;
   if (int rc = mv_remote(cx, u, f)) return rc;
   pl->last_launches = cx.launches;
@@ -2983,7 +3030,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
       return 0;
     }
   }
-  if (!pl->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  if (!pl->cap_stream) CUDA_TRY(make_cap_stream(&pl->cap_stream));
   if (!pl->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->copy_stream, cudaStreamNonBlocking));
   while (pl->ov_ev.size() < 10) {
     cudaEvent_t e;

@@ -1,6 +1,7 @@
+# A/B: leaf z sweep from u with the upward pass on the side stream; SMs left to the side stream
 export PYTHONPATH=$PWD
-for w in cfg4 cfg2; do
-HTLR_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-  --master-port 29511 bench.py --workload $w --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b_w2_$w.json 2> gpurun_out/b_w2_$w.err
-tail -c 250 gpurun_out/b_w2_$w.json
+for cfg in "0 20" "1 48" "1 64" "1 0" "0 20" "1 48" "1 40" "1 56"; do
+set -- $cfg
+echo "== HTLR_Z_FROM_U=$1 HTLR_LEVEL_SMS=$2" >> gpurun_out/ab.log
+HTLR_Z_FROM_U=$1 HTLR_LEVEL_SMS=$2 timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['e2e']['ms_per_step'])" >> gpurun_out/ab.log
 done
