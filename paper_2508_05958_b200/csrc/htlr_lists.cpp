@@ -126,8 +126,18 @@ struct Builder {
   // split > 0: stop the recursion at that level and record the pending
   // subtree (kind -1) instead, in DFS position
   int split = -1;
+  int truncate = -1;              // >= 0: inadmissible pairs of that level are dropped, not refined
+  size_t n_adm = 0, n_near = 0;   // pushed leaves by kind
+  // Uniform grid with n a power of two: h = 2^-k, so every box bound, gap,
+  // square and sum in the predicate is exact in double and the predicate is a
+  // function of (level, |offset| per axis) alone -- evaluated once per such
+  // key by build_tree (with the reference's arithmetic, on the pair (0, o))
+  // and looked up here.  -1: no such pair on the level.
+  static constexpr int kMemo = kOffsetMemo;
+  const int8_t* memo = nullptr;
 
-  Builder(const TreeSpec& s, const Tree& t, std::vector<LeafRec>* o) : spec(s), tree(t), out(o) {
+  Builder(const TreeSpec& s, const Tree& t, std::vector<LeafRec>* o, const int8_t* m = nullptr)
+      : spec(s), tree(t), out(o), memo(m) {
     // np.ndindex(*([2] * d)): last dimension varies fastest
     ncombo = 1 << spec.d;
     for (int i = 0; i < ncombo; ++i) {
@@ -138,7 +148,19 @@ struct Builder {
     }
   }
 
-  void visit(const int* tc, const int* sc, int level) {
+  bool admissible(const int* tc, const int* sc, int level) {
+    if (memo) {
+      int o[3] = {0, 0, 0};
+      bool fits = true;
+      for (int a = 0; a < spec.d; ++a) {
+        o[a] = tc[a] > sc[a] ? tc[a] - sc[a] : sc[a] - tc[a];
+        fits = fits && o[a] < kMemo;
+      }
+      if (fits) {
+        const int8_t v = memo[(((size_t)level * kMemo + o[0]) * kMemo + o[1]) * kMemo + o[2]];
+        if (v >= 0) return v != 0;
+      }
+    }
     const int side = tree.side(level);
     int tlo[3], thi[3], slo[3], shi[3];
     for (int a = 0; a < spec.d; ++a) {
@@ -147,7 +169,11 @@ struct Builder {
       slo[a] = sc[a] * side;
       shi[a] = slo[a] + side;
     }
-    if (admissible_boxes(spec, tlo, thi, slo, shi)) {
+    return admissible_boxes(spec, tlo, thi, slo, shi);
+  }
+
+  void visit(const int* tc, const int* sc, int level) {
+    if (admissible(tc, sc, level)) {
       push(0, level, tc, sc);
       return;
     }
@@ -155,6 +181,7 @@ struct Builder {
       push(1, level, tc, sc);
       return;
     }
+    if (level == truncate) return;
     if (level == split) {
       push(-1, level, tc, sc);
       return;
@@ -182,6 +209,10 @@ struct Builder {
   }
 
   void push(int kind, int level, const int* tc, const int* sc) {
+    if (kind == 0)
+      ++n_adm;
+    else if (kind == 1)
+      ++n_near;
     if (!out && !dst) {
       ++count;
       return;
@@ -222,7 +253,32 @@ void mapped_tables(int n, double amplitude, std::vector<double>& bounds, std::ve
   }
 }
 
-int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
+std::vector<int8_t> offset_memo(const TreeSpec& spec, int depth) {
+  std::vector<int8_t> memo;
+  if (!spec.bounds.empty() || spec.n < 1 || (spec.n & (spec.n - 1)) != 0) return memo;
+  constexpr int K = kOffsetMemo;
+  memo.assign((size_t)(depth + 1) * K * K * K, -1);
+  for (int l = 0; l <= depth; ++l) {
+    const int m = 1 << l, sd = spec.n >> l;
+    const int kz = spec.d == 3 ? K : 1;
+    for (int ox = 0; ox < K && ox < m; ++ox)
+      for (int oy = 0; oy < K && oy < m; ++oy)
+        for (int oz = 0; oz < kz && oz < m; ++oz) {
+          const int o[3] = {ox, oy, oz};
+          int tlo[3], thi[3], slo[3], shi[3];
+          for (int a = 0; a < spec.d; ++a) {
+            tlo[a] = 0;
+            thi[a] = sd;
+            slo[a] = o[a] * sd;
+            shi[a] = slo[a] + sd;
+          }
+          memo[(((size_t)l * K + ox) * K + oy) * K + oz] = admissible_boxes(spec, tlo, thi, slo, shi) ? 1 : 0;
+        }
+  }
+  return memo;
+}
+
+int build_tree(const TreeSpec& spec, Tree& out, std::string& err, int max_level) {
   if (spec.d != 2 && spec.d != 3) {
     err = "only d = 2 and d = 3 are supported";
     return -1;
@@ -246,9 +302,15 @@ int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
   // DFS down to a split level sequentially (the recursion's order), then the
   // pending subtrees in parallel, concatenated in DFS position: the same
   // leaf list as one sequential recursion
+  const std::vector<int8_t> memo = offset_memo(spec, depth);
+  const int8_t* mp = memo.empty() ? nullptr : memo.data();
   std::vector<LeafRec> top;
-  Builder b(spec, out, &top);
+  Builder b(spec, out, &top, mp);
   b.split = depth >= 3 ? 2 : (depth >= 2 ? 1 : -1);
+  if (max_level >= 0 && max_level < depth) {
+    b.truncate = max_level;
+    out.truncated = true;
+  }
   int root[3] = {0, 0, 0};
   b.visit(root, root, 0);
   std::vector<size_t> pend;
@@ -270,10 +332,14 @@ int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
     work();
     for (auto& th : pool) th.join();
   };
+  std::vector<size_t> cadm(pend.size(), 0), cnear(pend.size(), 0);
   parallel([&](size_t k) {
-    Builder w(spec, out, nullptr);
+    Builder w(spec, out, nullptr, mp);
+    w.truncate = b.truncate;
     w.expand(top[pend[k]]);
     cnt[k] = w.count;
+    cadm[k] = w.n_adm;
+    cnear[k] = w.n_near;
   });
   std::vector<size_t> pos(top.size() + 1, 0);
   {
@@ -288,15 +354,20 @@ int build_tree(const TreeSpec& spec, Tree& out, std::string& err) {
   for (size_t i = 0; i < top.size(); ++i)
     if (top[i].kind >= 0) out.leaves[pos[i]] = top[i];
   parallel([&](size_t k) {
-    Builder w(spec, out, nullptr);
+    Builder w(spec, out, nullptr, mp);
+    w.truncate = b.truncate;
     w.dst = out.leaves.data() + pos[pend[k]];
     w.expand(top[pend[k]]);
   });
-  for (const auto& r : out.leaves) {
+  for (const auto& r : top) {
     if (r.kind == 0)
       ++out.num_adm;
-    else
+    else if (r.kind == 1)
       ++out.num_near;
+  }
+  for (size_t k = 0; k < pend.size(); ++k) {
+    out.num_adm += (int64_t)cadm[k];
+    out.num_near += (int64_t)cnear[k];
   }
   return 0;
 }

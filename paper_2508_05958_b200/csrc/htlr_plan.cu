@@ -106,6 +106,8 @@ struct Pass {
   double sep_own_frac = 1.0;     // their share of the pass's (pair, box) work
   int zpitch = 0;                // z-plane pitch of the pass's stored source vectors (0: natural)
   int64_t sep_groups = 0;
+  bool analytic = false;         // no pair list: the level's lists are the product sets of the banded sweeps
+                                 // (verified per offset on uniform dyadic grids, htlr_build_lists)
   bool band = false;             // pass as banded line sweeps (sep_band_kernel)
   DevBuf band_ws;                // its term buffers [term][box][rhs][512]
   DevBuf band_ws2;               // y-swept terms of the line-kernel y-x sweep (z-slab shards)
@@ -224,6 +226,7 @@ struct htlr_plan {
   int leaf_pass = -1;
   int near_mats = 0;          // leaf pass: matrices [0, near_mats) are near blocks
   bool merged = false;        // leaf-level admissible cores live in the leaf pass
+  int analytic_from = 0;      // > 0: levels >= this have no pair lists (Pass::analytic); the DFS stops above them
   bool sep = false;           // separable-core formulation (tensor-product kernel, htlr_sep.cu)
   bool cube_ok = false;       // separable plan whose upward / downward passes run over cubes (htlr_cube.cu)
   DevBuf sep_corr;            // self-block diagonal correction of the separable near field
@@ -520,6 +523,108 @@ int htlr_plan_destroy(htlr_plan* pl) {
   return 0;
 }
 
+static bool sep_wanted(const htlr_plan* pl);
+
+// In-domain offsets of the banded terms per box position q along a line of nb
+// boxes: A = C4's, B = {-2, 2}, M = {-1, 0, 1}, P = {3 - 6c} (htlr_band.cu)
+struct BandLine {
+  int A, B, M, P;
+};
+static BandLine band_line(int q, int nb) {
+  const int c = q & 1;
+  auto in = [&](int o) { return q + o >= 0 && q + o < nb; };
+  BandLine v{0, in(-2) + in(2), in(-1) + in(0) + in(1), in(3 - 6 * c)};
+  for (int o : {-4 - c, -3 - c, 4 - c, 5 - c}) v.A += in(o);
+  return v;
+}
+
+// Analytic banded levels.  On a uniform grid with n a power of two the
+// predicate is exactly a function of (level, |offset|) (htlr_lists.h
+// offset_memo).  If on every level the inadmissible offsets are exactly
+// {|o_a| <= 2} minus the corners {|o_a| = 2 for all a} (strong admissibility
+// at eta = 1), then by induction over the levels the pairs the DFS reaches on
+// level l are the in-domain children of such parent pairs, i.e. per axis the
+// offsets R10 = {-4-c..5-c} minus the corner parents' children A4^3 -- the
+// product sets the banded sweeps apply (band_check verifies the same
+// statement pair by pair on a built list).  Plans that would run those levels
+// as banded sweeps then need no pair lists below level 2: the DFS stops
+// there, the leaf counts come from the product sets, and the full DFS list
+// is built only when an export asks for it (ensure_leaves).
+static bool analytic_bands_ok(const htlr_plan* pl, const htlr::TreeSpec& ts, int depth, int leaf_side) {
+  const char* e = std::getenv("HTLR_SEP_BAND");
+  if (e && e[0] == '0') return false;
+  const char* e2 = std::getenv("HTLR_ANALYTIC");
+  if (e2 && e2[0] == '0') return false;
+  if (pl->mapped || pl->lowrank || pl->shard_world != 1 || pl->d != 3 || ts.rule != 1) return false;
+  if (pl->kp.kind != HTLR_KERNEL_GAUSSIAN || pl->p != htlr::kSepP || leaf_side != htlr::kSepP) return false;
+  const char* e3 = std::getenv("HTLR_SEPARABLE");
+  if (e3 && e3[0] == '0') return false;
+  if (depth < 3 || depth > 4) return false;   // band_check: banded passes on levels 3 and 4
+  const std::vector<int8_t> memo = htlr::offset_memo(ts, depth);
+  if (memo.empty()) return false;
+  constexpr int K = htlr::kOffsetMemo;
+  for (int l = 0; l <= depth; ++l) {
+    const int m = 1 << l;
+    for (int ox = 0; ox < K && ox < m; ++ox)
+      for (int oy = 0; oy < K && oy < m; ++oy)
+        for (int oz = 0; oz < K && oz < m; ++oz) {
+          const bool nearshape = ox <= 2 && oy <= 2 && oz <= 2 && !(ox == 2 && oy == 2 && oz == 2);
+          if ((memo[(((size_t)l * K + ox) * K + oy) * K + oz] == 0) != nearshape) return false;
+        }
+  }
+  return true;
+}
+
+// leaf counts of an analytic level: admissible pairs (R10^3 - A4^3 - R5^3 +
+// C2^3 in the domain) and, at the leaf level, near pairs (R5^3 - C2^3)
+static void analytic_counts(int level, int64_t& adm, int64_t& near) {
+  const int nb = 1 << level;
+  int64_t s10 = 0, s4 = 0, s5 = 0, s2 = 0;
+  for (int q = 0; q < nb; ++q) {
+    const BandLine v = band_line(q, nb);
+    s10 += v.A + v.B + v.M + v.P;
+    s4 += v.A;
+    s5 += v.B + v.M;
+    s2 += v.B;
+  }
+  near = s5 * s5 * s5 - s2 * s2 * s2;
+  adm = s10 * s10 * s10 - s4 * s4 * s4 - near;
+}
+
+// mode products the three sweeps of a banded pass run (per rhs) over the
+// nt target boxes of a box region: the y sweep applies each term's band (28
+// offsets away from the boundary at the leaf level); the z and x sweeps share
+// band pieces between the terms (htlr_band.cu bcount / boff): z 15 (B, M, P,
+// C4 and EB, EM once each), x 19 (C4 + P, M, B, C4 and EM, EB)
+static double band_flops_of(int level, bool leaf, int64_t nt) {
+  const int nb = 1 << level;
+  double per_line = 0;
+  for (int q = 0; q < nb; ++q) {
+    const BandLine v = band_line(q, nb);
+    const int nk = leaf ? 2 : 1;   // factor kinds with a {-2..2} and a {-2, 2} term
+    const int ysw = (v.A + v.B + v.M + v.P) + v.A + nk * ((v.B + v.M) + v.B);
+    const int zsw = v.A + v.P + nk * (v.B + v.M);
+    const int xsw = (v.A + v.P) + v.A + nk * (v.M + v.B);
+    per_line += ysw + zsw + xsw;
+  }
+  // the region's share of the sweeps (halo lines of the z sweep not counted)
+  return (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * level));
+}
+
+// the full DFS leaf list of a plan whose tree stopped above its analytic levels
+static int ensure_leaves(const htlr_plan* cpl) {
+  htlr_plan* pl = const_cast<htlr_plan*>(cpl);
+  if (!pl->tree.truncated) return 0;
+  htlr::Tree full;
+  std::string err;
+  if (htlr::build_tree(pl->tree.spec, full, err)) return fail(-1, err);
+  if (full.num_adm != pl->tree.num_adm || full.num_near != pl->tree.num_near)
+    return fail(2, "analytic banded levels: leaf counts differ from the DFS list");
+  pl->tree.leaves.swap(full.leaves);
+  pl->tree.truncated = false;
+  return 0;
+}
+
 int htlr_build_lists(htlr_plan* pl) {
   if (!pl) return fail(-1, "null plan");
   htlr::TreeSpec ts;
@@ -531,7 +636,16 @@ int htlr_build_lists(htlr_plan* pl) {
   if (pl->mapped) ts.bounds = pl->mb;
   std::string err;
   PhaseTimer tm;
-  if (htlr::build_tree(ts, pl->tree, err)) return fail(-1, err);
+  pl->analytic_from = 0;
+  {
+    int side = 0, depth = 0;
+    if (pl->n >= 1 && htlr::compute_leaf_side(ts.n, ts.leaf_side_max, &side, err) == 0) {
+      for (int sd = ts.n; sd > side; sd /= 2) ++depth;
+      if (analytic_bands_ok(pl, ts, depth, side)) pl->analytic_from = 3;
+    }
+    err.clear();
+  }
+  if (htlr::build_tree(ts, pl->tree, err, pl->analytic_from ? pl->analytic_from - 1 : -1)) return fail(-1, err);
   tm.mark("lists: tree (DFS)");
   const Tree& tr = pl->tree;
   pl->L = tr.depth;
@@ -724,6 +838,16 @@ int htlr_build_lists(htlr_plan* pl) {
     });
   }
   tm.mark("lists: offset tables");
+  for (int l = pl->analytic_from; pl->analytic_from && l <= pl->L; ++l) {
+    int64_t adm = 0, near = 0;
+    analytic_counts(l, adm, near);
+    pl->levels[l].num_adm = adm;
+    pl->tree.num_adm += adm;
+    if (l == pl->L) {
+      pl->num_near = near;
+      pl->tree.num_near += near;
+    }
+  }
   // validation the reference performs at build time (tensor.py:112-113 via
   // blocks.py:160): admissible blocks need box side >= rank
   for (const auto& lv : pl->levels) {
@@ -807,6 +931,10 @@ int htlr_build_lists(htlr_plan* pl) {
     ps.from_ub = false;
     ps.to_y = false;
     if (fill_pass(ps, {&lv.adm})) return 1;
+    if (pl->analytic_from && l >= pl->analytic_from) {
+      ps.analytic = true;
+      ps.npairs = (int)lv.num_adm;
+    }
   }
   pl->passes.emplace_back();
   pl->leaf_pass = (int)pl->passes.size() - 1;
@@ -820,6 +948,10 @@ int htlr_build_lists(htlr_plan* pl) {
     if (pl->merged) tabs.push_back(&pl->levels[pl->L].adm);
     pl->near_mats = (int)pl->near.members.size();
     if (fill_pass(ps, tabs)) return 1;
+    if (pl->analytic_from) {
+      ps.analytic = true;
+      ps.npairs = (int)(pl->num_near + (pl->merged ? pl->levels[pl->L].num_adm : 0));
+    }
   }
   tm.mark("lists: passes (sorted pairs)");
   pl->lists_built = true;
@@ -968,7 +1100,7 @@ int htlr_tree_info(const htlr_plan* pl, int32_t* depth, int32_t* leaf_side, int6
   if (!pl->lists_built) return fail(-1, "lists not built");
   if (depth) *depth = pl->tree.depth;
   if (leaf_side) *leaf_side = pl->tree.leaf_side;
-  if (num_leaves) *num_leaves = (int64_t)pl->tree.leaves.size();
+  if (num_leaves) *num_leaves = pl->tree.truncated ? pl->tree.num_adm + pl->tree.num_near : (int64_t)pl->tree.leaves.size();
   if (num_adm) *num_adm = pl->tree.num_adm;
   if (num_near) *num_near = pl->tree.num_near;
   return 0;
@@ -977,6 +1109,7 @@ int htlr_tree_info(const htlr_plan* pl, int32_t* depth, int32_t* leaf_side, int6
 int htlr_export_lists(const htlr_plan* pl, int32_t* rows, int64_t cap) {
   if (!pl || !rows) return fail(-1, "null argument");
   if (!pl->lists_built) return fail(-1, "lists not built");
+  if (int rc = ensure_leaves(pl)) return rc;
   const int d = pl->d, w = 3 + 4 * d;
   const auto& lv = pl->tree.leaves;
   if (cap < (int64_t)lv.size() * w) return fail(-1, "export buffer too small");
@@ -1463,30 +1596,47 @@ static bool band_check(const htlr_plan* pl, Pass& ps, int OR, const std::vector<
     if (!same) ok.store(false);
   });
   if (!ok.load()) return false;
-  // mode products the three sweeps run (per rhs), per box position q along a
-  // line: the y sweep applies each term's band (28 offsets away from the
-  // boundary at the leaf level); the z and x sweeps share band pieces between
-  // the terms (htlr_band.cu bcount / boff): z 15 (B, M, P, C4 and EB, EM once
-  // each), x 19 (C4 + P, M, B, C4 and EM, EB)
-  double per_line = 0;
-  for (int q = 0; q < nb; ++q) {
-    const int c = q & 1;
-    auto in = [&](int o) { return q + o >= 0 && q + o < nb; };
-    int A = 0, B = in(-2) + in(2), M = in(-1) + in(0) + in(1), P = in(3 - 6 * c);
-    for (int o : {-4 - c, -3 - c, 4 - c, 5 - c}) A += in(o);
-    const int nk = ps.to_y ? 2 : 1;   // factor kinds with a {-2..2} and a {-2, 2} term
-    const int ysw = (A + B + M + P) + A + nk * ((B + M) + B);
-    const int zsw = A + P + nk * (B + M);
-    const int xsw = (A + P) + A + nk * (M + B);
-    per_line += ysw + zsw + xsw;
-  }
-  // per rhs, the region's share of the sweeps (halo lines of the z sweep not counted)
-  flops = (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * L));
+  flops = band_flops_of(L, ps.to_y, nt);
   for (int a = 0; a < 3; ++a) {
     ps.band_lo[a] = lo[a];
     ps.band_hi[a] = hi[a];
   }
   return true;
+}
+
+// factor tables of a separable pass: kind 0 (admissible, level factor folded)
+// and kind 1 (near), per-axis offsets -OR..OR
+static int sep_factor_tables(htlr_plan* pl, Pass& ps, int OR, cudaStream_t st) {
+  const bool leaf = ps.to_y;
+  const Level& lv = pl->levels[ps.level];
+  const int NO = 2 * OR + 1;
+  const int nslots = 2 * NO;
+  if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;
+  CUDA_TRY(cudaMemsetAsync(ps.sep_tab.ptr, 0, (size_t)nslots * htlr::kSepSlot * sizeof(double), st));
+  std::vector<htlr::SepJob> jobs;
+  for (int kind = 0; kind < 2; ++kind) {
+    if (kind == 0 && !lv.R.ptr) continue;
+    if (kind == 1 && !leaf) continue;
+    for (int o = -OR; o <= OR; ++o) {
+      htlr::SepJob j;
+      j.kind = kind;
+      j.o = o;
+      j.t0 = std::max(0, -o);
+      j.side = kind == 0 ? lv.side : pl->sL;
+      j.R = kind == 0 ? lv.R.d() : nullptr;
+      j.dst = ps.sep_tab.d() + (int64_t)(kind * NO + o + OR) * htlr::kSepSlot;
+      jobs.push_back(j);
+    }
+  }
+  DevBuf jb;
+  if (jb.alloc(std::max<size_t>(1, jobs.size()) * sizeof(htlr::SepJob))) return 1;
+  CUDA_TRY(cudaMemcpyAsync(jb.ptr, jobs.data(), jobs.size() * sizeof(htlr::SepJob), cudaMemcpyHostToDevice, st));
+  htlr::launch_sep_tables((const htlr::SepJob*)jb.ptr, (int)jobs.size(), pl->p, pl->sL, pl->h, pl->kp, pl->diag.d(),
+                          pl->hd, leaf ? pl->sep_corr.d() : nullptr, st);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  pl->device_scalars += (int64_t)nslots * htlr::kSepSlot;
+  return 0;
 }
 
 // Per-target pair runs of one pass: (source, code) sorted by code, where code
@@ -1507,6 +1657,7 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
       OR = std::max(OR, std::abs(mo[m][1 + a]));
     }
   }
+  if (ps.analytic) OR = std::min(5, (1 << ps.level) - 1);   // the banded terms' offsets inside the level
   const int NO = 2 * OR + 1;
   if (NO > htlr::kSepMaxNO) {
     fits = false;
@@ -1514,6 +1665,22 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
   }
   fits = true;
   PhaseTimer tm;
+  if (ps.analytic) {
+    // the level's lists are the banded sweeps' product sets (analytic_bands_ok):
+    // the whole level as one box region, no pair runs
+    const int nb = 1 << ps.level;
+    ps.sep_NO = NO;
+    ps.sep_groups = 0;
+    ps.sep_nblocks = 0;
+    ps.sep_nitems = 0;
+    ps.band = true;
+    ps.band_flops = band_flops_of(ps.level, leaf, lv.nclusters);
+    for (int a = 0; a < 3; ++a) {
+      ps.band_lo[a] = 0;
+      ps.band_hi[a] = nb;
+    }
+    return sep_factor_tables(pl, ps, OR, st);
+  }
   // counting sort by target, then each target's run by (code, source)
   const int64_t t0 = pl->own_lo[ps.level], nt = pl->own_hi[ps.level] - t0;
   std::vector<int64_t> ptr((size_t)nt + 1, 0);
@@ -1605,34 +1772,7 @@ static int build_sep_pass(htlr_plan* pl, Pass& ps, bool& fits, cudaStream_t st) 
     ps.sep_nitems = (int)items.size();
     if (upload_sep(ps, ent, items)) return 1;
   }
-  // factor tables: kind 0 (admissible, level factor folded) and kind 1 (near)
-  const int nslots = 2 * NO;
-  if (ps.sep_tab.alloc((size_t)nslots * htlr::kSepSlot * sizeof(double))) return 1;
-  CUDA_TRY(cudaMemsetAsync(ps.sep_tab.ptr, 0, (size_t)nslots * htlr::kSepSlot * sizeof(double), st));
-  std::vector<htlr::SepJob> jobs;
-  for (int kind = 0; kind < 2; ++kind) {
-    if (kind == 0 && !lv.R.ptr) continue;
-    if (kind == 1 && !leaf) continue;
-    for (int o = -OR; o <= OR; ++o) {
-      htlr::SepJob j;
-      j.kind = kind;
-      j.o = o;
-      j.t0 = std::max(0, -o);
-      j.side = kind == 0 ? lv.side : pl->sL;
-      j.R = kind == 0 ? lv.R.d() : nullptr;
-      j.dst = ps.sep_tab.d() + (int64_t)(kind * NO + o + OR) * htlr::kSepSlot;
-      jobs.push_back(j);
-    }
-  }
-  DevBuf jb;
-  if (jb.alloc(std::max<size_t>(1, jobs.size()) * sizeof(htlr::SepJob))) return 1;
-  CUDA_TRY(cudaMemcpyAsync(jb.ptr, jobs.data(), jobs.size() * sizeof(htlr::SepJob), cudaMemcpyHostToDevice, st));
-  htlr::launch_sep_tables((const htlr::SepJob*)jb.ptr, (int)jobs.size(), pl->p, pl->sL, pl->h, pl->kp, pl->diag.d(),
-                          pl->hd, leaf ? pl->sep_corr.d() : nullptr, st);
-  CUDA_TRY(cudaStreamSynchronize(st));
-  CUDA_TRY(cudaGetLastError());
-  pl->device_scalars += (int64_t)nslots * htlr::kSepSlot;
-  return 0;
+  return sep_factor_tables(pl, ps, OR, st);
 }
 
 // Mapped grid construction: geometry tables, per (level, interval) nodes and
@@ -3551,6 +3691,7 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
                       int64_t factor_cap, int32_t* shapes) {
   if (!pl || !core_or_dense || !shapes) return fail(-1, "null argument");
   if (!pl->constructed) return fail(-1, "plan not constructed");
+  if (int rc = ensure_leaves(pl)) return rc;
   if (leaf_id < 0 || leaf_id >= (int64_t)pl->tree.leaves.size()) return fail(-1, "leaf id out of range");
   CUDA_TRY(cudaSetDevice(pl->device));
   CUDA_TRY(cudaDeviceSynchronize());
@@ -3558,11 +3699,13 @@ int htlr_export_block(htlr_plan* pl, int64_t leaf_id, double* core_or_dense, int
   if (pl->mapped) return export_block_mapped(pl, lf, core_or_dense, cap, factors, factor_cap, shapes);
   const int d = pl->d, p = pl->p;
   const Level& lv = pl->levels[lf.level];
+  // separable plans regenerate the block from the 1-D factors (no table id;
+  // analytic levels have no offset tables)
+  if (pl->sep) return export_block_sep(pl, lf, core_or_dense, cap, factors, factor_cap, shapes);
   const OffsetTable& tab = lf.kind == 0 ? lv.adm : pl->near;
   const int64_t key = pack_offset(lf.tc, lf.sc, d, lv.m);
   const int id = tab.dense.empty() ? tab.id.at(key) : tab.dense[key] - 1;
   if (id < 0) return fail(2, "leaf offset missing from the plan's tables");
-  if (pl->sep) return export_block_sep(pl, lf, core_or_dense, cap, factors, factor_cap, shapes);
   const Pass* ps = nullptr;
   int mat = id;
   if (lf.kind == 0) {

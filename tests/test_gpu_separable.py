@@ -358,3 +358,21 @@ def test_banded_only_for_eta_one():
         assert op.leaf_pass() != "banded"
     op = make(64)
     assert op.leaf_pass() == "banded"
+
+
+@pytest.mark.parametrize("n,R,a", [(64, 2, 0.25), (128, 1, 0.0)])
+def test_analytic_banded_plan_equals_listed_plan(tmp_path, n, R, a):
+    """A plan whose banded levels were proven per offset (no pair lists below
+    level 2, htlr_plan.cu analytic_bands_ok) against the plan that builds the
+    lists and checks them pair by pair (HTLR_ANALYTIC=0): the same kernels on
+    the same tables, so the same bits; and an exported block of the analytic
+    plan (the lazily built DFS list) equals the oracle's."""
+    outs = {}
+    for mode in ("1", "0"):
+        out = tmp_path / f"f{mode}.npy"
+        r = subprocess.run([sys.executable, "-c", _BAND_SCRIPT, str(out), str(n), str(R), str(a)], check=True,
+                           cwd=ROOT, capture_output=True, text=True,
+                           env={**os.environ, "PYTHONPATH": ROOT, "HTLR_ANALYTIC": mode}, timeout=900)
+        assert r.stdout.strip().splitlines()[-1] == "banded"
+        outs[mode] = np.load(out)
+    assert np.array_equal(outs["1"], outs["0"])

@@ -161,3 +161,69 @@ def test_storage_accounting_matches_reference_cfg1():
         L.htlr_plan_destroy(plan)
     gold = np.load(os.path.join(GOLD, "cfg1_matvec.npz"))["storage"]
     assert list(out[:4]) == list(gold)
+
+
+def _gaussian_host_plan(n, eta=1.0):
+    """Host-only plan of a separable-eligible problem (Gaussian, p = leaf side
+    = 8, 3-D): the kind whose levels 3 and 4 can be built analytically."""
+    import ctypes
+    from paper_2508_05958_b200.operators import _desc
+    cfg = H.BuildConfig(rank=8, leaf_side=8, rule=H.AdmissibilityRule.strong(eta), kernel=H.gaussian(0.1),
+                        coeff=H.CoefficientFn.constant(0.0))
+    plan = ctypes.c_void_p()
+    _lib.check(_lib.lib().htlr_plan_create(ctypes.byref(_desc(cfg, H.UniformGrid(3, n))), -1, ctypes.byref(plan)))
+    return plan
+
+
+def _tree_info(plan):
+    import ctypes
+    depth, side = ctypes.c_int32(), ctypes.c_int32()
+    nl, na, nn = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().htlr_tree_info(plan, ctypes.byref(depth), ctypes.byref(side), ctypes.byref(nl),
+                                         ctypes.byref(na), ctypes.byref(nn)))
+    return depth.value, side.value, nl.value, na.value, nn.value
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_analytic_banded_levels_equal_the_dfs_lists(n, monkeypatch):
+    """Uniform grid, n a power of two, eta = 1: the plan proves the banded
+    product-set structure per (level, offset) and builds no pair lists below
+    level 2 (htlr_plan.cu analytic_bands_ok).  Its leaf counts (from the
+    product sets) and its lazily built DFS list must equal the plan that
+    walks the whole DFS (HTLR_ANALYTIC=0) and the reference fixture."""
+    from paper_2508_05958_b200.grids import export_leaf_array
+    L = _lib.lib()
+    info, arrs = {}, {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("HTLR_ANALYTIC", mode)
+        plan = _gaussian_host_plan(n)
+        try:
+            _lib.check(L.htlr_build_lists(plan))
+            info[mode] = _tree_info(plan)          # before any export: the analytic counts
+            arrs[mode] = export_leaf_array(plan, 3)
+            assert _tree_info(plan) == info[mode]  # after the lazy DFS
+        finally:
+            L.htlr_plan_destroy(plan)
+    assert info["1"] == info["0"]
+    assert np.array_equal(arrs["1"], arrs["0"])
+    g = gold_lists()
+    key = [k for k in all_list_keys() if tuple(int(v) for v in g["meta_" + k][:3]) == (3, n, 8)
+           and float(g["meta_" + k][3]) == 1.0]
+    assert key, "no reference fixture for this tree"
+    assert hashlib.sha256(np.ascontiguousarray(arrs["1"], dtype=np.int32).tobytes()).digest() == bytes(g["sha_" + key[0]])
+
+
+def test_analytic_banded_levels_need_eta_one():
+    """eta = 2 has other near sets: the per-offset check fails, the plan walks
+    the DFS (and still reproduces the reference's list)."""
+    from paper_2508_05958_b200.grids import export_leaf_array
+    L = _lib.lib()
+    plan = _gaussian_host_plan(64, eta=2.0)
+    try:
+        _lib.check(L.htlr_build_lists(plan))
+        arr = export_leaf_array(plan, 3)
+    finally:
+        L.htlr_plan_destroy(plan)
+    grid = H.UniformGrid(3, 64)
+    ref = H.build_block_cluster_tree(H.build_cluster_tree(grid, 8), H.AdmissibilityRule.strong(2.0)).leaf_array
+    assert np.array_equal(arr, ref)
