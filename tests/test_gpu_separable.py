@@ -365,8 +365,7 @@ def test_analytic_banded_plan_equals_listed_plan(tmp_path, n, R, a):
     """A plan whose banded levels were proven per offset (no pair lists below
     level 2, htlr_plan.cu analytic_bands_ok) against the plan that builds the
     lists and checks them pair by pair (HTLR_ANALYTIC=0): the same kernels on
-    the same tables, so the same bits; and an exported block of the analytic
-    plan (the lazily built DFS list) equals the oracle's."""
+    the same tables, equal up to the order of the upward pass's fp64 REDs."""
     outs = {}
     for mode in ("1", "0"):
         out = tmp_path / f"f{mode}.npy"
@@ -375,4 +374,6 @@ def test_analytic_banded_plan_equals_listed_plan(tmp_path, n, R, a):
                            env={**os.environ, "PYTHONPATH": ROOT, "HTLR_ANALYTIC": mode}, timeout=900)
         assert r.stdout.strip().splitlines()[-1] == "banded"
         outs[mode] = np.load(out)
-    assert np.array_equal(outs["1"], outs["0"])
+    err = rel(outs["1"], outs["0"])
+    print(f"n={n} R={R} analytic vs listed plan", err)
+    assert err <= 1e-14
