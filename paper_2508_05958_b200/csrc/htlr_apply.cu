@@ -420,163 +420,10 @@ void launch_upward(const double* u, double* W, int d, int n, int side, int p, in
 }
 
 // ---------------------------------------------------------------------------
-// gathered fp64 tensor-core GEMM
-//
-// task = (mat, pairs [b, b+cnt), r0): for its pairs (tgt, src) and rhs r the
-// CTA computes C[tgt][r][rows] += A_mat[rows][:] . B[src][r][:], rows = its
-// MT-row tile.  Columns n = j*Rc + (r - r0).  Warp tile 32x32 = 2 x 4
-// m16n8k8 fragments; A comes pre-tiled (one contiguous chunk per stage),
-// B columns are gathered with cp.async (zero-filled when a column is empty).
-// Tasks of one offset are consecutive so the 148 SMs share G[o] in L2.
-// The epilogue adds with fp64 RED into L2-resident accumulators; rows of one
-// target get contributions from many offsets.
+// gathered fp64 tensor-core GEMM: the kernels are in htlr_gemm.cu
+// (gemm_persistent_kernel, gemm_thin_kernel); here the tile choice and the
+// dispatch.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ void mma_m16n8k8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
-}
-
-template <int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(WM* WN * 32, 2)
-    gemm_gather_kernel(const double* __restrict__ A, int64_t mat_stride, const double* __restrict__ B,
-                       double* __restrict__ C, const GemmTask* __restrict__ tasks,
-                       const int2* __restrict__ pairs, int R, int Rc, int K_pad, int M_valid, int ldc,
-                       int RT) {
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC, BST = KC + 4;
-  constexpr int NTH = WM * WN * 32;
-  extern __shared__ __align__(16) double smem[];
-  double* sA = smem;
-  double* sB = smem + STAGES * MT * KC;
-  __shared__ int64_t colB[NT];
-  __shared__ int64_t colC[NT];
-
-  const int task = blockIdx.x / RT, rt = blockIdx.x % RT;
-  const GemmTask tk = tasks[task];
-  for (int n = threadIdx.x; n < NT; n += NTH) {
-    int j = n / Rc, r = tk.r0 + n % Rc;
-    if (j < tk.pair_count && r < R) {
-      int2 pr = pairs[tk.pair_begin + j];
-      colB[n] = ((int64_t)pr.y * R + r) * K_pad;
-      colC[n] = ((int64_t)pr.x * R + r) * ldc;
-    } else {
-      colB[n] = -1;
-      colC[n] = -1;
-    }
-  }
-  __syncthreads();
-
-  const double* Ablk = A + (int64_t)tk.mat * mat_stride + (int64_t)rt * MT * K_pad + (int64_t)tk.kc0 * MT * KC;
-  const int nk = tk.nkc;
-  const int tid = threadIdx.x;
-
-  auto load_stage = [&](int kc, int st) {
-    const double* src = Ablk + (int64_t)kc * (MT * KC);
-    double* dA = sA + st * MT * KC;
-#pragma unroll
-    for (int i = tid; i < MT * KC / 2; i += NTH) cp_async16(dA + 2 * i, src + 2 * i, 16);
-    double* dB = sB + st * NT * BST;
-#pragma unroll
-    for (int i = tid; i < NT * KC / 2; i += NTH) {
-      int n = i / (KC / 2), c2 = i % (KC / 2);
-      int64_t cb = colB[n];
-      const double* g = cb >= 0 ? B + cb + (tk.kc0 + kc) * KC + 2 * c2 : B;
-      cp_async16(dB + n * BST + 2 * c2, g, cb >= 0 ? 16 : 0);
-    }
-  };
-
-  const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp % WM, wn = warp / WM;
-  const int g = lane >> 2, t = lane & 3;
-  // warp-uniform extent of real work: empty n8 column tiles (offsets with
-  // few pairs) and padded m16 row tiles (P not a multiple of MT) are skipped
-  const int ncols = (Rc == NT) ? min(NT, R - tk.r0) : tk.pair_count * Rc;
-  const int n_tiles = max(0, min(4, (ncols - wn * 32 + 7) >> 3));
-  const int row0 = rt * MT + wm * 32;
-  const int m_tiles = max(0, min(2, (M_valid - row0 + 15) >> 4));
-  double acc[2][4][4];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(s, s);
-    cp_async_commit();
-  }
-  for (int kc = 0; kc < nk; ++kc) {
-    int nxt = kc + STAGES - 1;
-    if (nxt < nk) load_stage(nxt, nxt % STAGES);
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
-    const double* cA = sA + (kc % STAGES) * MT * KC;
-    const double* cB = sB + (kc % STAGES) * NT * BST;
-    if (n_tiles > 0 && m_tiles > 0) {
-#pragma unroll
-      for (int ks = 0; ks < KC / 8; ++ks) {
-        double a[2][4];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) {
-          const double2* pa =
-              reinterpret_cast<const double2*>(cA + ((wm * 2 + mi) * (KC / 8) + ks) * 128 + lane * 4);
-          double2 v0 = pa[0], v1 = pa[1];
-          a[mi][0] = v0.x;
-          a[mi][1] = v0.y;
-          a[mi][2] = v1.x;
-          a[mi][3] = v1.y;
-        }
-        double b[4][2];
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          if (ni < n_tiles) {
-            const double* pb = cB + (wn * 32 + ni * 8 + g) * BST + ks * 8 + t;
-            b[ni][0] = pb[0];
-            b[ni][1] = pb[4];
-          }
-        }
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
-            if (mi < m_tiles && ni < n_tiles) mma_m16n8k8(acc[mi][ni], a[mi], b[ni]);
-      }
-    }
-    __syncthreads();
-  }
-
-#pragma unroll
-  for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-    for (int cix = 0; cix < 2; ++cix) {
-      int n = wn * 32 + ni * 8 + 2 * t + cix;
-      int64_t cc = colC[n];
-      if (cc < 0) continue;
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-#pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-          int m = rt * MT + wm * 32 + mi * 16 + g + 8 * hi;
-          if (m < M_valid) atomicAdd(C + cc + m, acc[mi][ni][2 * hi + cix]);
-        }
-      }
-    }
-  }
-}
-
 // Tile layout per matrix size: "thin" (MT = -M_pad, whole matrix per item,
 // m8n8k4 chains) when 8-row padding of P is a supported instantiation, else
 // 128- (or 64-) row tiles of m16n8k8 fragments.
@@ -588,20 +435,6 @@ int gemm_mt_for(int P_out) {
 int gemm_wide_wn() { return 3; }   // 12 consumer warps: measured +1.3% over 8 (cfg4 leaf pass)
 int gemm_nt(int MT) { return (MT == 128 && gemm_use_persistent()) ? 32 * gemm_wide_wn() : 64; }
 
-template <int WM, int WN, int STAGES>
-static void launch_gemm_t(const double* A, int64_t mat_stride, const double* B, double* C,
-                          const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
-                          int M_valid, int ldc, int RT, cudaStream_t st) {
-  constexpr int MT = 32 * WM, NT = 32 * WN, KC = kKC;
-  size_t smem = sizeof(double) * STAGES * (size_t)(MT * KC + NT * (KC + 4));
-  cudaFuncSetAttribute(gemm_gather_kernel<WM, WN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  int64_t nblocks = (int64_t)ntasks * RT;
-  if (nblocks == 0) return;
-  gemm_gather_kernel<WM, WN, STAGES><<<(unsigned)nblocks, WM * WN * 32, smem, st>>>(
-      A, mat_stride, B, C, tasks, pairs, R, Rc, K_pad, M_valid, ldc, RT);
-}
-
 void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const double* B, double* C,
                  const GemmTask* tasks, int ntasks, const int2* pairs, int R, int Rc, int K_pad,
                  int M_valid, int ldc, int RT, cudaStream_t st, const double* gen) {
@@ -609,15 +442,7 @@ void launch_gemm(int MT, int NT, const double* A, int64_t mat_stride, const doub
     launch_gemm_thin(-MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, st);
     return;
   }
-  if (gemm_use_persistent()) {
-    launch_gemm_persistent(MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st,
-                           gen);
-    return;
-  }
-  if (MT == 64)
-    launch_gemm_t<2, 2, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
-  else
-    launch_gemm_t<4, 2, 2>(A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st);
+  launch_gemm_persistent(MT, NT, A, mat_stride, B, C, tasks, ntasks, pairs, R, Rc, K_pad, M_valid, ldc, RT, st, gen);
 }
 
 // ---------------------------------------------------------------------------

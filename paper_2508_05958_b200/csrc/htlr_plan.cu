@@ -596,9 +596,9 @@ static void analytic_counts(int level, int64_t& adm, int64_t& near) {
 // offsets away from the boundary at the leaf level); the z and x sweeps share
 // band pieces between the terms (htlr_band.cu bcount / boff): z 15 (B, M, P,
 // C4 and EB, EM once each), x 19 (C4 + P, M, B, C4 and EM, EB)
-static double band_flops_of(int level, bool leaf, int64_t nt) {
+static double band_flops_of(int level, bool leaf, int64_t nt, double* z_share = nullptr) {
   const int nb = 1 << level;
-  double per_line = 0;
+  double per_line = 0, z_line = 0;
   for (int q = 0; q < nb; ++q) {
     const BandLine v = band_line(q, nb);
     const int nk = leaf ? 2 : 1;   // factor kinds with a {-2..2} and a {-2, 2} term
@@ -606,7 +606,9 @@ static double band_flops_of(int level, bool leaf, int64_t nt) {
     const int zsw = v.A + v.P + nk * (v.B + v.M);
     const int xsw = (v.A + v.P) + v.A + nk * (v.M + v.B);
     per_line += ysw + zsw + xsw;
+    z_line += zsw;
   }
+  if (z_share) *z_share = z_line / per_line;
   // the region's share of the sweeps (halo lines of the z sweep not counted)
   return (double)nb * nb * per_line * 2.0 * 4096.0 * (double)nt / (double)((int64_t)1 << (3 * level));
 }
@@ -2509,7 +2511,10 @@ bool prologue_params(MvCtx& cx, const double* u, const htlr::ZeroList& zl, htlr:
 // plane kernels over whole x-y planes), so nothing on the leaf pass's path
 // waits for the upward pass: that runs on the side stream, before the level
 // passes, beside the leaf z sweep -- and writes no permuted copy of u.
-static bool leaf_from_u(const htlr_plan* pl) {
+static bool leaf_from_u(const htlr_plan* pl, int R) {
+  // several right-hand sides: u is [point][rhs], a line's points are R doubles
+  // apart; the permuted boxes keep each rhs contiguous
+  if (R != 1) return false;
   if (!pl->sep || pl->mapped || pl->d != 3 || pl->leaf_pass < 0) return false;
   const Pass& lp = pl->passes[pl->leaf_pass];
   const int nb = 1 << lp.level;
@@ -2566,7 +2571,7 @@ int mv_local(MvCtx& cx, const double* u) {
     }
     // leaf pass reading u itself: no permuted copy, and (unprofiled, outside
     // the host pipeline) the zeroing and the upward pass go to the side stream
-    const bool from_u = leaf_from_u(pl);
+    const bool from_u = leaf_from_u(pl, R);
     double* const ub_out = from_u ? nullptr : cx.ub;
     cudaStream_t ust = cx.st;
     if (from_u && cx.whole && !pl->zslab && !pl->profiling && !cx.pipe) {
@@ -2659,7 +2664,7 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
     // sharded plans: u itself (every rank holds it; the permuted copy covers
     // the own boxes only); unsharded: the permuted boxes the cube upward wrote (the
     // pitched box rows load with fewer address instructions: 108 vs 115 us)
-    const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab || leaf_from_u(pl));
+    const bool fo = ps.from_ub && u != nullptr && (pl->shard_world > 1 || pl->zslab || leaf_from_u(pl, R));
     const double* src = fo ? u : B;
     const int n = fo ? pl->n : 0;
     if (sweep == 0)
@@ -2743,9 +2748,18 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         // buffers written and read back, the accumulator read and written
         const double nv = R8 * (double)ps.P * (double)pl->levels[ps.level].nclusters;
         const double nterm = ps.to_y ? 6.0 : 4.0;
-        if (cx.prof_begin(ps.to_y ? 8 : 7, ps.level, ps.band_flops * R, nv * (1.0 + 2.0 * nterm + 2.0))) return 1;
-        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) launch_band_sweep(pl, ps, sw, B, C, R, sst, u);
-        if (cx.prof_end()) return 1;
+        // profiled per kernel: the z sweep (kind 9: reads the sources, writes
+        // the term buffers) and the y-x sweep (kind 10: reads the term buffers
+        // and the self pairs' sources, writes the accumulator)
+        double zs = 0.0;
+        band_flops_of(ps.level, ps.to_y, 1, &zs);
+        for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) {
+          if (sw == 0 && cx.prof_begin(9, ps.level, zs * ps.band_flops * R, nv * (1.0 + nterm))) return 1;
+          if (sw == 1 && cx.prof_begin(10, ps.level, (1.0 - zs) * ps.band_flops * R, nv * (nterm + 2.0))) return 1;
+          launch_band_sweep(pl, ps, sw, B, C, R, sst, u);
+          if (sw == 0 && cx.prof_end()) return 1;
+          if (sw == 2 && cx.prof_end()) return 1;
+        }
         continue;
       }
       if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;

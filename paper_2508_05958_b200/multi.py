@@ -174,9 +174,10 @@ class ShardedOperator:
         if not hasattr(self, "_graphs"):
             self._graphs = {}
         if R not in self._graphs:
-            u_st = torch.empty_like(ud)
+            # captured over the first caller's u itself (kept alive here): a
+            # caller that reuses its input vector pays no staging copy
+            u_st = ud
             f_st = torch.zeros_like(ud)
-            u_st.copy_(ud)
             bufs = self.exchange_buffers(R)
             side = torch.cuda.Stream(device=self.device)
             side.wait_stream(torch.cuda.current_stream())
@@ -186,15 +187,20 @@ class ShardedOperator:
                     allreduce_sum(bufs, self.group)
                 self.remote_phase(u_st, f_st, R)
             torch.cuda.current_stream().wait_stream(side)
+            # the warm-up collective has completed before the capture starts,
+            # and the capture is thread-local: the process group's watchdog
+            # thread may query its events meanwhile
+            torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self.local_phase(u_st, R)
                 if self.world > 1:
                     allreduce_sum(bufs, self.group)
                 self.remote_phase(u_st, f_st, R)
             self._graphs[R] = (g, u_st, f_st)
         g, u_st, f_st = self._graphs[R]
-        u_st.copy_(ud)
+        if ud.data_ptr() != u_st.data_ptr():
+            u_st.copy_(ud)
         g.replay()
         return f_st.clone()
 

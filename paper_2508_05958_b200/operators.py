@@ -195,7 +195,7 @@ class HTLRMatrix:
         return int(_lib.lib().htlr_last_launch_count(self._plan))
 
     PHASES = ("permute", "upward", "gemm_level", "gemm_leaf", "downward", "regen_level", "regen_near", "sep_level",
-              "sep_leaf")
+              "sep_leaf", "band_z", "band_yx")
 
     def profile(self, on: bool = True) -> None:
         """Bracket every kernel launch of later matvecs with CUDA events."""

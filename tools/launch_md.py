@@ -19,7 +19,7 @@ def table(path, title):
         if name.startswith("at::"):   # the driver script's own checksum kernels
             continue
         recs.append((name, r[gi] if gi is not None else "", us))
-    starts = [i for i, rec in enumerate(recs) if "permute_in" in rec[0] or "prologue_kernel" in rec[0] or "upward8" in rec[0]]
+    starts = [i for i, rec in enumerate(recs) if "permute_in" in rec[0] or "prologue_kernel" in rec[0] or "upward8" in rec[0] or "upward_cube" in rec[0]]
     last = recs[starts[-1]:] if starts else recs
     tot = sum(x[2] for x in last)
     out = [f"## {title}: one matvec = {tot:.1f} us of kernel time", "", "| kernel | grid | us | share |",
