@@ -352,3 +352,34 @@ def test_field_shaped_input_flattens_in_fortran_order():
         f = f.cpu().numpy() if isinstance(f, torch.Tensor) else np.asarray(f)
         assert f.shape == (4096,)
         assert rel(f, gold) <= TOL
+
+
+def test_cfg4_full_size_properties():
+    """BASELINE config 4 at its own size (N = 2,097,152), through properties
+    that do not need the reference's (infeasible) full matvec: the operator
+    the reference defines is symmetric (uniform weights, a symmetric kernel,
+    Tucker blocks whose (tau, sigma) and (sigma, tau) cores are transposes:
+    blocks.py:126-164), commutes with the grid's reflections x_a -> 1 - x_a
+    (the tree, the lists and the Chebyshev nodes are reflection symmetric) and
+    is linear.  Sampled rows of the same matvec are checked against the
+    reference's fixture in test_matvec_sampled_rows_vs_reference."""
+    import torch
+    w, op = build("cfg4")
+    assert op.leaf_pass() == "banded"
+    n = w.grid.n
+    rng = np.random.default_rng(11)
+    u, v = (torch.from_numpy(rng.standard_normal(n ** 3)).cuda() for _ in range(2))
+    Au, Av = H.matvec(op, u).clone(), H.matvec(op, v).clone()
+    # symmetry: <v, A u> = <u, A v>
+    s1, s2 = float(torch.dot(v, Au)), float(torch.dot(u, Av))
+    scale = float(torch.linalg.norm(v) * torch.linalg.norm(Au))
+    assert abs(s1 - s2) <= 1e-12 * scale, (s1, s2)
+    # linearity
+    lhs = H.matvec(op, 2.0 * u - 0.5 * v)
+    assert float(torch.linalg.norm(lhs - (2.0 * Au - 0.5 * Av)) / torch.linalg.norm(lhs)) <= 1e-13
+    # reflections: the F-order vector as an (x, y, z) field is u.reshape(z, y, x)
+    for dims in ((0,), (1,), (2,), (0, 1, 2)):
+        ur = torch.flip(u.reshape(n, n, n), dims).reshape(-1).contiguous()
+        Aur = H.matvec(op, ur)
+        ref = torch.flip(Au.reshape(n, n, n), dims).reshape(-1)
+        assert float(torch.linalg.norm(Aur - ref) / torch.linalg.norm(ref)) <= 1e-12, dims
