@@ -295,6 +295,12 @@ struct htlr_plan {
   // concurrent level passes (mv_remote): side stream + fork / join events
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_ev[2] = {nullptr, nullptr};
+  // z-slab shards: the leaf pass reads only u, so the local phase starts it
+  // on its own stream, beside the upward pass and the exchange; the remote
+  // phase joins it before the downward pass
+  cudaStream_t leaf_stream = nullptr;
+  cudaEvent_t leaf_ev[2] = {nullptr, nullptr};
+  bool leaf_pending = false;
   std::vector<cudaEvent_t> ov_ev;
   std::vector<cudaEvent_t> prof_ev;      // 2 per launch
   std::vector<int32_t> prof_kind;
@@ -470,6 +476,9 @@ int htlr_plan_destroy(htlr_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
   for (auto& e : pl->side_ev)
+    if (e) cudaEventDestroy(e);
+  if (pl->leaf_stream) cudaStreamDestroy(pl->leaf_stream);
+  for (auto& e : pl->leaf_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : pl->ov_ev) cudaEventDestroy(e);
   for (auto& lv : pl->levels) {
@@ -2507,6 +2516,9 @@ bool prologue_params(MvCtx& cx, const double* u, const htlr::ZeroList& zl, htlr:
   return true;
 }
 
+static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
+                              cudaStream_t st, const double* u, int max_ctas);
+
 // The banded leaf pass of an unsharded plan reads the F-order u itself (line /
 // plane kernels over whole x-y planes), so nothing on the leaf pass's path
 // waits for the upward pass: that runs on the side stream, before the level
@@ -2600,6 +2612,17 @@ int mv_local(MvCtx& cx, const double* u) {
       cx.launches += hp->S;
       return 0;
     }
+    if (pl->zslab && lp.band && !pl->profiling && !cx.pipe) {
+      // z-slab shard: the whole leaf pass of the own slab beside the upward pass
+      if (!pl->leaf_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->leaf_stream, cudaStreamNonBlocking));
+      for (auto& ev : pl->leaf_ev)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(pl->leaf_ev[0], cx.st));
+      CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, pl->leaf_ev[0], 0));
+      for (int sw = 0; sw < 3; ++sw) launch_band_sweep(pl, lp, sw, cx.ub, pl->Y.d(), R, pl->leaf_stream, u, 0);
+      CUDA_TRY(cudaEventRecord(pl->leaf_ev[1], pl->leaf_stream));
+      pl->leaf_pending = true;
+    }
     htlr::launch_upward_cube(cl, pl->L, R, nb, ust, u, ub_out, lp.K_pad, lp.zpitch, pl->n,
                              pl->zslab ? pl->zs_lo : 0, pl->zslab ? pl->zs_hi : 1 << 30);
     if (cx.prof_end()) return 1;
@@ -2655,7 +2678,7 @@ static int level_sms(bool with_upward) { return with_upward ? 48 : 20; }
 // F-order u itself (no permuted copy).  Octant regions of Morton-sharded
 // plans keep the staged sweeps of htlr_sep.cu.
 static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
-                              cudaStream_t st, const double* u, int max_ctas = 0) {
+                              cudaStream_t st, const double* u, int max_ctas) {
   const int nb = 1 << ps.level;
   const bool xy_full = ps.band_lo[0] == 0 && ps.band_lo[1] == 0 && ps.band_hi[0] == nb && ps.band_hi[1] == nb;
   const double* corr = ps.to_y ? pl->sep_corr.d() : nullptr;
@@ -2699,7 +2722,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     Level& lv = pl->levels[ps.level];
     CUDA_TRY(cudaMemsetAsync(lv.H.ptr, 0, (size_t)lv.nclusters * R * P * sizeof(double), cx.st));
   }
-  if ((stages & 1) && !cx.zeroed && !rest_only)
+  if ((stages & 1) && !cx.zeroed && !rest_only && !pl->leaf_pending)
     CUDA_TRY(cudaMemsetAsync(pl->Y.ptr, 0, (size_t)nleaf * R * lp.P * sizeof(double), cx.st));
   // The level passes (-> H_l) and the leaf pass (-> Y) are independent: the
   // level passes go to a side stream (a parallel branch of the graph), so
@@ -2724,7 +2747,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
     CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
   }
-  if (fork && !own_only && !rest_only) {
+  if (fork && !own_only && !rest_only && !pl->leaf_pending) {
     const Pass& lq = pl->passes[pl->leaf_pass];
     if (pl->sep && lq.band) {
       int sms = 148;
@@ -2735,7 +2758,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   }
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
-    const cudaStream_t sst = (fork && !ps.to_y) ? pl->side_stream : cx.st;
+    if (ps.to_y && pl->leaf_pending) continue;   // started by the local phase (z-slab shards)
+    // level passes on the side stream; with the leaf pass already running
+    // elsewhere the main stream is free, so they alternate between the two
+    const cudaStream_t sst = (fork && !ps.to_y && !(pl->leaf_pending && (i & 1))) ? pl->side_stream : cx.st;
     if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
       if (ps.band && own_only) continue;   // the sweeps need every (gathered) source box
@@ -2756,7 +2782,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) {
           if (sw == 0 && cx.prof_begin(9, ps.level, zs * ps.band_flops * R, nv * (1.0 + nterm))) return 1;
           if (sw == 1 && cx.prof_begin(10, ps.level, (1.0 - zs) * ps.band_flops * R, nv * (nterm + 2.0))) return 1;
-          launch_band_sweep(pl, ps, sw, B, C, R, sst, u);
+          launch_band_sweep(pl, ps, sw, B, C, R, sst, u, 0);
           if (sw == 0 && cx.prof_end()) return 1;
           if (sw == 2 && cx.prof_end()) return 1;
         }
@@ -2819,6 +2845,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   if (fork || cx.side_forked) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
     CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
+  }
+  if (pl->leaf_pending && (stages & 1)) {
+    CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->leaf_ev[1], 0));
+    pl->leaf_pending = false;
   }
   htlr::DownParams dp{};
   dp.nlev = 0;
