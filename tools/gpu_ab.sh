@@ -1,5 +1,7 @@
 export PYTHONPATH=$PWD
-timeout 900 python -m pytest tests/test_gpu_multi.py tests/test_gpu_mapped.py -m gpu -x -q 2>&1 | tail -2 > gpurun_out/ab.log
-timeout 600 python tools/shard_graph_probe.py >> gpurun_out/ab.log 2>&1
-timeout 600 python tools/shard_probe.py 2>&1 | tail -5 | cut -c1-330 >> gpurun_out/ab.log
-HTLR_DIST_BACKEND=gloo timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | cut -c1-200 >> gpurun_out/ab.log
+timeout 900 python -m pytest tests/test_gpu_separable.py tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2 > gpurun_out/ab.log
+for v in 1 0; do
+echo "== HTLR_HALF_PLANES=$v" >> gpurun_out/ab.log
+HTLR_HALF_PLANES=$v timeout 300 python tools/phases.py cfg4 50 2>&1 | head -4 >> gpurun_out/ab.log
+HTLR_HALF_PLANES=$v timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['e2e']['ms_per_step'])" >> gpurun_out/ab.log
+done
