@@ -612,7 +612,8 @@ def run_b200(args):
         "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(phases.items())},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": io_bytes,
-                "d2h_bytes_per_step": io_bytes, "ms_per_step": e2e_total / args.steps},
+                "d2h_bytes_per_step": io_bytes, "ms_per_step": e2e_total / args.steps,
+                "ms_min": min(e2e_ms), "ms_median": sorted(e2e_ms)[len(e2e_ms) // 2], "ms_max": max(e2e_ms)},
         "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
     }

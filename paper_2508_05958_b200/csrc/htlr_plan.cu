@@ -704,6 +704,97 @@ int htlr_build_lists(htlr_plan* pl) {
   // inside a member list is not kept: every consumer sorts it.
   const size_t nlf = tr.leaves.size();
   const size_t ntab = pl->levels.size() + 1;   // adm per level, then near
+  if (pl->mapped) {
+    // Mapped grids regenerate their blocks: no offset tables, only the CSR of
+    // the own targets per level and of the near field (sources sorted by
+    // Morton id), built straight from the leaves: per-chunk counts per
+    // (table, target row), an exclusive prefix over (row, chunk), then every
+    // chunk writes its sources at its own positions (all cores, no atomics).
+    std::vector<int64_t> rbase(ntab + 1, 0);   // first row of each table in the concatenated row space
+    auto tlevel = [&](size_t t) { return t + 1 < ntab ? (int)t : pl->L; };
+    for (size_t t = 0; t < ntab; ++t) {
+      const int l = tlevel(t);
+      rbase[t + 1] = rbase[t] + (pl->own_lo[l] < 0 ? 0 : pl->own_hi[l] - pl->own_lo[l]);
+    }
+    const int64_t nrows = rbase[ntab];
+    const size_t chunk = 1 << 15, nchunks = (nlf + chunk - 1) / chunk;
+    std::vector<std::vector<int>> cnt(nchunks, std::vector<int>((size_t)nrows, 0));
+    std::vector<std::vector<int64_t>> lcount(nchunks, std::vector<int64_t>(ntab, 0));
+    std::atomic<bool> bad_level{false};
+    auto row_of = [&](const htlr::LeafRec& lf) -> int64_t {   // -1: not an own target
+      const size_t t = lf.kind == 0 ? (size_t)lf.level : ntab - 1;
+      if (pl->own_lo[lf.level] < 0) return -2;
+      const int64_t tl = htlr::morton_encode(lf.tc, d, lf.level);
+      if (tl < pl->own_lo[lf.level] || tl >= pl->own_hi[lf.level]) return -1;
+      return rbase[t] + tl - pl->own_lo[lf.level];
+    };
+    parallel_for(nchunks, [&](size_t c) {
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i) {
+        const auto& lf = tr.leaves[i];
+        lcount[c][lf.kind == 0 ? (size_t)lf.level : ntab - 1]++;
+        const int64_t r = row_of(lf);
+        if (r == -2) bad_level = true;
+        if (r >= 0) cnt[c][(size_t)r]++;
+      }
+    });
+    if (bad_level) return fail(-1, "admissible blocks on a level with fewer clusters than shards");
+    for (size_t c = 0; c < nchunks; ++c) {
+      for (size_t t = 0; t + 1 < ntab; ++t) pl->levels[t].num_adm += lcount[c][t];
+      pl->num_near += lcount[c][ntab - 1];
+    }
+    std::vector<int64_t> rptr((size_t)nrows + 1, 0);
+    {
+      int64_t acc = 0;
+      for (int64_t r = 0; r < nrows; ++r) {
+        rptr[(size_t)r] = acc;
+        for (size_t c = 0; c < nchunks; ++c) {
+          const int v = cnt[c][(size_t)r];
+          cnt[c][(size_t)r] = (int)(acc - rptr[(size_t)r]);   // offset inside the row
+          acc += v;
+        }
+      }
+      rptr[(size_t)nrows] = acc;
+    }
+    std::vector<int> cols((size_t)rptr[(size_t)nrows]);
+    parallel_for(nchunks, [&](size_t c) {
+      const size_t e = std::min(nlf, (c + 1) * chunk);
+      for (size_t i = c * chunk; i < e; ++i) {
+        const auto& lf = tr.leaves[i];
+        const int64_t r = row_of(lf);
+        if (r >= 0) cols[(size_t)(rptr[(size_t)r] + cnt[c][(size_t)r]++)] = (int)htlr::morton_encode(lf.sc, d, lf.level);
+      }
+    });
+    parallel_for((size_t)nrows, [&](size_t r) { std::sort(cols.begin() + rptr[r], cols.begin() + rptr[r + 1]); });
+    tm.mark("lists: mapped CSR (from the leaves)");
+    for (const auto& lv : pl->levels) {
+      if (lv.num_adm > 0 && lv.side < p) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "qr requires rows >= cols, got shape (%d, %d)", lv.side, p);
+        return fail(-1, buf);
+      }
+    }
+    if (ipow(pl->sL, d) > 4096) return fail(-1, "leaf boxes above 4096 points are not supported by the B200 path");
+    if (ipow(p, d) > 4096) return fail(-1, "rank^d above 4096 is not supported by the B200 path");
+    pl->passes.clear();
+    auto slice = [&](size_t t, std::vector<int64_t>& ptr, std::vector<int>& out) {
+      const int64_t r0 = rbase[t], r1 = rbase[t + 1];
+      ptr.assign((size_t)(r1 - r0) + 1, 0);
+      for (int64_t r = r0; r <= r1; ++r) ptr[(size_t)(r - r0)] = rptr[(size_t)r] - rptr[(size_t)r0];
+      out.assign(cols.begin() + rptr[(size_t)r0], cols.begin() + rptr[(size_t)r1]);
+    };
+    for (int l = 0; l <= pl->L; ++l) {
+      Level& lv = pl->levels[l];
+      lv.needs_up = lv.num_adm > 0;
+      if (lv.needs_up) slice((size_t)l, lv.csr_ptr, lv.csr_cols);
+    }
+    slice(ntab - 1, pl->near_ptr, pl->near_cols);
+    if (pl->sL > 16) return fail(-1, "mapped grids support leaf sides up to 16");
+    pl->merged = false;
+    pl->lists_built = true;
+    pl->constructed = false;
+    return 0;
+  }
   std::vector<OffsetTable*> tabs;
   for (auto& lv : pl->levels) tabs.push_back(&lv.adm);
   tabs.push_back(&pl->near);
@@ -873,36 +964,6 @@ int htlr_build_lists(htlr_plan* pl) {
   if (PL > 4096) return fail(-1, "leaf boxes above 4096 points are not supported by the B200 path");
   if (P > 4096) return fail(-1, "rank^d above 4096 is not supported by the B200 path");
   pl->passes.clear();
-  if (pl->mapped) {
-    // CSR of the own targets per level (sources sorted by Morton id)
-    auto csr = [&](const OffsetTable& tab, int level, std::vector<int64_t>& ptr, std::vector<int>& cols) {
-      const int64_t lo = pl->own_lo[level], hi = pl->own_hi[level];
-      ptr.assign(hi - lo + 1, 0);
-      for (const auto& mem : tab.members)
-        for (const auto& q : mem) ptr[q.first - lo + 1]++;
-      for (int64_t r = 0; r < hi - lo; ++r) ptr[r + 1] += ptr[r];
-      cols.assign((size_t)ptr[hi - lo], 0);
-      std::vector<int64_t> fillp(ptr.begin(), ptr.end() - 1);
-      for (const auto& mem : tab.members)
-        for (const auto& q : mem) cols[fillp[q.first - lo]++] = q.second;
-      parallel_for((size_t)(hi - lo), [&](size_t r) { std::sort(cols.begin() + ptr[r], cols.begin() + ptr[r + 1]); });
-    };
-    for (int l = 0; l <= pl->L; ++l) {
-      Level& lv = pl->levels[l];
-      lv.needs_up = lv.num_adm > 0;
-      if (lv.needs_up) {
-        if (pl->own_lo[l] < 0) return fail(-1, "admissible blocks on a level with fewer clusters than shards");
-        csr(lv.adm, l, lv.csr_ptr, lv.csr_cols);
-      }
-    }
-    csr(pl->near, pl->L, pl->near_ptr, pl->near_cols);
-    tm.mark("lists: mapped CSR");
-    if (pl->sL > 16) return fail(-1, "mapped grids support leaf sides up to 16");
-    pl->merged = false;
-    pl->lists_built = true;
-    pl->constructed = false;
-    return 0;
-  }
   pl->merged = pl->levels[pl->L].num_adm > 0 && pl->sL == p;
   // passes
   auto fill_pass = [&](Pass& ps, std::vector<const OffsetTable*> tabs) {
@@ -2517,7 +2578,7 @@ bool prologue_params(MvCtx& cx, const double* u, const htlr::ZeroList& zl, htlr:
 }
 
 static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
-                              cudaStream_t st, const double* u, int max_ctas);
+                              cudaStream_t st, const double* u, int max_ctas, int zlo_o = -1, int zhi_o = -1);
 
 // The banded leaf pass of an unsharded plan reads the F-order u itself (line /
 // plane kernels over whole x-y planes), so nothing on the leaf pass's path
@@ -2678,8 +2739,10 @@ static int level_sms(bool with_upward) { return with_upward ? 48 : 20; }
 // F-order u itself (no permuted copy).  Octant regions of Morton-sharded
 // plans keep the staged sweeps of htlr_sep.cu.
 static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const double* B, double* C, int R,
-                              cudaStream_t st, const double* u, int max_ctas) {
+                              cudaStream_t st, const double* u, int max_ctas, int zlo_o, int zhi_o) {
   const int nb = 1 << ps.level;
+  // target z boxes: the pass's region, or a part of it (host pipeline)
+  const int zlo = zlo_o >= 0 ? zlo_o : ps.band_lo[2], zhi = zhi_o >= 0 ? zhi_o : ps.band_hi[2];
   const bool xy_full = ps.band_lo[0] == 0 && ps.band_lo[1] == 0 && ps.band_hi[0] == nb && ps.band_hi[1] == nb;
   const double* corr = ps.to_y ? pl->sep_corr.d() : nullptr;
   const int nterms = ps.to_y ? 6 : 4;
@@ -2692,13 +2755,13 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
     const int n = fo ? pl->n : 0;
     if (sweep == 0)
       htlr::launch_band_lines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
-                              ps.band_ws.d(), st, n, ps.band_lo[2], ps.band_hi[2], max_ctas);
+                              ps.band_ws.d(), st, n, zlo, zhi, max_ctas);
     else if (sweep == 1 && band_xy_lines(pl))
       htlr::launch_band_ylines(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, ps.band_ws.d(), ps.band_ws2.d(), C, src,
-                               ps.K_pad, ps.zpitch, n, corr, pl->kp.scale, st, ps.band_lo[2], ps.band_hi[2]);
+                               ps.K_pad, ps.zpitch, n, corr, pl->kp.scale, st, zlo, zhi);
     else if (sweep == 1)
       htlr::launch_band_planes(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
-                               ps.band_ws.d(), C, corr, pl->kp.scale, st, n, ps.band_lo[2], ps.band_hi[2]);
+                               ps.band_ws.d(), C, corr, pl->kp.scale, st, n, zlo, zhi);
     return;
   }
   htlr::launch_sep_band(sweep, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C, corr,
@@ -2747,7 +2810,32 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[0], cx.st));
     CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->side_ev[0], 0));
   }
-  if (fork && !own_only && !rest_only && !pl->leaf_pending) {
+  // Host pipeline: the leaf pass in two parts on its own stream.  The target
+  // boxes z < za reach no source in the last slab of u, so their sweeps start
+  // when the slab before it has landed and run under the last slab's copy;
+  // the rest starts when the last slab has landed.  The first slabs of f need
+  // only the first part (and the level passes) before their downward pass.
+  int pipe_za = 0;
+  if (cx.pipe && fork && !own_only && !rest_only && !pl->leaf_pending && pl->sep && leaf_from_u(pl, R)) {
+    HostPipe* hp = cx.pipe;
+    const Pass& lq = pl->passes[pl->leaf_pass];
+    const int nbz = 1 << lq.level;
+    const int za = hp->S >= 2 ? ((hp->zu[hp->S - 1] - 5) & ~1) : 0;
+    if (za >= 2 && za < nbz) {
+      if (!pl->leaf_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->leaf_stream, cudaStreamNonBlocking));
+      for (auto& ev : pl->leaf_ev)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, hp->ev[1 + hp->S - 2], 0));
+      for (int sw = 0; sw < 2; ++sw) launch_band_sweep(pl, lq, sw, cx.ub, pl->Y.d(), R, pl->leaf_stream, u, 0, 0, za);
+      CUDA_TRY(cudaEventRecord(pl->leaf_ev[0], pl->leaf_stream));
+      CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, hp->ev[1 + hp->S - 1], 0));
+      for (int sw = 0; sw < 2; ++sw) launch_band_sweep(pl, lq, sw, cx.ub, pl->Y.d(), R, pl->leaf_stream, u, 0, za, nbz);
+      CUDA_TRY(cudaEventRecord(pl->leaf_ev[1], pl->leaf_stream));
+      cx.launches += 4;
+      pipe_za = za;
+    }
+  }
+  if (fork && !own_only && !rest_only && !pl->leaf_pending && !pipe_za) {
     const Pass& lq = pl->passes[pl->leaf_pass];
     if (pl->sep && lq.band) {
       int sms = 148;
@@ -2759,6 +2847,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     if (ps.to_y && pl->leaf_pending) continue;   // started by the local phase (z-slab shards)
+    if (ps.to_y && pipe_za) continue;            // running in two parts on the leaf stream (host pipeline)
     // level passes on the side stream; with the leaf pass already running
     // elsewhere the main stream is free, so they alternate between the two
     const cudaStream_t sst = (fork && !ps.to_y && !(pl->leaf_pending && (i & 1))) ? pl->side_stream : cx.st;
@@ -2871,7 +2960,13 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   if (HostPipe* hp = cx.pipe) {
     if (!cube) return fail(2, "host pipeline: cube downward not applicable");
     // one launch per slab of f, each copied out while the next is computed
+    bool joined_b = false;
+    if (pipe_za) CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->leaf_ev[0], 0));
     for (int k = 0; k < hp->S; ++k) {
+      if (pipe_za && hp->zf[k + 1] > pipe_za && !joined_b) {
+        CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->leaf_ev[1], 0));
+        joined_b = true;
+      }
       htlr::launch_downward_cube(cl, pl->L, R, b0, nb, cx.st, u, f, pl->Y.d(), av, pl->desc.coeff_const, pl->n,
                                  hp->zf[k], hp->zf[k + 1]);
       CUDA_TRY(cudaEventRecord(hp->ev[1 + hp->S + k], cx.st));
@@ -2880,6 +2975,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       CUDA_TRY(cudaMemcpyAsync(hp->fh + o, f + o, c * sizeof(double), cudaMemcpyDefault, hp->cs));
     }
     cx.launches += hp->S;
+    if (pipe_za && !joined_b) CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->leaf_ev[1], 0));
     CUDA_TRY(cudaEventRecord(hp->ev[2 * hp->S + 1], hp->cs));
     CUDA_TRY(cudaStreamWaitEvent(cx.st, hp->ev[2 * hp->S + 1], 0));
     CUDA_TRY(cudaGetLastError());
