@@ -2849,8 +2849,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     if (ps.to_y && pl->leaf_pending) continue;   // started by the local phase (z-slab shards)
     if (ps.to_y && pipe_za) continue;            // running in two parts on the leaf stream (host pipeline)
     // level passes on the side stream; with the leaf pass already running
-    // elsewhere the main stream is free, so they alternate between the two
-    const cudaStream_t sst = (fork && !ps.to_y && !(pl->leaf_pending && (i & 1))) ? pl->side_stream : cx.st;
+    // elsewhere (z-slab shards, host pipeline) the main stream is free, so
+    // they alternate between the two
+    const cudaStream_t sst =
+        (fork && !ps.to_y && !((pl->leaf_pending || pipe_za) && (i & 1))) ? pl->side_stream : cx.st;
     if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
       if (ps.band && own_only) continue;   // the sweeps need every (gathered) source box
