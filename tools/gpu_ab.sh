@@ -1,4 +1,4 @@
 export PYTHONPATH=$PWD
-timeout 900 python -m pytest tests/test_gpu_separable.py -m gpu -x -q -k "host or out_buffer or graph" 2>&1 | tail -2 > gpurun_out/ab.log
-timeout 300 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned" >> gpurun_out/ab.log
-timeout 300 python tools/e2e_probe.py cfg4 2>&1 | grep "pinned" >> gpurun_out/ab.log
+for i in 1 2 3 4; do
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['e2e']['ms_per_step'], d['e2e']['ms_min'])" >> gpurun_out/ab.log
+done
