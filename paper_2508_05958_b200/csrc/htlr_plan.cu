@@ -3068,7 +3068,7 @@ int htlr_matvec(htlr_plan* pl, const double* u, double* f, int64_t nrhs, void* s
         hit = nullptr;
       }
       cudaGraphExec_t exec = nullptr;
-      if (!hit && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+      if (!hit && cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority) == cudaSuccess) {
         if (pl->graph_cache.size() >= 8) drop_graphs(pl);
         pl->graph_cache.push_back({cx.R, u, f, pl->profiling, exec, {}, {}, {}, {}, 0});
         hit = &pl->graph_cache.back();
@@ -3327,7 +3327,7 @@ int htlr_matvec_host(htlr_plan* pl, const double* u, double* f, int64_t nrhs, vo
   cudaGraph_t graph = nullptr;
   cudaError_t ce = cudaStreamEndCapture(cc.st, &graph);
   cudaGraphExec_t exec = nullptr;
-  if (rc || ce != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+  if (rc || ce != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority) != cudaSuccess) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
     return rc ? rc : fail(2, std::string("overlapped matvec capture failed: ") + cudaGetErrorString(ce));
