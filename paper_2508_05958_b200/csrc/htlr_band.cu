@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
                                                                 const double* __restrict__ ws, int64_t tstride,
                                                                 double* __restrict__ Y,
                                                                 const double* __restrict__ corr_ptr, double scale,
-                                                                int n, int zlo) {
+                                                                int n, int zlo, double* __restrict__ fred, int nf) {
   constexpr int NQ = NB / 4;   // quarters of a row of cells (4 cells = 16 TMEM columns)
   const int R = R1 ? 1 : R_;
   extern __shared__ __align__(16) double smp[];
@@ -615,11 +615,18 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
                                    (int64_t)n * n * (8 * bz + zl)) * R + r
                            : ub + m * ldub + zpub * zl + 16 * q + g;
       const int64_t ustep = n ? (int64_t)n * R : 8;
+      // fred: the plane's share of f summed straight into the F-order result
+      // (the downward pass adds its own with REDs too: no Y round trip and no
+      // order between the two)
+      double* of = fred ? fred + ((int64_t)(8 * (4 * Q + c) + g) + (int64_t)nf * (8 * w + 2 * q) +
+                                  (int64_t)nf * nf * (8 * bz + zl)) * R + r
+                        : nullptr;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         double val = scale * v[c][j];
         if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
-        o[8 * j] = val;
+        if (fred) atomicAdd(of + (int64_t)j * nf * R, val);
+        else o[8 * j] = val;
       }
     }
   }
@@ -888,7 +895,8 @@ void launch_lines_t(const double* tab, int NO, int R, const double* ub, int ldub
 
 template <int NB, int NT>
 void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldub, int zpub, const double* ws,
-                     double* Y, const double* corr, double scale, cudaStream_t st, int n, int zlo, int zhi) {
+                     double* Y, const double* corr, double scale, cudaStream_t st, int n, int zlo, int zhi,
+                     double* fred, int nf) {
   if (zhi <= zlo) return;
   const int64_t tstride = (int64_t)NB * NB * NB * R * 512;
   const size_t smem = (size_t)NB * NB * 32 * sizeof(double2) + (size_t)2 * NO * kTabSlot * sizeof(double);
@@ -900,10 +908,10 @@ void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldu
   }
   if (R == 1)
     band_plane_kernel<NB, NT, true><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
-        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo);
+        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo, fred, nf);
   else
     band_plane_kernel<NB, NT, false><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
-        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo);
+        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo, fred, nf);
 }
 
 }  // namespace
@@ -926,15 +934,15 @@ void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, cons
 
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
                         const double* ws, double* Y, const double* corr, double scale, cudaStream_t st, int n,
-                        int zlo, int zhi) {
+                        int zlo, int zhi, double* fred, int nf) {
   zpub = zpub ? zpub : 64;
   zhi = std::min(zhi, 1 << L);
-  if (L == 4) nterms == 6 ? launch_planes_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
-                          : launch_planes_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
-  else if (L == 3) nterms == 6 ? launch_planes_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
-                               : launch_planes_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
-  else nterms == 6 ? launch_planes_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi)
-                   : launch_planes_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi);
+  if (L == 4) nterms == 6 ? launch_planes_t<16, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf)
+                          : launch_planes_t<16, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf);
+  else if (L == 3) nterms == 6 ? launch_planes_t<8, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf)
+                               : launch_planes_t<8, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf);
+  else nterms == 6 ? launch_planes_t<4, 6>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf)
+                   : launch_planes_t<4, 4>(tab, NO, R, ub, ldub, zpub, ws, Y, corr, scale, st, n, zlo, zhi, fred, nf);
 }
 
 void launch_band_ylines(int L, int nterms, const double* tab, int NO, int R, const double* ws, double* ws2, double* Y,

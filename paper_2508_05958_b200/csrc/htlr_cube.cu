@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kCubeThreads, 4)
 __global__ void __launch_bounds__(kCubeThreads, 4)
     downward_cube_kernel(CubeLevels cl, int L, int R, int64_t b0, int64_t nb, const double* __restrict__ u,
                          double* __restrict__ f, const double* __restrict__ Y, const double* __restrict__ avec,
-                         double aconst, int n, int zlo, int zhi) {
+                         double aconst, int n, int zlo, int zhi, int red) {
   extern __shared__ __align__(16) double smc[];
   double* qs = smc;                      // Q_c [16][8]
   double* ms = qs + 128;                 // [coarse level][axis][8 x 8]
@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(kCubeThreads, 4)
           const double a = avec ? __ldg(avec + gi + j) : aconst;
           if (a != 0.0) o[j] = fma(a, __ldg(u + (gi + j) * R + r), o[j]);
         }
-        if (R == 1) {
+        if (red) {   // f is summed: the leaf pass adds its share itself (band_plane_kernel, fred)
+          atomicAdd(f + gi * R + r, o[0]);
+          atomicAdd(f + (gi + 1) * R + r, o[1]);
+        } else if (R == 1) {
           *reinterpret_cast<double2*>(f + gi) = make_double2(o[0], o[1]);
         } else {
           f[gi * R + r] = o[0];
@@ -344,7 +347,7 @@ void launch_upward_cube(const CubeLevels& cl, int L, int R, int64_t nb, cudaStre
 
 void launch_downward_cube(const CubeLevels& cl, int L, int R, int64_t b0, int64_t nb, cudaStream_t st,
                           const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n,
-                          int zlo, int zhi) {
+                          int zlo, int zhi, bool red) {
   if (nb <= 0) return;
   const size_t smem =
       (size_t)(128 + kMaxCubeCoarse * 192 + (kMaxCubeCoarse + 1) * 512 + 8 * kHP + 1024) * sizeof(double);
@@ -354,7 +357,8 @@ void launch_downward_cube(const CubeLevels& cl, int L, int R, int64_t b0, int64_
     attr = true;
   }
   downward_cube_kernel<<<dim3((unsigned)((nb + 7) / 8), R), kCubeThreads, smem, st>>>(cl, L, R, b0, nb, u, f, Y,
-                                                                                      a_vec, a_const, n, zlo, zhi);
+                                                                                      a_vec, a_const, n, zlo, zhi,
+                                                                                      red ? 1 : 0);
 }
 
 }  // namespace htlr

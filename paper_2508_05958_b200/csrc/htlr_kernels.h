@@ -238,7 +238,7 @@ void launch_band_lines(int L, int nterms, const double* tab, int NO, int R, cons
                        double* ws, cudaStream_t st, int n = 0, int zlo = 0, int zhi = 1 << 30, int max_ctas = 0);
 void launch_band_planes(int L, int nterms, const double* tab, int NO, int R, const double* ub, int ldub, int zpub,
                         const double* ws, double* Y, const double* corr, double scale, cudaStream_t st, int n = 0,
-                        int zlo = 0, int zhi = 1 << 30);
+                        int zlo = 0, int zhi = 1 << 30, double* fred = nullptr, int nf = 0);
 // the y-x sweep as two line kernels over all SMs (z-slab shards: a slab has
 // few planes): ws (z-swept terms) -> ws2 (y-swept, B-fragment order) -> Y
 void launch_band_ylines(int L, int nterms, const double* tab, int NO, int R, const double* ws, double* ws2, double* Y,
@@ -278,7 +278,7 @@ void launch_upward_cube(const CubeLevels& cl, int L, int R, int64_t nb, cudaStre
                         double* ub_out, int ldub, int zpub, int n, int zlo = 0, int zhi = 1 << 30);
 void launch_downward_cube(const CubeLevels& cl, int L, int R, int64_t b0, int64_t nb, cudaStream_t st,
                           const double* u, double* f, const double* Y, const double* a_vec, double a_const, int n,
-                          int zlo = 0, int zhi = 1 << 30);
+                          int zlo = 0, int zhi = 1 << 30, bool red = false);
 // mapped grid (htlr_mapped.cu)
 void launch_mapped_factors(const MappedFactorJob* jobs, int njobs, int total_intervals, const double* bounds,
                            const double* coords, const double* widths, int p, cudaStream_t st);

@@ -295,6 +295,11 @@ struct htlr_plan {
   // concurrent level passes (mv_remote): side stream + fork / join events
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_ev[2] = {nullptr, nullptr};
+  // direct-f matvec (mv_remote): the leaf y-x sweep and the downward pass both
+  // sum into a zeroed f; f_red is set while that leaf sweep is launched
+  cudaEvent_t fz_ev = nullptr;
+  cudaEvent_t fd_ev[2] = {nullptr, nullptr};   // fork / join of the third stream (leaf_stream) of that matvec
+  double* f_red = nullptr;
   // z-slab shards: the leaf pass reads only u, so the local phase starts it
   // on its own stream, beside the upward pass and the exchange; the remote
   // phase joins it before the downward pass
@@ -397,6 +402,12 @@ int choose_nt(const Pass& ps, int R) {
 // plane kernel (one SM per z-point plane): z-slab shards, whose slab has few
 // planes (on one GPU the plane kernel is faster: 108 vs 136 us, config 4)
 static bool band_xy_lines(const htlr_plan* pl) { return pl->zslab; }
+// HTLR_FDIRECT=0: the leaf pass writes Y and the downward pass follows it
+// (the formulation the parity tests cross-check the direct-f one against)
+static bool fdirect_enabled() {
+  const char* e = getenv("HTLR_FDIRECT");
+  return !(e && e[0] == '0');
+}
 
 int make_tasks(Pass& ps, int R, std::vector<htlr::GemmTask>& out) {
   const int NT = choose_nt(ps, R);
@@ -476,6 +487,9 @@ int htlr_plan_destroy(htlr_plan* pl) {
   if (pl->copy_stream) cudaStreamDestroy(pl->copy_stream);
   if (pl->side_stream) cudaStreamDestroy(pl->side_stream);
   for (auto& e : pl->side_ev)
+    if (e) cudaEventDestroy(e);
+  if (pl->fz_ev) cudaEventDestroy(pl->fz_ev);
+  for (auto& e : pl->fd_ev)
     if (e) cudaEventDestroy(e);
   if (pl->leaf_stream) cudaStreamDestroy(pl->leaf_stream);
   for (auto& e : pl->leaf_ev)
@@ -2761,7 +2775,8 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
                                ps.K_pad, ps.zpitch, n, corr, pl->kp.scale, st, zlo, zhi);
     else if (sweep == 1)
       htlr::launch_band_planes(ps.level, nterms, ps.sep_tab.d(), ps.sep_NO, R, src, ps.K_pad, ps.zpitch,
-                               ps.band_ws.d(), C, corr, pl->kp.scale, st, n, zlo, zhi);
+                               ps.band_ws.d(), C, corr, pl->kp.scale, st, n, zlo, zhi, ps.to_y ? pl->f_red : nullptr,
+                               pl->n);
     return;
   }
   htlr::launch_sep_band(sweep, ps.sep_tab.d(), ps.sep_NO, ps.level, R, B, ps.K_pad, ps.zpitch, ps.band_ws.d(), C, corr,
@@ -2844,6 +2859,35 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
       leaf_z_done = true;
     }
   }
+  // Direct f: nothing but the downward pass reads Y, and f = Y + (expansion of
+  // H_eff) + a u is a sum of two independent parts.  With f zeroed, the plane
+  // kernel adds the leaf pass's share straight into the F-order f and the cube
+  // downward adds the rest, both with fp64 REDs (0 + a + b: the same value in
+  // either order) -- so the downward pass leaves the critical path: it runs
+  // on the side stream after the level passes, beside the leaf y-x sweep, and
+  // Y is neither written nor read.
+  bool fdirect = false;
+  htlr::CubeLevels fcl;
+  if (leaf_z_done && (stages & 2) && !cx.pipe && pl->shard_world == 1 && !pl->zslab && !band_xy_lines(pl) &&
+      fdirect_enabled()) {
+    const Pass& lq = pl->passes[pl->leaf_pass];
+    const int nbx = 1 << lq.level;
+    const bool planes = htlr::band_lines_supported(lq.level) && lq.band_lo[0] == 0 && lq.band_lo[1] == 0 &&
+                        lq.band_hi[0] == nbx && lq.band_hi[1] == nbx && lq.band_lo[2] == 0 && lq.band_hi[2] == nbx;
+    if (planes && lq.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && cube_params(pl, nullptr, fcl)) {
+      // a third stream, forked behind the upward pass: the zeroing of f and
+      // the cooperative (non-banded) level passes run beside the banded ones
+      if (!pl->fz_ev) CUDA_TRY(cudaEventCreateWithFlags(&pl->fz_ev, cudaEventDisableTiming));
+      for (auto& ev : pl->fd_ev)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      if (!pl->leaf_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->leaf_stream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventRecord(pl->fd_ev[0], pl->side_stream));
+      CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, pl->fd_ev[0], 0));
+      CUDA_TRY(cudaMemsetAsync(f, 0, (size_t)pl->N * R * sizeof(double), pl->leaf_stream));
+      CUDA_TRY(cudaEventRecord(pl->fz_ev, pl->leaf_stream));
+      fdirect = true;
+    }
+  }
   for (size_t i = 0; i < pl->passes.size() && (stages & 1); ++i) {
     Pass& ps = pl->passes[i];
     if (ps.to_y && pl->leaf_pending) continue;   // started by the local phase (z-slab shards)
@@ -2851,8 +2895,8 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     // level passes on the side stream; with the leaf pass already running
     // elsewhere (z-slab shards, host pipeline) the main stream is free, so
     // they alternate between the two
-    const cudaStream_t sst =
-        (fork && !ps.to_y && !((pl->leaf_pending || pipe_za) && (i & 1))) ? pl->side_stream : cx.st;
+    cudaStream_t sst = (fork && !ps.to_y && !((pl->leaf_pending || pipe_za) && (i & 1))) ? pl->side_stream : cx.st;
+    if (fdirect && !ps.to_y && !ps.band) sst = pl->leaf_stream;
     if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
       if (ps.band && own_only) continue;   // the sweeps need every (gathered) source box
@@ -2870,6 +2914,10 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         // and the self pairs' sources, writes the accumulator)
         double zs = 0.0;
         band_flops_of(ps.level, ps.to_y, 1, &zs);
+        if (ps.to_y && fdirect) {
+          CUDA_TRY(cudaStreamWaitEvent(sst, pl->fz_ev, 0));
+          pl->f_red = f;
+        }
         for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) {
           if (sw == 0 && cx.prof_begin(9, ps.level, zs * ps.band_flops * R, nv * (1.0 + nterm))) return 1;
           if (sw == 1 && cx.prof_begin(10, ps.level, (1.0 - zs) * ps.band_flops * R, nv * (nterm + 2.0))) return 1;
@@ -2877,6 +2925,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
           if (sw == 0 && cx.prof_end()) return 1;
           if (sw == 2 && cx.prof_end()) return 1;
         }
+        pl->f_red = nullptr;
         continue;
       }
       if (ps.sep_nitems == 0 && ps.sep_nblocks == 0) continue;
@@ -2933,9 +2982,21 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
                       ps.gen.ptr ? ps.gen.d() : nullptr);
     if (cx.prof_end()) return 1;
   }
+  if (fdirect) {
+    CUDA_TRY(cudaEventRecord(pl->fd_ev[1], pl->leaf_stream));
+    CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->fd_ev[1], 0));
+    const int64_t fb0 = pl->own_lo[pl->L], fnb = pl->own_hi[pl->L] - fb0;
+    htlr::launch_downward_cube(fcl, pl->L, R, fb0, fnb, pl->side_stream, u, f, nullptr,
+                               pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n, 0, 1 << 30, true);
+    ++cx.launches;
+  }
   if (fork || cx.side_forked) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
     CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->side_ev[1], 0));
+  }
+  if (fdirect) {
+    CUDA_TRY(cudaGetLastError());
+    return 0;
   }
   if (pl->leaf_pending && (stages & 1)) {
     CUDA_TRY(cudaStreamWaitEvent(cx.st, pl->leaf_ev[1], 0));

@@ -413,3 +413,46 @@ def test_banded_random_sweep_vs_oracle():
         Up = torch.from_numpy(U).pin_memory()
         Fp = H.matmat(op, Up).numpy()
         assert rel(Fp, F) <= 1e-13, (case, "host pipeline")
+
+
+@pytest.mark.parametrize("n,R,a", [(64, 1, 0.5), (64, 3, 0.25), (128, 1, 0.0), (128, 2, 0.75)])
+def test_direct_f_equals_downward_after_leaf_pass(n, R, a):
+    """Unsharded banded matvec: by default the plane kernel and the cube
+    downward pass both add their share into a zeroed f with fp64 REDs
+    (htlr_plan.cu mv_remote, "Direct f"), so the downward pass runs beside the
+    leaf y-x sweep and Y is never written.  HTLR_FDIRECT=0 keeps Y and the
+    downward pass after it.  0 + a + b has the same value in either order, so
+    the two differ only through the upward pass's unordered REDs (and, with a
+    coefficient, the a u term joining the expansion first instead of last):
+    equal to rounding.  (Fresh vectors each time: graphs are keyed by the
+    caller's vectors, so each call captures under its own setting.)"""
+    import torch
+    op = make(n, a=a)
+    assert op.leaf_pass() == "banded"
+    rng = np.random.default_rng(n + R)
+    U = rng.standard_normal((n ** 3, R)) if R > 1 else rng.standard_normal(n ** 3)
+    outs = {}
+    old = os.environ.get("HTLR_FDIRECT")
+    try:
+        for mode in ("0", "1"):
+            os.environ["HTLR_FDIRECT"] = mode
+            u = torch.from_numpy(U).cuda()
+            apply = H.matmat if R > 1 else H.matvec
+            f = apply(op, u)
+            f2 = apply(op, u)   # replay of the captured graph
+            torch.cuda.synchronize()
+            assert rel(f2.cpu().numpy(), f.cpu().numpy()) <= 1e-14
+            outs[mode] = f.cpu().numpy()
+    finally:
+        if old is None:
+            os.environ.pop("HTLR_FDIRECT", None)
+        else:
+            os.environ["HTLR_FDIRECT"] = old
+    assert rel(outs["1"], outs["0"]) <= 1e-14
+    # and against the oracle's rows of corner, edge and interior leaf boxes
+    if n == 64:
+        U2 = U.reshape(n ** 3, -1)
+        rows = O.sampled_matvec(problem(n, a=a), U2, BOXES[64])
+        F = outs["1"].reshape(n ** 3, -1)
+        for i, bx in enumerate(BOXES[64]):
+            assert rel(F[O.box_linear_indices(n, bx)], rows[i]) <= TOL
