@@ -22,7 +22,7 @@ BUILD = os.path.join(HERE, "..", "build", "htlr")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["htlr_build.cu", "htlr_apply.cu", "htlr_gemm.cu", "htlr_mapped.cu", "htlr_regen_sym.cu", "htlr_rows.cu",
-              "htlr_quasi.cu", "htlr_lowrank.cu", "htlr_sep.cu", "htlr_band.cu", "htlr_cube.cu", "htlr_tensor.cu", "htlr_interp.cu", "htlr_plan.cu"]
+              "htlr_quasi.cu", "htlr_lowrank.cu", "htlr_sep.cu", "htlr_band.cu", "htlr_cube.cu", "htlr_tensor.cu", "htlr_interp.cu", "htlr_plan.cu", "htlr_matvec.cu", "htlr_capi.cu"]
 CPP_SOURCES = ["htlr_lists.cpp"]
 
 
