@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) band_line_kernel(const double* 
 }
 
 // y and x sweeps of one z-point plane (blockIdx.x = 8 bz + zl), warps = NB
-template <int NB, int NT, bool R1>
+template <int NB, int NT, bool R1, bool FRED>
 __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __restrict__ tables, int NO, int R_,
                                                                 const double* __restrict__ ub, int ldub, int zpub,
                                                                 const double* __restrict__ ws, int64_t tstride,
@@ -615,18 +615,26 @@ __global__ void __launch_bounds__(NB * 32, 1) band_plane_kernel(const double* __
                                    (int64_t)n * n * (8 * bz + zl)) * R + r
                            : ub + m * ldub + zpub * zl + 16 * q + g;
       const int64_t ustep = n ? (int64_t)n * R : 8;
-      // fred: the plane's share of f summed straight into the F-order result
+      // FRED: the plane's share of f summed straight into the F-order result
       // (the downward pass adds its own with REDs too: no Y round trip and no
-      // order between the two)
-      double* of = fred ? fred + ((int64_t)(8 * (4 * Q + c) + g) + (int64_t)nf * (8 * w + 2 * q) +
-                                  (int64_t)nf * nf * (8 * bz + zl)) * R + r
-                        : nullptr;
+      // order between the two); a separate instantiation, so the kernel that
+      // stores Y keeps its register allocation
+      if constexpr (FRED) {
+        double* of = fred + ((int64_t)(8 * (4 * Q + c) + g) + (int64_t)nf * (8 * w + 2 * q) +
+                             (int64_t)nf * nf * (8 * bz + zl)) * R + r;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        double val = scale * v[c][j];
-        if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
-        if (fred) atomicAdd(of + (int64_t)j * nf * R, val);
-        else o[8 * j] = val;
+        for (int j = 0; j < 2; ++j) {
+          double val = scale * v[c][j];
+          if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
+          atomicAdd(of + (int64_t)j * nf * R, val);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double val = scale * v[c][j];
+          if (corr_ptr) val = fma(cv, __ldg(us + j * ustep), val);
+          o[8 * j] = val;
+        }
       }
     }
   }
@@ -902,16 +910,18 @@ void launch_planes_t(const double* tab, int NO, int R, const double* ub, int ldu
   const size_t smem = (size_t)NB * NB * 32 * sizeof(double2) + (size_t)2 * NO * kTabSlot * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(band_plane_kernel<NB, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(band_plane_kernel<NB, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(band_plane_kernel<NB, NT, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  if (R == 1)
-    band_plane_kernel<NB, NT, true><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
-        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo, fred, nf);
-  else
-    band_plane_kernel<NB, NT, false><<<dim3(8 * (zhi - zlo), R), NB * 32, smem, st>>>(
-        tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo, fred, nf);
+  const dim3 grid(8 * (zhi - zlo), R);
+  auto go = [&](auto kern) {
+    kern<<<grid, NB * 32, smem, st>>>(tab, NO, R, ub, ldub, zpub, ws, tstride, Y, corr, scale, n, zlo, fred, nf);
+  };
+  if (fred) R == 1 ? go(band_plane_kernel<NB, NT, true, true>) : go(band_plane_kernel<NB, NT, false, true>);
+  else R == 1 ? go(band_plane_kernel<NB, NT, true, false>) : go(band_plane_kernel<NB, NT, false, false>);
 }
 
 }  // namespace

@@ -419,7 +419,7 @@ def test_banded_random_sweep_vs_oracle():
 def test_direct_f_equals_downward_after_leaf_pass(n, R, a):
     """Unsharded banded matvec: by default the plane kernel and the cube
     downward pass both add their share into a zeroed f with fp64 REDs
-    (htlr_plan.cu mv_remote, "Direct f"), so the downward pass runs beside the
+    (htlr_matvec.cu mv_remote, "Direct f"), so the downward pass runs beside the
     leaf y-x sweep and Y is never written.  HTLR_FDIRECT=0 keeps Y and the
     downward pass after it.  0 + a + b has the same value in either order, so
     the two differ only through the upward pass's unordered REDs (and, with a
