@@ -610,10 +610,10 @@ def run_b200(args):
                          "includes": "host list build + device sampling, QR and tiling (first construct "
                                      "of the process)"},
         "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in sorted(phases.items())},
-        "phases_note": "per-kernel times of a profiled pass (launches serialised on one stream, the leaf pass storing Y "
-                       "and the downward pass after it); the timed step replays a graph with the level passes on side "
-                       "streams and, for unsharded banded plans, the downward pass beside the leaf y-x sweep "
-                       "(both add into a zeroed f with fp64 REDs; HTLR_FDIRECT=0 restores the serial order)",
+        "phases_note": "per-kernel times of a profiled pass: the same kernels with their launches serialised on one "
+                       "stream; the timed step replays a graph with the level passes on side streams and, for "
+                       "unsharded banded plans, the downward pass beside the leaf y-x sweep (both add into a zeroed f "
+                       "with fp64 REDs; HTLR_FDIRECT=0 stores Y and runs the downward pass after it)",
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": io_bytes,
                 "d2h_bytes_per_step": io_bytes, "ms_per_step": e2e_total / args.steps,

@@ -604,8 +604,11 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   // Y is neither written nor read.
   bool fdirect = false;
   htlr::CubeLevels fcl;
-  if (leaf_z_done && (stages & 2) && !cx.pipe && pl->shard_world == 1 && !pl->zslab && !band_xy_lines(pl) &&
-      fdirect_enabled()) {
+  // a profiled matvec runs the same two kernels, serialised on the one stream
+  const bool prof_serial = pl->profiling && !fork && (stages & 1) && !own_only && !rest_only && !pl->leaf_pending &&
+                           !pipe_za && pl->sep && pl->passes[pl->leaf_pass].band;
+  if ((leaf_z_done || prof_serial) && (stages & 2) && !cx.pipe && pl->shard_world == 1 && !pl->zslab &&
+      !band_xy_lines(pl) && fdirect_enabled()) {
     const Pass& lq = pl->passes[pl->leaf_pass];
     const int nbx = 1 << lq.level;
     const bool planes = htlr::band_lines_supported(lq.level) && lq.band_lo[0] == 0 && lq.band_lo[1] == 0 &&
@@ -613,14 +616,18 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     if (planes && lq.P == htlr::kSepP * htlr::kSepP * htlr::kSepP && cube_params(pl, nullptr, fcl)) {
       // a third stream, forked behind the upward pass: the zeroing of f and
       // the cooperative (non-banded) level passes run beside the banded ones
-      if (!pl->fz_ev) CUDA_TRY(cudaEventCreateWithFlags(&pl->fz_ev, cudaEventDisableTiming));
-      for (auto& ev : pl->fd_ev)
-        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      if (!pl->leaf_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->leaf_stream, cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventRecord(pl->fd_ev[0], pl->side_stream));
-      CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, pl->fd_ev[0], 0));
-      CUDA_TRY(cudaMemsetAsync(f, 0, (size_t)pl->N * R * sizeof(double), pl->leaf_stream));
-      CUDA_TRY(cudaEventRecord(pl->fz_ev, pl->leaf_stream));
+      if (fork) {
+        if (!pl->fz_ev) CUDA_TRY(cudaEventCreateWithFlags(&pl->fz_ev, cudaEventDisableTiming));
+        for (auto& ev : pl->fd_ev)
+          if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        if (!pl->leaf_stream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->leaf_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventRecord(pl->fd_ev[0], pl->side_stream));
+        CUDA_TRY(cudaStreamWaitEvent(pl->leaf_stream, pl->fd_ev[0], 0));
+        CUDA_TRY(cudaMemsetAsync(f, 0, (size_t)pl->N * R * sizeof(double), pl->leaf_stream));
+        CUDA_TRY(cudaEventRecord(pl->fz_ev, pl->leaf_stream));
+      } else {
+        CUDA_TRY(cudaMemsetAsync(f, 0, (size_t)pl->N * R * sizeof(double), cx.st));
+      }
       fdirect = true;
     }
   }
@@ -632,7 +639,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     // elsewhere (z-slab shards, host pipeline) the main stream is free, so
     // they alternate between the two
     cudaStream_t sst = (fork && !ps.to_y && !((pl->leaf_pending || pipe_za) && (i & 1))) ? pl->side_stream : cx.st;
-    if (fdirect && !ps.to_y && !ps.band) sst = pl->leaf_stream;
+    if (fdirect && fork && !ps.to_y && !ps.band) sst = pl->leaf_stream;
     if (!pl->sep && own_only) continue;   // dense passes all run after the exchange
     if (pl->sep) {
       if (ps.band && own_only) continue;   // the sweeps need every (gathered) source box
@@ -651,7 +658,7 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         double zs = 0.0;
         band_flops_of(ps.level, ps.to_y, 1, &zs);
         if (ps.to_y && fdirect) {
-          CUDA_TRY(cudaStreamWaitEvent(sst, pl->fz_ev, 0));
+          if (fork) CUDA_TRY(cudaStreamWaitEvent(sst, pl->fz_ev, 0));
           pl->f_red = f;
         }
         for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) {
@@ -719,12 +726,18 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
     if (cx.prof_end()) return 1;
   }
   if (fdirect) {
-    CUDA_TRY(cudaEventRecord(pl->fd_ev[1], pl->leaf_stream));
-    CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->fd_ev[1], 0));
+    if (fork) {
+      CUDA_TRY(cudaEventRecord(pl->fd_ev[1], pl->leaf_stream));
+      CUDA_TRY(cudaStreamWaitEvent(pl->side_stream, pl->fd_ev[1], 0));
+    }
     const int64_t fb0 = pl->own_lo[pl->L], fnb = pl->own_hi[pl->L] - fb0;
-    htlr::launch_downward_cube(fcl, pl->L, R, fb0, fnb, pl->side_stream, u, f, nullptr,
+    // work: the expansion's three mode products per leaf box; bytes: f summed (+ u read with a coefficient)
+    const double sl = pl->sL;
+    const double macs = sl * p * p * p + sl * sl * p * p + sl * sl * sl * p;
+    if (cx.prof_begin(4, pl->L, 2.0 * macs * fnb * R, R8 * 2.0 * (double)pl->N)) return 1;
+    htlr::launch_downward_cube(fcl, pl->L, R, fb0, fnb, fork ? pl->side_stream : cx.st, u, f, nullptr,
                                pl->has_coeff ? pl->coeff.d() : nullptr, pl->desc.coeff_const, pl->n, 0, 1 << 30, true);
-    ++cx.launches;
+    if (cx.prof_end()) return 1;
   }
   if (fork || cx.side_forked) {
     CUDA_TRY(cudaEventRecord(pl->side_ev[1], pl->side_stream));
