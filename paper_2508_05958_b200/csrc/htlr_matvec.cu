@@ -479,7 +479,9 @@ int mv_local(MvCtx& cx, const double* u) {
 // the upward pass then ends with it; measured 20 / 40 / 48 / 56 / 64: config
 // 4's step 0.1307 (upward first, on the main stream) / 0.1323 / 0.1280 /
 // 0.1286 / 0.1284 ms; with the direct-f order 8 / 20 / 32 / 40 / 48 / 64 / 80:
-// 0.1311 / 0.1331 / 0.1351 / 0.1290 / 0.1229 / 0.1250 / 0.1311 ms)
+// 0.1311 / 0.1331 / 0.1351 / 0.1290 / 0.1229 / 0.1250 / 0.1311 ms, flat from 48
+// to 62: the z sweep's 4096 half-line units take three rounds of its 16 warps
+// per SM on any grid of 86 to 127 SMs)
 static int level_sms(bool with_upward) { return with_upward ? 48 : 20; }
 
 // One sweep of a banded pass (0: z sweep, 1: the fused y-x sweep; 2: the
