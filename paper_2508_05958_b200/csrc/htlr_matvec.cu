@@ -346,6 +346,7 @@ static bool leaf_from_u(const htlr_plan* pl, int R) {
 
 int mv_local(MvCtx& cx, const double* u) {
   htlr_plan* pl = cx.pl;
+  pl->f_red = nullptr;
   if (pl->mapped) return mv_local_mapped(cx, u);
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const double R8 = 8.0 * R;
@@ -523,6 +524,7 @@ static void launch_band_sweep(htlr_plan* pl, const Pass& ps, int sweep, const do
 
 int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
   htlr_plan* pl = cx.pl;
+  pl->f_red = nullptr;
   if (pl->mapped) return mv_remote_mapped(cx, u, f, stages);
   const int d = cx.d, p = cx.p, P = cx.P, R = cx.R;
   const double R8 = 8.0 * R;
@@ -659,10 +661,8 @@ int mv_remote(MvCtx& cx, const double* u, double* f, int stages = 3) {
         // and the self pairs' sources, writes the accumulator)
         double zs = 0.0;
         band_flops_of(ps.level, ps.to_y, 1, &zs);
-        if (ps.to_y && fdirect) {
-          if (fork) CUDA_TRY(cudaStreamWaitEvent(sst, pl->fz_ev, 0));
-          pl->f_red = f;
-        }
+        if (ps.to_y && fdirect && fork) CUDA_TRY(cudaStreamWaitEvent(sst, pl->fz_ev, 0));
+        pl->f_red = (ps.to_y && fdirect) ? f : nullptr;   // never stale: an error return may have skipped the reset below
         for (int sw = (ps.to_y && leaf_z_done) ? 1 : 0; sw < 3; ++sw) {
           if (sw == 0 && cx.prof_begin(9, ps.level, zs * ps.band_flops * R, nv * (1.0 + nterm))) return 1;
           if (sw == 1 && cx.prof_begin(10, ps.level, (1.0 - zs) * ps.band_flops * R, nv * (nterm + 2.0))) return 1;
